@@ -1,0 +1,251 @@
+/* vscreen_gpu C-ABI — the drop-in boundary of the B200 dock-and-score path.
+ *
+ * Plain C: POD structs, raw pointers and sizes, int status codes, no
+ * exceptions and no torch types.  One handle per host thread / GPU; handles
+ * are not shared between threads.  All host buffers are caller-owned.
+ *
+ * The reference has no FFI layer for this path: its boundary is the C++
+ * header API (proj/include/vscreen/{dock,batcher,chem,pipeline}.hpp) plus
+ * the pybind11 module (proj/bindings/module.cpp).  Each entry point below
+ * names the reference function it replaces; include/vscreen_gpu/vscreen_gpu.hpp
+ * maps these status codes back onto the reference exception types so C++
+ * callers compile unchanged, and paper_2304_09953_b200/ is the Python mirror.
+ */
+#ifndef VSCREEN_GPU_CAPI_H
+#define VSCREEN_GPU_CAPI_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------- status -- */
+enum vs_status {
+  VS_OK = 0,
+  VS_ERR_INVALID_ARGUMENT = -1, /* std::invalid_argument   dock.cpp:322-323 */
+  VS_ERR_ATOM_COUNT = -2,       /* dock::AtomCountMismatch dock.cpp:219-230,299-301,324 */
+  VS_ERR_EMPTY_BOUNDS = -3,     /* dock::EmptyBounds       dock.cpp:321 */
+  VS_ERR_LENGTH = -4,           /* dock::LengthMismatch    dock.cpp:393-396 */
+  VS_ERR_OUT_OF_RANGE = -5,     /* batcher::OutOfRange     batcher.cpp:23-25,161 */
+  VS_ERR_ITEM_TOO_LARGE = -6,   /* batcher::ItemTooLarge   batcher.cpp:31-34 */
+  VS_ERR_POCKET = -7,           /* std::runtime_error      dock.cpp:441,448 */
+  VS_ERR_PARSE = -8,            /* chem::ParseError        chem.cpp:109-264 */
+  VS_ERR_CAPACITY = -9,         /* ligand beyond GPU limits (atoms>128, torsions>64,
+                                   restarts>64, flex_angles>16) or buffer too small */
+  VS_ERR_CUDA = -10,
+  VS_ERR_NO_DEVICE = -11,
+  VS_ERR_STATE = -12,           /* call order (e.g. dock before pocket/library) */
+  VS_ERR_DISCONNECTED = -13     /* chem::DisconnectedGraph chem.cpp:408 */
+};
+
+/* ------------------------------------------------------------- pocket -- */
+/* dock::Site (dock.hpp:18-23); kind 0 steric, 1 hbond, 2 lipophilic */
+typedef struct {
+  double center[3];
+  double weight;
+  double sigma;
+  int32_t kind;
+  int32_t reserved;
+} vs_site;
+
+/* dock::Pocket (dock.hpp:32-37) */
+typedef struct {
+  const vs_site* sites;
+  int32_t n_sites;
+  int32_t reserved;
+  double lo[3];
+  double hi[3];
+  double clash_radius;
+  double clash_penalty;
+} vs_pocket;
+
+/* ------------------------------------------------------------ library -- */
+/* A ligand library in the reference's own types, flattened: chem::Conformer
+ * coords (chem.hpp:78-81, FP64), dock::TorsionTopology axes and moving lists
+ * (dock.hpp:65-71), the element class used by rescore (dock.cpp:309), the
+ * per-ligand dock seed (pipeline.cpp:483) and the rank of the ligand id in
+ * std::map order (the rank_ligands tie-break, pipeline.cpp:243-251). */
+typedef struct {
+  int32_t n_ligands;
+  int32_t reserved;
+  const int32_t* n_atoms;      /* [n] */
+  const int32_t* n_tors;       /* [n] */
+  const int32_t* rot_bonds;    /* [n] descriptor for size classes (may be NULL: = n_tors) */
+  const double* coords;        /* [sum n_atoms][3] */
+  const int32_t* atom_class;   /* [sum n_atoms] 0 other, 1 C, 2 N or O */
+  const int32_t* axis_a;       /* [sum n_tors] */
+  const int32_t* axis_b;       /* [sum n_tors] */
+  const int32_t* moving_count; /* [sum n_tors] */
+  const int32_t* moving;       /* [sum moving_count] */
+  const uint64_t* seeds;       /* [n] */
+  const uint32_t* id_rank;     /* [n] */
+} vs_library;
+
+/* batcher::SizeClass (batcher.hpp:33-40), half-open ranges */
+typedef struct {
+  int32_t atom_lo, atom_hi, rot_lo, rot_hi;
+} vs_size_class;
+
+/* ------------------------------------------------------------- params -- */
+/* dock(restarts, diversity_delta, seed, max_steps) (dock.hpp:107-109) plus
+ * StageKnobs keep_top/min_score (pipeline.hpp:33-40) and the sweep-v1
+ * knobs (docs/SWEEP_V1.md).  max_steps of the reference ascent has no
+ * meaning for sweep-v1 and is not taken. */
+typedef struct {
+  int32_t restarts;        /* R >= 1, <= 64 */
+  int32_t rotations;       /* K >= 1 */
+  int32_t flex_angles;     /* A in [1, 16] */
+  int32_t flex_passes;     /* F >= 0 */
+  double diversity_delta;  /* >= 0 */
+  int32_t keep_top;        /* >= 0 */
+  int32_t write_all_poses; /* also return every kept pose (dock() output) */
+  double min_score;
+  uint64_t rotation_seed;
+} vs_dock_params;
+
+/* One pose (dock::Pose, dock.hpp:39-46) in FP32 plus its sweep-v1 index
+ * tuple.  Torsions are returned in a parallel array. */
+typedef struct {
+  float t[3];
+  float q[4]; /* w, x, y, z */
+  float score;
+  float rescore;
+  int16_t restart;
+  int16_t attempt;
+  int16_t rot;
+  int16_t reserved;
+} vs_pose;
+
+/* Results of one dock run, caller-owned host buffers.  Ligand i's torsion
+ * block starts at tors_off(i) * slots where tors_off is the prefix sum of
+ * n_tors and slots = keep_top (surv) or restarts (all). */
+typedef struct {
+  float* best;        /* [n] max rescore over survivors; -inf when dropped */
+  int32_t* n_kept;    /* [n] kept (diverse) poses; -1 = out of every size class */
+  int32_t* n_surv;    /* [n] poses surviving filter_poses */
+  vs_pose* surv;      /* [n * keep_top] */
+  float* surv_tors;   /* [sum n_tors * keep_top] */
+  vs_pose* all;       /* optional [n * restarts] */
+  float* all_tors;    /* optional [sum n_tors * restarts] */
+  uint64_t* keys;     /* optional [n] top-k keys */
+} vs_results;
+
+typedef struct vs_handle vs_handle;
+
+/* ------------------------------------------------------ GPU runtime ----- */
+int vs_create(int device, vs_handle** out);
+void vs_destroy(vs_handle* h);
+const char* vs_last_error(const vs_handle* h);
+/* name (<= 255 chars), SM count, SM clock (kHz) */
+int vs_device_info(const vs_handle* h, char* name, int32_t* sm_count, int32_t* clock_khz);
+
+/* Upload the pocket (parse_pocket_json result, dock.cpp:432) and, when
+ * grid_spacing > 0, build the three FP32 grid maps (steric / hbond /
+ * lipophilic) over bounds +- grid_pad on the device.  Validation as
+ * dock.cpp:321, 441, 448. */
+int vs_set_pocket(vs_handle* h, const vs_pocket* pocket, double grid_spacing, double grid_pad);
+int vs_grid_info(const vs_handle* h, int32_t dims[3], float origin[3], float* spacing);
+int vs_grid_fetch(vs_handle* h, float* steric, float* hbond, float* lipo);
+
+/* Pack the library into the device SoA (size-class buckets, LPT order
+ * within a bucket) and upload it.  classes == NULL: automatic atom-count
+ * buckets.  Ligands outside every class are dropped (pipeline.cpp:447-452). */
+int vs_upload_library(vs_handle* h, const vs_library* lib, const vs_size_class* classes,
+                      int32_t n_classes);
+/* Run the path on the resident library; stream = cudaStream_t or NULL. */
+int vs_dock(vs_handle* h, const vs_dock_params* params, void* stream);
+int vs_fetch_results(vs_handle* h, vs_results* out);
+/* Upload + dock + fetch in one call (host buffers in and out). */
+int vs_dock_host(vs_handle* h, const vs_library* lib, const vs_size_class* classes,
+                 int32_t n_classes, const vs_dock_params* params, vs_results* out);
+/* Device time (ms, CUDA events on the launch stream) of the dock kernels of
+ * the last vs_dock call, and the number of kernels this handle launched. */
+double vs_last_dock_ms(const vs_handle* h);
+uint64_t vs_launch_count(const vs_handle* h);
+
+/* Global top-k of the last run: keys ascending = (score desc, id_rank asc)
+ * (rank_ligands, pipeline.cpp:243-251).  key = (~orderable(score) << 32) |
+ * id_rank; dropped ligands are ~0. */
+int vs_topk(vs_handle* h, int32_t k, uint64_t* out_keys);
+int vs_topk_device(vs_handle* h, int32_t k, uint64_t* out_keys_dev, void* stream);
+/* Merge of gathered per-rank top-k keys (device buffers). */
+int vs_topk_merge_device(vs_handle* h, const uint64_t* keys_dev, int64_t n, int32_t k,
+                         uint64_t* out_keys_dev, void* stream);
+float vs_key_score(uint64_t key);
+uint32_t vs_key_id_rank(uint64_t key);
+
+/* geometric_score + rescore of given poses (dock.cpp:278, 297).  pose_lig
+ * must be non-decreasing; torsions of pose p are tors[tors_off_p ...] in
+ * pose order, n_tors of its ligand each. */
+int vs_rescore(vs_handle* h, const vs_library* lib, int64_t n_poses, const int32_t* pose_lig,
+               const float* t, const float* q, const float* tors, float* geo, float* resc);
+
+/* --------------------------------------------------- host-side (CPU) --- */
+/* Rng(seed).split(path...) then n next_u64 (rng.hpp:14-21) */
+int vs_rng_u64(uint64_t seed, const uint64_t* path, int32_t depth, int32_t n, uint64_t* out);
+/* corpus::random_smiles(Rng(seed).split(i)) (tools/smiles_corpus.hpp:13) */
+int vs_random_smiles(uint64_t seed, uint64_t i, char* out, int32_t cap);
+
+/* One ligand: parse_smiles + rotatable_bonds + embed_3d + torsion_topology
+ * (chem.cpp:109,319,406; dock.cpp:234).  iterations < 0: no embedding. */
+typedef struct {
+  int32_t cap_atoms, cap_bonds, cap_tors, cap_moving;
+  int32_t n_atoms, n_bonds, n_tors, n_moving, rot_bonds;
+  int32_t parse_kind, parse_pos; /* on VS_ERR_PARSE */
+  double* coords;                /* [cap_atoms*3] */
+  int32_t* atom_class;           /* [cap_atoms] */
+  char* elements;                /* [cap_atoms*3] NUL-padded element symbols */
+  uint8_t* aromatic;             /* [cap_atoms] */
+  int32_t* bonds;                /* [cap_bonds*3] a, b, order */
+  uint8_t* ring;                 /* [cap_bonds] */
+  int32_t* axis_a;               /* [cap_tors] */
+  int32_t* axis_b;
+  int32_t* moving_count;
+  int32_t* moving;               /* [cap_moving] */
+} vs_ligand_buf;
+int vs_ligand_build(const char* smiles, uint64_t embed_seed, int32_t iterations,
+                    vs_ligand_buf* out);
+
+/* Many ligands on `threads` host threads.  smiles: NUL-separated blob. */
+typedef struct vs_libbuild vs_libbuild;
+int vs_libbuild_run(const char* smiles_blob, int32_t n, const uint64_t* embed_seeds,
+                    int32_t iterations, int32_t threads, vs_libbuild** out);
+/* totals and per-ligand status (0 ok, VS_ERR_PARSE, VS_ERR_DISCONNECTED) */
+int vs_libbuild_sizes(const vs_libbuild* b, int64_t* atoms, int64_t* tors, int64_t* moving);
+int vs_libbuild_fetch(const vs_libbuild* b, int32_t* status, int32_t* n_atoms, int32_t* n_tors,
+                      int32_t* rot_bonds, double* coords, int32_t* atom_class, int32_t* axis_a,
+                      int32_t* axis_b, int32_t* moving_count, int32_t* moving);
+void vs_libbuild_free(vs_libbuild* b);
+
+/* batcher (batcher.cpp:7-86) */
+int vs_default_classes(vs_size_class* out, int32_t cap);
+int vs_size_class_of(int32_t atoms, int32_t rot, const vs_size_class* classes, int32_t n);
+int vs_target_batch_size(const vs_size_class* cls, double memory_capacity, double mem_fixed,
+                         double mem_per_atom, double mem_per_rotbond, int64_t* out);
+double vs_simulate_throughput(int64_t n_items, double launch_overhead, double service_time);
+/* dock-stage bucket replay of run_campaign (pipeline.cpp:439-461): per
+ * ligand in_range[i]; batches as (class, length) + flattened members.
+ * Returns the number of batches (or a negative status). */
+int vs_bucket_replay(const int32_t* atoms, const int32_t* rot, int32_t n,
+                     const vs_size_class* classes, int32_t n_classes, double memory_capacity,
+                     double mem_fixed, double mem_per_atom, double mem_per_rotbond,
+                     double max_age, int32_t* in_range, int32_t* batch_cls, int32_t* batch_len,
+                     int32_t* batch_members);
+/* dock seeds Rng(master).split(2).split(i), i = post-compaction index
+ * (pipeline.cpp:481-484) */
+int vs_campaign_seeds(uint64_t master_seed, int32_t stage, const int32_t* in_range, int32_t n,
+                      uint64_t* out);
+/* filter_poses on bare scores (dock.cpp:373-390) */
+int vs_filter_poses(const double* scores, int32_t n, int64_t keep_top, double min_score,
+                    int32_t* out_idx);
+/* rank_ligands (pipeline.cpp:243-251): ids NUL-separated */
+int vs_rank_ligands(const char* ids_blob, const double* scores, int32_t n, int32_t* out_order);
+/* id_rank[i] = rank of id i in std::map (bytewise) order */
+int vs_id_ranks(const char* ids_blob, int32_t n, uint32_t* out_rank);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VSCREEN_GPU_CAPI_H */

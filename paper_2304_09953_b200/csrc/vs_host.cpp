@@ -1,0 +1,341 @@
+// Host-side C-ABI entry points (capi.h "host-side" section): RNG, ligand
+// ingest, batcher, filter, rank.  Pure C++ on the CPU; no CUDA.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <exception>
+#include <numeric>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/vscreen_gpu/capi.h"
+#include "vs_ingest.h"
+#include "vs_rng.h"
+
+using namespace vs;
+
+namespace {
+
+std::vector<std::string> split_blob(const char* blob, int n) {
+  std::vector<std::string> out;
+  out.reserve(static_cast<std::size_t>(n));
+  const char* p = blob;
+  for (int i = 0; i < n; ++i) {
+    out.emplace_back(p);
+    p += out.back().size() + 1;
+  }
+  return out;
+}
+
+struct BuiltLigand {
+  int status = 0;
+  int rot = 0;
+  std::vector<double> coords;
+  std::vector<int> cls;
+  Topology topo;
+};
+
+BuiltLigand build_one(const std::string& smiles, std::uint64_t seed, int iterations) {
+  BuiltLigand b;
+  try {
+    Graph g = parse_smiles(smiles);
+    b.rot = rotatable_bond_count(g);
+    b.topo = torsion_axes(g);
+    b.cls.resize(g.elements.size());
+    for (std::size_t i = 0; i < g.elements.size(); ++i) b.cls[i] = element_class(g.elements[i]);
+    if (iterations >= 0) {
+      b.coords = embed(g, seed, iterations);
+    } else {
+      b.coords.assign(3 * g.elements.size(), 0.0);
+    }
+  } catch (const ParseFailure&) {
+    b.status = VS_ERR_PARSE;
+  } catch (const std::exception&) {
+    b.status = VS_ERR_DISCONNECTED;
+  }
+  return b;
+}
+
+}  // namespace
+
+struct vs_libbuild {
+  std::vector<BuiltLigand> ligs;
+};
+
+extern "C" {
+
+int vs_rng_u64(uint64_t seed, const uint64_t* path, int32_t depth, int32_t n, uint64_t* out) {
+  HostRng r(seed);
+  for (int d = 0; d < depth; ++d) r = r.split(path[d]);
+  for (int i = 0; i < n; ++i) out[i] = r.next_u64();
+  return VS_OK;
+}
+
+int vs_random_smiles(uint64_t seed, uint64_t i, char* out, int32_t cap) {
+  const std::string s = random_smiles(seed, i);
+  if (static_cast<int>(s.size()) + 1 > cap) return VS_ERR_CAPACITY;
+  std::memcpy(out, s.c_str(), s.size() + 1);
+  return static_cast<int>(s.size());
+}
+
+int vs_ligand_build(const char* smiles, uint64_t embed_seed, int32_t iterations,
+                    vs_ligand_buf* o) {
+  Graph g;
+  try {
+    g = parse_smiles(smiles);
+  } catch (const ParseFailure& e) {
+    o->parse_kind = e.kind;
+    o->parse_pos = static_cast<int32_t>(e.pos);
+    return VS_ERR_PARSE;
+  }
+  const Topology t = torsion_axes(g);
+  const int n = static_cast<int>(g.elements.size());
+  int mv = 0;
+  for (const auto& a : t.axes) mv += static_cast<int>(a.moving.size());
+  o->n_atoms = n;
+  o->n_bonds = static_cast<int>(g.bonds.size());
+  o->n_tors = static_cast<int>(t.axes.size());
+  o->n_moving = mv;
+  o->rot_bonds = rotatable_bond_count(g);
+  if (n > o->cap_atoms || o->n_bonds > o->cap_bonds || o->n_tors > o->cap_tors ||
+      mv > o->cap_moving)
+    return VS_ERR_CAPACITY;
+  std::vector<double> xyz;
+  try {
+    xyz = iterations >= 0 ? embed(g, embed_seed, iterations) : std::vector<double>(3 * n, 0.0);
+  } catch (const std::exception&) {
+    return VS_ERR_DISCONNECTED;
+  }
+  for (int i = 0; i < n; ++i) {
+    for (int c = 0; c < 3; ++c) o->coords[3 * i + c] = xyz[3 * i + c];
+    o->atom_class[i] = element_class(g.elements[i]);
+    std::memset(o->elements + 3 * i, 0, 3);
+    std::memcpy(o->elements + 3 * i, g.elements[i].c_str(), std::min<std::size_t>(2, g.elements[i].size()));
+    o->aromatic[i] = g.aromatic[i] ? 1 : 0;
+  }
+  for (int e = 0; e < o->n_bonds; ++e) {
+    o->bonds[3 * e] = g.bonds[e].a;
+    o->bonds[3 * e + 1] = g.bonds[e].b;
+    o->bonds[3 * e + 2] = g.bonds[e].order;
+    o->ring[e] = g.ring[e] ? 1 : 0;
+  }
+  int k = 0;
+  for (int j = 0; j < o->n_tors; ++j) {
+    o->axis_a[j] = t.axes[j].a;
+    o->axis_b[j] = t.axes[j].b;
+    o->moving_count[j] = static_cast<int>(t.axes[j].moving.size());
+    for (int m : t.axes[j].moving) o->moving[k++] = m;
+  }
+  return VS_OK;
+}
+
+int vs_libbuild_run(const char* blob, int32_t n, const uint64_t* seeds, int32_t iterations,
+                    int32_t threads, vs_libbuild** out) {
+  auto* b = new vs_libbuild;
+  b->ligs.resize(static_cast<std::size_t>(n));
+  const auto smiles = split_blob(blob, n);
+  std::atomic<int> next{0};
+  auto work = [&] {
+    for (int i = next.fetch_add(1); i < n; i = next.fetch_add(1))
+      b->ligs[i] = build_one(smiles[i], seeds[i], iterations);
+  };
+  const int nt = std::max(1, std::min<int>(threads, n));
+  if (nt == 1) {
+    work();
+  } else {
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nt; ++t) pool.emplace_back(work);
+    for (auto& th : pool) th.join();
+  }
+  *out = b;
+  return VS_OK;
+}
+
+int vs_libbuild_sizes(const vs_libbuild* b, int64_t* atoms, int64_t* tors, int64_t* moving) {
+  int64_t a = 0, t = 0, m = 0;
+  for (const auto& l : b->ligs) {
+    if (l.status) continue;
+    a += static_cast<int64_t>(l.cls.size());
+    t += static_cast<int64_t>(l.topo.axes.size());
+    for (const auto& ax : l.topo.axes) m += static_cast<int64_t>(ax.moving.size());
+  }
+  *atoms = a;
+  *tors = t;
+  *moving = m;
+  return VS_OK;
+}
+
+// Failed ligands contribute zero atoms/torsions and a non-zero status.
+int vs_libbuild_fetch(const vs_libbuild* b, int32_t* status, int32_t* n_atoms, int32_t* n_tors,
+                      int32_t* rot_bonds, double* coords, int32_t* atom_class, int32_t* axis_a,
+                      int32_t* axis_b, int32_t* moving_count, int32_t* moving) {
+  std::size_t ao = 0, to = 0, mo = 0;
+  for (std::size_t i = 0; i < b->ligs.size(); ++i) {
+    const auto& l = b->ligs[i];
+    status[i] = l.status;
+    if (l.status) {
+      n_atoms[i] = n_tors[i] = rot_bonds[i] = 0;
+      continue;
+    }
+    n_atoms[i] = static_cast<int32_t>(l.cls.size());
+    n_tors[i] = static_cast<int32_t>(l.topo.axes.size());
+    rot_bonds[i] = l.rot;
+    std::memcpy(coords + 3 * ao, l.coords.data(), l.coords.size() * sizeof(double));
+    std::memcpy(atom_class + ao, l.cls.data(), l.cls.size() * sizeof(int32_t));
+    ao += l.cls.size();
+    for (const auto& ax : l.topo.axes) {
+      axis_a[to] = ax.a;
+      axis_b[to] = ax.b;
+      moving_count[to] = static_cast<int32_t>(ax.moving.size());
+      ++to;
+      for (int m : ax.moving) moving[mo++] = m;
+    }
+  }
+  return VS_OK;
+}
+
+void vs_libbuild_free(vs_libbuild* b) { delete b; }
+
+// ---------------------------------------------------------------- batcher --
+int vs_default_classes(vs_size_class* out, int32_t cap) {
+  static const int atoms[4] = {1, 20, 40, 80};  // batcher.cpp:9-10
+  static const int rots[3] = {0, 4, 12};
+  if (cap < 6) return VS_ERR_CAPACITY;
+  int k = 0;
+  for (int ai = 0; ai < 3; ++ai)
+    for (int ri = 0; ri < 2; ++ri) out[k++] = {atoms[ai], atoms[ai + 1], rots[ri], rots[ri + 1]};
+  return k;
+}
+
+int vs_size_class_of(int32_t atoms, int32_t rot, const vs_size_class* c, int32_t n) {
+  for (int i = 0; i < n; ++i) {
+    if (atoms >= c[i].atom_lo && atoms < c[i].atom_hi && rot >= c[i].rot_lo && rot < c[i].rot_hi)
+      return i;
+  }
+  return VS_ERR_OUT_OF_RANGE;
+}
+
+int vs_target_batch_size(const vs_size_class* cls, double cap, double fixed, double per_atom,
+                         double per_rot, int64_t* out) {
+  const double item = per_atom * cls->atom_hi + per_rot * cls->rot_hi;
+  const double budget = cap - fixed;
+  if (item > budget) return VS_ERR_ITEM_TOO_LARGE;
+  if (item <= 0.0) {
+    *out = 1;
+    return VS_OK;
+  }
+  const auto n = static_cast<int64_t>(std::floor(budget / item));
+  *out = n < 1 ? 1 : n;
+  return VS_OK;
+}
+
+double vs_simulate_throughput(int64_t n_items, double overhead, double service) {
+  const double n = static_cast<double>(n_items);
+  return n / (overhead + n * service);
+}
+
+int vs_bucket_replay(const int32_t* atoms, const int32_t* rot, int32_t n,
+                     const vs_size_class* classes, int32_t nc, double cap, double fixed,
+                     double per_atom, double per_rot, double max_age, int32_t* in_range,
+                     int32_t* batch_cls, int32_t* batch_len, int32_t* members) {
+  std::vector<int64_t> target(static_cast<std::size_t>(nc));
+  for (int c = 0; c < nc; ++c) {
+    const int rc = vs_target_batch_size(&classes[c], cap, fixed, per_atom, per_rot, &target[c]);
+    if (rc) return rc;
+  }
+  struct Pending {
+    std::vector<int> ids;
+    std::vector<double> t;
+    std::size_t head = 0;
+  };
+  std::vector<Pending> buf(static_cast<std::size_t>(nc));
+  int nb = 0, nm = 0;
+  auto emit = [&](int c) {
+    batch_cls[nb] = c;
+    batch_len[nb] = static_cast<int32_t>(buf[c].ids.size());
+    for (int id : buf[c].ids) members[nm++] = id;
+    ++nb;
+    buf[c].ids.clear();
+    buf[c].t.clear();
+  };
+  double now = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const int c = vs_size_class_of(atoms[i], rot[i], classes, nc);
+    if (c < 0) {
+      in_range[i] = 0;
+      continue;
+    }
+    in_range[i] = 1;
+    now += 0.001;  // pipeline.cpp:453
+    for (int k = 0; k < nc; ++k) {  // flush_aged (batcher.cpp:69-77)
+      if (!buf[k].ids.empty() && now - buf[k].t.front() > max_age) emit(k);
+    }
+    buf[c].ids.push_back(i);  // enqueue (batcher.cpp:59-67)
+    buf[c].t.push_back(now);
+    if (static_cast<int64_t>(buf[c].ids.size()) >= target[c]) emit(c);
+  }
+  for (int k = 0; k < nc; ++k)
+    if (!buf[k].ids.empty()) emit(k);
+  return nb;
+}
+
+int vs_campaign_seeds(uint64_t master, int32_t stage, const int32_t* in_range, int32_t n,
+                      uint64_t* out) {
+  const HostRng st = HostRng(master).split(static_cast<std::uint64_t>(stage));
+  std::uint64_t idx = 0;
+  for (int i = 0; i < n; ++i) {
+    if (in_range && !in_range[i]) {
+      out[i] = 0;
+      continue;
+    }
+    HostRng r = st.split(idx++);
+    out[i] = r.next_u64();
+  }
+  return VS_OK;
+}
+
+int vs_filter_poses(const double* scores, int32_t n, int64_t keep_top, double min_score,
+                    int32_t* out_idx) {
+  std::vector<int32_t> idx;
+  for (int i = 0; i < n; ++i)
+    if (scores[i] >= min_score) idx.push_back(i);
+  if (static_cast<int64_t>(idx.size()) > keep_top) {
+    std::stable_sort(idx.begin(), idx.end(),
+                     [&](int32_t a, int32_t b) { return scores[a] > scores[b]; });
+    idx.resize(static_cast<std::size_t>(keep_top));
+    std::sort(idx.begin(), idx.end());
+  }
+  std::copy(idx.begin(), idx.end(), out_idx);
+  return static_cast<int>(idx.size());
+}
+
+int vs_id_ranks(const char* blob, int32_t n, uint32_t* out_rank) {
+  const auto ids = split_blob(blob, n);
+  std::vector<int32_t> ord(static_cast<std::size_t>(n));
+  std::iota(ord.begin(), ord.end(), 0);
+  std::sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) { return ids[a] < ids[b]; });
+  for (int r = 0; r < n; ++r) out_rank[ord[r]] = static_cast<uint32_t>(r);
+  return VS_OK;
+}
+
+// rank_ligands: std::map iteration (bytewise id order; a repeated id keeps
+// its last score, as map operator[] does) then stable sort by score desc.
+int vs_rank_ligands(const char* blob, const double* scores, int32_t n, int32_t* out_order) {
+  const auto ids = split_blob(blob, n);
+  std::vector<int32_t> ord(static_cast<std::size_t>(n));
+  std::iota(ord.begin(), ord.end(), 0);
+  std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) { return ids[a] < ids[b]; });
+  std::vector<int32_t> uniq;
+  for (std::size_t k = 0; k < ord.size(); ++k) {
+    if (k + 1 < ord.size() && ids[ord[k]] == ids[ord[k + 1]]) continue;  // last one wins
+    uniq.push_back(ord[k]);
+  }
+  std::stable_sort(uniq.begin(), uniq.end(),
+                   [&](int32_t a, int32_t b) { return scores[a] > scores[b]; });
+  std::copy(uniq.begin(), uniq.end(), out_order);
+  return static_cast<int>(uniq.size());
+}
+
+}  // extern "C"

@@ -1,0 +1,768 @@
+// GPU runtime behind the C-ABI (capi.h "GPU runtime" section): device
+// handle, pocket upload + grid build, the library packer (size-class
+// buckets, SoA, LPT order), dock launches per bucket, results, top-k and
+// the rescoring path.  Host C++; the kernels live in vs_kernels.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/vscreen_gpu/capi.h"
+#include "vs_rng.h"
+#include "vs_types.h"
+
+namespace vs {
+size_t dock_smem_per_block(int nmax, int tmax, int mvmax);
+int dock_blocks_per_sm(bool grid, size_t smem);
+cudaError_t launch_dock(bool grid, int blocks, size_t smem, cudaStream_t st, const LibDev& lib,
+                        const PocketDev& pk, const float4* rots, const DockParams& prm,
+                        const int* order, int n_order, int* counter, int nmax, int tmax,
+                        int mvmax, float4* sx, float* sp, int* sm, const DockOut& out);
+cudaError_t launch_rescore(bool grid, int blocks, size_t smem, cudaStream_t st, const LibDev& lib,
+                           const PocketDev& pk, const int* ligs, int n_ligs, int* counter,
+                           const int* pose_off, const long* tors_base, const float4* pt,
+                           const float4* pq, const float* ptors, int nmax, int tmax, int mvmax,
+                           float* geo, float* resc);
+cudaError_t launch_grid(cudaStream_t st, const PocketDev& pk, float* steric, float* hb,
+                        float* lipo);
+int topk_chunk();
+cudaError_t launch_topk(cudaStream_t st, const unsigned long long* in, long n,
+                        unsigned long long* out, int k, int blocks);
+}  // namespace vs
+
+using namespace vs;
+
+namespace {
+
+// grow-only device buffer
+struct DBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    const size_t want = std::max<size_t>(bytes, 256);
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+struct Bucket {
+  int start = 0, count = 0;  // range in the order array
+  int nmax = 1, tmax = 1, mvmax = 16;
+};
+
+// Packed library (host staging + device copies) for one set of ligands.
+struct Packed {
+  int n = 0;
+  std::vector<int4> meta;
+  std::vector<int2> mov;
+  std::vector<double4> atoms;
+  std::vector<int4> axes;
+  std::vector<uint8_t> moving;
+  std::vector<unsigned long long> seeds;
+  std::vector<unsigned int> id_rank;
+  std::vector<int> order;
+  std::vector<int> cls;          // class per ligand (-1 dropped)
+  std::vector<long> tors_off;    // prefix sum of n_tors
+  std::vector<Bucket> buckets;
+  long total_tors = 0;
+  DBuf d_meta, d_mov, d_atoms, d_axes, d_moving, d_seeds, d_idr, d_order;
+  void release() {
+    d_meta.release(); d_mov.release(); d_atoms.release(); d_axes.release();
+    d_moving.release(); d_seeds.release(); d_idr.release(); d_order.release();
+  }
+  LibDev dev() const {
+    LibDev l;
+    l.meta = d_meta.as<const int4>();
+    l.mov = d_mov.as<const int2>();
+    l.atoms = d_atoms.as<const double4>();
+    l.axes = d_axes.as<const int4>();
+    l.moving = d_moving.as<const uint8_t>();
+    l.seeds = d_seeds.as<const unsigned long long>();
+    l.id_rank = d_idr.as<const unsigned int>();
+    return l;
+  }
+};
+
+}  // namespace
+
+struct vs_handle {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t last = nullptr;
+  std::string err;
+  int sms = 148;
+  char name[256] = {0};
+  int clock_khz = 0;
+  uint64_t launches = 0;
+  // pocket
+  bool has_pocket = false;
+  bool empty_bounds = false;
+  PocketDev pk{};
+  DBuf d_sites, d_maps;
+  int gdims[3] = {0, 0, 0};
+  // library + results
+  bool has_lib = false;
+  Packed lib;
+  vs_dock_params last_prm{};
+  bool has_results = false;
+  DBuf d_surv, d_surv_tors, d_all, d_all_tors, d_best, d_nkept, d_nsurv, d_keys, d_counters;
+  DBuf d_sx, d_sp, d_sm, d_rots, d_topk_a, d_topk_b;
+  int rots_k = -1;
+  uint64_t rots_seed = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  bool timed = false;
+};
+
+namespace {
+
+int fail(vs_handle* h, int code, const std::string& msg) {
+  if (h) h->err = msg;
+  return code;
+}
+
+int cuda_fail(vs_handle* h, cudaError_t e, const char* what) {
+  return fail(h, VS_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define VS_CUDA(h, call)                                  \
+  do {                                                    \
+    cudaError_t e_ = (call);                              \
+    if (e_ != cudaSuccess) return cuda_fail(h, e_, #call); \
+  } while (0)
+
+cudaStream_t pick(vs_handle* h, void* s) {
+  h->last = s ? static_cast<cudaStream_t>(s) : h->own;
+  return h->last;
+}
+
+size_t align16z(size_t x) { return (x + 15) & ~size_t(15); }
+
+// Validation + packing of a host library (SURVEY §8 row A7/A11 checks:
+// AtomCountMismatch for empty conformers and axes outside the conformer).
+int pack_library(vs_handle* h, const vs_library* L, const vs_size_class* classes, int nc,
+                 Packed& P) {
+  const int n = L->n_ligands;
+  if (n < 0) return fail(h, VS_ERR_INVALID_ARGUMENT, "negative ligand count");
+  P.n = n;
+  P.meta.assign(n, int4{0, 0, 0, 0});
+  P.mov.assign(n, int2{0, 0});
+  P.atoms.clear();
+  P.axes.clear();
+  P.moving.clear();
+  P.seeds.assign(n, 0ull);
+  P.id_rank.assign(n, 0u);
+  P.cls.assign(n, -1);
+  P.tors_off.assign(n + 1, 0);
+  long ao = 0, to = 0, mo = 0;
+  std::vector<long> cost(n, 0);
+  for (int i = 0; i < n; ++i) {
+    const int N = L->n_atoms[i], T = L->n_tors[i];
+    if (N < 1) return fail(h, VS_ERR_ATOM_COUNT, "conformer has no atoms (ligand " + std::to_string(i) + ")");
+    if (N > kMaxAtoms || T > kMaxTors)
+      return fail(h, VS_ERR_CAPACITY, "ligand " + std::to_string(i) + " exceeds GPU limits");
+    P.tors_off[i] = to;
+    P.meta[i] = int4{static_cast<int>(P.atoms.size()), N, static_cast<int>(P.axes.size()), T};
+    for (int a = 0; a < N; ++a) {
+      const double* c = L->coords + 3 * (ao + a);
+      P.atoms.push_back(double4{c[0], c[1], c[2], static_cast<double>(L->atom_class[ao + a])});
+    }
+    const size_t mov_start = P.moving.size();
+    int mv = 0;
+    for (int j = 0; j < T; ++j) {
+      const int a = L->axis_a[to + j], b = L->axis_b[to + j], cnt = L->moving_count[to + j];
+      if (a < 0 || b < 0 || a >= N || b >= N)
+        return fail(h, VS_ERR_ATOM_COUNT, "torsion topology does not fit conformer");
+      P.axes.push_back(int4{a, b, mv, cnt});
+      for (int m = 0; m < cnt; ++m) {
+        const int idx = L->moving[mo + m];
+        if (idx < 0 || idx >= N)
+          return fail(h, VS_ERR_ATOM_COUNT, "moving atom outside conformer");
+        P.moving.push_back(static_cast<uint8_t>(idx));
+      }
+      mo += cnt;
+      mv += cnt;
+    }
+    const size_t padded = align16z(static_cast<size_t>(mv));
+    P.moving.resize(mov_start + padded, 0);
+    P.mov[i] = int2{static_cast<int>(mov_start), static_cast<int>(padded)};
+    P.seeds[i] = L->seeds ? L->seeds[i] : 0ull;
+    P.id_rank[i] = L->id_rank ? L->id_rank[i] : static_cast<unsigned>(i);
+    const int rot = L->rot_bonds ? L->rot_bonds[i] : T;
+    if (classes && nc > 0) {
+      P.cls[i] = vs_size_class_of(N, rot, classes, nc);
+      if (P.cls[i] < 0) P.cls[i] = -1;
+    } else {
+      P.cls[i] = N <= 16 ? 0 : N <= 32 ? 1 : N <= 48 ? 2 : N <= 64 ? 3 : N <= 96 ? 4 : 5;
+    }
+    const long pairs = static_cast<long>(N) * (N - 1) / 2;
+    cost[i] = 256L * N + 32L * T * (N + pairs + mv);
+    ao += N;
+    to += T;
+  }
+  P.tors_off[n] = to;
+  P.total_tors = to;
+  if (P.atoms.empty()) P.atoms.push_back(double4{0, 0, 0, 0});
+  if (P.axes.empty()) P.axes.push_back(int4{0, 0, 0, 0});
+  if (P.moving.empty()) P.moving.assign(16, 0);
+  // buckets: class order, LPT (descending cost, then index) inside
+  const int ncls = (classes && nc > 0) ? nc : 6;
+  P.order.clear();
+  P.buckets.clear();
+  for (int c = 0; c < ncls; ++c) {
+    Bucket b;
+    b.start = static_cast<int>(P.order.size());
+    std::vector<int> ids;
+    for (int i = 0; i < n; ++i)
+      if (P.cls[i] == c) ids.push_back(i);
+    if (ids.empty()) continue;
+    std::stable_sort(ids.begin(), ids.end(), [&](int a, int b2) { return cost[a] > cost[b2]; });
+    for (int i : ids) {
+      b.nmax = std::max(b.nmax, P.meta[i].y);
+      b.tmax = std::max(b.tmax, P.meta[i].w);
+      b.mvmax = std::max(b.mvmax, P.mov[i].y);
+      P.order.push_back(i);
+    }
+    b.count = static_cast<int>(ids.size());
+    P.buckets.push_back(b);
+  }
+  if (P.order.empty()) P.order.push_back(0);
+  return VS_OK;
+}
+
+int upload_packed(vs_handle* h, Packed& P, cudaStream_t st) {
+  auto up = [&](DBuf& d, const void* src, size_t bytes) -> cudaError_t {
+    cudaError_t e = d.ensure(bytes);
+    if (e != cudaSuccess) return e;
+    return cudaMemcpyAsync(d.p, src, bytes, cudaMemcpyHostToDevice, st);
+  };
+  VS_CUDA(h, up(P.d_meta, P.meta.data(), std::max<size_t>(16, P.meta.size() * sizeof(int4))));
+  VS_CUDA(h, up(P.d_mov, P.mov.data(), std::max<size_t>(8, P.mov.size() * sizeof(int2))));
+  VS_CUDA(h, up(P.d_atoms, P.atoms.data(), P.atoms.size() * sizeof(double4)));
+  VS_CUDA(h, up(P.d_axes, P.axes.data(), P.axes.size() * sizeof(int4)));
+  VS_CUDA(h, up(P.d_moving, P.moving.data(), P.moving.size()));
+  VS_CUDA(h, up(P.d_seeds, P.seeds.data(), std::max<size_t>(8, P.seeds.size() * 8)));
+  VS_CUDA(h, up(P.d_idr, P.id_rank.data(), std::max<size_t>(4, P.id_rank.size() * 4)));
+  VS_CUDA(h, up(P.d_order, P.order.data(), P.order.size() * sizeof(int)));
+  return VS_OK;
+}
+
+int check_params(vs_handle* h, const vs_dock_params* p) {
+  if (p->restarts < 1) return fail(h, VS_ERR_INVALID_ARGUMENT, "restarts must be >= 1");
+  if (p->diversity_delta < 0.0)
+    return fail(h, VS_ERR_INVALID_ARGUMENT, "diversity_delta must be >= 0");
+  if (p->restarts > kMaxRestarts) return fail(h, VS_ERR_CAPACITY, "restarts > 64");
+  if (p->flex_angles < 1 || p->flex_angles > kMaxFlexAngles)
+    return fail(h, VS_ERR_CAPACITY, "flex_angles must be in [1, 16]");
+  if (p->rotations < 1) return fail(h, VS_ERR_INVALID_ARGUMENT, "rotations must be >= 1");
+  if (p->flex_passes < 0 || p->keep_top < 0)
+    return fail(h, VS_ERR_INVALID_ARGUMENT, "negative flex_passes/keep_top");
+  return VS_OK;
+}
+
+// Fixed rotation set of the sweep: k = 0 identity, k >= 1 the normalized
+// 4-normal draw of Rng(seed).split(k) (FP64, then rounded to FP32).
+std::vector<float4> rotation_set(int K, uint64_t seed) {
+  std::vector<float4> r(static_cast<size_t>(K));
+  const HostRng root(seed);
+  for (int k = 0; k < K; ++k) {
+    if (k == 0) {
+      r[0] = float4{1.0f, 0.0f, 0.0f, 0.0f};
+      continue;
+    }
+    HostRng g = root.split(static_cast<uint64_t>(k));
+    const double w = g.normal(), x = g.normal(), y = g.normal(), z = g.normal();
+    const double n = std::sqrt(w * w + x * x + y * y + z * z);
+    r[k] = float4{static_cast<float>(w / n), static_cast<float>(x / n), static_cast<float>(y / n),
+                  static_cast<float>(z / n)};
+  }
+  return r;
+}
+
+}  // namespace
+
+extern "C" {
+
+int vs_create(int device, vs_handle** out) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return VS_ERR_NO_DEVICE;
+  }
+  if (device < 0 || device >= count) return VS_ERR_NO_DEVICE;
+  auto* h = new vs_handle;
+  h->device = device;
+  cudaSetDevice(device);
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, device);
+  h->sms = prop.multiProcessorCount;
+  std::snprintf(h->name, sizeof(h->name), "%s", prop.name);
+  cudaDeviceGetAttribute(&h->clock_khz, cudaDevAttrClockRate, device);
+  if (cudaStreamCreateWithFlags(&h->own, cudaStreamNonBlocking) != cudaSuccess) {
+    delete h;
+    return VS_ERR_CUDA;
+  }
+  cudaEventCreate(&h->ev0);
+  cudaEventCreate(&h->ev1);
+  h->last = h->own;
+  *out = h;
+  return VS_OK;
+}
+
+void vs_destroy(vs_handle* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  cudaStreamSynchronize(h->own);
+  h->lib.release();
+  for (DBuf* b : {&h->d_sites, &h->d_maps, &h->d_surv, &h->d_surv_tors, &h->d_all, &h->d_all_tors,
+                  &h->d_best, &h->d_nkept, &h->d_nsurv, &h->d_keys, &h->d_counters, &h->d_sx,
+                  &h->d_sp, &h->d_sm, &h->d_rots, &h->d_topk_a, &h->d_topk_b})
+    b->release();
+  cudaEventDestroy(h->ev0);
+  cudaEventDestroy(h->ev1);
+  cudaStreamDestroy(h->own);
+  delete h;
+}
+
+const char* vs_last_error(const vs_handle* h) { return h ? h->err.c_str() : "null handle"; }
+
+int vs_device_info(const vs_handle* h, char* name, int32_t* sm_count, int32_t* clock_khz) {
+  if (name) std::snprintf(name, 256, "%s", h->name);
+  if (sm_count) *sm_count = h->sms;
+  if (clock_khz) *clock_khz = h->clock_khz;
+  return VS_OK;
+}
+
+int vs_set_pocket(vs_handle* h, const vs_pocket* p, double spacing, double pad) {
+  cudaSetDevice(h->device);
+  cudaStream_t st = h->own;
+  std::vector<SiteF> sites;
+  int counts[3] = {0, 0, 0};
+  for (int kind = 0; kind < 3; ++kind) {
+    for (int s = 0; s < p->n_sites; ++s) {
+      const vs_site& v = p->sites[s];
+      if (v.kind < 0 || v.kind > 2) return fail(h, VS_ERR_POCKET, "unknown site kind");
+      if (!(v.sigma > 0.0)) return fail(h, VS_ERR_POCKET, "site sigma must be > 0");
+      if (v.kind != kind) continue;
+      SiteF f{};
+      f.cx = static_cast<float>(v.center[0]);
+      f.cy = static_cast<float>(v.center[1]);
+      f.cz = static_cast<float>(v.center[2]);
+      f.w = static_cast<float>(v.weight);
+      f.inv2s2 = static_cast<float>(1.0 / (2.0 * v.sigma * v.sigma));
+      sites.push_back(f);
+      ++counts[kind];
+    }
+  }
+  if (p->clash_penalty < 0.0) return fail(h, VS_ERR_POCKET, "clash_penalty must be >= 0");
+  if (sites.empty()) sites.push_back(SiteF{});
+  VS_CUDA(h, h->d_sites.ensure(sites.size() * sizeof(SiteF)));
+  VS_CUDA(h, cudaMemcpyAsync(h->d_sites.p, sites.data(), sites.size() * sizeof(SiteF),
+                             cudaMemcpyHostToDevice, st));
+  PocketDev& pk = h->pk;
+  pk = PocketDev{};
+  for (int c = 0; c < 3; ++c) {
+    pk.lo[c] = static_cast<float>(p->lo[c]);
+    pk.hi[c] = static_cast<float>(p->hi[c]);
+    pk.lo_d[c] = p->lo[c];
+    pk.hi_d[c] = p->hi[c];
+  }
+  h->empty_bounds = p->hi[0] <= p->lo[0] || p->hi[1] <= p->lo[1] || p->hi[2] <= p->lo[2];
+  pk.r = static_cast<float>(p->clash_radius);
+  pk.lam = static_cast<float>(p->clash_penalty);
+  const float rr = pk.r + 3.0f;
+  pk.cut2 = rr * rr;
+  pk.n_steric = counts[0];
+  pk.n_hbond = counts[1];
+  pk.n_lipo = counts[2];
+  pk.sites = h->d_sites.as<const SiteF>();
+  pk.grid_mode = 0;
+  h->gdims[0] = h->gdims[1] = h->gdims[2] = 0;
+  if (spacing > 0.0 && !h->empty_bounds) {
+    GridDev& g = pk.grid;
+    g.h = static_cast<float>(spacing);
+    g.inv_h = 1.0f / g.h;
+    g.ox = static_cast<float>(p->lo[0] - pad);
+    g.oy = static_cast<float>(p->lo[1] - pad);
+    g.oz = static_cast<float>(p->lo[2] - pad);
+    int* dims[3] = {&g.nx, &g.ny, &g.nz};
+    for (int c = 0; c < 3; ++c)
+      *dims[c] = static_cast<int>(std::ceil((p->hi[c] - p->lo[c] + 2.0 * pad) / spacing)) + 1;
+    const size_t nodes = static_cast<size_t>(g.nx) * g.ny * g.nz;
+    VS_CUDA(h, h->d_maps.ensure(3 * nodes * sizeof(float)));
+    float* m = h->d_maps.as<float>();
+    g.steric = m;
+    g.hbond = m + nodes;
+    g.lipo = m + 2 * nodes;
+    VS_CUDA(h, launch_grid(st, pk, m, m + nodes, m + 2 * nodes));
+    ++h->launches;
+    pk.grid_mode = 1;
+    h->gdims[0] = g.nx;
+    h->gdims[1] = g.ny;
+    h->gdims[2] = g.nz;
+  }
+  VS_CUDA(h, cudaStreamSynchronize(st));
+  h->has_pocket = true;
+  return VS_OK;
+}
+
+int vs_grid_info(const vs_handle* h, int32_t dims[3], float origin[3], float* spacing) {
+  for (int c = 0; c < 3; ++c) dims[c] = h->gdims[c];
+  origin[0] = h->pk.grid.ox;
+  origin[1] = h->pk.grid.oy;
+  origin[2] = h->pk.grid.oz;
+  *spacing = h->pk.grid.h;
+  return h->pk.grid_mode ? VS_OK : VS_ERR_STATE;
+}
+
+int vs_grid_fetch(vs_handle* h, float* steric, float* hbond, float* lipo) {
+  if (!h->pk.grid_mode) return fail(h, VS_ERR_STATE, "no grid maps");
+  const size_t nodes = static_cast<size_t>(h->gdims[0]) * h->gdims[1] * h->gdims[2];
+  const float* m = h->d_maps.as<float>();
+  VS_CUDA(h, cudaMemcpy(steric, m, nodes * 4, cudaMemcpyDeviceToHost));
+  VS_CUDA(h, cudaMemcpy(hbond, m + nodes, nodes * 4, cudaMemcpyDeviceToHost));
+  VS_CUDA(h, cudaMemcpy(lipo, m + 2 * nodes, nodes * 4, cudaMemcpyDeviceToHost));
+  return VS_OK;
+}
+
+int vs_upload_library(vs_handle* h, const vs_library* L, const vs_size_class* classes,
+                      int32_t nc) {
+  cudaSetDevice(h->device);
+  h->has_lib = false;
+  h->has_results = false;
+  int rc = pack_library(h, L, classes, nc, h->lib);
+  if (rc) return rc;
+  rc = upload_packed(h, h->lib, h->own);
+  if (rc) return rc;
+  VS_CUDA(h, cudaStreamSynchronize(h->own));
+  h->has_lib = true;
+  return VS_OK;
+}
+
+int vs_dock(vs_handle* h, const vs_dock_params* prm, void* stream) {
+  cudaSetDevice(h->device);
+  if (!h->has_pocket) return fail(h, VS_ERR_STATE, "no pocket");
+  if (!h->has_lib) return fail(h, VS_ERR_STATE, "no library");
+  if (h->empty_bounds) return fail(h, VS_ERR_EMPTY_BOUNDS, "pocket bounds box is empty");
+  int rc = check_params(h, prm);
+  if (rc) return rc;
+  cudaStream_t st = pick(h, stream);
+  Packed& P = h->lib;
+  const int n = P.n;
+  const int R = prm->restarts, KT = prm->keep_top;
+  if (h->rots_k != prm->rotations || h->rots_seed != prm->rotation_seed) {
+    const auto rs = rotation_set(prm->rotations, prm->rotation_seed);
+    VS_CUDA(h, h->d_rots.ensure(rs.size() * sizeof(float4)));
+    VS_CUDA(h, cudaMemcpyAsync(h->d_rots.p, rs.data(), rs.size() * sizeof(float4),
+                               cudaMemcpyHostToDevice, st));
+    VS_CUDA(h, cudaStreamSynchronize(st));
+    h->rots_k = prm->rotations;
+    h->rots_seed = prm->rotation_seed;
+  }
+  const size_t nn = static_cast<size_t>(std::max(n, 1));
+  VS_CUDA(h, h->d_surv.ensure(nn * std::max(KT, 1) * sizeof(PoseOut)));
+  VS_CUDA(h, h->d_surv_tors.ensure(std::max<size_t>(1, P.total_tors) * std::max(KT, 1) * 4));
+  if (prm->write_all_poses) {
+    VS_CUDA(h, h->d_all.ensure(nn * R * sizeof(PoseOut)));
+    VS_CUDA(h, h->d_all_tors.ensure(std::max<size_t>(1, P.total_tors) * R * 4));
+  }
+  VS_CUDA(h, h->d_best.ensure(nn * 4));
+  VS_CUDA(h, h->d_nkept.ensure(nn * 4));
+  VS_CUDA(h, h->d_nsurv.ensure(nn * 4));
+  VS_CUDA(h, h->d_keys.ensure(nn * 8));
+  VS_CUDA(h, h->d_counters.ensure(64 * sizeof(int)));
+  VS_CUDA(h, cudaMemsetAsync(h->d_keys.p, 0xff, nn * 8, st));
+  VS_CUDA(h, cudaMemsetAsync(h->d_nkept.p, 0, nn * 4, st));
+  VS_CUDA(h, cudaMemsetAsync(h->d_nsurv.p, 0, nn * 4, st));
+  VS_CUDA(h, cudaMemsetAsync(h->d_counters.p, 0, 64 * sizeof(int), st));
+
+  DockParams dp;
+  dp.R = R;
+  dp.K = prm->rotations;
+  dp.A = prm->flex_angles;
+  dp.F = prm->flex_passes;
+  dp.keep_top = KT;
+  dp.write_all = prm->write_all_poses ? 1 : 0;
+  dp.delta = static_cast<float>(prm->diversity_delta);
+  dp.min_score = prm->min_score;
+  DockOut out;
+  out.surv = h->d_surv.as<PoseOut>();
+  out.surv_tors = h->d_surv_tors.as<float>();
+  out.all = prm->write_all_poses ? h->d_all.as<PoseOut>() : nullptr;
+  out.all_tors = prm->write_all_poses ? h->d_all_tors.as<float>() : nullptr;
+  out.best = h->d_best.as<float>();
+  out.n_kept = h->d_nkept.as<int>();
+  out.n_surv = h->d_nsurv.as<int>();
+  out.keys = h->d_keys.as<unsigned long long>();
+
+  const bool grid = h->pk.grid_mode != 0;
+  const LibDev ld = P.dev();
+  // plan launches and scratch (persistent warps, one scratch slot each)
+  struct Plan {
+    int blocks;
+    size_t smem;
+  };
+  std::vector<Plan> plans;
+  size_t need_x = 0, need_p = 0, need_m = 0;
+  for (const Bucket& b : P.buckets) {
+    const size_t smem = dock_smem_per_block(b.nmax, b.tmax, b.mvmax);
+    if (smem > 227 * 1024) return fail(h, VS_ERR_CAPACITY, "bucket needs too much shared memory");
+    int per_sm = dock_blocks_per_sm(grid, smem);
+    if (per_sm < 1) per_sm = 1;
+    const int want = (b.count + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    const int blocks = std::max(1, std::min(want, per_sm * h->sms));
+    plans.push_back({blocks, smem});
+    const size_t warps = static_cast<size_t>(blocks) * kWarpsPerBlock;
+    need_x = std::max(need_x, warps * R * b.nmax * sizeof(float4));
+    need_p = std::max(need_p, warps * R * (8 + b.tmax) * sizeof(float));
+    need_m = std::max(need_m, warps * R * 4 * sizeof(int));
+  }
+  VS_CUDA(h, h->d_sx.ensure(need_x));
+  VS_CUDA(h, h->d_sp.ensure(need_p));
+  VS_CUDA(h, h->d_sm.ensure(need_m));
+  VS_CUDA(h, cudaEventRecord(h->ev0, st));
+  for (size_t bi = 0; bi < P.buckets.size(); ++bi) {
+    const Bucket& b = P.buckets[bi];
+    VS_CUDA(h, launch_dock(grid, plans[bi].blocks, plans[bi].smem, st, ld, h->pk,
+                           h->d_rots.as<const float4>(), dp, P.d_order.as<int>() + b.start,
+                           b.count, h->d_counters.as<int>() + (bi % 64), b.nmax, b.tmax, b.mvmax,
+                           h->d_sx.as<float4>(), h->d_sp.as<float>(), h->d_sm.as<int>(), out));
+    ++h->launches;
+  }
+  VS_CUDA(h, cudaEventRecord(h->ev1, st));
+  h->timed = true;
+  h->last_prm = *prm;
+  h->has_results = true;
+  return VS_OK;
+}
+
+double vs_last_dock_ms(const vs_handle* h) {
+  if (!h->timed) return -1.0;
+  cudaEventSynchronize(h->ev1);
+  float ms = 0.0f;
+  cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+  return ms;
+}
+
+uint64_t vs_launch_count(const vs_handle* h) { return h->launches; }
+
+int vs_fetch_results(vs_handle* h, vs_results* o) {
+  cudaSetDevice(h->device);
+  if (!h->has_results) return fail(h, VS_ERR_STATE, "no results");
+  cudaStream_t st = h->last;
+  const Packed& P = h->lib;
+  const size_t n = static_cast<size_t>(P.n);
+  const int KT = h->last_prm.keep_top, R = h->last_prm.restarts;
+  if (o->best) VS_CUDA(h, cudaMemcpyAsync(o->best, h->d_best.p, n * 4, cudaMemcpyDeviceToHost, st));
+  if (o->n_kept) VS_CUDA(h, cudaMemcpyAsync(o->n_kept, h->d_nkept.p, n * 4, cudaMemcpyDeviceToHost, st));
+  if (o->n_surv) VS_CUDA(h, cudaMemcpyAsync(o->n_surv, h->d_nsurv.p, n * 4, cudaMemcpyDeviceToHost, st));
+  if (o->surv && KT > 0)
+    VS_CUDA(h, cudaMemcpyAsync(o->surv, h->d_surv.p, n * KT * sizeof(vs_pose), cudaMemcpyDeviceToHost, st));
+  if (o->surv_tors && KT > 0 && P.total_tors > 0)
+    VS_CUDA(h, cudaMemcpyAsync(o->surv_tors, h->d_surv_tors.p, P.total_tors * KT * 4, cudaMemcpyDeviceToHost, st));
+  if (o->all && h->last_prm.write_all_poses)
+    VS_CUDA(h, cudaMemcpyAsync(o->all, h->d_all.p, n * R * sizeof(vs_pose), cudaMemcpyDeviceToHost, st));
+  if (o->all_tors && h->last_prm.write_all_poses && P.total_tors > 0)
+    VS_CUDA(h, cudaMemcpyAsync(o->all_tors, h->d_all_tors.p, P.total_tors * R * 4, cudaMemcpyDeviceToHost, st));
+  if (o->keys) VS_CUDA(h, cudaMemcpyAsync(o->keys, h->d_keys.p, n * 8, cudaMemcpyDeviceToHost, st));
+  VS_CUDA(h, cudaStreamSynchronize(st));
+  for (size_t i = 0; i < n; ++i) {
+    if (P.cls[i] < 0) {
+      if (o->n_kept) o->n_kept[i] = -1;
+      if (o->n_surv) o->n_surv[i] = 0;
+      if (o->best) o->best[i] = -INFINITY;
+    } else if (o->best && o->n_surv && o->n_surv[i] == 0) {
+      o->best[i] = -INFINITY;
+    }
+  }
+  return VS_OK;
+}
+
+int vs_dock_host(vs_handle* h, const vs_library* L, const vs_size_class* classes, int32_t nc,
+                 const vs_dock_params* prm, vs_results* out) {
+  int rc = vs_upload_library(h, L, classes, nc);
+  if (rc) return rc;
+  rc = vs_dock(h, prm, nullptr);
+  if (rc) return rc;
+  return vs_fetch_results(h, out);
+}
+
+// tournament: chunks of C keys -> k smallest each, until one chunk remains
+static int topk_run(vs_handle* h, const unsigned long long* in, long n, int k,
+                    unsigned long long* out_dev, cudaStream_t st) {
+  const int C = topk_chunk();
+  if (k < 1 || 2 * k > C) return fail(h, VS_ERR_CAPACITY, "top-k needs 1 <= k <= 2048");
+  long cur = std::max<long>(n, 1);
+  const unsigned long long* src = in;
+  bool first = true;
+  while (true) {
+    const long blocks = (cur + C - 1) / C;
+    unsigned long long* dst;
+    if (blocks == 1) {
+      dst = out_dev;
+    } else {
+      DBuf& tgt = (first || src == h->d_topk_b.as<unsigned long long>()) ? h->d_topk_a : h->d_topk_b;
+      VS_CUDA(h, tgt.ensure(static_cast<size_t>(blocks) * k * 8));
+      dst = tgt.as<unsigned long long>();
+    }
+    VS_CUDA(h, launch_topk(st, src, first ? n : cur, dst, k, static_cast<int>(blocks)));
+    ++h->launches;
+    if (blocks == 1) break;
+    cur = blocks * k;
+    src = dst;
+    first = false;
+  }
+  return VS_OK;
+}
+
+int vs_topk_device(vs_handle* h, int32_t k, uint64_t* out_dev, void* stream) {
+  cudaSetDevice(h->device);
+  if (!h->has_results) return fail(h, VS_ERR_STATE, "no results");
+  cudaStream_t st = pick(h, stream);
+  return topk_run(h, h->d_keys.as<unsigned long long>(), h->lib.n, k,
+                  reinterpret_cast<unsigned long long*>(out_dev), st);
+}
+
+int vs_topk_merge_device(vs_handle* h, const uint64_t* keys_dev, int64_t n, int32_t k,
+                         uint64_t* out_dev, void* stream) {
+  cudaSetDevice(h->device);
+  cudaStream_t st = pick(h, stream);
+  return topk_run(h, reinterpret_cast<const unsigned long long*>(keys_dev), static_cast<long>(n),
+                  k, reinterpret_cast<unsigned long long*>(out_dev), st);
+}
+
+int vs_topk(vs_handle* h, int32_t k, uint64_t* out_keys) {
+  DBuf tmp;
+  VS_CUDA(h, tmp.ensure(static_cast<size_t>(k) * 8));
+  int rc = vs_topk_device(h, k, tmp.as<uint64_t>(), nullptr);
+  if (rc == VS_OK) {
+    cudaError_t e = cudaMemcpyAsync(out_keys, tmp.p, static_cast<size_t>(k) * 8,
+                                    cudaMemcpyDeviceToHost, h->last);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->last);
+    if (e != cudaSuccess) rc = cuda_fail(h, e, "topk fetch");
+  }
+  tmp.release();
+  return rc;
+}
+
+float vs_key_score(uint64_t key) {
+  const uint32_t ord = ~static_cast<uint32_t>(key >> 32);
+  const uint32_t bits = (ord & 0x80000000u) ? (ord & 0x7fffffffu) : ~ord;
+  float f;
+  std::memcpy(&f, &bits, 4);
+  return f;
+}
+
+uint32_t vs_key_id_rank(uint64_t key) { return static_cast<uint32_t>(key & 0xffffffffu); }
+
+int vs_rescore(vs_handle* h, const vs_library* L, int64_t n_poses, const int32_t* pose_lig,
+               const float* t, const float* q, const float* tors, float* geo, float* resc) {
+  cudaSetDevice(h->device);
+  if (!h->has_pocket) return fail(h, VS_ERR_STATE, "no pocket");
+  for (int64_t p = 1; p < n_poses; ++p)
+    if (pose_lig[p] < pose_lig[p - 1])
+      return fail(h, VS_ERR_INVALID_ARGUMENT, "pose_lig must be non-decreasing");
+  Packed P;
+  int rc = pack_library(h, L, nullptr, 0, P);
+  if (rc) return rc;
+  for (int64_t p = 0; p < n_poses; ++p)
+    if (pose_lig[p] < 0 || pose_lig[p] >= P.n)
+      return fail(h, VS_ERR_INVALID_ARGUMENT, "pose ligand index out of range");
+  cudaStream_t st = h->own;
+  rc = upload_packed(h, P, st);
+  if (rc) return rc;
+  // per-ligand pose ranges (contiguous: pose_lig is non-decreasing) and the
+  // offset of each ligand's first torsion vector in `tors`
+  std::vector<int> first(P.n, -1), cnt(P.n, 0);
+  std::vector<long> tb(P.n, 0);
+  long toff = 0;
+  for (int64_t p = 0; p < n_poses; ++p) {
+    const int l = pose_lig[p];
+    if (first[l] < 0) {
+      first[l] = static_cast<int>(p);
+      tb[l] = toff;
+    }
+    ++cnt[l];
+    toff += P.meta[l].w;
+  }
+  const bool grid = h->pk.grid_mode != 0;
+  const LibDev ld = P.dev();
+  // one launch per size bucket with bucket-local, LPT-ordered pose lists
+  for (const Bucket& b : P.buckets) {
+    std::vector<int> rl, ro, orig;
+    std::vector<long> rt;
+    std::vector<float4> rpt, rpq;
+    std::vector<float> rtors;
+    for (int w = b.start; w < b.start + b.count; ++w) {
+      const int l = P.order[w];
+      if (cnt[l] == 0) continue;
+      rl.push_back(l);
+      ro.push_back(static_cast<int>(orig.size()));
+      rt.push_back(static_cast<long>(rtors.size()));
+      for (int p = first[l]; p < first[l] + cnt[l]; ++p) {
+        orig.push_back(p);
+        rpt.push_back(float4{t[3 * p], t[3 * p + 1], t[3 * p + 2], 0.0f});
+        rpq.push_back(float4{q[4 * p], q[4 * p + 1], q[4 * p + 2], q[4 * p + 3]});
+      }
+      const long nt = static_cast<long>(cnt[l]) * P.meta[l].w;
+      rtors.insert(rtors.end(), tors + tb[l], tors + tb[l] + nt);
+    }
+    if (rl.empty()) continue;
+    ro.push_back(static_cast<int>(orig.size()));
+    if (rtors.empty()) rtors.push_back(0.0f);
+    DBuf a, bo, c, d, e, f, g, gr, cc;
+    auto up = [&](DBuf& dst, const void* src, size_t bytes) -> cudaError_t {
+      cudaError_t err = dst.ensure(bytes);
+      if (err != cudaSuccess) return err;
+      return cudaMemcpyAsync(dst.p, src, bytes, cudaMemcpyHostToDevice, st);
+    };
+    VS_CUDA(h, up(a, rl.data(), rl.size() * 4));
+    VS_CUDA(h, up(bo, ro.data(), ro.size() * 4));
+    VS_CUDA(h, up(c, rt.data(), rt.size() * 8));
+    VS_CUDA(h, up(d, rpt.data(), rpt.size() * 16));
+    VS_CUDA(h, up(e, rpq.data(), rpq.size() * 16));
+    VS_CUDA(h, up(f, rtors.data(), rtors.size() * 4));
+    VS_CUDA(h, g.ensure(orig.size() * 4));
+    VS_CUDA(h, gr.ensure(orig.size() * 4));
+    VS_CUDA(h, cc.ensure(4));
+    VS_CUDA(h, cudaMemsetAsync(cc.p, 0, 4, st));
+    const int count = static_cast<int>(rl.size());
+    const size_t smem = dock_smem_per_block(b.nmax, b.tmax, b.mvmax);
+    const int blocks = std::max(1, std::min((count + kWarpsPerBlock - 1) / kWarpsPerBlock, 4 * h->sms));
+    VS_CUDA(h, launch_rescore(grid, blocks, smem, st, ld, h->pk, a.as<int>(), count, cc.as<int>(),
+                              bo.as<int>(), c.as<long>(), d.as<float4>(), e.as<float4>(),
+                              f.as<float>(), b.nmax, b.tmax, b.mvmax, g.as<float>(), gr.as<float>()));
+    ++h->launches;
+    std::vector<float> og(orig.size()), orr(orig.size());
+    VS_CUDA(h, cudaMemcpyAsync(og.data(), g.p, og.size() * 4, cudaMemcpyDeviceToHost, st));
+    VS_CUDA(h, cudaMemcpyAsync(orr.data(), gr.p, orr.size() * 4, cudaMemcpyDeviceToHost, st));
+    VS_CUDA(h, cudaStreamSynchronize(st));
+    for (size_t k = 0; k < orig.size(); ++k) {
+      if (geo) geo[orig[k]] = og[k];
+      if (resc) resc[orig[k]] = orr[k];
+    }
+    for (DBuf* x : {&a, &bo, &c, &d, &e, &f, &g, &gr, &cc}) x->release();
+  }
+  P.release();
+  return VS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,84 @@
+// Device-side data layout of the dock-and-score path.
+// Plain structs shared by the kernels (vs_kernels.cu) and the host runtime
+// (vs_runtime.cpp).  Nothing here crosses the public C-ABI.
+#pragma once
+#include <stdint.h>
+
+namespace vs {
+
+constexpr int kMaxRestarts = 64;   // kept-pose bookkeeping in shared memory
+constexpr int kMaxFlexAngles = 16; // one lane pair per candidate angle
+constexpr int kMaxAtoms = 128;     // moving lists are u8 atom indices
+constexpr int kMaxTors = 64;
+constexpr int kWarpsPerBlock = 4;
+
+// One analytic Gaussian site (dock.hpp:18-23) in FP32.
+struct SiteF {
+  float cx, cy, cz, w;
+  float inv2s2;  // 1 / (2 sigma^2), computed in FP64 then rounded
+  float pad[3];
+};
+
+struct GridDev {
+  float ox, oy, oz;  // node (0,0,0) position
+  float h, inv_h;
+  int nx, ny, nz;
+  const float* steric;  // node values, x fastest
+  const float* hbond;
+  const float* lipo;
+};
+
+struct PocketDev {
+  float lo[3], hi[3];       // bounds (FP32) for the wall term
+  double lo_d[3], hi_d[3];  // bounds (FP64) for the RNG start draws
+  float r;                  // clash_radius
+  float lam;                // clash_penalty
+  float cut2;               // (r + 3)^2: pair skip threshold (z < -30)
+  int n_steric, n_hbond, n_lipo;
+  const SiteF* sites;       // [steric | hbond | lipo], pocket order within kind
+  int grid_mode;            // 0 analytic field, 1 grid maps
+  GridDev grid;
+};
+
+// Output pose record (40 B); torsions live in a parallel float array.
+struct PoseOut {
+  float t[3];
+  float q[4];
+  float score;    // geometric score (canonical FP32)
+  float rescore;  // geometric + kind bonuses
+  int16_t restart;
+  int16_t attempt;  // start attempt that was accepted (dock.cpp:345)
+  int16_t rot;      // winning rotation index of the sweep
+  int16_t pad;
+};
+
+struct LibDev {
+  const int4* meta;        // {atom_off, n_atoms, tors_off, n_tors}
+  const int2* mov;         // {byte offset (16B aligned), padded byte count}
+  const double4* atoms;    // x, y, z, class (0 other, 1 C, 2 N/O), FP64
+  const int4* axes;        // {a, b, mov_start (rel. to ligand), mov_cnt}
+  const uint8_t* moving;
+  const unsigned long long* seeds;
+  const unsigned int* id_rank;
+};
+
+struct DockParams {
+  int R, K, A, F;
+  int keep_top;
+  int write_all;
+  float delta;
+  double min_score;
+};
+
+struct DockOut {
+  PoseOut* surv;        // [n][keep_top]
+  float* surv_tors;     // [tors_off * keep_top + slot * T + j]
+  PoseOut* all;         // [n][R] (optional)
+  float* all_tors;      // [tors_off * R + slot * T + j]
+  float* best;          // [n]
+  int* n_kept;          // [n]
+  int* n_surv;          // [n]
+  unsigned long long* keys;  // [n] top-k keys (score desc, id_rank asc)
+};
+
+}  // namespace vs

@@ -1,0 +1,526 @@
+"""Dock/score entry points — the Python mirror of proj/include/vscreen/dock.hpp
+on top of the B200 kernels (through the C-ABI, capi.h).
+
+Scoring (`geometric_score`, `rescore`) and pose generation (`dock`) run on
+the GPU; there is no CPU path.  `apply_pose`, `rmsd` and the JSON helpers
+are plain host utilities, as in the reference.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import math
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+
+from . import _capi
+from ._capi import lib as _lib, ptr
+from .chem import Conformer, Library, Ligand, TorsionTopology, id_ranks
+from .errors import (AtomCountMismatch, EmptyBounds, LengthMismatch, PocketError, check)
+
+KINDS = {"steric": 0, "hbond": 1, "lipophilic": 2}
+KIND_NAMES = {v: k for k, v in KINDS.items()}
+
+
+@dataclass
+class Site:
+    """dock::Site (dock.hpp:18-23)."""
+    center: tuple[float, float, float]
+    weight: float = 1.0
+    sigma: float = 1.0
+    kind: str = "steric"
+
+
+@dataclass
+class Pocket:
+    """dock::Pocket (dock.hpp:32-37); bounds as (lo, hi) triples."""
+    sites: list[Site] = field(default_factory=list)
+    lo: tuple[float, float, float] = (0.0, 0.0, 0.0)
+    hi: tuple[float, float, float] = (0.0, 0.0, 0.0)
+    clash_radius: float = 0.8
+    clash_penalty: float = 1.0
+
+    def empty(self) -> bool:
+        return any(h <= l for l, h in zip(self.lo, self.hi))
+
+    def as_c(self):
+        arr = (_capi.vs_site * max(1, len(self.sites)))()
+        for i, s in enumerate(self.sites):
+            arr[i].center[:] = [float(v) for v in s.center]
+            arr[i].weight = float(s.weight)
+            arr[i].sigma = float(s.sigma)
+            arr[i].kind = KINDS[s.kind]
+        p = _capi.vs_pocket()
+        p.sites = C.cast(arr, C.POINTER(_capi.vs_site))
+        p.n_sites = len(self.sites)
+        p.lo[:] = [float(v) for v in self.lo]
+        p.hi[:] = [float(v) for v in self.hi]
+        p.clash_radius = float(self.clash_radius)
+        p.clash_penalty = float(self.clash_penalty)
+        p._keep = arr
+        return p
+
+
+@dataclass
+class Pose:
+    """dock::Pose (dock.hpp:39-46) plus the sweep-v1 index tuple."""
+    ligand_id: str = ""
+    translation: tuple[float, float, float] = (0.0, 0.0, 0.0)
+    rotation: tuple[float, float, float, float] = (1.0, 0.0, 0.0, 0.0)
+    torsions: list[float] = field(default_factory=list)
+    geometric_score: float = 0.0
+    rescore: float | None = None
+    restart: int = -1
+    attempt: int = -1
+    rot_index: int = -1
+
+
+# ------------------------------------------------------------------- JSON --
+def parse_pocket_json(text: str) -> Pocket:
+    """dock::parse_pocket_json (dock.cpp:432-450)."""
+    try:
+        j = json.loads(text)
+        sites = []
+        for js in j["sites"]:
+            kind = js["kind"]
+            if kind not in KINDS:
+                raise PocketError(f"unknown site kind: {kind}")
+            s = Site(tuple(float(v) for v in js["center"][:3]), float(js["weight"]),
+                     float(js["sigma"]), kind)
+            if not s.sigma > 0.0:
+                raise PocketError("site sigma must be > 0")
+            sites.append(s)
+        p = Pocket(sites, tuple(float(v) for v in j["bounds"]["min"][:3]),
+                   tuple(float(v) for v in j["bounds"]["max"][:3]),
+                   float(j["clash_radius"]), float(j["clash_penalty"]))
+    except PocketError:
+        raise
+    except (KeyError, TypeError, ValueError, IndexError) as e:
+        raise PocketError(f"bad pocket JSON: {e}") from e
+    if p.clash_penalty < 0.0:
+        raise PocketError("clash_penalty must be >= 0")
+    return p
+
+
+def load_pocket_file(path: str) -> Pocket:
+    """dock::load_pocket_file (dock.cpp:452-458)."""
+    try:
+        with open(path) as f:
+            return parse_pocket_json(f.read())
+    except OSError as e:
+        raise PocketError(f"cannot open pocket file: {path}") from e
+
+
+def pocket_to_json(p: Pocket) -> str:
+    """dock::pocket_to_json (dock.cpp:460-474)."""
+    j = {"sites": [{"center": list(s.center), "weight": s.weight, "sigma": s.sigma,
+                    "kind": s.kind} for s in p.sites],
+         "bounds": {"min": list(p.lo), "max": list(p.hi)},
+         "clash_radius": p.clash_radius, "clash_penalty": p.clash_penalty}
+    return json.dumps(j, indent=2)
+
+
+def pose_to_json(pose: Pose) -> str:
+    """dock::pose_to_json (dock.cpp:476-489)."""
+    return json.dumps({"ligand": pose.ligand_id, "translation": list(pose.translation),
+                       "rotation": list(pose.rotation), "torsions": list(pose.torsions),
+                       "geometric_score": pose.geometric_score, "rescore": pose.rescore},
+                      separators=(",", ":"))
+
+
+# --------------------------------------------------------------- params ---
+@dataclass
+class DockParams:
+    """dock(restarts, diversity_delta) + StageKnobs keep_top/min_score
+    (pipeline.hpp:33-40) + the sweep-v1 knobs (docs/SWEEP_V1.md)."""
+    restarts: int = 30
+    diversity_delta: float = 1.0
+    rotations: int = 256
+    flex_angles: int = 16
+    flex_passes: int = 2
+    keep_top: int = 4
+    min_score: float = -1e30
+    rotation_seed: int = 0x5EED
+    write_all_poses: bool = False
+
+    def as_c(self) -> _capi.vs_dock_params:
+        p = _capi.vs_dock_params()
+        p.restarts, p.rotations = self.restarts, self.rotations
+        p.flex_angles, p.flex_passes = self.flex_angles, self.flex_passes
+        p.diversity_delta, p.keep_top = self.diversity_delta, self.keep_top
+        p.write_all_poses = 1 if self.write_all_poses else 0
+        p.min_score, p.rotation_seed = self.min_score, self.rotation_seed
+        return p
+
+
+POSE_DTYPE = np.dtype([("t", np.float32, 3), ("q", np.float32, 4), ("score", np.float32),
+                       ("rescore", np.float32), ("restart", np.int16), ("attempt", np.int16),
+                       ("rot", np.int16), ("reserved", np.int16)])
+assert POSE_DTYPE.itemsize == C.sizeof(_capi.vs_pose)
+
+
+@dataclass
+class DockResults:
+    best: np.ndarray          # (n,) float32, -inf when dropped
+    n_kept: np.ndarray        # (n,) int32, -1 = out of every size class
+    n_surv: np.ndarray
+    surv: np.ndarray          # (n, keep_top) POSE_DTYPE
+    surv_tors: np.ndarray
+    keys: np.ndarray          # (n,) uint64
+    all: np.ndarray | None = None
+    all_tors: np.ndarray | None = None
+    tors_off: np.ndarray | None = None
+    keep_top: int = 0
+    restarts: int = 0
+
+    def poses(self, i: int, n_tors: int, which: str = "surv", ligand_id: str = "") -> list[Pose]:
+        if which == "surv":
+            cnt, rec, tors, slots = int(self.n_surv[i]), self.surv[i], self.surv_tors, self.keep_top
+        else:
+            cnt, rec, tors, slots = int(self.n_kept[i]), self.all[i], self.all_tors, self.restarts
+        out = []
+        base = int(self.tors_off[i]) * slots
+        for s in range(max(cnt, 0)):
+            r = rec[s]
+            th = [float(v) for v in tors[base + s * n_tors: base + (s + 1) * n_tors]]
+            resc = float(r["rescore"]) if (which == "surv" or s < int(self.n_surv[i])) else None
+            out.append(Pose(ligand_id, tuple(float(v) for v in r["t"]),
+                            tuple(float(v) for v in r["q"]), th, float(r["score"]), resc,
+                            int(r["restart"]), int(r["attempt"]), int(r["rot"])))
+        return out
+
+
+def key_score(key: int) -> float:
+    return float(_lib.vs_key_score(int(key)))
+
+
+def key_id_rank(key: int) -> int:
+    return int(_lib.vs_key_id_rank(int(key)))
+
+
+# ---------------------------------------------------------------- engine ---
+class Engine:
+    """One GPU handle (vs_handle): pocket + resident library + results."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        check(_lib.vs_create(device, C.byref(h)), None, f"vs_create(device={device})")
+        self._h = h
+        self.device = device
+        self._lib = None
+        self._prm = None
+        self.pocket = None
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.vs_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    @property
+    def handle(self):
+        return self._h
+
+    def device_info(self) -> dict:
+        name = C.create_string_buffer(256)
+        sms, clk = C.c_int32(), C.c_int32()
+        _lib.vs_device_info(self._h, name, C.byref(sms), C.byref(clk))
+        return {"name": name.value.decode(), "sm_count": sms.value, "clock_khz": clk.value}
+
+    def set_pocket(self, pocket: Pocket, grid_spacing: float = 0.0, grid_pad: float = 2.0):
+        cp = pocket.as_c()
+        check(_lib.vs_set_pocket(self._h, C.byref(cp), grid_spacing, grid_pad), self._h, "set_pocket")
+        self.pocket = pocket
+
+    def grid_maps(self):
+        dims = (C.c_int32 * 3)()
+        origin = (C.c_float * 3)()
+        sp = C.c_float()
+        check(_lib.vs_grid_info(self._h, dims, origin, C.byref(sp)), self._h, "grid_info")
+        n = dims[0] * dims[1] * dims[2]
+        maps = [np.zeros(n, np.float32) for _ in range(3)]
+        check(_lib.vs_grid_fetch(self._h, *(ptr(m, C.c_float) for m in maps)), self._h, "grid_fetch")
+        shape = (dims[2], dims[1], dims[0])
+        return ([m.reshape(shape) for m in maps], tuple(origin), sp.value)
+
+    def upload(self, lib: Library, classes=None):
+        cl, ncl = _classes_c(classes)
+        self._lib_c = lib.as_c()
+        check(_lib.vs_upload_library(self._h, C.byref(self._lib_c), cl, ncl), self._h, "upload")
+        self._lib = lib
+
+    def dock(self, params: DockParams, stream: int | None = None):
+        self._prm_c = params.as_c()
+        check(_lib.vs_dock(self._h, C.byref(self._prm_c), C.c_void_p(stream or 0)), self._h, "dock")
+        self._prm = params
+
+    def fetch(self) -> DockResults:
+        return self._fetch(self._lib, self._prm, None)
+
+    def _alloc(self, lib: Library, prm: DockParams):
+        n, tt = len(lib), int(np.sum(lib.n_tors))
+        kt, R = max(prm.keep_top, 1), prm.restarts
+        res = DockResults(best=np.zeros(max(n, 1), np.float32), n_kept=np.zeros(max(n, 1), np.int32),
+                          n_surv=np.zeros(max(n, 1), np.int32),
+                          surv=np.zeros((max(n, 1), kt), POSE_DTYPE),
+                          surv_tors=np.zeros(max(tt * kt, 1), np.float32),
+                          keys=np.zeros(max(n, 1), np.uint64),
+                          tors_off=np.concatenate([[0], np.cumsum(lib.n_tors, dtype=np.int64)]),
+                          keep_top=prm.keep_top, restarts=R)
+        if prm.write_all_poses:
+            res.all = np.zeros((max(n, 1), R), POSE_DTYPE)
+            res.all_tors = np.zeros(max(tt * R, 1), np.float32)
+        r = _capi.vs_results()
+        r.best = ptr(res.best, C.c_float)
+        r.n_kept = ptr(res.n_kept, C.c_int32)
+        r.n_surv = ptr(res.n_surv, C.c_int32)
+        r.surv = res.surv.ctypes.data_as(C.c_void_p)
+        r.surv_tors = ptr(res.surv_tors, C.c_float)
+        r.keys = ptr(res.keys, C.c_uint64)
+        if prm.write_all_poses:
+            r.all = res.all.ctypes.data_as(C.c_void_p)
+            r.all_tors = ptr(res.all_tors, C.c_float)
+        return res, r
+
+    def _fetch(self, lib, prm, _):
+        res, r = self._alloc(lib, prm)
+        check(_lib.vs_fetch_results(self._h, C.byref(r)), self._h, "fetch")
+        return _trim(res, len(lib))
+
+    def dock_host(self, lib: Library, params: DockParams, classes=None) -> DockResults:
+        """Upload + dock + fetch in one C-ABI call (host buffers in and out)."""
+        cl, ncl = _classes_c(classes)
+        lc = lib.as_c()
+        pc = params.as_c()
+        res, r = self._alloc(lib, params)
+        check(_lib.vs_dock_host(self._h, C.byref(lc), cl, ncl, C.byref(pc), C.byref(r)),
+              self._h, "dock_host")
+        self._lib, self._prm = lib, params
+        return _trim(res, len(lib))
+
+    def topk(self, k: int) -> np.ndarray:
+        out = np.zeros(k, np.uint64)
+        check(_lib.vs_topk(self._h, k, ptr(out, C.c_uint64)), self._h, "topk")
+        return out
+
+    def topk_device(self, k: int, out_ptr: int, stream: int | None = None):
+        check(_lib.vs_topk_device(self._h, k, C.c_void_p(out_ptr), C.c_void_p(stream or 0)),
+              self._h, "topk_device")
+
+    def topk_merge_device(self, keys_ptr: int, n: int, k: int, out_ptr: int,
+                          stream: int | None = None):
+        check(_lib.vs_topk_merge_device(self._h, C.c_void_p(keys_ptr), n, k, C.c_void_p(out_ptr),
+                                        C.c_void_p(stream or 0)), self._h, "topk_merge")
+
+    def last_dock_ms(self) -> float:
+        return float(_lib.vs_last_dock_ms(self._h))
+
+    def launch_count(self) -> int:
+        return int(_lib.vs_launch_count(self._h))
+
+    def rescore(self, lib: Library, pose_lig, t, q, tors):
+        """K3a: canonical geometric score and rescore of given poses."""
+        pose_lig = np.ascontiguousarray(pose_lig, np.int32)
+        t = np.ascontiguousarray(t, np.float32).reshape(-1)
+        q = np.ascontiguousarray(q, np.float32).reshape(-1)
+        tors = np.ascontiguousarray(tors, np.float32).reshape(-1)
+        if tors.size == 0:
+            tors = np.zeros(1, np.float32)
+        n = len(pose_lig)
+        geo = np.zeros(max(n, 1), np.float32)
+        resc = np.zeros(max(n, 1), np.float32)
+        lc = lib.as_c()
+        check(_lib.vs_rescore(self._h, C.byref(lc), n, ptr(pose_lig, C.c_int32), ptr(t, C.c_float),
+                              ptr(q, C.c_float), ptr(tors, C.c_float), ptr(geo, C.c_float),
+                              ptr(resc, C.c_float)), self._h, "rescore")
+        return geo[:n], resc[:n]
+
+
+def _classes_c(classes):
+    if not classes:
+        return None, 0
+    arr = (_capi.vs_size_class * len(classes))()
+    for i, c in enumerate(classes):
+        arr[i].atom_lo, arr[i].atom_hi = c[0], c[1]
+        arr[i].rot_lo, arr[i].rot_hi = c[2], c[3]
+    return arr, len(classes)
+
+
+def _trim(res: DockResults, n: int) -> DockResults:
+    res.best, res.n_kept, res.n_surv = res.best[:n], res.n_kept[:n], res.n_surv[:n]
+    res.surv, res.keys = res.surv[:n], res.keys[:n]
+    if res.all is not None:
+        res.all = res.all[:n]
+    return res
+
+
+_ENGINES: dict[int, Engine] = {}
+
+
+def default_engine(device: int = 0) -> Engine:
+    e = _ENGINES.get(device)
+    if e is None:
+        e = _ENGINES[device] = Engine(device)
+    return e
+
+
+# ------------------------------------------------- single-ligand drop-ins ---
+def _one_ligand_library(conf: Conformer, topo: TorsionTopology, classes=None, seed: int = 0,
+                        atom_class=None) -> Library:
+    n = len(conf.coords)
+    for ax in topo.axes:
+        if ax.a >= n or ax.b >= n:
+            raise AtomCountMismatch("torsion topology does not fit conformer")
+    cls = np.zeros(n, np.int32) if atom_class is None else np.asarray(atom_class, np.int32)
+    mv = [m for ax in topo.axes for m in ax.moving]
+    return Library(ids=[conf.ligand_id or "x"], n_atoms=np.array([n], np.int32),
+                   n_tors=np.array([len(topo.axes)], np.int32),
+                   rot_bonds=np.array([len(topo.axes)], np.int32),
+                   coords=np.asarray(conf.coords, np.float64).reshape(-1, 3), atom_class=cls,
+                   axis_a=np.array([a.a for a in topo.axes], np.int32),
+                   axis_b=np.array([a.b for a in topo.axes], np.int32),
+                   moving_count=np.array([len(a.moving) for a in topo.axes], np.int32),
+                   moving=np.array(mv, np.int32), seeds=np.array([seed & (2**64 - 1)], np.uint64),
+                   id_rank=np.zeros(1, np.uint32))
+
+
+def _check_counts(conf: Conformer, topo: TorsionTopology, pose: Pose):
+    # dock.cpp:219-230
+    if len(pose.torsions) != len(topo.axes):
+        raise AtomCountMismatch(f"pose has {len(pose.torsions)} torsions, topology has "
+                                f"{len(topo.axes)}")
+    n = len(conf.coords)
+    for ax in topo.axes:
+        if ax.a >= n or ax.b >= n:
+            raise AtomCountMismatch("torsion topology does not fit conformer")
+
+
+def _score(conf, topo, poses, pocket, atom_class, engine=None):
+    eng = engine or default_engine()
+    if eng.pocket is not pocket:
+        eng.set_pocket(pocket)
+    if not len(conf.coords):
+        raise AtomCountMismatch("conformer has no atoms")
+    lib = _one_ligand_library(conf, topo, atom_class=atom_class)
+    n = len(poses)
+    t = np.array([p.translation for p in poses], np.float32)
+    q = np.array([p.rotation for p in poses], np.float32)
+    tors = np.array([v for p in poses for v in p.torsions], np.float32)
+    return eng.rescore(lib, np.zeros(n, np.int32), t, q, tors)
+
+
+def geometric_score(conf: Conformer, topo: TorsionTopology, pose: Pose, pocket: Pocket,
+                    engine: Engine | None = None) -> float:
+    """dock::geometric_score (dock.cpp:278-282) on the GPU (canonical FP32)."""
+    _check_counts(conf, topo, pose)
+    return float(_score(conf, topo, [pose], pocket, None, engine)[0][0])
+
+
+def rescore(ligand: Ligand, conf: Conformer, topo: TorsionTopology, pose: Pose, pocket: Pocket,
+            engine: Engine | None = None) -> float:
+    """dock::rescore (dock.cpp:297-316) on the GPU."""
+    if ligand.heavy_atoms != len(conf.coords):
+        raise AtomCountMismatch("graph and conformer disagree on atom count")
+    _check_counts(conf, topo, pose)
+    return float(_score(conf, topo, [pose], pocket, ligand.atom_classes(), engine)[1][0])
+
+
+def dock(conf: Conformer, topo: TorsionTopology, pocket: Pocket, restarts: int,
+         diversity_delta: float, seed: int, max_steps: int = 500, params: DockParams | None = None,
+         engine: Engine | None = None, atom_class=None) -> list[Pose]:
+    """dock::dock (dock.cpp:318-371) with the sweep-v1 generator: kept poses,
+    pairwise RMSD >= diversity_delta, sorted by geometric score descending.
+    `max_steps` (reference ascent length) has no meaning for sweep-v1."""
+    if pocket.empty():
+        raise EmptyBounds()
+    if restarts < 1:
+        raise ValueError("restarts must be >= 1")
+    if diversity_delta < 0.0:
+        raise ValueError("diversity_delta must be >= 0")
+    if not len(conf.coords):
+        raise AtomCountMismatch("conformer has no atoms")
+    prm = params or DockParams()
+    prm = DockParams(restarts=restarts, diversity_delta=diversity_delta, rotations=prm.rotations,
+                     flex_angles=prm.flex_angles, flex_passes=prm.flex_passes,
+                     keep_top=prm.keep_top, min_score=prm.min_score,
+                     rotation_seed=prm.rotation_seed, write_all_poses=True)
+    eng = engine or default_engine()
+    if eng.pocket is not pocket:
+        eng.set_pocket(pocket)
+    lib = _one_ligand_library(conf, topo, seed=seed, atom_class=atom_class)
+    res = eng.dock_host(lib, prm)
+    out = res.poses(0, len(topo.axes), which="all", ligand_id=conf.ligand_id)
+    for p in out:
+        p.rescore = None
+    return out
+
+
+def filter_poses(poses: Sequence[Pose], keep_top: int, min_score: float) -> list[Pose]:
+    """dock::filter_poses (dock.cpp:373-390), via the native host function."""
+    scores = np.array([p.geometric_score for p in poses], np.float64)
+    out = np.zeros(max(len(poses), 1), np.int32)
+    n = _lib.vs_filter_poses(ptr(scores, C.c_double), len(poses), int(min(keep_top, 2**62)),
+                             float(min_score), ptr(out, C.c_int32))
+    return [poses[i] for i in out[:n]]
+
+
+def rmsd(a, b) -> float:
+    """dock::rmsd (dock.cpp:392-401): no alignment."""
+    a = np.asarray(a, np.float64).reshape(-1, 3)
+    b = np.asarray(b, np.float64).reshape(-1, 3)
+    if len(a) != len(b):
+        raise LengthMismatch(f"coordinate sets have different lengths: {len(a)} vs {len(b)}")
+    if len(a) == 0:
+        return 0.0
+    s = 0.0
+    for (ax, ay, az), (bx, by, bz) in zip(a.tolist(), b.tolist()):
+        dx, dy, dz = ax - bx, ay - by, az - bz
+        s += dx * dx + dy * dy + dz * dz
+    return math.sqrt(s / len(a))
+
+
+def apply_pose(conf: Conformer, topo: TorsionTopology, pose: Pose) -> np.ndarray:
+    """dock::apply_pose (dock.cpp:52-67, 272-276) in FP64 on the host."""
+    _check_counts(conf, topo, pose)
+    pts = [list(map(float, p)) for p in np.asarray(conf.coords, np.float64).reshape(-1, 3)]
+
+    def qrot(w, x, y, z, v):
+        ux, uy, uz = x, y, z
+        cx, cy, cz = uy * v[2] - uz * v[1], uz * v[0] - ux * v[2], ux * v[1] - uy * v[0]
+        dx, dy, dz = uy * cz - uz * cy, uz * cx - ux * cz, ux * cy - uy * cx
+        return [v[0] + 2.0 * w * cx + 2.0 * dx, v[1] + 2.0 * w * cy + 2.0 * dy,
+                v[2] + 2.0 * w * cz + 2.0 * dz]
+
+    for j, ax in enumerate(topo.axes):
+        o = pts[ax.a]
+        d = [pts[ax.b][k] - o[k] for k in range(3)]
+        n = math.sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2])
+        u = [v / n for v in d] if n > 0 else [0.0, 0.0, 0.0]
+        h = 0.5 * pose.torsions[j]
+        s = math.sin(h)
+        for idx in ax.moving:
+            r = qrot(math.cos(h), u[0] * s, u[1] * s, u[2] * s,
+                     [pts[idx][k] - o[k] for k in range(3)])
+            pts[idx] = [o[k] + r[k] for k in range(3)]
+    w, x, y, z = pose.rotation
+    n = math.sqrt(w * w + x * x + y * y + z * z)
+    w, x, y, z = w / n, x / n, y / n, z / n
+    return np.array([[a + b for a, b in zip(qrot(w, x, y, z, p), pose.translation)] for p in pts])
+
+
+def pose_rmsd(conf: Conformer, topo: TorsionTopology, a: Pose, b: Pose) -> float:
+    """dock::pose_rmsd (dock.cpp:403-406)."""
+    return rmsd(apply_pose(conf, topo, a), apply_pose(conf, topo, b))

@@ -1,0 +1,293 @@
+"""GPU parity: the B200 kernels (through the C-ABI) against the CPU oracle
+(bit-exact) and against the reference FP64 scoring (1e-5 * max(|ref|, 1)).
+
+Tolerances (BASELINE.json north_star / SURVEY §8(d)):
+  * GPU vs oracle: every score, pose parameter, index tuple and top-k key is
+    bit-identical (same deterministic FP32/FP64 arithmetic, fixed-order sums);
+  * GPU vs reference dock::geometric_score / dock::rescore on the emitted
+    poses: |gpu - ref| <= 1e-5 * max(|ref|, 1).
+"""
+import json
+
+import numpy as np
+import pytest
+
+from conftest import corpus_library, gpu_available, need_ref
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
+
+TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def V():
+    import paper_2304_09953_b200 as V
+    return V
+
+
+@pytest.fixture(scope="module")
+def engine(V):
+    e = V.Engine(0)
+    yield e
+    e.close()
+
+
+@pytest.fixture(scope="module")
+def lib200(V):
+    lib, smis = corpus_library(200)
+    return lib, smis
+
+
+def _params(V, **kw):
+    base = dict(restarts=8, rotations=64, flex_angles=16, flex_passes=2, keep_top=4,
+                min_score=-5.0, diversity_delta=1.0, write_all_poses=True)
+    base.update(kw)
+    return V.DockParams(**base)
+
+
+def _oracle_dock(pocket, lib, prm, grid=0.0, threads=8):
+    from oracle import sweep
+    op = sweep.OraclePocket(pocket, grid_spacing=grid, grid_pad=2.0)
+    return sweep.dock_library(op, lib, prm, threads=threads)
+
+
+def _bits(a):
+    return np.ascontiguousarray(a).view(np.uint8)
+
+
+def _assert_same(res, ora, keep_top):
+    n = len(res.best)
+    np.testing.assert_array_equal(res.n_kept, ora["n_kept"])
+    np.testing.assert_array_equal(res.n_surv, ora["n_surv"])
+    np.testing.assert_array_equal(res.keys, ora["keys"])
+    np.testing.assert_array_equal(res.best.view(np.uint32), ora["best"].view(np.uint32))
+    for i in range(n):
+        k = int(res.n_surv[i])
+        g, o = res.surv[i][:k], ora["surv"][i][:k]
+        for f in ("t", "q", "score", "rescore", "restart", "attempt", "rot"):
+            np.testing.assert_array_equal(_bits(g[f]), _bits(o[f]), err_msg=f"ligand {i} field {f}")
+        kk = int(res.n_kept[i])
+        if res.all is not None:
+            for f in ("t", "q", "score", "restart", "attempt", "rot"):
+                np.testing.assert_array_equal(_bits(res.all[i][:kk][f]), _bits(ora["all"][i][:kk][f]),
+                                              err_msg=f"ligand {i} all-field {f}")
+    np.testing.assert_array_equal(res.surv_tors.view(np.uint32)[:len(ora["surv_tors"])],
+                                  ora["surv_tors"].view(np.uint32))
+
+
+@pytest.mark.parametrize("grid", [0.0, 0.4])
+def test_dock_bit_exact_vs_oracle(V, engine, lib200, pocket_json, grid):
+    lib, _ = lib200
+    pocket = V.parse_pocket_json(pocket_json)
+    prm = _params(V)
+    engine.set_pocket(pocket, grid_spacing=grid)
+    res = engine.dock_host(lib, prm)
+    ora = _oracle_dock(pocket, lib, prm, grid)
+    _assert_same(res, ora, prm.keep_top)
+
+
+def test_grid_maps_bit_exact(V, engine, pocket_json):
+    from oracle import sweep
+    pocket = V.parse_pocket_json(pocket_json)
+    engine.set_pocket(pocket, grid_spacing=0.4, grid_pad=2.0)
+    (gs, gh, gl), origin, h = engine.grid_maps()
+    (os_, oh, ol), oorigin, oh_ = sweep.OraclePocket(pocket, 0.4, 2.0).grid_maps()
+    assert origin == oorigin and h == oh_
+    for a, b in ((gs, os_), (gh, oh), (gl, ol)):
+        np.testing.assert_array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def test_rescore_kernel_vs_oracle_and_reference(V, engine, lib200, pocket_json):
+    """K3a on random poses: bit-exact vs oracle; 1e-5 vs reference FP64."""
+    from oracle import sweep
+    lib, smis = lib200
+    pocket = V.parse_pocket_json(pocket_json)
+    engine.set_pocket(pocket)
+    rng = np.random.default_rng(7)
+    sub = list(range(0, 200, 4))
+    L = lib.subset(sub)
+    pl, T, Q, TH = [], [], [], []
+    for i in range(len(L)):
+        for _ in range(20):
+            pl.append(i)
+            T.append(rng.uniform(-5, 5, 3))
+            q = rng.normal(size=4)
+            Q.append(q / np.linalg.norm(q))
+            TH.extend(rng.uniform(-np.pi, np.pi, int(L.n_tors[i])))
+    T = np.array(T, np.float32); Q = np.array(Q, np.float32); TH = np.array(TH, np.float32)
+    geo, resc = engine.rescore(L, pl, T, Q, TH)
+    og, orr = sweep.score_poses(sweep.OraclePocket(pocket), L, pl, T, Q, TH)
+    np.testing.assert_array_equal(geo.view(np.uint32), og.view(np.uint32))
+    np.testing.assert_array_equal(resc.view(np.uint32), orr.view(np.uint32))
+    from oracle import ref as R
+    if not R.available():
+        return
+    rp = R.RefPocket(pocket_json)
+    ao, to, _ = L.offsets()
+    toff, worst = 0, 0.0
+    for p, i in enumerate(pl):
+        nt = int(L.n_tors[i])
+        rl = R.RefLigand(smis[sub[i]])
+        rl.set_coords(L.coords[ao[i]:ao[i + 1]])
+        th = TH[toff:toff + nt].astype(np.float64)
+        toff += nt
+        g = rl.geometric_score(rp, T[p].astype(np.float64), Q[p].astype(np.float64), th)
+        r = rl.rescore(rp, T[p].astype(np.float64), Q[p].astype(np.float64), th)
+        worst = max(worst, abs(g - geo[p]) / max(abs(g), 1.0), abs(r - resc[p]) / max(abs(r), 1.0))
+    assert worst <= TOL, worst
+
+
+def test_docked_poses_rescored_by_reference(V, engine, lib200, pocket_json):
+    """Every emitted pose, re-scored by the reference in FP64, matches the
+    GPU's geometric score and rescore within 1e-5 * max(|ref|, 1)."""
+    R = need_ref()
+    lib, smis = lib200
+    pocket = V.parse_pocket_json(pocket_json)
+    engine.set_pocket(pocket)
+    prm = _params(V)
+    res = engine.dock_host(lib, prm)
+    rp = R.RefPocket(pocket_json)
+    ao, to, _ = lib.offsets()
+    worst, n = 0.0, 0
+    for i in range(0, len(lib), 3):
+        rl = R.RefLigand(smis[i])
+        rl.set_coords(lib.coords[ao[i]:ao[i + 1]])
+        for pose in res.poses(i, int(lib.n_tors[i]), "surv"):
+            t = np.array(pose.translation, np.float64)
+            q = np.array(pose.rotation, np.float64)
+            th = np.array(pose.torsions, np.float64)
+            g = rl.geometric_score(rp, t, q, th)
+            r = rl.rescore(rp, t, q, th)
+            worst = max(worst, abs(g - pose.geometric_score) / max(abs(g), 1.0),
+                        abs(r - pose.rescore) / max(abs(r), 1.0))
+            n += 1
+    assert n > 50
+    assert worst <= TOL, worst
+
+
+def test_restart_starts_match_reference_rng(V, engine, lib200, pocket_json):
+    """The accepted start of each kept pose is the reference Rng stream's
+    attempt (dock.cpp:343-354): FP32 casts of uniform/normal draws."""
+    R = need_ref()
+    lib, _ = lib200
+    pocket = V.parse_pocket_json(pocket_json)
+    engine.set_pocket(pocket)
+    res = engine.dock_host(lib, _params(V, rotations=1, flex_passes=0))
+    # rotations=1 (identity) and no flex: the emitted pose is the start pose
+    # re-expressed about its centroid; torsions are the start torsions.
+    lo, hi = pocket.lo, pocket.hi
+    checked = 0
+    for i in range(0, len(lib), 5):
+        T = int(lib.n_tors[i])
+        for pose in res.poses(i, T, "all"):
+            D = 11 + T
+            kinds = [1, 1, 1] + [2] * 4 + [1] * T
+            los = list(lo) + [0] * 4 + [-np.pi] * T
+            his = list(hi) + [1] * 4 + [np.pi] * T
+            draws = R.rng_draws(int(lib.seeds[i]), [pose.restart], kinds * (pose.attempt + 1),
+                                los * (pose.attempt + 1), his * (pose.attempt + 1))
+            d = draws[-(7 + T):]
+            th = np.float32(d[7:])
+            np.testing.assert_array_equal(np.array(pose.torsions, np.float32), th)
+            checked += 1
+    assert checked > 20
+
+
+def test_topk_matches_oracle(V, engine, lib200, pocket_json):
+    from oracle import sweep
+    lib, _ = lib200
+    pocket = V.parse_pocket_json(pocket_json)
+    engine.set_pocket(pocket, grid_spacing=0.4)
+    prm = _params(V, write_all_poses=False)
+    res = engine.dock_host(lib, prm)
+    for k in (1, 10, 150, 1000):
+        keys = engine.topk(k)
+        np.testing.assert_array_equal(keys, sweep.topk(res.keys, k))
+    keys = engine.topk(50)
+    scores = [V.dock.key_score(k) for k in keys if k != 2**64 - 1]
+    assert all(a >= b for a, b in zip(scores, scores[1:]))
+    # ranking order = rank_ligands over (id, best) (pipeline.cpp:243-251)
+    from paper_2304_09953_b200.pipeline import ids_by_rank, keys_to_ranked, rank_ligands
+    kept = {lib.ids[i]: float(res.best[i]) for i in range(len(lib)) if res.n_surv[i] > 0}
+    ranked = rank_ligands(kept)[:50]
+    got = keys_to_ranked(keys, ids_by_rank(lib))
+    assert [r.id for r in got] == [r[0] for r in ranked]
+
+
+def test_rerun_bit_identical(V, engine, lib200, pocket_json):
+    lib, _ = lib200
+    engine.set_pocket(V.parse_pocket_json(pocket_json), grid_spacing=0.4)
+    prm = _params(V)
+    a = engine.dock_host(lib, prm)
+    b = engine.dock_host(lib, prm)
+    np.testing.assert_array_equal(a.keys, b.keys)
+    np.testing.assert_array_equal(_bits(a.surv), _bits(b.surv))
+
+
+def test_edge_cases(V, engine, pocket_json):
+    pocket = V.parse_pocket_json(pocket_json)
+    engine.set_pocket(pocket)
+    # single atom, no torsions; a ring (no torsions); one-torsion chain
+    ligs = [V.make_ligand(f"E{i}", s, embed_seed=i) for i, s in enumerate(["C", "C1CCCCC1", "CCCC", "CO"])]
+    lib = V.Library.from_ligands(ligs, [1, 2, 3, 4])
+    prm = _params(V)
+    res = engine.dock_host(lib, prm)
+    ora = _oracle_dock(pocket, lib, prm)
+    _assert_same(res, ora, prm.keep_top)
+    # out-of-class ligand is dropped (pipeline.cpp:447-452)
+    res2 = engine.dock_host(lib, prm, classes=[(1, 3, 0, 4)])
+    assert res2.n_kept[0] >= 1 and res2.n_kept[1] == -1 and res2.best[1] == -np.inf
+    # min_score above every score drops the ligand
+    res3 = engine.dock_host(lib, _params(V, min_score=1e9))
+    assert (res3.n_surv == 0).all() and (res3.keys == 2**64 - 1).all()
+    # keep_top = 0 keeps nothing
+    res4 = engine.dock_host(lib, _params(V, keep_top=0))
+    assert (res4.n_surv == 0).all()
+
+
+def test_error_mapping(V, engine, pocket_json):
+    pocket = V.parse_pocket_json(pocket_json)
+    lig = V.make_ligand("x", "CCO", embed_seed=1)
+    bad = V.Pocket(pocket.sites, (5, 5, 5), (-5, -5, -5), 0.7, 0.5)
+    with pytest.raises(V.EmptyBounds):
+        V.dock(lig.conformer, lig.topology, bad, 1, 0.0, 0, engine=engine)
+    with pytest.raises(ValueError):
+        V.dock(lig.conformer, lig.topology, pocket, 0, 0.0, 0, engine=engine)
+    with pytest.raises(ValueError):
+        V.dock(lig.conformer, lig.topology, pocket, 1, -1.0, 0, engine=engine)
+    wrong = V.Pose(torsions=[0.1, 0.2])
+    with pytest.raises(V.AtomCountMismatch):
+        V.geometric_score(lig.conformer, lig.topology, wrong, pocket, engine=engine)
+
+
+def test_reference_known_answers_on_gpu(V, engine):
+    """test_dock.cpp:40-61 / 288-323 closed forms through the GPU scorer."""
+    P = V.Pocket([V.Site((1.0, 0.5, -0.5), 1.0, 1.0, "steric")], (-5, -5, -5), (5, 5, 5), 0.7, 0.5)
+    c = V.Conformer("x", np.zeros((1, 3)))
+    topo = V.chem.TorsionTopology()
+    s = V.geometric_score(c, topo, V.Pose(translation=(1.0, 0.5, -0.5)), P, engine=engine)
+    assert abs(s - 1.0) <= 1e-6
+    s2 = V.geometric_score(c, topo, V.Pose(translation=(1.0 + 2 ** 0.5, 0.5, -0.5)), P, engine=engine)
+    assert abs(s2 - np.exp(-1.0)) <= 1e-6
+    P2 = V.Pocket([V.Site((0, 0, 0), 1.0, 1.0, "steric"), V.Site((0, 0, 0), 0.5, 1.0, "hbond")],
+                  (-5, -5, -5), (5, 5, 5), 0.5, 0.0)
+    o = V.make_ligand("o", "O")
+    assert abs(V.rescore(o, c, topo, V.Pose(), P2, engine=engine) - 1.5) <= 1e-6
+    cl = V.make_ligand("c", "C")
+    g = V.geometric_score(c, topo, V.Pose(), P2, engine=engine)
+    assert V.rescore(cl, c, topo, V.Pose(), P2, engine=engine) == g
+
+
+def test_dock_smiles_single_site(V):
+    """tests/python/test_smoke.py:39-50 through the GPU dock."""
+    pocket = {"sites": [{"center": [1.0, 0.5, -0.5], "weight": 1.0, "sigma": 1.0, "kind": "steric"}],
+              "bounds": {"min": [-5, -5, -5], "max": [5, 5, 5]},
+              "clash_radius": 0.6, "clash_penalty": 0.4}
+    poses = V.dock_smiles("C", json.dumps(pocket), restarts=2, seed=3)
+    assert poses
+    best = poses[0]
+    # the sweep has no continuous refinement: the best of 2 random starts
+    # is reported, sorted by score
+    assert best["geometric_score"] >= poses[-1]["geometric_score"]
+    assert set(best) == {"ligand", "translation", "rotation", "torsions", "geometric_score", "rescore"}

@@ -1,0 +1,84 @@
+"""Host ligand ingest (parse, descriptors, embed, torsion topology, corpus,
+library text) — bit-exact against the reference library, plus the
+reference's own known answers (test_chem / test_dock / test_smoke)."""
+import math
+
+import numpy as np
+import pytest
+
+from conftest import need_ref
+
+
+@pytest.fixture(scope="module")
+def V():
+    import paper_2304_09953_b200 as V
+    return V
+
+
+def test_smoke_known_answers(V):
+    # tests/python/test_smoke.py:12-28
+    g = V.parse_smiles("CCO")
+    assert g["atoms"] == [("C", False), ("C", False), ("O", False)]
+    assert g["bonds"] == [(0, 1, 1), (1, 2, 1)]
+    assert V.rotatable_bonds("CCCC") == 1
+    assert V.rotatable_bonds("C1CCCCC1") == 0
+    with pytest.raises(V.ParseError):
+        V.parse_smiles("C(")
+    a = V.embed_3d("CCO", seed=5)
+    assert a == V.embed_3d("CCO", seed=5)
+    assert len(a) == 3
+    assert 1.3 < math.dist(a[0], a[1]) < 1.7
+
+
+def test_torsion_topology_known_answer(V):
+    # test_dock.cpp:378-385
+    t = V.torsion_topology("CCCC")
+    assert len(t.axes) == 1 and (t.axes[0].a, t.axes[0].b) == (1, 2) and t.axes[0].moving == [3]
+
+
+@pytest.mark.parametrize("bad,kind", [("C(", "UnbalancedBranch"), ("C)", "UnbalancedBranch"),
+                                      ("C1CC", "UnclosedRingBond"), ("CX", "UnknownToken"),
+                                      ("=C", "UnknownToken"), ("", "UnknownToken")])
+def test_parse_errors(V, bad, kind):
+    with pytest.raises(V.ParseError) as e:
+        V.parse_smiles(bad)
+    assert e.value.kind == kind
+
+
+def test_corpus_and_embed_bit_exact_vs_reference(V):
+    R = need_ref()
+    for i in range(400):
+        smi = V.random_smiles(99, i)
+        assert smi == R.random_smiles(99, i)
+        lig = V.make_ligand("x", smi, embed_seed=7 * i + 1)
+        r = R.RefLigand(smi, 7 * i + 1)
+        assert np.array_equal(lig.conformer.coords, r.coords()), smi
+        assert [(a.a, a.b, a.moving) for a in lig.topology.axes] == r.axes()
+        assert lig.rotatable_bonds == r.rot_bonds
+        assert np.array_equal(lig.atom_classes(), r.classes())
+        rb = r.bonds()
+        assert [tuple(b) for b in lig.graph.bonds] == [tuple(int(v) for v in row[:3]) for row in rb]
+        assert lig.graph.ring_bond_flags == [bool(v) for v in rb[:, 3]]
+
+
+def test_library_builder_matches_single_builds(V):
+    smis = [V.random_smiles(5, i) for i in range(64)]
+    lib = V.build_library(smis, embed_seeds=list(range(64)), threads=4)
+    ao, to, mo = lib.offsets()
+    for i, s in enumerate(smis):
+        lg = V.make_ligand("x", s, embed_seed=i)
+        assert np.array_equal(lib.coords[ao[i]:ao[i + 1]], lg.conformer.coords)
+        assert int(lib.n_tors[i]) == len(lg.topology.axes)
+
+
+def test_read_library_records(V, tmp_path):
+    p = tmp_path / "lib.smi"
+    p.write_bytes(b"# header\nCCO\tethanol\n\nc1ccccc1\nCCN\t\r\n")
+    recs = V.chem.read_library_file(str(p))
+    assert [(r.smiles, r.id, r.line_number) for r in recs] == [
+        ("CCO", "ethanol", 2), ("c1ccccc1", "L4", 4), ("CCN", "L5", 5)]
+
+
+def test_aromatic_atoms_count_as_carbon(V):
+    lig = V.make_ligand("b", "c1ccccc1O")
+    assert list(lig.atom_classes()) == [1] * 6 + [2]
