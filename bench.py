@@ -1,0 +1,452 @@
+#!/usr/bin/env python
+"""Dock-and-score throughput on B200 (BASELINE.json metric: ligands/s docked +
+scored, and the fraction of the bounding FP32/XU roofline).
+
+Workload (BASELINE.json configs[1], "C2"): 100k synthetic drug-like ligands
+per GPU (reference corpus sampler, 10-40 heavy atoms, <= 10 torsions,
+reference embed_3d conformers), one synthetic 400-site pocket in a 24 A box
+with 0.4 A grid maps; sweep-v1 with 30 restarts x 256 rotations, 16 flex
+angles x 2 passes, delta 1.0, keep_top 4, min_score -5; global top-1000.
+
+A step = one full pass of the path over the resident library (dock every
+size bucket -> per-ligand best -> device top-k; across GPUs one NCCL
+all-gather of 1000 keys per rank + device merge).  `e2e` is the same pass
+through the C-ABI with host buffers (pack + H2D, dock, D2H of the results).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ligands/sec docked+scored (1/2/4/8 B200) and % of HBM/FP32 roofline"
+UNIT = "ligands/s"
+CORPUS_SEED = 99
+MASTER_SEED = 2024
+TOP_K = 1000
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ligands", type=int, default=100_000, help="ligands per GPU")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--json-out", default=None)
+    return ap.parse_args()
+
+
+def make_pocket():
+    """Synthetic many-site pocket: 24 A box, 400 Gaussian
+    sites 60/25/15 % steric/hbond/lipophilic, w ~ U[0.3, 2], sigma ~
+    U[0.8, 1.6], seed 7; clash radius / penalty of proj/data/pocket.json."""
+    import paper_2304_09953_b200 as V
+    rng = np.random.default_rng(7)
+    sites = []
+    for _ in range(400):
+        u = rng.uniform()
+        kind = "steric" if u < 0.6 else ("hbond" if u < 0.85 else "lipophilic")
+        sites.append(V.Site(tuple(float(v) for v in rng.uniform(-12, 12, 3)),
+                            float(rng.uniform(0.3, 2.0)), float(rng.uniform(0.8, 1.6)), kind))
+    return V.Pocket(sites, (-12.0, -12.0, -12.0), (12.0, 12.0, 12.0), 0.7, 0.5)
+
+
+def params():
+    import paper_2304_09953_b200 as V
+    return V.DockParams(restarts=30, rotations=256, flex_angles=16, flex_passes=2,
+                        diversity_delta=1.0, keep_top=4, min_score=-5.0, rotation_seed=0x5EED)
+
+
+CONFIG = {"workload": "C2: 100k synthetic drug-like ligands/GPU (10-40 heavy atoms, <=10 torsions, "
+                      "reference corpus + embed_3d), 400-site synthetic pocket, 0.4 A grid maps",
+          "restarts": 30, "rotations": 256, "flex_angles": 16, "flex_passes": 2,
+          "diversity_delta": 1.0, "keep_top": 4, "min_score": -5.0, "top_k": TOP_K,
+          "grid_spacing": 0.4}
+
+
+def build_workload(n_per: int, rank: int, world: int, threads: int):
+    """Library shard of this rank: entries [rank*n_per, (rank+1)*n_per) of the
+    filtered corpus; ids ranked globally (bytewise) so top-k keys merge."""
+    import paper_2304_09953_b200 as V
+    from paper_2304_09953_b200.chem import corpus_indices, _fetch_built
+    from paper_2304_09953_b200.pipeline import campaign_seeds
+    import ctypes as C
+    from paper_2304_09953_b200._capi import lib as _lib, ptr
+    total = n_per * world
+    idx = corpus_indices(CORPUS_SEED, total, (10, 40), (0, 10), threads)
+    ids_all = [f"Z{int(i)}" for i in idx]
+    order = sorted(range(total), key=lambda i: ids_all[i].encode())
+    grank = np.empty(total, np.uint32)
+    grank[order] = np.arange(total, dtype=np.uint32)
+    lo, hi = rank * n_per, (rank + 1) * n_per
+    es = campaign_seeds(MASTER_SEED, total, stage=1)[lo:hi]
+    ds = campaign_seeds(MASTER_SEED, total, stage=2)[lo:hi]
+    sidx = np.ascontiguousarray(idx[lo:hi])
+    h = C.c_void_p()
+    _lib.vs_libbuild_corpus(CORPUS_SEED, ptr(sidx, C.c_int64), len(sidx), ptr(es, C.c_uint64), 200,
+                            threads, C.byref(h))
+    lib = _fetch_built(h, len(sidx), ids_all[lo:hi], ds, drop_failed=False)
+    lib.id_rank = grank[lo:hi].copy()
+    return lib, ids_all, order
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    """nvidia-smi sampled during the timed region (B200_PROFILING.md)."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- roofline --
+def algorithmic_work(lib, prm, stats, grid: bool, n_steric: int):
+    """Frozen work formula (SURVEY §8(d) extended by the
+    translation sweep).  FMA = 2 flops.
+      states = R + flex_states          torsion states (full chain each)
+      poses  = R*K + 27*trans_iters + flex_states   rigid placements scored
+      FLOP   = states*(27*Mv + 14*T + 15*P) + poses*(24 + 12 + Fld)*N
+      XU     = states*(2*T + 3*P)         + poses*(3 + Xf)*N
+      Fld = 25 (grid, one map) | 11*S_steric ; Xf = 0 (grid) | S_steric"""
+    R, K, A, F = prm.restarts, prm.rotations, prm.flex_angles, prm.flex_passes
+    N = lib.n_atoms.astype(np.float64)
+    T = lib.n_tors.astype(np.float64)
+    ao, to, mo = lib.offsets()
+    cm = np.concatenate([[0.0], np.cumsum(lib.moving_count.astype(np.float64))])
+    Mv = cm[to[1:]] - cm[to[:-1]]
+    P = N * (N - 1) / 2
+    flex = np.where((T > 0) & (F > 0), R * F * T * A, R)
+    states = R + flex
+    fld = 25.0 if grid else 11.0 * n_steric
+    xf = 0.0 if grid else float(n_steric)
+    flop_states = float(np.sum(states * (27 * Mv + 14 * T + 15 * P)))
+    xu_states = float(np.sum(states * (2 * T + 3 * P)))
+    pose_atoms = float(np.sum((R * K + flex) * N)) + 27.0 * stats["translation_iter_atoms"]
+    flop = flop_states + pose_atoms * (36.0 + fld)
+    xu = xu_states + pose_atoms * (3.0 + xf)
+    return flop, xu
+
+
+def roofline(flop, xu, dock_ms, peaks, traffic):
+    t = dock_ms * 1e-3
+    t_fp32 = flop / peaks["fp32_flops"]
+    t_xu = xu / peaks["xu_ops"]
+    if t_fp32 >= t_xu:
+        bound, achieved, peak, unit = "fp32", flop / t / 1e12, peaks["fp32_flops"] / 1e12, "TFLOP/s"
+    else:
+        bound, achieved, peak, unit = "xu", xu / t / 1e12, peaks["xu_ops"] / 1e12, "Tops/s"
+    return {"bound": bound, "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": unit,
+            "frac": round(achieved / peak, 4), "traffic": traffic,
+            "peak_source": "measured on this GPU by vs_measure_peaks (FFMA / MUFU.EX2 microbenchmarks)",
+            "fp32": {"achieved_tflops": round(flop / t / 1e12, 3),
+                     "peak_tflops": round(peaks["fp32_flops"] / 1e12, 3),
+                     "frac": round(flop / t / peaks["fp32_flops"], 4)},
+            "xu": {"achieved_tops": round(xu / t / 1e12, 3), "peak_tops": round(peaks["xu_ops"] / 1e12, 3),
+                   "frac": round(xu / t / peaks["xu_ops"], 4)},
+            "flop_per_step": flop, "xu_per_step": xu, "dock_kernel_ms": round(dock_ms, 3)}
+
+
+def load_traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_dock_traffic.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p)).get("dram_bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+# ------------------------------------------------------------ CPU baseline --
+def cpu_baseline(lib, pocket, prm, seconds: float):
+    """The sweep-v1 C oracle (a port of the path) on the host cores, grid
+    mode, on a bounded stride sample of the same library."""
+    from oracle import sweep
+    threads = os.cpu_count() or 1
+    op = sweep.OraclePocket(pocket, grid_spacing=0.4, grid_pad=2.0)
+    n = len(lib)
+    probe = list(range(0, n, max(1, n // (2 * threads))))[: 2 * threads]
+    t0 = time.perf_counter()
+    sweep.dock_library(op, lib, prm, threads=threads, sel=probe)
+    dt = time.perf_counter() - t0
+    per = dt / len(probe)
+    m = int(max(threads, min(n, seconds / max(per, 1e-6))))
+    sel = list(range(0, n, max(1, n // m)))[:m]
+    t0 = time.perf_counter()
+    sweep.dock_library(op, lib, prm, threads=threads, sel=sel)
+    dt = time.perf_counter() - t0
+    return {"value": round(len(sel) / dt, 3), "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{len(sel)} ligands (stride sample of the C2 library), sweep-v1 C oracle, "
+                      f"grid mode, {threads} threads, {dt:.1f} s"}
+
+
+# -------------------------------------------------------------- reference --
+def run_reference(args, rank, world):
+    """The reference's own CPU path (oracle/_ref: dock::dock gradient ascent,
+    rescore, filter_poses, best), all host threads, analytic pocket (the
+    reference has no grid maps), C2 knobs with ls_max_steps 500."""
+    if rank != 0:
+        return
+    from oracle import ref as R
+    import paper_2304_09953_b200 as V
+    threads = os.cpu_count() or 1
+    pocket = make_pocket()
+    pj = V.pocket_to_json(pocket)
+    rp = R.RefPocket(pj)
+    n_lib = 4 * threads * (args.steps + 1)
+    lib, ids_all, _ = build_workload(max(n_lib, 64), 0, 1, threads)
+    ao, to, mo = lib.offsets()
+
+    def ref_lig(i):
+        # conformer + topology of the library entry (same bytes as our arm)
+        from paper_2304_09953_b200.chem import random_smiles
+        smi = random_smiles(CORPUS_SEED, int(lib.ids[i][1:]))
+        lg = R.RefLigand(smi, iterations=-1)
+        lg.set_coords(lib.coords[ao[i]:ao[i + 1]])
+        return lg
+
+    prm = params()
+    stride = max(1, len(lib) // (threads * max(args.steps, 1)))
+    cursor = [0]
+
+    def step(count):
+        sel = [(cursor[0] + k * stride) % len(lib) for k in range(count)]
+        cursor[0] += 1
+        ligs = [ref_lig(i) for i in sel]
+        seeds = [int(lib.seeds[i]) for i in sel]
+        t0 = time.perf_counter()
+        R.dock_best_many(ligs, rp, prm.restarts, prm.diversity_delta, seeds, 500, prm.keep_top,
+                         prm.min_score, threads)
+        return count, time.perf_counter() - t0
+
+    for _ in range(args.warmup):
+        step(1)
+    done, secs = 0, 0.0
+    for _ in range(args.steps):
+        c, dt = step(threads)
+        done += c
+        secs += dt
+    value = done / secs
+    line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * secs / args.steps, 1),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": dict(CONFIG, workload=CONFIG["workload"] + "; reference: analytic pocket "
+                           "(no grid maps in the reference), dock() ascent ls_max_steps 500"),
+            "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads,
+                             "kind": "reference",
+                             "sample": f"{done} ligands over {args.steps} steps ({threads} per step, "
+                                       f"stride sample), reference dock()+rescore+filter_poses, "
+                                       f"{threads} threads"},
+            "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------- ours --
+def h2d_bytes(lib):
+    A = int(np.sum(lib.n_atoms))
+    T = int(np.sum(lib.n_tors))
+    _, to, _ = lib.offsets()
+    cm = np.concatenate([[0], np.cumsum(lib.moving_count.astype(np.int64))])
+    m = cm[to[1:]] - cm[to[:-1]]
+    mv = int(np.sum((m + 15) // 16 * 16))
+    n = len(lib)
+    return 32 * A + 16 * n + 8 * n + 16 * T + mv + 8 * n + 4 * n + 4 * n
+
+
+def d2h_bytes(lib, prm):
+    n = len(lib)
+    T = int(np.sum(lib.n_tors))
+    return 4 * n * 3 + 40 * n * prm.keep_top + 4 * T * prm.keep_top + 8 * n + 8 * TOP_K
+
+
+def main():
+    args = parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    import torch.distributed as dist
+    import paper_2304_09953_b200 as V
+    from paper_2304_09953_b200.pipeline import gather_topk
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    threads = max(1, (os.cpu_count() or 1) // world)
+    t_build = time.perf_counter()
+    lib, ids_all, order = build_workload(args.ligands, rank, world, threads)
+    t_build = time.perf_counter() - t_build
+    pocket = make_pocket()
+    prm = params()
+    eng = V.Engine(local)
+    eng.set_pocket(pocket, grid_spacing=0.4, grid_pad=2.0)
+    peaks = eng.measure_peaks()
+    eng.upload(lib)
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+    keys = torch.empty(TOP_K, dtype=torch.int64, device="cuda")
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > L2
+
+    def step():
+        eng.dock(prm, sptr)
+        if world > 1:
+            return gather_topk(eng, TOP_K)
+        eng.topk_device(TOP_K, keys.data_ptr(), sptr)
+        return keys
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches0 = eng.launch_count()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    dock_ms = []
+    with ClockSampler(local) as clocks:
+        for k in range(args.steps):
+            flush.zero_()  # L2 flush between timed iterations
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            ev[k][0].record(stream)
+            out = step()
+            ev[k][1].record(stream)
+            torch.cuda.synchronize()
+            dock_ms.append(eng.last_dock_ms())
+    launches = eng.launch_count() - launches0
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    stats = eng.stats()
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    n_total = len(lib) * world
+    value = n_total * args.steps / (total_ms * 1e-3)
+    flop, xu = algorithmic_work(lib, prm, stats, True, sum(s.kind == "steric" for s in pocket.sites))
+    rl = roofline(flop, xu, float(np.mean(dock_ms)), peaks, load_traffic())
+    top = out.cpu().numpy().view(np.uint64)
+    n_ranked = int(np.sum(top != np.uint64(2**64 - 1)))
+
+    e2e = None
+    if not args.no_e2e:
+        n_e2e = max(1, min(args.steps, 3))
+        eng.dock_host(lib, prm)  # warm the host path
+        if world > 1:
+            dist.barrier()
+        e2e_t = []
+        for _ in range(n_e2e):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            eng.dock_host(lib, prm)
+            if world > 1:
+                merged = gather_topk(eng, TOP_K).cpu()
+            else:
+                eng.topk(TOP_K)
+            e2e_t.append(time.perf_counter() - t0)
+        te = torch.tensor([sum(e2e_t)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(n_total * n_e2e / float(te.item()), 2), "unit": UNIT,
+               "h2d_bytes_per_step": h2d_bytes(lib) * world,
+               "d2h_bytes_per_step": d2h_bytes(lib, prm) * world,
+               "steps": n_e2e,
+               "path": "vs_dock_host (pack + H2D + dock + D2H results) + top-k D2H, host wall clock"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(lib, pocket, prm, args.cpu_seconds)
+
+    if rank == 0:
+        info = eng.device_info()
+        line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": round(total_ms / args.steps, 3), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64",
+                "data": "synthetic",
+                "config": dict(CONFIG, ligands_per_gpu=len(lib), ligands_total=n_total,
+                               parallelism=f"dp{world}" if world > 1 else "single",
+                               l2="flushed (512 MB write) before every timed step",
+                               timed="device-resident library -> per-ligand best + global top-1000"),
+                "roofline": rl, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clocks.summary(), "device": info["name"], "peaks": peaks,
+                "work": stats, "ranked": n_ranked, "library_build_s": round(t_build, 2)}
+        s = json.dumps(line)
+        print(s, flush=True)
+        if args.json_out:
+            with open(args.json_out, "w") as f:
+                f.write(s + "\n")
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    eng.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -163,6 +163,12 @@ int vs_dock_host(vs_handle* h, const vs_library* lib, const vs_size_class* class
  * the last vs_dock call, and the number of kernels this handle launched. */
 double vs_last_dock_ms(const vs_handle* h);
 uint64_t vs_launch_count(const vs_handle* h);
+/* work counters of the last vs_dock: [0] translation-sweep iterations,
+ * [1] the same weighted by ligand atoms, [2] start attempts, [3] flex
+ * candidate states */
+int vs_last_stats(vs_handle* h, uint64_t out[4]);
+/* measured device peaks (ops/s): FP32 FMA (2 flops), FP64 FMA, MUFU ex2 */
+int vs_measure_peaks(vs_handle* h, double* fp32_flops, double* fp64_flops, double* xu_ops);
 
 /* Global top-k of the last run: keys ascending = (score desc, id_rank asc)
  * (rank_ligands, pipeline.cpp:243-251).  key = (~orderable(score) << 32) |
@@ -217,6 +223,14 @@ int vs_libbuild_fetch(const vs_libbuild* b, int32_t* status, int32_t* n_atoms, i
                       int32_t* rot_bonds, double* coords, int32_t* atom_class, int32_t* axis_a,
                       int32_t* axis_b, int32_t* moving_count, int32_t* moving);
 void vs_libbuild_free(vs_libbuild* b);
+/* synthetic libraries from the reference corpus sampler: indices i of the
+ * first n_want entries random_smiles(Rng(seed).split(i)) within the atom /
+ * torsion bounds (inclusive); then build those entries */
+int vs_corpus_select(uint64_t seed, int64_t n_want, int32_t atom_lo, int32_t atom_hi,
+                     int32_t tors_lo, int32_t tors_hi, int64_t max_scan, int32_t threads,
+                     int64_t* out_index);
+int vs_libbuild_corpus(uint64_t seed, const int64_t* index, int32_t n, const uint64_t* embed_seeds,
+                       int32_t iterations, int32_t threads, vs_libbuild** out);
 
 /* batcher (batcher.cpp:7-86) */
 int vs_default_classes(vs_size_class* out, int32_t cap);

@@ -102,6 +102,8 @@ _SIGS = {
                                P(vs_dock_params), P(vs_results)]),
     "vs_last_dock_ms": (C.c_double, [C.c_void_p]),
     "vs_launch_count": (C.c_uint64, [C.c_void_p]),
+    "vs_last_stats": (C.c_int, [C.c_void_p, P(C.c_uint64)]),
+    "vs_measure_peaks": (C.c_int, [C.c_void_p, P(C.c_double), P(C.c_double), P(C.c_double)]),
     "vs_topk": (C.c_int, [C.c_void_p, C.c_int32, P(C.c_uint64)]),
     "vs_topk_device": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
     "vs_topk_merge_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,
@@ -119,6 +121,10 @@ _SIGS = {
     "vs_libbuild_fetch": (C.c_int, [C.c_void_p] + [P(C.c_int32)] * 4 + [P(C.c_double)] +
                           [P(C.c_int32)] * 5),
     "vs_libbuild_free": (None, [C.c_void_p]),
+    "vs_corpus_select": (C.c_int, [C.c_uint64, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
+                                   C.c_int32, C.c_int64, C.c_int32, P(C.c_int64)]),
+    "vs_libbuild_corpus": (C.c_int, [C.c_uint64, P(C.c_int64), C.c_int32, P(C.c_uint64),
+                                     C.c_int32, C.c_int32, P(C.c_void_p)]),
     "vs_default_classes": (C.c_int, [P(vs_size_class), C.c_int32]),
     "vs_size_class_of": (C.c_int, [C.c_int32, C.c_int32, P(vs_size_class), C.c_int32]),
     "vs_target_batch_size": (C.c_int, [P(vs_size_class), C.c_double, C.c_double, C.c_double,

@@ -285,18 +285,36 @@ def id_ranks(ids: Sequence[str]) -> np.ndarray:
     return out[:len(ids)]
 
 
-def build_library(smiles: Sequence[str], ids: Sequence[str] | None = None,
-                  embed_seeds: Sequence[int] | None = None, dock_seeds: Sequence[int] | None = None,
-                  iterations: int = 200, threads: int = 8, drop_failed: bool = True) -> Library:
-    """Parse + embed + topology for many ligands on `threads` host threads
-    (the parse/embed stages of run_campaign, pipeline.cpp:383-431)."""
-    n = len(smiles)
-    ids = list(ids) if ids is not None else [f"L{i + 1}" for i in range(n)]
-    es = np.array([int(s) & (2**64 - 1) for s in (embed_seeds if embed_seeds is not None else [0] * n)],
-                  np.uint64)
-    blob = b"".join(s.encode() + b"\0" for s in smiles) or b"\0"
+def corpus_indices(seed: int, n: int, atoms: tuple[int, int], tors: tuple[int, int],
+                   threads: int = 8, max_scan: int | None = None) -> np.ndarray:
+    """Indices of the first n corpus entries random_smiles(Rng(seed).split(i))
+    whose heavy atoms / torsion axes lie in the inclusive bounds."""
+    out = np.zeros(max(n, 1), np.int64)
+    got = _lib.vs_corpus_select(seed, n, atoms[0], atoms[1], tors[0], tors[1],
+                                max_scan or 50 * n + 100000, threads, ptr(out, C.c_int64))
+    check(got)
+    return out[:got]
+
+
+def corpus_library(seed: int, n: int, atoms: tuple[int, int], tors: tuple[int, int],
+                   embed_master: int = 2024, dock_master: int = 2024, iterations: int = 200,
+                   threads: int = 8) -> Library:
+    """Synthetic library: corpus entries filtered to the size
+    bounds; embed seed Rng(master).split(1).split(i), dock seed .split(2)
+    .split(i) with i the index in the library (pipeline.cpp:422-484)."""
+    from .pipeline import campaign_seeds
+    idx = corpus_indices(seed, n, atoms, tors, threads)
+    m = len(idx)
+    es = campaign_seeds(embed_master, m, stage=1)
+    ds = campaign_seeds(dock_master, m, stage=2)
     h = C.c_void_p()
-    check(_lib.vs_libbuild_run(blob, n, ptr(es, C.c_uint64), iterations, threads, C.byref(h)))
+    check(_lib.vs_libbuild_corpus(seed, ptr(idx, C.c_int64), m, ptr(es, C.c_uint64), iterations,
+                                  threads, C.byref(h)))
+    ids = [f"Z{int(i)}" for i in idx]
+    return _fetch_built(h, m, ids, ds)
+
+
+def _fetch_built(h, n, ids, ds, drop_failed=True) -> Library:
     try:
         A, T, M = C.c_int64(), C.c_int64(), C.c_int64()
         _lib.vs_libbuild_sizes(h, C.byref(A), C.byref(T), C.byref(M))
@@ -313,11 +331,10 @@ def build_library(smiles: Sequence[str], ids: Sequence[str] | None = None,
     finally:
         _lib.vs_libbuild_free(h)
     st, na, nt, rb = st[:n], na[:n], nt[:n], rb[:n]
-    ds = np.array([int(s) & (2**64 - 1) for s in (dock_seeds if dock_seeds is not None else [0] * n)],
-                  np.uint64)
-    lib = Library(ids=ids, n_atoms=na, n_tors=nt, rot_bonds=rb, coords=coords[:A.value],
+    lib = Library(ids=list(ids), n_atoms=na, n_tors=nt, rot_bonds=rb, coords=coords[:A.value],
                   atom_class=cls[:A.value], axis_a=aa[:T.value], axis_b=ab[:T.value],
-                  moving_count=mc[:T.value], moving=mv[:M.value], seeds=ds, id_rank=id_ranks(ids))
+                  moving_count=mc[:T.value], moving=mv[:M.value],
+                  seeds=np.asarray(ds, np.uint64), id_rank=id_ranks(ids))
     lib.status = st
     if drop_failed and (st != 0).any():
         keep = np.nonzero(st == 0)[0]
@@ -325,3 +342,20 @@ def build_library(smiles: Sequence[str], ids: Sequence[str] | None = None,
         lib = lib.subset(keep)
         lib.status = status
     return lib
+
+
+def build_library(smiles: Sequence[str], ids: Sequence[str] | None = None,
+                  embed_seeds: Sequence[int] | None = None, dock_seeds: Sequence[int] | None = None,
+                  iterations: int = 200, threads: int = 8, drop_failed: bool = True) -> Library:
+    """Parse + embed + topology for many ligands on `threads` host threads
+    (the parse/embed stages of run_campaign, pipeline.cpp:383-431)."""
+    n = len(smiles)
+    ids = list(ids) if ids is not None else [f"L{i + 1}" for i in range(n)]
+    es = np.array([int(s) & (2**64 - 1) for s in (embed_seeds if embed_seeds is not None else [0] * n)],
+                  np.uint64)
+    blob = b"".join(s.encode() + b"\0" for s in smiles) or b"\0"
+    h = C.c_void_p()
+    check(_lib.vs_libbuild_run(blob, n, ptr(es, C.c_uint64), iterations, threads, C.byref(h)))
+    ds = np.array([int(s) & (2**64 - 1) for s in (dock_seeds if dock_seeds is not None else [0] * n)],
+                  np.uint64)
+    return _fetch_built(h, n, ids, ds, drop_failed)

@@ -198,6 +198,58 @@ int vs_libbuild_fetch(const vs_libbuild* b, int32_t* status, int32_t* n_atoms, i
 
 void vs_libbuild_free(vs_libbuild* b) { delete b; }
 
+// Scan corpus::random_smiles(Rng(seed).split(i)) for i = 0, 1, ... and keep
+// the first n_want whose heavy atoms lie in [atom_lo, atom_hi] and torsion
+// axes in [tors_lo, tors_hi] (the C1-C4 library filters).
+int vs_corpus_select(uint64_t seed, int64_t n_want, int32_t atom_lo, int32_t atom_hi,
+                     int32_t tors_lo, int32_t tors_hi, int64_t max_scan, int32_t threads,
+                     int64_t* out_index) {
+  const int nt = std::max(1, threads);
+  const int64_t chunk = 4096;
+  int64_t found = 0;
+  std::vector<char> ok(static_cast<std::size_t>(chunk));
+  for (int64_t base = 0; base < max_scan && found < n_want; base += chunk) {
+    std::atomic<int64_t> next{0};
+    auto work = [&] {
+      for (int64_t k = next.fetch_add(1); k < chunk; k = next.fetch_add(1)) {
+        ok[k] = 0;
+        try {
+          const Graph g = parse_smiles(random_smiles(seed, static_cast<uint64_t>(base + k)));
+          const int n = static_cast<int>(g.elements.size());
+          const int t = static_cast<int>(torsion_axes(g).axes.size());
+          ok[k] = (n >= atom_lo && n <= atom_hi && t >= tors_lo && t <= tors_hi) ? 1 : 0;
+        } catch (const std::exception&) {
+        }
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nt; ++t) pool.emplace_back(work);
+    for (auto& th : pool) th.join();
+    for (int64_t k = 0; k < chunk && found < n_want && base + k < max_scan; ++k)
+      if (ok[k]) out_index[found++] = base + k;
+  }
+  return static_cast<int>(found);
+}
+
+// vs_libbuild_run over corpus entries given by index (SMILES generated here).
+int vs_libbuild_corpus(uint64_t seed, const int64_t* index, int32_t n, const uint64_t* embed_seeds,
+                       int32_t iterations, int32_t threads, vs_libbuild** out) {
+  auto* b = new vs_libbuild;
+  b->ligs.resize(static_cast<std::size_t>(n));
+  std::atomic<int> next{0};
+  auto work = [&] {
+    for (int i = next.fetch_add(1); i < n; i = next.fetch_add(1))
+      b->ligs[i] = build_one(random_smiles(seed, static_cast<uint64_t>(index[i])), embed_seeds[i],
+                             iterations);
+  };
+  const int nt = std::max(1, std::min<int>(threads, n));
+  std::vector<std::thread> pool;
+  for (int t = 0; t < nt; ++t) pool.emplace_back(work);
+  for (auto& th : pool) th.join();
+  *out = b;
+  return VS_OK;
+}
+
 // ---------------------------------------------------------------- batcher --
 int vs_default_classes(vs_size_class* out, int32_t cap) {
   static const int atoms[4] = {1, 20, 40, 80};  // batcher.cpp:9-10

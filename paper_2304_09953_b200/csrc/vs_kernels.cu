@@ -18,6 +18,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "vs_detmath.cuh"
 #include "vs_types.h"
 
@@ -466,6 +468,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     const int N = meta.y, T = meta.w;
     const unsigned long long root = rng_mix(lib.seeds[lig] ^ kGolden);
     int nk = 0;
+    unsigned long long st_trans = 0, st_att = 0, st_flex = 0;
 
     for (int r = 0; r < R; ++r) {
       const unsigned long long rkey =
@@ -575,8 +578,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
           } else {
             sc = sc * 0.5f;
           }
+          ++st_trans;
         }
       }
+      st_att += static_cast<unsigned long long>(att) + 1;
       const Mat3d RD = det_pose_mat_d(pw, px, py, pz);
       const double tdx = ptx, tdy = pty, tdz = ptz;
 
@@ -584,6 +589,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
       // columns start from the shared prefix (torsions < j at state values)
       const bool do_flex = T > 0 && prm.F > 0;
       const int steps = do_flex ? prm.F * T : 1;
+      st_flex += do_flex ? static_cast<unsigned long long>(steps) * prm.A : 1ull;
       float S_cur = 0.0f;
       int win = 0;
       for (int st = 0; st < steps; ++st) {
@@ -740,6 +746,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
           n_surv > 0 ? ((static_cast<unsigned long long>(~det_orderable(bmax)) << 32) |
                         lib.id_rank[lig])
                      : ~0ull;
+      if (out.stats) {
+        atomicAdd(out.stats + 0, st_trans);
+        atomicAdd(out.stats + 1, st_trans * static_cast<unsigned long long>(N));
+        atomicAdd(out.stats + 2, st_att);
+        atomicAdd(out.stats + 3, st_flex);
+      }
     }
     __syncwarp();
   }
@@ -863,6 +875,43 @@ __global__ void __launch_bounds__(1024)
     out[static_cast<long>(blockIdx.x) * k + i] = sk[i];
 }
 
+// ====================================================== peak microbenchmarks
+// Independent FMA / MUFU chains per thread; the result is stored only under a
+// never-true predicate so the chains are not dead code.
+__global__ void vs_peak_fp32(float* out, int iters, float seed) {
+  float a[8];
+  for (int k = 0; k < 8; ++k) a[k] = seed + threadIdx.x * 1e-7f + k;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = fmaf(a[k], 0.999999f, 1e-7f);
+  }
+  float s = 0.0f;
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == -1.2345f) out[threadIdx.x] = s;
+}
+__global__ void vs_peak_fp64(double* out, int iters, double seed) {
+  double a[8];
+  for (int k = 0; k < 8; ++k) a[k] = seed + threadIdx.x * 1e-9 + k;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = fma(a[k], 0.999999999, 1e-9);
+  }
+  double s = 0.0;
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == -1.2345) out[threadIdx.x] = s;
+}
+__global__ void vs_peak_xu(float* out, int iters, float seed) {
+  float a[8];
+  for (int k = 0; k < 8; ++k) a[k] = seed * 1e-3f + threadIdx.x * 1e-9f + k * 1e-3f;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[k]));
+  }
+  float s = 0.0f;
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == -1.2345f) out[threadIdx.x] = s;
+}
+
 }  // namespace vs
 
 // ------------------------------------------------------ launch wrappers --
@@ -938,6 +987,33 @@ cudaError_t launch_grid(cudaStream_t st, const PocketDev& pk, float* steric, flo
 }
 
 int topk_chunk() { return kTopkC; }
+
+// kind 0 fp32 fma, 1 fp64 fma, 2 ex2; returns ops/s (best of 3)
+double measure_peak(int kind, int sms) {
+  void* buf = nullptr;
+  cudaMalloc(&buf, 1024 * 8);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const int blocks = sms * 8, threads = 256, iters = 4096;
+  double best = 0.0;
+  for (int rep = 0; rep < 4; ++rep) {
+    cudaEventRecord(a);
+    if (kind == 0) vs_peak_fp32<<<blocks, threads>>>(static_cast<float*>(buf), iters, 1.0f);
+    else if (kind == 1) vs_peak_fp64<<<blocks, threads>>>(static_cast<double*>(buf), iters, 1.0);
+    else vs_peak_xu<<<blocks, threads>>>(static_cast<float*>(buf), iters, 1.0f);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, a, b);
+    const double ops = static_cast<double>(blocks) * threads * iters * 8 * (kind == 2 ? 1.0 : 2.0);
+    if (rep > 0) best = std::max(best, ops / (ms * 1e-3));
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(buf);
+  return best;
+}
 
 cudaError_t launch_topk(cudaStream_t st, const unsigned long long* in, long n,
                         unsigned long long* out, int k, int blocks) {

@@ -31,6 +31,7 @@ cudaError_t launch_rescore(bool grid, int blocks, size_t smem, cudaStream_t st, 
 cudaError_t launch_grid(cudaStream_t st, const PocketDev& pk, float* steric, float* hb,
                         float* lipo);
 int topk_chunk();
+double measure_peak(int kind, int sms);
 cudaError_t launch_topk(cudaStream_t st, const unsigned long long* in, long n,
                         unsigned long long* out, int k, int blocks);
 }  // namespace vs
@@ -125,7 +126,7 @@ struct vs_handle {
   vs_dock_params last_prm{};
   bool has_results = false;
   DBuf d_surv, d_surv_tors, d_all, d_all_tors, d_best, d_nkept, d_nsurv, d_keys, d_counters;
-  DBuf d_sx, d_sp, d_sm, d_rots, d_topk_a, d_topk_b;
+  DBuf d_sx, d_sp, d_sm, d_rots, d_topk_a, d_topk_b, d_stats;
   int rots_k = -1;
   uint64_t rots_seed = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -334,7 +335,7 @@ void vs_destroy(vs_handle* h) {
   h->lib.release();
   for (DBuf* b : {&h->d_sites, &h->d_maps, &h->d_surv, &h->d_surv_tors, &h->d_all, &h->d_all_tors,
                   &h->d_best, &h->d_nkept, &h->d_nsurv, &h->d_keys, &h->d_counters, &h->d_sx,
-                  &h->d_sp, &h->d_sm, &h->d_rots, &h->d_topk_a, &h->d_topk_b})
+                  &h->d_sp, &h->d_sm, &h->d_rots, &h->d_topk_a, &h->d_topk_b, &h->d_stats})
     b->release();
   cudaEventDestroy(h->ev0);
   cudaEventDestroy(h->ev1);
@@ -489,6 +490,8 @@ int vs_dock(vs_handle* h, const vs_dock_params* prm, void* stream) {
   VS_CUDA(h, h->d_nsurv.ensure(nn * 4));
   VS_CUDA(h, h->d_keys.ensure(nn * 8));
   VS_CUDA(h, h->d_counters.ensure(64 * sizeof(int)));
+  VS_CUDA(h, h->d_stats.ensure(4 * sizeof(unsigned long long)));
+  VS_CUDA(h, cudaMemsetAsync(h->d_stats.p, 0, 4 * sizeof(unsigned long long), st));
   VS_CUDA(h, cudaMemsetAsync(h->d_keys.p, 0xff, nn * 8, st));
   VS_CUDA(h, cudaMemsetAsync(h->d_nkept.p, 0, nn * 4, st));
   VS_CUDA(h, cudaMemsetAsync(h->d_nsurv.p, 0, nn * 4, st));
@@ -512,6 +515,7 @@ int vs_dock(vs_handle* h, const vs_dock_params* prm, void* stream) {
   out.n_kept = h->d_nkept.as<int>();
   out.n_surv = h->d_nsurv.as<int>();
   out.keys = h->d_keys.as<unsigned long long>();
+  out.stats = h->d_stats.as<unsigned long long>();
 
   const bool grid = h->pk.grid_mode != 0;
   const LibDev ld = P.dev();
@@ -563,6 +567,23 @@ double vs_last_dock_ms(const vs_handle* h) {
 }
 
 uint64_t vs_launch_count(const vs_handle* h) { return h->launches; }
+
+int vs_last_stats(vs_handle* h, uint64_t out[4]) {
+  if (!h->has_results) return fail(h, VS_ERR_STATE, "no results");
+  VS_CUDA(h, cudaStreamSynchronize(h->last));
+  VS_CUDA(h, cudaMemcpy(out, h->d_stats.p, 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  return VS_OK;
+}
+
+int vs_measure_peaks(vs_handle* h, double* fp32, double* fp64, double* xu) {
+  cudaSetDevice(h->device);
+  VS_CUDA(h, cudaDeviceSynchronize());
+  if (fp32) *fp32 = measure_peak(0, h->sms);
+  if (fp64) *fp64 = measure_peak(1, h->sms);
+  if (xu) *xu = measure_peak(2, h->sms);
+  VS_CUDA(h, cudaGetLastError());
+  return VS_OK;
+}
 
 int vs_fetch_results(vs_handle* h, vs_results* o) {
   cudaSetDevice(h->device);

@@ -79,6 +79,7 @@ struct DockOut {
   int* n_kept;          // [n]
   int* n_surv;          // [n]
   unsigned long long* keys;  // [n] top-k keys (score desc, id_rank asc)
+  unsigned long long* stats; // [4] work counters (capi.h vs_last_stats)
 };
 
 }  // namespace vs

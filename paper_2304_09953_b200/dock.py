@@ -331,6 +331,19 @@ class Engine:
     def launch_count(self) -> int:
         return int(_lib.vs_launch_count(self._h))
 
+    def stats(self) -> dict:
+        """Work counters of the last dock (capi.h vs_last_stats)."""
+        out = np.zeros(4, np.uint64)
+        check(_lib.vs_last_stats(self._h, ptr(out, C.c_uint64)), self._h, "stats")
+        return {"translation_iters": int(out[0]), "translation_iter_atoms": int(out[1]),
+                "start_attempts": int(out[2]), "flex_states": int(out[3])}
+
+    def measure_peaks(self) -> dict:
+        """Measured FP32 / FP64 FMA (flop/s) and MUFU ex2 (op/s) peaks."""
+        a, b, c = C.c_double(), C.c_double(), C.c_double()
+        check(_lib.vs_measure_peaks(self._h, C.byref(a), C.byref(b), C.byref(c)), self._h, "peaks")
+        return {"fp32_flops": a.value, "fp64_flops": b.value, "xu_ops": c.value}
+
     def rescore(self, lib: Library, pose_lig, t, q, tors):
         """K3a: canonical geometric score and rescore of given poses."""
         pose_lig = np.ascontiguousarray(pose_lig, np.int32)

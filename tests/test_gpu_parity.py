@@ -205,7 +205,8 @@ def test_topk_matches_oracle(V, engine, lib200, pocket_json):
         keys = engine.topk(k)
         np.testing.assert_array_equal(keys, sweep.topk(res.keys, k))
     keys = engine.topk(50)
-    scores = [V.dock.key_score(k) for k in keys if k != 2**64 - 1]
+    from paper_2304_09953_b200.dock import key_score
+    scores = [key_score(k) for k in keys if k != 2**64 - 1]
     assert all(a >= b for a, b in zip(scores, scores[1:]))
     # ranking order = rank_ligands over (id, best) (pipeline.cpp:243-251)
     from paper_2304_09953_b200.pipeline import ids_by_rank, keys_to_ranked, rank_ligands
