@@ -350,7 +350,8 @@ def main():
     eng.set_pocket(pocket, grid_spacing=0.4, grid_pad=2.0)
     peaks = eng.measure_peaks()
     eng.upload(lib)
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()  # non-default stream shared by torch events and the C-ABI
+    torch.cuda.set_stream(stream)
     sptr = stream.cuda_stream
     keys = torch.empty(TOP_K, dtype=torch.int64, device="cuda")
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > L2

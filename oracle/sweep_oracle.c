@@ -392,6 +392,49 @@ static void pose_coords(const lig_t* L, const double* y, const mat3d* R, const d
   }
 }
 
+/* field + wall of one local coordinate under (R, t): FP64 transform */
+static void atom_terms(const vso_pocket* p, const mat3d* R, const double* t, const double* y,
+                       float* f, float* w, float* xo) {
+  double v[3];
+  apply_d(R, y, t, v);
+  float x[3] = {(float)v[0], (float)v[1], (float)v[2]};
+  *f = field(p, x);
+  *w = wall(p, x);
+  if (xo) memcpy(xo, x, 12);
+}
+
+/* pair clash softplus from FP64 coordinates (dock.cpp:86-97) */
+static float pair_d(const vso_pocket* p, const double* a, const double* b) {
+  double d2 = n2d(a[0] - b[0], a[1] - b[1], a[2] - b[2]);
+  if (d2 > (double)p->cut2) return 0.0f;
+  return vso_softplus((p->r - sqrtf((float)d2)) * 10.0f);
+}
+
+/* xor butterfly over 32 lane partial sums (warp_sum of the kernel) */
+static float butterfly(const float* in) {
+  float a[32], b[32];
+  memcpy(a, in, sizeof(a));
+  for (int off = 16; off > 0; off >>= 1) {
+    for (int l = 0; l < 32; ++l) b[l] = a[l] + a[l ^ off];
+    memcpy(a, b, sizeof(a));
+  }
+  return a[0];
+}
+
+/* flex move rotation: about axis o->b by th_new - th_old (FP64), half angle
+ * folded into [-pi/2, pi/2] (q -> -q leaves the matrix unchanged) */
+static mat3d flex_mat(const double* o, const double* b, float th_new, float th_old) {
+  double dx = b[0] - o[0], dy = b[1] - o[1], dz = b[2] - o[2];
+  double n = sqrt(n2d(dx, dy, dz));
+  double hh = 0.5 * ((double)th_new - (double)th_old);
+  if (hh > 1.57079632679489661923) hh = hh - PI_D;
+  else if (hh < -1.57079632679489661923) hh = hh + PI_D;
+  double s, c;
+  sincos_d(hh, &s, &c);
+  double ks = n > 0.0 ? s / n : 0.0;
+  return quat_mat_d(c, dx * ks, dy * ks, dz * ks);
+}
+
 /* canonical score S = (Fe+Fo) - lam*((Pe+Po) + (We+Wo)), parity sums;
  * FP64 geometry, FP32 terms */
 static float score_state(const vso_pocket* p, const lig_t* L, const double* y, const mat3d* R,
@@ -457,8 +500,8 @@ static uint32_t orderable(float f) {
   return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
 }
 
-#define TRANS_ITERS 24
-#define TRANS_MIN (1.0f / 512.0f)
+#define TRANS_ITERS 16
+#define TRANS_MIN (1.0f / 64.0f)
 /* translation lattice: 0 = current, 1..26 = {-1,0,1}^3 \ 0, x fastest */
 static void trans_offset(int l, float sc, float* o) {
   if (l == 0) { o[0] = o[1] = o[2] = 0.0f; return; }
@@ -567,29 +610,75 @@ static void dock_one(const vso_pocket* p, const lig_t* L, uint64_t seed, uint32_
     mat3d RS = pose_mat_d(pq);
     double ptd[3] = {pt[0], pt[1], pt[2]};
 
-    /* greedy torsion flex (FP64 geometry, canonical score) */
+    /* incremental greedy torsion flex (SWEEP_V1.md §2.5): per-atom terms
+     * of the posed state; per (pass, axis j) the candidate score is
+     * base(atoms outside moving_j, pairs not crossing it; 32-lane strided
+     * sums + xor butterfly) + moved part(moving_j atoms rotated about the
+     * state's axis j, and their cross pairs; two parity sums). */
+    float* fa = (float*)malloc(sizeof(float) * (size_t)N);
+    float* wa = (float*)malloc(sizeof(float) * (size_t)N);
+    unsigned char* inm = (unsigned char*)malloc((size_t)N);
+    for (int i = 0; i < N; ++i) atom_terms(p, &RS, ptd, &y[3 * i], &fa[i], &wa[i], NULL);
     float S = 0.0f;
-    if (T == 0 || prm->flex_passes == 0) {
-      S = score_state(p, L, y, &RS, ptd, NULL);
-    } else {
-      for (int f = 0; f < prm->flex_passes; ++f) {
-        for (int j = 0; j < T; ++j) {
-          float bestS = -INFINITY, best_th = th[j];
-          for (int a = 0; a < prm->flex_angles; ++a) {
-            float v2 = th[j];
-            if (a > 0) { v2 = th[j] + (float)a * step; if (v2 >= PI_F) v2 = v2 - TWO_PI_F; }
-            memcpy(thc, th, sizeof(float) * (size_t)T);
-            thc[j] = v2;
-            chain(L, thc, yc);
-            float Sa = score_state(p, L, yc, &RS, ptd, NULL);
-            if (Sa > bestS) { bestS = Sa; best_th = v2; }
+    const int do_flex = T > 0 && prm->flex_passes > 0;
+    const int steps = do_flex ? prm->flex_passes * T : 1;
+    for (int st = 0; st < steps; ++st) {
+      const int j = do_flex ? st % T : -1;
+      const int m = do_flex ? L->cnt[j] : 0;
+      const int* mv = do_flex ? L->moving + L->mstart[j] : NULL;
+      memset(inm, 0, (size_t)N);
+      for (int q2 = 0; q2 < m; ++q2) inm[mv[q2]] = 1;
+      float lf[32], lw[32], lp[32];
+      for (int l = 0; l < 32; ++l) lf[l] = lw[l] = lp[l] = 0.0f;
+      for (int i = 0; i < N; ++i)
+        if (!inm[i]) { lf[i & 31] = lf[i & 31] + fa[i]; lw[i & 31] = lw[i & 31] + wa[i]; }
+      long pi = 0;
+      for (int i = 0; i < N; ++i)
+        for (int k = i + 1; k < N; ++k, ++pi)
+          if (inm[i] == inm[k]) lp[pi & 31] = lp[pi & 31] + pair_d(p, &y[3 * i], &y[3 * k]);
+      const float fb = butterfly(lf), wb = butterfly(lw), pb = butterfly(lp);
+      float bestS = -INFINITY, best_th = 0.0f;
+      int best_a = 0;
+      const int nc = do_flex ? prm->flex_angles : 1;
+      for (int a = 0; a < nc; ++a) {
+        float fm[2] = {0, 0}, wm[2] = {0, 0}, pc[2] = {0, 0};
+        float thn = 0.0f;
+        if (do_flex) {
+          const float tho = th[j];
+          thn = tho;
+          if (a > 0) { thn = tho + (float)a * step; if (thn >= PI_F) thn = thn - TWO_PI_F; }
+          mat3d M = flex_mat(&y[3 * L->a[j]], &y[3 * L->b[j]], thn, tho);
+          const double* o = &y[3 * L->a[j]];
+          for (int q2 = 0; q2 < m; ++q2) {
+            const int idx = mv[q2], hh = q2 & 1;
+            double v[3] = {y[3 * idx] - o[0], y[3 * idx + 1] - o[1], y[3 * idx + 2] - o[2]}, yn[3];
+            apply_d(&M, v, o, yn);
+            float fi, wi;
+            atom_terms(p, &RS, ptd, yn, &fi, &wi, NULL);
+            fm[hh] = fm[hh] + fi;
+            wm[hh] = wm[hh] + wi;
+            for (int k = 0; k < N; ++k)
+              if (!inm[k]) pc[hh] = pc[hh] + pair_d(p, yn, &y[3 * k]);
           }
-          th[j] = best_th;
-          S = bestS;
         }
+        const float Sa = (fb + (fm[0] + fm[1])) - p->lam * ((pb + (pc[0] + pc[1])) + (wb + (wm[0] + wm[1])));
+        if (Sa > bestS) { bestS = Sa; best_th = thn; best_a = a; }
+      }
+      S = bestS;
+      if (do_flex && best_a != 0) {
+        /* move the state to the winner (skipped when candidate 0 wins) */
+        mat3d M = flex_mat(&y[3 * L->a[j]], &y[3 * L->b[j]], best_th, th[j]);
+        const double o[3] = {y[3 * L->a[j]], y[3 * L->a[j] + 1], y[3 * L->a[j] + 2]};
+        for (int q2 = 0; q2 < m; ++q2) {
+          const int idx = mv[q2];
+          double v[3] = {y[3 * idx] - o[0], y[3 * idx + 1] - o[1], y[3 * idx + 2] - o[2]};
+          apply_d(&M, v, o, &y[3 * idx]);
+          atom_terms(p, &RS, ptd, &y[3 * idx], &fa[idx], &wa[idx], NULL);
+        }
+        th[j] = best_th;
       }
     }
-    chain(L, th, y);
+    free(fa); free(wa); free(inm);
     pose_coords(L, y, &RS, ptd, x);
     if (nk == 0 || !near_any(x, kx, nk, N, delta)) { /* dock.cpp:359-361 */
       memcpy(kx + (size_t)nk * 3 * N, x, sizeof(float) * 3 * N);

@@ -20,7 +20,9 @@ namespace vs {
 // e^x for x <= 0; 0 below -87 (e^-87 < 1.7e-38).
 __device__ __forceinline__ float det_exp_neg(float x) {
   if (x < -87.0f) return 0.0f;
-  const float k = rintf(x * 1.44269504f);
+  // k = rint(x log2 e) by the 1.5*2^23 shifter (same value as rintf, no F2I)
+  const float sh = __fadd_rn(x * 1.44269504f, 12582912.0f);
+  const float k = sh - 12582912.0f;
   float r = fmaf(k, -0.693145752f, x);
   r = fmaf(k, -1.42860677e-06f, r);
   float p = 1.98412698e-04f;
@@ -31,7 +33,7 @@ __device__ __forceinline__ float det_exp_neg(float x) {
   p = fmaf(p, r, 0.5f);
   p = fmaf(p, r, 1.0f);
   p = fmaf(p, r, 1.0f);
-  const float s = __int_as_float((static_cast<int>(k) + 127) << 23);
+  const float s = __int_as_float((__float_as_int(sh) - 0x4B400000 + 127) << 23);
   return p * s;
 }
 

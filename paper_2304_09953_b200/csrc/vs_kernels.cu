@@ -1,20 +1,21 @@
 // sm_100a kernels of the dock-and-score path.
 //
 //   vs_dock_kernel     K2+K3+K4a  sweep-v1 pose generation (rigid
-//                      roto-translation sweep + torsion flex), canonical
-//                      scoring, diversity, keep-top filter, rescore,
-//                      per-ligand best and top-k key.  One warp per ligand,
-//                      persistent warps pulling ligands from an atomic
-//                      counter (LPT order from the packer).
+//                      roto-translation sweep + incremental torsion flex),
+//                      canonical scoring, diversity, keep-top filter,
+//                      rescore, per-ligand best and top-k key.  One warp per
+//                      ligand, persistent warps pulling ligands from an
+//                      atomic counter (LPT order from the packer).
 //   vs_rescore_kernel  K3a  geometric_score / rescore of given poses.
-//   vs_grid_kernel     N1   pocket grid maps (steric / hbond / lipophilic).
+//   vs_grid_kernel     N1   pocket grid maps (steric / hbond / lipophilic),
+//   vs_pack_kernel          + corner-packed cells for one-sector lookups.
 //   vs_topk_kernel     K4b  block-bitonic tournament top-k over u64 keys.
 //
 // Ligand records are staged into shared memory with one-dimensional TMA
 // bulk copies (cp.async.bulk + mbarrier complete_tx).  All arithmetic that
-// feeds a score or a decision is the deterministic FP32 arithmetic of
-// vs_detmath.cuh; sums are fixed-order (two parity accumulators per term,
-// docs/SWEEP_V1.md §3) so the CPU oracle reproduces them bit for bit.
+// feeds a score or a decision is the deterministic arithmetic of
+// vs_detmath.cuh with fixed-order sums (docs/SWEEP_V1.md §3), so the CPU
+// oracle reproduces every score and decision bit for bit.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -28,6 +29,7 @@ namespace vs {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr unsigned long long kGolden = 0x9e3779b97f4a7c15ull;
 constexpr double kPiD = 3.14159265358979323846;
+constexpr double kHalfPiD = 1.57079632679489661923;
 constexpr float kPiF = 3.14159274f;     // (float)pi, rounds up
 constexpr float kTwoPiF = 6.28318548f;  // (float)(2 pi)
 
@@ -98,8 +100,11 @@ __device__ __forceinline__ float site_sum(const SiteF* __restrict__ s, int n, fl
   return acc;
 }
 
-__device__ __forceinline__ float trilinear(const GridDev& g, const float* __restrict__ m, float x,
-                                           float y, float z) {
+// Trilinear interpolation on one corner-packed cell (two 16 B loads of the
+// same 32 B sector).  Same corner values and lerp order as the node layout,
+// so the result is bit-identical to interpolating the node map.
+__device__ __forceinline__ float trilinear(const GridDev& g, const float4* __restrict__ cells,
+                                           float x, float y, float z) {
   const float gx = (x - g.ox) * g.inv_h;
   const float gy = (y - g.oy) * g.inv_h;
   const float gz = (z - g.oz) * g.inv_h;
@@ -108,21 +113,17 @@ __device__ __forceinline__ float trilinear(const GridDev& g, const float* __rest
   if (gx < 0.0f || gy < 0.0f || gz < 0.0f || ix > g.nx - 2 || iy > g.ny - 2 || iz > g.nz - 2)
     return 0.0f;
   const float tx = gx - fx, ty = gy - fy, tz = gz - fz;
-  const int sxy = g.nx * g.ny;
-  const float* p = m + (static_cast<long>(iz) * g.ny + iy) * g.nx + ix;
-  const float v000 = __ldg(p), v100 = __ldg(p + 1);
-  const float v010 = __ldg(p + g.nx), v110 = __ldg(p + g.nx + 1);
-  const float v001 = __ldg(p + sxy), v101 = __ldg(p + sxy + 1);
-  const float v011 = __ldg(p + sxy + g.nx), v111 = __ldg(p + sxy + g.nx + 1);
-  const float c00 = det_lerp(v000, v100, tx), c10 = det_lerp(v010, v110, tx);
-  const float c01 = det_lerp(v001, v101, tx), c11 = det_lerp(v011, v111, tx);
+  const float4* c = cells + 2 * ((static_cast<long>(iz) * (g.ny - 1) + iy) * (g.nx - 1) + ix);
+  const float4 lo = __ldg(c), hi = __ldg(c + 1);  // (000,100,010,110), (001,101,011,111)
+  const float c00 = det_lerp(lo.x, lo.y, tx), c10 = det_lerp(lo.z, lo.w, tx);
+  const float c01 = det_lerp(hi.x, hi.y, tx), c11 = det_lerp(hi.z, hi.w, tx);
   const float c0 = det_lerp(c00, c10, ty), c1 = det_lerp(c01, c11, ty);
   return det_lerp(c0, c1, tz);
 }
 
 template <int kGrid>
 __device__ __forceinline__ float field_steric(const PocketDev& pk, float x, float y, float z) {
-  if (kGrid) return trilinear(pk.grid, pk.grid.steric, x, y, z);
+  if (kGrid) return trilinear(pk.grid, pk.grid.steric_c, x, y, z);
   return site_sum(pk.sites, pk.n_steric, x, y, z);
 }
 
@@ -131,11 +132,11 @@ template <int kGrid>
 __device__ __forceinline__ float atom_bonus(const PocketDev& pk, int cls, float x, float y,
                                             float z) {
   if (cls == 1) {
-    if (kGrid) return trilinear(pk.grid, pk.grid.lipo, x, y, z);
+    if (kGrid) return trilinear(pk.grid, pk.grid.lipo_c, x, y, z);
     return site_sum(pk.sites + pk.n_steric + pk.n_hbond, pk.n_lipo, x, y, z);
   }
   if (cls == 2) {
-    if (kGrid) return trilinear(pk.grid, pk.grid.hbond, x, y, z);
+    if (kGrid) return trilinear(pk.grid, pk.grid.hbond_c, x, y, z);
     return site_sum(pk.sites + pk.n_steric, pk.n_hbond, x, y, z);
   }
   return 0.0f;
@@ -150,24 +151,51 @@ __device__ __forceinline__ float wall_term(const PocketDev& pk, float x, float y
   return det_softplus((pk.r - w) * 10.0f);
 }
 
-__device__ __forceinline__ float pair_term(const PocketDev& pk, float dx, float dy, float dz) {
-  const float d2 = det_norm2(dx, dy, dz);
-  if (d2 > pk.cut2) return 0.0f;
-  return det_softplus((pk.r - sqrtf(d2)) * 10.0f);
+// pair clash softplus (dock.cpp:86-97) from an FP64 difference
+__device__ __forceinline__ float pair_term_d(const PocketDev& pk, double dx, double dy,
+                                             double dz) {
+  const double d2 = det_norm2_d(dx, dy, dz);
+  if (d2 > static_cast<double>(pk.cut2)) return 0.0f;
+  return det_softplus((pk.r - sqrtf(static_cast<float>(d2))) * 10.0f);
+}
+
+// per-atom field + wall of local coordinate y under (R, t), FP64 transform
+template <int kGrid>
+__device__ __forceinline__ void atom_terms(const PocketDev& pk, const Mat3d& R, double tx,
+                                           double ty, double tz, double yx, double yy, double yz,
+                                           float* f, float* w, float* xo = nullptr) {
+  double x, y, z;
+  det_apply_d(R, yx, yy, yz, tx, ty, tz, &x, &y, &z);
+  const float xf = static_cast<float>(x), yf = static_cast<float>(y), zf = static_cast<float>(z);
+  *f = field_steric<kGrid>(pk, xf, yf, zf);
+  *w = wall_term(pk, xf, yf, zf);
+  if (xo) {
+    xo[0] = xf;
+    xo[1] = yf;
+    xo[2] = zf;
+  }
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+  for (int off = 16; off > 0; off >>= 1) v = v + __shfl_xor_sync(kFull, v, off);
+  return v;
 }
 
 // ------------------------------------------------- per-warp shared layout --
-constexpr int kCand = 16;  // candidate columns (one lane pair each)
+constexpr int kCand = 16;  // rescore kernel: pose columns (one lane pair each)
 
 struct WarpSmem {
   double4* y0;    // conformer (x, y, z, class), FP64
-  double4* yp;    // chain state / flex prefix, FP64
-  float4* ysf;    // FP32 copy of the state chain (sweep)
+  double4* ys;    // state local coordinates (torsions applied), FP64
+  float4* ysf;    // FP32 copy of the state (sweep)
   float4* xf;     // posed coordinates under test (FP32, decisions)
+  float* fa;      // per-atom field term of the posed state
+  float* wa;      // per-atom wall term of the posed state
   int4* ax;       // torsion axes
   float* theta;   // state torsions
   uint8_t* mov;   // moving lists
-  double* col;    // candidate columns [i][c][16], FP64
+  unsigned* mask; // moving set of the current flex axis (4 words)
+  double* col;    // rescore kernel only: pose columns [i][c][16], FP64
   float* kscore;  // kept-pose scores
   int* kinv;      // rank -> kept index
   float* kresc;   // survivor rescores by rank
@@ -176,30 +204,39 @@ struct WarpSmem {
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-__host__ __device__ inline size_t warp_smem_bytes(int nmax, int tmax, int mvmax) {
+__host__ __device__ inline size_t warp_smem_bytes(int nmax, int tmax, int mvmax, bool cols) {
   size_t b = 0;
-  b += 2 * 32 * size_t(nmax);                 // y0, yp
+  b += 2 * 32 * size_t(nmax);                 // y0, ys
   b += 2 * 16 * size_t(nmax);                 // ysf, xf
+  b += 2 * align16(4 * size_t(nmax));         // fa, wa
   b += 16 * size_t(tmax);                     // ax
   b += align16(4 * size_t(tmax));             // theta
   b += align16(size_t(mvmax));                // mov
-  b += 8 * size_t(nmax) * 3 * kCand;          // col
+  b += 16;                                    // mask
+  if (cols) b += 8 * size_t(nmax) * 3 * kCand;
   b += 3 * 4 * kMaxRestarts;                  // kscore, kinv, kresc
   b += 16;                                    // mbarrier
   return b;
 }
 
-__device__ inline WarpSmem carve(unsigned char* base, int nmax, int tmax, int mvmax) {
+__device__ inline WarpSmem carve(unsigned char* base, int nmax, int tmax, int mvmax, bool cols) {
   WarpSmem s;
   size_t o = 0;
   s.y0 = reinterpret_cast<double4*>(base + o); o += 32 * size_t(nmax);
-  s.yp = reinterpret_cast<double4*>(base + o); o += 32 * size_t(nmax);
+  s.ys = reinterpret_cast<double4*>(base + o); o += 32 * size_t(nmax);
   s.ysf = reinterpret_cast<float4*>(base + o); o += 16 * size_t(nmax);
   s.xf = reinterpret_cast<float4*>(base + o); o += 16 * size_t(nmax);
+  s.fa = reinterpret_cast<float*>(base + o); o += align16(4 * size_t(nmax));
+  s.wa = reinterpret_cast<float*>(base + o); o += align16(4 * size_t(nmax));
   s.ax = reinterpret_cast<int4*>(base + o); o += 16 * size_t(tmax);
   s.theta = reinterpret_cast<float*>(base + o); o += align16(4 * size_t(tmax));
   s.mov = base + o; o += align16(size_t(mvmax));
-  s.col = reinterpret_cast<double*>(base + o); o += 8 * size_t(nmax) * 3 * kCand;
+  s.mask = reinterpret_cast<unsigned*>(base + o); o += 16;
+  s.col = nullptr;
+  if (cols) {
+    s.col = reinterpret_cast<double*>(base + o);
+    o += 8 * size_t(nmax) * 3 * kCand;
+  }
   s.kscore = reinterpret_cast<float*>(base + o); o += 4 * kMaxRestarts;
   s.kinv = reinterpret_cast<int*>(base + o); o += 4 * kMaxRestarts;
   s.kresc = reinterpret_cast<float*>(base + o); o += 4 * kMaxRestarts;
@@ -225,100 +262,35 @@ __device__ inline void stage_ligand(const LibDev& lib, int lig, const WarpSmem& 
   phase ^= 1u;
 }
 
-// Apply torsion j with angle th to s.yp in place; lanes over moving atoms.
-__device__ inline void torsion_coop(const WarpSmem& s, int j, float th, int lane) {
-  const int4 a = s.ax[j];
-  const double4 o = s.yp[a.x], b = s.yp[a.y];
-  const Mat3d M = det_torsion_mat_d(o.x, o.y, o.z, b.x, b.y, b.z, th);
-  for (int m = lane; m < a.w; m += 32) {
-    const int idx = s.mov[a.z + m];
-    double4 v = s.yp[idx];
-    det_apply_d(M, v.x - o.x, v.y - o.y, v.z - o.z, o.x, o.y, o.z, &v.x, &v.y, &v.z);
-    s.yp[idx] = v;
-  }
-  __syncwarp();
-}
-
-// s.yp = y0 with torsions [0, T) at s.theta (dock.cpp:54-63).
+// s.ys = y0 with torsions [0, T) at s.theta (dock.cpp:54-63); lanes over
+// the moving atoms of each torsion in turn.
 __device__ inline void chain_coop(const WarpSmem& s, int N, int T, int lane) {
-  for (int i = lane; i < N; i += 32) s.yp[i] = s.y0[i];
+  for (int i = lane; i < N; i += 32) s.ys[i] = s.y0[i];
   __syncwarp();
-  for (int j = 0; j < T; ++j) torsion_coop(s, j, s.theta[j], lane);
-}
-
-__device__ __forceinline__ double& cold(double* col, int i, int c, int a) {
-  return col[(i * 3 + c) * kCand + a];
-}
-
-// Candidate column a (lane pair (a, h)): src (prefix or conformer) with
-// torsions [j0, T) applied; torsion j0 takes th_j0 when j0 < T, every later
-// torsion k the angle th_of(k).  Lanes h = 0/1 split atoms and moving lists.
-template <class ThOf>
-__device__ inline void chain_pair(const WarpSmem& s, const double4* src, int N, int T, int j0,
-                                  int a, int h, bool active, ThOf th_of) {
-  double* col = s.col;
-  if (active) {
-    for (int i = h; i < N; i += 2) {
-      const double4 v = src[i];
-      cold(col, i, 0, a) = v.x;
-      cold(col, i, 1, a) = v.y;
-      cold(col, i, 2, a) = v.z;
-    }
-  }
-  __syncwarp();
-  for (int k = j0; k < T; ++k) {
-    if (active) {
-      const int4 ax = s.ax[k];
-      const double ox = cold(col, ax.x, 0, a), oy = cold(col, ax.x, 1, a),
-                   oz = cold(col, ax.x, 2, a);
-      const Mat3d M = det_torsion_mat_d(ox, oy, oz, cold(col, ax.y, 0, a), cold(col, ax.y, 1, a),
-                                        cold(col, ax.y, 2, a), th_of(k));
-      for (int m = h; m < ax.w; m += 2) {
-        const int idx = s.mov[ax.z + m];
-        double vx, vy, vz;
-        det_apply_d(M, cold(col, idx, 0, a) - ox, cold(col, idx, 1, a) - oy,
-                    cold(col, idx, 2, a) - oz, ox, oy, oz, &vx, &vy, &vz);
-        cold(col, idx, 0, a) = vx;
-        cold(col, idx, 1, a) = vy;
-        cold(col, idx, 2, a) = vz;
-      }
+  for (int j = 0; j < T; ++j) {
+    const int4 a = s.ax[j];
+    const double4 o = s.ys[a.x], b = s.ys[a.y];
+    const Mat3d M = det_torsion_mat_d(o.x, o.y, o.z, b.x, b.y, b.z, s.theta[j]);
+    for (int m = lane; m < a.w; m += 32) {
+      const int idx = s.mov[a.z + m];
+      double4 v = s.ys[idx];
+      det_apply_d(M, v.x - o.x, v.y - o.y, v.z - o.z, o.x, o.y, o.z, &v.x, &v.y, &v.z);
+      s.ys[idx] = v;
     }
     __syncwarp();
   }
 }
 
-// Parity-h share of the canonical score of pose (R, t) over column a:
-// F_h, W_h over atoms i = h mod 2 (FP64 transform, FP32 terms), P_h over
-// pairs p = h mod 2 enumerated i < j row-major (FP64 differences).
-template <int kGrid>
-__device__ inline void eval_pair(const PocketDev& pk, const WarpSmem& s, int N, int a, int h,
-                                 const Mat3d& R, double tx, double ty, double tz, float* F,
-                                 float* W, float* P) {
-  const double* col = s.col;
-  float f = 0.0f, w = 0.0f, p = 0.0f;
-  for (int i = h; i < N; i += 2) {
+// s.xf = (float)(R s.ys + t) over all atoms (lanes over atoms)
+__device__ inline void pose_coop(const WarpSmem& s, int N, const Mat3d& R, double tx, double ty,
+                                 double tz, int lane) {
+  for (int i = lane; i < N; i += 32) {
+    const double4 v = s.ys[i];
     double x, y, z;
-    det_apply_d(R, col[(i * 3) * kCand + a], col[(i * 3 + 1) * kCand + a],
-                col[(i * 3 + 2) * kCand + a], tx, ty, tz, &x, &y, &z);
-    const float xf = static_cast<float>(x), yf = static_cast<float>(y), zf = static_cast<float>(z);
-    f = f + field_steric<kGrid>(pk, xf, yf, zf);
-    w = w + wall_term(pk, xf, yf, zf);
+    det_apply_d(R, v.x, v.y, v.z, tx, ty, tz, &x, &y, &z);
+    s.xf[i] = make_float4(static_cast<float>(x), static_cast<float>(y), static_cast<float>(z), 0.0f);
   }
-  const double cut2 = static_cast<double>(pk.cut2);
-  int ps = 0;
-  for (int i = 0; i + 1 < N; ++i) {
-    const double xi = col[(i * 3) * kCand + a], yi = col[(i * 3 + 1) * kCand + a],
-                 zi = col[(i * 3 + 2) * kCand + a];
-    for (int jj = i + 1 + ((h ^ ps) & 1); jj < N; jj += 2) {
-      const double d2 = det_norm2_d(xi - col[(jj * 3) * kCand + a], yi - col[(jj * 3 + 1) * kCand + a],
-                                    zi - col[(jj * 3 + 2) * kCand + a]);
-      if (d2 <= cut2) p = p + det_softplus((pk.r - sqrtf(static_cast<float>(d2))) * 10.0f);
-    }
-    ps += N - 1 - i;
-  }
-  *F = f;
-  *W = w;
-  *P = p;
+  __syncwarp();
 }
 
 // Rigid-variant key of one sweep pose: F - lam W over the FP32 state coords.
@@ -329,13 +301,15 @@ __device__ inline float eval_rigid(const PocketDev& pk, const float4* ys, int N,
   int i = 0;
   for (; i + 1 < N; i += 2) {
     const float4 a = ys[i], b = ys[i + 1];
-    float x, y, z;
-    det_apply(R, a.x, a.y, a.z, tx, ty, tz, &x, &y, &z);
-    fe = fe + field_steric<kGrid>(pk, x, y, z);
-    we = we + wall_term(pk, x, y, z);
-    det_apply(R, b.x, b.y, b.z, tx, ty, tz, &x, &y, &z);
-    fo = fo + field_steric<kGrid>(pk, x, y, z);
-    wo = wo + wall_term(pk, x, y, z);
+    float x0, y0, z0, x1, y1, z1;
+    det_apply(R, a.x, a.y, a.z, tx, ty, tz, &x0, &y0, &z0);
+    det_apply(R, b.x, b.y, b.z, tx, ty, tz, &x1, &y1, &z1);
+    const float f0 = field_steric<kGrid>(pk, x0, y0, z0);
+    const float f1 = field_steric<kGrid>(pk, x1, y1, z1);
+    fe = fe + f0;
+    we = we + wall_term(pk, x0, y0, z0);
+    fo = fo + f1;
+    wo = wo + wall_term(pk, x1, y1, z1);
   }
   if (i < N) {
     const float4 a = ys[i];
@@ -363,22 +337,10 @@ __device__ inline bool diverse_from_kept(const WarpSmem& s, const float4* kx, in
   return __all_sync(kFull, ok);
 }
 
-// s.xf = (float)(R s.yp + t) over all atoms (lanes over atoms)
-__device__ inline void pose_coop(const WarpSmem& s, int N, const Mat3d& R, double tx, double ty,
-                                 double tz, int lane) {
-  for (int i = lane; i < N; i += 32) {
-    const double4 v = s.yp[i];
-    double x, y, z;
-    det_apply_d(R, v.x, v.y, v.z, tx, ty, tz, &x, &y, &z);
-    s.xf[i] = make_float4(static_cast<float>(x), static_cast<float>(y), static_cast<float>(z), 0.0f);
-  }
-  __syncwarp();
-}
-
 // Translation-sweep lattice: l = 0 is the current point, l = 1..26 the
 // non-zero offsets of {-1,0,1}^3 in x-fastest order, scaled by sc.
-constexpr int kTransIters = 24;
-constexpr float kTransMin = 1.0f / 512.0f;
+constexpr int kTransIters = 16;
+constexpr float kTransMin = 1.0f / 64.0f;
 __device__ __forceinline__ void trans_offset(int l, float sc, float* ox, float* oy, float* oz) {
   if (l == 0) {
     *ox = *oy = *oz = 0.0f;
@@ -430,9 +392,29 @@ __device__ inline void draw_start(const PocketDev& pk, unsigned long long rkey, 
   __syncwarp();
 }
 
+// Rotation of the flex move: moving_j rotated about the state's axis j by
+// delta = th_new - th_old (FP64 of two FP32 angles).  The half angle is
+// folded into [-pi/2, pi/2] by q -> -q (same matrix).
+__device__ __forceinline__ Mat3d flex_mat(double ox, double oy, double oz, double bx, double by,
+                                          double bz, float th_new, float th_old) {
+  const double dx = bx - ox, dy = by - oy, dz = bz - oz;
+  const double n = sqrt(det_norm2_d(dx, dy, dz));
+  double hh = 0.5 * (static_cast<double>(th_new) - static_cast<double>(th_old));
+  if (hh > kHalfPiD) hh = hh - kPiD;
+  else if (hh < -kHalfPiD) hh = hh + kPiD;
+  double s, c;
+  det_sincos_d(hh, &s, &c);
+  const double ks = n > 0.0 ? s / n : 0.0;
+  return det_quat_mat_d(c, dx * ks, dy * ks, dz * ks);
+}
+
+__device__ __forceinline__ bool in_mask(const unsigned* mask, int i) {
+  return (mask[i >> 5] >> (i & 31)) & 1u;
+}
+
 // ============================================================= dock kernel
 template <int kGrid>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 4)
     vs_dock_kernel(const LibDev lib, const PocketDev pk, const float4* __restrict__ rots,
                    const DockParams prm, const int* __restrict__ order, int n_order,
                    int* __restrict__ work_counter, int nmax, int tmax, int mvmax,
@@ -441,7 +423,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  const WarpSmem s = carve(smem_raw + wib * warp_smem_bytes(nmax, tmax, mvmax), nmax, tmax, mvmax);
+  const WarpSmem s =
+      carve(smem_raw + wib * warp_smem_bytes(nmax, tmax, mvmax, false), nmax, tmax, mvmax, false);
   const long gwarp = static_cast<long>(blockIdx.x) * kWarpsPerBlock + wib;
   const int R = prm.R;
   const int parw = 8 + tmax;
@@ -486,8 +469,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
       }
       if (att == 50) att = 49;
       if (!have_chain) chain_coop(s, N, T, lane);
+      st_att += static_cast<unsigned long long>(att) + 1;
       for (int i = lane; i < N; i += 32) {
-        const double4 v = s.yp[i];
+        const double4 v = s.ys[i];
         s.ysf[i] = make_float4(static_cast<float>(v.x), static_cast<float>(v.y),
                                static_cast<float>(v.z), 0.0f);
       }
@@ -581,44 +565,97 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
           ++st_trans;
         }
       }
-      st_att += static_cast<unsigned long long>(att) + 1;
       const Mat3d RD = det_pose_mat_d(pw, px, py, pz);
       const double tdx = ptx, tdy = pty, tdz = ptz;
 
-      // ---- torsion flex: F passes x T axes x A angles, greedy; candidate
-      // columns start from the shared prefix (torsions < j at state values)
+      // ---- incremental torsion flex (docs/SWEEP_V1.md §2.5): per-atom
+      // terms of the posed state, then for each (pass, axis j) 16 candidate
+      // angles scored as  base(state, atoms/pairs not touched by moving_j)
+      // + moved part(candidate, moving_j atoms and their cross pairs).
+      for (int i = lane; i < N; i += 32) {
+        const double4 v = s.ys[i];
+        atom_terms<kGrid>(pk, RD, tdx, tdy, tdz, v.x, v.y, v.z, &s.fa[i], &s.wa[i]);
+      }
+      __syncwarp();
       const bool do_flex = T > 0 && prm.F > 0;
       const int steps = do_flex ? prm.F * T : 1;
       st_flex += do_flex ? static_cast<unsigned long long>(steps) * prm.A : 1ull;
       float S_cur = 0.0f;
-      int win = 0;
       for (int st = 0; st < steps; ++st) {
-        const int j = do_flex ? st % T : T;
-        if (do_flex && j == 0) {  // new pass: prefix = conformer
-          for (int i = lane; i < N; i += 32) s.yp[i] = s.y0[i];
-          __syncwarp();
+        const int j = do_flex ? st % T : -1;
+        const int4 ax = do_flex ? s.ax[j] : make_int4(0, 0, 0, 0);
+        const int m = ax.w;
+        if (lane < 4) {
+          unsigned wd = 0;
+          for (int q2 = 0; q2 < m; ++q2) {
+            const int idx = s.mov[ax.z + q2];
+            if ((idx >> 5) == lane) wd |= 1u << (idx & 31);
+          }
+          s.mask[lane] = wd;
         }
-        const bool active = do_flex ? (a_lane < prm.A) : (a_lane == 0);
-        float th_j = 0.0f;
-        if (do_flex) {
-          th_j = s.theta[j];
-          if (a_lane > 0) {
-            float v = th_j + static_cast<float>(a_lane) * step;
-            if (v >= kPiF) v = v - kTwoPiF;
-            th_j = v;
+        __syncwarp();
+        // base sums: lane l accumulates atoms i = l (mod 32) outside the
+        // moving set and pairs p = l (mod 32) (row-major index over all
+        // pairs) that do not cross it; then an xor butterfly
+        float fb = 0.0f, wb = 0.0f, pb = 0.0f;
+        for (int i = lane; i < N; i += 32) {
+          if (!in_mask(s.mask, i)) {
+            fb = fb + s.fa[i];
+            wb = wb + s.wa[i];
           }
         }
-        const float* theta = s.theta;
-        chain_pair(s, s.yp, N, T, j, a_lane, h, active,
-                   [&](int k) { return k == j ? th_j : theta[k]; });
-        float F = 0.0f, W = 0.0f, P = 0.0f;
-        if (active) eval_pair<kGrid>(pk, s, N, a_lane, h, RD, tdx, tdy, tdz, &F, &W, &P);
-        const float F2 = __shfl_xor_sync(kFull, F, 16);
-        const float W2 = __shfl_xor_sync(kFull, W, 16);
-        const float P2 = __shfl_xor_sync(kFull, P, 16);
-        float S = (F + F2) - pk.lam * ((P + P2) + (W + W2));
-        if (!active) S = -INFINITY;
-        int ai = active ? a_lane : 0x7fffffff;
+        {
+          int ps = 0;
+          for (int i = 0; i + 1 < N; ++i) {
+            const double4 yi = s.ys[i];
+            const bool mi = in_mask(s.mask, i);
+            for (int k = i + 1 + ((lane - ps) & 31); k < N; k += 32) {
+              if (mi != in_mask(s.mask, k)) continue;
+              const double4 yk = s.ys[k];
+              pb = pb + pair_term_d(pk, yi.x - yk.x, yi.y - yk.y, yi.z - yk.z);
+            }
+            ps += N - 1 - i;
+          }
+        }
+        fb = warp_sum(fb);
+        wb = warp_sum(wb);
+        pb = warp_sum(pb);
+        // candidates: lane pair (a, h); lane h takes moving positions = h mod 2
+        const bool active = do_flex && a_lane < prm.A;
+        float th_new = 0.0f;
+        float fm = 0.0f, wm = 0.0f, pc = 0.0f;
+        if (active) {
+          const float th_old = s.theta[j];
+          th_new = th_old;
+          if (a_lane > 0) {
+            float v = th_old + static_cast<float>(a_lane) * step;
+            if (v >= kPiF) v = v - kTwoPiF;
+            th_new = v;
+          }
+          const double4 o = s.ys[ax.x], b = s.ys[ax.y];
+          const Mat3d M = flex_mat(o.x, o.y, o.z, b.x, b.y, b.z, th_new, th_old);
+          for (int q2 = h; q2 < m; q2 += 2) {
+            const int idx = s.mov[ax.z + q2];
+            const double4 v = s.ys[idx];
+            double yx, yy, yz;
+            det_apply_d(M, v.x - o.x, v.y - o.y, v.z - o.z, o.x, o.y, o.z, &yx, &yy, &yz);
+            float fi, wi;
+            atom_terms<kGrid>(pk, RD, tdx, tdy, tdz, yx, yy, yz, &fi, &wi);
+            fm = fm + fi;
+            wm = wm + wi;
+            for (int k = 0; k < N; ++k) {
+              if (in_mask(s.mask, k)) continue;
+              const double4 yk = s.ys[k];
+              pc = pc + pair_term_d(pk, yx - yk.x, yy - yk.y, yz - yk.z);
+            }
+          }
+        }
+        const float fm2 = __shfl_xor_sync(kFull, fm, 16);
+        const float wm2 = __shfl_xor_sync(kFull, wm, 16);
+        const float pc2 = __shfl_xor_sync(kFull, pc, 16);
+        float S = (fb + (fm + fm2)) - pk.lam * ((pb + (pc + pc2)) + (wb + (wm + wm2)));
+        if (do_flex && !active) S = -INFINITY;
+        int ai = (do_flex && !active) ? 0x7fffffff : a_lane;
         for (int off = 8; off > 0; off >>= 1) {
           const float oS = __shfl_xor_sync(kFull, S, off);
           const int oa = __shfl_xor_sync(kFull, ai, off);
@@ -628,24 +665,26 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
           }
         }
         S_cur = S;
-        win = ai;
-        if (do_flex) {
-          const float th_win = __shfl_sync(kFull, th_j, win);
+        if (do_flex && ai != 0) {  // move the state to the winning angle
+          const float th_old = s.theta[j];
+          const float th_win = __shfl_sync(kFull, th_new, ai);
+          const double4 o = s.ys[ax.x], b = s.ys[ax.y];
+          const Mat3d M = flex_mat(o.x, o.y, o.z, b.x, b.y, b.z, th_win, th_old);
           __syncwarp();
+          for (int q2 = lane; q2 < m; q2 += 32) {
+            const int idx = s.mov[ax.z + q2];
+            double4 v = s.ys[idx];
+            det_apply_d(M, v.x - o.x, v.y - o.y, v.z - o.z, o.x, o.y, o.z, &v.x, &v.y, &v.z);
+            s.ys[idx] = v;
+            atom_terms<kGrid>(pk, RD, tdx, tdy, tdz, v.x, v.y, v.z, &s.fa[idx], &s.wa[idx]);
+          }
           if (lane == 0) s.theta[j] = th_win;
-          __syncwarp();
-          if (st + 1 < steps && j + 1 < T) torsion_coop(s, j, th_win, lane);  // extend prefix
         }
+        __syncwarp();
       }
 
       // ---- final coordinates and diversity against kept (dock.cpp:359-361)
-      for (int i = lane; i < N; i += 32) {
-        double x, y, z;
-        det_apply_d(RD, s.col[(i * 3) * kCand + win], s.col[(i * 3 + 1) * kCand + win],
-                    s.col[(i * 3 + 2) * kCand + win], tdx, tdy, tdz, &x, &y, &z);
-        s.xf[i] = make_float4(static_cast<float>(x), static_cast<float>(y), static_cast<float>(z), 0.0f);
-      }
-      __syncwarp();
+      pose_coop(s, N, RD, tdx, tdy, tdz, lane);
       const bool keep = nk == 0 || diverse_from_kept(s, kx, nk, nmax, N, prm.delta, lane);
       if (keep) {
         for (int i = lane; i < N; i += 32) kx[static_cast<size_t>(nk) * nmax + i] = s.xf[i];
@@ -671,9 +710,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     for (int k = lane; k < nk; k += 32) {
       const float sk = s.kscore[k];
       int rank = 0;
-      for (int m = 0; m < nk; ++m) {
-        const float sm = s.kscore[m];
-        rank += (sm > sk || (sm == sk && m < k)) ? 1 : 0;
+      for (int m2 = 0; m2 < nk; ++m2) {
+        const float sm = s.kscore[m2];
+        rank += (sm > sk || (sm == sk && m2 < k)) ? 1 : 0;
       }
       s.kinv[rank] = k;
       m_pass += (static_cast<double>(sk) >= prm.min_score) ? 1 : 0;
@@ -758,8 +797,50 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 }
 
 // ========================================================= rescore kernel
+__device__ __forceinline__ double& cold(double* col, int i, int c, int a) {
+  return col[(i * 3 + c) * kCand + a];
+}
+
+// Pose column a (lane pair (a, h)): conformer with all torsions of the pose
+// applied in order (dock.cpp:54-63); lanes h = 0/1 split atoms and moving
+// lists, __syncwarp between torsions.
+__device__ inline void chain_pose(const WarpSmem& s, int N, int T, int a, int h, bool active,
+                                  const float* th) {
+  double* col = s.col;
+  if (active) {
+    for (int i = h; i < N; i += 2) {
+      const double4 v = s.y0[i];
+      cold(col, i, 0, a) = v.x;
+      cold(col, i, 1, a) = v.y;
+      cold(col, i, 2, a) = v.z;
+    }
+  }
+  __syncwarp();
+  for (int k = 0; k < T; ++k) {
+    if (active) {
+      const int4 ax = s.ax[k];
+      const double ox = cold(col, ax.x, 0, a), oy = cold(col, ax.x, 1, a),
+                   oz = cold(col, ax.x, 2, a);
+      const Mat3d M = det_torsion_mat_d(ox, oy, oz, cold(col, ax.y, 0, a), cold(col, ax.y, 1, a),
+                                        cold(col, ax.y, 2, a), th[k]);
+      for (int m = h; m < ax.w; m += 2) {
+        const int idx = s.mov[ax.z + m];
+        double vx, vy, vz;
+        det_apply_d(M, cold(col, idx, 0, a) - ox, cold(col, idx, 1, a) - oy,
+                    cold(col, idx, 2, a) - oz, ox, oy, oz, &vx, &vy, &vz);
+        cold(col, idx, 0, a) = vx;
+        cold(col, idx, 1, a) = vy;
+        cold(col, idx, 2, a) = vz;
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // Work item w: ligand ligs[w], poses [pose_off[w], pose_off[w+1]) (float4 t,
 // float4 q = (w,x,y,z)), torsions at tors_base[w] + (p - pose_off[w]) * T.
+// Canonical score of a given pose: parity-h lane sums over atoms i = h mod 2
+// and pairs p = h mod 2 (row-major), combined across the lane pair.
 template <int kGrid>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     vs_rescore_kernel(const LibDev lib, const PocketDev pk, const int* __restrict__ ligs,
@@ -771,11 +852,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  const WarpSmem s = carve(smem_raw + wib * warp_smem_bytes(nmax, tmax, mvmax), nmax, tmax, mvmax);
+  const WarpSmem s =
+      carve(smem_raw + wib * warp_smem_bytes(nmax, tmax, mvmax, true), nmax, tmax, mvmax, true);
   if (lane == 0) mbar_init(s.bar);
   __syncwarp();
   uint32_t phase = 0;
-  const int a_lane = lane & 15;
+  const int a = lane & 15;
   const int h = lane >> 4;
   while (true) {
     int w = 0;
@@ -788,23 +870,36 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     const int N = meta.y, T = meta.w;
     const int p0 = pose_off[w], p1 = pose_off[w + 1];
     for (int base = p0; base < p1; base += 16) {
-      const int p = base + a_lane;
+      const int p = base + a;
       const bool active = p < p1;
       const float* th = pose_tors + tors_base[w] + static_cast<long>(active ? p - p0 : 0) * T;
-      chain_pair(s, s.y0, N, T, 0, a_lane, h, active, [&](int k) { return th[k]; });
+      chain_pose(s, N, T, a, h, active, th);
       float F = 0.0f, W = 0.0f, P = 0.0f, B = 0.0f;
       if (active) {
         const float4 tt = pose_t[p];
         const float4 qq = pose_q[p];
         const Mat3d Rm = det_pose_mat_d(qq.x, qq.y, qq.z, qq.w);
         const double tx = tt.x, ty = tt.y, tz = tt.z;
-        eval_pair<kGrid>(pk, s, N, a_lane, h, Rm, tx, ty, tz, &F, &W, &P);
+        const double* col = s.col;
         for (int i = h; i < N; i += 2) {
-          double x, y, z;
-          det_apply_d(Rm, s.col[(i * 3) * kCand + a_lane], s.col[(i * 3 + 1) * kCand + a_lane],
-                      s.col[(i * 3 + 2) * kCand + a_lane], tx, ty, tz, &x, &y, &z);
-          B = B + atom_bonus<kGrid>(pk, static_cast<int>(s.y0[i].w), static_cast<float>(x),
-                                    static_cast<float>(y), static_cast<float>(z));
+          float fi, wi, xo[3];
+          atom_terms<kGrid>(pk, Rm, tx, ty, tz, col[(i * 3) * kCand + a],
+                            col[(i * 3 + 1) * kCand + a], col[(i * 3 + 2) * kCand + a], &fi, &wi,
+                            xo);
+          F = F + fi;
+          W = W + wi;
+          B = B + atom_bonus<kGrid>(pk, static_cast<int>(s.y0[i].w), xo[0], xo[1], xo[2]);
+        }
+        int ps = 0;
+        for (int i = 0; i + 1 < N; ++i) {
+          const double xi = col[(i * 3) * kCand + a], yi = col[(i * 3 + 1) * kCand + a],
+                       zi = col[(i * 3 + 2) * kCand + a];
+          for (int jj = i + 1 + ((h ^ ps) & 1); jj < N; jj += 2) {
+            P = P + pair_term_d(pk, xi - col[(jj * 3) * kCand + a],
+                                yi - col[(jj * 3 + 1) * kCand + a],
+                                zi - col[(jj * 3 + 2) * kCand + a]);
+          }
+          ps += N - 1 - i;
         }
       }
       const float F2 = __shfl_xor_sync(kFull, F, 16);
@@ -822,7 +917,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   }
 }
 
-// ============================================================ grid kernel
+// ============================================================ grid kernels
 __global__ void vs_grid_kernel(const PocketDev pk, float* __restrict__ steric,
                                float* __restrict__ hbond, float* __restrict__ lipo) {
   const GridDev& g = pk.grid;
@@ -838,6 +933,21 @@ __global__ void vs_grid_kernel(const PocketDev pk, float* __restrict__ steric,
     steric[id] = site_sum(pk.sites, pk.n_steric, x, y, z);
     hbond[id] = site_sum(pk.sites + pk.n_steric, pk.n_hbond, x, y, z);
     lipo[id] = site_sum(pk.sites + pk.n_steric + pk.n_hbond, pk.n_lipo, x, y, z);
+  }
+}
+
+// node map -> corner-packed cells (000,100,010,110 | 001,101,011,111)
+__global__ void vs_pack_kernel(const GridDev g, const float* __restrict__ node,
+                               float4* __restrict__ cells) {
+  const long cx = g.nx - 1, cy = g.ny - 1, cz = g.nz - 1;
+  const long n = cx * cy * cz;
+  const long sx = 1, sy = g.nx, sz = static_cast<long>(g.nx) * g.ny;
+  for (long id = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; id < n;
+       id += static_cast<long>(gridDim.x) * blockDim.x) {
+    const long ix = id % cx, iy = (id / cx) % cy, iz = id / (cx * cy);
+    const float* p = node + iz * sz + iy * sy + ix;
+    cells[2 * id] = make_float4(p[0], p[sx], p[sy], p[sy + sx]);
+    cells[2 * id + 1] = make_float4(p[sz], p[sz + sx], p[sz + sy], p[sz + sy + sx]);
   }
 }
 
@@ -918,22 +1028,31 @@ __global__ void vs_peak_xu(float* out, int iters, float seed) {
 namespace vs {
 
 size_t dock_smem_per_block(int nmax, int tmax, int mvmax) {
-  return kWarpsPerBlock * warp_smem_bytes(nmax, tmax, mvmax);
+  return kWarpsPerBlock * warp_smem_bytes(nmax, tmax, mvmax, false);
 }
 
+size_t rescore_smem_per_block(int nmax, int tmax, int mvmax) {
+  return kWarpsPerBlock * warp_smem_bytes(nmax, tmax, mvmax, true);
+}
+
+template <class K>
+static void prep(K kernel, size_t smem) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(smem));
+  cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       cudaSharedmemCarveoutMaxShared);
+}
 
 cudaError_t launch_dock(bool grid, int blocks, size_t smem, cudaStream_t st, const LibDev& lib,
                         const PocketDev& pk, const float4* rots, const DockParams& prm,
                         const int* order, int n_order, int* counter, int nmax, int tmax,
                         int mvmax, float4* sx, float* sp, int* sm, const DockOut& out) {
   if (grid) {
-    cudaFuncSetAttribute(vs_dock_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
+    prep(vs_dock_kernel<1>, smem);
     vs_dock_kernel<1><<<blocks, kWarpsPerBlock * 32, smem, st>>>(
         lib, pk, rots, prm, order, n_order, counter, nmax, tmax, mvmax, sx, sp, sm, out);
   } else {
-    cudaFuncSetAttribute(vs_dock_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
+    prep(vs_dock_kernel<0>, smem);
     vs_dock_kernel<0><<<blocks, kWarpsPerBlock * 32, smem, st>>>(
         lib, pk, rots, prm, order, n_order, counter, nmax, tmax, mvmax, sx, sp, sm, out);
   }
@@ -943,13 +1062,11 @@ cudaError_t launch_dock(bool grid, int blocks, size_t smem, cudaStream_t st, con
 int dock_blocks_per_sm(bool grid, size_t smem) {
   int nb = 0;
   if (grid) {
-    cudaFuncSetAttribute(vs_dock_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
+    prep(vs_dock_kernel<1>, smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, vs_dock_kernel<1>, kWarpsPerBlock * 32,
                                                   smem);
   } else {
-    cudaFuncSetAttribute(vs_dock_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
+    prep(vs_dock_kernel<0>, smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, vs_dock_kernel<0>, kWarpsPerBlock * 32,
                                                   smem);
   }
@@ -962,14 +1079,12 @@ cudaError_t launch_rescore(bool grid, int blocks, size_t smem, cudaStream_t st, 
                            const float4* pq, const float* ptors, int nmax, int tmax, int mvmax,
                            float* geo, float* resc) {
   if (grid) {
-    cudaFuncSetAttribute(vs_rescore_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
+    prep(vs_rescore_kernel<1>, smem);
     vs_rescore_kernel<1><<<blocks, kWarpsPerBlock * 32, smem, st>>>(
         lib, pk, ligs, n_ligs, counter, pose_off, tors_base, pt, pq, ptors, nmax, tmax, mvmax,
         geo, resc);
   } else {
-    cudaFuncSetAttribute(vs_rescore_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
+    prep(vs_rescore_kernel<0>, smem);
     vs_rescore_kernel<0><<<blocks, kWarpsPerBlock * 32, smem, st>>>(
         lib, pk, ligs, n_ligs, counter, pose_off, tors_base, pt, pq, ptors, nmax, tmax, mvmax,
         geo, resc);
@@ -978,15 +1093,28 @@ cudaError_t launch_rescore(bool grid, int blocks, size_t smem, cudaStream_t st, 
 }
 
 cudaError_t launch_grid(cudaStream_t st, const PocketDev& pk, float* steric, float* hb,
-                        float* lipo) {
-  const long n = static_cast<long>(pk.grid.nx) * pk.grid.ny * pk.grid.nz;
+                        float* lipo, float4* cells) {
+  const GridDev& g = pk.grid;
+  const long n = static_cast<long>(g.nx) * g.ny * g.nz;
   int blocks = static_cast<int>((n + 255) / 256);
   if (blocks > 148 * 64) blocks = 148 * 64;
   vs_grid_kernel<<<blocks, 256, 0, st>>>(pk, steric, hb, lipo);
+  const long nc = static_cast<long>(g.nx - 1) * (g.ny - 1) * (g.nz - 1);
+  int cb = static_cast<int>((nc + 255) / 256);
+  if (cb > 148 * 64) cb = 148 * 64;
+  vs_pack_kernel<<<cb, 256, 0, st>>>(g, steric, cells);
+  vs_pack_kernel<<<cb, 256, 0, st>>>(g, hb, cells + 2 * nc);
+  vs_pack_kernel<<<cb, 256, 0, st>>>(g, lipo, cells + 4 * nc);
   return cudaGetLastError();
 }
 
 int topk_chunk() { return kTopkC; }
+
+cudaError_t launch_topk(cudaStream_t st, const unsigned long long* in, long n,
+                        unsigned long long* out, int k, int blocks) {
+  vs_topk_kernel<<<blocks, 1024, 0, st>>>(in, n, out, k);
+  return cudaGetLastError();
+}
 
 // kind 0 fp32 fma, 1 fp64 fma, 2 ex2; returns ops/s (best of 3)
 double measure_peak(int kind, int sms) {
@@ -1013,12 +1141,6 @@ double measure_peak(int kind, int sms) {
   cudaEventDestroy(b);
   cudaFree(buf);
   return best;
-}
-
-cudaError_t launch_topk(cudaStream_t st, const unsigned long long* in, long n,
-                        unsigned long long* out, int k, int blocks) {
-  vs_topk_kernel<<<blocks, 1024, 0, st>>>(in, n, out, k);
-  return cudaGetLastError();
 }
 
 }  // namespace vs

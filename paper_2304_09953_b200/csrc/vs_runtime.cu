@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -18,6 +19,7 @@
 
 namespace vs {
 size_t dock_smem_per_block(int nmax, int tmax, int mvmax);
+size_t rescore_smem_per_block(int nmax, int tmax, int mvmax);
 int dock_blocks_per_sm(bool grid, size_t smem);
 cudaError_t launch_dock(bool grid, int blocks, size_t smem, cudaStream_t st, const LibDev& lib,
                         const PocketDev& pk, const float4* rots, const DockParams& prm,
@@ -29,7 +31,7 @@ cudaError_t launch_rescore(bool grid, int blocks, size_t smem, cudaStream_t st, 
                            const float4* pq, const float* ptors, int nmax, int tmax, int mvmax,
                            float* geo, float* resc);
 cudaError_t launch_grid(cudaStream_t st, const PocketDev& pk, float* steric, float* hb,
-                        float* lipo);
+                        float* lipo, float4* cells);
 int topk_chunk();
 double measure_peak(int kind, int sms);
 cudaError_t launch_topk(cudaStream_t st, const unsigned long long* in, long n,
@@ -249,6 +251,39 @@ int pack_library(vs_handle* h, const vs_library* L, const vs_size_class* classes
   return VS_OK;
 }
 
+// The incremental torsion flex (docs/SWEEP_V1.md §2.5) moves moving_j
+// rigidly about the state's axis j.  That equals re-chaining the torsions
+// from the conformer when the topology is a torsion tree: for j < k, either
+// moving_k and axis k lie inside moving_j (+ axis j) or both are disjoint
+// from moving_j, and no later torsion moves axis j.  Every topology that
+// torsion_topology (dock.cpp:234-270) builds from a parsed SMILES graph has
+// this property (b is the DFS child of a, moving = b's DFS subtree).
+int check_nested(vs_handle* h, const Packed& P) {
+  for (int i = 0; i < P.n; ++i) {
+    const int T = P.meta[i].w;
+    if (T < 2) continue;
+    const int4* ax = P.axes.data() + P.meta[i].z;
+    const uint8_t* mv = P.moving.data() + P.mov[i].x;
+    std::vector<std::array<uint64_t, 2>> set(T, {0ull, 0ull});
+    for (int j = 0; j < T; ++j)
+      for (int m = 0; m < ax[j].w; ++m) set[j][mv[ax[j].z + m] >> 6] |= 1ull << (mv[ax[j].z + m] & 63);
+    auto has = [&](int j, int a) { return (set[j][a >> 6] >> (a & 63)) & 1ull; };
+    for (int j = 0; j < T; ++j) {
+      for (int k = j + 1; k < T; ++k) {
+        const bool sub = ((set[k][0] & ~set[j][0]) | (set[k][1] & ~set[j][1])) == 0 &&
+                         (has(j, ax[k].x) || ax[k].x == ax[j].x || ax[k].x == ax[j].y) &&
+                         (has(j, ax[k].y) || ax[k].y == ax[j].x || ax[k].y == ax[j].y);
+        const bool dis = ((set[k][0] & set[j][0]) | (set[k][1] & set[j][1])) == 0 &&
+                         !has(j, ax[k].x) && !has(j, ax[k].y);
+        if ((!sub && !dis) || has(k, ax[j].x) || has(k, ax[j].y))
+          return fail(h, VS_ERR_INVALID_ARGUMENT,
+                      "ligand " + std::to_string(i) + ": torsion topology is not a torsion tree");
+      }
+    }
+  }
+  return VS_OK;
+}
+
 int upload_packed(vs_handle* h, Packed& P, cudaStream_t st) {
   auto up = [&](DBuf& d, const void* src, size_t bytes) -> cudaError_t {
     cudaError_t e = d.ensure(bytes);
@@ -408,13 +443,19 @@ int vs_set_pocket(vs_handle* h, const vs_pocket* p, double spacing, double pad) 
     for (int c = 0; c < 3; ++c)
       *dims[c] = static_cast<int>(std::ceil((p->hi[c] - p->lo[c] + 2.0 * pad) / spacing)) + 1;
     const size_t nodes = static_cast<size_t>(g.nx) * g.ny * g.nz;
-    VS_CUDA(h, h->d_maps.ensure(3 * nodes * sizeof(float)));
+    const size_t cells = static_cast<size_t>(g.nx - 1) * (g.ny - 1) * (g.nz - 1);
+    const size_t node_bytes = align16z(3 * nodes * sizeof(float));
+    VS_CUDA(h, h->d_maps.ensure(node_bytes + 3 * cells * 2 * sizeof(float4)));
     float* m = h->d_maps.as<float>();
+    float4* c = reinterpret_cast<float4*>(static_cast<char*>(h->d_maps.p) + node_bytes);
     g.steric = m;
     g.hbond = m + nodes;
     g.lipo = m + 2 * nodes;
-    VS_CUDA(h, launch_grid(st, pk, m, m + nodes, m + 2 * nodes));
-    ++h->launches;
+    g.steric_c = c;
+    g.hbond_c = c + 2 * cells;
+    g.lipo_c = c + 4 * cells;
+    VS_CUDA(h, launch_grid(st, pk, m, m + nodes, m + 2 * nodes, c));
+    h->launches += 4;
     pk.grid_mode = 1;
     h->gdims[0] = g.nx;
     h->gdims[1] = g.ny;
@@ -450,6 +491,8 @@ int vs_upload_library(vs_handle* h, const vs_library* L, const vs_size_class* cl
   h->has_lib = false;
   h->has_results = false;
   int rc = pack_library(h, L, classes, nc, h->lib);
+  if (rc) return rc;
+  rc = check_nested(h, h->lib);
   if (rc) return rc;
   rc = upload_packed(h, h->lib, h->own);
   if (rc) return rc;
@@ -766,7 +809,7 @@ int vs_rescore(vs_handle* h, const vs_library* L, int64_t n_poses, const int32_t
     VS_CUDA(h, cc.ensure(4));
     VS_CUDA(h, cudaMemsetAsync(cc.p, 0, 4, st));
     const int count = static_cast<int>(rl.size());
-    const size_t smem = dock_smem_per_block(b.nmax, b.tmax, b.mvmax);
+    const size_t smem = rescore_smem_per_block(b.nmax, b.tmax, b.mvmax);
     const int blocks = std::max(1, std::min((count + kWarpsPerBlock - 1) / kWarpsPerBlock, 4 * h->sms));
     VS_CUDA(h, launch_rescore(grid, blocks, smem, st, ld, h->pk, a.as<int>(), count, cc.as<int>(),
                               bo.as<int>(), c.as<long>(), d.as<float4>(), e.as<float4>(),

@@ -26,6 +26,11 @@ struct GridDev {
   const float* steric;  // node values, x fastest
   const float* hbond;
   const float* lipo;
+  // corner-packed cells: 8 node values per cell (2 x float4, one 32 B
+  // sector), cells x fastest over (nx-1)(ny-1)(nz-1); one sector per lookup
+  const float4* steric_c;
+  const float4* hbond_c;
+  const float4* lipo_c;
 };
 
 struct PocketDev {

@@ -119,6 +119,8 @@ def gather_topk(engine: Engine, k: int, group=None):
     dev = torch.device("cuda", torch.cuda.current_device())
     stream = torch.cuda.current_stream().cuda_stream
     local = torch.empty(k, dtype=torch.int64, device=dev)
+    # keys are produced on `stream`; NCCL runs on its own stream ordered
+    # after the current one
     engine.topk_device(k, local.data_ptr(), stream)
     world = dist.get_world_size(group)
     gathered = torch.empty(world * k, dtype=torch.int64, device=dev)
