@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libvscreen_gpu.so")
+LIB_PATH = os.environ.get("VSCREEN_GPU_LIB") or os.path.join(_HERE, "libvscreen_gpu.so")
 
 # status codes (capi.h vs_status)
 VS_OK = 0

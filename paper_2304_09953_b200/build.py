@@ -15,7 +15,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libvscreen_gpu.so")
-SOURCES = ["vs_kernels.cu", "vs_runtime.cu", "vs_host.cpp", "vs_ingest.cpp"]
+SOURCES = ["vs_kernels.cu", "vs_dock.cu", "vs_runtime.cu", "vs_host.cpp", "vs_ingest.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "--fmad=false", "-ccbin", "/usr/bin/g++",
@@ -32,24 +32,29 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """Build the library; `defines`/`out` produce experiment variants
+    (e.g. defines=("VS_MINB=5",), out=".../libvscreen_gpu.minb5.so")."""
+    lib = out or LIB
+    if not force and not defines and out is None and not _stale():
         return LIB
+    tag = "_".join(d.replace("=", "") for d in defines) or "default"
     objs = []
     for src in SOURCES:
-        obj = os.path.join(CSRC, "_build", src + ".o")
+        obj = os.path.join(CSRC, "_build", tag, src + ".o")
         os.makedirs(os.path.dirname(obj), exist_ok=True)
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src),
+               "-o", obj]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
         objs.append(obj)
-    cmd = [NVCC, *ARCH, "-shared", "-ccbin", "/usr/bin/g++", *objs, "-o", LIB + ".tmp", "-lpthread"]
+    cmd = [NVCC, *ARCH, "-shared", "-ccbin", "/usr/bin/g++", *objs, "-o", lib + ".tmp", "-lpthread"]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":

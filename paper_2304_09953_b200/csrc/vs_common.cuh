@@ -1,0 +1,404 @@
+// Shared device helpers of the dock-and-score kernels (vs_dock.cu,
+// vs_kernels.cu): RNG, TMA bulk staging, field/wall/pair terms, per-warp
+// shared-memory layout, torsion chain, sweep key, start draws.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "vs_detmath.cuh"
+#include "vs_types.h"
+
+namespace vs {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr unsigned long long kGolden = 0x9e3779b97f4a7c15ull;
+constexpr double kPiD = 3.14159265358979323846;
+constexpr double kHalfPiD = 1.57079632679489661923;
+constexpr float kPiF = 3.14159274f;     // (float)pi, rounds up
+constexpr float kTwoPiF = 6.28318548f;  // (float)(2 pi)
+
+// ------------------------------------------------------------------ RNG --
+// Counter-based splitmix64 of rng.hpp:14-41, evaluated at an explicit
+// counter so that any draw of any start attempt is random-access.
+__device__ __forceinline__ unsigned long long rng_mix(unsigned long long z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ unsigned long long rng_draw(unsigned long long key,
+                                                       unsigned long long ctr) {
+  return rng_mix(key + kGolden * ctr);
+}
+__device__ __forceinline__ double rng_unit(unsigned long long u) {
+  return static_cast<double>(u >> 11) * 0x1.0p-53;
+}
+
+// ------------------------------------------------------ TMA bulk staging --
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ---------------------------------------------------------------- field --
+__device__ __forceinline__ float site_sum(const SiteF* __restrict__ s, int n, float x, float y,
+                                          float z) {
+  float acc = 0.0f;
+  for (int k = 0; k < n; ++k) {
+    const float4 c = *reinterpret_cast<const float4*>(&s[k].cx);
+    const float inv = s[k].inv2s2;
+    const float dx = x - c.x, dy = y - c.y, dz = z - c.z;
+    const float e = det_exp_neg(-(det_norm2(dx, dy, dz) * inv));
+    acc = fmaf(c.w, e, acc);
+  }
+  return acc;
+}
+
+// Trilinear interpolation on one corner-packed cell (two 16 B loads of the
+// same 32 B sector).  Same corner values and lerp order as the node layout,
+// so the result is bit-identical to interpolating the node map.
+__device__ __forceinline__ float trilinear(const GridDev& g, const float4* __restrict__ cells,
+                                           float x, float y, float z) {
+  const float gx = (x - g.ox) * g.inv_h;
+  const float gy = (y - g.oy) * g.inv_h;
+  const float gz = (z - g.oz) * g.inv_h;
+  const float fx = floorf(gx), fy = floorf(gy), fz = floorf(gz);
+  const int ix = static_cast<int>(fx), iy = static_cast<int>(fy), iz = static_cast<int>(fz);
+  if (gx < 0.0f || gy < 0.0f || gz < 0.0f || ix > g.nx - 2 || iy > g.ny - 2 || iz > g.nz - 2)
+    return 0.0f;
+  const float tx = gx - fx, ty = gy - fy, tz = gz - fz;
+  const float4* c = cells + 2 * ((static_cast<long>(iz) * (g.ny - 1) + iy) * (g.nx - 1) + ix);
+  const float4 lo = __ldg(c), hi = __ldg(c + 1);  // (000,100,010,110), (001,101,011,111)
+  const float c00 = det_lerp(lo.x, lo.y, tx), c10 = det_lerp(lo.z, lo.w, tx);
+  const float c01 = det_lerp(hi.x, hi.y, tx), c11 = det_lerp(hi.z, hi.w, tx);
+  const float c0 = det_lerp(c00, c10, ty), c1 = det_lerp(c01, c11, ty);
+  return det_lerp(c0, c1, tz);
+}
+
+template <int kGrid>
+__device__ __forceinline__ float field_steric(const PocketDev& pk, float x, float y, float z) {
+  if (kGrid) return trilinear(pk.grid, pk.grid.steric_c, x, y, z);
+  return site_sum(pk.sites, pk.n_steric, x, y, z);
+}
+
+// kind bonus of rescore (dock.cpp:304-314): C -> lipophilic, N/O -> hbond
+template <int kGrid>
+__device__ __forceinline__ float atom_bonus(const PocketDev& pk, int cls, float x, float y,
+                                            float z) {
+  if (cls == 1) {
+    if (kGrid) return trilinear(pk.grid, pk.grid.lipo_c, x, y, z);
+    return site_sum(pk.sites + pk.n_steric + pk.n_hbond, pk.n_lipo, x, y, z);
+  }
+  if (cls == 2) {
+    if (kGrid) return trilinear(pk.grid, pk.grid.hbond_c, x, y, z);
+    return site_sum(pk.sites + pk.n_steric, pk.n_hbond, x, y, z);
+  }
+  return 0.0f;
+}
+
+// wall softplus of one atom (dock.cpp:31-44, 98-101)
+__device__ __forceinline__ float wall_term(const PocketDev& pk, float x, float y, float z) {
+  const float d0 = x - pk.lo[0], d1 = pk.hi[0] - x;
+  const float d2 = y - pk.lo[1], d3 = pk.hi[1] - y;
+  const float d4 = z - pk.lo[2], d5 = pk.hi[2] - z;
+  const float w = fminf(fminf(fminf(d0, d1), fminf(d2, d3)), fminf(d4, d5));
+  return det_softplus((pk.r - w) * 10.0f);
+}
+
+// pair clash softplus (dock.cpp:86-97) from an FP64 difference
+__device__ __forceinline__ float pair_term_d(const PocketDev& pk, double dx, double dy,
+                                             double dz) {
+  const double d2 = det_norm2_d(dx, dy, dz);
+  if (d2 > static_cast<double>(pk.cut2)) return 0.0f;
+  return det_softplus((pk.r - sqrtf(static_cast<float>(d2))) * 10.0f);
+}
+
+// per-atom field + wall of local coordinate y under (R, t), FP64 transform
+template <int kGrid>
+__device__ __forceinline__ void atom_terms(const PocketDev& pk, const Mat3d& R, double tx,
+                                           double ty, double tz, double yx, double yy, double yz,
+                                           float* f, float* w, float* xo = nullptr) {
+  double x, y, z;
+  det_apply_d(R, yx, yy, yz, tx, ty, tz, &x, &y, &z);
+  const float xf = static_cast<float>(x), yf = static_cast<float>(y), zf = static_cast<float>(z);
+  *f = field_steric<kGrid>(pk, xf, yf, zf);
+  *w = wall_term(pk, xf, yf, zf);
+  if (xo) {
+    xo[0] = xf;
+    xo[1] = yf;
+    xo[2] = zf;
+  }
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+  for (int off = 16; off > 0; off >>= 1) v = v + __shfl_xor_sync(kFull, v, off);
+  return v;
+}
+
+// ------------------------------------------------- per-warp shared layout --
+constexpr int kCand = 16;  // rescore kernel: pose columns (one lane pair each)
+
+struct WarpSmem {
+  double4* y0;    // conformer (x, y, z, class), FP64
+  double4* ys;    // state local coordinates (torsions applied), FP64
+  float4* ysf;    // FP32 copy of the state (sweep)
+  float4* xf;     // posed coordinates under test (FP32, decisions)
+  float* fa;      // per-atom field term of the posed state
+  float* wa;      // per-atom wall term of the posed state
+  int4* ax;       // torsion axes
+  float* theta;   // state torsions
+  uint8_t* mov;   // moving lists
+  unsigned* mask; // moving set of the current flex axis (4 words)
+  double* col;    // rescore kernel only: pose columns [i][c][16], FP64
+  float* kscore;  // kept-pose scores
+  int* kinv;      // rank -> kept index
+  float* kresc;   // survivor rescores by rank
+  uint64_t* bar;
+};
+
+__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+__host__ __device__ inline size_t warp_smem_bytes(int nmax, int tmax, int mvmax, bool cols) {
+  size_t b = 0;
+  b += 2 * 32 * size_t(nmax);                 // y0, ys
+  b += 2 * 16 * size_t(nmax);                 // ysf, xf
+  b += 2 * align16(4 * size_t(nmax));         // fa, wa
+  b += 16 * size_t(tmax);                     // ax
+  b += align16(4 * size_t(tmax));             // theta
+  b += align16(size_t(mvmax));                // mov
+  b += 16;                                    // mask
+  if (cols) b += 8 * size_t(nmax) * 3 * kCand;
+  b += 3 * 4 * kMaxRestarts;                  // kscore, kinv, kresc
+  b += 16;                                    // mbarrier
+  return b;
+}
+
+__device__ inline WarpSmem carve(unsigned char* base, int nmax, int tmax, int mvmax, bool cols) {
+  WarpSmem s;
+  size_t o = 0;
+  s.y0 = reinterpret_cast<double4*>(base + o); o += 32 * size_t(nmax);
+  s.ys = reinterpret_cast<double4*>(base + o); o += 32 * size_t(nmax);
+  s.ysf = reinterpret_cast<float4*>(base + o); o += 16 * size_t(nmax);
+  s.xf = reinterpret_cast<float4*>(base + o); o += 16 * size_t(nmax);
+  s.fa = reinterpret_cast<float*>(base + o); o += align16(4 * size_t(nmax));
+  s.wa = reinterpret_cast<float*>(base + o); o += align16(4 * size_t(nmax));
+  s.ax = reinterpret_cast<int4*>(base + o); o += 16 * size_t(tmax);
+  s.theta = reinterpret_cast<float*>(base + o); o += align16(4 * size_t(tmax));
+  s.mov = base + o; o += align16(size_t(mvmax));
+  s.mask = reinterpret_cast<unsigned*>(base + o); o += 16;
+  s.col = nullptr;
+  if (cols) {
+    s.col = reinterpret_cast<double*>(base + o);
+    o += 8 * size_t(nmax) * 3 * kCand;
+  }
+  s.kscore = reinterpret_cast<float*>(base + o); o += 4 * kMaxRestarts;
+  s.kinv = reinterpret_cast<int*>(base + o); o += 4 * kMaxRestarts;
+  s.kresc = reinterpret_cast<float*>(base + o); o += 4 * kMaxRestarts;
+  s.bar = reinterpret_cast<uint64_t*>(base + o);
+  return s;
+}
+
+// Stage one ligand's atoms, axes and moving lists with TMA bulk copies.
+__device__ inline void stage_ligand(const LibDev& lib, int lig, const WarpSmem& s, int lane,
+                                    uint32_t& phase, int4& meta) {
+  meta = lib.meta[lig];
+  const int2 mv = lib.mov[lig];
+  __syncwarp();
+  if (lane == 0) {
+    fence_proxy_async();
+    const uint32_t bytes = 32u * meta.y + 16u * meta.w + static_cast<uint32_t>(mv.y);
+    mbar_expect_tx(s.bar, bytes);
+    bulk_g2s(s.y0, lib.atoms + meta.x, 32u * meta.y, s.bar);
+    if (meta.w > 0) bulk_g2s(s.ax, lib.axes + meta.z, 16u * meta.w, s.bar);
+    if (mv.y > 0) bulk_g2s(s.mov, lib.moving + mv.x, static_cast<uint32_t>(mv.y), s.bar);
+  }
+  mbar_wait(s.bar, phase);
+  phase ^= 1u;
+}
+
+// s.ys = y0 with torsions [0, T) at s.theta (dock.cpp:54-63); lanes over
+// the moving atoms of each torsion in turn.
+static __device__ __noinline__ void chain_coop(const WarpSmem& s, int N, int T, int lane) {
+  for (int i = lane; i < N; i += 32) s.ys[i] = s.y0[i];
+  __syncwarp();
+  for (int j = 0; j < T; ++j) {
+    const int4 a = s.ax[j];
+    const double4 o = s.ys[a.x], b = s.ys[a.y];
+    const Mat3d M = det_torsion_mat_d(o.x, o.y, o.z, b.x, b.y, b.z, s.theta[j]);
+    for (int m = lane; m < a.w; m += 32) {
+      const int idx = s.mov[a.z + m];
+      double4 v = s.ys[idx];
+      det_apply_d(M, v.x - o.x, v.y - o.y, v.z - o.z, o.x, o.y, o.z, &v.x, &v.y, &v.z);
+      s.ys[idx] = v;
+    }
+    __syncwarp();
+  }
+}
+
+// s.xf = (float)(R s.ys + t) over all atoms (lanes over atoms)
+static __device__ __noinline__ void pose_coop(const WarpSmem& s, int N, const Mat3d& R, double tx, double ty,
+                                 double tz, int lane) {
+  for (int i = lane; i < N; i += 32) {
+    const double4 v = s.ys[i];
+    double x, y, z;
+    det_apply_d(R, v.x, v.y, v.z, tx, ty, tz, &x, &y, &z);
+    s.xf[i] = make_float4(static_cast<float>(x), static_cast<float>(y), static_cast<float>(z), 0.0f);
+  }
+  __syncwarp();
+}
+
+// Rigid-variant key of one sweep pose: F - lam W over the FP32 state coords.
+template <int kGrid>
+#ifdef VS_RIGID_INLINE
+static __device__ __forceinline__
+#else
+static __device__ __noinline__
+#endif
+float eval_rigid(const PocketDev& pk, const float4* ys, int N, const Mat3 R,
+                                   float tx, float ty, float tz) {
+  float fe = 0.0f, fo = 0.0f, we = 0.0f, wo = 0.0f;
+  int i = 0;
+  for (; i + 1 < N; i += 2) {
+    const float4 a = ys[i], b = ys[i + 1];
+    float x0, y0, z0, x1, y1, z1;
+    det_apply(R, a.x, a.y, a.z, tx, ty, tz, &x0, &y0, &z0);
+    det_apply(R, b.x, b.y, b.z, tx, ty, tz, &x1, &y1, &z1);
+    const float f0 = field_steric<kGrid>(pk, x0, y0, z0);
+    const float f1 = field_steric<kGrid>(pk, x1, y1, z1);
+    fe = fe + f0;
+    we = we + wall_term(pk, x0, y0, z0);
+    fo = fo + f1;
+    wo = wo + wall_term(pk, x1, y1, z1);
+  }
+  if (i < N) {
+    const float4 a = ys[i];
+    float x, y, z;
+    det_apply(R, a.x, a.y, a.z, tx, ty, tz, &x, &y, &z);
+    fe = fe + field_steric<kGrid>(pk, x, y, z);
+    we = we + wall_term(pk, x, y, z);
+  }
+  return (fe + fo) - pk.lam * (we + wo);
+}
+
+// all kept poses at RMSD >= delta from s.xf (dock.cpp:335-340, 392-401)
+static __device__ __noinline__ bool diverse_from_kept(const WarpSmem& s, const float4* kx, int nk, int nmax,
+                                         int N, float delta, int lane) {
+  bool ok = true;
+  for (int k = lane; k < nk; k += 32) {
+    const float4* X = kx + static_cast<size_t>(k) * nmax;
+    float acc = 0.0f;
+    for (int i = 0; i < N; ++i) {
+      const float4 a = s.xf[i], b = X[i];
+      acc = acc + det_norm2(a.x - b.x, a.y - b.y, a.z - b.z);
+    }
+    if (sqrtf(acc / static_cast<float>(N)) < delta) ok = false;
+  }
+  return __all_sync(kFull, ok);
+}
+
+// Translation-sweep lattice: l = 0 is the current point, l = 1..26 the
+// non-zero offsets of {-1,0,1}^3 in x-fastest order, scaled by sc.
+constexpr int kTransIters = 16;
+constexpr float kTransMin = 1.0f / 64.0f;
+__device__ __forceinline__ void trans_offset(int l, float sc, float* ox, float* oy, float* oz) {
+  if (l == 0) {
+    *ox = *oy = *oz = 0.0f;
+    return;
+  }
+  const int m = l - 1 < 13 ? l - 1 : l;
+  *ox = static_cast<float>(m % 3 - 1) * sc;
+  *oy = static_cast<float>((m / 3) % 3 - 1) * sc;
+  *oz = static_cast<float>(m / 9 - 1) * sc;
+}
+
+// Start attempt `att` of restart key rkey (dock.cpp:346-354): writes
+// s.theta and returns t (FP32) and q (FP64-normalized, cast to FP32).
+static __device__ __noinline__ void draw_start(const PocketDev& pk, unsigned long long rkey, int att, int T,
+                                  const WarpSmem& s, int lane, float* t, float* q) {
+  const unsigned long long base = static_cast<unsigned long long>(att) * (11ull + T);
+  double tv = 0.0, nv = 0.0;
+  for (int l = lane; l < 7 + T; l += 32) {
+    if (l < 3) {
+      const double u = rng_unit(rng_draw(rkey, base + 1 + l));
+      tv = pk.lo_d[l] + (pk.hi_d[l] - pk.lo_d[l]) * u;
+    } else if (l < 7) {
+      const int m = l - 3;
+      const unsigned long long ua = rng_draw(rkey, base + 4 + 2 * m);
+      const unsigned long long ub = rng_draw(rkey, base + 5 + 2 * m);
+      const double u1 = static_cast<double>((ua >> 11) + 1) * 0x1.0p-53;
+      const double u2 = rng_unit(ub);
+      nv = sqrt(-2.0 * log(u1)) * cos(2.0 * kPiD * u2);
+    } else {
+      const double u = rng_unit(rng_draw(rkey, base + 12 + (l - 7)));
+      s.theta[l - 7] = static_cast<float>(-kPiD + (kPiD - -kPiD) * u);
+    }
+  }
+  t[0] = static_cast<float>(__shfl_sync(kFull, tv, 0));
+  t[1] = static_cast<float>(__shfl_sync(kFull, tv, 1));
+  t[2] = static_cast<float>(__shfl_sync(kFull, tv, 2));
+  const double w = __shfl_sync(kFull, nv, 3), x = __shfl_sync(kFull, nv, 4),
+               y = __shfl_sync(kFull, nv, 5), z = __shfl_sync(kFull, nv, 6);
+  const double n = sqrt(w * w + x * x + y * y + z * z);
+  if (n > 1e-12) {
+    q[0] = static_cast<float>(w / n);
+    q[1] = static_cast<float>(x / n);
+    q[2] = static_cast<float>(y / n);
+    q[3] = static_cast<float>(z / n);
+  } else {
+    q[0] = 1.0f;
+    q[1] = q[2] = q[3] = 0.0f;
+  }
+  __syncwarp();
+}
+
+// Rotation of the flex move: moving_j rotated about the state's axis j by
+// delta = th_new - th_old (FP64 of two FP32 angles).  The half angle is
+// folded into [-pi/2, pi/2] by q -> -q (same matrix).
+__device__ __forceinline__ Mat3d flex_mat(double ox, double oy, double oz, double bx, double by,
+                                          double bz, float th_new, float th_old) {
+  const double dx = bx - ox, dy = by - oy, dz = bz - oz;
+  const double n = sqrt(det_norm2_d(dx, dy, dz));
+  double hh = 0.5 * (static_cast<double>(th_new) - static_cast<double>(th_old));
+  if (hh > kHalfPiD) hh = hh - kPiD;
+  else if (hh < -kHalfPiD) hh = hh + kPiD;
+  double s, c;
+  det_sincos_d(hh, &s, &c);
+  const double ks = n > 0.0 ? s / n : 0.0;
+  return det_quat_mat_d(c, dx * ks, dy * ks, dz * ks);
+}
+
+__device__ __forceinline__ bool in_mask(const unsigned* mask, int i) {
+  return (mask[i >> 5] >> (i & 31)) & 1u;
+}
+
+}  // namespace vs

@@ -1,0 +1,515 @@
+// The dock kernel (K2 + K3 + K4a of DESIGN.md §4): sweep-v1 pose generation,
+// canonical scoring, diversity, keep-top filter, rescore, per-ligand best
+// and top-k key — one warp per ligand, persistent warps pulling ligands from
+// an atomic counter over one global LPT order (largest ligands first).
+//
+// The per-restart work is split into non-inlined phases (start, sweep, flex,
+// keep, finish): the fully inlined kernel was ~126 KB of SASS and stalled on
+// instruction fetch; the phases keep each hot loop small and shared.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "vs_common.cuh"
+
+namespace vs {
+
+struct Dims {
+  int nmax, tmax, mvmax;
+};
+
+struct PoseF {
+  float t[3];
+  float q[4];
+};
+
+__device__ __forceinline__ WarpSmem dock_smem(const Dims d) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  return carve(smem_raw + (threadIdx.x >> 5) * warp_smem_bytes(d.nmax, d.tmax, d.mvmax, false),
+               d.nmax, d.tmax, d.mvmax, false);
+}
+
+// ---- start of restart r (dock.cpp:343-356): first attempt whose start
+// coordinates are at RMSD >= delta from every kept pose (or the 50th);
+// leaves the torsion-applied state in s.ys / s.ysf and s.theta.
+static __device__ __noinline__ int start_phase(const PocketDev& pk, const Dims d,
+                                               unsigned long long rkey, int N, int T,
+                                               const float4* kx, int nk, float delta, int lane,
+                                               PoseF* P) {
+  const WarpSmem s = dock_smem(d);
+  float t[3], q[4];
+  int att = 0;
+  bool have_chain = false;
+  for (; att < 50; ++att) {
+    draw_start(pk, rkey, att, T, s, lane, t, q);
+    if (nk == 0) break;
+    chain_coop(s, N, T, lane);
+    have_chain = true;
+    pose_coop(s, N, det_pose_mat_d(q[0], q[1], q[2], q[3]), t[0], t[1], t[2], lane);
+    if (diverse_from_kept(s, kx, nk, d.nmax, N, delta, lane)) break;
+  }
+  if (att == 50) att = 49;
+  if (!have_chain) chain_coop(s, N, T, lane);
+  for (int i = lane; i < N; i += 32) {
+    const double4 v = s.ys[i];
+    s.ysf[i] = make_float4(static_cast<float>(v.x), static_cast<float>(v.y),
+                           static_cast<float>(v.z), 0.0f);
+  }
+  __syncwarp();
+  for (int c = 0; c < 3; ++c) P->t[c] = t[c];
+  for (int c = 0; c < 4; ++c) P->q[c] = q[c];
+  return att;
+}
+
+// ---- rigid roto-translation sweep (SWEEP_V1.md §2.3-2.4): K orientations
+// about the posed centroid (lanes over rotations), then a compass search
+// over the 26 lattice neighbours with halving steps.  FP32 key F - lam W.
+template <int kGrid>
+static __device__ __noinline__ int sweep_phase(const PocketDev& pk, const Dims d,
+                                               const float4* __restrict__ rots, int K, int N,
+                                               int lane, PoseF* P, int* n_trans) {
+  const WarpSmem s = dock_smem(d);
+  float qs0 = P->q[0], qs1 = P->q[1], qs2 = P->q[2], qs3 = P->q[3];
+  det_quat_normalize(&qs0, &qs1, &qs2, &qs3);
+  float cx = 0.0f, cy = 0.0f, cz = 0.0f;
+  for (int i = 0; i < N; ++i) {
+    const float4 v = s.ysf[i];
+    cx = cx + v.x;
+    cy = cy + v.y;
+    cz = cz + v.z;
+  }
+  const float fN = static_cast<float>(N);
+  cx = cx / fN;
+  cy = cy / fN;
+  cz = cz / fN;
+  float Cx, Cy, Cz;
+  det_apply(det_quat_mat(qs0, qs1, qs2, qs3), cx, cy, cz, P->t[0], P->t[1], P->t[2], &Cx, &Cy,
+            &Cz);
+
+  float best_key = -INFINITY;
+  int best_k = 0x7fffffff;
+  for (int k = lane; k < K; k += 32) {
+    const float4 rq = rots[k];
+    float w4, x4, y4, z4;
+    det_quat_mul(rq.x, rq.y, rq.z, rq.w, qs0, qs1, qs2, qs3, &w4, &x4, &y4, &z4);
+    det_quat_normalize(&w4, &x4, &y4, &z4);
+    const Mat3 Rk = det_quat_mat(w4, x4, y4, z4);
+    float vx, vy, vz;
+    det_apply(Rk, cx, cy, cz, 0.0f, 0.0f, 0.0f, &vx, &vy, &vz);
+    const float key = eval_rigid<kGrid>(pk, s.ysf, N, Rk, Cx - vx, Cy - vy, Cz - vz);
+    if (key > best_key) {
+      best_key = key;
+      best_k = k;
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    const float ok = __shfl_xor_sync(kFull, best_key, off);
+    const int oi = __shfl_xor_sync(kFull, best_k, off);
+    if (ok > best_key || (ok == best_key && oi < best_k)) {
+      best_key = ok;
+      best_k = oi;
+    }
+  }
+  float pw, px, py, pz;
+  {
+    const float4 rq = rots[best_k];
+    det_quat_mul(rq.x, rq.y, rq.z, rq.w, qs0, qs1, qs2, qs3, &pw, &px, &py, &pz);
+    det_quat_normalize(&pw, &px, &py, &pz);
+  }
+  const Mat3 RS = det_quat_mat(pw, px, py, pz);
+  float ptx, pty, ptz;
+  {
+    float vx, vy, vz;
+    det_apply(RS, cx, cy, cz, 0.0f, 0.0f, 0.0f, &vx, &vy, &vz);
+    ptx = Cx - vx;
+    pty = Cy - vy;
+    ptz = Cz - vz;
+  }
+  float sc = 1.0f;
+  int it = 0;
+  for (; it < kTransIters && sc >= kTransMin; ++it) {
+    float key = -INFINITY, ox = 0.0f, oy = 0.0f, oz = 0.0f;
+    if (lane < 27) {
+      trans_offset(lane, sc, &ox, &oy, &oz);
+      key = eval_rigid<kGrid>(pk, s.ysf, N, RS, ptx + ox, pty + oy, ptz + oz);
+    }
+    int li = lane < 27 ? lane : 0x7fffffff;
+    for (int off = 16; off > 0; off >>= 1) {
+      const float ok = __shfl_xor_sync(kFull, key, off);
+      const int oi = __shfl_xor_sync(kFull, li, off);
+      if (ok > key || (ok == key && oi < li)) {
+        key = ok;
+        li = oi;
+      }
+    }
+    if (li != 0) {
+      float wx, wy, wz;
+      trans_offset(li, sc, &wx, &wy, &wz);
+      ptx = ptx + wx;
+      pty = pty + wy;
+      ptz = ptz + wz;
+    } else {
+      sc = sc * 0.5f;
+    }
+  }
+  *n_trans += it;
+  P->t[0] = ptx;
+  P->t[1] = pty;
+  P->t[2] = ptz;
+  P->q[0] = pw;
+  P->q[1] = px;
+  P->q[2] = py;
+  P->q[3] = pz;
+  return best_k;
+}
+
+// ---- incremental greedy torsion flex (SWEEP_V1.md §2.5).  Per (pass,
+// axis j) the 16 candidate angles are scored as base(state: atoms outside
+// moving_j, pairs not crossing it; 32-lane strided sums + xor butterfly)
+// + moved part(candidate: moving_j atoms rotated about the state's axis j
+// and their cross pairs; lane pair (a, h), lane h takes moving positions
+// = h mod 2).  Returns the score of the final state.
+template <int kGrid>
+static __device__ __noinline__ float flex_phase(const PocketDev& pk, const Dims d, int N, int T,
+                                                int F, int A, float step, const PoseF* P,
+                                                int lane) {
+  const WarpSmem s = dock_smem(d);
+  const int a_lane = lane & 15;
+  const int h = lane >> 4;
+  const Mat3d RD = det_pose_mat_d(P->q[0], P->q[1], P->q[2], P->q[3]);
+  const double tdx = P->t[0], tdy = P->t[1], tdz = P->t[2];
+  for (int i = lane; i < N; i += 32) {
+    const double4 v = s.ys[i];
+    atom_terms<kGrid>(pk, RD, tdx, tdy, tdz, v.x, v.y, v.z, &s.fa[i], &s.wa[i]);
+  }
+  __syncwarp();
+  const bool do_flex = T > 0 && F > 0;
+  const int steps = do_flex ? F * T : 1;
+  float S_cur = 0.0f;
+  for (int st = 0; st < steps; ++st) {
+    const int j = do_flex ? st % T : -1;
+    const int4 ax = do_flex ? s.ax[j] : make_int4(0, 0, 0, 0);
+    const int m = ax.w;
+    if (lane < 4) {
+      unsigned wd = 0;
+      for (int q2 = 0; q2 < m; ++q2) {
+        const int idx = s.mov[ax.z + q2];
+        if ((idx >> 5) == lane) wd |= 1u << (idx & 31);
+      }
+      s.mask[lane] = wd;
+    }
+    __syncwarp();
+    float fb = 0.0f, wb = 0.0f, pb = 0.0f;
+    for (int i = lane; i < N; i += 32) {
+      if (!in_mask(s.mask, i)) {
+        fb = fb + s.fa[i];
+        wb = wb + s.wa[i];
+      }
+    }
+    {
+      int ps = 0;
+      for (int i = 0; i + 1 < N; ++i) {
+        const double4 yi = s.ys[i];
+        const bool mi = in_mask(s.mask, i);
+        for (int k = i + 1 + ((lane - ps) & 31); k < N; k += 32) {
+          if (mi != in_mask(s.mask, k)) continue;
+          const double4 yk = s.ys[k];
+          pb = pb + pair_term_d(pk, yi.x - yk.x, yi.y - yk.y, yi.z - yk.z);
+        }
+        ps += N - 1 - i;
+      }
+    }
+    fb = warp_sum(fb);
+    wb = warp_sum(wb);
+    pb = warp_sum(pb);
+    const bool active = do_flex && a_lane < A;
+    float th_new = 0.0f;
+    float fm = 0.0f, wm = 0.0f, pc = 0.0f;
+    if (active) {
+      const float th_old = s.theta[j];
+      th_new = th_old;
+      if (a_lane > 0) {
+        float v = th_old + static_cast<float>(a_lane) * step;
+        if (v >= kPiF) v = v - kTwoPiF;
+        th_new = v;
+      }
+      const double4 o = s.ys[ax.x], b = s.ys[ax.y];
+      const Mat3d M = flex_mat(o.x, o.y, o.z, b.x, b.y, b.z, th_new, th_old);
+      for (int q2 = h; q2 < m; q2 += 2) {
+        const int idx = s.mov[ax.z + q2];
+        const double4 v = s.ys[idx];
+        double yx, yy, yz;
+        det_apply_d(M, v.x - o.x, v.y - o.y, v.z - o.z, o.x, o.y, o.z, &yx, &yy, &yz);
+        float fi, wi;
+        atom_terms<kGrid>(pk, RD, tdx, tdy, tdz, yx, yy, yz, &fi, &wi);
+        fm = fm + fi;
+        wm = wm + wi;
+        for (int k = 0; k < N; ++k) {
+          if (in_mask(s.mask, k)) continue;
+          const double4 yk = s.ys[k];
+          pc = pc + pair_term_d(pk, yx - yk.x, yy - yk.y, yz - yk.z);
+        }
+      }
+    }
+    const float fm2 = __shfl_xor_sync(kFull, fm, 16);
+    const float wm2 = __shfl_xor_sync(kFull, wm, 16);
+    const float pc2 = __shfl_xor_sync(kFull, pc, 16);
+    float S = (fb + (fm + fm2)) - pk.lam * ((pb + (pc + pc2)) + (wb + (wm + wm2)));
+    if (do_flex && !active) S = -INFINITY;
+    int ai = (do_flex && !active) ? 0x7fffffff : a_lane;
+    for (int off = 8; off > 0; off >>= 1) {
+      const float oS = __shfl_xor_sync(kFull, S, off);
+      const int oa = __shfl_xor_sync(kFull, ai, off);
+      if (oS > S || (oS == S && oa < ai)) {
+        S = oS;
+        ai = oa;
+      }
+    }
+    S_cur = S;
+    if (do_flex && ai != 0) {  // move the state to the winning angle
+      const float th_old = s.theta[j];
+      const float th_win = __shfl_sync(kFull, th_new, ai);
+      const double4 o = s.ys[ax.x], b = s.ys[ax.y];
+      const Mat3d M = flex_mat(o.x, o.y, o.z, b.x, b.y, b.z, th_win, th_old);
+      __syncwarp();
+      for (int q2 = lane; q2 < m; q2 += 32) {
+        const int idx = s.mov[ax.z + q2];
+        double4 v = s.ys[idx];
+        det_apply_d(M, v.x - o.x, v.y - o.y, v.z - o.z, o.x, o.y, o.z, &v.x, &v.y, &v.z);
+        s.ys[idx] = v;
+        atom_terms<kGrid>(pk, RD, tdx, tdy, tdz, v.x, v.y, v.z, &s.fa[idx], &s.wa[idx]);
+      }
+      if (lane == 0) s.theta[j] = th_win;
+    }
+    __syncwarp();
+  }
+  return S_cur;
+}
+
+// ---- final coordinates, diversity against kept (dock.cpp:359-361), store
+static __device__ __noinline__ bool keep_phase(const Dims d, int N, int T, const PoseF* P,
+                                               float S, int r, int att, int best_k, float4* kx,
+                                               float* kp, int* km, int nk, float delta,
+                                               int lane) {
+  const WarpSmem s = dock_smem(d);
+  pose_coop(s, N, det_pose_mat_d(P->q[0], P->q[1], P->q[2], P->q[3]), P->t[0], P->t[1], P->t[2],
+            lane);
+  const bool keep = nk == 0 || diverse_from_kept(s, kx, nk, d.nmax, N, delta, lane);
+  if (keep) {
+    const int parw = 8 + d.tmax;
+    for (int i = lane; i < N; i += 32) kx[static_cast<size_t>(nk) * d.nmax + i] = s.xf[i];
+    float* Q = kp + static_cast<size_t>(nk) * parw;
+    if (lane == 0) {
+      for (int c = 0; c < 3; ++c) Q[c] = P->t[c];
+      for (int c = 0; c < 4; ++c) Q[3 + c] = P->q[c];
+      Q[7] = S;
+      km[nk * 4 + 0] = r;
+      km[nk * 4 + 1] = att;
+      km[nk * 4 + 2] = best_k;
+      s.kscore[nk] = S;
+    }
+    for (int jj = lane; jj < T; jj += 32) Q[8 + jj] = s.theta[jj];
+  }
+  __syncwarp();
+  return keep;
+}
+
+__device__ __forceinline__ PoseOut pose_out(const float* Q, const int* kmk, float resc) {
+  PoseOut o;
+  o.t[0] = Q[0]; o.t[1] = Q[1]; o.t[2] = Q[2];
+  o.q[0] = Q[3]; o.q[1] = Q[4]; o.q[2] = Q[5]; o.q[3] = Q[6];
+  o.score = Q[7];
+  o.rescore = resc;
+  o.restart = static_cast<int16_t>(kmk[0]);
+  o.attempt = static_cast<int16_t>(kmk[1]);
+  o.rot = static_cast<int16_t>(kmk[2]);
+  o.pad = 0;
+  return o;
+}
+
+// ---- stable sort by score desc (dock.cpp:364-366), keep-top filter
+// (dock.cpp:373-390), rescore (dock.cpp:297-316), best (pipeline.cpp:508)
+template <int kGrid>
+static __device__ __noinline__ void finish_phase(const PocketDev& pk, const Dims d,
+                                                 const DockParams& prm, const DockOut& out,
+                                                 int lig, int4 meta, int nk, const float4* kx,
+                                                 const float* kp, const int* km,
+                                                 unsigned id_rank, int lane,
+                                                 const unsigned long long* st) {
+  const WarpSmem s = dock_smem(d);
+  const int N = meta.y, T = meta.w, R = prm.R;
+  const int parw = 8 + d.tmax;
+  const int a_lane = lane & 15, h = lane >> 4;
+  int m_pass = 0;
+  for (int k = lane; k < nk; k += 32) {
+    const float sk = s.kscore[k];
+    int rank = 0;
+    for (int m2 = 0; m2 < nk; ++m2) {
+      const float sm = s.kscore[m2];
+      rank += (sm > sk || (sm == sk && m2 < k)) ? 1 : 0;
+    }
+    s.kinv[rank] = k;
+    m_pass += (static_cast<double>(sk) >= prm.min_score) ? 1 : 0;
+  }
+  for (int off = 16; off > 0; off >>= 1) m_pass += __shfl_xor_sync(kFull, m_pass, off);
+  __syncwarp();
+  const int n_surv = min(m_pass, prm.keep_top);
+  if (prm.write_all) {
+    for (int rank = lane; rank < nk; rank += 32) {
+      const int k = s.kinv[rank];
+      const float* Q = kp + static_cast<size_t>(k) * parw;
+      out.all[static_cast<size_t>(lig) * R + rank] = pose_out(Q, km + k * 4, 0.0f);
+      float* tt = out.all_tors + static_cast<size_t>(meta.z) * R + static_cast<size_t>(rank) * T;
+      for (int jj = 0; jj < T; ++jj) tt[jj] = Q[8 + jj];
+    }
+    __syncwarp();
+  }
+  for (int base = 0; base < n_surv; base += 16) {
+    const int p = base + a_lane;
+    float B = 0.0f;
+    if (p < n_surv) {
+      const float4* X = kx + static_cast<size_t>(s.kinv[p]) * d.nmax;
+      for (int i = h; i < N; i += 2) {
+        const float4 v = X[i];
+        B = B + atom_bonus<kGrid>(pk, static_cast<int>(s.y0[i].w), v.x, v.y, v.z);
+      }
+    }
+    const float B2 = __shfl_xor_sync(kFull, B, 16);
+    if (p < n_surv && h == 0) {
+      const int k = s.kinv[p];
+      const float* Q = kp + static_cast<size_t>(k) * parw;
+      const float resc = Q[7] + (B + B2);
+      s.kresc[p] = resc;
+      out.surv[static_cast<size_t>(lig) * prm.keep_top + p] = pose_out(Q, km + k * 4, resc);
+      float* tt = out.surv_tors + static_cast<size_t>(meta.z) * prm.keep_top +
+                  static_cast<size_t>(p) * T;
+      for (int jj = 0; jj < T; ++jj) tt[jj] = Q[8 + jj];
+      if (prm.write_all) out.all[static_cast<size_t>(lig) * R + p].rescore = resc;
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    float bmax = -INFINITY;
+    for (int p = 0; p < n_surv; ++p) bmax = p == 0 ? s.kresc[p] : fmaxf(bmax, s.kresc[p]);
+    out.best[lig] = bmax;
+    out.n_kept[lig] = nk;
+    out.n_surv[lig] = n_surv;
+    out.keys[lig] = n_surv > 0 ? ((static_cast<unsigned long long>(~det_orderable(bmax)) << 32) |
+                                  id_rank)
+                               : ~0ull;
+    if (out.stats) {
+      atomicAdd(out.stats + 0, st[0]);
+      atomicAdd(out.stats + 1, st[0] * static_cast<unsigned long long>(N));
+      atomicAdd(out.stats + 2, st[1]);
+      atomicAdd(out.stats + 3, st[2]);
+    }
+  }
+  __syncwarp();
+}
+
+#ifndef VS_MINB
+#define VS_MINB 8  // resident blocks per SM the register budget is sized for (64 regs)
+#endif
+
+template <int kGrid>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB)
+    vs_dock_kernel(const __grid_constant__ LibDev lib, const __grid_constant__ PocketDev pk,
+                   const float4* __restrict__ rots, const __grid_constant__ DockParams prm,
+                   const int* __restrict__ order, int n_order, int* __restrict__ work_counter,
+                   int nmax, int tmax, int mvmax, float4* __restrict__ scratch_xyz,
+                   float* __restrict__ scratch_par, int* __restrict__ scratch_meta,
+                   const __grid_constant__ DockOut out) {
+  const Dims d{nmax, tmax, mvmax};
+  const WarpSmem s = dock_smem(d);
+  const int lane = threadIdx.x & 31;
+  const long gwarp = static_cast<long>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
+  const int R = prm.R;
+  float4* kx = scratch_xyz + gwarp * R * nmax;
+  float* kp = scratch_par + gwarp * R * (8 + tmax);
+  int* km = scratch_meta + gwarp * R * 4;
+  if (lane == 0) mbar_init(s.bar);
+  __syncwarp();
+  uint32_t phase = 0;
+  const float step = kTwoPiF / static_cast<float>(prm.A);
+  while (true) {
+    int w = 0;
+    if (lane == 0) w = atomicAdd(work_counter, 1);
+    w = __shfl_sync(kFull, w, 0);
+    if (w >= n_order) break;
+    const int lig = order[w];
+    int4 meta;
+    stage_ligand(lib, lig, s, lane, phase, meta);
+    const int N = meta.y, T = meta.w;
+    const unsigned long long root = rng_mix(lib.seeds[lig] ^ kGolden);
+    int nk = 0;
+    int n_trans = 0;
+    unsigned long long st[3] = {0, 0, 0};  // translation iters, attempts, flex states
+    long long cyc[4] = {0, 0, 0, 0};       // start, sweep, flex, keep (SM cycles)
+    for (int r = 0; r < R; ++r) {
+      const unsigned long long rkey =
+          rng_mix(root ^ rng_mix(static_cast<unsigned long long>(r) + kGolden));
+      PoseF P;
+      const long long c0 = clock64();
+      const int att = start_phase(pk, d, rkey, N, T, kx, nk, prm.delta, lane, &P);
+      const long long c1 = clock64();
+      const int best_k = sweep_phase<kGrid>(pk, d, rots, prm.K, N, lane, &P, &n_trans);
+      const long long c2 = clock64();
+      const float S = flex_phase<kGrid>(pk, d, N, T, prm.F, prm.A, step, &P, lane);
+      const long long c3 = clock64();
+      if (keep_phase(d, N, T, &P, S, r, att, best_k, kx, kp, km, nk, prm.delta, lane)) ++nk;
+      cyc[0] += c1 - c0;
+      cyc[1] += c2 - c1;
+      cyc[2] += c3 - c2;
+      cyc[3] += clock64() - c3;
+      st[1] += static_cast<unsigned long long>(att) + 1;
+      st[2] += (T > 0 && prm.F > 0) ? static_cast<unsigned long long>(prm.F) * T * prm.A : 1ull;
+    }
+    st[0] = static_cast<unsigned long long>(n_trans);
+    finish_phase<kGrid>(pk, d, prm, out, lig, meta, nk, kx, kp, km, lib.id_rank[lig], lane, st);
+    if (lane == 0 && out.stats)
+      for (int c = 0; c < 4; ++c) atomicAdd(out.stats + 4 + c, static_cast<unsigned long long>(cyc[c]));
+  }
+}
+
+size_t dock_smem_per_block(int nmax, int tmax, int mvmax) {
+  return kWarpsPerBlock * warp_smem_bytes(nmax, tmax, mvmax, false);
+}
+
+template <class K>
+static void prep_dock(K kernel, size_t smem) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(smem));
+  cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       cudaSharedmemCarveoutMaxShared);
+}
+
+cudaError_t launch_dock(bool grid, int blocks, size_t smem, cudaStream_t st, const LibDev& lib,
+                        const PocketDev& pk, const float4* rots, const DockParams& prm,
+                        const int* order, int n_order, int* counter, int nmax, int tmax,
+                        int mvmax, float4* sx, float* sp, int* sm, const DockOut& out) {
+  if (grid) {
+    prep_dock(vs_dock_kernel<1>, smem);
+    vs_dock_kernel<1><<<blocks, kWarpsPerBlock * 32, smem, st>>>(
+        lib, pk, rots, prm, order, n_order, counter, nmax, tmax, mvmax, sx, sp, sm, out);
+  } else {
+    prep_dock(vs_dock_kernel<0>, smem);
+    vs_dock_kernel<0><<<blocks, kWarpsPerBlock * 32, smem, st>>>(
+        lib, pk, rots, prm, order, n_order, counter, nmax, tmax, mvmax, sx, sp, sm, out);
+  }
+  return cudaGetLastError();
+}
+
+int dock_blocks_per_sm(bool grid, size_t smem) {
+  int nb = 0;
+  if (grid) {
+    prep_dock(vs_dock_kernel<1>, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, vs_dock_kernel<1>, kWarpsPerBlock * 32,
+                                                  smem);
+  } else {
+    prep_dock(vs_dock_kernel<0>, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, vs_dock_kernel<0>, kWarpsPerBlock * 32,
+                                                  smem);
+  }
+  return nb;
+}
+
+}  // namespace vs

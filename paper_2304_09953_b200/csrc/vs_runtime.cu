@@ -86,6 +86,7 @@ struct Packed {
   std::vector<int> cls;          // class per ligand (-1 dropped)
   std::vector<long> tors_off;    // prefix sum of n_tors
   std::vector<Bucket> buckets;
+  Bucket all;  // global LPT order (dock launch)
   long total_tors = 0;
   DBuf d_meta, d_mov, d_atoms, d_axes, d_moving, d_seeds, d_idr, d_order;
   void release() {
@@ -246,6 +247,23 @@ int pack_library(vs_handle* h, const vs_library* L, const vs_size_class* classes
     }
     b.count = static_cast<int>(ids.size());
     P.buckets.push_back(b);
+  }
+  // one global LPT queue over every bucket for the dock launch: a single
+  // persistent launch has one tail instead of one per bucket
+  P.all = Bucket{};
+  P.all.start = static_cast<int>(P.order.size());
+  {
+    std::vector<int> ids;
+    for (int i = 0; i < n; ++i)
+      if (P.cls[i] >= 0) ids.push_back(i);
+    std::stable_sort(ids.begin(), ids.end(), [&](int a, int b2) { return cost[a] > cost[b2]; });
+    for (int i : ids) {
+      P.all.nmax = std::max(P.all.nmax, P.meta[i].y);
+      P.all.tmax = std::max(P.all.tmax, P.meta[i].w);
+      P.all.mvmax = std::max(P.all.mvmax, P.mov[i].y);
+      P.order.push_back(i);
+    }
+    P.all.count = static_cast<int>(ids.size());
   }
   if (P.order.empty()) P.order.push_back(0);
   return VS_OK;
@@ -533,8 +551,8 @@ int vs_dock(vs_handle* h, const vs_dock_params* prm, void* stream) {
   VS_CUDA(h, h->d_nsurv.ensure(nn * 4));
   VS_CUDA(h, h->d_keys.ensure(nn * 8));
   VS_CUDA(h, h->d_counters.ensure(64 * sizeof(int)));
-  VS_CUDA(h, h->d_stats.ensure(4 * sizeof(unsigned long long)));
-  VS_CUDA(h, cudaMemsetAsync(h->d_stats.p, 0, 4 * sizeof(unsigned long long), st));
+  VS_CUDA(h, h->d_stats.ensure(8 * sizeof(unsigned long long)));
+  VS_CUDA(h, cudaMemsetAsync(h->d_stats.p, 0, 8 * sizeof(unsigned long long), st));
   VS_CUDA(h, cudaMemsetAsync(h->d_keys.p, 0xff, nn * 8, st));
   VS_CUDA(h, cudaMemsetAsync(h->d_nkept.p, 0, nn * 4, st));
   VS_CUDA(h, cudaMemsetAsync(h->d_nsurv.p, 0, nn * 4, st));
@@ -562,36 +580,25 @@ int vs_dock(vs_handle* h, const vs_dock_params* prm, void* stream) {
 
   const bool grid = h->pk.grid_mode != 0;
   const LibDev ld = P.dev();
-  // plan launches and scratch (persistent warps, one scratch slot each)
-  struct Plan {
-    int blocks;
-    size_t smem;
-  };
-  std::vector<Plan> plans;
-  size_t need_x = 0, need_p = 0, need_m = 0;
-  for (const Bucket& b : P.buckets) {
+  // one persistent launch over the global LPT queue (every size bucket),
+  // shared memory sized for the largest ligand; one scratch slot per warp
+  const Bucket& b = P.all;
+  VS_CUDA(h, cudaEventRecord(h->ev0, st));
+  if (b.count > 0) {
     const size_t smem = dock_smem_per_block(b.nmax, b.tmax, b.mvmax);
-    if (smem > 227 * 1024) return fail(h, VS_ERR_CAPACITY, "bucket needs too much shared memory");
+    if (smem > 227 * 1024) return fail(h, VS_ERR_CAPACITY, "ligands need too much shared memory");
     int per_sm = dock_blocks_per_sm(grid, smem);
     if (per_sm < 1) per_sm = 1;
     const int want = (b.count + kWarpsPerBlock - 1) / kWarpsPerBlock;
     const int blocks = std::max(1, std::min(want, per_sm * h->sms));
-    plans.push_back({blocks, smem});
     const size_t warps = static_cast<size_t>(blocks) * kWarpsPerBlock;
-    need_x = std::max(need_x, warps * R * b.nmax * sizeof(float4));
-    need_p = std::max(need_p, warps * R * (8 + b.tmax) * sizeof(float));
-    need_m = std::max(need_m, warps * R * 4 * sizeof(int));
-  }
-  VS_CUDA(h, h->d_sx.ensure(need_x));
-  VS_CUDA(h, h->d_sp.ensure(need_p));
-  VS_CUDA(h, h->d_sm.ensure(need_m));
-  VS_CUDA(h, cudaEventRecord(h->ev0, st));
-  for (size_t bi = 0; bi < P.buckets.size(); ++bi) {
-    const Bucket& b = P.buckets[bi];
-    VS_CUDA(h, launch_dock(grid, plans[bi].blocks, plans[bi].smem, st, ld, h->pk,
-                           h->d_rots.as<const float4>(), dp, P.d_order.as<int>() + b.start,
-                           b.count, h->d_counters.as<int>() + (bi % 64), b.nmax, b.tmax, b.mvmax,
-                           h->d_sx.as<float4>(), h->d_sp.as<float>(), h->d_sm.as<int>(), out));
+    VS_CUDA(h, h->d_sx.ensure(warps * R * b.nmax * sizeof(float4)));
+    VS_CUDA(h, h->d_sp.ensure(warps * R * (8 + b.tmax) * sizeof(float)));
+    VS_CUDA(h, h->d_sm.ensure(warps * R * 4 * sizeof(int)));
+    VS_CUDA(h, launch_dock(grid, blocks, smem, st, ld, h->pk, h->d_rots.as<const float4>(), dp,
+                           P.d_order.as<int>() + b.start, b.count, h->d_counters.as<int>(),
+                           b.nmax, b.tmax, b.mvmax, h->d_sx.as<float4>(), h->d_sp.as<float>(),
+                           h->d_sm.as<int>(), out));
     ++h->launches;
   }
   VS_CUDA(h, cudaEventRecord(h->ev1, st));
@@ -611,10 +618,10 @@ double vs_last_dock_ms(const vs_handle* h) {
 
 uint64_t vs_launch_count(const vs_handle* h) { return h->launches; }
 
-int vs_last_stats(vs_handle* h, uint64_t out[4]) {
+int vs_last_stats(vs_handle* h, uint64_t out[8]) {
   if (!h->has_results) return fail(h, VS_ERR_STATE, "no results");
   VS_CUDA(h, cudaStreamSynchronize(h->last));
-  VS_CUDA(h, cudaMemcpy(out, h->d_stats.p, 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  VS_CUDA(h, cudaMemcpy(out, h->d_stats.p, 8 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
   return VS_OK;
 }
 

@@ -333,10 +333,14 @@ class Engine:
 
     def stats(self) -> dict:
         """Work counters of the last dock (capi.h vs_last_stats)."""
-        out = np.zeros(4, np.uint64)
+        out = np.zeros(8, np.uint64)
         check(_lib.vs_last_stats(self._h, ptr(out, C.c_uint64)), self._h, "stats")
+        cyc = [int(v) for v in out[4:8]]
+        tot = max(sum(cyc), 1)
         return {"translation_iters": int(out[0]), "translation_iter_atoms": int(out[1]),
-                "start_attempts": int(out[2]), "flex_states": int(out[3])}
+                "start_attempts": int(out[2]), "flex_states": int(out[3]),
+                "phase_cycle_share": {k: round(c / tot, 4) for k, c in
+                                      zip(("start", "sweep", "flex", "keep"), cyc)}}
 
     def measure_peaks(self) -> dict:
         """Measured FP32 / FP64 FMA (flop/s) and MUFU ex2 (op/s) peaks."""
