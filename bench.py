@@ -164,30 +164,53 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- roofline --
+# per-unit work of sweep-v1 as implemented; FMA = 2 flops
+ATOM_FLOP_GRID = 63      # FP32 transform 18 + trilinear 30 + wall 13 + sums 2
+ATOM_XU_GRID = 3         # float->int cell index conversions
+POSE_ROT_FLOP = 80       # quaternion product, normalize, matrix, t = C - R c
+POSE_ROT_XU = 5          # sqrt + 4 divisions of the normalization
+TERMS_FLOP = 79          # FP64 transform 18 + ATOM_FLOP_GRID - sums
+TERMS_XU = 6             # 3 FP64->FP32 conversions + 3 cell indices
+PAIR_TEST_FLOP = 9       # FP64 difference, norm, compare
+PAIR_ACTIVE_FLOP = 35    # sqrt fix-up, z, softplus (exp + log1p polynomials)
+PAIR_ACTIVE_XU = 3       # sqrt, exp shift, log1p reciprocal
+AXIS_FLOP = 40           # flex rotation: norm, sincos_d, matrix (FP64)
+MOVE_FLOP = 18           # FP64 rotation of one moving atom
+
+
 def algorithmic_work(lib, prm, stats, grid: bool, n_steric: int):
-    """Frozen work formula (SURVEY §8(d) extended by the
-    translation sweep).  FMA = 2 flops.
-      states = R + flex_states          torsion states (full chain each)
-      poses  = R*K + 27*trans_iters + flex_states   rigid placements scored
-      FLOP   = states*(27*Mv + 14*T + 15*P) + poses*(24 + 12 + Fld)*N
-      XU     = states*(2*T + 3*P)         + poses*(3 + Xf)*N
-      Fld = 25 (grid, one map) | 11*S_steric ; Xf = 0 (grid) | S_steric"""
+    """Algorithmic FLOP / XU ops of one pass of sweep-v1 over `lib`, from
+    the ligand descriptors and the device work counters:
+      rigid poses   R*K*N + 27*sum(trans_iters*N) pose-atoms, R*K pose setups
+      flex steps    F*T per restart: base (N atom sums + non-crossing pairs)
+                    + A candidates x (axis rotation + m_j moved atoms
+                    + m_j*(N-m_j) cross pairs)
+      pairs inside the cutoff (device counter) add the softplus cost."""
     R, K, A, F = prm.restarts, prm.rotations, prm.flex_angles, prm.flex_passes
     N = lib.n_atoms.astype(np.float64)
-    T = lib.n_tors.astype(np.float64)
-    ao, to, mo = lib.offsets()
-    cm = np.concatenate([[0.0], np.cumsum(lib.moving_count.astype(np.float64))])
-    Mv = cm[to[1:]] - cm[to[:-1]]
+    T = lib.n_tors.astype(np.int64)
+    _, to, _ = lib.offsets()
+    m = lib.moving_count.astype(np.float64)
+    Nt = np.repeat(N, T)                       # ligand atom count per torsion
+    pnc = m * (m - 1) / 2 + (Nt - m) * (Nt - m - 1) / 2
+    step_flop = (2 * Nt + PAIR_TEST_FLOP * pnc
+                 + A * (AXIS_FLOP + m * (MOVE_FLOP + TERMS_FLOP) + PAIR_TEST_FLOP * m * (Nt - m)))
+    step_xu = A * m * TERMS_XU
+    flex_flop = float(np.sum(step_flop)) * R * F
+    flex_xu = float(np.sum(step_xu)) * R * F
     P = N * (N - 1) / 2
-    flex = np.where((T > 0) & (F > 0), R * F * T * A, R)
-    states = R + flex
-    fld = 25.0 if grid else 11.0 * n_steric
-    xf = 0.0 if grid else float(n_steric)
-    flop_states = float(np.sum(states * (27 * Mv + 14 * T + 15 * P)))
-    xu_states = float(np.sum(states * (2 * T + 3 * P)))
-    pose_atoms = float(np.sum((R * K + flex) * N)) + 27.0 * stats["translation_iter_atoms"]
-    flop = flop_states + pose_atoms * (36.0 + fld)
-    xu = xu_states + pose_atoms * (3.0 + xf)
+    no_flex = (T == 0) | (F == 0)
+    flex_flop += float(np.sum(np.where(no_flex, R * (2 * N + PAIR_TEST_FLOP * P), 0.0)))
+    init_flop = float(np.sum(R * N * TERMS_FLOP))          # state atom terms per restart
+    chain_flop = float(np.sum(np.add.reduceat(np.r_[AXIS_FLOP + MOVE_FLOP * m, 0.0],
+                                              np.minimum(to[:-1], len(m))) * (T > 0))) * R
+    atom_f = ATOM_FLOP_GRID if grid else 31 + 11 * n_steric
+    atom_x = ATOM_XU_GRID if grid else 2 * n_steric
+    pose_atoms = float(np.sum(R * K * N)) + 27.0 * stats["translation_iter_atoms"]
+    flop = (pose_atoms * atom_f + R * K * len(lib) * POSE_ROT_FLOP + flex_flop + init_flop
+            + chain_flop + stats["active_pairs"] * PAIR_ACTIVE_FLOP)
+    xu = (pose_atoms * atom_x + R * K * len(lib) * POSE_ROT_XU + flex_xu
+          + stats["active_pairs"] * PAIR_ACTIVE_XU + R * float(np.sum(N)) * TERMS_XU)
     return flop, xu
 
 

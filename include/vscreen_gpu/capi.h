@@ -164,9 +164,9 @@ int vs_dock_host(vs_handle* h, const vs_library* lib, const vs_size_class* class
 double vs_last_dock_ms(const vs_handle* h);
 uint64_t vs_launch_count(const vs_handle* h);
 /* work counters of the last vs_dock: [0] translation-sweep iterations,
- * [1] the same weighted by ligand atoms, [2] start attempts, [3] flex
- * candidate states, [4..7] SM cycles summed over warps in the start, sweep,
- * flex and keep phases */
+ * [1] the same weighted by ligand atoms, [2] start attempts, [3] flex pair
+ * softplus evaluations (pairs inside the cutoff), [4..7] SM cycles summed
+ * over warps in the start, sweep, flex and keep phases */
 int vs_last_stats(vs_handle* h, uint64_t out[8]);
 /* measured device peaks (ops/s): FP32 FMA (2 flops), FP64 FMA, MUFU ex2 */
 int vs_measure_peaks(vs_handle* h, double* fp32_flops, double* fp64_flops, double* xu_ops);

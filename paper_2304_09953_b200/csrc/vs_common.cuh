@@ -142,6 +142,14 @@ __device__ __forceinline__ float pair_term_d(const PocketDev& pk, double dx, dou
   if (d2 > static_cast<double>(pk.cut2)) return 0.0f;
   return det_softplus((pk.r - sqrtf(static_cast<float>(d2))) * 10.0f);
 }
+// same, counting the pairs inside the cutoff (work counter)
+__device__ __forceinline__ float pair_term_d(const PocketDev& pk, double dx, double dy, double dz,
+                                             int& n_active) {
+  const double d2 = det_norm2_d(dx, dy, dz);
+  if (d2 > static_cast<double>(pk.cut2)) return 0.0f;
+  ++n_active;
+  return det_softplus((pk.r - sqrtf(static_cast<float>(d2))) * 10.0f);
+}
 
 // per-atom field + wall of local coordinate y under (R, t), FP64 transform
 template <int kGrid>

@@ -171,7 +171,7 @@ static __device__ __noinline__ int sweep_phase(const PocketDev& pk, const Dims d
 template <int kGrid>
 static __device__ __noinline__ float flex_phase(const PocketDev& pk, const Dims d, int N, int T,
                                                 int F, int A, float step, const PoseF* P,
-                                                int lane) {
+                                                int lane, unsigned long long* n_active) {
   const WarpSmem s = dock_smem(d);
   const int a_lane = lane & 15;
   const int h = lane >> 4;
@@ -185,6 +185,7 @@ static __device__ __noinline__ float flex_phase(const PocketDev& pk, const Dims 
   const bool do_flex = T > 0 && F > 0;
   const int steps = do_flex ? F * T : 1;
   float S_cur = 0.0f;
+  int nact = 0;  // pair softplus evaluations of this lane (work counter)
   for (int st = 0; st < steps; ++st) {
     const int j = do_flex ? st % T : -1;
     const int4 ax = do_flex ? s.ax[j] : make_int4(0, 0, 0, 0);
@@ -213,7 +214,7 @@ static __device__ __noinline__ float flex_phase(const PocketDev& pk, const Dims 
         for (int k = i + 1 + ((lane - ps) & 31); k < N; k += 32) {
           if (mi != in_mask(s.mask, k)) continue;
           const double4 yk = s.ys[k];
-          pb = pb + pair_term_d(pk, yi.x - yk.x, yi.y - yk.y, yi.z - yk.z);
+          pb = pb + pair_term_d(pk, yi.x - yk.x, yi.y - yk.y, yi.z - yk.z, nact);
         }
         ps += N - 1 - i;
       }
@@ -246,7 +247,7 @@ static __device__ __noinline__ float flex_phase(const PocketDev& pk, const Dims 
         for (int k = 0; k < N; ++k) {
           if (in_mask(s.mask, k)) continue;
           const double4 yk = s.ys[k];
-          pc = pc + pair_term_d(pk, yx - yk.x, yy - yk.y, yz - yk.z);
+          pc = pc + pair_term_d(pk, yx - yk.x, yy - yk.y, yz - yk.z, nact);
         }
       }
     }
@@ -282,6 +283,8 @@ static __device__ __noinline__ float flex_phase(const PocketDev& pk, const Dims 
     }
     __syncwarp();
   }
+  for (int off = 16; off > 0; off >>= 1) nact += __shfl_xor_sync(kFull, nact, off);
+  *n_active += static_cast<unsigned long long>(nact);
   return S_cur;
 }
 
@@ -442,7 +445,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB)
     const unsigned long long root = rng_mix(lib.seeds[lig] ^ kGolden);
     int nk = 0;
     int n_trans = 0;
-    unsigned long long st[3] = {0, 0, 0};  // translation iters, attempts, flex states
+    unsigned long long st[3] = {0, 0, 0};  // translation iters, attempts, active pairs
     long long cyc[4] = {0, 0, 0, 0};       // start, sweep, flex, keep (SM cycles)
     for (int r = 0; r < R; ++r) {
       const unsigned long long rkey =
@@ -453,7 +456,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB)
       const long long c1 = clock64();
       const int best_k = sweep_phase<kGrid>(pk, d, rots, prm.K, N, lane, &P, &n_trans);
       const long long c2 = clock64();
-      const float S = flex_phase<kGrid>(pk, d, N, T, prm.F, prm.A, step, &P, lane);
+      const float S = flex_phase<kGrid>(pk, d, N, T, prm.F, prm.A, step, &P, lane, &st[2]);
       const long long c3 = clock64();
       if (keep_phase(d, N, T, &P, S, r, att, best_k, kx, kp, km, nk, prm.delta, lane)) ++nk;
       cyc[0] += c1 - c0;
@@ -461,7 +464,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB)
       cyc[2] += c3 - c2;
       cyc[3] += clock64() - c3;
       st[1] += static_cast<unsigned long long>(att) + 1;
-      st[2] += (T > 0 && prm.F > 0) ? static_cast<unsigned long long>(prm.F) * T * prm.A : 1ull;
     }
     st[0] = static_cast<unsigned long long>(n_trans);
     finish_phase<kGrid>(pk, d, prm, out, lig, meta, nk, kx, kp, km, lib.id_rank[lig], lane, st);

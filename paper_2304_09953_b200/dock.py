@@ -338,7 +338,7 @@ class Engine:
         cyc = [int(v) for v in out[4:8]]
         tot = max(sum(cyc), 1)
         return {"translation_iters": int(out[0]), "translation_iter_atoms": int(out[1]),
-                "start_attempts": int(out[2]), "flex_states": int(out[3]),
+                "start_attempts": int(out[2]), "active_pairs": int(out[3]),
                 "phase_cycle_share": {k: round(c / tot, 4) for k, c in
                                       zip(("start", "sweep", "flex", "keep"), cyc)}}
 
