@@ -10,6 +10,11 @@
 
 namespace vs {
 
+// The pocket lives in constant memory (one copy per translation unit, set
+// by that unit's launch wrapper): uniform, cached loads in the inner loops
+// instead of generic loads through a parameter pointer.
+static __constant__ PocketDev c_pk;
+
 constexpr unsigned kFull = 0xffffffffu;
 constexpr unsigned long long kGolden = 0x9e3779b97f4a7c15ull;
 constexpr double kPiD = 3.14159265358979323846;
@@ -107,8 +112,8 @@ __device__ __forceinline__ float trilinear(const GridDev& g, const float4* __res
 
 template <int kGrid>
 __device__ __forceinline__ float field_steric(const PocketDev& pk, float x, float y, float z) {
-  if (kGrid) return trilinear(pk.grid, pk.grid.steric_c, x, y, z);
-  return site_sum(pk.sites, pk.n_steric, x, y, z);
+  if (kGrid) return trilinear(c_pk.grid, c_pk.grid.steric_c, x, y, z);
+  return site_sum(c_pk.sites, c_pk.n_steric, x, y, z);
 }
 
 // kind bonus of rescore (dock.cpp:304-314): C -> lipophilic, N/O -> hbond
@@ -116,39 +121,39 @@ template <int kGrid>
 __device__ __forceinline__ float atom_bonus(const PocketDev& pk, int cls, float x, float y,
                                             float z) {
   if (cls == 1) {
-    if (kGrid) return trilinear(pk.grid, pk.grid.lipo_c, x, y, z);
-    return site_sum(pk.sites + pk.n_steric + pk.n_hbond, pk.n_lipo, x, y, z);
+    if (kGrid) return trilinear(c_pk.grid, c_pk.grid.lipo_c, x, y, z);
+    return site_sum(c_pk.sites + c_pk.n_steric + c_pk.n_hbond, c_pk.n_lipo, x, y, z);
   }
   if (cls == 2) {
-    if (kGrid) return trilinear(pk.grid, pk.grid.hbond_c, x, y, z);
-    return site_sum(pk.sites + pk.n_steric, pk.n_hbond, x, y, z);
+    if (kGrid) return trilinear(c_pk.grid, c_pk.grid.hbond_c, x, y, z);
+    return site_sum(c_pk.sites + c_pk.n_steric, c_pk.n_hbond, x, y, z);
   }
   return 0.0f;
 }
 
 // wall softplus of one atom (dock.cpp:31-44, 98-101)
 __device__ __forceinline__ float wall_term(const PocketDev& pk, float x, float y, float z) {
-  const float d0 = x - pk.lo[0], d1 = pk.hi[0] - x;
-  const float d2 = y - pk.lo[1], d3 = pk.hi[1] - y;
-  const float d4 = z - pk.lo[2], d5 = pk.hi[2] - z;
+  const float d0 = x - c_pk.lo[0], d1 = c_pk.hi[0] - x;
+  const float d2 = y - c_pk.lo[1], d3 = c_pk.hi[1] - y;
+  const float d4 = z - c_pk.lo[2], d5 = c_pk.hi[2] - z;
   const float w = fminf(fminf(fminf(d0, d1), fminf(d2, d3)), fminf(d4, d5));
-  return det_softplus((pk.r - w) * 10.0f);
+  return det_softplus((c_pk.r - w) * 10.0f);
 }
 
 // pair clash softplus (dock.cpp:86-97) from an FP64 difference
 __device__ __forceinline__ float pair_term_d(const PocketDev& pk, double dx, double dy,
                                              double dz) {
   const double d2 = det_norm2_d(dx, dy, dz);
-  if (d2 > static_cast<double>(pk.cut2)) return 0.0f;
-  return det_softplus((pk.r - sqrtf(static_cast<float>(d2))) * 10.0f);
+  if (d2 > static_cast<double>(c_pk.cut2)) return 0.0f;
+  return det_softplus((c_pk.r - sqrtf(static_cast<float>(d2))) * 10.0f);
 }
 // same, counting the pairs inside the cutoff (work counter)
 __device__ __forceinline__ float pair_term_d(const PocketDev& pk, double dx, double dy, double dz,
                                              int& n_active) {
   const double d2 = det_norm2_d(dx, dy, dz);
-  if (d2 > static_cast<double>(pk.cut2)) return 0.0f;
+  if (d2 > static_cast<double>(c_pk.cut2)) return 0.0f;
   ++n_active;
-  return det_softplus((pk.r - sqrtf(static_cast<float>(d2))) * 10.0f);
+  return det_softplus((c_pk.r - sqrtf(static_cast<float>(d2))) * 10.0f);
 }
 
 // per-atom field + wall of local coordinate y under (R, t), FP64 transform
@@ -315,7 +320,7 @@ float eval_rigid(const PocketDev& pk, const float4* ys, int N, const Mat3 R,
     fe = fe + field_steric<kGrid>(pk, x, y, z);
     we = we + wall_term(pk, x, y, z);
   }
-  return (fe + fo) - pk.lam * (we + wo);
+  return (fe + fo) - c_pk.lam * (we + wo);
 }
 
 // all kept poses at RMSD >= delta from s.xf (dock.cpp:335-340, 392-401)
@@ -358,7 +363,7 @@ static __device__ __noinline__ void draw_start(const PocketDev& pk, unsigned lon
   for (int l = lane; l < 7 + T; l += 32) {
     if (l < 3) {
       const double u = rng_unit(rng_draw(rkey, base + 1 + l));
-      tv = pk.lo_d[l] + (pk.hi_d[l] - pk.lo_d[l]) * u;
+      tv = c_pk.lo_d[l] + (c_pk.hi_d[l] - c_pk.lo_d[l]) * u;
     } else if (l < 7) {
       const int m = l - 3;
       const unsigned long long ua = rng_draw(rkey, base + 4 + 2 * m);

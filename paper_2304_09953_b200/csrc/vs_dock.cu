@@ -254,7 +254,7 @@ static __device__ __noinline__ float flex_phase(const PocketDev& pk, const Dims 
     const float fm2 = __shfl_xor_sync(kFull, fm, 16);
     const float wm2 = __shfl_xor_sync(kFull, wm, 16);
     const float pc2 = __shfl_xor_sync(kFull, pc, 16);
-    float S = (fb + (fm + fm2)) - pk.lam * ((pb + (pc + pc2)) + (wb + (wm + wm2)));
+    float S = (fb + (fm + fm2)) - c_pk.lam * ((pb + (pc + pc2)) + (wb + (wm + wm2)));
     if (do_flex && !active) S = -INFINITY;
     int ai = (do_flex && !active) ? 0x7fffffff : a_lane;
     for (int off = 8; off > 0; off >>= 1) {
@@ -488,6 +488,9 @@ cudaError_t launch_dock(bool grid, int blocks, size_t smem, cudaStream_t st, con
                         const PocketDev& pk, const float4* rots, const DockParams& prm,
                         const int* order, int n_order, int* counter, int nmax, int tmax,
                         int mvmax, float4* sx, float* sp, int* sm, const DockOut& out) {
+  cudaError_t e = cudaMemcpyToSymbolAsync(c_pk, &pk, sizeof(PocketDev), 0, cudaMemcpyHostToDevice,
+                                          st);
+  if (e != cudaSuccess) return e;
   if (grid) {
     prep_dock(vs_dock_kernel<1>, smem);
     vs_dock_kernel<1><<<blocks, kWarpsPerBlock * 32, smem, st>>>(

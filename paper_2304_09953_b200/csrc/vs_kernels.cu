@@ -276,6 +276,9 @@ cudaError_t launch_rescore(bool grid, int blocks, size_t smem, cudaStream_t st, 
                            const int* pose_off, const long* tors_base, const float4* pt,
                            const float4* pq, const float* ptors, int nmax, int tmax, int mvmax,
                            float* geo, float* resc) {
+  cudaError_t e = cudaMemcpyToSymbolAsync(c_pk, &pk, sizeof(PocketDev), 0, cudaMemcpyHostToDevice,
+                                          st);
+  if (e != cudaSuccess) return e;
   if (grid) {
     prep(vs_rescore_kernel<1>, smem);
     vs_rescore_kernel<1><<<blocks, kWarpsPerBlock * 32, smem, st>>>(
