@@ -213,7 +213,7 @@ __host__ __device__ inline size_t warp_smem_bytes(int nmax, int tmax, int mvmax,
   if (cols) b += 8 * size_t(nmax) * 3 * kCand;
   b += 3 * 4 * kMaxRestarts;                  // kscore, kinv, kresc
   b += 16;                                    // mbarrier
-  return b;
+  return (b + 127) & ~size_t(127);  // warp bases stay 128 B aligned
 }
 
 __device__ inline WarpSmem carve(unsigned char* base, int nmax, int tmax, int mvmax, bool cols) {

@@ -23,7 +23,7 @@ struct PoseF {
 };
 
 __device__ __forceinline__ WarpSmem dock_smem(const Dims d) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   return carve(smem_raw + (threadIdx.x >> 5) * warp_smem_bytes(d.nmax, d.tmax, d.mvmax, false),
                d.nmax, d.tmax, d.mvmax, false);
 }

@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
                       const float4* __restrict__ pose_q, const float* __restrict__ pose_tors,
                       int nmax, int tmax, int mvmax, float* __restrict__ geo,
                       float* __restrict__ resc) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const WarpSmem s =
