@@ -232,6 +232,11 @@ int vs_corpus_select(uint64_t seed, int64_t n_want, int32_t atom_lo, int32_t ato
                      int64_t* out_index);
 int vs_libbuild_corpus(uint64_t seed, const int64_t* index, int32_t n, const uint64_t* embed_seeds,
                        int32_t iterations, int32_t threads, vs_libbuild** out);
+/* flexible ligands (C4): consecutive corpus entries concatenated until
+ * >= atom_lo atoms; accepted ligand k is entries [first[k], first[k]+count[k]) */
+int vs_flexible_select(uint64_t seed, int32_t n_want, int32_t atom_lo, int32_t atom_hi,
+                       int32_t tors_lo, int32_t tors_hi, int64_t max_scan, int64_t* first,
+                       int32_t* count);
 
 /* batcher (batcher.cpp:7-86) */
 int vs_default_classes(vs_size_class* out, int32_t cap);

@@ -123,6 +123,8 @@ _SIGS = {
     "vs_libbuild_free": (None, [C.c_void_p]),
     "vs_corpus_select": (C.c_int, [C.c_uint64, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
                                    C.c_int32, C.c_int64, C.c_int32, P(C.c_int64)]),
+    "vs_flexible_select": (C.c_int, [C.c_uint64, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                     C.c_int32, C.c_int64, P(C.c_int64), P(C.c_int32)]),
     "vs_libbuild_corpus": (C.c_int, [C.c_uint64, P(C.c_int64), C.c_int32, P(C.c_uint64),
                                      C.c_int32, C.c_int32, P(C.c_void_p)]),
     "vs_default_classes": (C.c_int, [P(vs_size_class), C.c_int32]),

@@ -314,6 +314,18 @@ def corpus_library(seed: int, n: int, atoms: tuple[int, int], tors: tuple[int, i
     return _fetch_built(h, m, ids, ds)
 
 
+def flexible_smiles(seed: int, n: int, atoms=(60, 80), tors=(15, 20), max_scan: int = 400000):
+    """C4 population: concatenations of consecutive corpus
+    entries random_smiles(Rng(seed).split(i)) until the graph has >= atoms[0]
+    heavy atoms; kept when atoms and torsion axes fall inside the bounds."""
+    first = np.zeros(max(n, 1), np.int64)
+    count = np.zeros(max(n, 1), np.int32)
+    got = check(_lib.vs_flexible_select(seed, n, atoms[0], atoms[1], tors[0], tors[1], max_scan,
+                                        ptr(first, C.c_int64), ptr(count, C.c_int32)))
+    return ["".join(random_smiles(seed, int(first[k]) + c) for c in range(int(count[k])))
+            for k in range(got)]
+
+
 def _fetch_built(h, n, ids, ds, drop_failed=True) -> Library:
     try:
         A, T, M = C.c_int64(), C.c_int64(), C.c_int64()

@@ -11,6 +11,10 @@
 
 #include "vs_common.cuh"
 
+#ifndef VS_PHASE
+#define VS_PHASE __noinline__  // phases as separate functions (see header comment)
+#endif
+
 namespace vs {
 
 struct Dims {
@@ -31,7 +35,7 @@ __device__ __forceinline__ WarpSmem dock_smem(const Dims d) {
 // ---- start of restart r (dock.cpp:343-356): first attempt whose start
 // coordinates are at RMSD >= delta from every kept pose (or the 50th);
 // leaves the torsion-applied state in s.ys / s.ysf and s.theta.
-static __device__ __noinline__ int start_phase(const PocketDev& pk, const Dims d,
+static __device__ VS_PHASE int start_phase(const PocketDev& pk, const Dims d,
                                                unsigned long long rkey, int N, int T,
                                                const float4* kx, int nk, float delta, int lane,
                                                PoseF* P) {
@@ -64,7 +68,7 @@ static __device__ __noinline__ int start_phase(const PocketDev& pk, const Dims d
 // about the posed centroid (lanes over rotations), then a compass search
 // over the 26 lattice neighbours with halving steps.  FP32 key F - lam W.
 template <int kGrid>
-static __device__ __noinline__ int sweep_phase(const PocketDev& pk, const Dims d,
+static __device__ VS_PHASE int sweep_phase(const PocketDev& pk, const Dims d,
                                                const float4* __restrict__ rots, int K, int N,
                                                int lane, PoseF* P, int* n_trans) {
   const WarpSmem s = dock_smem(d);
@@ -169,7 +173,7 @@ static __device__ __noinline__ int sweep_phase(const PocketDev& pk, const Dims d
 // and their cross pairs; lane pair (a, h), lane h takes moving positions
 // = h mod 2).  Returns the score of the final state.
 template <int kGrid>
-static __device__ __noinline__ float flex_phase(const PocketDev& pk, const Dims d, int N, int T,
+static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, int N, int T,
                                                 int F, int A, float step, const PoseF* P,
                                                 int lane, unsigned long long* n_active) {
   const WarpSmem s = dock_smem(d);
@@ -289,7 +293,7 @@ static __device__ __noinline__ float flex_phase(const PocketDev& pk, const Dims 
 }
 
 // ---- final coordinates, diversity against kept (dock.cpp:359-361), store
-static __device__ __noinline__ bool keep_phase(const Dims d, int N, int T, const PoseF* P,
+static __device__ VS_PHASE bool keep_phase(const Dims d, int N, int T, const PoseF* P,
                                                float S, int r, int att, int best_k, float4* kx,
                                                float* kp, int* km, int nk, float delta,
                                                int lane) {
@@ -332,7 +336,7 @@ __device__ __forceinline__ PoseOut pose_out(const float* Q, const int* kmk, floa
 // ---- stable sort by score desc (dock.cpp:364-366), keep-top filter
 // (dock.cpp:373-390), rescore (dock.cpp:297-316), best (pipeline.cpp:508)
 template <int kGrid>
-static __device__ __noinline__ void finish_phase(const PocketDev& pk, const Dims d,
+static __device__ VS_PHASE void finish_phase(const PocketDev& pk, const Dims d,
                                                  const DockParams& prm, const DockOut& out,
                                                  int lig, int4 meta, int nk, const float4* kx,
                                                  const float* kp, const int* km,

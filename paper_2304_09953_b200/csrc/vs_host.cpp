@@ -231,6 +231,40 @@ int vs_corpus_select(uint64_t seed, int64_t n_want, int32_t atom_lo, int32_t ato
   return static_cast<int>(found);
 }
 
+// C4 population: concatenate consecutive corpus entries until the graph has
+// >= atom_lo heavy atoms; keep the string when atoms <= atom_hi and the
+// torsion axes lie in [tors_lo, tors_hi].  Writes [first entry, count) per
+// accepted ligand; returns how many were found.
+int vs_flexible_select(uint64_t seed, int32_t n_want, int32_t atom_lo, int32_t atom_hi,
+                       int32_t tors_lo, int32_t tors_hi, int64_t max_scan, int64_t* first,
+                       int32_t* count) {
+  int found = 0;
+  int64_t i = 0;
+  while (found < n_want && i < max_scan) {
+    const int64_t start = i;
+    std::string s;
+    int na = 0, nt = 0;
+    bool ok = true;
+    while (na < atom_lo) {
+      s += random_smiles(seed, static_cast<uint64_t>(i++));
+      try {
+        const Graph g = parse_smiles(s);
+        na = static_cast<int>(g.elements.size());
+        if (na >= atom_lo) nt = static_cast<int>(torsion_axes(g).axes.size());
+      } catch (const std::exception&) {
+        ok = false;
+        break;
+      }
+    }
+    if (ok && na <= atom_hi && nt >= tors_lo && nt <= tors_hi) {
+      first[found] = start;
+      count[found] = static_cast<int32_t>(i - start);
+      ++found;
+    }
+  }
+  return found;
+}
+
 // vs_libbuild_run over corpus entries given by index (SMILES generated here).
 int vs_libbuild_corpus(uint64_t seed, const int64_t* index, int32_t n, const uint64_t* embed_seeds,
                        int32_t iterations, int32_t threads, vs_libbuild** out) {
