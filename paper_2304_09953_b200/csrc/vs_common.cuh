@@ -99,15 +99,19 @@ __device__ __forceinline__ float trilinear(const GridDev& g, const float4* __res
   const float gz = (z - g.oz) * g.inv_h;
   const float fx = floorf(gx), fy = floorf(gy), fz = floorf(gz);
   const int ix = static_cast<int>(fx), iy = static_cast<int>(fy), iz = static_cast<int>(fz);
-  if (gx < 0.0f || gy < 0.0f || gz < 0.0f || ix > g.nx - 2 || iy > g.ny - 2 || iz > g.nz - 2)
-    return 0.0f;
+  // gx < 0 <=> ix < 0 (floor), so one unsigned compare per axis covers both
+  // ends; out-of-grid lanes read cell 0 and are zeroed (no divergent branch)
+  const bool in = static_cast<unsigned>(ix) <= static_cast<unsigned>(g.nx - 2) &&
+                  static_cast<unsigned>(iy) <= static_cast<unsigned>(g.ny - 2) &&
+                  static_cast<unsigned>(iz) <= static_cast<unsigned>(g.nz - 2);
   const float tx = gx - fx, ty = gy - fy, tz = gz - fz;
-  const float4* c = cells + 2 * ((static_cast<long>(iz) * (g.ny - 1) + iy) * (g.nx - 1) + ix);
+  const int cell = in ? (iz * (g.ny - 1) + iy) * (g.nx - 1) + ix : 0;
+  const float4* c = cells + 2 * cell;
   const float4 lo = __ldg(c), hi = __ldg(c + 1);  // (000,100,010,110), (001,101,011,111)
   const float c00 = det_lerp(lo.x, lo.y, tx), c10 = det_lerp(lo.z, lo.w, tx);
   const float c01 = det_lerp(hi.x, hi.y, tx), c11 = det_lerp(hi.z, hi.w, tx);
   const float c0 = det_lerp(c00, c10, ty), c1 = det_lerp(c01, c11, ty);
-  return det_lerp(c0, c1, tz);
+  return in ? det_lerp(c0, c1, tz) : 0.0f;
 }
 
 template <int kGrid>

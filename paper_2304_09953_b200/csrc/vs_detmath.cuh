@@ -54,11 +54,33 @@ __device__ __forceinline__ float det_log1p01(float u) {
 
 // softplus(z) = log1p(exp z) (dock.cpp:23); z > 30 -> z; z < -30 -> 0
 // (contribution < 1e-13, the spec's skip rule).
+// Branch-free: the core is evaluated on z clamped to [-30, 30] (where it
+// equals the unclamped core and exp_neg's underflow guard cannot fire) and
+// the two tails are selected afterwards, so warps whose lanes straddle the
+// tails do not diverge.
 __device__ __forceinline__ float det_softplus(float z) {
+#ifdef VS_SP_BRANCHY
   if (z > 30.0f) return z;
   if (z < -30.0f) return 0.0f;
-  const float u = det_exp_neg(-fabsf(z));
-  return fmaxf(z, 0.0f) + det_log1p01(u);
+  return fmaxf(z, 0.0f) + det_log1p01(det_exp_neg(-fabsf(z)));
+#endif
+  const float zc = fminf(fmaxf(z, -30.0f), 30.0f);
+  const float a = -fabsf(zc);
+  const float sh = __fadd_rn(a * 1.44269504f, 12582912.0f);
+  const float k = sh - 12582912.0f;
+  float r = fmaf(k, -0.693145752f, a);
+  r = fmaf(k, -1.42860677e-06f, r);
+  float p = 1.98412698e-04f;
+  p = fmaf(p, r, 1.38888889e-03f);
+  p = fmaf(p, r, 8.33333333e-03f);
+  p = fmaf(p, r, 4.16666667e-02f);
+  p = fmaf(p, r, 1.66666667e-01f);
+  p = fmaf(p, r, 0.5f);
+  p = fmaf(p, r, 1.0f);
+  p = fmaf(p, r, 1.0f);
+  const float u = p * __int_as_float((__float_as_int(sh) - 0x4B400000 + 127) << 23);
+  const float core = fmaxf(zc, 0.0f) + det_log1p01(u);
+  return z > 30.0f ? z : (z < -30.0f ? 0.0f : core);
 }
 
 // sin and cos for |x| <= ~1.6 (half torsion angles).

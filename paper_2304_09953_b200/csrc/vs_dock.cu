@@ -188,6 +188,7 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
   __syncwarp();
   const bool do_flex = T > 0 && F > 0;
   const int steps = do_flex ? F * T : 1;
+  const int W = (N + 31) >> 5;
   float S_cur = 0.0f;
   int nact = 0;  // pair softplus evaluations of this lane (work counter)
   for (int st = 0; st < steps; ++st) {
@@ -239,19 +240,23 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
       }
       const double4 o = s.ys[ax.x], b = s.ys[ax.y];
       const Mat3d M = flex_mat(o.x, o.y, o.z, b.x, b.y, b.z, th_new, th_old);
+      // partners: the atoms outside moving_j, walked as set bits of the
+      // complemented mask (ascending k, same trip count in both halves)
       for (int q2 = h; q2 < m; q2 += 2) {
-        const int idx = s.mov[ax.z + q2];
-        const double4 v = s.ys[idx];
+        const double4 v = s.ys[s.mov[ax.z + q2]];
         double yx, yy, yz;
         det_apply_d(M, v.x - o.x, v.y - o.y, v.z - o.z, o.x, o.y, o.z, &yx, &yy, &yz);
         float fi, wi;
         atom_terms<kGrid>(pk, RD, tdx, tdy, tdz, yx, yy, yz, &fi, &wi);
         fm = fm + fi;
         wm = wm + wi;
-        for (int k = 0; k < N; ++k) {
-          if (in_mask(s.mask, k)) continue;
-          const double4 yk = s.ys[k];
-          pc = pc + pair_term_d(pk, yx - yk.x, yy - yk.y, yz - yk.z, nact);
+        for (int wd = 0; wd < W; ++wd) {
+          unsigned b2 = ~s.mask[wd];
+          if (wd == W - 1 && (N & 31)) b2 &= (1u << (N & 31)) - 1u;
+          for (; b2; b2 &= b2 - 1u) {
+            const double4 yk = s.ys[wd * 32 + __ffs(b2) - 1];
+            pc = pc + pair_term_d(pk, yx - yk.x, yy - yk.y, yz - yk.z, nact);
+          }
         }
       }
     }

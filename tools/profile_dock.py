@@ -1,8 +1,8 @@
 """Small fixed workload for ncu captures of the dock kernel: the bench's C2
 library (first N ligands), pocket and knobs; one warm-up dock then one
-profiled dock (3 bucket launches: <= 16, <= 32, <= 48 atoms).
+profiled dock (one persistent launch).
 
-  ncu --set full --import-source on -k regex:vs_dock_kernel -s 3 -c 3 \
+  ncu --set full --import-source on -k regex:vs_dock_kernel -s 1 -c 1 \
       -o gpurun_out/prof python tools/profile_dock.py --ligands 4000
 """
 import argparse
