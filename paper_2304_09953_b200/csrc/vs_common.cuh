@@ -177,6 +177,20 @@ __device__ __forceinline__ void atom_terms(const PocketDev& pk, const Mat3d& R, 
   }
 }
 
+// same, with the warp-uniform transform read from shared memory at each use
+// (keeps 24 FP64 registers free in the flex loops)
+template <int kGrid>
+__device__ __forceinline__ void atom_terms_s(const double* pm, double yx, double yy, double yz,
+                                             float* f, float* w) {
+  const volatile double* v = pm;
+  const double x = fma(v[0], yx, fma(v[1], yy, fma(v[2], yz, v[9])));
+  const double y = fma(v[3], yx, fma(v[4], yy, fma(v[5], yz, v[10])));
+  const double z = fma(v[6], yx, fma(v[7], yy, fma(v[8], yz, v[11])));
+  const float xf = static_cast<float>(x), yf = static_cast<float>(y), zf = static_cast<float>(z);
+  *f = field_steric<kGrid>(c_pk, xf, yf, zf);
+  *w = wall_term(c_pk, xf, yf, zf);
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
   for (int off = 16; off > 0; off >>= 1) v = v + __shfl_xor_sync(kFull, v, off);
   return v;
@@ -188,6 +202,7 @@ constexpr int kCand = 16;  // rescore kernel: pose columns (one lane pair each)
 struct WarpSmem {
   double4* y0;    // conformer (x, y, z, class), FP64
   double4* ys;    // state local coordinates (torsions applied), FP64
+  double* pose;   // flex: posed transform R (row-major 9) and t (3), FP64, warp-uniform
   float4* ysf;    // FP32 copy of the state (sweep)
   float4* xf;     // posed coordinates under test (FP32, decisions)
   float* fa;      // per-atom field term of the posed state
@@ -208,6 +223,7 @@ __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(
 __host__ __device__ inline size_t warp_smem_bytes(int nmax, int tmax, int mvmax, bool cols) {
   size_t b = 0;
   b += 2 * 32 * size_t(nmax);                 // y0, ys
+  b += 96;                                    // pose
   b += 2 * 16 * size_t(nmax);                 // ysf, xf
   b += 2 * align16(4 * size_t(nmax));         // fa, wa
   b += 16 * size_t(tmax);                     // ax
@@ -225,6 +241,7 @@ __device__ inline WarpSmem carve(unsigned char* base, int nmax, int tmax, int mv
   size_t o = 0;
   s.y0 = reinterpret_cast<double4*>(base + o); o += 32 * size_t(nmax);
   s.ys = reinterpret_cast<double4*>(base + o); o += 32 * size_t(nmax);
+  s.pose = reinterpret_cast<double*>(base + o); o += 96;
   s.ysf = reinterpret_cast<float4*>(base + o); o += 16 * size_t(nmax);
   s.xf = reinterpret_cast<float4*>(base + o); o += 16 * size_t(nmax);
   s.fa = reinterpret_cast<float*>(base + o); o += align16(4 * size_t(nmax));

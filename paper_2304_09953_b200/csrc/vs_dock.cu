@@ -179,11 +179,18 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
   const WarpSmem s = dock_smem(d);
   const int a_lane = lane & 15;
   const int h = lane >> 4;
-  const Mat3d RD = det_pose_mat_d(P->q[0], P->q[1], P->q[2], P->q[3]);
-  const double tdx = P->t[0], tdy = P->t[1], tdz = P->t[2];
+  if (lane == 0) {
+    const Mat3d RD = det_pose_mat_d(P->q[0], P->q[1], P->q[2], P->q[3]);
+    double* pm = s.pose;
+    pm[0] = RD.m00; pm[1] = RD.m01; pm[2] = RD.m02;
+    pm[3] = RD.m10; pm[4] = RD.m11; pm[5] = RD.m12;
+    pm[6] = RD.m20; pm[7] = RD.m21; pm[8] = RD.m22;
+    pm[9] = P->t[0]; pm[10] = P->t[1]; pm[11] = P->t[2];
+  }
+  __syncwarp();
   for (int i = lane; i < N; i += 32) {
     const double4 v = s.ys[i];
-    atom_terms<kGrid>(pk, RD, tdx, tdy, tdz, v.x, v.y, v.z, &s.fa[i], &s.wa[i]);
+    atom_terms_s<kGrid>(s.pose, v.x, v.y, v.z, &s.fa[i], &s.wa[i]);
   }
   __syncwarp();
   const bool do_flex = T > 0 && F > 0;
@@ -247,7 +254,7 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
         double yx, yy, yz;
         det_apply_d(M, v.x - o.x, v.y - o.y, v.z - o.z, o.x, o.y, o.z, &yx, &yy, &yz);
         float fi, wi;
-        atom_terms<kGrid>(pk, RD, tdx, tdy, tdz, yx, yy, yz, &fi, &wi);
+        atom_terms_s<kGrid>(s.pose, yx, yy, yz, &fi, &wi);
         fm = fm + fi;
         wm = wm + wi;
         for (int wd = 0; wd < W; ++wd) {
@@ -286,7 +293,7 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
         double4 v = s.ys[idx];
         det_apply_d(M, v.x - o.x, v.y - o.y, v.z - o.z, o.x, o.y, o.z, &v.x, &v.y, &v.z);
         s.ys[idx] = v;
-        atom_terms<kGrid>(pk, RD, tdx, tdy, tdz, v.x, v.y, v.z, &s.fa[idx], &s.wa[idx]);
+        atom_terms_s<kGrid>(s.pose, v.x, v.y, v.z, &s.fa[idx], &s.wa[idx]);
       }
       if (lane == 0) s.theta[j] = th_win;
     }
