@@ -62,18 +62,18 @@ float vso_exp_neg(float x) {
   return p * s;
 }
 
-float vso_log1p01(float u) {
-  float w = u / (2.0f + u);
-  float w2 = w * w;
-  float p = 0.133333333f;
-  p = fmaf(p, w2, 0.153846154f);
-  p = fmaf(p, w2, 0.181818182f);
-  p = fmaf(p, w2, 0.222222222f);
-  p = fmaf(p, w2, 0.285714286f);
-  p = fmaf(p, w2, 0.4f);
-  p = fmaf(p, w2, 0.666666667f);
-  p = fmaf(p, w2, 2.0f);
-  return w * p;
+float vso_log1p01(float u) { /* u * P9(u), P9 ~ log1p(u)/u on [0, 1] (rel err ~1.3e-7) */
+  float p = -0x1.b5963cp-9f;
+  p = fmaf(p, u, 0x1.4c35fap-6f);
+  p = fmaf(p, u, -0x1.d92392p-5f);
+  p = fmaf(p, u, 0x1.b59fa2p-4f);
+  p = fmaf(p, u, -0x1.3a6dfep-3f);
+  p = fmaf(p, u, 0x1.934c92p-3f);
+  p = fmaf(p, u, -0x1.ff203ap-3f);
+  p = fmaf(p, u, 0x1.554d4ep-2f);
+  p = fmaf(p, u, -0x1.ffffc6p-2f);
+  p = fmaf(p, u, 1.0f);
+  return u * p;
 }
 
 /* dock.cpp:23 plus the |z| > 30 rules of the spec */
