@@ -89,11 +89,17 @@ __device__ __forceinline__ float site_sum(const SiteF* __restrict__ s, int n, fl
   return acc;
 }
 
-// Trilinear interpolation on one corner-packed cell (two 16 B loads of the
-// same 32 B sector).  Same corner values and lerp order as the node layout,
-// so the result is bit-identical to interpolating the node map.
-__device__ __forceinline__ float trilinear(const GridDev& g, const float4* __restrict__ cells,
-                                           float x, float y, float z) {
+// One trilinear lookup split in two halves so that callers can issue the
+// next lookup's loads before consuming this one.
+struct TriCell {
+  float4 lo, hi;  // corners (000,100,010,110), (001,101,011,111)
+  float tx, ty, tz;
+  bool in;
+};
+
+// address + fractional part + the two cell loads (issued, not consumed)
+__device__ __forceinline__ TriCell tri_issue(const GridDev& g, const float4* __restrict__ cells,
+                                             float x, float y, float z) {
   const float gx = (x - g.ox) * g.inv_h;
   const float gy = (y - g.oy) * g.inv_h;
   const float gz = (z - g.oz) * g.inv_h;
@@ -101,17 +107,33 @@ __device__ __forceinline__ float trilinear(const GridDev& g, const float4* __res
   const int ix = static_cast<int>(fx), iy = static_cast<int>(fy), iz = static_cast<int>(fz);
   // gx < 0 <=> ix < 0 (floor), so one unsigned compare per axis covers both
   // ends; out-of-grid lanes read cell 0 and are zeroed (no divergent branch)
-  const bool in = static_cast<unsigned>(ix) <= static_cast<unsigned>(g.nx - 2) &&
-                  static_cast<unsigned>(iy) <= static_cast<unsigned>(g.ny - 2) &&
-                  static_cast<unsigned>(iz) <= static_cast<unsigned>(g.nz - 2);
-  const float tx = gx - fx, ty = gy - fy, tz = gz - fz;
-  const int cell = in ? (iz * (g.ny - 1) + iy) * (g.nx - 1) + ix : 0;
-  const float4* c = cells + 2 * cell;
-  const float4 lo = __ldg(c), hi = __ldg(c + 1);  // (000,100,010,110), (001,101,011,111)
-  const float c00 = det_lerp(lo.x, lo.y, tx), c10 = det_lerp(lo.z, lo.w, tx);
-  const float c01 = det_lerp(hi.x, hi.y, tx), c11 = det_lerp(hi.z, hi.w, tx);
-  const float c0 = det_lerp(c00, c10, ty), c1 = det_lerp(c01, c11, ty);
-  return in ? det_lerp(c0, c1, tz) : 0.0f;
+  TriCell c;
+  c.in = static_cast<unsigned>(ix) <= static_cast<unsigned>(g.nx - 2) &&
+         static_cast<unsigned>(iy) <= static_cast<unsigned>(g.ny - 2) &&
+         static_cast<unsigned>(iz) <= static_cast<unsigned>(g.nz - 2);
+  c.tx = gx - fx;
+  c.ty = gy - fy;
+  c.tz = gz - fz;
+  const int cell = c.in ? (iz * (g.ny - 1) + iy) * (g.nx - 1) + ix : 0;
+  const float4* p = cells + 2 * cell;
+  c.lo = __ldg(p);
+  c.hi = __ldg(p + 1);
+  return c;
+}
+
+__device__ __forceinline__ float tri_finish(const TriCell& c) {
+  const float c00 = det_lerp(c.lo.x, c.lo.y, c.tx), c10 = det_lerp(c.lo.z, c.lo.w, c.tx);
+  const float c01 = det_lerp(c.hi.x, c.hi.y, c.tx), c11 = det_lerp(c.hi.z, c.hi.w, c.tx);
+  const float c0 = det_lerp(c00, c10, c.ty), c1 = det_lerp(c01, c11, c.ty);
+  return c.in ? det_lerp(c0, c1, c.tz) : 0.0f;
+}
+
+// Trilinear interpolation on one corner-packed cell (two 16 B loads of the
+// same 32 B sector).  Same corner values and lerp order as the node layout,
+// so the result is bit-identical to interpolating the node map.
+__device__ __forceinline__ float trilinear(const GridDev& g, const float4* __restrict__ cells,
+                                           float x, float y, float z) {
+  return tri_finish(tri_issue(g, cells, x, y, z));
 }
 
 template <int kGrid>
@@ -151,13 +173,20 @@ __device__ __forceinline__ float pair_term_d(const PocketDev& pk, double dx, dou
   if (d2 > static_cast<double>(c_pk.cut2)) return 0.0f;
   return det_softplus((c_pk.r - sqrtf(static_cast<float>(d2))) * 10.0f);
 }
-// same, counting the pairs inside the cutoff (work counter)
+#ifndef VS_SOFT_ATTR
+#define VS_SOFT_ATTR __forceinline__
+#endif
+// clash softplus of a pair inside the cutoff, from its FP64 squared distance
+static __device__ VS_SOFT_ATTR float pair_soft(double d2) {
+  return det_softplus((c_pk.r - sqrtf(static_cast<float>(d2))) * 10.0f);
+}
+// same as pair_term_d, counting the pairs inside the cutoff (work counter)
 __device__ __forceinline__ float pair_term_d(const PocketDev& pk, double dx, double dy, double dz,
                                              int& n_active) {
   const double d2 = det_norm2_d(dx, dy, dz);
   if (d2 > static_cast<double>(c_pk.cut2)) return 0.0f;
   ++n_active;
-  return det_softplus((c_pk.r - sqrtf(static_cast<float>(d2))) * 10.0f);
+  return pair_soft(d2);
 }
 
 // per-atom field + wall of local coordinate y under (R, t), FP64 transform
@@ -179,8 +208,11 @@ __device__ __forceinline__ void atom_terms(const PocketDev& pk, const Mat3d& R, 
 
 // same, with the warp-uniform transform read from shared memory at each use
 // (keeps 24 FP64 registers free in the flex loops)
+#ifndef VS_TERMS_ATTR
+#define VS_TERMS_ATTR __forceinline__
+#endif
 template <int kGrid>
-__device__ __forceinline__ void atom_terms_s(const double* pm, double yx, double yy, double yz,
+static __device__ VS_TERMS_ATTR void atom_terms_s(const double* pm, double yx, double yy, double yz,
                                              float* f, float* w) {
   const volatile double* v = pm;
   const double x = fma(v[0], yx, fma(v[1], yy, fma(v[2], yz, v[9])));
@@ -320,26 +352,25 @@ static __device__ __noinline__
 #endif
 float eval_rigid(const PocketDev& pk, const float4* ys, int N, const Mat3 R,
                                    float tx, float ty, float tz) {
+  // one atom per iteration, never unrolled: the loop body (~2 KB of SASS)
+  // stays resident in the ~6 KB L0 instruction cache next to the flex
+  // loops of the other warps (the 2x-unrolled body missed it and stalled
+  // on instruction fetch at every 128 B line)
   float fe = 0.0f, fo = 0.0f, we = 0.0f, wo = 0.0f;
-  int i = 0;
-  for (; i + 1 < N; i += 2) {
-    const float4 a = ys[i], b = ys[i + 1];
-    float x0, y0, z0, x1, y1, z1;
-    det_apply(R, a.x, a.y, a.z, tx, ty, tz, &x0, &y0, &z0);
-    det_apply(R, b.x, b.y, b.z, tx, ty, tz, &x1, &y1, &z1);
-    const float f0 = field_steric<kGrid>(pk, x0, y0, z0);
-    const float f1 = field_steric<kGrid>(pk, x1, y1, z1);
-    fe = fe + f0;
-    we = we + wall_term(pk, x0, y0, z0);
-    fo = fo + f1;
-    wo = wo + wall_term(pk, x1, y1, z1);
-  }
-  if (i < N) {
+#pragma unroll 1
+  for (int i = 0; i < N; ++i) {
     const float4 a = ys[i];
     float x, y, z;
     det_apply(R, a.x, a.y, a.z, tx, ty, tz, &x, &y, &z);
-    fe = fe + field_steric<kGrid>(pk, x, y, z);
-    we = we + wall_term(pk, x, y, z);
+    const float f = field_steric<kGrid>(pk, x, y, z);
+    const float w = wall_term(pk, x, y, z);
+    if (i & 1) {
+      fo = fo + f;
+      wo = wo + w;
+    } else {
+      fe = fe + f;
+      we = we + w;
+    }
   }
   return (fe + fo) - c_pk.lam * (we + wo);
 }
