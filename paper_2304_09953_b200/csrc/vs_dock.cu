@@ -219,16 +219,24 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
       }
     }
     {
-      int ps = 0;
-      for (int i = 0; i + 1 < N; ++i) {
-        const double4 yi = s.ys[i];
-        const bool mi = in_mask(s.mask, i);
-        for (int k = i + 1 + ((lane - ps) & 31); k < N; k += 32) {
-          if (mi != in_mask(s.mask, k)) continue;
-          const double4 yk = s.ys[k];
+      // lane l takes the pairs p = l, l + 32, ... of the row-major (i < k)
+      // order, (i, k) advanced incrementally: every lane busy, same pairs and
+      // per-lane order as a 32-strided walk of each row
+      int i = 0, k = lane + 1;
+      while (i < N - 1 && k >= N) {
+        k = k - N + i + 2;
+        ++i;
+      }
+      while (i < N - 1) {
+        if (in_mask(s.mask, i) == in_mask(s.mask, k)) {
+          const double4 yi = s.ys[i], yk = s.ys[k];
           pb = pb + pair_term_d(pk, yi.x - yk.x, yi.y - yk.y, yi.z - yk.z, nact);
         }
-        ps += N - 1 - i;
+        k += 32;
+        while (i < N - 1 && k >= N) {
+          k = k - N + i + 2;
+          ++i;
+        }
       }
     }
     fb = warp_sum(fb);
