@@ -220,6 +220,7 @@ struct vso_pocket {
   float gx0, gy0, gz0, h, inv_h;
   int nx, ny, nz;
   float *steric, *hbond, *lipo;
+  float* key; /* sweep-key map: steric - lam * wall at each node */
 };
 
 static float site_sum(const site_f* s, int n, float x, float y, float z) {
@@ -308,6 +309,7 @@ int vso_pocket_new(const vso_pocket_desc* d, vso_pocket** out) {
     p->steric = (float*)malloc(nodes * 4);
     p->hbond = (float*)malloc(nodes * 4);
     p->lipo = (float*)malloc(nodes * 4);
+    p->key = (float*)malloc(nodes * 4);
     for (size_t id = 0; id < nodes; ++id) {
       int ix = (int)(id % (size_t)p->nx), iy = (int)((id / (size_t)p->nx) % (size_t)p->ny);
       int iz = (int)(id / ((size_t)p->nx * p->ny));
@@ -316,6 +318,8 @@ int vso_pocket_new(const vso_pocket_desc* d, vso_pocket** out) {
       p->steric[id] = site_sum(p->sites, p->n_st, x, y, z);
       p->hbond[id] = site_sum(p->sites + p->n_st, p->n_hb, x, y, z);
       p->lipo[id] = site_sum(p->sites + p->n_st + p->n_hb, p->n_li, x, y, z);
+      const float xn[3] = {x, y, z};
+      p->key[id] = fmaf(-p->lam, wall(p, xn), p->steric[id]);
     }
   }
   *out = p;
@@ -324,7 +328,7 @@ int vso_pocket_new(const vso_pocket_desc* d, vso_pocket** out) {
 
 void vso_pocket_free(vso_pocket* p) {
   if (!p) return;
-  free(p->sites); free(p->steric); free(p->hbond); free(p->lipo);
+  free(p->sites); free(p->steric); free(p->hbond); free(p->lipo); free(p->key);
   free(p);
 }
 
@@ -459,8 +463,43 @@ static float score_state(const vso_pocket* p, const lig_t* L, const double* y, c
   return (F[0] + F[1]) - p->lam * ((P[0] + P[1]) + (W[0] + W[1]));
 }
 
+/* sweep key (SWEEP_V1.md §2.3): grid mode works in grid coordinates,
+ * g = (R/h) y + (t - o)/h, and interpolates the key map K = S - lam W; an
+ * atom off the grid scores -lam * wall at x = g h + o.  Analytic mode:
+ * F - lam W over the FP32 state copy.  Parity sums over atoms. */
 static float rigid_key(const vso_pocket* p, const lig_t* L, const float* y, const mat3* R,
-                       const float* t) { /* FP32 sweep key over the FP32 state copy */
+                       const float* t) {
+  if (p->grid) {
+    const float ih = p->inv_h;
+    float A[9];
+    for (int e = 0; e < 9; ++e) A[e] = R->m[e] * ih;
+    const float u[3] = {(t[0] - p->gx0) * ih, (t[1] - p->gy0) * ih, (t[2] - p->gz0) * ih};
+    float K[2] = {0, 0};
+    for (int i = 0; i < L->N; ++i) {
+      const float* v = &y[3 * i];
+      float g[3];
+      for (int c = 0; c < 3; ++c)
+        g[c] = fmaf(A[3 * c], v[0], fmaf(A[3 * c + 1], v[1], fmaf(A[3 * c + 2], v[2], u[c])));
+      float fx = floorf(g[0]), fy = floorf(g[1]), fz = floorf(g[2]);
+      int ix = (int)fx, iy = (int)fy, iz = (int)fz;
+      float term;
+      if ((unsigned)ix <= (unsigned)(p->nx - 2) && (unsigned)iy <= (unsigned)(p->ny - 2) &&
+          (unsigned)iz <= (unsigned)(p->nz - 2)) {
+        float tx = g[0] - fx, ty = g[1] - fy, tz = g[2] - fz;
+        long sx = p->nx, sxy = (long)p->nx * p->ny;
+        const float* b = p->key + ((long)iz * p->ny + iy) * p->nx + ix;
+        float c00 = lerp(b[0], b[1], tx), c10 = lerp(b[sx], b[sx + 1], tx);
+        float c01 = lerp(b[sxy], b[sxy + 1], tx), c11 = lerp(b[sxy + sx], b[sxy + sx + 1], tx);
+        term = lerp(lerp(c00, c10, ty), lerp(c01, c11, ty), tz);
+      } else {
+        const float xw[3] = {fmaf(g[0], p->h, p->gx0), fmaf(g[1], p->h, p->gy0),
+                             fmaf(g[2], p->h, p->gz0)};
+        term = -(p->lam * wall(p, xw));
+      }
+      K[i & 1] = K[i & 1] + term;
+    }
+    return K[0] + K[1];
+  }
   float F[2] = {0, 0}, W[2] = {0, 0};
   for (int i = 0; i < L->N; ++i) {
     float x[3];

@@ -158,12 +158,15 @@ __device__ __forceinline__ float atom_bonus(const PocketDev& pk, int cls, float 
 }
 
 // wall softplus of one atom (dock.cpp:31-44, 98-101)
-__device__ __forceinline__ float wall_term(const PocketDev& pk, float x, float y, float z) {
-  const float d0 = x - c_pk.lo[0], d1 = c_pk.hi[0] - x;
-  const float d2 = y - c_pk.lo[1], d3 = c_pk.hi[1] - y;
-  const float d4 = z - c_pk.lo[2], d5 = c_pk.hi[2] - z;
+__device__ __forceinline__ float wall_of(const PocketDev& P, float x, float y, float z) {
+  const float d0 = x - P.lo[0], d1 = P.hi[0] - x;
+  const float d2 = y - P.lo[1], d3 = P.hi[1] - y;
+  const float d4 = z - P.lo[2], d5 = P.hi[2] - z;
   const float w = fminf(fminf(fminf(d0, d1), fminf(d2, d3)), fminf(d4, d5));
-  return det_softplus((c_pk.r - w) * 10.0f);
+  return det_softplus((P.r - w) * 10.0f);
+}
+__device__ __forceinline__ float wall_term(const PocketDev& pk, float x, float y, float z) {
+  return wall_of(c_pk, x, y, z);
 }
 
 // pair clash softplus (dock.cpp:86-97) from an FP64 difference
@@ -343,7 +346,20 @@ static __device__ __noinline__ void pose_coop(const WarpSmem& s, int N, const Ma
   __syncwarp();
 }
 
-// Rigid-variant key of one sweep pose: F - lam W over the FP32 state coords.
+// Sweep key of one rigid pose over the FP32 state copy (SWEEP_V1.md §2.3),
+// one atom per iteration and never unrolled so the loop body stays resident
+// in the ~6 KB L0 instruction cache next to the other warps' flex loops.
+//  analytic: F - lam W (parity sums of field and wall)
+//  grid:     sum of the key map K = S - lam W interpolated at the atom, the
+//            pose composed with the grid frame (g = (R/h) y + (t - o)/h) so
+//            one FMA chain yields cell coordinates; atoms off the grid score
+//            -lam * wall at x = g h + o (cold, out of line).
+static __device__ __noinline__ float off_grid_term(float gx, float gy, float gz) {
+  const GridDev& g = c_pk.grid;
+  return -(c_pk.lam * wall_of(c_pk, fmaf(gx, g.h, g.ox), fmaf(gy, g.h, g.oy),
+                              fmaf(gz, g.h, g.oz)));
+}
+
 template <int kGrid>
 #ifdef VS_RIGID_INLINE
 static __device__ __forceinline__
@@ -352,10 +368,43 @@ static __device__ __noinline__
 #endif
 float eval_rigid(const PocketDev& pk, const float4* ys, int N, const Mat3 R,
                                    float tx, float ty, float tz) {
-  // one atom per iteration, never unrolled: the loop body (~2 KB of SASS)
-  // stays resident in the ~6 KB L0 instruction cache next to the flex
-  // loops of the other warps (the 2x-unrolled body missed it and stalled
-  // on instruction fetch at every 128 B line)
+  if (kGrid) {
+    const GridDev& g = c_pk.grid;
+    const float ih = g.inv_h;
+    const float a00 = R.m00 * ih, a01 = R.m01 * ih, a02 = R.m02 * ih;
+    const float a10 = R.m10 * ih, a11 = R.m11 * ih, a12 = R.m12 * ih;
+    const float a20 = R.m20 * ih, a21 = R.m21 * ih, a22 = R.m22 * ih;
+    const float ux = (tx - g.ox) * ih, uy = (ty - g.oy) * ih, uz = (tz - g.oz) * ih;
+    const unsigned mx = static_cast<unsigned>(g.nx - 2), my = static_cast<unsigned>(g.ny - 2),
+                   mz = static_cast<unsigned>(g.nz - 2);
+    float ke = 0.0f, ko = 0.0f;
+#pragma unroll 1
+    for (int i = 0; i < N; ++i) {
+      const float4 a = ys[i];
+      const float gx = fmaf(a00, a.x, fmaf(a01, a.y, fmaf(a02, a.z, ux)));
+      const float gy = fmaf(a10, a.x, fmaf(a11, a.y, fmaf(a12, a.z, uy)));
+      const float gz = fmaf(a20, a.x, fmaf(a21, a.y, fmaf(a22, a.z, uz)));
+      const float fx = floorf(gx), fy = floorf(gy), fz = floorf(gz);
+      const int ix = static_cast<int>(fx), iy = static_cast<int>(fy), iz = static_cast<int>(fz);
+      float term;
+      if (static_cast<unsigned>(ix) <= mx && static_cast<unsigned>(iy) <= my &&
+          static_cast<unsigned>(iz) <= mz) {
+        const float4* c = g.key_c + 2 * ((iz * (g.ny - 1) + iy) * (g.nx - 1) + ix);
+        const float4 lo = __ldg(c), hi = __ldg(c + 1);
+        const float tx1 = gx - fx, ty1 = gy - fy, tz1 = gz - fz;
+        const float c00 = det_lerp(lo.x, lo.y, tx1), c10 = det_lerp(lo.z, lo.w, tx1);
+        const float c01 = det_lerp(hi.x, hi.y, tx1), c11 = det_lerp(hi.z, hi.w, tx1);
+        term = det_lerp(det_lerp(c00, c10, ty1), det_lerp(c01, c11, ty1), tz1);
+      } else {
+        term = off_grid_term(gx, gy, gz);
+      }
+      if (i & 1)
+        ko = ko + term;
+      else
+        ke = ke + term;
+    }
+    return ke + ko;
+  }
   float fe = 0.0f, fo = 0.0f, we = 0.0f, wo = 0.0f;
 #pragma unroll 1
   for (int i = 0; i < N; ++i) {

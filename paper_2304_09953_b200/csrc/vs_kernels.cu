@@ -8,7 +8,8 @@
 //                      atomic counter (LPT order from the packer).
 //   vs_rescore_kernel  K3a  geometric_score / rescore of given poses.
 //   vs_grid_kernel     N1   pocket grid maps (steric / hbond / lipophilic),
-//   vs_pack_kernel          + corner-packed cells for one-sector lookups.
+//   vs_pack_kernel          + the sweep-key map and corner-packed cells for
+//                           one-sector lookups.
 //   vs_topk_kernel     K4b  block-bitonic tournament top-k over u64 keys.
 //
 // Ligand records are staged into shared memory with one-dimensional TMA
@@ -151,7 +152,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 
 // ============================================================ grid kernels
 __global__ void vs_grid_kernel(const PocketDev pk, float* __restrict__ steric,
-                               float* __restrict__ hbond, float* __restrict__ lipo) {
+                               float* __restrict__ hbond, float* __restrict__ lipo,
+                               float* __restrict__ key) {
   const GridDev& g = pk.grid;
   const long n = static_cast<long>(g.nx) * g.ny * g.nz;
   for (long id = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; id < n;
@@ -165,6 +167,7 @@ __global__ void vs_grid_kernel(const PocketDev pk, float* __restrict__ steric,
     steric[id] = site_sum(pk.sites, pk.n_steric, x, y, z);
     hbond[id] = site_sum(pk.sites + pk.n_steric, pk.n_hbond, x, y, z);
     lipo[id] = site_sum(pk.sites + pk.n_steric + pk.n_hbond, pk.n_lipo, x, y, z);
+    key[id] = fmaf(-pk.lam, wall_of(pk, x, y, z), steric[id]);
   }
 }
 
@@ -294,18 +297,19 @@ cudaError_t launch_rescore(bool grid, int blocks, size_t smem, cudaStream_t st, 
 }
 
 cudaError_t launch_grid(cudaStream_t st, const PocketDev& pk, float* steric, float* hb,
-                        float* lipo, float4* cells) {
+                        float* lipo, float* key, float4* cells) {
   const GridDev& g = pk.grid;
   const long n = static_cast<long>(g.nx) * g.ny * g.nz;
   int blocks = static_cast<int>((n + 255) / 256);
   if (blocks > 148 * 64) blocks = 148 * 64;
-  vs_grid_kernel<<<blocks, 256, 0, st>>>(pk, steric, hb, lipo);
+  vs_grid_kernel<<<blocks, 256, 0, st>>>(pk, steric, hb, lipo, key);
   const long nc = static_cast<long>(g.nx - 1) * (g.ny - 1) * (g.nz - 1);
   int cb = static_cast<int>((nc + 255) / 256);
   if (cb > 148 * 64) cb = 148 * 64;
   vs_pack_kernel<<<cb, 256, 0, st>>>(g, steric, cells);
   vs_pack_kernel<<<cb, 256, 0, st>>>(g, hb, cells + 2 * nc);
   vs_pack_kernel<<<cb, 256, 0, st>>>(g, lipo, cells + 4 * nc);
+  vs_pack_kernel<<<cb, 256, 0, st>>>(g, key, cells + 6 * nc);
   return cudaGetLastError();
 }
 

@@ -31,7 +31,7 @@ cudaError_t launch_rescore(bool grid, int blocks, size_t smem, cudaStream_t st, 
                            const float4* pq, const float* ptors, int nmax, int tmax, int mvmax,
                            float* geo, float* resc);
 cudaError_t launch_grid(cudaStream_t st, const PocketDev& pk, float* steric, float* hb,
-                        float* lipo, float4* cells);
+                        float* lipo, float* key, float4* cells);
 int topk_chunk();
 double measure_peak(int kind, int sms);
 cudaError_t launch_topk(cudaStream_t st, const unsigned long long* in, long n,
@@ -462,8 +462,8 @@ int vs_set_pocket(vs_handle* h, const vs_pocket* p, double spacing, double pad) 
       *dims[c] = static_cast<int>(std::ceil((p->hi[c] - p->lo[c] + 2.0 * pad) / spacing)) + 1;
     const size_t nodes = static_cast<size_t>(g.nx) * g.ny * g.nz;
     const size_t cells = static_cast<size_t>(g.nx - 1) * (g.ny - 1) * (g.nz - 1);
-    const size_t node_bytes = align16z(3 * nodes * sizeof(float));
-    VS_CUDA(h, h->d_maps.ensure(node_bytes + 3 * cells * 2 * sizeof(float4)));
+    const size_t node_bytes = align16z(4 * nodes * sizeof(float));
+    VS_CUDA(h, h->d_maps.ensure(node_bytes + 4 * cells * 2 * sizeof(float4)));
     float* m = h->d_maps.as<float>();
     float4* c = reinterpret_cast<float4*>(static_cast<char*>(h->d_maps.p) + node_bytes);
     g.steric = m;
@@ -472,8 +472,10 @@ int vs_set_pocket(vs_handle* h, const vs_pocket* p, double spacing, double pad) 
     g.steric_c = c;
     g.hbond_c = c + 2 * cells;
     g.lipo_c = c + 4 * cells;
-    VS_CUDA(h, launch_grid(st, pk, m, m + nodes, m + 2 * nodes, c));
-    h->launches += 4;
+    g.key = m + 3 * nodes;
+    g.key_c = c + 6 * cells;
+    VS_CUDA(h, launch_grid(st, pk, m, m + nodes, m + 2 * nodes, m + 3 * nodes, c));
+    h->launches += 5;
     pk.grid_mode = 1;
     h->gdims[0] = g.nx;
     h->gdims[1] = g.ny;

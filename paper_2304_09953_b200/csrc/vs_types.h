@@ -31,6 +31,9 @@ struct GridDev {
   const float4* steric_c;
   const float4* hbond_c;
   const float4* lipo_c;
+  // sweep-key map K = steric - lam * wall at the nodes (SWEEP_V1.md §2.3)
+  const float* key;
+  const float4* key_c;
 };
 
 struct PocketDev {
