@@ -465,7 +465,8 @@ static float score_state(const vso_pocket* p, const lig_t* L, const double* y, c
 
 /* sweep key (SWEEP_V1.md §2.3): grid mode works in grid coordinates,
  * g = (R/h) y + (t - o)/h, and interpolates the key map K = S - lam W; an
- * atom off the grid scores -lam * wall at x = g h + o.  Analytic mode:
+ * atom off the grid scores the linear wall -lam * 10 (r - w) at x = g h + o
+ * (the wall softplus there is its argument to ~1e-11).  Analytic mode:
  * F - lam W over the FP32 state copy.  Parity sums over atoms. */
 static float rigid_key(const vso_pocket* p, const lig_t* L, const float* y, const mat3* R,
                        const float* t) {
@@ -492,9 +493,12 @@ static float rigid_key(const vso_pocket* p, const lig_t* L, const float* y, cons
         float c01 = lerp(b[sxy], b[sxy + 1], tx), c11 = lerp(b[sxy + sx], b[sxy + sx + 1], tx);
         term = lerp(lerp(c00, c10, ty), lerp(c01, c11, ty), tz);
       } else {
-        const float xw[3] = {fmaf(g[0], p->h, p->gx0), fmaf(g[1], p->h, p->gy0),
-                             fmaf(g[2], p->h, p->gz0)};
-        term = -(p->lam * wall(p, xw));
+        /* linear wall: the softplus at z = 10 (r - w) >= 10 (r + pad) is z */
+        const float x = fmaf(g[0], p->h, p->gx0), y = fmaf(g[1], p->h, p->gy0);
+        const float z = fmaf(g[2], p->h, p->gz0);
+        const float w = fminf(fminf(fminf(x - p->lo[0], p->hi[0] - x), fminf(y - p->lo[1], p->hi[1] - y)),
+                              fminf(z - p->lo[2], p->hi[2] - z));
+        term = -(p->lam * ((p->r - w) * 10.0f));
       }
       K[i & 1] = K[i & 1] + term;
     }

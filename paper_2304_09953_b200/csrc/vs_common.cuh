@@ -353,11 +353,16 @@ static __device__ __noinline__ void pose_coop(const WarpSmem& s, int N, const Ma
 //  grid:     sum of the key map K = S - lam W interpolated at the atom, the
 //            pose composed with the grid frame (g = (R/h) y + (t - o)/h) so
 //            one FMA chain yields cell coordinates; atoms off the grid score
-//            -lam * wall at x = g h + o (cold, out of line).
-static __device__ __noinline__ float off_grid_term(float gx, float gy, float gz) {
+//            the linear wall -lam * 10 (r - w) at x = g h + o.
+__device__ __forceinline__ float off_grid_term(float gx, float gy, float gz) {
+  // -lam * 10 (r - w), w the (negative) signed distance to the box: the wall
+  // softplus at z = 10 (r - w) >= 10 (r + pad) is z to ~1e-11 there
   const GridDev& g = c_pk.grid;
-  return -(c_pk.lam * wall_of(c_pk, fmaf(gx, g.h, g.ox), fmaf(gy, g.h, g.oy),
-                              fmaf(gz, g.h, g.oz)));
+  const float x = fmaf(gx, g.h, g.ox), y = fmaf(gy, g.h, g.oy), z = fmaf(gz, g.h, g.oz);
+  const float w = fminf(fminf(fminf(x - c_pk.lo[0], c_pk.hi[0] - x),
+                              fminf(y - c_pk.lo[1], c_pk.hi[1] - y)),
+                        fminf(z - c_pk.lo[2], c_pk.hi[2] - z));
+  return -(c_pk.lam * ((c_pk.r - w) * 10.0f));
 }
 
 template <int kGrid>
@@ -378,6 +383,45 @@ float eval_rigid(const PocketDev& pk, const float4* ys, int N, const Mat3 R,
     const unsigned mx = static_cast<unsigned>(g.nx - 2), my = static_cast<unsigned>(g.ny - 2),
                    mz = static_cast<unsigned>(g.nz - 2);
     float ke = 0.0f, ko = 0.0f;
+#ifdef VS_KEY_U2
+    // two atoms per iteration (even -> ke, odd -> ko): both lookups are in
+    // flight before either is consumed; a missing odd tail atom reads atom
+    // i again and is dropped
+    auto cell = [&](const float4 a, float& gx, float& gy, float& gz, float& tx1, float& ty1,
+                    float& tz1, bool& in) {
+      gx = fmaf(a00, a.x, fmaf(a01, a.y, fmaf(a02, a.z, ux)));
+      gy = fmaf(a10, a.x, fmaf(a11, a.y, fmaf(a12, a.z, uy)));
+      gz = fmaf(a20, a.x, fmaf(a21, a.y, fmaf(a22, a.z, uz)));
+      const float fx = floorf(gx), fy = floorf(gy), fz = floorf(gz);
+      const int ix = static_cast<int>(fx), iy = static_cast<int>(fy), iz = static_cast<int>(fz);
+      in = static_cast<unsigned>(ix) <= mx && static_cast<unsigned>(iy) <= my &&
+           static_cast<unsigned>(iz) <= mz;
+      tx1 = gx - fx;
+      ty1 = gy - fy;
+      tz1 = gz - fz;
+      return g.key_c + 2 * (in ? (iz * (g.ny - 1) + iy) * (g.nx - 1) + ix : 0);
+    };
+    auto interp = [](const float4 lo, const float4 hi, float tx1, float ty1, float tz1) {
+      const float c00 = det_lerp(lo.x, lo.y, tx1), c10 = det_lerp(lo.z, lo.w, tx1);
+      const float c01 = det_lerp(hi.x, hi.y, tx1), c11 = det_lerp(hi.z, hi.w, tx1);
+      return det_lerp(det_lerp(c00, c10, ty1), det_lerp(c01, c11, ty1), tz1);
+    };
+#pragma unroll 1
+    for (int i = 0; i < N; i += 2) {
+      const bool two = i + 1 < N;
+      float gx0, gy0, gz0, tx0, ty0, tz0, gx1, gy1, gz1, tx1, ty1, tz1;
+      bool in0, in1;
+      const float4* c0 = cell(ys[i], gx0, gy0, gz0, tx0, ty0, tz0, in0);
+      const float4* c1 = cell(ys[two ? i + 1 : i], gx1, gy1, gz1, tx1, ty1, tz1, in1);
+      const float4 lo0 = __ldg(c0), hi0 = __ldg(c0 + 1), lo1 = __ldg(c1), hi1 = __ldg(c1 + 1);
+      const float t0 = in0 ? interp(lo0, hi0, tx0, ty0, tz0) : off_grid_term(gx0, gy0, gz0);
+      ke = ke + t0;
+      if (two) {
+        const float t1 = in1 ? interp(lo1, hi1, tx1, ty1, tz1) : off_grid_term(gx1, gy1, gz1);
+        ko = ko + t1;
+      }
+    }
+#else
 #pragma unroll 1
     for (int i = 0; i < N; ++i) {
       const float4 a = ys[i];
@@ -403,6 +447,7 @@ float eval_rigid(const PocketDev& pk, const float4* ys, int N, const Mat3 R,
       else
         ke = ke + term;
     }
+#endif
     return ke + ko;
   }
   float fe = 0.0f, fo = 0.0f, we = 0.0f, wo = 0.0f;
