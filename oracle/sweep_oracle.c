@@ -364,6 +364,7 @@ typedef struct {
   double* y0;  /* N*3, FP64 conformer */
   int* cls;
   int *a, *b, *cnt, *mstart;
+  double* inv_len; /* 1 / |y0[b] - y0[a]| per torsion (0 for a degenerate axis) */
   const int* moving;
 } lig_t;
 
@@ -372,10 +373,10 @@ static void chain(const lig_t* L, const float* th, double* y) {
   memcpy(y, L->y0, sizeof(double) * 3 * (size_t)L->N);
   for (int j = 0; j < L->T; ++j) {
     double o[3] = {y[3 * L->a[j]], y[3 * L->a[j] + 1], y[3 * L->a[j] + 2]};
-    double dx = y[3 * L->b[j]] - o[0], dy = y[3 * L->b[j] + 1] - o[1], dz = y[3 * L->b[j] + 2] - o[2];
-    double n = sqrt(n2d(dx, dy, dz));
-    double ux = 0.0, uy = 0.0, uz = 0.0;
-    if (n > 0.0) { ux = dx / n; uy = dy / n; uz = dz / n; }
+    /* unit axis = (b - o) / |axis of the conformer| (invariant under the chain) */
+    const double il = L->inv_len[j];
+    double ux = (y[3 * L->b[j]] - o[0]) * il, uy = (y[3 * L->b[j] + 1] - o[1]) * il;
+    double uz = (y[3 * L->b[j] + 2] - o[2]) * il;
     double s, c;
     sincos_d(0.5 * (double)th[j], &s, &c);
     mat3d M = quat_mat_d(c, ux * s, uy * s, uz * s);
@@ -427,15 +428,14 @@ static float butterfly(const float* in) {
 
 /* flex move rotation: about axis o->b by th_new - th_old (FP64), half angle
  * folded into [-pi/2, pi/2] (q -> -q leaves the matrix unchanged) */
-static mat3d flex_mat(const double* o, const double* b, float th_new, float th_old) {
+static mat3d flex_mat(const double* o, const double* b, float th_new, float th_old, double inv_len) {
   double dx = b[0] - o[0], dy = b[1] - o[1], dz = b[2] - o[2];
-  double n = sqrt(n2d(dx, dy, dz));
   double hh = 0.5 * ((double)th_new - (double)th_old);
   if (hh > 1.57079632679489661923) hh = hh - PI_D;
   else if (hh < -1.57079632679489661923) hh = hh + PI_D;
   double s, c;
   sincos_d(hh, &s, &c);
-  double ks = n > 0.0 ? s / n : 0.0;
+  double ks = s * inv_len;
   return quat_mat_d(c, dx * ks, dy * ks, dz * ks);
 }
 
@@ -690,7 +690,7 @@ static void dock_one(const vso_pocket* p, const lig_t* L, uint64_t seed, uint32_
           const float tho = th[j];
           thn = tho;
           if (a > 0) { thn = tho + (float)a * step; if (thn >= PI_F) thn = thn - TWO_PI_F; }
-          mat3d M = flex_mat(&y[3 * L->a[j]], &y[3 * L->b[j]], thn, tho);
+          mat3d M = flex_mat(&y[3 * L->a[j]], &y[3 * L->b[j]], thn, tho, L->inv_len[j]);
           const double* o = &y[3 * L->a[j]];
           for (int q2 = 0; q2 < m; ++q2) {
             const int idx = mv[q2], hh = q2 & 1;
@@ -710,7 +710,7 @@ static void dock_one(const vso_pocket* p, const lig_t* L, uint64_t seed, uint32_
       S = bestS;
       if (do_flex && best_a != 0) {
         /* move the state to the winner (skipped when candidate 0 wins) */
-        mat3d M = flex_mat(&y[3 * L->a[j]], &y[3 * L->b[j]], best_th, th[j]);
+        mat3d M = flex_mat(&y[3 * L->a[j]], &y[3 * L->b[j]], best_th, th[j], L->inv_len[j]);
         const double o[3] = {y[3 * L->a[j]], y[3 * L->a[j] + 1], y[3 * L->a[j] + 2]};
         for (int q2 = 0; q2 < m; ++q2) {
           const int idx = mv[q2];
@@ -805,16 +805,21 @@ static void make_lig(const job_t* J, int i, lig_t* L) {
   L->b = (int*)malloc(sizeof(int) * (size_t)T);
   L->cnt = (int*)malloc(sizeof(int) * (size_t)T);
   L->mstart = (int*)malloc(sizeof(int) * (size_t)T);
+  L->inv_len = (double*)malloc(sizeof(double) * (size_t)T);
   int ms = 0;
   for (int j = 0; j < L->T; ++j) {
     long k = J->tors_off[i] + j;
     L->a[j] = lib->axis_a[k]; L->b[j] = lib->axis_b[k]; L->cnt[j] = lib->moving_count[k];
     L->mstart[j] = ms; ms += L->cnt[j];
+    const double* ya = &L->y0[3 * L->a[j]];
+    const double* yb = &L->y0[3 * L->b[j]];
+    const double n = sqrt(n2d(yb[0] - ya[0], yb[1] - ya[1], yb[2] - ya[2]));
+    L->inv_len[j] = n > 0.0 ? 1.0 / n : 0.0;
   }
   L->moving = lib->moving + J->mov_off[i];
 }
 
-static void free_lig(lig_t* L) { free(L->y0); free(L->cls); free(L->a); free(L->b); free(L->cnt); free(L->mstart); }
+static void free_lig(lig_t* L) { free(L->y0); free(L->cls); free(L->a); free(L->b); free(L->cnt); free(L->mstart); free(L->inv_len); }
 
 static void* worker(void* arg) {
   job_t* J = (job_t*)arg;

@@ -245,7 +245,9 @@ struct WarpSmem {
   int4* ax;       // torsion axes
   float* theta;   // state torsions
   uint8_t* mov;   // moving lists
-  unsigned* mask; // moving set of the current flex axis (4 words)
+  unsigned* mask; // all-zero moving set (4 words; rigid ligands)
+  unsigned* tmask;  // moving set of each torsion (4 words per torsion)
+  double* axl;      // 1 / |y0[b_j] - y0[a_j]| per torsion (0 for a degenerate axis)
   double* col;    // rescore kernel only: pose columns [i][c][16], FP64
   float* kscore;  // kept-pose scores
   int* kinv;      // rank -> kept index
@@ -265,6 +267,8 @@ __host__ __device__ inline size_t warp_smem_bytes(int nmax, int tmax, int mvmax,
   b += align16(4 * size_t(tmax));             // theta
   b += align16(size_t(mvmax));                // mov
   b += 16;                                    // mask
+  b += 16 * size_t(tmax);                     // tmask
+  b += 8 * size_t(tmax);                      // axl
   if (cols) b += 8 * size_t(nmax) * 3 * kCand;
   b += 3 * 4 * kMaxRestarts;                  // kscore, kinv, kresc
   b += 16;                                    // mbarrier
@@ -285,6 +289,8 @@ __device__ inline WarpSmem carve(unsigned char* base, int nmax, int tmax, int mv
   s.theta = reinterpret_cast<float*>(base + o); o += align16(4 * size_t(tmax));
   s.mov = base + o; o += align16(size_t(mvmax));
   s.mask = reinterpret_cast<unsigned*>(base + o); o += 16;
+  s.tmask = reinterpret_cast<unsigned*>(base + o); o += 16 * size_t(tmax);
+  s.axl = reinterpret_cast<double*>(base + o); o += 8 * size_t(tmax);
   s.col = nullptr;
   if (cols) {
     s.col = reinterpret_cast<double*>(base + o);
@@ -313,6 +319,27 @@ __device__ inline void stage_ligand(const LibDev& lib, int lig, const WarpSmem& 
   }
   mbar_wait(s.bar, phase);
   phase ^= 1u;
+  // per-ligand torsion tables: moving-set bitmasks and inverse axis lengths
+  // of the conformer (the axis length is invariant under the torsion chain)
+  const int T = meta.w;
+  if (lane < 4) s.mask[lane] = 0u;
+  for (int e = lane; e < 4 * T; e += 32) {
+    const int j = e >> 2, w = e & 3;
+    const int4 a = s.ax[j];
+    unsigned bits = 0u;
+    for (int q = 0; q < a.w; ++q) {
+      const int idx = s.mov[a.z + q];
+      if ((idx >> 5) == w) bits |= 1u << (idx & 31);
+    }
+    s.tmask[e] = bits;
+  }
+  for (int j = lane; j < T; j += 32) {
+    const int4 a = s.ax[j];
+    const double4 o = s.y0[a.x], b = s.y0[a.y];
+    const double n = sqrt(det_norm2_d(b.x - o.x, b.y - o.y, b.z - o.z));
+    s.axl[j] = n > 0.0 ? 1.0 / n : 0.0;
+  }
+  __syncwarp();
 }
 
 // s.ys = y0 with torsions [0, T) at s.theta (dock.cpp:54-63); lanes over
@@ -323,7 +350,7 @@ static __device__ __noinline__ void chain_coop(const WarpSmem& s, int N, int T, 
   for (int j = 0; j < T; ++j) {
     const int4 a = s.ax[j];
     const double4 o = s.ys[a.x], b = s.ys[a.y];
-    const Mat3d M = det_torsion_mat_d(o.x, o.y, o.z, b.x, b.y, b.z, s.theta[j]);
+    const Mat3d M = det_torsion_mat_d(o.x, o.y, o.z, b.x, b.y, b.z, s.theta[j], s.axl[j]);
     for (int m = lane; m < a.w; m += 32) {
       const int idx = s.mov[a.z + m];
       double4 v = s.ys[idx];
@@ -541,18 +568,17 @@ static __device__ __noinline__ void draw_start(const PocketDev& pk, unsigned lon
 }
 
 // Rotation of the flex move: moving_j rotated about the state's axis j by
-// delta = th_new - th_old (FP64 of two FP32 angles).  The half angle is
-// folded into [-pi/2, pi/2] by q -> -q (same matrix).
+// delta = th_new - th_old (FP64 of two FP32 angles), unit axis d * inv_len.
+// The half angle is folded into [-pi/2, pi/2] by q -> -q (same matrix).
 __device__ __forceinline__ Mat3d flex_mat(double ox, double oy, double oz, double bx, double by,
-                                          double bz, float th_new, float th_old) {
+                                          double bz, float th_new, float th_old, double inv_len) {
   const double dx = bx - ox, dy = by - oy, dz = bz - oz;
-  const double n = sqrt(det_norm2_d(dx, dy, dz));
   double hh = 0.5 * (static_cast<double>(th_new) - static_cast<double>(th_old));
   if (hh > kHalfPiD) hh = hh - kPiD;
   else if (hh < -kHalfPiD) hh = hh + kPiD;
   double s, c;
   det_sincos_d(hh, &s, &c);
-  const double ks = n > 0.0 ? s / n : 0.0;
+  const double ks = s * inv_len;
   return det_quat_mat_d(c, dx * ks, dy * ks, dz * ks);
 }
 

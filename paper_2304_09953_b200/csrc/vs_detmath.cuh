@@ -251,17 +251,12 @@ __device__ __forceinline__ Mat3d det_pose_mat_d(float qw, float qx, float qy, fl
   return det_quat_mat_d(w / n, x / n, y / n, z / n);
 }
 
-// One torsion step (dock.cpp:57-59) in FP64: axis o -> b, FP32 angle th.
+// One torsion step (dock.cpp:57-59) in FP64: axis o -> b with unit vector
+// (b - o) * inv_len (inv_len = 1 / |axis| of the conformer), FP32 angle th.
 __device__ __forceinline__ Mat3d det_torsion_mat_d(double ox, double oy, double oz, double bx,
-                                                   double by, double bz, float th) {
-  const double dx = bx - ox, dy = by - oy, dz = bz - oz;
-  const double n = sqrt(det_norm2_d(dx, dy, dz));
-  double ux = 0.0, uy = 0.0, uz = 0.0;
-  if (n > 0.0) {
-    ux = dx / n;
-    uy = dy / n;
-    uz = dz / n;
-  }
+                                                   double by, double bz, float th,
+                                                   double inv_len) {
+  const double ux = (bx - ox) * inv_len, uy = (by - oy) * inv_len, uz = (bz - oz) * inv_len;
   double s, c;
   det_sincos_d(0.5 * static_cast<double>(th), &s, &c);
   return det_quat_mat_d(c, ux * s, uy * s, uz * s);

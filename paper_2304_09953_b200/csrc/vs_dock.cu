@@ -202,18 +202,10 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
     const int j = do_flex ? st % T : -1;
     const int4 ax = do_flex ? s.ax[j] : make_int4(0, 0, 0, 0);
     const int m = ax.w;
-    if (lane < 4) {
-      unsigned wd = 0;
-      for (int q2 = 0; q2 < m; ++q2) {
-        const int idx = s.mov[ax.z + q2];
-        if ((idx >> 5) == lane) wd |= 1u << (idx & 31);
-      }
-      s.mask[lane] = wd;
-    }
-    __syncwarp();
+    const unsigned* mk = do_flex ? s.tmask + 4 * j : s.mask;
     float fb = 0.0f, wb = 0.0f, pb = 0.0f;
     for (int i = lane; i < N; i += 32) {
-      if (!in_mask(s.mask, i)) {
+      if (!in_mask(mk, i)) {
         fb = fb + s.fa[i];
         wb = wb + s.wa[i];
       }
@@ -228,7 +220,7 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
         ++i;
       }
       while (i < N - 1) {
-        if (in_mask(s.mask, i) == in_mask(s.mask, k)) {
+        if (in_mask(mk, i) == in_mask(mk, k)) {
           const double4 yi = s.ys[i], yk = s.ys[k];
           pb = pb + pair_term_d(pk, yi.x - yk.x, yi.y - yk.y, yi.z - yk.z, nact);
         }
@@ -254,7 +246,7 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
         th_new = v;
       }
       const double4 o = s.ys[ax.x], b = s.ys[ax.y];
-      const Mat3d M = flex_mat(o.x, o.y, o.z, b.x, b.y, b.z, th_new, th_old);
+      const Mat3d M = flex_mat(o.x, o.y, o.z, b.x, b.y, b.z, th_new, th_old, s.axl[j]);
       // partners: the atoms outside moving_j, walked as set bits of the
       // complemented mask (ascending k, same trip count in both halves)
       for (int q2 = h; q2 < m; q2 += 2) {
@@ -266,7 +258,7 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
         fm = fm + fi;
         wm = wm + wi;
         for (int wd = 0; wd < W; ++wd) {
-          unsigned b2 = ~s.mask[wd];
+          unsigned b2 = ~mk[wd];
           if (wd == W - 1 && (N & 31)) b2 &= (1u << (N & 31)) - 1u;
           for (; b2; b2 &= b2 - 1u) {
             const double4 yk = s.ys[wd * 32 + __ffs(b2) - 1];
@@ -294,7 +286,7 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
       const float th_old = s.theta[j];
       const float th_win = __shfl_sync(kFull, th_new, ai);
       const double4 o = s.ys[ax.x], b = s.ys[ax.y];
-      const Mat3d M = flex_mat(o.x, o.y, o.z, b.x, b.y, b.z, th_win, th_old);
+      const Mat3d M = flex_mat(o.x, o.y, o.z, b.x, b.y, b.z, th_win, th_old, s.axl[j]);
       __syncwarp();
       for (int q2 = lane; q2 < m; q2 += 32) {
         const int idx = s.mov[ax.z + q2];

@@ -55,7 +55,7 @@ __device__ inline void chain_pose(const WarpSmem& s, int N, int T, int a, int h,
       const double ox = cold(col, ax.x, 0, a), oy = cold(col, ax.x, 1, a),
                    oz = cold(col, ax.x, 2, a);
       const Mat3d M = det_torsion_mat_d(ox, oy, oz, cold(col, ax.y, 0, a), cold(col, ax.y, 1, a),
-                                        cold(col, ax.y, 2, a), th[k]);
+                                        cold(col, ax.y, 2, a), th[k], s.axl[k]);
       for (int m = h; m < ax.w; m += 2) {
         const int idx = s.mov[ax.z + m];
         double vx, vy, vz;
