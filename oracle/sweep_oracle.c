@@ -131,9 +131,10 @@ static void apply(const mat3* R, const float* v, const float* t, float* o) {
   o[0] = x; o[1] = y; o[2] = z;
 }
 
-static void qnormalize(float* q) { /* geom.hpp:167-170 */
+static void qnormalize(float* q) { /* geom.hpp:167-170, one reciprocal */
   float n = sqrtf(fmaf(q[3], q[3], fmaf(q[2], q[2], fmaf(q[1], q[1], q[0] * q[0]))));
-  q[0] = q[0] / n; q[1] = q[1] / n; q[2] = q[2] / n; q[3] = q[3] / n;
+  float inv = 1.0f / n;
+  q[0] = q[0] * inv; q[1] = q[1] * inv; q[2] = q[2] * inv; q[3] = q[3] * inv;
 }
 
 static void qmul(const float* r, const float* q, float* o) {
@@ -202,8 +203,8 @@ static void apply_d(const mat3d* R, const double* v, const double* t, double* o)
 /* rigid rotation of an FP32 quaternion normalized in FP64 (geom.hpp:167) */
 static mat3d pose_mat_d(const float* qf) {
   double w = qf[0], x = qf[1], y = qf[2], z = qf[3];
-  double n = sqrt(fma(z, z, fma(y, y, fma(x, x, w * w))));
-  return quat_mat_d(w / n, x / n, y / n, z / n);
+  double inv = 1.0 / sqrt(fma(z, z, fma(y, y, fma(x, x, w * w))));
+  return quat_mat_d(w * inv, x * inv, y * inv, z * inv);
 }
 
 /* ----------------------------------------------------------- pocket --- */

@@ -140,13 +140,13 @@ __device__ __forceinline__ void det_apply(const Mat3& R, float vx, float vy, flo
   *oz = fmaf(R.m20, vx, fmaf(R.m21, vy, fmaf(R.m22, vz, tz)));
 }
 
-// q / |q| (Quat::normalized, geom.hpp:167-170)
+// q / |q| (Quat::normalized, geom.hpp:167-170) as q * (1 / |q|)
 __device__ __forceinline__ void det_quat_normalize(float* w, float* x, float* y, float* z) {
-  const float n = sqrtf(fmaf(*z, *z, fmaf(*y, *y, fmaf(*x, *x, (*w) * (*w)))));
-  *w = *w / n;
-  *x = *x / n;
-  *y = *y / n;
-  *z = *z / n;
+  const float inv = 1.0f / sqrtf(fmaf(*z, *z, fmaf(*y, *y, fmaf(*x, *x, (*w) * (*w)))));
+  *w = *w * inv;
+  *x = *x * inv;
+  *y = *y * inv;
+  *z = *z * inv;
 }
 
 // Hamilton product r (x) q
@@ -247,8 +247,8 @@ __device__ __forceinline__ void det_apply_d(const Mat3d& R, double vx, double vy
 // Quat::normalized (geom.hpp:167-170) does.
 __device__ __forceinline__ Mat3d det_pose_mat_d(float qw, float qx, float qy, float qz) {
   double w = qw, x = qx, y = qy, z = qz;
-  const double n = sqrt(fma(z, z, fma(y, y, fma(x, x, w * w))));
-  return det_quat_mat_d(w / n, x / n, y / n, z / n);
+  const double inv = 1.0 / sqrt(fma(z, z, fma(y, y, fma(x, x, w * w))));
+  return det_quat_mat_d(w * inv, x * inv, y * inv, z * inv);
 }
 
 // One torsion step (dock.cpp:57-59) in FP64: axis o -> b with unit vector
