@@ -3,16 +3,19 @@
 // and top-k key — one warp per ligand, persistent warps pulling ligands from
 // an atomic counter over one global LPT order (largest ligands first).
 //
-// The per-restart work is split into non-inlined phases (start, sweep, flex,
-// keep, finish): the fully inlined kernel was ~126 KB of SASS and stalled on
-// instruction fetch; the phases keep each hot loop small and shared.
+// The per-restart phases (start, sweep, flex, keep, finish) are inlined into
+// the kernel (out-of-line phases paid ABI register saves on every call, and
+// that local-memory traffic cost more than the call-free code's size); the
+// hot inner loops are kept small instead (sweep key: ~120 instructions,
+// never unrolled), because the SM's ~6 KB L0 instruction cache is shared by
+// warps in different phases.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include "vs_common.cuh"
 
 #ifndef VS_PHASE
-#define VS_PHASE __noinline__  // phases as separate functions (see header comment)
+#define VS_PHASE __forceinline__  // see header comment
 #endif
 
 namespace vs {
