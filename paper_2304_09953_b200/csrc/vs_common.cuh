@@ -89,6 +89,15 @@ __device__ __forceinline__ float site_sum(const SiteF* __restrict__ s, int n, fl
   return acc;
 }
 
+// One corner-packed cell (32 B, one sector) in a single 256-bit load
+// (LDG.E.ENL2.256 on sm_100a): one L1 request per lookup instead of two.
+__device__ __forceinline__ void ldg_cell(const float4* c, float4& lo, float4& hi) {
+  asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(lo.x), "=f"(lo.y), "=f"(lo.z), "=f"(lo.w), "=f"(hi.x), "=f"(hi.y),
+                 "=f"(hi.z), "=f"(hi.w)
+               : "l"(c));
+}
+
 // One trilinear lookup split in two halves so that callers can issue the
 // next lookup's loads before consuming this one.
 struct TriCell {
@@ -115,9 +124,7 @@ __device__ __forceinline__ TriCell tri_issue(const GridDev& g, const float4* __r
   c.ty = gy - fy;
   c.tz = gz - fz;
   const int cell = c.in ? (iz * (g.ny - 1) + iy) * (g.nx - 1) + ix : 0;
-  const float4* p = cells + 2 * cell;
-  c.lo = __ldg(p);
-  c.hi = __ldg(p + 1);
+  ldg_cell(cells + 2 * cell, c.lo, c.hi);
   return c;
 }
 
@@ -257,49 +264,75 @@ struct WarpSmem {
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-__host__ __device__ inline size_t warp_smem_bytes(int nmax, int tmax, int mvmax, bool cols) {
-  size_t b = 0;
-  b += 2 * 32 * size_t(nmax);                 // y0, ys
-  b += 96;                                    // pose
-  b += 2 * 16 * size_t(nmax);                 // ysf, xf
-  b += 2 * align16(4 * size_t(nmax));         // fa, wa
-  b += 16 * size_t(tmax);                     // ax
-  b += align16(4 * size_t(tmax));             // theta
-  b += align16(size_t(mvmax));                // mov
-  b += 16;                                    // mask
-  b += 16 * size_t(tmax);                     // tmask
-  b += 8 * size_t(tmax);                      // axl
-  if (cols) b += 8 * size_t(nmax) * 3 * kCand;
-  b += 3 * 4 * kMaxRestarts;                  // kscore, kinv, kresc
-  b += 16;                                    // mbarrier
-  return (b + 127) & ~size_t(127);  // warp bases stay 128 B aligned
+// Layout parts: a kernel carves only the arrays its phases touch.
+enum : int {
+  kLayLig = 1,     // y0, ax, mov, mask, tmask, axl (ligand topology)
+  kLayState = 2,   // ys (FP64 state), theta
+  kLaySweep = 4,   // ysf
+  kLayPosed = 8,   // xf
+  kLayFlex = 16,   // pose, fa, wa
+  kLayKept = 32,   // kscore, kinv, kresc
+  kLayCols = 64,   // rescore pose columns
+  kLayAll = kLayLig | kLayState | kLaySweep | kLayPosed | kLayFlex | kLayKept,
+};
+
+// byte offsets of every part (0 size when absent), in carve order
+__host__ __device__ inline size_t warp_layout(int nmax, int tmax, int mvmax, int lay,
+                                              size_t* off) {
+  const size_t n = size_t(nmax), t = size_t(tmax);
+  const size_t sz[18] = {
+      (lay & kLayLig) ? 32 * n : 0,                 // 0 y0
+      (lay & kLayState) ? 32 * n : 0,               // 1 ys
+      (lay & kLayFlex) ? size_t(96) : 0,                    // 2 pose
+      (lay & kLaySweep) ? 16 * n : 0,               // 3 ysf
+      (lay & kLayPosed) ? 16 * n : 0,               // 4 xf
+      (lay & kLayFlex) ? align16(4 * n) : 0,        // 5 fa
+      (lay & kLayFlex) ? align16(4 * n) : 0,        // 6 wa
+      (lay & kLayLig) ? 16 * t : 0,                 // 7 ax
+      (lay & kLayState) ? align16(4 * t) : 0,       // 8 theta
+      (lay & kLayLig) ? align16(size_t(mvmax)) : 0, // 9 mov
+      (lay & kLayLig) ? size_t(16) : 0,                     // 10 mask
+      (lay & kLayLig) ? 16 * t : 0,                 // 11 tmask
+      (lay & kLayLig) ? align16(8 * t) : 0,         // 12 axl
+      (lay & kLayCols) ? 8 * n * 3 * kCand : 0,     // 13 col
+      (lay & kLayKept) ? size_t(4 * kMaxRestarts) : 0,      // 14 kscore
+      (lay & kLayKept) ? size_t(4 * kMaxRestarts) : 0,      // 15 kinv
+      (lay & kLayKept) ? size_t(4 * kMaxRestarts) : 0,      // 16 kresc
+      16};                                          // 17 mbarrier
+  size_t o = 0;
+  for (int k = 0; k < 18; ++k) {
+    if (off) off[k] = o;
+    o += sz[k];
+  }
+  return o;
 }
 
-__device__ inline WarpSmem carve(unsigned char* base, int nmax, int tmax, int mvmax, bool cols) {
+__host__ __device__ inline size_t warp_smem_bytes(int nmax, int tmax, int mvmax, int lay) {
+  return (warp_layout(nmax, tmax, mvmax, lay, nullptr) + 127) & ~size_t(127);  // 128 B bases
+}
+
+__device__ inline WarpSmem carve(unsigned char* base, int nmax, int tmax, int mvmax, int lay) {
+  size_t o[18];
+  warp_layout(nmax, tmax, mvmax, lay, o);
   WarpSmem s;
-  size_t o = 0;
-  s.y0 = reinterpret_cast<double4*>(base + o); o += 32 * size_t(nmax);
-  s.ys = reinterpret_cast<double4*>(base + o); o += 32 * size_t(nmax);
-  s.pose = reinterpret_cast<double*>(base + o); o += 96;
-  s.ysf = reinterpret_cast<float4*>(base + o); o += 16 * size_t(nmax);
-  s.xf = reinterpret_cast<float4*>(base + o); o += 16 * size_t(nmax);
-  s.fa = reinterpret_cast<float*>(base + o); o += align16(4 * size_t(nmax));
-  s.wa = reinterpret_cast<float*>(base + o); o += align16(4 * size_t(nmax));
-  s.ax = reinterpret_cast<int4*>(base + o); o += 16 * size_t(tmax);
-  s.theta = reinterpret_cast<float*>(base + o); o += align16(4 * size_t(tmax));
-  s.mov = base + o; o += align16(size_t(mvmax));
-  s.mask = reinterpret_cast<unsigned*>(base + o); o += 16;
-  s.tmask = reinterpret_cast<unsigned*>(base + o); o += 16 * size_t(tmax);
-  s.axl = reinterpret_cast<double*>(base + o); o += 8 * size_t(tmax);
-  s.col = nullptr;
-  if (cols) {
-    s.col = reinterpret_cast<double*>(base + o);
-    o += 8 * size_t(nmax) * 3 * kCand;
-  }
-  s.kscore = reinterpret_cast<float*>(base + o); o += 4 * kMaxRestarts;
-  s.kinv = reinterpret_cast<int*>(base + o); o += 4 * kMaxRestarts;
-  s.kresc = reinterpret_cast<float*>(base + o); o += 4 * kMaxRestarts;
-  s.bar = reinterpret_cast<uint64_t*>(base + o);
+  s.y0 = (lay & kLayLig) ? reinterpret_cast<double4*>(base + o[0]) : nullptr;
+  s.ys = (lay & kLayState) ? reinterpret_cast<double4*>(base + o[1]) : nullptr;
+  s.pose = (lay & kLayFlex) ? reinterpret_cast<double*>(base + o[2]) : nullptr;
+  s.ysf = (lay & kLaySweep) ? reinterpret_cast<float4*>(base + o[3]) : nullptr;
+  s.xf = (lay & kLayPosed) ? reinterpret_cast<float4*>(base + o[4]) : nullptr;
+  s.fa = (lay & kLayFlex) ? reinterpret_cast<float*>(base + o[5]) : nullptr;
+  s.wa = (lay & kLayFlex) ? reinterpret_cast<float*>(base + o[6]) : nullptr;
+  s.ax = (lay & kLayLig) ? reinterpret_cast<int4*>(base + o[7]) : nullptr;
+  s.theta = (lay & kLayState) ? reinterpret_cast<float*>(base + o[8]) : nullptr;
+  s.mov = (lay & kLayLig) ? base + o[9] : nullptr;
+  s.mask = (lay & kLayLig) ? reinterpret_cast<unsigned*>(base + o[10]) : nullptr;
+  s.tmask = (lay & kLayLig) ? reinterpret_cast<unsigned*>(base + o[11]) : nullptr;
+  s.axl = (lay & kLayLig) ? reinterpret_cast<double*>(base + o[12]) : nullptr;
+  s.col = (lay & kLayCols) ? reinterpret_cast<double*>(base + o[13]) : nullptr;
+  s.kscore = (lay & kLayKept) ? reinterpret_cast<float*>(base + o[14]) : nullptr;
+  s.kinv = (lay & kLayKept) ? reinterpret_cast<int*>(base + o[15]) : nullptr;
+  s.kresc = (lay & kLayKept) ? reinterpret_cast<float*>(base + o[16]) : nullptr;
+  s.bar = reinterpret_cast<uint64_t*>(base + o[17]);
   return s;
 }
 
@@ -393,13 +426,8 @@ __device__ __forceinline__ float off_grid_term(float gx, float gy, float gz) {
 }
 
 template <int kGrid>
-#ifdef VS_RIGID_INLINE
-static __device__ __forceinline__
-#else
-static __device__ __noinline__
-#endif
-float eval_rigid(const PocketDev& pk, const float4* ys, int N, const Mat3 R,
-                                   float tx, float ty, float tz) {
+static __device__ __forceinline__ float eval_key(const PocketDev& pk, const float4* ys, int N,
+                                                 const Mat3 R, float tx, float ty, float tz) {
   if (kGrid) {
     const GridDev& g = c_pk.grid;
     const float ih = g.inv_h;
@@ -460,8 +488,8 @@ float eval_rigid(const PocketDev& pk, const float4* ys, int N, const Mat3 R,
       float term;
       if (static_cast<unsigned>(ix) <= mx && static_cast<unsigned>(iy) <= my &&
           static_cast<unsigned>(iz) <= mz) {
-        const float4* c = g.key_c + 2 * ((iz * (g.ny - 1) + iy) * (g.nx - 1) + ix);
-        const float4 lo = __ldg(c), hi = __ldg(c + 1);
+        float4 lo, hi;
+        ldg_cell(g.key_c + 2 * ((iz * (g.ny - 1) + iy) * (g.nx - 1) + ix), lo, hi);
         const float tx1 = gx - fx, ty1 = gy - fy, tz1 = gz - fz;
         const float c00 = det_lerp(lo.x, lo.y, tx1), c10 = det_lerp(lo.z, lo.w, tx1);
         const float c01 = det_lerp(hi.x, hi.y, tx1), c11 = det_lerp(hi.z, hi.w, tx1);
@@ -494,6 +522,13 @@ float eval_rigid(const PocketDev& pk, const float4* ys, int N, const Mat3 R,
     }
   }
   return (fe + fo) - c_pk.lam * (we + wo);
+}
+
+// out-of-line copy for the fused kernel (one shared body for both sweep loops)
+template <int kGrid>
+static __device__ __noinline__ float eval_rigid(const PocketDev& pk, const float4* ys, int N,
+                                                const Mat3 R, float tx, float ty, float tz) {
+  return eval_key<kGrid>(pk, ys, N, R, tx, ty, tz);
 }
 
 // all kept poses at RMSD >= delta from s.xf (dock.cpp:335-340, 392-401)

@@ -21,7 +21,7 @@
 namespace vs {
 
 struct Dims {
-  int nmax, tmax, mvmax;
+  int nmax, tmax, mvmax, lay;
 };
 
 struct PoseF {
@@ -31,8 +31,8 @@ struct PoseF {
 
 __device__ __forceinline__ WarpSmem dock_smem(const Dims d) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  return carve(smem_raw + (threadIdx.x >> 5) * warp_smem_bytes(d.nmax, d.tmax, d.mvmax, false),
-               d.nmax, d.tmax, d.mvmax, false);
+  return carve(smem_raw + (threadIdx.x >> 5) * warp_smem_bytes(d.nmax, d.tmax, d.mvmax, d.lay),
+               d.nmax, d.tmax, d.mvmax, d.lay);
 }
 
 // ---- start of restart r (dock.cpp:343-356): first attempt whose start
@@ -40,8 +40,8 @@ __device__ __forceinline__ WarpSmem dock_smem(const Dims d) {
 // leaves the torsion-applied state in s.ys / s.ysf and s.theta.
 static __device__ VS_PHASE int start_phase(const PocketDev& pk, const Dims d,
                                                unsigned long long rkey, int N, int T,
-                                               const float4* kx, int nk, float delta, int lane,
-                                               PoseF* P) {
+                                               const float4* kx, int kstride, int nk, float delta,
+                                               int lane, PoseF* P) {
   const WarpSmem s = dock_smem(d);
   float t[3], q[4];
   int att = 0;
@@ -52,14 +52,16 @@ static __device__ VS_PHASE int start_phase(const PocketDev& pk, const Dims d,
     chain_coop(s, N, T, lane);
     have_chain = true;
     pose_coop(s, N, det_pose_mat_d(q[0], q[1], q[2], q[3]), t[0], t[1], t[2], lane);
-    if (diverse_from_kept(s, kx, nk, d.nmax, N, delta, lane)) break;
+    if (diverse_from_kept(s, kx, nk, kstride, N, delta, lane)) break;
   }
   if (att == 50) att = 49;
   if (!have_chain) chain_coop(s, N, T, lane);
-  for (int i = lane; i < N; i += 32) {
-    const double4 v = s.ys[i];
-    s.ysf[i] = make_float4(static_cast<float>(v.x), static_cast<float>(v.y),
-                           static_cast<float>(v.z), 0.0f);
+  if (s.ysf) {
+    for (int i = lane; i < N; i += 32) {
+      const double4 v = s.ys[i];
+      s.ysf[i] = make_float4(static_cast<float>(v.x), static_cast<float>(v.y),
+                             static_cast<float>(v.z), 0.0f);
+    }
   }
   __syncwarp();
   for (int c = 0; c < 3; ++c) P->t[c] = t[c];
@@ -70,7 +72,7 @@ static __device__ VS_PHASE int start_phase(const PocketDev& pk, const Dims d,
 // ---- rigid roto-translation sweep (SWEEP_V1.md §2.3-2.4): K orientations
 // about the posed centroid (lanes over rotations), then a compass search
 // over the 26 lattice neighbours with halving steps.  FP32 key F - lam W.
-template <int kGrid>
+template <int kGrid, bool kInl = false>
 static __device__ VS_PHASE int sweep_phase(const PocketDev& pk, const Dims d,
                                                const float4* __restrict__ rots, int K, int N,
                                                int lane, PoseF* P, int* n_trans) {
@@ -102,7 +104,8 @@ static __device__ VS_PHASE int sweep_phase(const PocketDev& pk, const Dims d,
     const Mat3 Rk = det_quat_mat(w4, x4, y4, z4);
     float vx, vy, vz;
     det_apply(Rk, cx, cy, cz, 0.0f, 0.0f, 0.0f, &vx, &vy, &vz);
-    const float key = eval_rigid<kGrid>(pk, s.ysf, N, Rk, Cx - vx, Cy - vy, Cz - vz);
+    const float key = kInl ? eval_key<kGrid>(pk, s.ysf, N, Rk, Cx - vx, Cy - vy, Cz - vz)
+                           : eval_rigid<kGrid>(pk, s.ysf, N, Rk, Cx - vx, Cy - vy, Cz - vz);
     if (key > best_key) {
       best_key = key;
       best_k = k;
@@ -137,7 +140,8 @@ static __device__ VS_PHASE int sweep_phase(const PocketDev& pk, const Dims d,
     float key = -INFINITY, ox = 0.0f, oy = 0.0f, oz = 0.0f;
     if (lane < 27) {
       trans_offset(lane, sc, &ox, &oy, &oz);
-      key = eval_rigid<kGrid>(pk, s.ysf, N, RS, ptx + ox, pty + oy, ptz + oz);
+      key = kInl ? eval_key<kGrid>(pk, s.ysf, N, RS, ptx + ox, pty + oy, ptz + oz)
+                 : eval_rigid<kGrid>(pk, s.ysf, N, RS, ptx + ox, pty + oy, ptz + oz);
     }
     int li = lane < 27 ? lane : 0x7fffffff;
     for (int off = 16; off > 0; off >>= 1) {
@@ -310,15 +314,14 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
 // ---- final coordinates, diversity against kept (dock.cpp:359-361), store
 static __device__ VS_PHASE bool keep_phase(const Dims d, int N, int T, const PoseF* P,
                                                float S, int r, int att, int best_k, float4* kx,
-                                               float* kp, int* km, int nk, float delta,
-                                               int lane) {
+                                               int kstride, float* kp, int parw, int* km, int nk,
+                                               float delta, int lane) {
   const WarpSmem s = dock_smem(d);
   pose_coop(s, N, det_pose_mat_d(P->q[0], P->q[1], P->q[2], P->q[3]), P->t[0], P->t[1], P->t[2],
             lane);
-  const bool keep = nk == 0 || diverse_from_kept(s, kx, nk, d.nmax, N, delta, lane);
+  const bool keep = nk == 0 || diverse_from_kept(s, kx, nk, kstride, N, delta, lane);
   if (keep) {
-    const int parw = 8 + d.tmax;
-    for (int i = lane; i < N; i += 32) kx[static_cast<size_t>(nk) * d.nmax + i] = s.xf[i];
+    for (int i = lane; i < N; i += 32) kx[static_cast<size_t>(nk) * kstride + i] = s.xf[i];
     float* Q = kp + static_cast<size_t>(nk) * parw;
     if (lane == 0) {
       for (int c = 0; c < 3; ++c) Q[c] = P->t[c];
@@ -327,7 +330,7 @@ static __device__ VS_PHASE bool keep_phase(const Dims d, int N, int T, const Pos
       km[nk * 4 + 0] = r;
       km[nk * 4 + 1] = att;
       km[nk * 4 + 2] = best_k;
-      s.kscore[nk] = S;
+      if (s.kscore) s.kscore[nk] = S;
     }
     for (int jj = lane; jj < T; jj += 32) Q[8 + jj] = s.theta[jj];
   }
@@ -354,12 +357,11 @@ template <int kGrid>
 static __device__ VS_PHASE void finish_phase(const PocketDev& pk, const Dims d,
                                                  const DockParams& prm, const DockOut& out,
                                                  int lig, int4 meta, int nk, const float4* kx,
-                                                 const float* kp, const int* km,
-                                                 unsigned id_rank, int lane,
+                                                 int kstride, const float* kp, int parw,
+                                                 const int* km, unsigned id_rank, int lane,
                                                  const unsigned long long* st) {
   const WarpSmem s = dock_smem(d);
   const int N = meta.y, T = meta.w, R = prm.R;
-  const int parw = 8 + d.tmax;
   const int a_lane = lane & 15, h = lane >> 4;
   int m_pass = 0;
   for (int k = lane; k < nk; k += 32) {
@@ -389,7 +391,7 @@ static __device__ VS_PHASE void finish_phase(const PocketDev& pk, const Dims d,
     const int p = base + a_lane;
     float B = 0.0f;
     if (p < n_surv) {
-      const float4* X = kx + static_cast<size_t>(s.kinv[p]) * d.nmax;
+      const float4* X = kx + static_cast<size_t>(s.kinv[p]) * kstride;
       for (int i = h; i < N; i += 2) {
         const float4 v = X[i];
         B = B + atom_bonus<kGrid>(pk, static_cast<int>(s.y0[i].w), v.x, v.y, v.z);
@@ -440,7 +442,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB)
                    int nmax, int tmax, int mvmax, float4* __restrict__ scratch_xyz,
                    float* __restrict__ scratch_par, int* __restrict__ scratch_meta,
                    const __grid_constant__ DockOut out) {
-  const Dims d{nmax, tmax, mvmax};
+  const Dims d{nmax, tmax, mvmax, kLayAll};
   const WarpSmem s = dock_smem(d);
   const int lane = threadIdx.x & 31;
   const long gwarp = static_cast<long>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
@@ -471,13 +473,15 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB)
           rng_mix(root ^ rng_mix(static_cast<unsigned long long>(r) + kGolden));
       PoseF P;
       const long long c0 = clock64();
-      const int att = start_phase(pk, d, rkey, N, T, kx, nk, prm.delta, lane, &P);
+      const int att = start_phase(pk, d, rkey, N, T, kx, nmax, nk, prm.delta, lane, &P);
       const long long c1 = clock64();
       const int best_k = sweep_phase<kGrid>(pk, d, rots, prm.K, N, lane, &P, &n_trans);
       const long long c2 = clock64();
       const float S = flex_phase<kGrid>(pk, d, N, T, prm.F, prm.A, step, &P, lane, &st[2]);
       const long long c3 = clock64();
-      if (keep_phase(d, N, T, &P, S, r, att, best_k, kx, kp, km, nk, prm.delta, lane)) ++nk;
+      if (keep_phase(d, N, T, &P, S, r, att, best_k, kx, nmax, kp, 8 + tmax, km, nk, prm.delta,
+                     lane))
+        ++nk;
       cyc[0] += c1 - c0;
       cyc[1] += c2 - c1;
       cyc[2] += c3 - c2;
@@ -485,14 +489,220 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB)
       st[1] += static_cast<unsigned long long>(att) + 1;
     }
     st[0] = static_cast<unsigned long long>(n_trans);
-    finish_phase<kGrid>(pk, d, prm, out, lig, meta, nk, kx, kp, km, lib.id_rank[lig], lane, st);
+    finish_phase<kGrid>(pk, d, prm, out, lig, meta, nk, kx, nmax, kp, 8 + tmax, km,
+                        lib.id_rank[lig], lane, st);
     if (lane == 0 && out.stats)
       for (int c = 0; c < 4; ++c) atomicAdd(out.stats + 4 + c, static_cast<unsigned long long>(cyc[c]));
   }
 }
 
+// ===================================================== staged dock kernels
+// The same phases as vs_dock_kernel, one kernel per phase and restart, the
+// per-ligand state handed over in HBM (StageBufs): each phase runs at its
+// own occupancy and instruction footprint (the sweep needs ~40 registers
+// and 1 KB of shared memory per warp; the flex needs 64 and ~5 KB), and an
+// SM only ever holds one phase's code.  Launch order per restart r:
+// start(r) -> sweep -> flex+keep(r); then finish.  Decisions and scores are
+// those of the fused kernel, bit for bit.
+
+__device__ __forceinline__ int next_item(int* counter, int lane) {
+  int w = 0;
+  if (lane == 0) w = atomicAdd(counter, 1);
+  return __shfl_sync(kFull, w, 0);
+}
+
+// one TMA bulk copy of `bytes` (multiple of 16, 16 B aligned) into smem
+__device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar, uint32_t& phase, int lane) {
+  __syncwarp();
+  if (lane == 0) {
+    fence_proxy_async();
+    mbar_expect_tx(bar, bytes);
+    bulk_g2s(dst, src, bytes, bar);
+  }
+  mbar_wait(bar, phase);
+  phase ^= 1u;
+}
+
+#ifndef VS_MINB_SWEEP
+#define VS_MINB_SWEEP 12
+#endif
+#ifndef VS_MINB_FLEX
+#define VS_MINB_FLEX 8
+#endif
+
+template <int kGrid>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 8)
+    vs_start_kernel(const __grid_constant__ LibDev lib, const __grid_constant__ DockParams prm,
+                    const int* __restrict__ order, int n_order, int* __restrict__ counter,
+                    int nmax, int tmax, int mvmax, int r, const __grid_constant__ StageBufs sb) {
+  const Dims d{nmax, tmax, mvmax, kLayLig | kLayState | kLayPosed};
+  const WarpSmem s = dock_smem(d);
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) mbar_init(s.bar);
+  __syncwarp();
+  uint32_t phase = 0;
+  const PocketDev& pk = c_pk;
+  for (int w = next_item(counter, lane); w < n_order; w = next_item(counter, lane)) {
+    const int lig = order[w];
+    int4 meta;
+    stage_ligand(lib, lig, s, lane, phase, meta);
+    const int N = meta.y, T = meta.w, R = prm.R;
+    const long long c0 = clock64();
+    const unsigned long long root = rng_mix(lib.seeds[lig] ^ kGolden);
+    const unsigned long long rkey =
+        rng_mix(root ^ rng_mix(static_cast<unsigned long long>(r) + kGolden));
+    const int nk = r == 0 ? 0 : sb.nk[lig];
+    const float4* kx = sb.kx + static_cast<size_t>(meta.x) * R;
+    PoseF P;
+    const int att = start_phase(pk, d, rkey, N, T, kx, N, nk, prm.delta, lane, &P);
+    // start_phase leaves the FP32 copy in ysf; this layout has none, so the
+    // FP32 state is written from ys here (same conversion)
+    for (int i = lane; i < N; i += 32) {
+      const double4 v = s.ys[i];
+      sb.ys[meta.x + i] = v;
+      sb.ysf[meta.x + i] = make_float4(static_cast<float>(v.x), static_cast<float>(v.y),
+                                       static_cast<float>(v.z), 0.0f);
+    }
+    for (int j = lane; j < T; j += 32) sb.th[meta.z + j] = s.theta[j];
+    if (lane == 0) {
+      sb.pose[2 * lig] = make_float4(P.t[0], P.t[1], P.t[2], __int_as_float(att));
+      sb.pose[2 * lig + 1] = make_float4(P.q[0], P.q[1], P.q[2], P.q[3]);
+      if (r == 0) {
+        sb.nk[lig] = 0;
+        for (int c = 0; c < 8; ++c) sb.st[8 * lig + c] = 0ull;
+      }
+      sb.st[8 * lig + 1] += static_cast<unsigned long long>(att) + 1;
+      sb.st[8 * lig + 4] += static_cast<unsigned long long>(clock64() - c0);
+    }
+    __syncwarp();
+  }
+}
+
+template <int kGrid>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_SWEEP)
+    vs_sweep_kernel(const __grid_constant__ LibDev lib, const float4* __restrict__ rots,
+                    const __grid_constant__ DockParams prm, const int* __restrict__ order,
+                    int n_order, int* __restrict__ counter, int nmax,
+                    const __grid_constant__ StageBufs sb) {
+  const Dims d{nmax, 0, 0, kLaySweep};
+  const WarpSmem s = dock_smem(d);
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) mbar_init(s.bar);
+  __syncwarp();
+  uint32_t phase = 0;
+  const PocketDev& pk = c_pk;
+  for (int w = next_item(counter, lane); w < n_order; w = next_item(counter, lane)) {
+    const int lig = order[w];
+    const int4 meta = lib.meta[lig];
+    const int N = meta.y;
+    tma_load(s.ysf, sb.ysf + meta.x, 16u * N, s.bar, phase, lane);
+    const long long c0 = clock64();
+    const float4 pt = sb.pose[2 * lig], pq = sb.pose[2 * lig + 1];
+    PoseF P;
+    P.t[0] = pt.x;
+    P.t[1] = pt.y;
+    P.t[2] = pt.z;
+    P.q[0] = pq.x;
+    P.q[1] = pq.y;
+    P.q[2] = pq.z;
+    P.q[3] = pq.w;
+    int n_trans = 0;
+    const int best_k = sweep_phase<kGrid, true>(pk, d, rots, prm.K, N, lane, &P, &n_trans);
+    if (lane == 0) {
+      sb.pose[2 * lig] = make_float4(P.t[0], P.t[1], P.t[2], pt.w);
+      sb.pose[2 * lig + 1] = make_float4(P.q[0], P.q[1], P.q[2], P.q[3]);
+      sb.bk[lig] = best_k;
+      sb.st[8 * lig + 0] += static_cast<unsigned long long>(n_trans);
+      sb.st[8 * lig + 5] += static_cast<unsigned long long>(clock64() - c0);
+    }
+    __syncwarp();
+  }
+}
+
+template <int kGrid>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_FLEX)
+    vs_flex_kernel(const __grid_constant__ LibDev lib, const __grid_constant__ DockParams prm,
+                   const int* __restrict__ order, int n_order, int* __restrict__ counter,
+                   int nmax, int tmax, int mvmax, int r, const __grid_constant__ StageBufs sb) {
+  const Dims d{nmax, tmax, mvmax, kLayLig | kLayState | kLayPosed | kLayFlex};
+  const WarpSmem s = dock_smem(d);
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) mbar_init(s.bar);
+  __syncwarp();
+  uint32_t phase = 0;
+  const PocketDev& pk = c_pk;
+  const float step = kTwoPiF / static_cast<float>(prm.A);
+  for (int w = next_item(counter, lane); w < n_order; w = next_item(counter, lane)) {
+    const int lig = order[w];
+    int4 meta;
+    stage_ligand(lib, lig, s, lane, phase, meta);
+    const int N = meta.y, T = meta.w, R = prm.R;
+    tma_load(s.ys, sb.ys + meta.x, 32u * N, s.bar, phase, lane);
+    for (int j = lane; j < T; j += 32) s.theta[j] = sb.th[meta.z + j];
+    const long long c0 = clock64();
+    const float4 pt = sb.pose[2 * lig], pq = sb.pose[2 * lig + 1];
+    PoseF P;
+    P.t[0] = pt.x;
+    P.t[1] = pt.y;
+    P.t[2] = pt.z;
+    P.q[0] = pq.x;
+    P.q[1] = pq.y;
+    P.q[2] = pq.z;
+    P.q[3] = pq.w;
+    __syncwarp();
+    unsigned long long nact = 0;
+    const float S = flex_phase<kGrid>(pk, d, N, T, prm.F, prm.A, step, &P, lane, &nact);
+    const long long c1 = clock64();
+    const int nk = sb.nk[lig];
+    float4* kx = sb.kx + static_cast<size_t>(meta.x) * R;
+    float* kp = sb.kp + (static_cast<size_t>(lig) * 8 + meta.z) * R;
+    int* km = sb.km + static_cast<size_t>(lig) * R * 4;
+    const bool kept = keep_phase(d, N, T, &P, S, r, __float_as_int(pt.w), sb.bk[lig], kx, N, kp,
+                                 8 + T, km, nk, prm.delta, lane);
+    if (lane == 0) {
+      if (kept) sb.nk[lig] = nk + 1;
+      sb.st[8 * lig + 2] += nact;
+      sb.st[8 * lig + 6] += static_cast<unsigned long long>(c1 - c0);
+      sb.st[8 * lig + 7] += static_cast<unsigned long long>(clock64() - c1);
+    }
+    __syncwarp();
+  }
+}
+
+template <int kGrid>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 8)
+    vs_finish_kernel(const __grid_constant__ LibDev lib, const __grid_constant__ DockParams prm,
+                     const int* __restrict__ order, int n_order, int* __restrict__ counter,
+                     int nmax, int tmax, int mvmax, const __grid_constant__ StageBufs sb,
+                     const __grid_constant__ DockOut out) {
+  const Dims d{nmax, tmax, mvmax, kLayLig | kLayKept};
+  const WarpSmem s = dock_smem(d);
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) mbar_init(s.bar);
+  __syncwarp();
+  uint32_t phase = 0;
+  const PocketDev& pk = c_pk;
+  for (int w = next_item(counter, lane); w < n_order; w = next_item(counter, lane)) {
+    const int lig = order[w];
+    int4 meta;
+    stage_ligand(lib, lig, s, lane, phase, meta);
+    const int T = meta.w, R = prm.R;
+    const int nk = sb.nk[lig];
+    const float* kp = sb.kp + (static_cast<size_t>(lig) * 8 + meta.z) * R;
+    for (int k = lane; k < nk; k += 32) s.kscore[k] = kp[static_cast<size_t>(k) * (8 + T) + 7];
+    __syncwarp();
+    const unsigned long long* st = sb.st + 8 * lig;
+    finish_phase<kGrid>(pk, d, prm, out, lig, meta, nk, sb.kx + static_cast<size_t>(meta.x) * R,
+                        meta.y, kp, 8 + T, sb.km + static_cast<size_t>(lig) * R * 4,
+                        lib.id_rank[lig], lane, st);
+    if (lane == 0 && out.stats)
+      for (int c = 4; c < 8; ++c) atomicAdd(out.stats + c, st[c]);
+  }
+}
+
 size_t dock_smem_per_block(int nmax, int tmax, int mvmax) {
-  return kWarpsPerBlock * warp_smem_bytes(nmax, tmax, mvmax, false);
+  return kWarpsPerBlock * warp_smem_bytes(nmax, tmax, mvmax, kLayAll);
 }
 
 template <class K>
@@ -520,6 +730,74 @@ cudaError_t launch_dock(bool grid, int blocks, size_t smem, cudaStream_t st, con
         lib, pk, rots, prm, order, n_order, counter, nmax, tmax, mvmax, sx, sp, sm, out);
   }
   return cudaGetLastError();
+}
+
+// ---------------------------------------------------------- staged launch
+template <class K>
+static int stage_blocks(K kernel, size_t smem, int sms, int n_items) {
+  prep_dock(kernel, smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kWarpsPerBlock * 32, smem);
+  if (per_sm < 1) per_sm = 1;
+  const int want = (n_items + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  return want < per_sm * sms ? (want > 0 ? want : 1) : per_sm * sms;
+}
+
+size_t stage_smem_per_block(int nmax, int tmax, int mvmax) {
+  const int lays[4] = {kLayLig | kLayState | kLayPosed, kLaySweep,
+                       kLayLig | kLayState | kLayPosed | kLayFlex, kLayLig | kLayKept};
+  size_t m = 0;
+  for (int l : lays) {
+    const size_t b = kWarpsPerBlock * warp_smem_bytes(nmax, tmax, mvmax, l);
+    m = b > m ? b : m;
+  }
+  return m;
+}
+
+template <int kGrid>
+static cudaError_t staged_impl(int sms, cudaStream_t st, const LibDev& lib, const float4* rots,
+                               const DockParams& prm, const int* order, int n, int* counters,
+                               int nmax, int tmax, int mvmax, const StageBufs& sb,
+                               const DockOut& out, uint64_t* launches) {
+  const size_t sm_start = kWarpsPerBlock * warp_smem_bytes(nmax, tmax, mvmax,
+                                                           kLayLig | kLayState | kLayPosed);
+  const size_t sm_sweep = kWarpsPerBlock * warp_smem_bytes(nmax, 0, 0, kLaySweep);
+  const size_t sm_flex = kWarpsPerBlock * warp_smem_bytes(
+                                              nmax, tmax, mvmax,
+                                              kLayLig | kLayState | kLayPosed | kLayFlex);
+  const size_t sm_fin = kWarpsPerBlock * warp_smem_bytes(nmax, tmax, mvmax, kLayLig | kLayKept);
+  const int b_start = stage_blocks(vs_start_kernel<kGrid>, sm_start, sms, n);
+  const int b_sweep = stage_blocks(vs_sweep_kernel<kGrid>, sm_sweep, sms, n);
+  const int b_flex = stage_blocks(vs_flex_kernel<kGrid>, sm_flex, sms, n);
+  const int b_fin = stage_blocks(vs_finish_kernel<kGrid>, sm_fin, sms, n);
+  const int T = kWarpsPerBlock * 32;
+  int c = 0;
+  for (int r = 0; r < prm.R; ++r) {
+    vs_start_kernel<kGrid><<<b_start, T, sm_start, st>>>(lib, prm, order, n, counters + c++, nmax,
+                                                        tmax, mvmax, r, sb);
+    vs_sweep_kernel<kGrid><<<b_sweep, T, sm_sweep, st>>>(lib, rots, prm, order, n,
+                                                        counters + c++, nmax, sb);
+    vs_flex_kernel<kGrid><<<b_flex, T, sm_flex, st>>>(lib, prm, order, n, counters + c++, nmax,
+                                                     tmax, mvmax, r, sb);
+    *launches += 3;
+  }
+  vs_finish_kernel<kGrid><<<b_fin, T, sm_fin, st>>>(lib, prm, order, n, counters + c++, nmax, tmax,
+                                                   mvmax, sb, out);
+  *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_staged(bool grid, int sms, cudaStream_t st, const LibDev& lib,
+                          const PocketDev& pk, const float4* rots, const DockParams& prm,
+                          const int* order, int n, int* counters, int nmax, int tmax, int mvmax,
+                          const StageBufs& sb, const DockOut& out, uint64_t* launches) {
+  cudaError_t e = cudaMemcpyToSymbolAsync(c_pk, &pk, sizeof(PocketDev), 0, cudaMemcpyHostToDevice,
+                                          st);
+  if (e != cudaSuccess) return e;
+  return grid ? staged_impl<1>(sms, st, lib, rots, prm, order, n, counters, nmax, tmax, mvmax, sb,
+                               out, launches)
+              : staged_impl<0>(sms, st, lib, rots, prm, order, n, counters, nmax, tmax, mvmax, sb,
+                               out, launches);
 }
 
 int dock_blocks_per_sm(bool grid, size_t smem) {

@@ -86,7 +86,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const WarpSmem s =
-      carve(smem_raw + wib * warp_smem_bytes(nmax, tmax, mvmax, true), nmax, tmax, mvmax, true);
+      carve(smem_raw + wib * warp_smem_bytes(nmax, tmax, mvmax, kLayAll | kLayCols), nmax, tmax, mvmax,
+            kLayAll | kLayCols);
   if (lane == 0) mbar_init(s.bar);
   __syncwarp();
   uint32_t phase = 0;
@@ -263,7 +264,7 @@ __global__ void vs_peak_xu(float* out, int iters, float seed) {
 namespace vs {
 
 size_t rescore_smem_per_block(int nmax, int tmax, int mvmax) {
-  return kWarpsPerBlock * warp_smem_bytes(nmax, tmax, mvmax, true);
+  return kWarpsPerBlock * warp_smem_bytes(nmax, tmax, mvmax, kLayAll | kLayCols);
 }
 
 template <class K>

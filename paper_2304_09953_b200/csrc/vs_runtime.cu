@@ -21,6 +21,20 @@ namespace vs {
 size_t dock_smem_per_block(int nmax, int tmax, int mvmax);
 size_t rescore_smem_per_block(int nmax, int tmax, int mvmax);
 int dock_blocks_per_sm(bool grid, size_t smem);
+size_t stage_smem_per_block(int nmax, int tmax, int mvmax);
+
+// dock execution mode: "staged" (one kernel per phase and restart) or
+// "fused" (one persistent kernel); VSCREEN_DOCK_MODE overrides the default
+static bool staged_mode() {
+  const char* m = std::getenv("VSCREEN_DOCK_MODE");
+  if (m && std::strcmp(m, "fused") == 0) return false;
+  if (m && std::strcmp(m, "staged") == 0) return true;
+  return false;
+}
+cudaError_t launch_staged(bool grid, int sms, cudaStream_t st, const LibDev& lib,
+                          const PocketDev& pk, const float4* rots, const DockParams& prm,
+                          const int* order, int n, int* counters, int nmax, int tmax, int mvmax,
+                          const StageBufs& sb, const DockOut& out, uint64_t* launches);
 cudaError_t launch_dock(bool grid, int blocks, size_t smem, cudaStream_t st, const LibDev& lib,
                         const PocketDev& pk, const float4* rots, const DockParams& prm,
                         const int* order, int n_order, int* counter, int nmax, int tmax,
@@ -130,6 +144,7 @@ struct vs_handle {
   bool has_results = false;
   DBuf d_surv, d_surv_tors, d_all, d_all_tors, d_best, d_nkept, d_nsurv, d_keys, d_counters;
   DBuf d_sx, d_sp, d_sm, d_rots, d_topk_a, d_topk_b, d_stats;
+  DBuf d_sg_ys, d_sg_ysf, d_sg_th, d_sg_pose, d_sg_bk, d_sg_nk, d_sg_kx, d_sg_kp, d_sg_km, d_sg_st;
   int rots_k = -1;
   uint64_t rots_seed = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -388,7 +403,9 @@ void vs_destroy(vs_handle* h) {
   h->lib.release();
   for (DBuf* b : {&h->d_sites, &h->d_maps, &h->d_surv, &h->d_surv_tors, &h->d_all, &h->d_all_tors,
                   &h->d_best, &h->d_nkept, &h->d_nsurv, &h->d_keys, &h->d_counters, &h->d_sx,
-                  &h->d_sp, &h->d_sm, &h->d_rots, &h->d_topk_a, &h->d_topk_b, &h->d_stats})
+                  &h->d_sp, &h->d_sm, &h->d_rots, &h->d_topk_a, &h->d_topk_b, &h->d_stats,
+                  &h->d_sg_ys, &h->d_sg_ysf, &h->d_sg_th, &h->d_sg_pose, &h->d_sg_bk, &h->d_sg_nk,
+                  &h->d_sg_kx, &h->d_sg_kp, &h->d_sg_km, &h->d_sg_st})
     b->release();
   cudaEventDestroy(h->ev0);
   cudaEventDestroy(h->ev1);
@@ -462,7 +479,8 @@ int vs_set_pocket(vs_handle* h, const vs_pocket* p, double spacing, double pad) 
       *dims[c] = static_cast<int>(std::ceil((p->hi[c] - p->lo[c] + 2.0 * pad) / spacing)) + 1;
     const size_t nodes = static_cast<size_t>(g.nx) * g.ny * g.nz;
     const size_t cells = static_cast<size_t>(g.nx - 1) * (g.ny - 1) * (g.nz - 1);
-    const size_t node_bytes = align16z(4 * nodes * sizeof(float));
+    // cell arrays 256 B aligned: each 32 B cell is one 256-bit load (ldg_cell)
+    const size_t node_bytes = (4 * nodes * sizeof(float) + 255) & ~size_t(255);
     VS_CUDA(h, h->d_maps.ensure(node_bytes + 4 * cells * 2 * sizeof(float4)));
     float* m = h->d_maps.as<float>();
     float4* c = reinterpret_cast<float4*>(static_cast<char*>(h->d_maps.p) + node_bytes);
@@ -552,13 +570,13 @@ int vs_dock(vs_handle* h, const vs_dock_params* prm, void* stream) {
   VS_CUDA(h, h->d_nkept.ensure(nn * 4));
   VS_CUDA(h, h->d_nsurv.ensure(nn * 4));
   VS_CUDA(h, h->d_keys.ensure(nn * 8));
-  VS_CUDA(h, h->d_counters.ensure(64 * sizeof(int)));
+  VS_CUDA(h, h->d_counters.ensure(256 * sizeof(int)));
   VS_CUDA(h, h->d_stats.ensure(8 * sizeof(unsigned long long)));
   VS_CUDA(h, cudaMemsetAsync(h->d_stats.p, 0, 8 * sizeof(unsigned long long), st));
   VS_CUDA(h, cudaMemsetAsync(h->d_keys.p, 0xff, nn * 8, st));
   VS_CUDA(h, cudaMemsetAsync(h->d_nkept.p, 0, nn * 4, st));
   VS_CUDA(h, cudaMemsetAsync(h->d_nsurv.p, 0, nn * 4, st));
-  VS_CUDA(h, cudaMemsetAsync(h->d_counters.p, 0, 64 * sizeof(int), st));
+  VS_CUDA(h, cudaMemsetAsync(h->d_counters.p, 0, 256 * sizeof(int), st));
 
   DockParams dp;
   dp.R = R;
@@ -586,7 +604,37 @@ int vs_dock(vs_handle* h, const vs_dock_params* prm, void* stream) {
   // shared memory sized for the largest ligand; one scratch slot per warp
   const Bucket& b = P.all;
   VS_CUDA(h, cudaEventRecord(h->ev0, st));
-  if (b.count > 0) {
+  if (b.count > 0 && staged_mode()) {
+    // staged: one kernel per phase and restart, state handed over in HBM
+    const size_t smem = stage_smem_per_block(b.nmax, b.tmax, b.mvmax);
+    if (smem > 227 * 1024) return fail(h, VS_ERR_CAPACITY, "ligands need too much shared memory");
+    const size_t na = std::max<size_t>(1, P.atoms.size());
+    const size_t nt = static_cast<size_t>(std::max<long>(1, P.total_tors));
+    VS_CUDA(h, h->d_sg_ys.ensure(na * sizeof(double4)));
+    VS_CUDA(h, h->d_sg_ysf.ensure(na * sizeof(float4)));
+    VS_CUDA(h, h->d_sg_th.ensure(nt * sizeof(float)));
+    VS_CUDA(h, h->d_sg_pose.ensure(nn * 2 * sizeof(float4)));
+    VS_CUDA(h, h->d_sg_bk.ensure(nn * sizeof(int)));
+    VS_CUDA(h, h->d_sg_nk.ensure(nn * sizeof(int)));
+    VS_CUDA(h, h->d_sg_kx.ensure(na * R * sizeof(float4)));
+    VS_CUDA(h, h->d_sg_kp.ensure((nn * 8 + nt) * R * sizeof(float)));
+    VS_CUDA(h, h->d_sg_km.ensure(nn * R * 4 * sizeof(int)));
+    VS_CUDA(h, h->d_sg_st.ensure(nn * 8 * sizeof(unsigned long long)));
+    StageBufs sb;
+    sb.ys = h->d_sg_ys.as<double4>();
+    sb.ysf = h->d_sg_ysf.as<float4>();
+    sb.th = h->d_sg_th.as<float>();
+    sb.pose = h->d_sg_pose.as<float4>();
+    sb.bk = h->d_sg_bk.as<int>();
+    sb.nk = h->d_sg_nk.as<int>();
+    sb.kx = h->d_sg_kx.as<float4>();
+    sb.kp = h->d_sg_kp.as<float>();
+    sb.km = h->d_sg_km.as<int>();
+    sb.st = h->d_sg_st.as<unsigned long long>();
+    VS_CUDA(h, launch_staged(grid, h->sms, st, ld, h->pk, h->d_rots.as<const float4>(), dp,
+                             P.d_order.as<int>() + b.start, b.count, h->d_counters.as<int>(),
+                             b.nmax, b.tmax, b.mvmax, sb, out, &h->launches));
+  } else if (b.count > 0) {
     const size_t smem = dock_smem_per_block(b.nmax, b.tmax, b.mvmax);
     if (smem > 227 * 1024) return fail(h, VS_ERR_CAPACITY, "ligands need too much shared memory");
     int per_sm = dock_blocks_per_sm(grid, smem);

@@ -90,4 +90,19 @@ struct DockOut {
   unsigned long long* stats; // [4] work counters (capi.h vs_last_stats)
 };
 
+// Per-ligand state of the staged dock (one kernel per phase and restart):
+// what one phase hands to the next through HBM.
+struct StageBufs {
+  double4* ys;               // [total_atoms] FP64 state after start (torsions applied)
+  float4* ysf;               // [total_atoms] FP32 copy for the sweep
+  float* th;                 // [total_tors] state torsions
+  float4* pose;              // [n][2]: (t.xyz, attempt), q
+  int* bk;                   // [n] winning rotation of the sweep
+  int* nk;                   // [n] kept poses so far
+  float4* kx;                // kept coordinates: ligand base atom_off * R, pose k at k * N
+  float* kp;                 // kept (t, q, S, theta): base (lig * 8 + tors_off) * R, 8 + T each
+  int* km;                   // [n][R][4] kept (restart, attempt, rotation)
+  unsigned long long* st;    // [n][8] counters (trans iters, attempts, pairs, -, cycles x4)
+};
+
 }  // namespace vs
