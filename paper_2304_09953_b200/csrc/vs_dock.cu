@@ -525,7 +525,7 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t by
 }
 
 #ifndef VS_MINB_SWEEP
-#define VS_MINB_SWEEP 12
+#define VS_MINB_SWEEP 8
 #endif
 #ifndef VS_MINB_FLEX
 #define VS_MINB_FLEX 8

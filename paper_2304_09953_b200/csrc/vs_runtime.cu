@@ -28,8 +28,7 @@ size_t stage_smem_per_block(int nmax, int tmax, int mvmax);
 static bool staged_mode() {
   const char* m = std::getenv("VSCREEN_DOCK_MODE");
   if (m && std::strcmp(m, "fused") == 0) return false;
-  if (m && std::strcmp(m, "staged") == 0) return true;
-  return false;
+  return true;
 }
 cudaError_t launch_staged(bool grid, int sms, cudaStream_t st, const LibDev& lib,
                           const PocketDev& pk, const float4* rots, const DockParams& prm,
