@@ -165,27 +165,29 @@ class ClockSampler:
 
 # ---------------------------------------------------------------- roofline --
 # per-unit work of sweep-v1 as implemented; FMA = 2 flops
-ATOM_FLOP_GRID = 63      # FP32 transform 18 + trilinear 30 + wall 13 + sums 2
-ATOM_XU_GRID = 3         # float->int cell index conversions
-POSE_ROT_FLOP = 80       # quaternion product, normalize, matrix, t = C - R c
-POSE_ROT_XU = 5          # sqrt + 4 divisions of the normalization
-TERMS_FLOP = 79          # FP64 transform 18 + ATOM_FLOP_GRID - sums
+ATOM_FLOP_KEY = 43       # grid-frame FP32 transform 18 + fractions 3 + 7 lerps 21 + sum 1
+ATOM_XU_KEY = 3          # float->int cell index conversions
+POSE_ROT_FLOP = 97       # quaternion product, normalize, matrix, centroid, grid frame
+POSE_ROT_XU = 2          # sqrt + one reciprocal of the normalization
+TERMS_FLOP = 107         # FP64 transform 18 + grid frame and trilinear 30 + wall 13 + softplus 46
 TERMS_XU = 6             # 3 FP64->FP32 conversions + 3 cell indices
 PAIR_TEST_FLOP = 9       # FP64 difference, norm, compare
-PAIR_ACTIVE_FLOP = 35    # sqrt fix-up, z, softplus (exp + log1p polynomials)
-PAIR_ACTIVE_XU = 3       # sqrt, exp shift, log1p reciprocal
-AXIS_FLOP = 40           # flex rotation: norm, sincos_d, matrix (FP64)
+PAIR_ACTIVE_FLOP = 52    # sqrt fix-up 4, z 2, softplus 46 (exp 21 + log1p 21 + tails)
+PAIR_ACTIVE_XU = 3       # sqrt, exp shift, float conversion
+AXIS_FLOP = 81           # flex rotation: half angle 3, sincos_d 44, quaternion matrix 30, axis 4
 MOVE_FLOP = 18           # FP64 rotation of one moving atom
 
 
 def algorithmic_work(lib, prm, stats, grid: bool, n_steric: int):
-    """Algorithmic FLOP / XU ops of one pass of sweep-v1 over `lib`, from
-    the ligand descriptors and the device work counters:
-      rigid poses   R*K*N + 27*sum(trans_iters*N) pose-atoms, R*K pose setups
-      flex steps    F*T per restart: base (N atom sums + non-crossing pairs)
-                    + A candidates x (axis rotation + m_j moved atoms
-                    + m_j*(N-m_j) cross pairs)
-      pairs inside the cutoff (device counter) add the softplus cost."""
+    """Algorithmic FLOP / XU ops of one pass of sweep-v1 over `lib`, split
+    by the kernel that does it, from the ligand descriptors
+    and the device work counters:
+      sweep   R*K*N + 27*sum(trans_iters*N) pose-atoms, R*K pose setups
+      flex    per restart the state's atom terms, then F*T steps: base (N
+              atom sums + non-crossing pairs) + A candidates x (axis rotation
+              + m_j moved atoms + m_j*(N-m_j) cross pairs); pairs inside the
+              cutoff (device counter) add the softplus cost
+      start   the FP64 torsion chain of each restart"""
     R, K, A, F = prm.restarts, prm.rotations, prm.flex_angles, prm.flex_passes
     N = lib.n_atoms.astype(np.float64)
     T = lib.n_tors.astype(np.int64)
@@ -201,43 +203,58 @@ def algorithmic_work(lib, prm, stats, grid: bool, n_steric: int):
     P = N * (N - 1) / 2
     no_flex = (T == 0) | (F == 0)
     flex_flop += float(np.sum(np.where(no_flex, R * (2 * N + PAIR_TEST_FLOP * P), 0.0)))
-    init_flop = float(np.sum(R * N * TERMS_FLOP))          # state atom terms per restart
+    flex_flop += float(np.sum(R * N * TERMS_FLOP)) + stats["active_pairs"] * PAIR_ACTIVE_FLOP
+    flex_xu += stats["active_pairs"] * PAIR_ACTIVE_XU + R * float(np.sum(N)) * TERMS_XU
     chain_flop = float(np.sum(np.add.reduceat(np.r_[AXIS_FLOP + MOVE_FLOP * m, 0.0],
                                               np.minimum(to[:-1], len(m))) * (T > 0))) * R
-    atom_f = ATOM_FLOP_GRID if grid else 31 + 11 * n_steric
-    atom_x = ATOM_XU_GRID if grid else 2 * n_steric
+    atom_f = ATOM_FLOP_KEY if grid else 31 + 11 * n_steric
+    atom_x = ATOM_XU_KEY if grid else 2 * n_steric
     pose_atoms = float(np.sum(R * K * N)) + 27.0 * stats["translation_iter_atoms"]
-    flop = (pose_atoms * atom_f + R * K * len(lib) * POSE_ROT_FLOP + flex_flop + init_flop
-            + chain_flop + stats["active_pairs"] * PAIR_ACTIVE_FLOP)
-    xu = (pose_atoms * atom_x + R * K * len(lib) * POSE_ROT_XU + flex_xu
-          + stats["active_pairs"] * PAIR_ACTIVE_XU + R * float(np.sum(N)) * TERMS_XU)
-    return flop, xu
+    sweep_flop = pose_atoms * atom_f + R * K * len(lib) * POSE_ROT_FLOP
+    sweep_xu = pose_atoms * atom_x + R * K * len(lib) * POSE_ROT_XU
+    return {"sweep": (sweep_flop, sweep_xu), "flex": (flex_flop, flex_xu),
+            "start": (chain_flop, 0.0)}
 
 
-def roofline(flop, xu, dock_ms, peaks, traffic):
-    t = dock_ms * 1e-3
-    t_fp32 = flop / peaks["fp32_flops"]
-    t_xu = xu / peaks["xu_ops"]
-    if t_fp32 >= t_xu:
-        bound, achieved, peak, unit = "fp32", flop / t / 1e12, peaks["fp32_flops"] / 1e12, "TFLOP/s"
-    else:
-        bound, achieved, peak, unit = "xu", xu / t / 1e12, peaks["xu_ops"] / 1e12, "Tops/s"
-    return {"bound": bound, "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": unit,
-            "frac": round(achieved / peak, 4), "traffic": traffic,
-            "peak_source": "measured on this GPU by vs_measure_peaks (FFMA / MUFU.EX2 microbenchmarks)",
-            "fp32": {"achieved_tflops": round(flop / t / 1e12, 3),
-                     "peak_tflops": round(peaks["fp32_flops"] / 1e12, 3),
-                     "frac": round(flop / t / peaks["fp32_flops"], 4)},
-            "xu": {"achieved_tops": round(xu / t / 1e12, 3), "peak_tops": round(peaks["xu_ops"] / 1e12, 3),
-                   "frac": round(xu / t / peaks["xu_ops"], 4)},
-            "flop_per_step": flop, "xu_per_step": xu, "dock_kernel_ms": round(dock_ms, 3)}
+def roofline(work, phase_ms, dock_ms, peaks, traffic):
+    """Per-kernel achieved FP32 rate over its own device time; the headline
+    is the kernel with the largest share of the dock pass."""
+    per = {}
+    for k, (flop, xu) in work.items():
+        ms = phase_ms.get(k, 0.0)
+        if ms <= 0:
+            continue
+        t = ms * 1e-3
+        per[k] = {"ms": round(ms, 3), "flop": flop, "xu_ops": xu,
+                  "achieved_tflops": round(flop / t / 1e12, 3),
+                  "frac_fp32": round(flop / t / peaks["fp32_flops"], 4),
+                  "achieved_xu_tops": round(xu / t / 1e12, 3),
+                  "frac_xu": round(xu / t / peaks["xu_ops"], 4)}
+    dom = max(per, key=lambda k: per[k]["ms"])
+    d = per[dom]
+    flop_all = sum(w[0] for w in work.values())
+    name = {"sweep": "vs_sweep_kernel", "flex": "vs_flex_kernel", "start": "vs_start_kernel"}[dom]
+    return {"bound": "fp32", "achieved": d["achieved_tflops"],
+            "peak": round(peaks["fp32_flops"] / 1e12, 3), "unit": "TFLOP/s",
+            "frac": d["frac_fp32"], "traffic": (traffic or {}).get(name),
+            "kernel": name,
+            "peak_source": "measured on this GPU by vs_measure_peaks (FFMA microbenchmark)",
+            "per_kernel": per,
+            "dock_pass": {"ms": round(dock_ms, 3), "flop": flop_all,
+                          "achieved_tflops": round(flop_all / (dock_ms * 1e-3) / 1e12, 3),
+                          "frac_fp32": round(flop_all / (dock_ms * 1e-3) / peaks["fp32_flops"],
+                                             4)},
+            "phase_ms": {k: round(v, 3) for k, v in phase_ms.items()}}
 
 
 def load_traffic():
+    """DRAM bytes per launch of each dock kernel from the committed ncu pass
+    (profiles/ncu_dock_traffic.json, tools/ncu_summary.py)."""
     p = os.path.join(ROOT, "profiles", "ncu_dock_traffic.json")
     if os.path.exists(p):
         try:
-            return json.load(open(p)).get("dram_bytes_per_launch")
+            return {k: v.get("dram_bytes_per_launch")
+                    for k, v in json.load(open(p)).get("kernels", {}).items()}
         except Exception:
             return None
     return None
@@ -392,7 +409,7 @@ def main():
     launches0 = eng.launch_count()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
-    dock_ms = []
+    dock_ms, phase = [], []
     with ClockSampler(local) as clocks:
         for k in range(args.steps):
             flush.zero_()  # L2 flush between timed iterations
@@ -404,6 +421,7 @@ def main():
             ev[k][1].record(stream)
             torch.cuda.synchronize()
             dock_ms.append(eng.last_dock_ms())
+            phase.append(eng.phase_ms())
     launches = eng.launch_count() - launches0
     total_ms = sum(a.elapsed_time(b) for a, b in ev)
     stats = eng.stats()
@@ -413,8 +431,9 @@ def main():
     total_ms = float(t.item())
     n_total = len(lib) * world
     value = n_total * args.steps / (total_ms * 1e-3)
-    flop, xu = algorithmic_work(lib, prm, stats, True, sum(s.kind == "steric" for s in pocket.sites))
-    rl = roofline(flop, xu, float(np.mean(dock_ms)), peaks, load_traffic())
+    work = algorithmic_work(lib, prm, stats, True, sum(s.kind == "steric" for s in pocket.sites))
+    phase_ms = {k: float(np.mean([p[k] for p in phase])) for k in phase[0]}
+    rl = roofline(work, phase_ms, float(np.mean(dock_ms)), peaks, load_traffic())
     top = out.cpu().numpy().view(np.uint64)
     n_ranked = int(np.sum(top != np.uint64(2**64 - 1)))
 

@@ -163,6 +163,10 @@ int vs_dock_host(vs_handle* h, const vs_library* lib, const vs_size_class* class
  * the last vs_dock call, and the number of kernels this handle launched. */
 double vs_last_dock_ms(const vs_handle* h);
 uint64_t vs_launch_count(const vs_handle* h);
+/* Device time (ms) of the last vs_dock split by kernel: [0] start, [1] sweep,
+ * [2] flex+keep, [3] finish (staged mode; the fused kernel reports its whole
+ * time in [2]).  CUDA events around every launch on the launch stream. */
+int vs_last_phase_ms(vs_handle* h, double out[4]);
 /* work counters of the last vs_dock: [0] translation-sweep iterations,
  * [1] the same weighted by ligand atoms, [2] start attempts, [3] flex pair
  * softplus evaluations (pairs inside the cutoff), [4..7] SM cycles summed

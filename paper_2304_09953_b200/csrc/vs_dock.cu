@@ -758,7 +758,8 @@ template <int kGrid>
 static cudaError_t staged_impl(int sms, cudaStream_t st, const LibDev& lib, const float4* rots,
                                const DockParams& prm, const int* order, int n, int* counters,
                                int nmax, int tmax, int mvmax, const StageBufs& sb,
-                               const DockOut& out, uint64_t* launches) {
+                               const DockOut& out, uint64_t* launches, cudaEvent_t* evs,
+                               int* kinds) {
   const size_t sm_start = kWarpsPerBlock * warp_smem_bytes(nmax, tmax, mvmax,
                                                            kLayLig | kLayState | kLayPosed);
   const size_t sm_sweep = kWarpsPerBlock * warp_smem_bytes(nmax, 0, 0, kLaySweep);
@@ -772,17 +773,33 @@ static cudaError_t staged_impl(int sms, cudaStream_t st, const LibDev& lib, cons
   const int b_fin = stage_blocks(vs_finish_kernel<kGrid>, sm_fin, sms, n);
   const int T = kWarpsPerBlock * 32;
   int c = 0;
+  auto mark = [&](int kind, bool after) {  // event pair c: launch c (counter c)
+    if (!evs) return;
+    cudaEventRecord(evs[2 * c + (after ? 1 : 0)], st);
+    kinds[c] = kind;
+  };
   for (int r = 0; r < prm.R; ++r) {
-    vs_start_kernel<kGrid><<<b_start, T, sm_start, st>>>(lib, prm, order, n, counters + c++, nmax,
+    mark(0, false);
+    vs_start_kernel<kGrid><<<b_start, T, sm_start, st>>>(lib, prm, order, n, counters + c, nmax,
                                                         tmax, mvmax, r, sb);
-    vs_sweep_kernel<kGrid><<<b_sweep, T, sm_sweep, st>>>(lib, rots, prm, order, n,
-                                                        counters + c++, nmax, sb);
-    vs_flex_kernel<kGrid><<<b_flex, T, sm_flex, st>>>(lib, prm, order, n, counters + c++, nmax,
+    mark(0, true);
+    ++c;
+    mark(1, false);
+    vs_sweep_kernel<kGrid><<<b_sweep, T, sm_sweep, st>>>(lib, rots, prm, order, n, counters + c,
+                                                        nmax, sb);
+    mark(1, true);
+    ++c;
+    mark(2, false);
+    vs_flex_kernel<kGrid><<<b_flex, T, sm_flex, st>>>(lib, prm, order, n, counters + c, nmax,
                                                      tmax, mvmax, r, sb);
+    mark(2, true);
+    ++c;
     *launches += 3;
   }
-  vs_finish_kernel<kGrid><<<b_fin, T, sm_fin, st>>>(lib, prm, order, n, counters + c++, nmax, tmax,
+  mark(3, false);
+  vs_finish_kernel<kGrid><<<b_fin, T, sm_fin, st>>>(lib, prm, order, n, counters + c, nmax, tmax,
                                                    mvmax, sb, out);
+  mark(3, true);
   *launches += 1;
   return cudaGetLastError();
 }
@@ -790,14 +807,15 @@ static cudaError_t staged_impl(int sms, cudaStream_t st, const LibDev& lib, cons
 cudaError_t launch_staged(bool grid, int sms, cudaStream_t st, const LibDev& lib,
                           const PocketDev& pk, const float4* rots, const DockParams& prm,
                           const int* order, int n, int* counters, int nmax, int tmax, int mvmax,
-                          const StageBufs& sb, const DockOut& out, uint64_t* launches) {
+                          const StageBufs& sb, const DockOut& out, uint64_t* launches,
+                          cudaEvent_t* evs, int* kinds) {
   cudaError_t e = cudaMemcpyToSymbolAsync(c_pk, &pk, sizeof(PocketDev), 0, cudaMemcpyHostToDevice,
                                           st);
   if (e != cudaSuccess) return e;
   return grid ? staged_impl<1>(sms, st, lib, rots, prm, order, n, counters, nmax, tmax, mvmax, sb,
-                               out, launches)
+                               out, launches, evs, kinds)
               : staged_impl<0>(sms, st, lib, rots, prm, order, n, counters, nmax, tmax, mvmax, sb,
-                               out, launches);
+                               out, launches, evs, kinds);
 }
 
 int dock_blocks_per_sm(bool grid, size_t smem) {

@@ -33,7 +33,8 @@ static bool staged_mode() {
 cudaError_t launch_staged(bool grid, int sms, cudaStream_t st, const LibDev& lib,
                           const PocketDev& pk, const float4* rots, const DockParams& prm,
                           const int* order, int n, int* counters, int nmax, int tmax, int mvmax,
-                          const StageBufs& sb, const DockOut& out, uint64_t* launches);
+                          const StageBufs& sb, const DockOut& out, uint64_t* launches,
+                          cudaEvent_t* evs, int* kinds);
 cudaError_t launch_dock(bool grid, int blocks, size_t smem, cudaStream_t st, const LibDev& lib,
                         const PocketDev& pk, const float4* rots, const DockParams& prm,
                         const int* order, int n_order, int* counter, int nmax, int tmax,
@@ -147,7 +148,10 @@ struct vs_handle {
   int rots_k = -1;
   uint64_t rots_seed = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::vector<cudaEvent_t> pev;  // per-launch event pairs of the staged dock
+  std::vector<int> pkind;        // kernel kind of each pair (0 start .. 3 finish)
   bool timed = false;
+  bool staged_run = false;
 };
 
 namespace {
@@ -408,6 +412,7 @@ void vs_destroy(vs_handle* h) {
     b->release();
   cudaEventDestroy(h->ev0);
   cudaEventDestroy(h->ev1);
+  for (cudaEvent_t e : h->pev) cudaEventDestroy(e);
   cudaStreamDestroy(h->own);
   delete h;
 }
@@ -630,9 +635,18 @@ int vs_dock(vs_handle* h, const vs_dock_params* prm, void* stream) {
     sb.kp = h->d_sg_kp.as<float>();
     sb.km = h->d_sg_km.as<int>();
     sb.st = h->d_sg_st.as<unsigned long long>();
+    const size_t npairs = 3 * static_cast<size_t>(R) + 1;
+    while (h->pev.size() < 2 * npairs) {
+      cudaEvent_t e;
+      VS_CUDA(h, cudaEventCreate(&e));
+      h->pev.push_back(e);
+    }
+    h->pkind.assign(npairs, 0);
     VS_CUDA(h, launch_staged(grid, h->sms, st, ld, h->pk, h->d_rots.as<const float4>(), dp,
                              P.d_order.as<int>() + b.start, b.count, h->d_counters.as<int>(),
-                             b.nmax, b.tmax, b.mvmax, sb, out, &h->launches));
+                             b.nmax, b.tmax, b.mvmax, sb, out, &h->launches, h->pev.data(),
+                             h->pkind.data()));
+    h->staged_run = true;
   } else if (b.count > 0) {
     const size_t smem = dock_smem_per_block(b.nmax, b.tmax, b.mvmax);
     if (smem > 227 * 1024) return fail(h, VS_ERR_CAPACITY, "ligands need too much shared memory");
@@ -649,6 +663,7 @@ int vs_dock(vs_handle* h, const vs_dock_params* prm, void* stream) {
                            b.nmax, b.tmax, b.mvmax, h->d_sx.as<float4>(), h->d_sp.as<float>(),
                            h->d_sm.as<int>(), out));
     ++h->launches;
+    h->staged_run = false;
   }
   VS_CUDA(h, cudaEventRecord(h->ev1, st));
   h->timed = true;
@@ -666,6 +681,22 @@ double vs_last_dock_ms(const vs_handle* h) {
 }
 
 uint64_t vs_launch_count(const vs_handle* h) { return h->launches; }
+
+int vs_last_phase_ms(vs_handle* h, double out[4]) {
+  if (!h->timed) return fail(h, VS_ERR_STATE, "no dock has run");
+  for (int k = 0; k < 4; ++k) out[k] = 0.0;
+  VS_CUDA(h, cudaEventSynchronize(h->ev1));
+  if (!h->staged_run) {
+    out[2] = vs_last_dock_ms(h);
+    return VS_OK;
+  }
+  for (size_t i = 0; i < h->pkind.size(); ++i) {
+    float ms = 0.0f;
+    VS_CUDA(h, cudaEventElapsedTime(&ms, h->pev[2 * i], h->pev[2 * i + 1]));
+    out[h->pkind[i]] += ms;
+  }
+  return VS_OK;
+}
 
 int vs_last_stats(vs_handle* h, uint64_t out[8]) {
   if (!h->has_results) return fail(h, VS_ERR_STATE, "no results");

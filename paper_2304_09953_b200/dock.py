@@ -331,6 +331,12 @@ class Engine:
     def launch_count(self) -> int:
         return int(_lib.vs_launch_count(self._h))
 
+    def phase_ms(self) -> dict:
+        """Device ms of the last dock per kernel (capi.h vs_last_phase_ms)."""
+        out = (C.c_double * 4)()
+        check(_lib.vs_last_phase_ms(self._h, out), self._h, "phase_ms")
+        return dict(zip(("start", "sweep", "flex", "finish"), (float(v) for v in out)))
+
     def stats(self) -> dict:
         """Work counters of the last dock (capi.h vs_last_stats)."""
         out = np.zeros(8, np.uint64)

@@ -1,10 +1,11 @@
 """Summarise one profiling round (tools/profile_round.sh TAG) into profiles/:
 
   profiles/<TAG>_launches.json     per-kernel share of the bench launch list
-  profiles/<TAG>_dock_ncu.json     key metrics + stall breakdown of the dock kernel
-  profiles/<TAG>_dock_functions.txt per-subroutine samples (tools/ncu_funcs.py)
-  profiles/<TAG>_dock_lines.txt    hottest source lines (tools/sass_lines.py)
-  profiles/ncu_dock_traffic.json   DRAM bytes per C2 dock launch (bench roofline.traffic)
+  profiles/<TAG>_dock_ncu.json     key metrics + stall breakdown of each profiled dock kernel
+  profiles/<TAG>_<kernel>_functions.txt per-subroutine samples (tools/ncu_funcs.py)
+  profiles/<TAG>_<kernel>_lines.txt    hottest source lines (tools/sass_lines.py)
+  profiles/ncu_dock_traffic.json   DRAM bytes per C2 launch of each dock kernel (bench
+                                   roofline.traffic)
 
   python tools/ncu_summary.py TAG     (reads gpurun_out/*_TAG.*, needs ncu + nvdisasm)
 """
@@ -44,7 +45,7 @@ def launches(tag):
     ik, iv = h.index("Kernel Name"), h.index("Metric Value")
     agg = collections.defaultdict(lambda: [0, 0.0])
     for r in rows[1:]:
-        name = r[ik].split("(")[0].replace("void ", "")
+        name = r[ik].split("(")[0].replace("void ", "").split("<")[0]
         agg[name][0] += 1
         agg[name][1] += float(r[iv].replace(",", ""))
     tot = sum(v[1] for v in agg.values())
@@ -59,13 +60,21 @@ def launches(tag):
 def traffic(tag):
     rows = [r for r in csv.reader(open(os.path.join(OUT, f"traffic_{tag}.csv"))) if len(r) > 10]
     h = rows[0]
-    vals = {r[h.index("Metric Name")]: float(r[h.index("Metric Value")].replace(",", ""))
-            for r in rows[1:]}
-    rd, wr = vals["dram__bytes_read.sum"], vals["dram__bytes_write.sum"]
-    return {"source": f"ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum -k vs_dock_kernel "
-                      f"-c 1 on bench.py (C2, 100k ligands, one launch), gpurun_out/traffic_{tag}.csv",
-            "dram_bytes_read": rd, "dram_bytes_write": wr, "dram_bytes_per_launch": rd + wr,
-            "kernel_ns": vals.get("gpu__time_duration.sum")}
+    ik, im, iv = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value")
+    per = {}
+    for r in rows[1:]:
+        name = r[ik].split("(")[0].replace("void ", "").split("<")[0].split("::")[-1]
+        d = per.setdefault(name, {})
+        if r[im] not in d:  # first launch of each kernel
+            d[r[im]] = float(r[iv].replace(",", ""))
+    kernels = {}
+    for name, v in per.items():
+        rd, wr = v.get("dram__bytes_read.sum", 0.0), v.get("dram__bytes_write.sum", 0.0)
+        kernels[name] = {"dram_bytes_read": rd, "dram_bytes_write": wr,
+                         "dram_bytes_per_launch": rd + wr, "kernel_ns": v.get("gpu__time_duration.sum")}
+    return {"source": f"ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum on the first C2 "
+                      f"launch of each dock kernel (bench.py, 100k ligands), gpurun_out/traffic_{tag}.csv",
+            "kernels": kernels}
 
 
 def dock_report(tag):
@@ -73,22 +82,25 @@ def dock_report(tag):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
-    d = dict(zip(rows[0], rows[2]))
     out = {"source": f"ncu --set full --clock-control none --import-source on, tools/profile_dock.py "
                      f"--ligands 20000 (C2 library prefix), gpurun_out/prof_dock_{tag}.ncu-rep",
-           "metrics": {k: d.get(k) for k in METRICS}, "stalls_per_issue": {}}
-    for k, v in d.items():
-        if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith(
-                "_per_issue_active.ratio"):
-            try:
-                if float(v) >= 0.05:
-                    out["stalls_per_issue"][k[len("smsp__average_warps_issue_stalled_"):-len(
-                        "_per_issue_active.ratio")]] = round(float(v), 3)
-            except ValueError:
-                pass
-    src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
-                         capture_output=True, text=True).stdout
-    return out, src
+           "kernels": {}}
+    for row in rows[2:]:
+        d = dict(zip(rows[0], row))
+        name = d.get("Kernel Name", "?").split("(")[0].replace("void ", "").split("<")[0]
+        name = name.split("::")[-1]
+        k = {"metrics": {m: d.get(m) for m in METRICS}, "stalls_per_issue": {}}
+        for key, v in d.items():
+            if key.startswith("smsp__average_warps_issue_stalled_") and key.endswith(
+                    "_per_issue_active.ratio"):
+                try:
+                    if float(v) >= 0.05:
+                        k["stalls_per_issue"][key[len("smsp__average_warps_issue_stalled_"):-len(
+                            "_per_issue_active.ratio")]] = round(float(v), 3)
+                except ValueError:
+                    pass
+        out["kernels"][name] = k
+    return out, rep
 
 
 def main(tag):
@@ -96,26 +108,30 @@ def main(tag):
     json.dump(launches(tag), open(os.path.join(PROF, f"{tag}_launches.json"), "w"), indent=1)
     t = traffic(tag)
     json.dump(t, open(os.path.join(PROF, "ncu_dock_traffic.json"), "w"), indent=1)
-    summ, src = dock_report(tag)
-    summ["dram_traffic_c2_launch"] = t
+    summ, rep = dock_report(tag)
+    summ["dram_traffic_c2_first_launch"] = t["kernels"]
     json.dump(summ, open(os.path.join(PROF, f"{tag}_dock_ncu.json"), "w"), indent=1)
+    import ncu_funcs
+    import sass_lines
     with tempfile.TemporaryDirectory() as td:
         lib = os.path.join(ROOT, "paper_2304_09953_b200", "libvscreen_gpu.so")
         subprocess.run(["cuobjdump", "-xelf", "all", lib], cwd=td, capture_output=True)
         sass = os.path.join(td, "dock.sass")
         with open(sass, "w") as f:
             subprocess.run(["nvdisasm", "-g", os.path.join(td, "vs_dock.sm_100a.cubin")], stdout=f)
-        csvp = os.path.join(td, "src.csv")
-        open(csvp, "w").write(src)
-        import ncu_funcs
-        import sass_lines
-        kp = "_ZN2vs14vs_dock_kernelILi1EE"
-        for name, fn in (("functions", lambda: ncu_funcs.main(csvp, sass, kp)),
-                         ("lines", lambda: sass_lines.main(csvp, sass, kp, 40))):
-            buf = io.StringIO()
-            with redirect_stdout(buf):
-                fn()
-            open(os.path.join(PROF, f"{tag}_dock_{name}.txt"), "w").write(buf.getvalue())
+        for kname in summ["kernels"]:
+            src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source",
+                                  "sass", "--kernel-name", f"regex:{kname}"],
+                                 capture_output=True, text=True).stdout
+            csvp = os.path.join(td, f"{kname}.csv")
+            open(csvp, "w").write(src)
+            kp = f"_ZN2vs{len(kname)}{kname}ILi1EE"
+            for part, fn in (("functions", lambda: ncu_funcs.main(csvp, sass, kp)),
+                             ("lines", lambda: sass_lines.main(csvp, sass, kp, 40))):
+                buf = io.StringIO()
+                with redirect_stdout(buf):
+                    fn()
+                open(os.path.join(PROF, f"{tag}_{kname}_{part}.txt"), "w").write(buf.getvalue())
     print("wrote", sorted(f for f in os.listdir(PROF) if f.startswith(tag) or f.startswith("ncu_")))
 
 
