@@ -425,7 +425,11 @@ __device__ __forceinline__ float off_grid_term(float gx, float gy, float gz) {
   return -(c_pk.lam * ((c_pk.r - w) * 10.0f));
 }
 
-template <int kGrid>
+// kU atoms per iteration (kU even or 1): the kU cell loads are all issued
+// before the first interpolation, so a warp keeps kU lookups in flight; a
+// ragged tail re-reads the last atom and drops its term.  Atom i goes to the
+// parity accumulator of i, so every kU gives the same key bits.
+template <int kGrid, int kU = 1>
 static __device__ __forceinline__ float eval_key(const PocketDev& pk, const float4* ys, int N,
                                                  const Mat3 R, float tx, float ty, float tz) {
   if (kGrid) {
@@ -438,71 +442,46 @@ static __device__ __forceinline__ float eval_key(const PocketDev& pk, const floa
     const unsigned mx = static_cast<unsigned>(g.nx - 2), my = static_cast<unsigned>(g.ny - 2),
                    mz = static_cast<unsigned>(g.nz - 2);
     float ke = 0.0f, ko = 0.0f;
-#ifdef VS_KEY_U2
-    // two atoms per iteration (even -> ke, odd -> ko): both lookups are in
-    // flight before either is consumed; a missing odd tail atom reads atom
-    // i again and is dropped
-    auto cell = [&](const float4 a, float& gx, float& gy, float& gz, float& tx1, float& ty1,
-                    float& tz1, bool& in) {
-      gx = fmaf(a00, a.x, fmaf(a01, a.y, fmaf(a02, a.z, ux)));
-      gy = fmaf(a10, a.x, fmaf(a11, a.y, fmaf(a12, a.z, uy)));
-      gz = fmaf(a20, a.x, fmaf(a21, a.y, fmaf(a22, a.z, uz)));
-      const float fx = floorf(gx), fy = floorf(gy), fz = floorf(gz);
-      const int ix = static_cast<int>(fx), iy = static_cast<int>(fy), iz = static_cast<int>(fz);
-      in = static_cast<unsigned>(ix) <= mx && static_cast<unsigned>(iy) <= my &&
-           static_cast<unsigned>(iz) <= mz;
-      tx1 = gx - fx;
-      ty1 = gy - fy;
-      tz1 = gz - fz;
-      return g.key_c + 2 * (in ? (iz * (g.ny - 1) + iy) * (g.nx - 1) + ix : 0);
-    };
-    auto interp = [](const float4 lo, const float4 hi, float tx1, float ty1, float tz1) {
-      const float c00 = det_lerp(lo.x, lo.y, tx1), c10 = det_lerp(lo.z, lo.w, tx1);
-      const float c01 = det_lerp(hi.x, hi.y, tx1), c11 = det_lerp(hi.z, hi.w, tx1);
-      return det_lerp(det_lerp(c00, c10, ty1), det_lerp(c01, c11, ty1), tz1);
-    };
 #pragma unroll 1
-    for (int i = 0; i < N; i += 2) {
-      const bool two = i + 1 < N;
-      float gx0, gy0, gz0, tx0, ty0, tz0, gx1, gy1, gz1, tx1, ty1, tz1;
-      bool in0, in1;
-      const float4* c0 = cell(ys[i], gx0, gy0, gz0, tx0, ty0, tz0, in0);
-      const float4* c1 = cell(ys[two ? i + 1 : i], gx1, gy1, gz1, tx1, ty1, tz1, in1);
-      const float4 lo0 = __ldg(c0), hi0 = __ldg(c0 + 1), lo1 = __ldg(c1), hi1 = __ldg(c1 + 1);
-      const float t0 = in0 ? interp(lo0, hi0, tx0, ty0, tz0) : off_grid_term(gx0, gy0, gz0);
-      ke = ke + t0;
-      if (two) {
-        const float t1 = in1 ? interp(lo1, hi1, tx1, ty1, tz1) : off_grid_term(gx1, gy1, gz1);
-        ko = ko + t1;
+    for (int i0 = 0; i0 < N; i0 += kU) {
+      float gx[kU], gy[kU], gz[kU], fx[kU], fy[kU], fz[kU];
+      bool in[kU];
+      float4 lo[kU], hi[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const float4 a = ys[i0 + u < N ? i0 + u : N - 1];
+        gx[u] = fmaf(a00, a.x, fmaf(a01, a.y, fmaf(a02, a.z, ux)));
+        gy[u] = fmaf(a10, a.x, fmaf(a11, a.y, fmaf(a12, a.z, uy)));
+        gz[u] = fmaf(a20, a.x, fmaf(a21, a.y, fmaf(a22, a.z, uz)));
+        fx[u] = floorf(gx[u]);
+        fy[u] = floorf(gy[u]);
+        fz[u] = floorf(gz[u]);
+        const int ix = static_cast<int>(fx[u]), iy = static_cast<int>(fy[u]),
+                  iz = static_cast<int>(fz[u]);
+        in[u] = static_cast<unsigned>(ix) <= mx && static_cast<unsigned>(iy) <= my &&
+                static_cast<unsigned>(iz) <= mz;
+        ldg_cell(g.key_c + 2 * (in[u] ? (iz * (g.ny - 1) + iy) * (g.nx - 1) + ix : 0), lo[u],
+                 hi[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        float term;
+        if (in[u]) {
+          const float tx1 = gx[u] - fx[u], ty1 = gy[u] - fy[u], tz1 = gz[u] - fz[u];
+          const float c00 = det_lerp(lo[u].x, lo[u].y, tx1), c10 = det_lerp(lo[u].z, lo[u].w, tx1);
+          const float c01 = det_lerp(hi[u].x, hi[u].y, tx1), c11 = det_lerp(hi[u].z, hi[u].w, tx1);
+          term = det_lerp(det_lerp(c00, c10, ty1), det_lerp(c01, c11, ty1), tz1);
+        } else {
+          term = off_grid_term(gx[u], gy[u], gz[u]);
+        }
+        if (kU == 1 || i0 + u < N) {
+          if ((kU == 1 ? i0 : u) & 1)
+            ko = ko + term;
+          else
+            ke = ke + term;
+        }
       }
     }
-#else
-#pragma unroll 1
-    for (int i = 0; i < N; ++i) {
-      const float4 a = ys[i];
-      const float gx = fmaf(a00, a.x, fmaf(a01, a.y, fmaf(a02, a.z, ux)));
-      const float gy = fmaf(a10, a.x, fmaf(a11, a.y, fmaf(a12, a.z, uy)));
-      const float gz = fmaf(a20, a.x, fmaf(a21, a.y, fmaf(a22, a.z, uz)));
-      const float fx = floorf(gx), fy = floorf(gy), fz = floorf(gz);
-      const int ix = static_cast<int>(fx), iy = static_cast<int>(fy), iz = static_cast<int>(fz);
-      float term;
-      if (static_cast<unsigned>(ix) <= mx && static_cast<unsigned>(iy) <= my &&
-          static_cast<unsigned>(iz) <= mz) {
-        float4 lo, hi;
-        ldg_cell(g.key_c + 2 * ((iz * (g.ny - 1) + iy) * (g.nx - 1) + ix), lo, hi);
-        const float tx1 = gx - fx, ty1 = gy - fy, tz1 = gz - fz;
-        const float c00 = det_lerp(lo.x, lo.y, tx1), c10 = det_lerp(lo.z, lo.w, tx1);
-        const float c01 = det_lerp(hi.x, hi.y, tx1), c11 = det_lerp(hi.z, hi.w, tx1);
-        term = det_lerp(det_lerp(c00, c10, ty1), det_lerp(c01, c11, ty1), tz1);
-      } else {
-        term = off_grid_term(gx, gy, gz);
-      }
-      if (i & 1)
-        ko = ko + term;
-      else
-        ke = ke + term;
-    }
-#endif
     return ke + ko;
   }
   float fe = 0.0f, fo = 0.0f, we = 0.0f, wo = 0.0f;

@@ -12,6 +12,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+
 #include "vs_common.cuh"
 
 #ifndef VS_PHASE
@@ -72,6 +74,10 @@ static __device__ VS_PHASE int start_phase(const PocketDev& pk, const Dims d,
 // ---- rigid roto-translation sweep (SWEEP_V1.md §2.3-2.4): K orientations
 // about the posed centroid (lanes over rotations), then a compass search
 // over the 26 lattice neighbours with halving steps.  FP32 key F - lam W.
+#ifndef VS_SWEEP_U
+#define VS_SWEEP_U 1  // atoms per sweep-key iteration in the staged sweep kernel
+#endif
+
 template <int kGrid, bool kInl = false>
 static __device__ VS_PHASE int sweep_phase(const PocketDev& pk, const Dims d,
                                                const float4* __restrict__ rots, int K, int N,
@@ -104,7 +110,7 @@ static __device__ VS_PHASE int sweep_phase(const PocketDev& pk, const Dims d,
     const Mat3 Rk = det_quat_mat(w4, x4, y4, z4);
     float vx, vy, vz;
     det_apply(Rk, cx, cy, cz, 0.0f, 0.0f, 0.0f, &vx, &vy, &vz);
-    const float key = kInl ? eval_key<kGrid>(pk, s.ysf, N, Rk, Cx - vx, Cy - vy, Cz - vz)
+    const float key = kInl ? eval_key<kGrid, VS_SWEEP_U>(pk, s.ysf, N, Rk, Cx - vx, Cy - vy, Cz - vz)
                            : eval_rigid<kGrid>(pk, s.ysf, N, Rk, Cx - vx, Cy - vy, Cz - vz);
     if (key > best_key) {
       best_key = key;
@@ -140,7 +146,7 @@ static __device__ VS_PHASE int sweep_phase(const PocketDev& pk, const Dims d,
     float key = -INFINITY, ox = 0.0f, oy = 0.0f, oz = 0.0f;
     if (lane < 27) {
       trans_offset(lane, sc, &ox, &oy, &oz);
-      key = kInl ? eval_key<kGrid>(pk, s.ysf, N, RS, ptx + ox, pty + oy, ptz + oz)
+      key = kInl ? eval_key<kGrid, VS_SWEEP_U>(pk, s.ysf, N, RS, ptx + ox, pty + oy, ptz + oz)
                  : eval_rigid<kGrid>(pk, s.ysf, N, RS, ptx + ox, pty + oy, ptz + oz);
     }
     int li = lane < 27 ? lane : 0x7fffffff;
@@ -734,8 +740,19 @@ cudaError_t launch_dock(bool grid, int blocks, size_t smem, cudaStream_t st, con
 
 // ---------------------------------------------------------- staged launch
 template <class K>
-static int stage_blocks(K kernel, size_t smem, int sms, int n_items) {
+static int stage_blocks(K kernel, size_t smem, int sms, int n_items, int target_per_sm) {
   prep_dock(kernel, smem);
+  // shared-memory carveout just large enough for target_per_sm blocks: the
+  // rest of the 256 KB stays L1 for the grid-cell gathers (the sweep kernel
+  // needs ~32 KB of shared memory per SM and reuses cells across the
+  // translation lattice); VSCREEN_CARVEOUT_MAXSHARED=1 restores max shared
+  const char* ms = std::getenv("VSCREEN_CARVEOUT_MAXSHARED");
+  if (!(ms && ms[0] == '1')) {
+    const size_t need = static_cast<size_t>(target_per_sm) * (smem + 1024);
+    int pct = static_cast<int>((need * 100 + 228 * 1024 - 1) / (228 * 1024)) + 1;
+    pct = pct > 100 ? 100 : pct;
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+  }
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kWarpsPerBlock * 32, smem);
   if (per_sm < 1) per_sm = 1;
@@ -767,10 +784,10 @@ static cudaError_t staged_impl(int sms, cudaStream_t st, const LibDev& lib, cons
                                               nmax, tmax, mvmax,
                                               kLayLig | kLayState | kLayPosed | kLayFlex);
   const size_t sm_fin = kWarpsPerBlock * warp_smem_bytes(nmax, tmax, mvmax, kLayLig | kLayKept);
-  const int b_start = stage_blocks(vs_start_kernel<kGrid>, sm_start, sms, n);
-  const int b_sweep = stage_blocks(vs_sweep_kernel<kGrid>, sm_sweep, sms, n);
-  const int b_flex = stage_blocks(vs_flex_kernel<kGrid>, sm_flex, sms, n);
-  const int b_fin = stage_blocks(vs_finish_kernel<kGrid>, sm_fin, sms, n);
+  const int b_start = stage_blocks(vs_start_kernel<kGrid>, sm_start, sms, n, 8);
+  const int b_sweep = stage_blocks(vs_sweep_kernel<kGrid>, sm_sweep, sms, n, VS_MINB_SWEEP);
+  const int b_flex = stage_blocks(vs_flex_kernel<kGrid>, sm_flex, sms, n, VS_MINB_FLEX);
+  const int b_fin = stage_blocks(vs_finish_kernel<kGrid>, sm_fin, sms, n, 8);
   const int T = kWarpsPerBlock * 32;
   int c = 0;
   auto mark = [&](int kind, bool after) {  // event pair c: launch c (counter c)

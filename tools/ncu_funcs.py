@@ -27,19 +27,25 @@ def main(csv_path, sass_path, kprefix):
         if re.search(r'/\*[0-9a-f]{4,}\*/', l):
             ins.append(fn)
     rows = list(csv.reader(open(csv_path)))
-    hdr, data = rows[1], rows[2:]
+    hdr = rows[1]
+    data = []
+    for r in rows[2:]:  # first kernel section only
+        if len(r) < len(hdr):
+            break
+        data.append(r)
     ia = hdr.index("Warp Stall Sampling (All Samples)")
     ie = hdr.index("Instructions Executed")
     ino = hdr.index("stall_no_inst")
     ilsb = hdr.index("stall_long_sb")
     agg = collections.defaultdict(lambda: [0, 0, 0, 0, 0])
+    num = lambda v: int(v) if v.strip() else 0
     for f, r in zip(ins, data):
         a = agg[f]
         a[0] += 1
-        a[1] += int(r[ia])
-        a[2] += int(r[ie])
-        a[3] += int(r[ino])
-        a[4] += int(r[ilsb])
+        a[1] += num(r[ia])
+        a[2] += num(r[ie])
+        a[3] += num(r[ino])
+        a[4] += num(r[ilsb])
     tot = sum(a[1] for a in agg.values())
     te = sum(a[2] for a in agg.values())
     print(f"{'function':20s} {'instrs':>6s} {'samp%':>6s} {'exec%':>6s} {'no_inst':>7s} {'long_sb':>7s}")

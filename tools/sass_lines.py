@@ -27,20 +27,26 @@ def main(csv_path, sass_path, kprefix, top=60):
         if re.search(r'/\*[0-9a-f]{4,}\*/', l):
             lines.append((fn, cur))
     rows = list(csv.reader(open(csv_path)))
-    hdr, data = rows[1], rows[2:]
+    hdr = rows[1]
+    data = []
+    for r in rows[2:]:  # first kernel section only
+        if len(r) < len(hdr):
+            break
+        data.append(r)
     ia = hdr.index("Warp Stall Sampling (All Samples)")
     ie = hdr.index("Instructions Executed")
     cols = ["stall_no_inst", "stall_long_sb", "stall_wait", "stall_short_sb", "stall_math",
             "stall_branch_resolving", "stall_mio", "stall_lg"]
     ic = [hdr.index(c) for c in cols]
-    tot = sum(int(r[ia]) for r in data)
+    num = lambda v: int(v) if v.strip() else 0
+    tot = sum(num(r[ia]) for r in data)
     agg = collections.defaultdict(lambda: [0, 0] + [0] * len(cols))
     for (fn, ln), r in zip(lines, data):
         a = agg[ln]
-        a[0] += int(r[ia])
-        a[1] += int(r[ie])
+        a[0] += num(r[ia])
+        a[1] += num(r[ie])
         for k, c in enumerate(ic):
-            a[2 + k] += int(r[c])
+            a[2 + k] += num(r[c])
     print(f"{'line':28s} {'samp%':>6s} {'exec':>12s} " + " ".join(c[6:12] for c in cols))
     for ln, a in sorted(agg.items(), key=lambda x: -x[1][0])[:top]:
         print(f"{str(ln):28s} {100 * a[0] / tot:6.2f} {a[1]:12d} " +
