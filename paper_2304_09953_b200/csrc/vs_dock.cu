@@ -273,9 +273,17 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
         for (int wd = 0; wd < W; ++wd) {
           unsigned b2 = ~mk[wd];
           if (wd == W - 1 && (N & 31)) b2 &= (1u << (N & 31)) - 1u;
-          for (; b2; b2 &= b2 - 1u) {
-            const double4 yk = s.ys[wd * 32 + __ffs(b2) - 1];
+          if (!b2) continue;
+          // the next partner's coordinates are loaded before this pair's
+          // test (shared-memory latency off the dependent chain)
+          const double4* yw = s.ys + wd * 32;
+          double4 yk = yw[__ffs(b2) - 1];
+          while (true) {
+            b2 &= b2 - 1u;
+            const double4 yn = yw[b2 ? __ffs(b2) - 1 : 0];
             pc = pc + pair_term_d(pk, yx - yk.x, yy - yk.y, yz - yk.z, nact);
+            if (!b2) break;
+            yk = yn;
           }
         }
       }
