@@ -11,6 +11,7 @@
 #include <cstring>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/vscreen_gpu/capi.h"
@@ -87,13 +88,50 @@ struct Bucket {
 };
 
 // Packed library (host staging + device copies) for one set of ligands.
+// Growable page-locked host array: the packed library is written straight
+// into pinned memory, so the upload is one async DMA per array.
+template <class T>
+struct PinnedVec {
+  T* p = nullptr;
+  size_t n = 0, cap = 0;
+  PinnedVec() = default;
+  PinnedVec(const PinnedVec&) = delete;
+  PinnedVec& operator=(const PinnedVec&) = delete;
+  ~PinnedVec() {
+    if (p) cudaFreeHost(p);
+  }
+  bool resize(size_t m) {
+    if (m > cap) {
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+      cap = 0;
+      const size_t want = std::max<size_t>(m + m / 4, 64);
+      if (cudaHostAlloc(reinterpret_cast<void**>(&p), want * sizeof(T), cudaHostAllocDefault) !=
+          cudaSuccess) {
+        p = nullptr;
+        n = 0;
+        return false;
+      }
+      cap = want;
+    }
+    n = m;
+    return true;
+  }
+  size_t size() const { return n; }
+  bool empty() const { return n == 0; }
+  T* data() { return p; }
+  const T* data() const { return p; }
+  T& operator[](size_t i) { return p[i]; }
+  const T& operator[](size_t i) const { return p[i]; }
+};
+
 struct Packed {
   int n = 0;
-  std::vector<int4> meta;
-  std::vector<int2> mov;
-  std::vector<double4> atoms;
-  std::vector<int4> axes;
-  std::vector<uint8_t> moving;
+  PinnedVec<int4> meta;
+  PinnedVec<int2> mov;
+  PinnedVec<double4> atoms;
+  PinnedVec<int4> axes;
+  PinnedVec<uint8_t> moving;
   std::vector<unsigned long long> seeds;
   std::vector<unsigned int> id_rank;
   std::vector<int> order;
@@ -185,47 +223,25 @@ int pack_library(vs_handle* h, const vs_library* L, const vs_size_class* classes
   const int n = L->n_ligands;
   if (n < 0) return fail(h, VS_ERR_INVALID_ARGUMENT, "negative ligand count");
   P.n = n;
-  P.meta.assign(n, int4{0, 0, 0, 0});
-  P.mov.assign(n, int2{0, 0});
-  P.atoms.clear();
-  P.axes.clear();
-  P.moving.clear();
   P.seeds.assign(n, 0ull);
   P.id_rank.assign(n, 0u);
   P.cls.assign(n, -1);
   P.tors_off.assign(n + 1, 0);
-  long ao = 0, to = 0, mo = 0;
-  std::vector<long> cost(n, 0);
+  // pass 1 (sequential, O(n)): counts, offsets, classes, LPT cost
+  std::vector<long> cost(n, 0), aoff(n + 1, 0), moff(n + 1, 0), msrc(n + 1, 0), toff(n + 1, 0);
   for (int i = 0; i < n; ++i) {
     const int N = L->n_atoms[i], T = L->n_tors[i];
     if (N < 1) return fail(h, VS_ERR_ATOM_COUNT, "conformer has no atoms (ligand " + std::to_string(i) + ")");
     if (N > kMaxAtoms || T > kMaxTors)
       return fail(h, VS_ERR_CAPACITY, "ligand " + std::to_string(i) + " exceeds GPU limits");
-    P.tors_off[i] = to;
-    P.meta[i] = int4{static_cast<int>(P.atoms.size()), N, static_cast<int>(P.axes.size()), T};
-    for (int a = 0; a < N; ++a) {
-      const double* c = L->coords + 3 * (ao + a);
-      P.atoms.push_back(double4{c[0], c[1], c[2], static_cast<double>(L->atom_class[ao + a])});
-    }
-    const size_t mov_start = P.moving.size();
-    int mv = 0;
-    for (int j = 0; j < T; ++j) {
-      const int a = L->axis_a[to + j], b = L->axis_b[to + j], cnt = L->moving_count[to + j];
-      if (a < 0 || b < 0 || a >= N || b >= N)
-        return fail(h, VS_ERR_ATOM_COUNT, "torsion topology does not fit conformer");
-      P.axes.push_back(int4{a, b, mv, cnt});
-      for (int m = 0; m < cnt; ++m) {
-        const int idx = L->moving[mo + m];
-        if (idx < 0 || idx >= N)
-          return fail(h, VS_ERR_ATOM_COUNT, "moving atom outside conformer");
-        P.moving.push_back(static_cast<uint8_t>(idx));
-      }
-      mo += cnt;
-      mv += cnt;
-    }
-    const size_t padded = align16z(static_cast<size_t>(mv));
-    P.moving.resize(mov_start + padded, 0);
-    P.mov[i] = int2{static_cast<int>(mov_start), static_cast<int>(padded)};
+    if (T < 0) return fail(h, VS_ERR_INVALID_ARGUMENT, "negative torsion count");
+    long mv = 0;
+    for (int j = 0; j < T; ++j) mv += L->moving_count[toff[i] + j];
+    aoff[i + 1] = aoff[i] + N;
+    toff[i + 1] = toff[i] + T;
+    msrc[i + 1] = msrc[i] + mv;
+    moff[i + 1] = moff[i] + static_cast<long>(align16z(static_cast<size_t>(mv)));
+    P.tors_off[i] = toff[i];
     P.seeds[i] = L->seeds ? L->seeds[i] : 0ull;
     P.id_rank[i] = L->id_rank ? L->id_rank[i] : static_cast<unsigned>(i);
     const int rot = L->rot_bonds ? L->rot_bonds[i] : T;
@@ -237,52 +253,105 @@ int pack_library(vs_handle* h, const vs_library* L, const vs_size_class* classes
     }
     const long pairs = static_cast<long>(N) * (N - 1) / 2;
     cost[i] = 256L * N + 32L * T * (N + pairs + mv);
-    ao += N;
-    to += T;
   }
+  if (!P.meta.resize(std::max(n, 1)) || !P.mov.resize(std::max(n, 1)) ||
+      !P.atoms.resize(std::max<long>(aoff[n], 1)) || !P.axes.resize(std::max<long>(toff[n], 1)) ||
+      !P.moving.resize(std::max<long>(moff[n], 16)))
+    return fail(h, VS_ERR_CUDA, "pinned host allocation failed");
+  if (aoff[n] == 0) P.atoms[0] = double4{0, 0, 0, 0};
+  if (toff[n] == 0) P.axes[0] = int4{0, 0, 0, 0};
+  if (moff[n] == 0) std::memset(P.moving.data(), 0, 16);
+  // pass 2 (threads over ligand ranges): fill + validate; the error of the
+  // lowest failing ligand is the one reported (same as a sequential pass)
+  const int nth = std::max(1, std::min<int>(32, static_cast<int>(std::thread::hardware_concurrency())));
+  std::vector<int> bad(nth, -1), bad_code(nth, 0);
+  std::vector<std::string> bad_msg(nth);
+  auto fill = [&](int t) {
+    const int lo = static_cast<int>(static_cast<long>(n) * t / nth);
+    const int hi = static_cast<int>(static_cast<long>(n) * (t + 1) / nth);
+    for (int i = lo; i < hi; ++i) {
+      const int N = L->n_atoms[i], T = L->n_tors[i];
+      P.meta[i] = int4{static_cast<int>(aoff[i]), N, static_cast<int>(toff[i]), T};
+      for (int a = 0; a < N; ++a) {
+        const double* c = L->coords + 3 * (aoff[i] + a);
+        P.atoms[aoff[i] + a] = double4{c[0], c[1], c[2], static_cast<double>(L->atom_class[aoff[i] + a])};
+      }
+      long mo = msrc[i];
+      int mv = 0;
+      uint8_t* dst = P.moving.data() + moff[i];
+      for (int j = 0; j < T; ++j) {
+        const long tj = toff[i] + j;
+        const int a = L->axis_a[tj], b = L->axis_b[tj], cnt = L->moving_count[tj];
+        if (a < 0 || b < 0 || a >= N || b >= N) {
+          bad[t] = i;
+          bad_code[t] = VS_ERR_ATOM_COUNT;
+          bad_msg[t] = "torsion topology does not fit conformer";
+          return;
+        }
+        P.axes[tj] = int4{a, b, mv, cnt};
+        for (int m = 0; m < cnt; ++m) {
+          const int idx = L->moving[mo + m];
+          if (idx < 0 || idx >= N) {
+            bad[t] = i;
+            bad_code[t] = VS_ERR_ATOM_COUNT;
+            bad_msg[t] = "moving atom outside conformer";
+            return;
+          }
+          dst[mv + m] = static_cast<uint8_t>(idx);
+        }
+        mo += cnt;
+        mv += cnt;
+      }
+      for (long z = mv; z < moff[i + 1] - moff[i]; ++z) dst[z] = 0;
+      P.mov[i] = int2{static_cast<int>(moff[i]), static_cast<int>(moff[i + 1] - moff[i])};
+    }
+  };
+  if (nth == 1 || n < 4096) {
+    for (int t = 0; t < nth; ++t) fill(t);
+  } else {
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nth; ++t) pool.emplace_back(fill, t);
+    for (auto& th : pool) th.join();
+  }
+  for (int t = 0; t < nth; ++t)
+    if (bad[t] >= 0) return fail(h, bad_code[t], bad_msg[t]);
+  const long to = toff[n];
   P.tors_off[n] = to;
   P.total_tors = to;
-  if (P.atoms.empty()) P.atoms.push_back(double4{0, 0, 0, 0});
-  if (P.axes.empty()) P.axes.push_back(int4{0, 0, 0, 0});
-  if (P.moving.empty()) P.moving.assign(16, 0);
-  // buckets: class order, LPT (descending cost, then index) inside
+  // one stable LPT sort (descending cost, then index); the per-class buckets
+  // are class-filtered views of it (same order inside each class), and the
+  // global queue over every class is the dock launch's
+  std::vector<int> lpt;
+  lpt.reserve(n);
+  for (int i = 0; i < n; ++i)
+    if (P.cls[i] >= 0) lpt.push_back(i);
+  std::stable_sort(lpt.begin(), lpt.end(), [&](int a, int b2) { return cost[a] > cost[b2]; });
   const int ncls = (classes && nc > 0) ? nc : 6;
   P.order.clear();
+  P.order.reserve(2 * lpt.size() + 1);
   P.buckets.clear();
   for (int c = 0; c < ncls; ++c) {
     Bucket b;
     b.start = static_cast<int>(P.order.size());
-    std::vector<int> ids;
-    for (int i = 0; i < n; ++i)
-      if (P.cls[i] == c) ids.push_back(i);
-    if (ids.empty()) continue;
-    std::stable_sort(ids.begin(), ids.end(), [&](int a, int b2) { return cost[a] > cost[b2]; });
-    for (int i : ids) {
+    for (int i : lpt) {
+      if (P.cls[i] != c) continue;
       b.nmax = std::max(b.nmax, P.meta[i].y);
       b.tmax = std::max(b.tmax, P.meta[i].w);
       b.mvmax = std::max(b.mvmax, P.mov[i].y);
       P.order.push_back(i);
     }
-    b.count = static_cast<int>(ids.size());
-    P.buckets.push_back(b);
+    b.count = static_cast<int>(P.order.size()) - b.start;
+    if (b.count > 0) P.buckets.push_back(b);
   }
-  // one global LPT queue over every bucket for the dock launch: a single
-  // persistent launch has one tail instead of one per bucket
   P.all = Bucket{};
   P.all.start = static_cast<int>(P.order.size());
-  {
-    std::vector<int> ids;
-    for (int i = 0; i < n; ++i)
-      if (P.cls[i] >= 0) ids.push_back(i);
-    std::stable_sort(ids.begin(), ids.end(), [&](int a, int b2) { return cost[a] > cost[b2]; });
-    for (int i : ids) {
-      P.all.nmax = std::max(P.all.nmax, P.meta[i].y);
-      P.all.tmax = std::max(P.all.tmax, P.meta[i].w);
-      P.all.mvmax = std::max(P.all.mvmax, P.mov[i].y);
-      P.order.push_back(i);
-    }
-    P.all.count = static_cast<int>(ids.size());
+  for (int i : lpt) {
+    P.all.nmax = std::max(P.all.nmax, P.meta[i].y);
+    P.all.tmax = std::max(P.all.tmax, P.meta[i].w);
+    P.all.mvmax = std::max(P.all.mvmax, P.mov[i].y);
+    P.order.push_back(i);
   }
+  P.all.count = static_cast<int>(lpt.size());
   if (P.order.empty()) P.order.push_back(0);
   return VS_OK;
 }
@@ -295,28 +364,50 @@ int pack_library(vs_handle* h, const vs_library* L, const vs_size_class* classes
 // torsion_topology (dock.cpp:234-270) builds from a parsed SMILES graph has
 // this property (b is the DFS child of a, moving = b's DFS subtree).
 int check_nested(vs_handle* h, const Packed& P) {
-  for (int i = 0; i < P.n; ++i) {
-    const int T = P.meta[i].w;
-    if (T < 2) continue;
-    const int4* ax = P.axes.data() + P.meta[i].z;
-    const uint8_t* mv = P.moving.data() + P.mov[i].x;
-    std::vector<std::array<uint64_t, 2>> set(T, {0ull, 0ull});
-    for (int j = 0; j < T; ++j)
-      for (int m = 0; m < ax[j].w; ++m) set[j][mv[ax[j].z + m] >> 6] |= 1ull << (mv[ax[j].z + m] & 63);
-    auto has = [&](int j, int a) { return (set[j][a >> 6] >> (a & 63)) & 1ull; };
-    for (int j = 0; j < T; ++j) {
-      for (int k = j + 1; k < T; ++k) {
-        const bool sub = ((set[k][0] & ~set[j][0]) | (set[k][1] & ~set[j][1])) == 0 &&
-                         (has(j, ax[k].x) || ax[k].x == ax[j].x || ax[k].x == ax[j].y) &&
-                         (has(j, ax[k].y) || ax[k].y == ax[j].x || ax[k].y == ax[j].y);
-        const bool dis = ((set[k][0] & set[j][0]) | (set[k][1] & set[j][1])) == 0 &&
-                         !has(j, ax[k].x) && !has(j, ax[k].y);
-        if ((!sub && !dis) || has(k, ax[j].x) || has(k, ax[j].y))
-          return fail(h, VS_ERR_INVALID_ARGUMENT,
-                      "ligand " + std::to_string(i) + ": torsion topology is not a torsion tree");
+  const int n = P.n;
+  const int nth = std::max(1, std::min<int>(32, static_cast<int>(std::thread::hardware_concurrency())));
+  std::vector<int> bad(nth, -1);
+  auto run = [&](int t) {
+    const int lo = static_cast<int>(static_cast<long>(n) * t / nth);
+    const int hi = static_cast<int>(static_cast<long>(n) * (t + 1) / nth);
+    std::array<uint64_t, 2> set[kMaxTors];
+    for (int i = lo; i < hi; ++i) {
+      const int T = P.meta[i].w;
+      if (T < 2) continue;
+      const int4* ax = P.axes.data() + P.meta[i].z;
+      const uint8_t* mv = P.moving.data() + P.mov[i].x;
+      for (int j = 0; j < T; ++j) {
+        set[j] = {0ull, 0ull};
+        for (int m = 0; m < ax[j].w; ++m)
+          set[j][mv[ax[j].z + m] >> 6] |= 1ull << (mv[ax[j].z + m] & 63);
+      }
+      auto has = [&](int j, int a) { return (set[j][a >> 6] >> (a & 63)) & 1ull; };
+      for (int j = 0; j < T; ++j) {
+        for (int k = j + 1; k < T; ++k) {
+          const bool sub = ((set[k][0] & ~set[j][0]) | (set[k][1] & ~set[j][1])) == 0 &&
+                           (has(j, ax[k].x) || ax[k].x == ax[j].x || ax[k].x == ax[j].y) &&
+                           (has(j, ax[k].y) || ax[k].y == ax[j].x || ax[k].y == ax[j].y);
+          const bool dis = ((set[k][0] & set[j][0]) | (set[k][1] & set[j][1])) == 0 &&
+                           !has(j, ax[k].x) && !has(j, ax[k].y);
+          if ((!sub && !dis) || has(k, ax[j].x) || has(k, ax[j].y)) {
+            bad[t] = i;
+            return;
+          }
+        }
       }
     }
+  };
+  if (nth == 1 || n < 4096) {
+    for (int t = 0; t < nth; ++t) run(t);
+  } else {
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nth; ++t) pool.emplace_back(run, t);
+    for (auto& th : pool) th.join();
   }
+  for (int t = 0; t < nth; ++t)
+    if (bad[t] >= 0)
+      return fail(h, VS_ERR_INVALID_ARGUMENT,
+                  "ligand " + std::to_string(bad[t]) + ": torsion topology is not a torsion tree");
   return VS_OK;
 }
 
