@@ -186,6 +186,15 @@ int vs_topk_merge_device(vs_handle* h, const uint64_t* keys_dev, int64_t n, int3
 float vs_key_score(uint64_t key);
 uint32_t vs_key_id_rank(uint64_t key);
 
+/* score_gradient (dock.cpp:284-295, Objective::grad :117-160) of given
+ * poses, FP64 on the GPU (analytic pocket; the grid is not used): score,
+ * d/dt (3 per pose), tangent-projected d/dq (4 per pose, w x y z) and
+ * central-difference d/dtorsion (h = 1e-5; n_tors of the pose's ligand per
+ * pose, in pose order).  Poses are FP64 (reference Pose). */
+int vs_score_gradient(vs_handle* h, const vs_library* lib, int64_t n_poses,
+                      const int32_t* pose_lig, const double* t, const double* q,
+                      const double* tors, double* score, double* grad_t, double* grad_q,
+                      double* grad_tors);
 /* geometric_score + rescore of given poses (dock.cpp:278, 297).  pose_lig
  * must be non-decreasing; torsions of pose p are tors[tors_off_p ...] in
  * pose order, n_tors of its ligand each. */

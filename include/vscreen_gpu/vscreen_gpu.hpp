@@ -12,6 +12,7 @@
 // Link with paper_2304_09953_b200/libvscreen_gpu.so.
 #pragma once
 
+#include <array>
 #include <cstdint>
 #include <map>
 #include <optional>
@@ -236,6 +237,40 @@ inline std::pair<double, double> score_pose(Device& dev, const Conformer& conf,
 inline double geometric_score(Device& dev, const Conformer& conf, const TorsionTopology& topo,
                               const Pose& pose, const Pocket& pocket) {
   return detail::score_pose(dev, conf, topo, pose, pocket).first;
+}
+
+struct ScoreGradient {  // dock.hpp:86-91
+  double score = 0.0;
+  Vec3 translation;
+  std::array<double, 4> rotation{};  // d/d(w, x, y, z)
+  std::vector<double> torsions;
+};
+
+// score_gradient (dock.hpp:93-94) on the GPU, FP64: analytic translation /
+// rotation derivatives, central differences (h = 1e-5) for torsions.
+inline ScoreGradient score_gradient(Device& dev, const Conformer& conf,
+                                    const TorsionTopology& topo, const Pose& pose,
+                                    const Pocket& pocket) {
+  detail::check_counts(conf, topo, pose);
+  if (pocket.bounds.empty()) throw EmptyBounds();
+  detail::set_pocket(dev, pocket);
+  detail::FlatLibrary f = detail::one(conf, topo, 0);
+  vs_library L = f.view();
+  const int32_t lig = 0;
+  const double t[3] = {pose.translation.x, pose.translation.y, pose.translation.z};
+  const double q[4] = {pose.rotation.w, pose.rotation.x, pose.rotation.y, pose.rotation.z};
+  std::vector<double> th(pose.torsions.begin(), pose.torsions.end());
+  th.push_back(0.0);
+  ScoreGradient g;
+  double gt[3], gq[4];
+  std::vector<double> gth(th.size(), 0.0);
+  check(vs_score_gradient(dev.get(), &L, 1, &lig, t, q, th.data(), &g.score, gt, gq,
+                          gth.data()),
+        dev.get());
+  g.translation = {gt[0], gt[1], gt[2]};
+  g.rotation = {gq[0], gq[1], gq[2], gq[3]};
+  g.torsions.assign(gth.begin(), gth.begin() + static_cast<long>(pose.torsions.size()));
+  return g;
 }
 
 // rescore (dock.hpp:98-99); the element classes travel in conf.atom_class.

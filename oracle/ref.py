@@ -39,6 +39,9 @@ def lib() -> C.CDLL:
             "vsref_pocket_free": (None, [C.c_void_p]),
             "vsref_geometric_score": (C.c_int, [C.c_void_p, C.c_void_p, P(C.c_double), P(C.c_double),
                                                 P(C.c_double), C.c_int, P(C.c_double)]),
+            "vsref_score_gradient": (C.c_int, [C.c_void_p, C.c_void_p, P(C.c_double),
+                                               P(C.c_double), P(C.c_double), C.c_int,
+                                               P(C.c_double)]),
             "vsref_rescore": (C.c_int, [C.c_void_p, C.c_void_p, P(C.c_double), P(C.c_double),
                                         P(C.c_double), C.c_int, P(C.c_double)]),
             "vsref_apply_pose": (C.c_int, [C.c_void_p, P(C.c_double), P(C.c_double), P(C.c_double),
@@ -158,6 +161,14 @@ class RefLigand:
         _chk(lib().vsref_geometric_score(self.h, pocket.h, _p(t, C.c_double), _p(q, C.c_double),
                                          _p(th, C.c_double), nt, C.byref(out)))
         return out.value
+
+    def score_gradient(self, pocket: RefPocket, t, q, tors):
+        """(score, gt[3], gq[4], gtor[T]) of the reference score_gradient."""
+        t, q, th, nt = self._pose(t, q, tors)
+        out = np.zeros(8 + max(nt, 1), np.float64)
+        _chk(lib().vsref_score_gradient(self.h, pocket.h, _p(t, C.c_double), _p(q, C.c_double),
+                                        _p(th, C.c_double), nt, _p(out, C.c_double)))
+        return out[0], out[1:4].copy(), out[4:8].copy(), out[8:8 + nt].copy()
 
     def rescore(self, pocket: RefPocket, t, q, tors) -> float:
         t, q, th, nt = self._pose(t, q, tors)

@@ -197,6 +197,23 @@ int vsref_geometric_score(void* h, void* pk, const double* t, const double* q,
   });
 }
 
+// score_gradient (dock.cpp:284): out = score, gt[3], gq[4], gtor[nt]
+int vsref_score_gradient(void* h, void* pk, const double* t, const double* q,
+                         const double* tors, int nt, double* out) {
+  return guarded([&] {
+    auto* L = static_cast<RefLigand*>(h);
+    const dock::ScoreGradient g = dock::score_gradient(L->conf, L->topo, make_pose(t, q, tors, nt),
+                                                       *static_cast<dock::Pocket*>(pk));
+    out[0] = g.score;
+    out[1] = g.translation.x;
+    out[2] = g.translation.y;
+    out[3] = g.translation.z;
+    for (int k = 0; k < 4; ++k) out[4 + k] = g.rotation[k];
+    for (int j = 0; j < nt; ++j) out[8 + j] = g.torsions[j];
+    return 0;
+  });
+}
+
 // rescore (dock.cpp:297)
 int vsref_rescore(void* h, void* pk, const double* t, const double* q, const double* tors,
                   int nt, double* out) {

@@ -16,9 +16,9 @@ from .batcher import (BatchQueue, DeviceModel, SizeClass, bucket_replay, default
 from .chem import (Conformer, Library, Ligand, build_library, embed_3d, make_ligand,
                    parse_smiles, random_smiles, read_library_file, rotatable_bonds,
                    torsion_topology)
-from .dock import (DockParams, Engine, Pocket, Pose, Site, apply_pose, dock, filter_poses,
-                   geometric_score, load_pocket_file, parse_pocket_json, pocket_to_json,
-                   pose_rmsd, pose_to_json, rescore, rmsd)
+from .dock import (DockParams, Engine, Pocket, Pose, ScoreGradient, Site, apply_pose, dock,
+                   filter_poses, geometric_score, load_pocket_file, parse_pocket_json,
+                   pocket_to_json, pose_rmsd, pose_to_json, rescore, rmsd, score_gradient)
 from .errors import (AtomCountMismatch, EmptyBounds, ItemTooLarge, LengthMismatch, OutOfRange,
                      ParseError)
 from .pipeline import RankedLigand, rank_ligands, screen

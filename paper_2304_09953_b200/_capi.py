@@ -111,6 +111,10 @@ _SIGS = {
                                        C.c_void_p, C.c_void_p]),
     "vs_key_score": (C.c_float, [C.c_uint64]),
     "vs_key_id_rank": (C.c_uint32, [C.c_uint64]),
+    "vs_score_gradient": (C.c_int, [C.c_void_p, P(vs_library), C.c_int64, P(C.c_int32),
+                                    P(C.c_double), P(C.c_double), P(C.c_double),
+                                    P(C.c_double), P(C.c_double), P(C.c_double),
+                                    P(C.c_double)]),
     "vs_rescore": (C.c_int, [C.c_void_p, P(vs_library), C.c_int64, P(C.c_int32), P(C.c_float),
                              P(C.c_float), P(C.c_float), P(C.c_float), P(C.c_float)]),
     "vs_rng_u64": (C.c_int, [C.c_uint64, P(C.c_uint64), C.c_int32, C.c_int32, P(C.c_uint64)]),

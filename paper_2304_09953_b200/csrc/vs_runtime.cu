@@ -45,6 +45,12 @@ cudaError_t launch_rescore(bool grid, int blocks, size_t smem, cudaStream_t st, 
                            const int* pose_off, const long* tors_base, const float4* pt,
                            const float4* pq, const float* ptors, int nmax, int tmax, int mvmax,
                            float* geo, float* resc);
+size_t grad_smem_per_block(int nmax, int tmax);
+cudaError_t launch_grad(cudaStream_t st, const LibDev& lib, const SiteD* sites, int n_sites,
+                        const double lo[3], const double hi[3], double r, double lam,
+                        long n_poses, const int* pose_lig, const long* tb, const double* t,
+                        const double* q, const double* tors, int nmax, int tmax, double* score,
+                        double* gt, double* gq, double* gtor);
 cudaError_t launch_grid(cudaStream_t st, const PocketDev& pk, float* steric, float* hb,
                         float* lipo, float* key, float4* cells);
 int topk_chunk();
@@ -174,6 +180,9 @@ struct vs_handle {
   bool empty_bounds = false;
   PocketDev pk{};
   DBuf d_sites, d_maps;
+  DBuf d_sites64;               // FP64 sites, pocket order (score_gradient)
+  int n_sites64 = 0;
+  double box_lo[3] = {0, 0, 0}, box_hi[3] = {0, 0, 0}, r64 = 0.0, lam64 = 0.0;
   int gdims[3] = {0, 0, 0};
   // library + results
   bool has_lib = false;
@@ -495,7 +504,7 @@ void vs_destroy(vs_handle* h) {
   cudaSetDevice(h->device);
   cudaStreamSynchronize(h->own);
   h->lib.release();
-  for (DBuf* b : {&h->d_sites, &h->d_maps, &h->d_surv, &h->d_surv_tors, &h->d_all, &h->d_all_tors,
+  for (DBuf* b : {&h->d_sites, &h->d_sites64, &h->d_maps, &h->d_surv, &h->d_surv_tors, &h->d_all, &h->d_all_tors,
                   &h->d_best, &h->d_nkept, &h->d_nsurv, &h->d_keys, &h->d_counters, &h->d_sx,
                   &h->d_sp, &h->d_sm, &h->d_rots, &h->d_topk_a, &h->d_topk_b, &h->d_stats,
                   &h->d_sg_ys, &h->d_sg_ysf, &h->d_sg_th, &h->d_sg_pose, &h->d_sg_bk, &h->d_sg_nk,
@@ -540,6 +549,25 @@ int vs_set_pocket(vs_handle* h, const vs_pocket* p, double spacing, double pad) 
   }
   if (p->clash_penalty < 0.0) return fail(h, VS_ERR_POCKET, "clash_penalty must be >= 0");
   if (sites.empty()) sites.push_back(SiteF{});
+  {
+    std::vector<SiteD> sd(std::max(p->n_sites, 1));
+    for (int s = 0; s < p->n_sites; ++s) {
+      const vs_site& v = p->sites[s];
+      sd[s] = SiteD{v.center[0], v.center[1], v.center[2], v.weight,
+                    1.0 / (2.0 * v.sigma * v.sigma), v.kind, 0};
+    }
+    VS_CUDA(h, h->d_sites64.ensure(sd.size() * sizeof(SiteD)));
+    VS_CUDA(h, cudaMemcpyAsync(h->d_sites64.p, sd.data(), sd.size() * sizeof(SiteD),
+                               cudaMemcpyHostToDevice, st));
+    VS_CUDA(h, cudaStreamSynchronize(st));
+    h->n_sites64 = p->n_sites;
+    for (int c = 0; c < 3; ++c) {
+      h->box_lo[c] = p->lo[c];
+      h->box_hi[c] = p->hi[c];
+    }
+    h->r64 = p->clash_radius;
+    h->lam64 = p->clash_penalty;
+  }
   VS_CUDA(h, h->d_sites.ensure(sites.size() * sizeof(SiteF)));
   VS_CUDA(h, cudaMemcpyAsync(h->d_sites.p, sites.data(), sites.size() * sizeof(SiteF),
                              cudaMemcpyHostToDevice, st));
@@ -914,6 +942,72 @@ float vs_key_score(uint64_t key) {
 }
 
 uint32_t vs_key_id_rank(uint64_t key) { return static_cast<uint32_t>(key & 0xffffffffu); }
+
+int vs_score_gradient(vs_handle* h, const vs_library* L, int64_t n_poses,
+                      const int32_t* pose_lig, const double* t, const double* q,
+                      const double* tors, double* score, double* grad_t, double* grad_q,
+                      double* grad_tors) {
+  cudaSetDevice(h->device);
+  if (!h->has_pocket) return fail(h, VS_ERR_STATE, "no pocket");
+  if (h->empty_bounds) return fail(h, VS_ERR_EMPTY_BOUNDS, "pocket bounds are empty");
+  if (n_poses < 0) return fail(h, VS_ERR_INVALID_ARGUMENT, "negative pose count");
+  if (n_poses == 0) return VS_OK;
+  Packed P;
+  DBuf d_pl, d_tb, d_t, d_q, d_th, d_s, d_gt, d_gq, d_gth;
+  struct Release {  // device buffers of this call are freed on every exit path
+    std::vector<DBuf*> bufs;
+    Packed* packed;
+    ~Release() {
+      for (DBuf* b : bufs) b->release();
+      packed->release();
+    }
+  } guard{{&d_pl, &d_tb, &d_t, &d_q, &d_th, &d_s, &d_gt, &d_gq, &d_gth}, &P};
+  int rc = pack_library(h, L, nullptr, 0, P);
+  if (rc) return rc;
+  std::vector<long> tb(static_cast<size_t>(n_poses));
+  long toff = 0;
+  int nmax = 1, tmax = 1;
+  for (int64_t p = 0; p < n_poses; ++p) {
+    const int l = pose_lig[p];
+    if (l < 0 || l >= P.n) return fail(h, VS_ERR_INVALID_ARGUMENT, "pose ligand index out of range");
+    tb[p] = toff;
+    toff += P.meta[l].w;
+    nmax = std::max(nmax, P.meta[l].y);
+    tmax = std::max(tmax, P.meta[l].w);
+  }
+  if (grad_smem_per_block(nmax, tmax) > 227 * 1024)
+    return fail(h, VS_ERR_CAPACITY, "ligand too large for score_gradient");
+  cudaStream_t st = h->own;
+  rc = upload_packed(h, P, st);
+  if (rc) return rc;
+  const size_t np = static_cast<size_t>(n_poses), nt = static_cast<size_t>(std::max<long>(toff, 1));
+  VS_CUDA(h, d_pl.ensure(np * 4));
+  VS_CUDA(h, d_tb.ensure(np * 8));
+  VS_CUDA(h, d_t.ensure(np * 24));
+  VS_CUDA(h, d_q.ensure(np * 32));
+  VS_CUDA(h, d_th.ensure(nt * 8));
+  VS_CUDA(h, d_s.ensure(np * 8));
+  VS_CUDA(h, d_gt.ensure(np * 24));
+  VS_CUDA(h, d_gq.ensure(np * 32));
+  VS_CUDA(h, d_gth.ensure(nt * 8));
+  VS_CUDA(h, cudaMemcpyAsync(d_pl.p, pose_lig, np * 4, cudaMemcpyHostToDevice, st));
+  VS_CUDA(h, cudaMemcpyAsync(d_tb.p, tb.data(), np * 8, cudaMemcpyHostToDevice, st));
+  VS_CUDA(h, cudaMemcpyAsync(d_t.p, t, np * 24, cudaMemcpyHostToDevice, st));
+  VS_CUDA(h, cudaMemcpyAsync(d_q.p, q, np * 32, cudaMemcpyHostToDevice, st));
+  if (toff > 0) VS_CUDA(h, cudaMemcpyAsync(d_th.p, tors, toff * 8, cudaMemcpyHostToDevice, st));
+  VS_CUDA(h, launch_grad(st, P.dev(), h->d_sites64.as<const SiteD>(), h->n_sites64, h->box_lo,
+                         h->box_hi, h->r64, h->lam64, n_poses, d_pl.as<const int>(),
+                         d_tb.as<const long>(), d_t.as<const double>(), d_q.as<const double>(),
+                         d_th.as<const double>(), nmax, tmax, d_s.as<double>(), d_gt.as<double>(),
+                         d_gq.as<double>(), d_gth.as<double>()));
+  ++h->launches;
+  VS_CUDA(h, cudaMemcpyAsync(score, d_s.p, np * 8, cudaMemcpyDeviceToHost, st));
+  VS_CUDA(h, cudaMemcpyAsync(grad_t, d_gt.p, np * 24, cudaMemcpyDeviceToHost, st));
+  VS_CUDA(h, cudaMemcpyAsync(grad_q, d_gq.p, np * 32, cudaMemcpyDeviceToHost, st));
+  if (toff > 0) VS_CUDA(h, cudaMemcpyAsync(grad_tors, d_gth.p, toff * 8, cudaMemcpyDeviceToHost, st));
+  VS_CUDA(h, cudaStreamSynchronize(st));
+  return VS_OK;
+}
 
 int vs_rescore(vs_handle* h, const vs_library* L, int64_t n_poses, const int32_t* pose_lig,
                const float* t, const float* q, const float* tors, float* geo, float* resc) {

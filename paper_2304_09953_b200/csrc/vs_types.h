@@ -19,6 +19,12 @@ struct SiteF {
   float pad[3];
 };
 
+// FP64 site for score_gradient (vs_grad.cu): pocket order, kind kept
+struct SiteD {
+  double cx, cy, cz, w, inv2s2;
+  int kind, pad;
+};
+
 struct GridDev {
   float ox, oy, oz;  // node (0,0,0) position
   float h, inv_h;

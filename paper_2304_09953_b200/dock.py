@@ -354,6 +354,29 @@ class Engine:
         check(_lib.vs_measure_peaks(self._h, C.byref(a), C.byref(b), C.byref(c)), self._h, "peaks")
         return {"fp32_flops": a.value, "fp64_flops": b.value, "xu_ops": c.value}
 
+    def score_gradient(self, lib: Library, pose_lig, t, q, tors):
+        """FP64 score_gradient of given poses (capi.h vs_score_gradient):
+        (score[n], grad_t[n, 3], grad_q[n, 4], grad_tors[sum T])."""
+        pose_lig = np.ascontiguousarray(pose_lig, np.int32)
+        n = len(pose_lig)
+        t = np.ascontiguousarray(t, np.float64).reshape(-1)
+        q = np.ascontiguousarray(q, np.float64).reshape(-1)
+        tors = np.ascontiguousarray(tors, np.float64).reshape(-1)
+        nt = tors.size
+        if nt == 0:
+            tors = np.zeros(1, np.float64)
+        score = np.zeros(max(n, 1), np.float64)
+        gt = np.zeros(max(n, 1) * 3, np.float64)
+        gq = np.zeros(max(n, 1) * 4, np.float64)
+        gtor = np.zeros(max(nt, 1), np.float64)
+        lc = lib.as_c()
+        check(_lib.vs_score_gradient(self._h, C.byref(lc), n, ptr(pose_lig, C.c_int32),
+                                     ptr(t, C.c_double), ptr(q, C.c_double), ptr(tors, C.c_double),
+                                     ptr(score, C.c_double), ptr(gt, C.c_double),
+                                     ptr(gq, C.c_double), ptr(gtor, C.c_double)),
+              self._h, "score_gradient")
+        return score[:n], gt[:3 * n].reshape(n, 3), gq[:4 * n].reshape(n, 4), gtor[:nt]
+
     def rescore(self, lib: Library, pose_lig, t, q, tors):
         """K3a: canonical geometric score and rescore of given poses."""
         pose_lig = np.ascontiguousarray(pose_lig, np.int32)
@@ -450,6 +473,34 @@ def geometric_score(conf: Conformer, topo: TorsionTopology, pose: Pose, pocket: 
     """dock::geometric_score (dock.cpp:278-282) on the GPU (canonical FP32)."""
     _check_counts(conf, topo, pose)
     return float(_score(conf, topo, [pose], pocket, None, engine)[0][0])
+
+
+@dataclass
+class ScoreGradient:
+    """dock::ScoreGradient (dock.hpp:86-91)."""
+    score: float
+    translation: tuple
+    rotation: tuple  # d/d(w, x, y, z)
+    torsions: list
+
+
+def score_gradient(conf: Conformer, topo: TorsionTopology, pose: Pose, pocket: Pocket,
+                   engine: Engine | None = None) -> ScoreGradient:
+    """dock::score_gradient (dock.cpp:284-295) on the GPU in FP64: analytic
+    translation / rotation derivatives, central differences for torsions."""
+    _check_counts(conf, topo, pose)
+    if pocket.empty():
+        raise EmptyBounds()
+    eng = engine or default_engine()
+    if eng.pocket is not pocket:
+        eng.set_pocket(pocket)
+    if not len(conf.coords):
+        raise AtomCountMismatch("conformer has no atoms")
+    lib = _one_ligand_library(conf, topo)
+    s, gt, gq, gtor = eng.score_gradient(lib, np.zeros(1, np.int32), [pose.translation],
+                                         [pose.rotation], list(pose.torsions))
+    return ScoreGradient(float(s[0]), tuple(float(v) for v in gt[0]),
+                         tuple(float(v) for v in gq[0]), [float(v) for v in gtor])
 
 
 def rescore(ligand: Ligand, conf: Conformer, topo: TorsionTopology, pose: Pose, pocket: Pocket,

@@ -35,6 +35,9 @@ int main() {
     if (std::fabs(s - 1.0) > 1e-6) return 3;
     auto docked = vg::dock::dock(dev, c, topo, p, 4, 1.0, 42);
     if (docked.empty()) return 4;
+    // at the site centre the steric gradient vanishes (test_dock.cpp:62-80)
+    const auto gr = vg::dock::score_gradient(dev, c, topo, at, p);
+    if (std::fabs(gr.score - s) > 1e-9 || std::fabs(gr.translation.x) > 1e-9) return 5;
     std::printf("gpu ok %.6f %zu\n", s, docked.size());
   } catch (const vg::DeviceError& e) {
     std::printf("no device: %s\n", e.what());
