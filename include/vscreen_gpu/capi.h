@@ -227,7 +227,11 @@ typedef struct {
 int vs_ligand_build(const char* smiles, uint64_t embed_seed, int32_t iterations,
                     vs_ligand_buf* out);
 
-/* Many ligands on `threads` host threads.  smiles: NUL-separated blob. */
+/* Many ligands on `threads` host threads.  smiles: NUL-separated blob.
+ * iterations >= 0: embed_3d on the host with that many spring iterations;
+ * -1: zero coordinates; VS_EMBED_PLACE_ONLY: the BFS placement only, to be
+ * relaxed on the device by vs_libbuild_relax (GPU embed_3d). */
+#define VS_EMBED_PLACE_ONLY (-2)
 typedef struct vs_libbuild vs_libbuild;
 int vs_libbuild_run(const char* smiles_blob, int32_t n, const uint64_t* embed_seeds,
                     int32_t iterations, int32_t threads, vs_libbuild** out);
@@ -237,6 +241,11 @@ int vs_libbuild_fetch(const vs_libbuild* b, int32_t* status, int32_t* n_atoms, i
                       int32_t* rot_bonds, double* coords, int32_t* atom_class, int32_t* axis_a,
                       int32_t* axis_b, int32_t* moving_count, int32_t* moving);
 void vs_libbuild_free(vs_libbuild* b);
+/* The spring relaxation of embed_3d (chem.cpp:355-392, 434-445: `iterations`
+ * steps, then up to 20 rounds of 50 while the closest pair is < 0.5 A) on the
+ * device for every ligand built with VS_EMBED_PLACE_ONLY; FP64 in the
+ * reference's operation order, bit-identical to the host embed. */
+int vs_libbuild_relax(vs_handle* h, vs_libbuild* b, int32_t iterations);
 /* synthetic libraries from the reference corpus sampler: indices i of the
  * first n_want entries random_smiles(Rng(seed).split(i)) within the atom /
  * torsion bounds (inclusive); then build those entries */

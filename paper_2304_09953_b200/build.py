@@ -15,8 +15,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libvscreen_gpu.so")
-SOURCES = ["vs_kernels.cu", "vs_dock.cu", "vs_grad.cu", "vs_runtime.cu", "vs_host.cpp",
-           "vs_ingest.cpp"]
+SOURCES = ["vs_kernels.cu", "vs_dock.cu", "vs_grad.cu", "vs_embed.cu", "vs_runtime.cu",
+           "vs_host.cpp", "vs_ingest.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "--fmad=false", "-ccbin", "/usr/bin/g++",

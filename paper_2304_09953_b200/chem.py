@@ -20,6 +20,9 @@ from .errors import ParseError, check
 BOND_ORDER = {1: "single", 2: "double", 3: "triple", 4: "aromatic"}
 
 
+
+EMBED_PLACE_ONLY = -2  # capi.h VS_EMBED_PLACE_ONLY: BFS placement only
+
 @dataclass
 class Axis:
     """TorsionTopology::Axis (dock.hpp:66-69)."""
@@ -296,20 +299,33 @@ def corpus_indices(seed: int, n: int, atoms: tuple[int, int], tors: tuple[int, i
     return out[:got]
 
 
+def _relax_on(engine, h, iterations):
+    """Placement-only build -> the spring relaxation of embed_3d on the GPU."""
+    try:
+        check(_lib.vs_libbuild_relax(engine._h, h, iterations), engine._h, "embed relax")
+    except Exception:
+        _lib.vs_libbuild_free(h)
+        raise
+
+
 def corpus_library(seed: int, n: int, atoms: tuple[int, int], tors: tuple[int, int],
                    embed_master: int = 2024, dock_master: int = 2024, iterations: int = 200,
-                   threads: int = 8) -> Library:
+                   threads: int = 8, engine=None) -> Library:
     """Synthetic library: corpus entries filtered to the size
     bounds; embed seed Rng(master).split(1).split(i), dock seed .split(2)
-    .split(i) with i the index in the library (pipeline.cpp:422-484)."""
+    .split(i) with i the index in the library (pipeline.cpp:422-484).
+    With `engine`, embed_3d's spring relaxation runs on that GPU (bit-identical)."""
     from .pipeline import campaign_seeds
     idx = corpus_indices(seed, n, atoms, tors, threads)
     m = len(idx)
     es = campaign_seeds(embed_master, m, stage=1)
     ds = campaign_seeds(dock_master, m, stage=2)
     h = C.c_void_p()
-    check(_lib.vs_libbuild_corpus(seed, ptr(idx, C.c_int64), m, ptr(es, C.c_uint64), iterations,
-                                  threads, C.byref(h)))
+    check(_lib.vs_libbuild_corpus(seed, ptr(idx, C.c_int64), m, ptr(es, C.c_uint64),
+                                  EMBED_PLACE_ONLY if engine is not None else iterations, threads,
+                                  C.byref(h)))
+    if engine is not None:
+        _relax_on(engine, h, iterations)
     ids = [f"Z{int(i)}" for i in idx]
     return _fetch_built(h, m, ids, ds)
 
@@ -358,16 +374,24 @@ def _fetch_built(h, n, ids, ds, drop_failed=True) -> Library:
 
 def build_library(smiles: Sequence[str], ids: Sequence[str] | None = None,
                   embed_seeds: Sequence[int] | None = None, dock_seeds: Sequence[int] | None = None,
-                  iterations: int = 200, threads: int = 8, drop_failed: bool = True) -> Library:
+                  iterations: int = 200, threads: int = 8, drop_failed: bool = True,
+                  engine=None) -> Library:
     """Parse + embed + topology for many ligands on `threads` host threads
-    (the parse/embed stages of run_campaign, pipeline.cpp:383-431)."""
+    (the parse/embed stages of run_campaign, pipeline.cpp:383-431).  With
+    `engine` (a dock.Engine), the host does parse, topology and embed_3d's
+    BFS placement, and the spring relaxation runs on the GPU (bit-identical
+    coordinates)."""
     n = len(smiles)
     ids = list(ids) if ids is not None else [f"L{i + 1}" for i in range(n)]
     es = np.array([int(s) & (2**64 - 1) for s in (embed_seeds if embed_seeds is not None else [0] * n)],
                   np.uint64)
     blob = b"".join(s.encode() + b"\0" for s in smiles) or b"\0"
     h = C.c_void_p()
-    check(_lib.vs_libbuild_run(blob, n, ptr(es, C.c_uint64), iterations, threads, C.byref(h)))
+    check(_lib.vs_libbuild_run(blob, n, ptr(es, C.c_uint64),
+                               EMBED_PLACE_ONLY if engine is not None else iterations, threads,
+                               C.byref(h)))
+    if engine is not None:
+        _relax_on(engine, h, iterations)
     ds = np.array([int(s) & (2**64 - 1) for s in (dock_seeds if dock_seeds is not None else [0] * n)],
                   np.uint64)
     return _fetch_built(h, n, ids, ds, drop_failed)

@@ -34,6 +34,7 @@ struct BuiltLigand {
   int rot = 0;
   std::vector<double> coords;
   std::vector<int> cls;
+  std::vector<int> bonds;  // (a, b) pairs, kept for the device spring relaxation
   Topology topo;
 };
 
@@ -47,6 +48,13 @@ BuiltLigand build_one(const std::string& smiles, std::uint64_t seed, int iterati
     for (std::size_t i = 0; i < g.elements.size(); ++i) b.cls[i] = element_class(g.elements[i]);
     if (iterations >= 0) {
       b.coords = embed(g, seed, iterations);
+    } else if (iterations == VS_EMBED_PLACE_ONLY) {
+      b.coords = embed_place(g, seed);
+      b.bonds.reserve(2 * g.bonds.size());
+      for (const auto& e : g.bonds) {
+        b.bonds.push_back(e.a);
+        b.bonds.push_back(e.b);
+      }
     } else {
       b.coords.assign(3 * g.elements.size(), 0.0);
     }
@@ -197,6 +205,51 @@ int vs_libbuild_fetch(const vs_libbuild* b, int32_t* status, int32_t* n_atoms, i
 }
 
 void vs_libbuild_free(vs_libbuild* b) { delete b; }
+
+}  // extern "C"
+
+namespace vs {
+int relax_on_device(vs_handle* h, int n, const int64_t* atom_off, const int32_t* n_atoms,
+                    double* coords, const int64_t* bond_off, const int32_t* n_bonds,
+                    const int32_t* bonds, int iterations);
+}
+
+extern "C" {
+
+// Spring relaxation (chem.cpp:355-392, 434-445) of every ligand built with
+// iterations = VS_EMBED_PLACE_ONLY, on the device; coordinates updated in place.
+int vs_libbuild_relax(vs_handle* h, vs_libbuild* b, int32_t iterations) {
+  const int n = static_cast<int>(b->ligs.size());
+  std::vector<int64_t> aoff(n + 1, 0), boff(n + 1, 0);
+  std::vector<int32_t> na(n, 0), nb(n, 0);
+  for (int i = 0; i < n; ++i) {
+    const auto& l = b->ligs[i];
+    const bool use = l.status == 0 && !l.bonds.empty() && l.bonds.size() / 2 >= 1;
+    na[i] = use ? static_cast<int32_t>(l.coords.size() / 3) : 0;
+    nb[i] = use ? static_cast<int32_t>(l.bonds.size() / 2) : 0;
+    aoff[i + 1] = aoff[i] + na[i];
+    boff[i + 1] = boff[i] + nb[i];
+  }
+  std::vector<double> xyz(static_cast<std::size_t>(3 * std::max<int64_t>(aoff[n], 1)));
+  std::vector<int32_t> bd(static_cast<std::size_t>(2 * std::max<int64_t>(boff[n], 1)));
+  for (int i = 0; i < n; ++i) {
+    if (!na[i]) continue;
+    const auto& l = b->ligs[i];
+    std::memcpy(xyz.data() + 3 * aoff[i], l.coords.data(), l.coords.size() * sizeof(double));
+    std::memcpy(bd.data() + 2 * boff[i], l.bonds.data(), l.bonds.size() * sizeof(int32_t));
+  }
+  const int rc = relax_on_device(h, n, aoff.data(), na.data(), xyz.data(), boff.data(), nb.data(),
+                                 bd.data(), iterations);
+  if (rc) return rc;
+  for (int i = 0; i < n; ++i) {
+    if (!na[i]) continue;
+    auto& l = b->ligs[i];
+    std::memcpy(l.coords.data(), xyz.data() + 3 * aoff[i], l.coords.size() * sizeof(double));
+    l.bonds.clear();
+    l.bonds.shrink_to_fit();
+  }
+  return VS_OK;
+}
 
 // Scan corpus::random_smiles(Rng(seed).split(i)) for i = 0, 1, ... and keep
 // the first n_want whose heavy atoms lie in [atom_lo, atom_hi] and torsion

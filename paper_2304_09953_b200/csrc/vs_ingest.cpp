@@ -319,6 +319,12 @@ double closest_pair(const std::vector<V3>& pos) {
 
 }  // namespace
 
+// BFS tetrahedral placement with RNG jitter (chem.cpp:406-432): the embed
+// before the spring relaxation; throws on a disconnected graph.
+std::vector<double> embed_place(const Graph& g, std::uint64_t seed) {
+  return embed(g, seed, -1);
+}
+
 std::vector<double> embed(const Graph& g, std::uint64_t seed, int iterations) {
   const std::size_t n = g.elements.size();
   std::vector<V3> pos(n, V3{0, 0, 0});
@@ -370,8 +376,11 @@ std::vector<double> embed(const Graph& g, std::uint64_t seed, int iterations) {
       bfs.push_back(w);
     }
   }
-  springs(g, pos, iterations);
-  for (int round = 0; round < 20 && n > 1 && closest_pair(pos) < 0.5; ++round) springs(g, pos, 50);
+  if (iterations >= 0) {  // iterations < 0: placement only (embed_place)
+    springs(g, pos, iterations);
+    for (int round = 0; round < 20 && n > 1 && closest_pair(pos) < 0.5; ++round)
+      springs(g, pos, 50);
+  }
   std::vector<double> out(3 * n);
   for (std::size_t i = 0; i < n; ++i) {
     out[3 * i] = pos[i].x;

@@ -42,6 +42,7 @@ std::vector<int> degrees(const Graph& g);
 int rotatable_bond_count(const Graph& g);
 Topology torsion_axes(const Graph& g);
 std::vector<double> embed(const Graph& g, std::uint64_t seed, int iterations);
+std::vector<double> embed_place(const Graph& g, std::uint64_t seed);
 int element_class(const std::string& el);
 std::string random_smiles(std::uint64_t seed, std::uint64_t index);
 

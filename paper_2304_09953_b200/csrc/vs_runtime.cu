@@ -46,6 +46,11 @@ cudaError_t launch_rescore(bool grid, int blocks, size_t smem, cudaStream_t st, 
                            const float4* pq, const float* ptors, int nmax, int tmax, int mvmax,
                            float* geo, float* resc);
 size_t grad_smem_per_block(int nmax, int tmax);
+int relax_max_atoms();
+int relax_max_bonds();
+cudaError_t launch_relax(cudaStream_t st, const long long* atom_off, const int* n_atoms,
+                         const long long* bond_off, const int* n_bonds, const int2* bonds,
+                         double* coords, int n, int iterations);
 cudaError_t launch_grad(cudaStream_t st, const LibDev& lib, const SiteD* sites, int n_sites,
                         const double lo[3], const double hi[3], double r, double lam,
                         long n_poses, const int* pose_lig, const long* tb, const double* t,
@@ -942,6 +947,54 @@ float vs_key_score(uint64_t key) {
 }
 
 uint32_t vs_key_id_rank(uint64_t key) { return static_cast<uint32_t>(key & 0xffffffffu); }
+
+}  // extern "C"
+
+namespace vs {
+// device half of vs_libbuild_relax (vs_host.cpp): the spring relaxation of
+// embed_3d for a flattened batch of placed conformers, in place
+int relax_on_device(vs_handle* h, int n, const int64_t* atom_off, const int32_t* n_atoms,
+                    double* coords, const int64_t* bond_off, const int32_t* n_bonds,
+                    const int32_t* bonds, int iterations) {
+  cudaSetDevice(h->device);
+  if (iterations < 0) return fail(h, VS_ERR_INVALID_ARGUMENT, "iterations must be >= 0");
+  for (int i = 0; i < n; ++i)
+    if (n_atoms[i] > relax_max_atoms() || n_bonds[i] > relax_max_bonds())
+      return fail(h, VS_ERR_CAPACITY, "ligand " + std::to_string(i) + " too large for the device embed");
+  if (n == 0) return VS_OK;
+  const size_t na = static_cast<size_t>(std::max<int64_t>(atom_off[n], 1));
+  const size_t nbd = static_cast<size_t>(std::max<int64_t>(bond_off[n], 1));
+  DBuf d_ao, d_na, d_bo, d_nb, d_bd, d_xyz;
+  struct Release {
+    std::vector<DBuf*> bufs;
+    ~Release() {
+      for (DBuf* b : bufs) b->release();
+    }
+  } guard{{&d_ao, &d_na, &d_bo, &d_nb, &d_bd, &d_xyz}};
+  cudaStream_t st = h->own;
+  VS_CUDA(h, d_ao.ensure((n + 1) * 8));
+  VS_CUDA(h, d_na.ensure(n * 4));
+  VS_CUDA(h, d_bo.ensure((n + 1) * 8));
+  VS_CUDA(h, d_nb.ensure(n * 4));
+  VS_CUDA(h, d_bd.ensure(nbd * 8));
+  VS_CUDA(h, d_xyz.ensure(na * 24));
+  VS_CUDA(h, cudaMemcpyAsync(d_ao.p, atom_off, (n + 1) * 8, cudaMemcpyHostToDevice, st));
+  VS_CUDA(h, cudaMemcpyAsync(d_na.p, n_atoms, n * 4, cudaMemcpyHostToDevice, st));
+  VS_CUDA(h, cudaMemcpyAsync(d_bo.p, bond_off, (n + 1) * 8, cudaMemcpyHostToDevice, st));
+  VS_CUDA(h, cudaMemcpyAsync(d_nb.p, n_bonds, n * 4, cudaMemcpyHostToDevice, st));
+  VS_CUDA(h, cudaMemcpyAsync(d_bd.p, bonds, nbd * 8, cudaMemcpyHostToDevice, st));
+  VS_CUDA(h, cudaMemcpyAsync(d_xyz.p, coords, na * 24, cudaMemcpyHostToDevice, st));
+  VS_CUDA(h, launch_relax(st, d_ao.as<const long long>(), d_na.as<const int>(),
+                          d_bo.as<const long long>(), d_nb.as<const int>(), d_bd.as<const int2>(),
+                          d_xyz.as<double>(), n, iterations));
+  ++h->launches;
+  VS_CUDA(h, cudaMemcpyAsync(coords, d_xyz.p, na * 24, cudaMemcpyDeviceToHost, st));
+  VS_CUDA(h, cudaStreamSynchronize(st));
+  return VS_OK;
+}
+}  // namespace vs
+
+extern "C" {
 
 int vs_score_gradient(vs_handle* h, const vs_library* L, int64_t n_poses,
                       const int32_t* pose_lig, const double* t, const double* q,

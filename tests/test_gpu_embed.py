@@ -1,0 +1,59 @@
+"""embed_3d on the GPU: host BFS placement + device spring
+relaxation must give the host embed's (= the reference's, test_ingest.py)
+coordinates bit for bit."""
+import time
+
+import numpy as np
+import pytest
+
+from conftest import gpu_available
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
+
+
+@pytest.fixture(scope="module")
+def engine():
+    import paper_2304_09953_b200 as V
+    e = V.Engine(0)
+    yield e
+    e.close()
+
+
+def _same(a, b):
+    assert a.ids == b.ids
+    for f in ("n_atoms", "n_tors", "rot_bonds", "atom_class", "axis_a", "axis_b", "moving_count",
+              "moving", "seeds"):
+        np.testing.assert_array_equal(getattr(a, f), getattr(b, f), err_msg=f)
+    np.testing.assert_array_equal(a.coords.view(np.uint64), b.coords.view(np.uint64))
+
+
+def test_device_embed_bit_identical_corpus(engine):
+    from paper_2304_09953_b200.chem import corpus_library
+    host = corpus_library(99, 3000, (1, 40), (0, 10), threads=16)
+    dev = corpus_library(99, 3000, (1, 40), (0, 10), threads=16, engine=engine)
+    _same(host, dev)
+
+
+def test_device_embed_bit_identical_flexible(engine):
+    import paper_2304_09953_b200 as V
+    from paper_2304_09953_b200.chem import flexible_smiles
+    smis = flexible_smiles(7, 12)
+    ids = [f"F{i}" for i in range(len(smis))]
+    seeds = list(range(1, len(smis) + 1))
+    host = V.build_library(smis, ids, seeds, seeds, threads=16)
+    dev = V.build_library(smis, ids, seeds, seeds, threads=16, engine=engine)
+    assert host.n_atoms.min() >= 60
+    _same(host, dev)
+
+
+def test_device_embed_throughput(engine):
+    """Informational: the device relaxation against the 16-thread host embed."""
+    from paper_2304_09953_b200.chem import corpus_library
+    t0 = time.perf_counter()
+    corpus_library(5, 20000, (10, 40), (0, 10), threads=16)
+    th = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    corpus_library(5, 20000, (10, 40), (0, 10), threads=16, engine=engine)
+    td = time.perf_counter() - t0
+    print(f"library build 20k: host embed {th:.2f} s, device relax {td:.2f} s")
