@@ -320,7 +320,7 @@ int vso_pocket_new(const vso_pocket_desc* d, vso_pocket** out) {
       p->hbond[id] = site_sum(p->sites + p->n_st, p->n_hb, x, y, z);
       p->lipo[id] = site_sum(p->sites + p->n_st + p->n_hb, p->n_li, x, y, z);
       const float xn[3] = {x, y, z};
-      p->key[id] = fmaf(-p->lam, wall(p, xn), p->steric[id]);
+      p->key[id] = (float)(_Float16)fmaf(-p->lam, wall(p, xn), p->steric[id]); /* FP16 map, RNE */
     }
   }
   *out = p;

@@ -2,6 +2,7 @@
 // vs_kernels.cu): RNG, TMA bulk staging, field/wall/pair terms, per-warp
 // shared-memory layout, torsion chain, sweep key, start draws.
 #pragma once
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -96,6 +97,19 @@ __device__ __forceinline__ void ldg_cell(const float4* c, float4& lo, float4& hi
                : "=f"(lo.x), "=f"(lo.y), "=f"(lo.z), "=f"(lo.w), "=f"(hi.x), "=f"(hi.y),
                  "=f"(hi.z), "=f"(hi.w)
                : "l"(c));
+}
+
+// One FP16 corner cell (16 B, LDG.128), widened to FP32 exactly.
+__device__ __forceinline__ void ldg_hcell(const uint4* c, float4& lo, float4& hi) {
+  uint4 u;
+  asm("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w)
+      : "l"(c));
+  const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+  const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+  const float2 d = __half22float2(*reinterpret_cast<const __half2*>(&u.z));
+  const float2 e = __half22float2(*reinterpret_cast<const __half2*>(&u.w));
+  lo = make_float4(a.x, a.y, b.x, b.y);
+  hi = make_float4(d.x, d.y, e.x, e.y);
 }
 
 // One trilinear lookup split in two halves so that callers can issue the
@@ -460,8 +474,7 @@ static __device__ __forceinline__ float eval_key(const PocketDev& pk, const floa
                   iz = static_cast<int>(fz[u]);
         in[u] = static_cast<unsigned>(ix) <= mx && static_cast<unsigned>(iy) <= my &&
                 static_cast<unsigned>(iz) <= mz;
-        ldg_cell(g.key_c + 2 * (in[u] ? (iz * (g.ny - 1) + iy) * (g.nx - 1) + ix : 0), lo[u],
-                 hi[u]);
+        ldg_hcell(g.key_h + (in[u] ? (iz * (g.ny - 1) + iy) * (g.nx - 1) + ix : 0), lo[u], hi[u]);
       }
 #pragma unroll
       for (int u = 0; u < kU; ++u) {

@@ -17,6 +17,7 @@
 // feeds a score or a decision is the deterministic arithmetic of
 // vs_detmath.cuh with fixed-order sums (docs/SWEEP_V1.md §3), so the CPU
 // oracle reproduces every score and decision bit for bit.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -168,7 +169,8 @@ __global__ void vs_grid_kernel(const PocketDev pk, float* __restrict__ steric,
     steric[id] = site_sum(pk.sites, pk.n_steric, x, y, z);
     hbond[id] = site_sum(pk.sites + pk.n_steric, pk.n_hbond, x, y, z);
     lipo[id] = site_sum(pk.sites + pk.n_steric + pk.n_hbond, pk.n_lipo, x, y, z);
-    key[id] = fmaf(-pk.lam, wall_of(pk, x, y, z), steric[id]);
+    // the sweep-key map is stored in FP16 (node map holds the rounded value)
+    key[id] = __half2float(__float2half_rn(fmaf(-pk.lam, wall_of(pk, x, y, z), steric[id])));
   }
 }
 
@@ -184,6 +186,26 @@ __global__ void vs_pack_kernel(const GridDev g, const float* __restrict__ node,
     const float* p = node + iz * sz + iy * sy + ix;
     cells[2 * id] = make_float4(p[0], p[sx], p[sy], p[sy + sx]);
     cells[2 * id + 1] = make_float4(p[sz], p[sz + sx], p[sz + sy], p[sz + sy + sx]);
+  }
+}
+
+// FP16 node map -> 16 B corner cells (8 halves, same corner order): the
+// sweep key's lookups touch half the bytes and lines of an FP32 cell
+__global__ void vs_pack_half_kernel(const GridDev g, const float* __restrict__ node,
+                                    uint4* __restrict__ cells) {
+  const long cx = g.nx - 1, cy = g.ny - 1, cz = g.nz - 1;
+  const long n = cx * cy * cz;
+  const long sx = 1, sy = g.nx, sz = static_cast<long>(g.nx) * g.ny;
+  for (long id = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; id < n;
+       id += static_cast<long>(gridDim.x) * blockDim.x) {
+    const long ix = id % cx, iy = (id / cx) % cy, iz = id / (cx * cy);
+    const float* p = node + iz * sz + iy * sy + ix;
+    auto h2 = [](float a, float b) {
+      const __half2 v = __floats2half2_rn(a, b);
+      return *reinterpret_cast<const unsigned*>(&v);
+    };
+    cells[id] = make_uint4(h2(p[0], p[sx]), h2(p[sy], p[sy + sx]), h2(p[sz], p[sz + sx]),
+                           h2(p[sz + sy], p[sz + sy + sx]));
   }
 }
 
@@ -310,7 +332,7 @@ cudaError_t launch_grid(cudaStream_t st, const PocketDev& pk, float* steric, flo
   vs_pack_kernel<<<cb, 256, 0, st>>>(g, steric, cells);
   vs_pack_kernel<<<cb, 256, 0, st>>>(g, hb, cells + 2 * nc);
   vs_pack_kernel<<<cb, 256, 0, st>>>(g, lipo, cells + 4 * nc);
-  vs_pack_kernel<<<cb, 256, 0, st>>>(g, key, cells + 6 * nc);
+  vs_pack_half_kernel<<<cb, 256, 0, st>>>(g, key, reinterpret_cast<uint4*>(cells + 6 * nc));
   return cudaGetLastError();
 }
 

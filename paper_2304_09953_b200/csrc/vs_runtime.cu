@@ -620,6 +620,7 @@ int vs_set_pocket(vs_handle* h, const vs_pocket* p, double spacing, double pad) 
     g.lipo_c = c + 4 * cells;
     g.key = m + 3 * nodes;
     g.key_c = c + 6 * cells;
+    g.key_h = reinterpret_cast<const uint4*>(c + 6 * cells);
     VS_CUDA(h, launch_grid(st, pk, m, m + nodes, m + 2 * nodes, m + 3 * nodes, c));
     h->launches += 5;
     pk.grid_mode = 1;

@@ -40,6 +40,7 @@ struct GridDev {
   // sweep-key map K = steric - lam * wall at the nodes (SWEEP_V1.md §2.3)
   const float* key;
   const float4* key_c;
+  const uint4* key_h;  // FP16 corner cells of the key map (8 halves, 16 B), the sweep's map
 };
 
 struct PocketDev {
