@@ -102,6 +102,8 @@ typedef struct {
   int32_t write_all_poses; /* also return every kept pose (dock() output) */
   double min_score;
   uint64_t rotation_seed;
+  int32_t polish;          /* 0 off, 1 rigid compass, 2 + fine torsion pass (SWEEP_V1.md §3.5) */
+  int32_t reserved;
 } vs_dock_params;
 
 /* One pose (dock::Pose, dock.hpp:39-46) in FP32 plus its sweep-v1 index

@@ -30,7 +30,8 @@ class PocketDesc(C.Structure):
 class Params(C.Structure):
     _fields_ = [("restarts", C.c_int32), ("rotations", C.c_int32), ("flex_angles", C.c_int32),
                 ("flex_passes", C.c_int32), ("diversity_delta", C.c_double), ("keep_top", C.c_int32),
-                ("write_all", C.c_int32), ("min_score", C.c_double)]
+                ("write_all", C.c_int32), ("min_score", C.c_double), ("polish", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 class Lib(C.Structure):
@@ -168,6 +169,7 @@ def dock_library(pocket: OraclePocket, L, prm, threads: int = 1, sel=None):
     p = Params()
     p.restarts, p.rotations, p.flex_angles, p.flex_passes = prm.restarts, prm.rotations, prm.flex_angles, prm.flex_passes
     p.diversity_delta, p.keep_top, p.write_all, p.min_score = prm.diversity_delta, prm.keep_top, int(prm.write_all_poses), prm.min_score
+    p.polish = int(getattr(prm, "polish", 0))
     rots = rotation_set(prm.rotations, prm.rotation_seed)
     lc = _lib_c(L)
     selc = None if sel is None else np.ascontiguousarray(sel, np.int32)

@@ -544,6 +544,12 @@ static uint32_t orderable(float f) {
   return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
 }
 
+/* polish (SWEEP_V1.md §3.5): rigid compass on the flexed state */
+#define POLISH_ANG0 0.140625f  /* 8.06 deg */
+#define POLISH_SC0 0.25f
+#define POLISH_ANG_MIN 0.00390625f
+#define POLISH_ITERS 40
+
 #define TRANS_ITERS 16
 #define TRANS_MIN (1.0f / 64.0f)
 /* translation lattice: 0 = current, 1..26 = {-1,0,1}^3 \ 0, x fastest */
@@ -553,6 +559,59 @@ static void trans_offset(int l, float sc, float* o) {
   o[0] = (float)(m % 3 - 1) * sc;
   o[1] = (float)((m / 3) % 3 - 1) * sc;
   o[2] = (float)(m / 9 - 1) * sc;
+}
+
+/* polish rigid compass (SWEEP_V1.md §3.5): candidate l = 0 keeps the pose;
+ * l = 1..6 rotate by +-ang about world x, y, z through the posed centroid;
+ * l = 7..12 translate by +-sc along x, y, z.  The argmax of the sweep key
+ * (ties to the lowest l) is taken; when l = 0 wins, ang and sc halve. */
+static void rigid_compass(const vso_pocket* p, const lig_t* L, const float* ysf, const float* c,
+                          float* pq, float* pt) {
+  const float zero[3] = {0.0f, 0.0f, 0.0f};
+  float ang = POLISH_ANG0, sc = POLISH_SC0;
+  for (int it = 0; it < POLISH_ITERS && ang >= POLISH_ANG_MIN; ++it) {
+    const mat3 R0 = quat_mat(pq[0], pq[1], pq[2], pq[3]);
+    float Cw[3];
+    apply(&R0, c, pt, Cw);
+    float sh, ch;
+    vso_sincos(0.5f * ang, &sh, &ch);
+    float bk = -INFINITY, bq[4], bt[3];
+    int bl = 0;
+    for (int l = 0; l < 13; ++l) {
+      float q2[4] = {pq[0], pq[1], pq[2], pq[3]}, t2[3] = {pt[0], pt[1], pt[2]};
+      mat3 R2 = R0;
+      if (l >= 1 && l <= 6) {
+        const int ax = (l - 1) >> 1;
+        float dq[4] = {ch, 0.0f, 0.0f, 0.0f};
+        dq[1 + ax] = ((l - 1) & 1) ? -sh : sh;
+        qmul(dq, pq, q2);
+        qnormalize(q2);
+        R2 = quat_mat(q2[0], q2[1], q2[2], q2[3]);
+        float v[3];
+        apply(&R2, c, zero, v);
+        t2[0] = Cw[0] - v[0];
+        t2[1] = Cw[1] - v[1];
+        t2[2] = Cw[2] - v[2];
+      } else if (l >= 7) {
+        const int ax = (l - 7) >> 1;
+        t2[ax] = ((l - 7) & 1) ? pt[ax] - sc : pt[ax] + sc;
+      }
+      const float key = rigid_key(p, L, ysf, &R2, t2);
+      if (key > bk) {
+        bk = key;
+        bl = l;
+        memcpy(bq, q2, 16);
+        memcpy(bt, t2, 12);
+      }
+    }
+    if (bl == 0) {
+      ang = ang * 0.5f;
+      sc = sc * 0.5f;
+    } else {
+      memcpy(pq, bq, 16);
+      memcpy(pt, bt, 12);
+    }
+  }
 }
 
 /* sweep-v1 for one ligand (dock.cpp:318-371 restated with the sweep) */
@@ -665,8 +724,10 @@ static void dock_one(const vso_pocket* p, const lig_t* L, uint64_t seed, uint32_
     for (int i = 0; i < N; ++i) atom_terms(p, &RS, ptd, &y[3 * i], &fa[i], &wa[i], NULL);
     float S = 0.0f;
     const int do_flex = T > 0 && prm->flex_passes > 0;
-    const int steps = do_flex ? prm->flex_passes * T : 1;
+    const int steps0 = do_flex ? prm->flex_passes * T : 1;
+    const int steps = steps0 + ((do_flex && prm->polish >= 2) ? T : 0);
     for (int st = 0; st < steps; ++st) {
+      const int fine = st >= steps0; /* polish 2: one pass of fine angles (§3.5) */
       const int j = do_flex ? st % T : -1;
       const int m = do_flex ? L->cnt[j] : 0;
       const int* mv = do_flex ? L->moving + L->mstart[j] : NULL;
@@ -690,7 +751,16 @@ static void dock_one(const vso_pocket* p, const lig_t* L, uint64_t seed, uint32_
         if (do_flex) {
           const float tho = th[j];
           thn = tho;
-          if (a > 0) { thn = tho + (float)a * step; if (thn >= PI_F) thn = thn - TWO_PI_F; }
+          if (a > 0) {
+            if (fine) {
+              const int off = a <= prm->flex_angles / 2 ? a : a - prm->flex_angles;
+              thn = tho + (float)off * (step * 0.125f);
+              if (thn < -PI_F) thn = thn + TWO_PI_F;
+            } else {
+              thn = tho + (float)a * step;
+            }
+            if (thn >= PI_F) thn = thn - TWO_PI_F;
+          }
           mat3d M = flex_mat(&y[3 * L->a[j]], &y[3 * L->b[j]], thn, tho, L->inv_len[j]);
           const double* o = &y[3 * L->a[j]];
           for (int q2 = 0; q2 < m; ++q2) {
@@ -721,6 +791,30 @@ static void dock_one(const vso_pocket* p, const lig_t* L, uint64_t seed, uint32_
         }
         th[j] = best_th;
       }
+    }
+    if (prm->polish >= 1) { /* §3.5: rigid compass on the flexed state, then S re-scored */
+      for (int i = 0; i < 3 * N; ++i) ysf[i] = (float)y[i];
+      float cf[3] = {0.0f, 0.0f, 0.0f};
+      for (int i = 0; i < N; ++i) { cf[0] = cf[0] + ysf[3 * i]; cf[1] = cf[1] + ysf[3 * i + 1]; cf[2] = cf[2] + ysf[3 * i + 2]; }
+      cf[0] = cf[0] / (float)N; cf[1] = cf[1] / (float)N; cf[2] = cf[2] / (float)N;
+      rigid_compass(p, L, ysf, cf, pq, pt);
+      RS = pose_mat_d(pq);
+      ptd[0] = pt[0]; ptd[1] = pt[1]; ptd[2] = pt[2];
+      /* the flex-step score with an empty moving set: lane-strided atom and
+       * pair sums, xor butterflies */
+      float lf[32], lw[32], lp[32];
+      for (int l = 0; l < 32; ++l) lf[l] = lw[l] = lp[l] = 0.0f;
+      for (int i = 0; i < N; ++i) {
+        float fi, wi;
+        atom_terms(p, &RS, ptd, &y[3 * i], &fi, &wi, NULL);
+        lf[i & 31] = lf[i & 31] + fi;
+        lw[i & 31] = lw[i & 31] + wi;
+      }
+      long pi = 0;
+      for (int i = 0; i < N; ++i)
+        for (int k = i + 1; k < N; ++k, ++pi) lp[pi & 31] = lp[pi & 31] + pair_d(p, &y[3 * i], &y[3 * k]);
+      const float fb = butterfly(lf), wb = butterfly(lw), pb = butterfly(lp);
+      S = fb - p->lam * (pb + wb);
     }
     free(fa); free(wa); free(inm);
     pose_coords(L, y, &RS, ptd, x);

@@ -39,6 +39,7 @@ typedef struct {
   double diversity_delta;
   int32_t keep_top, write_all;
   double min_score;
+  int32_t polish, reserved; /* 0 off, 1 rigid compass, 2 + fine torsion pass (SWEEP_V1.md §3.5) */
 } vso_params;
 
 typedef struct {

@@ -60,7 +60,8 @@ class vs_dock_params(C.Structure):
     _fields_ = [("restarts", C.c_int32), ("rotations", C.c_int32), ("flex_angles", C.c_int32),
                 ("flex_passes", C.c_int32), ("diversity_delta", C.c_double),
                 ("keep_top", C.c_int32), ("write_all_poses", C.c_int32),
-                ("min_score", C.c_double), ("rotation_seed", C.c_uint64)]
+                ("min_score", C.c_double), ("rotation_seed", C.c_uint64), ("polish", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 class vs_pose(C.Structure):

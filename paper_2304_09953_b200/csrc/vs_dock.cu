@@ -188,7 +188,8 @@ static __device__ VS_PHASE int sweep_phase(const PocketDev& pk, const Dims d,
 template <int kGrid>
 static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, int N, int T,
                                                 int F, int A, float step, const PoseF* P,
-                                                int lane, unsigned long long* n_active) {
+                                                int lane, unsigned long long* n_active,
+                                                int polish) {
   const WarpSmem s = dock_smem(d);
   const int a_lane = lane & 15;
   const int h = lane >> 4;
@@ -207,7 +208,9 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
   }
   __syncwarp();
   const bool do_flex = T > 0 && F > 0;
-  const int steps = do_flex ? F * T : 1;
+  const int steps0 = do_flex ? F * T : 1;
+  // polish 2: one more pass over the torsions with fine candidate angles
+  const int steps = steps0 + ((do_flex && polish >= 2) ? T : 0);
   const int W = (N + 31) >> 5;
   float S_cur = 0.0f;
   int nact = 0;  // pair softplus evaluations of this lane (work counter)
@@ -254,7 +257,14 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
       const float th_old = s.theta[j];
       th_new = th_old;
       if (a_lane > 0) {
-        float v = th_old + static_cast<float>(a_lane) * step;
+        float v;
+        if (st >= steps0) {  // fine pass: offsets (-A/2, A/2] of step / 8
+          const int off = a_lane <= A / 2 ? a_lane : a_lane - A;
+          v = th_old + static_cast<float>(off) * (step * 0.125f);
+          if (v < -kPiF) v = v + kTwoPiF;
+        } else {
+          v = th_old + static_cast<float>(a_lane) * step;
+        }
         if (v >= kPiF) v = v - kTwoPiF;
         th_new = v;
       }
@@ -323,6 +333,142 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
   for (int off = 16; off > 0; off >>= 1) nact += __shfl_xor_sync(kFull, nact, off);
   *n_active += static_cast<unsigned long long>(nact);
   return S_cur;
+}
+
+// ---- polish (SWEEP_V1.md §3.5): rigid compass on the flexed state with the
+// sweep key (lanes 0..12: keep, +-ang about world x y z through the posed
+// centroid, +-sc along x y z; argmax, ties to the lowest lane; halve on keep),
+// then the canonical score of the final pose as a flex step with an empty
+// moving set (lane-strided atom and pair sums, xor butterflies).
+constexpr float kPolishAng0 = 0.140625f;
+constexpr float kPolishSc0 = 0.25f;
+constexpr float kPolishAngMin = 0.00390625f;
+constexpr int kPolishIters = 40;
+
+template <int kGrid, bool kInl>
+static __device__ VS_PHASE float polish_phase(const PocketDev& pk, const Dims d, int N, int lane,
+                                              PoseF* P) {
+  const WarpSmem s = dock_smem(d);
+  for (int i = lane; i < N; i += 32) {
+    const double4 v = s.ys[i];
+    s.ysf[i] = make_float4(static_cast<float>(v.x), static_cast<float>(v.y),
+                           static_cast<float>(v.z), 0.0f);
+  }
+  __syncwarp();
+  float cx = 0.0f, cy = 0.0f, cz = 0.0f;
+  for (int i = 0; i < N; ++i) {
+    const float4 v = s.ysf[i];
+    cx = cx + v.x;
+    cy = cy + v.y;
+    cz = cz + v.z;
+  }
+  const float fN = static_cast<float>(N);
+  cx = cx / fN;
+  cy = cy / fN;
+  cz = cz / fN;
+  float qw = P->q[0], qx = P->q[1], qy = P->q[2], qz = P->q[3];
+  float tx = P->t[0], ty = P->t[1], tz = P->t[2];
+  float ang = kPolishAng0, sc = kPolishSc0;
+  for (int it = 0; it < kPolishIters && ang >= kPolishAngMin; ++it) {
+    const Mat3 R0 = det_quat_mat(qw, qx, qy, qz);
+    float Cx, Cy, Cz;
+    det_apply(R0, cx, cy, cz, tx, ty, tz, &Cx, &Cy, &Cz);
+    float sh, ch;
+    det_sincos(0.5f * ang, &sh, &ch);
+    float w2 = qw, x2 = qx, y2 = qy, z2 = qz, u2 = tx, v2 = ty, s2 = tz;
+    float key = -INFINITY;
+    if (lane < 13) {
+      Mat3 R2 = R0;
+      if (lane >= 1 && lane <= 6) {
+        const int ax = (lane - 1) >> 1;
+        const float sg = ((lane - 1) & 1) ? -sh : sh;
+        det_quat_mul(ch, ax == 0 ? sg : 0.0f, ax == 1 ? sg : 0.0f, ax == 2 ? sg : 0.0f, qw, qx,
+                     qy, qz, &w2, &x2, &y2, &z2);
+        det_quat_normalize(&w2, &x2, &y2, &z2);
+        R2 = det_quat_mat(w2, x2, y2, z2);
+        float vx, vy, vz;
+        det_apply(R2, cx, cy, cz, 0.0f, 0.0f, 0.0f, &vx, &vy, &vz);
+        u2 = Cx - vx;
+        v2 = Cy - vy;
+        s2 = Cz - vz;
+      } else if (lane >= 7) {
+        const int ax = (lane - 7) >> 1;
+        const bool neg = (lane - 7) & 1;
+        if (ax == 0) u2 = neg ? tx - sc : tx + sc;
+        if (ax == 1) v2 = neg ? ty - sc : ty + sc;
+        if (ax == 2) s2 = neg ? tz - sc : tz + sc;
+      }
+      key = kInl ? eval_key<kGrid, 1>(pk, s.ysf, N, R2, u2, v2, s2)
+                 : eval_rigid<kGrid>(pk, s.ysf, N, R2, u2, v2, s2);
+    }
+    int li = lane < 13 ? lane : 0x7fffffff;
+    for (int off = 16; off > 0; off >>= 1) {
+      const float ok = __shfl_xor_sync(kFull, key, off);
+      const int oi = __shfl_xor_sync(kFull, li, off);
+      if (ok > key || (ok == key && oi < li)) {
+        key = ok;
+        li = oi;
+      }
+    }
+    if (li == 0) {
+      ang = ang * 0.5f;
+      sc = sc * 0.5f;
+    } else {
+      qw = __shfl_sync(kFull, w2, li);
+      qx = __shfl_sync(kFull, x2, li);
+      qy = __shfl_sync(kFull, y2, li);
+      qz = __shfl_sync(kFull, z2, li);
+      tx = __shfl_sync(kFull, u2, li);
+      ty = __shfl_sync(kFull, v2, li);
+      tz = __shfl_sync(kFull, s2, li);
+    }
+  }
+  P->q[0] = qw;
+  P->q[1] = qx;
+  P->q[2] = qy;
+  P->q[3] = qz;
+  P->t[0] = tx;
+  P->t[1] = ty;
+  P->t[2] = tz;
+  __syncwarp();
+  if (lane == 0) {
+    const Mat3d RD = det_pose_mat_d(qw, qx, qy, qz);
+    double* pm = s.pose;
+    pm[0] = RD.m00; pm[1] = RD.m01; pm[2] = RD.m02;
+    pm[3] = RD.m10; pm[4] = RD.m11; pm[5] = RD.m12;
+    pm[6] = RD.m20; pm[7] = RD.m21; pm[8] = RD.m22;
+    pm[9] = tx; pm[10] = ty; pm[11] = tz;
+  }
+  __syncwarp();
+  float fb = 0.0f, wb = 0.0f, pb = 0.0f;
+  for (int i = lane; i < N; i += 32) {
+    const double4 v = s.ys[i];
+    float fi, wi;
+    atom_terms_s<kGrid>(s.pose, v.x, v.y, v.z, &fi, &wi);
+    fb = fb + fi;
+    wb = wb + wi;
+  }
+  {
+    int i = 0, k = lane + 1;
+    while (i < N - 1 && k >= N) {
+      k = k - N + i + 2;
+      ++i;
+    }
+    int nact = 0;
+    while (i < N - 1) {
+      const double4 yi = s.ys[i], yk = s.ys[k];
+      pb = pb + pair_term_d(pk, yi.x - yk.x, yi.y - yk.y, yi.z - yk.z, nact);
+      k += 32;
+      while (i < N - 1 && k >= N) {
+        k = k - N + i + 2;
+        ++i;
+      }
+    }
+  }
+  fb = warp_sum(fb);
+  wb = warp_sum(wb);
+  pb = warp_sum(pb);
+  return fb - c_pk.lam * (pb + wb);
 }
 
 // ---- final coordinates, diversity against kept (dock.cpp:359-361), store
@@ -491,7 +637,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB)
       const long long c1 = clock64();
       const int best_k = sweep_phase<kGrid>(pk, d, rots, prm.K, N, lane, &P, &n_trans);
       const long long c2 = clock64();
-      const float S = flex_phase<kGrid>(pk, d, N, T, prm.F, prm.A, step, &P, lane, &st[2]);
+      float S = flex_phase<kGrid>(pk, d, N, T, prm.F, prm.A, step, &P, lane, &st[2], prm.polish);
+      if (prm.polish >= 1) S = polish_phase<kGrid, false>(pk, d, N, lane, &P);
       const long long c3 = clock64();
       if (keep_phase(d, N, T, &P, S, r, att, best_k, kx, nmax, kp, 8 + tmax, km, nk, prm.delta,
                      lane))
@@ -639,7 +786,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_FLEX)
     vs_flex_kernel(const __grid_constant__ LibDev lib, const __grid_constant__ DockParams prm,
                    const int* __restrict__ order, int n_order, int* __restrict__ counter,
                    int nmax, int tmax, int mvmax, int r, const __grid_constant__ StageBufs sb) {
-  const Dims d{nmax, tmax, mvmax, kLayLig | kLayState | kLayPosed | kLayFlex};
+  const Dims d{nmax, tmax, mvmax, kLayLig | kLayState | kLayPosed | kLayFlex | kLaySweep};
   const WarpSmem s = dock_smem(d);
   const int lane = threadIdx.x & 31;
   if (lane == 0) mbar_init(s.bar);
@@ -666,7 +813,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_FLEX)
     P.q[3] = pq.w;
     __syncwarp();
     unsigned long long nact = 0;
-    const float S = flex_phase<kGrid>(pk, d, N, T, prm.F, prm.A, step, &P, lane, &nact);
+    float S = flex_phase<kGrid>(pk, d, N, T, prm.F, prm.A, step, &P, lane, &nact, prm.polish);
+    if (prm.polish >= 1) S = polish_phase<kGrid, true>(pk, d, N, lane, &P);
     const long long c1 = clock64();
     const int nk = sb.nk[lig];
     float4* kx = sb.kx + static_cast<size_t>(meta.x) * R;
@@ -770,7 +918,8 @@ static int stage_blocks(K kernel, size_t smem, int sms, int n_items, int target_
 
 size_t stage_smem_per_block(int nmax, int tmax, int mvmax) {
   const int lays[4] = {kLayLig | kLayState | kLayPosed, kLaySweep,
-                       kLayLig | kLayState | kLayPosed | kLayFlex, kLayLig | kLayKept};
+                       kLayLig | kLayState | kLayPosed | kLayFlex | kLaySweep,
+                       kLayLig | kLayKept};
   size_t m = 0;
   for (int l : lays) {
     const size_t b = kWarpsPerBlock * warp_smem_bytes(nmax, tmax, mvmax, l);
@@ -790,7 +939,8 @@ static cudaError_t staged_impl(int sms, cudaStream_t st, const LibDev& lib, cons
   const size_t sm_sweep = kWarpsPerBlock * warp_smem_bytes(nmax, 0, 0, kLaySweep);
   const size_t sm_flex = kWarpsPerBlock * warp_smem_bytes(
                                               nmax, tmax, mvmax,
-                                              kLayLig | kLayState | kLayPosed | kLayFlex);
+                                              kLayLig | kLayState | kLayPosed | kLayFlex |
+                                                  kLaySweep);
   const size_t sm_fin = kWarpsPerBlock * warp_smem_bytes(nmax, tmax, mvmax, kLayLig | kLayKept);
   const int b_start = stage_blocks(vs_start_kernel<kGrid>, sm_start, sms, n, 8);
   const int b_sweep = stage_blocks(vs_sweep_kernel<kGrid>, sm_sweep, sms, n, VS_MINB_SWEEP);

@@ -452,6 +452,7 @@ int check_params(vs_handle* h, const vs_dock_params* p) {
   if (p->rotations < 1) return fail(h, VS_ERR_INVALID_ARGUMENT, "rotations must be >= 1");
   if (p->flex_passes < 0 || p->keep_top < 0)
     return fail(h, VS_ERR_INVALID_ARGUMENT, "negative flex_passes/keep_top");
+  if (p->polish < 0 || p->polish > 2) return fail(h, VS_ERR_INVALID_ARGUMENT, "polish must be 0, 1 or 2");
   return VS_OK;
 }
 
@@ -703,6 +704,14 @@ int vs_dock(vs_handle* h, const vs_dock_params* prm, void* stream) {
   VS_CUDA(h, h->d_stats.ensure(8 * sizeof(unsigned long long)));
   VS_CUDA(h, cudaMemsetAsync(h->d_stats.p, 0, 8 * sizeof(unsigned long long), st));
   VS_CUDA(h, cudaMemsetAsync(h->d_keys.p, 0xff, nn * 8, st));
+  // unused survivor / kept slots read as zeros (not a previous run's poses)
+  VS_CUDA(h, cudaMemsetAsync(h->d_surv.p, 0, nn * std::max(KT, 1) * sizeof(PoseOut), st));
+  VS_CUDA(h, cudaMemsetAsync(h->d_surv_tors.p, 0,
+                             std::max<size_t>(1, P.total_tors) * std::max(KT, 1) * 4, st));
+  if (prm->write_all_poses) {
+    VS_CUDA(h, cudaMemsetAsync(h->d_all.p, 0, nn * R * sizeof(PoseOut), st));
+    VS_CUDA(h, cudaMemsetAsync(h->d_all_tors.p, 0, std::max<size_t>(1, P.total_tors) * R * 4, st));
+  }
   VS_CUDA(h, cudaMemsetAsync(h->d_nkept.p, 0, nn * 4, st));
   VS_CUDA(h, cudaMemsetAsync(h->d_nsurv.p, 0, nn * 4, st));
   VS_CUDA(h, cudaMemsetAsync(h->d_counters.p, 0, 256 * sizeof(int), st));
@@ -716,6 +725,7 @@ int vs_dock(vs_handle* h, const vs_dock_params* prm, void* stream) {
   dp.write_all = prm->write_all_poses ? 1 : 0;
   dp.delta = static_cast<float>(prm->diversity_delta);
   dp.min_score = prm->min_score;
+  dp.polish = prm->polish;
   DockOut out;
   out.surv = h->d_surv.as<PoseOut>();
   out.surv_tors = h->d_surv_tors.as<float>();

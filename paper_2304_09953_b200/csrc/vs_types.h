@@ -83,6 +83,7 @@ struct DockParams {
   int write_all;
   float delta;
   double min_score;
+  int polish;  // 0 off, 1 rigid compass, 2 + fine torsion pass (SWEEP_V1.md §3.5)
 };
 
 struct DockOut {

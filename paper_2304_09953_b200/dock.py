@@ -144,6 +144,7 @@ class DockParams:
     min_score: float = -1e30
     rotation_seed: int = 0x5EED
     write_all_poses: bool = False
+    polish: int = 2  # 0 off, 1 rigid compass, 2 + fine torsion pass (SWEEP_V1.md §3.5)
 
     def as_c(self) -> _capi.vs_dock_params:
         p = _capi.vs_dock_params()
@@ -152,6 +153,7 @@ class DockParams:
         p.diversity_delta, p.keep_top = self.diversity_delta, self.keep_top
         p.write_all_poses = 1 if self.write_all_poses else 0
         p.min_score, p.rotation_seed = self.min_score, self.rotation_seed
+        p.polish = self.polish
         return p
 
 

@@ -1,0 +1,71 @@
+"""Docking quality of sweep-v1 against the reference ascent on the same
+ligands, conformers, seeds and pocket (C2 workload prefix, analytic pocket):
+per ligand, the best survivor rescore of our GPU dock vs the reference's
+dock() + rescore + filter_poses (both scored by the same function).
+
+  python tools/quality_vs_reference.py [n_ligands] [threads] [--grid]
+
+Prints one JSON line: mean / median of (ours - reference) best rescore, the
+fraction of ligands where ours >= reference, and both wall times."""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    n = int(args[0]) if args else 64
+    threads = int(args[1]) if len(args) > 1 else (os.cpu_count() or 1)
+    grid = "--grid" in sys.argv
+    import bench
+    import paper_2304_09953_b200 as V
+    from oracle import ref as R
+    from paper_2304_09953_b200.chem import random_smiles
+    lib_all, _, _ = bench.build_workload(max(4 * n, 64), 0, 1, threads)
+    sel = list(range(0, len(lib_all), len(lib_all) // n))[:n]
+    lib = lib_all.subset(sel)
+    lib.seeds = lib_all.seeds[sel]
+    pocket = bench.make_pocket()
+    prm = bench.params()
+    eng = V.Engine(0)
+    eng.set_pocket(pocket, grid_spacing=0.4 if grid else 0.0, grid_pad=2.0)
+    t0 = time.perf_counter()
+    res = eng.dock_host(lib, prm)
+    t_gpu = time.perf_counter() - t0
+    ours = np.where(res.n_surv > 0, res.best.astype(np.float64), np.nan)
+    # the reference arm: same conformer bytes, same dock seeds, its own ascent
+    rp = R.RefPocket(V.pocket_to_json(pocket))
+    ao, _, _ = lib.offsets()
+    ligs = []
+    for i in range(len(lib)):
+        lg = R.RefLigand(random_smiles(bench.CORPUS_SEED, int(lib.ids[i][1:])), iterations=-1)
+        lg.set_coords(lib.coords[ao[i]:ao[i + 1]])
+        ligs.append(lg)
+    t0 = time.perf_counter()
+    kept, best = R.dock_best_many(ligs, rp, prm.restarts, prm.diversity_delta,
+                                  [int(s) for s in lib.seeds], 500, prm.keep_top, prm.min_score,
+                                  threads)
+    t_ref = time.perf_counter() - t0
+    ref = np.where(kept > 0, best, np.nan)
+    both = ~np.isnan(ours) & ~np.isnan(ref)
+    d = ours[both] - ref[both]
+    out = {"ligands": len(lib), "compared": int(both.sum()), "grid": grid,
+           "ours_only": int((~np.isnan(ours) & np.isnan(ref)).sum()),
+           "ref_only": int((np.isnan(ours) & ~np.isnan(ref)).sum()),
+           "mean_delta": float(d.mean()) if d.size else None,
+           "median_delta": float(np.median(d)) if d.size else None,
+           "frac_ours_ge_ref": float((d >= -1e-9).mean()) if d.size else None,
+           "mean_ours": float(np.nanmean(ours)), "mean_ref": float(np.nanmean(ref)),
+           "gpu_s": round(t_gpu, 3), "ref_s": round(t_ref, 2), "ref_threads": threads}
+    print(json.dumps(out))
+    eng.close()
+
+
+if __name__ == "__main__":
+    main()
