@@ -70,13 +70,15 @@ def make_pocket():
 def params():
     import paper_2304_09953_b200 as V
     return V.DockParams(restarts=30, rotations=256, flex_angles=16, flex_passes=2,
-                        diversity_delta=1.0, keep_top=4, min_score=-5.0, rotation_seed=0x5EED)
+                        diversity_delta=1.0, keep_top=4, min_score=-5.0, rotation_seed=0x5EED,
+                        polish=1)
 
 
 CONFIG = {"workload": "C2: 100k synthetic drug-like ligands/GPU (10-40 heavy atoms, <=10 torsions, "
                       "reference corpus + embed_3d), 400-site synthetic pocket, 0.4 A grid maps",
           "restarts": 30, "rotations": 256, "flex_angles": 16, "flex_passes": 2,
           "diversity_delta": 1.0, "keep_top": 4, "min_score": -5.0, "top_k": TOP_K,
+          "polish": 1,
           "grid_spacing": 0.4}
 
 
@@ -209,7 +211,9 @@ def algorithmic_work(lib, prm, stats, grid: bool, n_steric: int):
                                               np.minimum(to[:-1], len(m))) * (T > 0))) * R
     atom_f = ATOM_FLOP_KEY if grid else 31 + 11 * n_steric
     atom_x = ATOM_XU_KEY if grid else 2 * n_steric
-    pose_atoms = float(np.sum(R * K * N)) + 27.0 * stats["translation_iter_atoms"]
+    # translation lattice (27 lanes) or, with polish, the rigid compass (25 lanes)
+    lanes = 25.0 if getattr(prm, "polish", 0) >= 1 else 27.0
+    pose_atoms = float(np.sum(R * K * N)) + lanes * stats["translation_iter_atoms"]
     sweep_flop = pose_atoms * atom_f + R * K * len(lib) * POSE_ROT_FLOP
     sweep_xu = pose_atoms * atom_x + R * K * len(lib) * POSE_ROT_XU
     return {"sweep": (sweep_flop, sweep_xu), "flex": (flex_flop, flex_xu),

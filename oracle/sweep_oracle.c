@@ -544,11 +544,12 @@ static uint32_t orderable(float f) {
   return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
 }
 
-/* polish (SWEEP_V1.md §3.5): rigid compass on the flexed state */
-#define POLISH_ANG0 0.140625f  /* 8.06 deg */
-#define POLISH_SC0 0.25f
-#define POLISH_ANG_MIN 0.00390625f
-#define POLISH_ITERS 40
+/* polish (SWEEP_V1.md §3.5): rigid compass before and after the flex */
+#define POLISH_ANG0 0.28125f    /* 16.1 deg */
+#define POLISH_SC0 0.5f         /* A */
+#define POLISH_ANG_MIN 0.015625f
+#define POLISH_ANG_MAX 0.5625f  /* expansion cap */
+#define POLISH_ITERS 24
 
 #define TRANS_ITERS 16
 #define TRANS_MIN (1.0f / 64.0f)
@@ -561,29 +562,34 @@ static void trans_offset(int l, float sc, float* o) {
   o[2] = (float)(m / 9 - 1) * sc;
 }
 
-/* polish rigid compass (SWEEP_V1.md §3.5): candidate l = 0 keeps the pose;
- * l = 1..6 rotate by +-ang about world x, y, z through the posed centroid;
- * l = 7..12 translate by +-sc along x, y, z.  The argmax of the sweep key
- * (ties to the lowest l) is taken; when l = 0 wins, ang and sc halve. */
-static void rigid_compass(const vso_pocket* p, const lig_t* L, const float* ysf, const float* c,
-                          float* pq, float* pt) {
+/* polish rigid compass (SWEEP_V1.md §3.5).  Candidates: l = 0 keeps the
+ * pose; l = 1..6 rotate by +-ang about world x, y, z through the posed
+ * centroid; l = 7..12 translate by +-sc along x, y, z; l = 13..24 are the
+ * same moves at twice the step.  The argmax of the sweep key (ties to the
+ * lowest l) is taken: l = 0 halves ang and sc; a twice-step winner doubles
+ * them while ang < POLISH_ANG_MAX.  Returns the iterations run. */
+static int rigid_compass(const vso_pocket* p, const lig_t* L, const float* ysf, const float* c,
+                         float* pq, float* pt) {
   const float zero[3] = {0.0f, 0.0f, 0.0f};
   float ang = POLISH_ANG0, sc = POLISH_SC0;
-  for (int it = 0; it < POLISH_ITERS && ang >= POLISH_ANG_MIN; ++it) {
+  int it = 0;
+  for (; it < POLISH_ITERS && ang >= POLISH_ANG_MIN; ++it) {
     const mat3 R0 = quat_mat(pq[0], pq[1], pq[2], pq[3]);
     float Cw[3];
     apply(&R0, c, pt, Cw);
-    float sh, ch;
-    vso_sincos(0.5f * ang, &sh, &ch);
     float bk = -INFINITY, bq[4], bt[3];
     int bl = 0;
-    for (int l = 0; l < 13; ++l) {
+    for (int l = 0; l < 25; ++l) {
+      const int big = l >= 13, lm = big ? l - 12 : l;
+      const float a2 = big ? 2.0f * ang : ang, s2 = big ? 2.0f * sc : sc;
       float q2[4] = {pq[0], pq[1], pq[2], pq[3]}, t2[3] = {pt[0], pt[1], pt[2]};
       mat3 R2 = R0;
-      if (l >= 1 && l <= 6) {
-        const int ax = (l - 1) >> 1;
+      if (lm >= 1 && lm <= 6) {
+        const int ax = (lm - 1) >> 1;
+        float sh, ch;
+        vso_sincos(0.5f * a2, &sh, &ch);
         float dq[4] = {ch, 0.0f, 0.0f, 0.0f};
-        dq[1 + ax] = ((l - 1) & 1) ? -sh : sh;
+        dq[1 + ax] = ((lm - 1) & 1) ? -sh : sh;
         qmul(dq, pq, q2);
         qnormalize(q2);
         R2 = quat_mat(q2[0], q2[1], q2[2], q2[3]);
@@ -592,9 +598,9 @@ static void rigid_compass(const vso_pocket* p, const lig_t* L, const float* ysf,
         t2[0] = Cw[0] - v[0];
         t2[1] = Cw[1] - v[1];
         t2[2] = Cw[2] - v[2];
-      } else if (l >= 7) {
-        const int ax = (l - 7) >> 1;
-        t2[ax] = ((l - 7) & 1) ? pt[ax] - sc : pt[ax] + sc;
+      } else if (lm >= 7) {
+        const int ax = (lm - 7) >> 1;
+        t2[ax] = ((lm - 7) & 1) ? pt[ax] - s2 : pt[ax] + s2;
       }
       const float key = rigid_key(p, L, ysf, &R2, t2);
       if (key > bk) {
@@ -610,8 +616,13 @@ static void rigid_compass(const vso_pocket* p, const lig_t* L, const float* ysf,
     } else {
       memcpy(pq, bq, 16);
       memcpy(pt, bt, 12);
+      if (bl >= 13 && ang < POLISH_ANG_MAX) {
+        ang = ang * 2.0f;
+        sc = sc * 2.0f;
+      }
     }
   }
+  return it;
 }
 
 /* sweep-v1 for one ligand (dock.cpp:318-371 restated with the sweep) */
@@ -688,8 +699,11 @@ static void dock_one(const vso_pocket* p, const lig_t* L, uint64_t seed, uint32_
     float v[3];
     apply(&RSf, c, zero, v);
     float pt[3] = {C[0] - v[0], C[1] - v[1], C[2] - v[2]};
-    /* translation sweep: compass search, 26 neighbours, halving steps */
-    {
+    /* translation sweep: compass search, 26 neighbours, halving steps
+     * (polish >= 1: the rigid compass of §3.5 instead) */
+    if (prm->polish >= 1) {
+      rigid_compass(p, L, ysf, c, pq, pt);
+    } else {
       float sc = 1.0f;
       for (int it = 0; it < TRANS_ITERS && sc >= TRANS_MIN; ++it) {
         float bk = -INFINITY;

@@ -78,10 +78,101 @@ static __device__ VS_PHASE int start_phase(const PocketDev& pk, const Dims d,
 #define VS_SWEEP_U 1  // atoms per sweep-key iteration in the staged sweep kernel
 #endif
 
+// ---- rigid compass of the polish (SWEEP_V1.md §3.5), on the FP32 state
+// copy with the sweep key.  Lane l < 25 is candidate l: 0 keeps the pose;
+// 1..6 rotate by +-ang about world x y z through the posed centroid (cx, cy,
+// cz); 7..12 translate by +-sc along x y z; 13..24 the same at twice the
+// step.  Argmax, ties to the lowest lane; l = 0 halves the steps, a
+// twice-step winner doubles them while ang < kPolishAngMax.
+constexpr float kPolishAng0 = 0.28125f;
+constexpr float kPolishSc0 = 0.5f;
+constexpr float kPolishAngMin = 0.015625f;
+constexpr float kPolishAngMax = 0.5625f;
+constexpr int kPolishIters = 24;
+
+template <int kGrid, bool kInl>
+static __device__ __forceinline__ int rigid_compass(const PocketDev& pk, const float4* ysf, int N,
+                                                    float cx, float cy, float cz, PoseF* P,
+                                                    int lane) {
+  float qw = P->q[0], qx = P->q[1], qy = P->q[2], qz = P->q[3];
+  float tx = P->t[0], ty = P->t[1], tz = P->t[2];
+  float ang = kPolishAng0, sc = kPolishSc0;
+  int it = 0;
+  for (; it < kPolishIters && ang >= kPolishAngMin; ++it) {
+    const Mat3 R0 = det_quat_mat(qw, qx, qy, qz);
+    float Cx, Cy, Cz;
+    det_apply(R0, cx, cy, cz, tx, ty, tz, &Cx, &Cy, &Cz);
+    float w2 = qw, x2 = qx, y2 = qy, z2 = qz, u2 = tx, v2 = ty, s2 = tz;
+    float key = -INFINITY;
+    if (lane < 25) {
+      const bool big = lane >= 13;
+      const int lm = big ? lane - 12 : lane;
+      const float a2 = big ? 2.0f * ang : ang, sc2 = big ? 2.0f * sc : sc;
+      Mat3 R2 = R0;
+      if (lm >= 1 && lm <= 6) {
+        const int ax = (lm - 1) >> 1;
+        float sh, ch;
+        det_sincos(0.5f * a2, &sh, &ch);
+        const float sg = ((lm - 1) & 1) ? -sh : sh;
+        det_quat_mul(ch, ax == 0 ? sg : 0.0f, ax == 1 ? sg : 0.0f, ax == 2 ? sg : 0.0f, qw, qx,
+                     qy, qz, &w2, &x2, &y2, &z2);
+        det_quat_normalize(&w2, &x2, &y2, &z2);
+        R2 = det_quat_mat(w2, x2, y2, z2);
+        float vx, vy, vz;
+        det_apply(R2, cx, cy, cz, 0.0f, 0.0f, 0.0f, &vx, &vy, &vz);
+        u2 = Cx - vx;
+        v2 = Cy - vy;
+        s2 = Cz - vz;
+      } else if (lm >= 7) {
+        const int ax = (lm - 7) >> 1;
+        const bool neg = (lm - 7) & 1;
+        if (ax == 0) u2 = neg ? tx - sc2 : tx + sc2;
+        if (ax == 1) v2 = neg ? ty - sc2 : ty + sc2;
+        if (ax == 2) s2 = neg ? tz - sc2 : tz + sc2;
+      }
+      key = kInl ? eval_key<kGrid, 1>(pk, ysf, N, R2, u2, v2, s2)
+                 : eval_rigid<kGrid>(pk, ysf, N, R2, u2, v2, s2);
+    }
+    int li = lane < 25 ? lane : 0x7fffffff;
+    for (int off = 16; off > 0; off >>= 1) {
+      const float ok = __shfl_xor_sync(kFull, key, off);
+      const int oi = __shfl_xor_sync(kFull, li, off);
+      if (ok > key || (ok == key && oi < li)) {
+        key = ok;
+        li = oi;
+      }
+    }
+    if (li == 0) {
+      ang = ang * 0.5f;
+      sc = sc * 0.5f;
+    } else {
+      qw = __shfl_sync(kFull, w2, li);
+      qx = __shfl_sync(kFull, x2, li);
+      qy = __shfl_sync(kFull, y2, li);
+      qz = __shfl_sync(kFull, z2, li);
+      tx = __shfl_sync(kFull, u2, li);
+      ty = __shfl_sync(kFull, v2, li);
+      tz = __shfl_sync(kFull, s2, li);
+      if (li >= 13 && ang < kPolishAngMax) {
+        ang = ang * 2.0f;
+        sc = sc * 2.0f;
+      }
+    }
+  }
+  P->q[0] = qw;
+  P->q[1] = qx;
+  P->q[2] = qy;
+  P->q[3] = qz;
+  P->t[0] = tx;
+  P->t[1] = ty;
+  P->t[2] = tz;
+  return it;
+}
+
 template <int kGrid, bool kInl = false>
 static __device__ VS_PHASE int sweep_phase(const PocketDev& pk, const Dims d,
                                                const float4* __restrict__ rots, int K, int N,
-                                               int lane, PoseF* P, int* n_trans) {
+                                               int lane, PoseF* P, int* n_trans, int polish) {
   const WarpSmem s = dock_smem(d);
   float qs0 = P->q[0], qs1 = P->q[1], qs2 = P->q[2], qs3 = P->q[3];
   det_quat_normalize(&qs0, &qs1, &qs2, &qs3);
@@ -139,6 +230,17 @@ static __device__ VS_PHASE int sweep_phase(const PocketDev& pk, const Dims d,
     ptx = Cx - vx;
     pty = Cy - vy;
     ptz = Cz - vz;
+  }
+  if (polish >= 1) {  // §3.5: the rigid compass replaces the translation lattice
+    P->t[0] = ptx;
+    P->t[1] = pty;
+    P->t[2] = ptz;
+    P->q[0] = pw;
+    P->q[1] = px;
+    P->q[2] = py;
+    P->q[3] = pz;
+    *n_trans += rigid_compass<kGrid, kInl>(pk, s.ysf, N, cx, cy, cz, P, lane);
+    return best_k;
   }
   float sc = 1.0f;
   int it = 0;
@@ -335,19 +437,12 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
   return S_cur;
 }
 
-// ---- polish (SWEEP_V1.md §3.5): rigid compass on the flexed state with the
-// sweep key (lanes 0..12: keep, +-ang about world x y z through the posed
-// centroid, +-sc along x y z; argmax, ties to the lowest lane; halve on keep),
-// then the canonical score of the final pose as a flex step with an empty
-// moving set (lane-strided atom and pair sums, xor butterflies).
-constexpr float kPolishAng0 = 0.140625f;
-constexpr float kPolishSc0 = 0.25f;
-constexpr float kPolishAngMin = 0.00390625f;
-constexpr int kPolishIters = 40;
-
+// ---- polish (SWEEP_V1.md §3.5) after the flex: the rigid compass on the
+// flexed state, then the canonical score of the final pose as a flex step
+// with an empty moving set (lane-strided atom and pair sums, butterflies).
 template <int kGrid, bool kInl>
 static __device__ VS_PHASE float polish_phase(const PocketDev& pk, const Dims d, int N, int lane,
-                                              PoseF* P) {
+                                              PoseF* P, int* n_iter) {
   const WarpSmem s = dock_smem(d);
   for (int i = lane; i < N; i += 32) {
     const double4 v = s.ys[i];
@@ -366,70 +461,9 @@ static __device__ VS_PHASE float polish_phase(const PocketDev& pk, const Dims d,
   cx = cx / fN;
   cy = cy / fN;
   cz = cz / fN;
-  float qw = P->q[0], qx = P->q[1], qy = P->q[2], qz = P->q[3];
-  float tx = P->t[0], ty = P->t[1], tz = P->t[2];
-  float ang = kPolishAng0, sc = kPolishSc0;
-  for (int it = 0; it < kPolishIters && ang >= kPolishAngMin; ++it) {
-    const Mat3 R0 = det_quat_mat(qw, qx, qy, qz);
-    float Cx, Cy, Cz;
-    det_apply(R0, cx, cy, cz, tx, ty, tz, &Cx, &Cy, &Cz);
-    float sh, ch;
-    det_sincos(0.5f * ang, &sh, &ch);
-    float w2 = qw, x2 = qx, y2 = qy, z2 = qz, u2 = tx, v2 = ty, s2 = tz;
-    float key = -INFINITY;
-    if (lane < 13) {
-      Mat3 R2 = R0;
-      if (lane >= 1 && lane <= 6) {
-        const int ax = (lane - 1) >> 1;
-        const float sg = ((lane - 1) & 1) ? -sh : sh;
-        det_quat_mul(ch, ax == 0 ? sg : 0.0f, ax == 1 ? sg : 0.0f, ax == 2 ? sg : 0.0f, qw, qx,
-                     qy, qz, &w2, &x2, &y2, &z2);
-        det_quat_normalize(&w2, &x2, &y2, &z2);
-        R2 = det_quat_mat(w2, x2, y2, z2);
-        float vx, vy, vz;
-        det_apply(R2, cx, cy, cz, 0.0f, 0.0f, 0.0f, &vx, &vy, &vz);
-        u2 = Cx - vx;
-        v2 = Cy - vy;
-        s2 = Cz - vz;
-      } else if (lane >= 7) {
-        const int ax = (lane - 7) >> 1;
-        const bool neg = (lane - 7) & 1;
-        if (ax == 0) u2 = neg ? tx - sc : tx + sc;
-        if (ax == 1) v2 = neg ? ty - sc : ty + sc;
-        if (ax == 2) s2 = neg ? tz - sc : tz + sc;
-      }
-      key = kInl ? eval_key<kGrid, 1>(pk, s.ysf, N, R2, u2, v2, s2)
-                 : eval_rigid<kGrid>(pk, s.ysf, N, R2, u2, v2, s2);
-    }
-    int li = lane < 13 ? lane : 0x7fffffff;
-    for (int off = 16; off > 0; off >>= 1) {
-      const float ok = __shfl_xor_sync(kFull, key, off);
-      const int oi = __shfl_xor_sync(kFull, li, off);
-      if (ok > key || (ok == key && oi < li)) {
-        key = ok;
-        li = oi;
-      }
-    }
-    if (li == 0) {
-      ang = ang * 0.5f;
-      sc = sc * 0.5f;
-    } else {
-      qw = __shfl_sync(kFull, w2, li);
-      qx = __shfl_sync(kFull, x2, li);
-      qy = __shfl_sync(kFull, y2, li);
-      qz = __shfl_sync(kFull, z2, li);
-      tx = __shfl_sync(kFull, u2, li);
-      ty = __shfl_sync(kFull, v2, li);
-      tz = __shfl_sync(kFull, s2, li);
-    }
-  }
-  P->q[0] = qw;
-  P->q[1] = qx;
-  P->q[2] = qy;
-  P->q[3] = qz;
-  P->t[0] = tx;
-  P->t[1] = ty;
-  P->t[2] = tz;
+  *n_iter += rigid_compass<kGrid, kInl>(pk, s.ysf, N, cx, cy, cz, P, lane);
+  const float qw = P->q[0], qx = P->q[1], qy = P->q[2], qz = P->q[3];
+  const float tx = P->t[0], ty = P->t[1], tz = P->t[2];
   __syncwarp();
   if (lane == 0) {
     const Mat3d RD = det_pose_mat_d(qw, qx, qy, qz);
@@ -635,10 +669,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB)
       const long long c0 = clock64();
       const int att = start_phase(pk, d, rkey, N, T, kx, nmax, nk, prm.delta, lane, &P);
       const long long c1 = clock64();
-      const int best_k = sweep_phase<kGrid>(pk, d, rots, prm.K, N, lane, &P, &n_trans);
+      const int best_k = sweep_phase<kGrid>(pk, d, rots, prm.K, N, lane, &P, &n_trans, prm.polish);
       const long long c2 = clock64();
       float S = flex_phase<kGrid>(pk, d, N, T, prm.F, prm.A, step, &P, lane, &st[2], prm.polish);
-      if (prm.polish >= 1) S = polish_phase<kGrid, false>(pk, d, N, lane, &P);
+      if (prm.polish >= 1) S = polish_phase<kGrid, false>(pk, d, N, lane, &P, &n_trans);
       const long long c3 = clock64();
       if (keep_phase(d, N, T, &P, S, r, att, best_k, kx, nmax, kp, 8 + tmax, km, nk, prm.delta,
                      lane))
@@ -769,7 +803,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_SWEEP)
     P.q[2] = pq.z;
     P.q[3] = pq.w;
     int n_trans = 0;
-    const int best_k = sweep_phase<kGrid, true>(pk, d, rots, prm.K, N, lane, &P, &n_trans);
+    const int best_k = sweep_phase<kGrid, true>(pk, d, rots, prm.K, N, lane, &P, &n_trans,
+                                                prm.polish);
     if (lane == 0) {
       sb.pose[2 * lig] = make_float4(P.t[0], P.t[1], P.t[2], pt.w);
       sb.pose[2 * lig + 1] = make_float4(P.q[0], P.q[1], P.q[2], P.q[3]);
@@ -814,7 +849,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_FLEX)
     __syncwarp();
     unsigned long long nact = 0;
     float S = flex_phase<kGrid>(pk, d, N, T, prm.F, prm.A, step, &P, lane, &nact, prm.polish);
-    if (prm.polish >= 1) S = polish_phase<kGrid, true>(pk, d, N, lane, &P);
+    int n_post = 0;
+    if (prm.polish >= 1) S = polish_phase<kGrid, true>(pk, d, N, lane, &P, &n_post);
     const long long c1 = clock64();
     const int nk = sb.nk[lig];
     float4* kx = sb.kx + static_cast<size_t>(meta.x) * R;
@@ -825,6 +861,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_FLEX)
     if (lane == 0) {
       if (kept) sb.nk[lig] = nk + 1;
       sb.st[8 * lig + 2] += nact;
+      sb.st[8 * lig + 0] += static_cast<unsigned long long>(n_post);
       sb.st[8 * lig + 6] += static_cast<unsigned long long>(c1 - c0);
       sb.st[8 * lig + 7] += static_cast<unsigned long long>(clock64() - c1);
     }

@@ -144,7 +144,7 @@ class DockParams:
     min_score: float = -1e30
     rotation_seed: int = 0x5EED
     write_all_poses: bool = False
-    polish: int = 2  # 0 off, 1 rigid compass, 2 + fine torsion pass (SWEEP_V1.md §3.5)
+    polish: int = 1  # 0 off, 1 rigid compass, 2 + fine torsion pass (SWEEP_V1.md §3.5)
 
     def as_c(self) -> _capi.vs_dock_params:
         p = _capi.vs_dock_params()
