@@ -174,6 +174,10 @@ int vs_last_phase_ms(vs_handle* h, double out[4]);
  * softplus evaluations (pairs inside the cutoff), [4..7] SM cycles summed
  * over warps in the start, sweep, flex and keep phases */
 int vs_last_stats(vs_handle* h, uint64_t out[8]);
+/* the same, up to n counters (returns how many were written): [8] rigid
+ * compass iterations after the flex (polish), [9] the same weighted by
+ * ligand atoms ([0]/[1] then count the sweep's lattice or compass only) */
+int vs_last_stats_ex(vs_handle* h, uint64_t* out, int32_t n);
 /* measured device peaks (ops/s): FP32 FMA (2 flops), FP64 FMA, MUFU ex2 */
 int vs_measure_peaks(vs_handle* h, double* fp32_flops, double* fp64_flops, double* xu_ops);
 

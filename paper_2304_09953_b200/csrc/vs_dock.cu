@@ -619,6 +619,8 @@ static __device__ VS_PHASE void finish_phase(const PocketDev& pk, const Dims d,
       atomicAdd(out.stats + 1, st[0] * static_cast<unsigned long long>(N));
       atomicAdd(out.stats + 2, st[1]);
       atomicAdd(out.stats + 3, st[2]);
+      atomicAdd(out.stats + 8, st[3]);
+      atomicAdd(out.stats + 9, st[3] * static_cast<unsigned long long>(N));
     }
   }
   __syncwarp();
@@ -659,8 +661,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB)
     const int N = meta.y, T = meta.w;
     const unsigned long long root = rng_mix(lib.seeds[lig] ^ kGolden);
     int nk = 0;
-    int n_trans = 0;
-    unsigned long long st[3] = {0, 0, 0};  // translation iters, attempts, active pairs
+    int n_trans = 0, n_post = 0;
+    unsigned long long st[4] = {0, 0, 0, 0};  // sweep refinement iters, attempts, pairs, post iters
     long long cyc[4] = {0, 0, 0, 0};       // start, sweep, flex, keep (SM cycles)
     for (int r = 0; r < R; ++r) {
       const unsigned long long rkey =
@@ -672,7 +674,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB)
       const int best_k = sweep_phase<kGrid>(pk, d, rots, prm.K, N, lane, &P, &n_trans, prm.polish);
       const long long c2 = clock64();
       float S = flex_phase<kGrid>(pk, d, N, T, prm.F, prm.A, step, &P, lane, &st[2], prm.polish);
-      if (prm.polish >= 1) S = polish_phase<kGrid, false>(pk, d, N, lane, &P, &n_trans);
+      if (prm.polish >= 1) S = polish_phase<kGrid, false>(pk, d, N, lane, &P, &n_post);
       const long long c3 = clock64();
       if (keep_phase(d, N, T, &P, S, r, att, best_k, kx, nmax, kp, 8 + tmax, km, nk, prm.delta,
                      lane))
@@ -684,6 +686,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB)
       st[1] += static_cast<unsigned long long>(att) + 1;
     }
     st[0] = static_cast<unsigned long long>(n_trans);
+    st[3] = static_cast<unsigned long long>(n_post);
     finish_phase<kGrid>(pk, d, prm, out, lig, meta, nk, kx, nmax, kp, 8 + tmax, km,
                         lib.id_rank[lig], lane, st);
     if (lane == 0 && out.stats)
@@ -861,7 +864,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_FLEX)
     if (lane == 0) {
       if (kept) sb.nk[lig] = nk + 1;
       sb.st[8 * lig + 2] += nact;
-      sb.st[8 * lig + 0] += static_cast<unsigned long long>(n_post);
+      sb.st[8 * lig + 3] += static_cast<unsigned long long>(n_post);
       sb.st[8 * lig + 6] += static_cast<unsigned long long>(c1 - c0);
       sb.st[8 * lig + 7] += static_cast<unsigned long long>(clock64() - c1);
     }

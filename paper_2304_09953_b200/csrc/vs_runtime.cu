@@ -23,6 +23,7 @@ size_t dock_smem_per_block(int nmax, int tmax, int mvmax);
 size_t rescore_smem_per_block(int nmax, int tmax, int mvmax);
 int dock_blocks_per_sm(bool grid, size_t smem);
 size_t stage_smem_per_block(int nmax, int tmax, int mvmax);
+constexpr int kStats = 10;  // work counters (capi.h vs_last_stats_ex)
 
 // dock execution mode: "staged" (one kernel per phase and restart) or
 // "fused" (one persistent kernel); VSCREEN_DOCK_MODE overrides the default
@@ -701,8 +702,8 @@ int vs_dock(vs_handle* h, const vs_dock_params* prm, void* stream) {
   VS_CUDA(h, h->d_nsurv.ensure(nn * 4));
   VS_CUDA(h, h->d_keys.ensure(nn * 8));
   VS_CUDA(h, h->d_counters.ensure(256 * sizeof(int)));
-  VS_CUDA(h, h->d_stats.ensure(8 * sizeof(unsigned long long)));
-  VS_CUDA(h, cudaMemsetAsync(h->d_stats.p, 0, 8 * sizeof(unsigned long long), st));
+  VS_CUDA(h, h->d_stats.ensure(kStats * sizeof(unsigned long long)));
+  VS_CUDA(h, cudaMemsetAsync(h->d_stats.p, 0, kStats * sizeof(unsigned long long), st));
   VS_CUDA(h, cudaMemsetAsync(h->d_keys.p, 0xff, nn * 8, st));
   // unused survivor / kept slots read as zeros (not a previous run's poses)
   VS_CUDA(h, cudaMemsetAsync(h->d_surv.p, 0, nn * std::max(KT, 1) * sizeof(PoseOut), st));
@@ -838,6 +839,15 @@ int vs_last_stats(vs_handle* h, uint64_t out[8]) {
   VS_CUDA(h, cudaStreamSynchronize(h->last));
   VS_CUDA(h, cudaMemcpy(out, h->d_stats.p, 8 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
   return VS_OK;
+}
+
+int vs_last_stats_ex(vs_handle* h, uint64_t* out, int32_t n) {
+  if (!h->has_results) return fail(h, VS_ERR_STATE, "no results");
+  if (n < 0) return fail(h, VS_ERR_INVALID_ARGUMENT, "negative count");
+  const int m = n < kStats ? n : kStats;
+  VS_CUDA(h, cudaStreamSynchronize(h->last));
+  VS_CUDA(h, cudaMemcpy(out, h->d_stats.p, m * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  return m;
 }
 
 int vs_measure_peaks(vs_handle* h, double* fp32, double* fp64, double* xu) {

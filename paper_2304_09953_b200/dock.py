@@ -341,12 +341,13 @@ class Engine:
 
     def stats(self) -> dict:
         """Work counters of the last dock (capi.h vs_last_stats)."""
-        out = np.zeros(8, np.uint64)
-        check(_lib.vs_last_stats(self._h, ptr(out, C.c_uint64)), self._h, "stats")
+        out = np.zeros(10, np.uint64)
+        check(_lib.vs_last_stats_ex(self._h, ptr(out, C.c_uint64), 10), self._h, "stats")
         cyc = [int(v) for v in out[4:8]]
         tot = max(sum(cyc), 1)
         return {"translation_iters": int(out[0]), "translation_iter_atoms": int(out[1]),
                 "start_attempts": int(out[2]), "active_pairs": int(out[3]),
+                "post_compass_iters": int(out[8]), "post_compass_iter_atoms": int(out[9]),
                 "phase_cycle_share": {k: round(c / tot, 4) for k, c in
                                       zip(("start", "sweep", "flex", "keep"), cyc)}}
 
