@@ -287,6 +287,9 @@ enum : int {
   kLayFlex = 16,   // pose, fa, wa
   kLayKept = 32,   // kscore, kinv, kresc
   kLayCols = 64,   // rescore pose columns
+  // ysf and xf alias the conformer y0 (a kernel that no longer needs y0
+  // after staging: the flex kernel) -> 32 B/atom less shared memory, more L1
+  kLayAliasY0 = 128,
   kLayAll = kLayLig | kLayState | kLaySweep | kLayPosed | kLayFlex | kLayKept,
 };
 
@@ -298,8 +301,8 @@ __host__ __device__ inline size_t warp_layout(int nmax, int tmax, int mvmax, int
       (lay & kLayLig) ? 32 * n : 0,                 // 0 y0
       (lay & kLayState) ? 32 * n : 0,               // 1 ys
       (lay & kLayFlex) ? size_t(96) : 0,                    // 2 pose
-      (lay & kLaySweep) ? 16 * n : 0,               // 3 ysf
-      (lay & kLayPosed) ? 16 * n : 0,               // 4 xf
+      (lay & kLaySweep) && !(lay & kLayAliasY0) ? 16 * n : 0,  // 3 ysf
+      (lay & kLayPosed) && !(lay & kLayAliasY0) ? 16 * n : 0,  // 4 xf
       (lay & kLayFlex) ? align16(4 * n) : 0,        // 5 fa
       (lay & kLayFlex) ? align16(4 * n) : 0,        // 6 wa
       (lay & kLayLig) ? 16 * t : 0,                 // 7 ax
@@ -334,6 +337,10 @@ __device__ inline WarpSmem carve(unsigned char* base, int nmax, int tmax, int mv
   s.pose = (lay & kLayFlex) ? reinterpret_cast<double*>(base + o[2]) : nullptr;
   s.ysf = (lay & kLaySweep) ? reinterpret_cast<float4*>(base + o[3]) : nullptr;
   s.xf = (lay & kLayPosed) ? reinterpret_cast<float4*>(base + o[4]) : nullptr;
+  if ((lay & kLayAliasY0) && (lay & kLayLig)) {
+    if (lay & kLaySweep) s.ysf = reinterpret_cast<float4*>(base + o[0]);
+    if (lay & kLayPosed) s.xf = reinterpret_cast<float4*>(base + o[0] + 16 * size_t(nmax));
+  }
   s.fa = (lay & kLayFlex) ? reinterpret_cast<float*>(base + o[5]) : nullptr;
   s.wa = (lay & kLayFlex) ? reinterpret_cast<float*>(base + o[6]) : nullptr;
   s.ax = (lay & kLayLig) ? reinterpret_cast<int4*>(base + o[7]) : nullptr;

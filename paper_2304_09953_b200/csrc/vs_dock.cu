@@ -824,7 +824,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_FLEX)
     vs_flex_kernel(const __grid_constant__ LibDev lib, const __grid_constant__ DockParams prm,
                    const int* __restrict__ order, int n_order, int* __restrict__ counter,
                    int nmax, int tmax, int mvmax, int r, const __grid_constant__ StageBufs sb) {
-  const Dims d{nmax, tmax, mvmax, kLayLig | kLayState | kLayPosed | kLayFlex | kLaySweep};
+  const Dims d{nmax, tmax, mvmax,
+               kLayLig | kLayState | kLayPosed | kLayFlex | kLaySweep | kLayAliasY0};
   const WarpSmem s = dock_smem(d);
   const int lane = threadIdx.x & 31;
   if (lane == 0) mbar_init(s.bar);
@@ -958,7 +959,7 @@ static int stage_blocks(K kernel, size_t smem, int sms, int n_items, int target_
 
 size_t stage_smem_per_block(int nmax, int tmax, int mvmax) {
   const int lays[4] = {kLayLig | kLayState | kLayPosed, kLaySweep,
-                       kLayLig | kLayState | kLayPosed | kLayFlex | kLaySweep,
+                       kLayLig | kLayState | kLayPosed | kLayFlex | kLaySweep | kLayAliasY0,
                        kLayLig | kLayKept};
   size_t m = 0;
   for (int l : lays) {
@@ -980,7 +981,7 @@ static cudaError_t staged_impl(int sms, cudaStream_t st, const LibDev& lib, cons
   const size_t sm_flex = kWarpsPerBlock * warp_smem_bytes(
                                               nmax, tmax, mvmax,
                                               kLayLig | kLayState | kLayPosed | kLayFlex |
-                                                  kLaySweep);
+                                                  kLaySweep | kLayAliasY0);
   const size_t sm_fin = kWarpsPerBlock * warp_smem_bytes(nmax, tmax, mvmax, kLayLig | kLayKept);
   const int b_start = stage_blocks(vs_start_kernel<kGrid>, sm_start, sms, n, 8);
   const int b_sweep = stage_blocks(vs_sweep_kernel<kGrid>, sm_sweep, sms, n, VS_MINB_SWEEP);
