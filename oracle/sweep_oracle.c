@@ -221,7 +221,8 @@ struct vso_pocket {
   float gx0, gy0, gz0, h, inv_h;
   int nx, ny, nz;
   float *steric, *hbond, *lipo;
-  float* key; /* sweep-key map: steric - lam * wall at each node */
+  float* key; /* sweep-key map: steric - lam * wall at each node (FP16-rounded) */
+  float* keyc; /* per cell: its trilinear polynomial, 8 FP16-rounded coefficients */
 };
 
 static float site_sum(const site_f* s, int n, float x, float y, float z) {
@@ -311,6 +312,7 @@ int vso_pocket_new(const vso_pocket_desc* d, vso_pocket** out) {
     p->hbond = (float*)malloc(nodes * 4);
     p->lipo = (float*)malloc(nodes * 4);
     p->key = (float*)malloc(nodes * 4);
+    p->keyc = (float*)malloc((size_t)(p->nx - 1) * (p->ny - 1) * (p->nz - 1) * 8 * 4 + 32);
     for (size_t id = 0; id < nodes; ++id) {
       int ix = (int)(id % (size_t)p->nx), iy = (int)((id / (size_t)p->nx) % (size_t)p->ny);
       int iz = (int)(id / ((size_t)p->nx * p->ny));
@@ -322,6 +324,22 @@ int vso_pocket_new(const vso_pocket_desc* d, vso_pocket** out) {
       const float xn[3] = {x, y, z};
       p->key[id] = (float)(_Float16)fmaf(-p->lam, wall(p, xn), p->steric[id]); /* FP16 map, RNE */
     }
+    { /* cell polynomials (vs_pack_half_kernel): FP32 differences, rounded to FP16 */
+      const long cx = p->nx - 1, cy = p->ny - 1, cz = p->nz - 1, sx = 1, sy = p->nx;
+      const long sz = (long)p->nx * p->ny;
+      for (long id = 0; id < cx * cy * cz; ++id) {
+        const long ix = id % cx, iy = (id / cx) % cy, iz = id / (cx * cy);
+        const float* v = p->key + iz * sz + iy * sy + ix;
+        const float v000 = v[0], v100 = v[sx], v010 = v[sy], v110 = v[sy + sx];
+        const float v001 = v[sz], v101 = v[sz + sx], v011 = v[sz + sy], v111 = v[sz + sy + sx];
+        const float c100 = v100 - v000, c010 = v010 - v000, c001 = v001 - v000;
+        const float c110 = (v110 - v100) - c010, c101 = (v101 - v100) - c001;
+        const float c011 = (v011 - v010) - c001;
+        const float c111 = ((v111 - v110) - (v101 - v100)) - c011;
+        const float cc[8] = {v000, c100, c010, c110, c001, c101, c011, c111};
+        for (int k = 0; k < 8; ++k) p->keyc[8 * id + k] = (float)(_Float16)cc[k];
+      }
+    }
   }
   *out = p;
   return 0;
@@ -329,7 +347,7 @@ int vso_pocket_new(const vso_pocket_desc* d, vso_pocket** out) {
 
 void vso_pocket_free(vso_pocket* p) {
   if (!p) return;
-  free(p->sites); free(p->steric); free(p->hbond); free(p->lipo); free(p->key);
+  free(p->sites); free(p->steric); free(p->hbond); free(p->lipo); free(p->key); free(p->keyc);
   free(p);
 }
 
@@ -489,10 +507,10 @@ static float rigid_key(const vso_pocket* p, const lig_t* L, const float* y, cons
           (unsigned)iz <= (unsigned)(p->nz - 2)) {
         float tx = g[0] - fx, ty = g[1] - fy, tz = g[2] - fz;
         long sx = p->nx, sxy = (long)p->nx * p->ny;
-        const float* b = p->key + ((long)iz * p->ny + iy) * p->nx + ix;
-        float c00 = lerp(b[0], b[1], tx), c10 = lerp(b[sx], b[sx + 1], tx);
-        float c01 = lerp(b[sxy], b[sxy + 1], tx), c11 = lerp(b[sxy + sx], b[sxy + sx + 1], tx);
-        term = lerp(lerp(c00, c10, ty), lerp(c01, c11, ty), tz);
+        (void)sx; (void)sxy;
+        const float* c8 = p->keyc + 8 * (((long)iz * (p->ny - 1) + iy) * (p->nx - 1) + ix);
+        term = fmaf(fmaf(fmaf(c8[7], tz, c8[3]), ty, fmaf(c8[5], tz, c8[1])), tx,
+                    fmaf(fmaf(c8[6], tz, c8[2]), ty, fmaf(c8[4], tz, c8[0])));
       } else {
         /* linear wall: the softplus at z = 10 (r - w) >= 10 (r + pad) is z */
         const float x = fmaf(g[0], p->h, p->gx0), y = fmaf(g[1], p->h, p->gy0);

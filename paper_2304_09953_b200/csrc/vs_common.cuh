@@ -486,11 +486,11 @@ static __device__ __forceinline__ float eval_key(const PocketDev& pk, const floa
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         float term;
-        if (in[u]) {
+        if (in[u]) {  // the cell's trilinear polynomial (vs_pack_half_kernel), 7 FMAs
           const float tx1 = gx[u] - fx[u], ty1 = gy[u] - fy[u], tz1 = gz[u] - fz[u];
-          const float c00 = det_lerp(lo[u].x, lo[u].y, tx1), c10 = det_lerp(lo[u].z, lo[u].w, tx1);
-          const float c01 = det_lerp(hi[u].x, hi[u].y, tx1), c11 = det_lerp(hi[u].z, hi[u].w, tx1);
-          term = det_lerp(det_lerp(c00, c10, ty1), det_lerp(c01, c11, ty1), tz1);
+          const float4 a = lo[u], b = hi[u];  // (c000 c100 c010 c110), (c001 c101 c011 c111)
+          term = fmaf(fmaf(fmaf(b.w, tz1, a.w), ty1, fmaf(b.y, tz1, a.y)), tx1,
+                      fmaf(fmaf(b.z, tz1, a.z), ty1, fmaf(b.x, tz1, a.x)));
         } else {
           term = off_grid_term(gx[u], gy[u], gz[u]);
         }

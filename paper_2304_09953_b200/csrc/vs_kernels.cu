@@ -189,8 +189,10 @@ __global__ void vs_pack_kernel(const GridDev g, const float* __restrict__ node,
   }
 }
 
-// FP16 node map -> 16 B corner cells (8 halves, same corner order): the
-// sweep key's lookups touch half the bytes and lines of an FP32 cell
+// FP16 node map -> 16 B cells holding the trilinear polynomial of the cell
+// (SWEEP_V1.md §3.2): c000, c100, c010, c110 | c001, c101, c011, c111, from
+// the corner values in the fixed FP32 order below, each rounded to FP16.
+// The sweep key evaluates it with 7 FMAs (the 7 lerps took 14 instructions).
 __global__ void vs_pack_half_kernel(const GridDev g, const float* __restrict__ node,
                                     uint4* __restrict__ cells) {
   const long cx = g.nx - 1, cy = g.ny - 1, cz = g.nz - 1;
@@ -204,8 +206,13 @@ __global__ void vs_pack_half_kernel(const GridDev g, const float* __restrict__ n
       const __half2 v = __floats2half2_rn(a, b);
       return *reinterpret_cast<const unsigned*>(&v);
     };
-    cells[id] = make_uint4(h2(p[0], p[sx]), h2(p[sy], p[sy + sx]), h2(p[sz], p[sz + sx]),
-                           h2(p[sz + sy], p[sz + sy + sx]));
+    const float v000 = p[0], v100 = p[sx], v010 = p[sy], v110 = p[sy + sx];
+    const float v001 = p[sz], v101 = p[sz + sx], v011 = p[sz + sy], v111 = p[sz + sy + sx];
+    const float c100 = v100 - v000, c010 = v010 - v000, c001 = v001 - v000;
+    const float c110 = (v110 - v100) - c010, c101 = (v101 - v100) - c001;
+    const float c011 = (v011 - v010) - c001;
+    const float c111 = ((v111 - v110) - (v101 - v100)) - c011;
+    cells[id] = make_uint4(h2(v000, c100), h2(c010, c110), h2(c001, c101), h2(c011, c111));
   }
 }
 
