@@ -1,7 +1,8 @@
 """Docking quality of sweep-v1 against the reference ascent on the same
 ligands, conformers, seeds and pocket (C2 workload prefix, analytic pocket):
-per ligand, the best survivor rescore of our GPU dock vs the reference's
-dock() + rescore + filter_poses (both scored by the same function).
+per ligand, the best survivor rescore of our GPU dock (each survivor pose
+re-scored by the reference's FP64 rescore, so grid mode is judged by the
+analytic score too) vs the reference's dock() + rescore + filter_poses.
 
   python tools/quality_vs_reference.py [n_ligands] [threads] [--grid]
 
@@ -39,6 +40,7 @@ def main():
     res = eng.dock_host(lib, prm)
     t_gpu = time.perf_counter() - t0
     ours = np.where(res.n_surv > 0, res.best.astype(np.float64), np.nan)
+    ours_ref_scored = np.full(len(lib), np.nan)  # our poses re-scored by the reference
     # the reference arm: same conformer bytes, same dock seeds, its own ascent
     rp = R.RefPocket(V.pocket_to_json(pocket))
     ao, _, _ = lib.offsets()
@@ -47,21 +49,28 @@ def main():
         lg = R.RefLigand(random_smiles(bench.CORPUS_SEED, int(lib.ids[i][1:])), iterations=-1)
         lg.set_coords(lib.coords[ao[i]:ao[i + 1]])
         ligs.append(lg)
+    for i in range(len(lib)):
+        vals = [ligs[i].rescore(rp, np.array(p.translation, np.float64),
+                                np.array(p.rotation, np.float64), np.array(p.torsions, np.float64))
+                for p in res.poses(i, int(lib.n_tors[i]), "surv")]
+        if vals:
+            ours_ref_scored[i] = max(vals)
     t0 = time.perf_counter()
     kept, best = R.dock_best_many(ligs, rp, prm.restarts, prm.diversity_delta,
                                   [int(s) for s in lib.seeds], 500, prm.keep_top, prm.min_score,
                                   threads)
     t_ref = time.perf_counter() - t0
     ref = np.where(kept > 0, best, np.nan)
-    both = ~np.isnan(ours) & ~np.isnan(ref)
-    d = ours[both] - ref[both]
+    both = ~np.isnan(ours_ref_scored) & ~np.isnan(ref)
+    d = ours_ref_scored[both] - ref[both]  # both sides scored by the reference's FP64 rescore
     out = {"ligands": len(lib), "compared": int(both.sum()), "grid": grid,
            "ours_only": int((~np.isnan(ours) & np.isnan(ref)).sum()),
            "ref_only": int((np.isnan(ours) & ~np.isnan(ref)).sum()),
            "mean_delta": float(d.mean()) if d.size else None,
            "median_delta": float(np.median(d)) if d.size else None,
            "frac_ours_ge_ref": float((d >= -1e-9).mean()) if d.size else None,
-           "mean_ours": float(np.nanmean(ours)), "mean_ref": float(np.nanmean(ref)),
+           "mean_ours": float(np.nanmean(ours_ref_scored)), "mean_ours_own_score": float(np.nanmean(ours)),
+           "mean_ref": float(np.nanmean(ref)), "polish": int(prm.polish),
            "gpu_s": round(t_gpu, 3), "ref_s": round(t_ref, 2), "ref_threads": threads}
     print(json.dumps(out))
     eng.close()
