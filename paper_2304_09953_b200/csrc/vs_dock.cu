@@ -853,6 +853,19 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_FLEX)
     __syncwarp();
     unsigned long long nact = 0;
     float S = flex_phase<kGrid>(pk, d, N, T, prm.F, prm.A, step, &P, lane, &nact, prm.polish);
+#ifndef VS_FUSED_POLISH
+    if (prm.polish >= 1) {
+      // the polish + keep run in vs_polish_kernel: hand over the flexed state
+      for (int i = lane; i < N; i += 32) sb.ys[meta.x + i] = s.ys[i];
+      for (int j = lane; j < T; j += 32) sb.th[meta.z + j] = s.theta[j];
+      if (lane == 0) {
+        sb.st[8 * lig + 2] += nact;
+        sb.st[8 * lig + 6] += static_cast<unsigned long long>(clock64() - c0);
+      }
+      __syncwarp();
+      continue;
+    }
+#endif
     int n_post = 0;
     if (prm.polish >= 1) S = polish_phase<kGrid, true>(pk, d, N, lane, &P, &n_post);
     const long long c1 = clock64();
@@ -865,6 +878,58 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_FLEX)
     if (lane == 0) {
       if (kept) sb.nk[lig] = nk + 1;
       sb.st[8 * lig + 2] += nact;
+      sb.st[8 * lig + 3] += static_cast<unsigned long long>(n_post);
+      sb.st[8 * lig + 6] += static_cast<unsigned long long>(c1 - c0);
+      sb.st[8 * lig + 7] += static_cast<unsigned long long>(clock64() - c1);
+    }
+    __syncwarp();
+  }
+}
+
+// polish (SWEEP_V1.md §3.5) + keep of restart r on the flexed state: the
+// compass runs here rather than in the flex kernel so it gets this kernel's
+// small shared-memory footprint (no conformer / topology) and a large L1 for
+// its key-map lookups.
+template <int kGrid>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 8)
+    vs_polish_kernel(const __grid_constant__ LibDev lib, const __grid_constant__ DockParams prm,
+                     const int* __restrict__ order, int n_order, int* __restrict__ counter,
+                     int nmax, int tmax, int r, const __grid_constant__ StageBufs sb) {
+  const Dims d{nmax, tmax, 0, kLayState | kLayPosed | kLayFlex | kLaySweep};
+  const WarpSmem s = dock_smem(d);
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) mbar_init(s.bar);
+  __syncwarp();
+  uint32_t phase = 0;
+  const PocketDev& pk = c_pk;
+  for (int w = next_item(counter, lane); w < n_order; w = next_item(counter, lane)) {
+    const int lig = order[w];
+    const int4 meta = lib.meta[lig];
+    const int N = meta.y, T = meta.w, R = prm.R;
+    tma_load(s.ys, sb.ys + meta.x, 32u * N, s.bar, phase, lane);
+    for (int j = lane; j < T; j += 32) s.theta[j] = sb.th[meta.z + j];
+    const long long c0 = clock64();
+    const float4 pt = sb.pose[2 * lig], pq = sb.pose[2 * lig + 1];
+    PoseF P;
+    P.t[0] = pt.x;
+    P.t[1] = pt.y;
+    P.t[2] = pt.z;
+    P.q[0] = pq.x;
+    P.q[1] = pq.y;
+    P.q[2] = pq.z;
+    P.q[3] = pq.w;
+    __syncwarp();
+    int n_post = 0;
+    const float S = polish_phase<kGrid, true>(pk, d, N, lane, &P, &n_post);
+    const long long c1 = clock64();
+    const int nk = sb.nk[lig];
+    float4* kx = sb.kx + static_cast<size_t>(meta.x) * R;
+    float* kp = sb.kp + (static_cast<size_t>(lig) * 8 + meta.z) * R;
+    int* km = sb.km + static_cast<size_t>(lig) * R * 4;
+    const bool kept = keep_phase(d, N, T, &P, S, r, __float_as_int(pt.w), sb.bk[lig], kx, N, kp,
+                                 8 + T, km, nk, prm.delta, lane);
+    if (lane == 0) {
+      if (kept) sb.nk[lig] = nk + 1;
       sb.st[8 * lig + 3] += static_cast<unsigned long long>(n_post);
       sb.st[8 * lig + 6] += static_cast<unsigned long long>(c1 - c0);
       sb.st[8 * lig + 7] += static_cast<unsigned long long>(clock64() - c1);
@@ -987,6 +1052,10 @@ static cudaError_t staged_impl(int sms, cudaStream_t st, const LibDev& lib, cons
   const int b_sweep = stage_blocks(vs_sweep_kernel<kGrid>, sm_sweep, sms, n, VS_MINB_SWEEP);
   const int b_flex = stage_blocks(vs_flex_kernel<kGrid>, sm_flex, sms, n, VS_MINB_FLEX);
   const int b_fin = stage_blocks(vs_finish_kernel<kGrid>, sm_fin, sms, n, 8);
+  const size_t sm_pol = kWarpsPerBlock * warp_smem_bytes(nmax, tmax, 0,
+                                                         kLayState | kLayPosed | kLayFlex |
+                                                             kLaySweep);
+  const int b_pol = stage_blocks(vs_polish_kernel<kGrid>, sm_pol, sms, n, 8);
   const int T = kWarpsPerBlock * 32;
   int c = 0;
   auto mark = [&](int kind, bool after) {  // event pair c: launch c (counter c)
@@ -1011,6 +1080,16 @@ static cudaError_t staged_impl(int sms, cudaStream_t st, const LibDev& lib, cons
     mark(2, true);
     ++c;
     *launches += 3;
+#ifndef VS_FUSED_POLISH
+    if (prm.polish >= 1) {
+      mark(2, false);
+      vs_polish_kernel<kGrid><<<b_pol, T, sm_pol, st>>>(lib, prm, order, n, counters + c, nmax,
+                                                       tmax, r, sb);
+      mark(2, true);
+      ++c;
+      *launches += 1;
+    }
+#endif
   }
   mark(3, false);
   vs_finish_kernel<kGrid><<<b_fin, T, sm_fin, st>>>(lib, prm, order, n, counters + c, nmax, tmax,

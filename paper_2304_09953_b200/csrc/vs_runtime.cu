@@ -701,7 +701,7 @@ int vs_dock(vs_handle* h, const vs_dock_params* prm, void* stream) {
   VS_CUDA(h, h->d_nkept.ensure(nn * 4));
   VS_CUDA(h, h->d_nsurv.ensure(nn * 4));
   VS_CUDA(h, h->d_keys.ensure(nn * 8));
-  VS_CUDA(h, h->d_counters.ensure(256 * sizeof(int)));
+  VS_CUDA(h, h->d_counters.ensure(320 * sizeof(int)));
   VS_CUDA(h, h->d_stats.ensure(kStats * sizeof(unsigned long long)));
   VS_CUDA(h, cudaMemsetAsync(h->d_stats.p, 0, kStats * sizeof(unsigned long long), st));
   VS_CUDA(h, cudaMemsetAsync(h->d_keys.p, 0xff, nn * 8, st));
@@ -715,7 +715,7 @@ int vs_dock(vs_handle* h, const vs_dock_params* prm, void* stream) {
   }
   VS_CUDA(h, cudaMemsetAsync(h->d_nkept.p, 0, nn * 4, st));
   VS_CUDA(h, cudaMemsetAsync(h->d_nsurv.p, 0, nn * 4, st));
-  VS_CUDA(h, cudaMemsetAsync(h->d_counters.p, 0, 256 * sizeof(int), st));
+  VS_CUDA(h, cudaMemsetAsync(h->d_counters.p, 0, 320 * sizeof(int), st));
 
   DockParams dp;
   dp.R = R;
@@ -771,13 +771,13 @@ int vs_dock(vs_handle* h, const vs_dock_params* prm, void* stream) {
     sb.kp = h->d_sg_kp.as<float>();
     sb.km = h->d_sg_km.as<int>();
     sb.st = h->d_sg_st.as<unsigned long long>();
-    const size_t npairs = 3 * static_cast<size_t>(R) + 1;
+    const size_t npairs = 4 * static_cast<size_t>(R) + 1;  // start, sweep, flex, polish; finish
     while (h->pev.size() < 2 * npairs) {
       cudaEvent_t e;
       VS_CUDA(h, cudaEventCreate(&e));
       h->pev.push_back(e);
     }
-    h->pkind.assign(npairs, 0);
+    h->pkind.assign(npairs, -1);  // -1: no launch recorded in this slot
     VS_CUDA(h, launch_staged(grid, h->sms, st, ld, h->pk, h->d_rots.as<const float4>(), dp,
                              P.d_order.as<int>() + b.start, b.count, h->d_counters.as<int>(),
                              b.nmax, b.tmax, b.mvmax, sb, out, &h->launches, h->pev.data(),
@@ -827,6 +827,7 @@ int vs_last_phase_ms(vs_handle* h, double out[4]) {
     return VS_OK;
   }
   for (size_t i = 0; i < h->pkind.size(); ++i) {
+    if (h->pkind[i] < 0) continue;
     float ms = 0.0f;
     VS_CUDA(h, cudaEventElapsedTime(&ms, h->pev[2 * i], h->pev[2 * i + 1]));
     out[h->pkind[i]] += ms;
