@@ -16,12 +16,12 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 1000 --
     --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e \
     > gpurun_out/ncu_launch_$TAG.log 2>&1 || echo "launch list failed"
 timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
-    --clock-control none -k regex:"vs_(start|sweep|flex|finish)_kernel" -c 4 --csv \
+    --clock-control none -k regex:"vs_(start|sweep|flex|polish|finish)_kernel" -c 5 --csv \
     --log-file gpurun_out/traffic_$TAG.csv \
     python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_traffic_$TAG.log 2>&1 || echo "traffic failed"
 timeout 300 python tools/profile_dock.py --ligands $NLIG > gpurun_out/profile_dock_$TAG.log 2>&1 || { echo "profile_dock failed"; exit 1; }
 cat gpurun_out/profile_dock_$TAG.log
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"vs_(sweep|flex)_kernel" -s 2 -c 2 \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"vs_(sweep|flex|polish)_kernel" -s 3 -c 3 \
     -f -o gpurun_out/prof_dock_$TAG python tools/profile_dock.py --ligands $NLIG \
     > gpurun_out/ncu_full_$TAG.log 2>&1 || echo "full capture failed"
 tail -3 gpurun_out/ncu_full_$TAG.log
