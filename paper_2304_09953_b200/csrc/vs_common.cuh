@@ -197,11 +197,8 @@ __device__ __forceinline__ float pair_term_d(const PocketDev& pk, double dx, dou
   if (d2 > static_cast<double>(c_pk.cut2)) return 0.0f;
   return det_softplus((c_pk.r - sqrtf(static_cast<float>(d2))) * 10.0f);
 }
-#ifndef VS_SOFT_ATTR
-#define VS_SOFT_ATTR __forceinline__
-#endif
 // clash softplus of a pair inside the cutoff, from its FP64 squared distance
-static __device__ VS_SOFT_ATTR float pair_soft(double d2) {
+__device__ __forceinline__ float pair_soft(double d2) {
   return det_softplus((c_pk.r - sqrtf(static_cast<float>(d2))) * 10.0f);
 }
 // same as pair_term_d, counting the pairs inside the cutoff (work counter)
@@ -232,11 +229,8 @@ __device__ __forceinline__ void atom_terms(const PocketDev& pk, const Mat3d& R, 
 
 // same, with the warp-uniform transform read from shared memory at each use
 // (keeps 24 FP64 registers free in the flex loops)
-#ifndef VS_TERMS_ATTR
-#define VS_TERMS_ATTR __forceinline__
-#endif
 template <int kGrid>
-static __device__ VS_TERMS_ATTR void atom_terms_s(const double* pm, double yx, double yy, double yz,
+__device__ __forceinline__ void atom_terms_s(const double* pm, double yx, double yy, double yz,
                                              float* f, float* w) {
   const volatile double* v = pm;
   const double x = fma(v[0], yx, fma(v[1], yy, fma(v[2], yz, v[9])));

@@ -60,11 +60,6 @@ __device__ __forceinline__ float det_log1p01(float u) {
 // the two tails are selected afterwards, so warps whose lanes straddle the
 // tails do not diverge.
 __device__ __forceinline__ float det_softplus(float z) {
-#ifdef VS_SP_BRANCHY
-  if (z > 30.0f) return z;
-  if (z < -30.0f) return 0.0f;
-  return fmaxf(z, 0.0f) + det_log1p01(det_exp_neg(-fabsf(z)));
-#endif
   const float zc = fminf(fmaxf(z, -30.0f), 30.0f);
   const float a = -fabsf(zc);
   const float sh = __fadd_rn(a * 1.44269504f, 12582912.0f);
