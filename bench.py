@@ -44,7 +44,10 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ligands", type=int, default=100_000, help="ligands per GPU")
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS),
+                    help="BASELINE.json config (c2 is the headline line)")
+    ap.add_argument("--ligands", type=int, default=None,
+                    help="ligands per GPU (c3: whole library, sharded)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -80,6 +83,45 @@ CONFIG = {"workload": "C2: 100k synthetic drug-like ligands/GPU (10-40 heavy ato
           "diversity_delta": 1.0, "keep_top": 4, "min_score": -5.0, "top_k": TOP_K,
           "polish": 1,
           "grid_spacing": 0.4}
+
+
+CONFIGS = {
+    "c2": dict(CONFIG, ligands_default=100_000, scaling="weak"),
+    "c3": dict(CONFIG, workload="C3: 1M synthetic drug-like ligands sharded across the GPUs "
+                                "(10-40 heavy atoms, <=10 torsions), 400-site synthetic pocket, 0.4 A "
+                                "grid maps, NCCL top-1000 gather", ligands_default=1_000_000,
+               scaling="strong"),
+    "c4": dict(CONFIG, workload="C4: 10k highly flexible ligands/GPU (60-80 heavy atoms, 15-20 "
+                                "torsions; concatenated reference corpus entries + embed_3d), 400-site "
+                                "synthetic pocket, 0.4 A grid maps, size classes {60..81}x{15..21}",
+               ligands_default=10_000, scaling="weak"),
+    "c5": dict(CONFIG, workload="C5: rescoring-only, 100k mixed ligands/GPU (96k corpus entries with "
+                                "1-40 heavy atoms + 4k flexible 60-80), keep_top 4 poses each from a "
+                                "C2-knob dock; 0.2 A maps over a 30 A box", ligands_default=100_000,
+               scaling="weak", grid_spacing=0.2),
+}
+C4_CLASSES = [(60, 81, 15, 21)]
+
+
+def build_flexible(n_per: int, rank: int, world: int, threads: int, seed: int = 7):
+    """C4 library shard: flexible_smiles (concatenated corpus entries, 60-80
+    atoms, 15-20 torsion axes), ids ranked globally, campaign seeds."""
+    import paper_2304_09953_b200 as V
+    from paper_2304_09953_b200.chem import flexible_smiles
+    from paper_2304_09953_b200.pipeline import campaign_seeds
+    total = n_per * world
+    smis = flexible_smiles(seed, total, max_scan=4000 * total + 100000)
+    assert len(smis) == total, f"flexible_smiles found {len(smis)} of {total}"
+    ids_all = [f"F{i}" for i in range(total)]
+    order = sorted(range(total), key=lambda i: ids_all[i].encode())
+    grank = np.empty(total, np.uint32)
+    grank[order] = np.arange(total, dtype=np.uint32)
+    lo, hi = rank * n_per, (rank + 1) * n_per
+    es = campaign_seeds(MASTER_SEED, total, stage=1)[lo:hi]
+    ds = campaign_seeds(MASTER_SEED, total, stage=2)[lo:hi]
+    lib = V.build_library(smis[lo:hi], ids_all[lo:hi], es, ds, threads=threads, drop_failed=False)
+    lib.id_rank = grank[lo:hi].copy()
+    return lib, ids_all, order
 
 
 def build_workload(n_per: int, rank: int, world: int, threads: int):
@@ -271,7 +313,7 @@ def load_traffic():
 
 
 # ------------------------------------------------------------ CPU baseline --
-def cpu_baseline(lib, pocket, prm, seconds: float):
+def cpu_baseline(lib, pocket, prm, seconds: float, name: str = "C2"):
     """The sweep-v1 C oracle (a port of the path) on the host cores, grid
     mode, on a bounded stride sample of the same library."""
     from oracle import sweep
@@ -289,7 +331,7 @@ def cpu_baseline(lib, pocket, prm, seconds: float):
     sweep.dock_library(op, lib, prm, threads=threads, sel=sel)
     dt = time.perf_counter() - t0
     return {"value": round(len(sel) / dt, 3), "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{len(sel)} ligands (stride sample of the C2 library), sweep-v1 C oracle, "
+            "sample": f"{len(sel)} ligands (stride sample of the {name} library), sweep-v1 C oracle, "
                       f"grid mode, {threads} threads, {dt:.1f} s"}
 
 
@@ -356,6 +398,137 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------- C5 rescoring-only --
+RESCORE_ATOM_FLOP = 18 + 3 * 25 + 13 + 46   # FP64 transform, 3 maps trilinear, wall + softplus
+RESCORE_ATOM_XU = 3 + 3 * 3 + 3              # conversions, cell indices, softplus
+
+
+def c5_library(n_per: int, rank: int, world: int, threads: int):
+    """96 % corpus entries with 1-40 heavy atoms (<= 10 torsions) + 4 %
+    flexible 60-80 atom ligands, in that order; ids ranked globally."""
+    import paper_2304_09953_b200 as V
+    from paper_2304_09953_b200.chem import corpus_indices, flexible_smiles, random_smiles
+    from paper_2304_09953_b200.pipeline import campaign_seeds
+    n_flex = max(1, n_per // 25)
+    n_small = n_per - n_flex
+    total = n_per * world
+    idx = corpus_indices(CORPUS_SEED, n_small * world, (1, 40), (0, 10), threads)
+    flex = flexible_smiles(11, n_flex * world, max_scan=4000 * n_flex * world + 100000)
+    sm = [random_smiles(CORPUS_SEED, int(i)) for i in idx[rank * n_small:(rank + 1) * n_small]]
+    sm += flex[rank * n_flex:(rank + 1) * n_flex]
+    ids = [f"M{rank * n_per + i}" for i in range(n_per)]
+    es = campaign_seeds(MASTER_SEED, total, stage=1)[rank * n_per:(rank + 1) * n_per]
+    ds = campaign_seeds(MASTER_SEED, total, stage=2)[rank * n_per:(rank + 1) * n_per]
+    lib = V.build_library(sm, ids, es, ds, threads=threads, drop_failed=False)
+    ids_all = [f"M{i}" for i in range(total)]
+    order = sorted(range(total), key=lambda i: ids_all[i].encode())
+    grank = np.empty(total, np.uint32)
+    grank[order] = np.arange(total, dtype=np.uint32)
+    lib.id_rank = grank[rank * n_per:(rank + 1) * n_per].copy()
+    return lib
+
+
+def survivor_poses(lib, res):
+    """Flatten the survivor poses of a dock (ligand-major, non-decreasing
+    ligand index) into the vs_rescore arrays."""
+    ns = np.maximum(res.n_surv, 0).astype(np.int64)
+    pl = np.repeat(np.arange(len(lib), dtype=np.int32), ns)
+    slot = np.arange(len(pl)) - np.repeat(np.cumsum(ns) - ns, ns)
+    rec = res.surv[pl, slot]
+    T = lib.n_tors.astype(np.int64)[pl]
+    start = res.tors_off[pl] * res.keep_top + slot * T
+    tix = np.repeat(start, T) + (np.arange(int(T.sum())) - np.repeat(np.cumsum(T) - T, T))
+    return pl, np.ascontiguousarray(rec["t"]), np.ascontiguousarray(rec["q"]), res.surv_tors[tix]
+
+
+def run_c5(args, rank, world, cfg):
+    """Rescoring-only (BASELINE configs[4]): every survivor pose of a C2-knob
+    dock re-scored (geometric score + rescore, K3a) against 0.2 A maps over a
+    30 A box.  value = ligands / device time of the rescore kernels; e2e =
+    the same through vs_rescore with host buffers (pack + H2D + kernels +
+    D2H), host wall clock."""
+    import torch
+    import torch.distributed as dist
+    import paper_2304_09953_b200 as V
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    threads = max(1, (os.cpu_count() or 1) // world)
+    n_per = args.ligands or cfg["ligands_default"]
+    t_build = time.perf_counter()
+    lib = c5_library(n_per, rank, world, threads)
+    t_build = time.perf_counter() - t_build
+    pocket = make_pocket()
+    eng = V.Engine(local)
+    eng.set_pocket(pocket, grid_spacing=0.4, grid_pad=2.0)
+    classes = [(1, 41, 0, 11), (60, 81, 11, 21)]
+    res = eng.dock_host(lib, params(), classes=classes)
+    pl, T, Q, TH = survivor_poses(lib, res)
+    box = V.Pocket(pocket.sites, (-15.0, -15.0, -15.0), (15.0, 15.0, 15.0), pocket.clash_radius,
+                   pocket.clash_penalty)
+    eng.set_pocket(box, grid_spacing=0.2, grid_pad=2.0)
+    peaks = eng.measure_peaks()
+    for _ in range(args.warmup):
+        eng.rescore(lib, pl, T, Q, TH)
+    dev_ms, wall = [], []
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            eng.rescore(lib, pl, T, Q, TH)
+            wall.append(time.perf_counter() - t0)
+            dev_ms.append(eng.last_rescore_ms())
+    t = torch.tensor([sum(dev_ms), sum(wall)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev_s, wall_s = float(t[0]) * 1e-3, float(t[1])
+    n_total = len(lib) * world
+    N = lib.n_atoms.astype(np.float64)[pl]
+    _, to, _ = lib.offsets()
+    m = lib.moving_count.astype(np.float64)
+    chain = np.add.reduceat(np.r_[AXIS_FLOP + MOVE_FLOP * m, 0.0], np.minimum(to[:-1], len(m)))
+    chain = np.where(lib.n_tors > 0, chain, 0.0)[pl]
+    flop = float(np.sum(chain + N * RESCORE_ATOM_FLOP + N * (N - 1) / 2 * PAIR_TEST_FLOP))
+    xu = float(np.sum(N * RESCORE_ATOM_XU))
+    per_s = np.mean(dev_ms) * 1e-3
+    if rank == 0:
+        bytes_in = h2d_bytes(lib) + len(pl) * (12 + 16 + 4) + TH.size * 4
+        line = {"metric": METRIC, "value": round(n_total * args.steps / dev_s, 2), "unit": UNIT,
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": round(1e3 * dev_s / args.steps, 3), "higher_is_better": True,
+                "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "f32+f64",
+                "data": "synthetic",
+                "config": {k: v for k, v in cfg.items() if k not in ("ligands_default", "scaling")}
+                | {"ligands_per_gpu": len(lib), "ligands_total": n_total, "poses_per_gpu": len(pl),
+                   "parallelism": f"dp{world}" if world > 1 else "single",
+                   "l2": "maps 4 x 150^3 cells (> L2 for the 3 score maps + key map); no flush",
+                   "timed": "rescore kernels over all survivor poses (device events)"},
+                "roofline": {"bound": "fp32", "achieved": round(flop / per_s / 1e12, 3),
+                             "peak": round(peaks["fp32_flops"] / 1e12, 3), "unit": "TFLOP/s",
+                             "frac": round(flop / per_s / peaks["fp32_flops"], 4), "traffic": None,
+                             "kernel": "vs_rescore_kernel",
+                             "xu_frac": round(xu / per_s / peaks["xu_ops"], 4)},
+                "cpu_baseline": None,
+                "e2e": {"value": round(n_total * args.steps / wall_s, 2), "unit": UNIT,
+                        "h2d_bytes_per_step": bytes_in * world,
+                        "d2h_bytes_per_step": 8 * len(pl) * world,
+                        "path": "vs_rescore (pack + H2D + rescore kernels + D2H), host wall clock"},
+                "gpu_launches": None, "clocks": clocks.summary(), "peaks": peaks,
+                "library_build_s": round(t_build, 2)}
+        s = json.dumps(line)
+        print(s, flush=True)
+        if args.json_out:
+            with open(args.json_out, "w") as f:
+                f.write(s + "\n")
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    eng.close()
+
+
 # ------------------------------------------------------------------- ours --
 def h2d_bytes(lib):
     A = int(np.sum(lib.n_atoms))
@@ -379,8 +552,12 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.config == "c5":
+        run_c5(args, rank, world, cfg)
         return
     import torch
     import torch.distributed as dist
@@ -392,14 +569,24 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     threads = max(1, (os.cpu_count() or 1) // world)
     t_build = time.perf_counter()
-    lib, ids_all, order = build_workload(args.ligands, rank, world, threads)
+    classes = None
+    if args.config == "c3":
+        n_per = (args.ligands or cfg["ligands_default"]) // world
+        lib, ids_all, order = build_workload(n_per, rank, world, threads)
+    elif args.config == "c4":
+        classes = C4_CLASSES
+        lib, ids_all, order = build_flexible(args.ligands or cfg["ligands_default"], rank, world,
+                                             threads)
+    else:
+        lib, ids_all, order = build_workload(args.ligands or cfg["ligands_default"], rank, world,
+                                             threads)
     t_build = time.perf_counter() - t_build
     pocket = make_pocket()
     prm = params()
     eng = V.Engine(local)
     eng.set_pocket(pocket, grid_spacing=0.4, grid_pad=2.0)
     peaks = eng.measure_peaks()
-    eng.upload(lib)
+    eng.upload(lib, classes)
     stream = torch.cuda.Stream()  # non-default stream shared by torch events and the C-ABI
     torch.cuda.set_stream(stream)
     sptr = stream.cuda_stream
@@ -450,14 +637,14 @@ def main():
     e2e = None
     if not args.no_e2e:
         n_e2e = max(1, min(args.steps, 3))
-        eng.dock_host(lib, prm)  # warm the host path
+        eng.dock_host(lib, prm, classes)  # warm the host path
         if world > 1:
             dist.barrier()
         e2e_t = []
         for _ in range(n_e2e):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            eng.dock_host(lib, prm)
+            eng.dock_host(lib, prm, classes)
             if world > 1:
                 merged = gather_topk(eng, TOP_K).cpu()
             else:
@@ -474,16 +661,18 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(lib, pocket, prm, args.cpu_seconds)
+        cpu = cpu_baseline(lib, pocket, prm, args.cpu_seconds, args.config.upper())
 
     if rank == 0:
         info = eng.device_info()
         line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": round(total_ms / args.steps, 3), "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64",
+                "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "f32+f64",
                 "data": "synthetic",
-                "config": dict(CONFIG, ligands_per_gpu=len(lib), ligands_total=n_total,
+                "config": dict({k: v for k, v in cfg.items()
+                                if k not in ("ligands_default", "scaling")},
+                               ligands_per_gpu=len(lib), ligands_total=n_total,
                                parallelism=f"dp{world}" if world > 1 else "single",
                                l2="flushed (512 MB write) before every timed step",
                                timed="device-resident library -> per-ligand best + global top-1000"),

@@ -206,6 +206,9 @@ int vs_score_gradient(vs_handle* h, const vs_library* lib, int64_t n_poses,
  * pose order, n_tors of its ligand each. */
 int vs_rescore(vs_handle* h, const vs_library* lib, int64_t n_poses, const int32_t* pose_lig,
                const float* t, const float* q, const float* tors, float* geo, float* resc);
+/* Device time (ms, CUDA events on the launch stream) of the rescore kernels
+ * of the last vs_rescore call (-1 before the first). */
+double vs_last_rescore_ms(const vs_handle* h);
 
 /* --------------------------------------------------- host-side (CPU) --- */
 /* Rng(seed).split(path...) then n next_u64 (rng.hpp:14-21) */
@@ -261,7 +264,10 @@ int vs_corpus_select(uint64_t seed, int64_t n_want, int32_t atom_lo, int32_t ato
 int vs_libbuild_corpus(uint64_t seed, const int64_t* index, int32_t n, const uint64_t* embed_seeds,
                        int32_t iterations, int32_t threads, vs_libbuild** out);
 /* flexible ligands (C4): consecutive corpus entries concatenated until
- * >= atom_lo atoms; accepted ligand k is entries [first[k], first[k]+count[k]) */
+ * >= atom_lo atoms; accepted ligand k is entries [first[k], first[k]+count[k]).
+ * The index space is scanned in fixed chunks of 16384 entries (each chunk
+ * from its own first entry) on all host threads; the selection does not
+ * depend on the thread count. */
 int vs_flexible_select(uint64_t seed, int32_t n_want, int32_t atom_lo, int32_t atom_hi,
                        int32_t tors_lo, int32_t tors_hi, int64_t max_scan, int64_t* first,
                        int32_t* count);

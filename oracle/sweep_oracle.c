@@ -486,7 +486,8 @@ static float score_state(const vso_pocket* p, const lig_t* L, const double* y, c
  * g = (R/h) y + (t - o)/h, and interpolates the key map K = S - lam W; an
  * atom off the grid scores the linear wall -lam * 10 (r - w) at x = g h + o
  * (the wall softplus there is its argument to ~1e-11).  Analytic mode:
- * F - lam W over the FP32 state copy.  Parity sums over atoms. */
+ * F - lam W over the FP32 state copy.  Grid mode sums the atoms in order
+ * into one accumulator; analytic mode uses parity sums. */
 static float rigid_key(const vso_pocket* p, const lig_t* L, const float* y, const mat3* R,
                        const float* t) {
   if (p->grid) {
@@ -494,7 +495,7 @@ static float rigid_key(const vso_pocket* p, const lig_t* L, const float* y, cons
     float A[9];
     for (int e = 0; e < 9; ++e) A[e] = R->m[e] * ih;
     const float u[3] = {(t[0] - p->gx0) * ih, (t[1] - p->gy0) * ih, (t[2] - p->gz0) * ih};
-    float K[2] = {0, 0};
+    float K = 0.0f;
     for (int i = 0; i < L->N; ++i) {
       const float* v = &y[3 * i];
       float g[3];
@@ -506,8 +507,6 @@ static float rigid_key(const vso_pocket* p, const lig_t* L, const float* y, cons
       if ((unsigned)ix <= (unsigned)(p->nx - 2) && (unsigned)iy <= (unsigned)(p->ny - 2) &&
           (unsigned)iz <= (unsigned)(p->nz - 2)) {
         float tx = g[0] - fx, ty = g[1] - fy, tz = g[2] - fz;
-        long sx = p->nx, sxy = (long)p->nx * p->ny;
-        (void)sx; (void)sxy;
         const float* c8 = p->keyc + 8 * (((long)iz * (p->ny - 1) + iy) * (p->nx - 1) + ix);
         term = fmaf(fmaf(fmaf(c8[7], tz, c8[3]), ty, fmaf(c8[5], tz, c8[1])), tx,
                     fmaf(fmaf(c8[6], tz, c8[2]), ty, fmaf(c8[4], tz, c8[0])));
@@ -519,9 +518,9 @@ static float rigid_key(const vso_pocket* p, const lig_t* L, const float* y, cons
                               fminf(z - p->lo[2], p->hi[2] - z));
         term = -(p->lam * ((p->r - w) * 10.0f));
       }
-      K[i & 1] = K[i & 1] + term;
+      K = K + term;
     }
-    return K[0] + K[1];
+    return K;
   }
   float F[2] = {0, 0}, W[2] = {0, 0};
   for (int i = 0; i < L->N; ++i) {

@@ -119,6 +119,7 @@ _SIGS = {
                                     P(C.c_double)]),
     "vs_rescore": (C.c_int, [C.c_void_p, P(vs_library), C.c_int64, P(C.c_int32), P(C.c_float),
                              P(C.c_float), P(C.c_float), P(C.c_float), P(C.c_float)]),
+    "vs_last_rescore_ms": (C.c_double, [C.c_void_p]),
     "vs_rng_u64": (C.c_int, [C.c_uint64, P(C.c_uint64), C.c_int32, C.c_int32, P(C.c_uint64)]),
     "vs_random_smiles": (C.c_int, [C.c_uint64, C.c_uint64, C.c_char_p, C.c_int32]),
     "vs_ligand_build": (C.c_int, [C.c_char_p, C.c_uint64, C.c_int32, P(vs_ligand_buf)]),
@@ -162,6 +163,8 @@ def _load() -> C.CDLL:
             "(there is no CPU fallback for the dock-and-score path)")
     lib = C.CDLL(LIB_PATH)
     for name, (res, args) in _SIGS.items():
+        if os.environ.get("VSCREEN_GPU_LIB") and not hasattr(lib, name):
+            continue  # an older experiment variant (A/B timing) may predate this entry point
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

@@ -137,8 +137,8 @@ __device__ __forceinline__ TriCell tri_issue(const GridDev& g, const float4* __r
   c.tx = gx - fx;
   c.ty = gy - fy;
   c.tz = gz - fz;
-  const int cell = c.in ? (iz * (g.ny - 1) + iy) * (g.nx - 1) + ix : 0;
-  ldg_cell(cells + 2 * cell, c.lo, c.hi);
+  const unsigned cell = static_cast<unsigned>(iz * g.cxy + iy * g.cx + ix);
+  ldg_cell(cells + 2 * (c.in ? cell : 0u), c.lo, c.hi);
   return c;
 }
 
@@ -440,10 +440,10 @@ __device__ __forceinline__ float off_grid_term(float gx, float gy, float gz) {
   return -(c_pk.lam * ((c_pk.r - w) * 10.0f));
 }
 
-// kU atoms per iteration (kU even or 1): the kU cell loads are all issued
-// before the first interpolation, so a warp keeps kU lookups in flight; a
-// ragged tail re-reads the last atom and drops its term.  Atom i goes to the
-// parity accumulator of i, so every kU gives the same key bits.
+// kU atoms per iteration: the kU cell loads are all issued before the first
+// interpolation, so a warp keeps kU lookups in flight; a ragged tail
+// re-reads the last atom and drops its term.  Grid mode sums the atom terms
+// in atom order into one accumulator, so every kU gives the same key bits.
 template <int kGrid, int kU = 1>
 static __device__ __forceinline__ float eval_key(const PocketDev& pk, const float4* ys, int N,
                                                  const Mat3 R, float tx, float ty, float tz) {
@@ -456,7 +456,7 @@ static __device__ __forceinline__ float eval_key(const PocketDev& pk, const floa
     const float ux = (tx - g.ox) * ih, uy = (ty - g.oy) * ih, uz = (tz - g.oz) * ih;
     const unsigned mx = static_cast<unsigned>(g.nx - 2), my = static_cast<unsigned>(g.ny - 2),
                    mz = static_cast<unsigned>(g.nz - 2);
-    float ke = 0.0f, ko = 0.0f;
+    float k = 0.0f;
 #pragma unroll 1
     for (int i0 = 0; i0 < N; i0 += kU) {
       float gx[kU], gy[kU], gz[kU], fx[kU], fy[kU], fz[kU];
@@ -475,7 +475,8 @@ static __device__ __forceinline__ float eval_key(const PocketDev& pk, const floa
                   iz = static_cast<int>(fz[u]);
         in[u] = static_cast<unsigned>(ix) <= mx && static_cast<unsigned>(iy) <= my &&
                 static_cast<unsigned>(iz) <= mz;
-        ldg_hcell(g.key_h + (in[u] ? (iz * (g.ny - 1) + iy) * (g.nx - 1) + ix : 0), lo[u], hi[u]);
+        const unsigned cell = static_cast<unsigned>(iz * g.cxy + iy * g.cx + ix);
+        ldg_hcell(g.key_h + (in[u] ? cell : 0u), lo[u], hi[u]);
       }
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
@@ -488,15 +489,10 @@ static __device__ __forceinline__ float eval_key(const PocketDev& pk, const floa
         } else {
           term = off_grid_term(gx[u], gy[u], gz[u]);
         }
-        if (kU == 1 || i0 + u < N) {
-          if ((kU == 1 ? i0 : u) & 1)
-            ko = ko + term;
-          else
-            ke = ke + term;
-        }
+        if (kU == 1 || i0 + u < N) k = k + term;
       }
     }
-    return ke + ko;
+    return k;
   }
   float fe = 0.0f, fo = 0.0f, we = 0.0f, wo = 0.0f;
 #pragma unroll 1

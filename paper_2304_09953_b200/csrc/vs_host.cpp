@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstring>
 #include <exception>
+#include <mutex>
 #include <numeric>
 #include <string>
 #include <thread>
@@ -291,30 +292,80 @@ int vs_corpus_select(uint64_t seed, int64_t n_want, int32_t atom_lo, int32_t ato
 int vs_flexible_select(uint64_t seed, int32_t n_want, int32_t atom_lo, int32_t atom_hi,
                        int32_t tors_lo, int32_t tors_hi, int64_t max_scan, int64_t* first,
                        int32_t* count) {
-  int found = 0;
-  int64_t i = 0;
-  while (found < n_want && i < max_scan) {
-    const int64_t start = i;
-    std::string s;
-    int na = 0, nt = 0;
-    bool ok = true;
-    while (na < atom_lo) {
-      s += random_smiles(seed, static_cast<uint64_t>(i++));
+  // The corpus index space is cut into fixed chunks of kChunk entries; each
+  // chunk is scanned on its own from its first entry (a candidate may read
+  // past the chunk end), so the selection is independent of the thread
+  // count.  Within a chunk: entries are appended while the summed per-entry
+  // heavy-atom count is < atom_lo (an entry that does not parse rejects the
+  // candidate, the next one starts after it); the concatenation is parsed
+  // once, and kept when its atoms and torsion axes fall inside the bounds.
+  constexpr int64_t kChunk = 16384;
+  const int64_t n_chunks = (max_scan + kChunk - 1) / kChunk;
+  if (n_want <= 0 || n_chunks <= 0) return 0;
+  std::vector<std::vector<std::pair<int64_t, int32_t>>> got(static_cast<std::size_t>(n_chunks));
+  std::vector<char> done(static_cast<std::size_t>(n_chunks), 0);
+  std::atomic<int64_t> next{0};
+  std::atomic<bool> enough{false};
+  std::mutex mu;
+  int64_t prefix = 0, prefix_found = 0;  // completed chunk prefix (under mu)
+  auto scan = [&](int64_t c) {
+    std::vector<std::pair<int64_t, int32_t>> out;
+    const int64_t end = std::min(max_scan, (c + 1) * kChunk);
+    int64_t i = c * kChunk;
+    while (i < end) {
+      const int64_t start = i;
+      std::string s;
+      int na = 0;
+      bool ok = true;
+      while (na < atom_lo && i < max_scan) {
+        const std::string e = random_smiles(seed, static_cast<uint64_t>(i++));
+        try {
+          na += static_cast<int>(parse_smiles(e).elements.size());
+        } catch (const std::exception&) {
+          ok = false;
+          break;
+        }
+        s += e;
+      }
+      if (!ok || na < atom_lo || na > atom_hi) continue;
       try {
         const Graph g = parse_smiles(s);
-        na = static_cast<int>(g.elements.size());
-        if (na >= atom_lo) nt = static_cast<int>(torsion_axes(g).axes.size());
+        const int n2 = static_cast<int>(g.elements.size());
+        const int nt = static_cast<int>(torsion_axes(g).axes.size());
+        if (n2 >= atom_lo && n2 <= atom_hi && nt >= tors_lo && nt <= tors_hi)
+          out.emplace_back(start, static_cast<int32_t>(i - start));
       } catch (const std::exception&) {
-        ok = false;
-        break;
       }
     }
-    if (ok && na <= atom_hi && nt >= tors_lo && nt <= tors_hi) {
-      first[found] = start;
-      count[found] = static_cast<int32_t>(i - start);
+    std::lock_guard<std::mutex> lk(mu);
+    got[static_cast<std::size_t>(c)] = std::move(out);
+    done[static_cast<std::size_t>(c)] = 1;
+    while (prefix < n_chunks && done[static_cast<std::size_t>(prefix)]) {
+      prefix_found += static_cast<int64_t>(got[static_cast<std::size_t>(prefix)].size());
+      ++prefix;
+    }
+    if (prefix_found >= n_want) enough = true;
+  };
+  auto work = [&] {
+    while (!enough) {
+      const int64_t c = next.fetch_add(1);
+      if (c >= n_chunks) break;
+      scan(c);
+    }
+  };
+  const int nt = std::max(1, std::min<int>(static_cast<int>(std::thread::hardware_concurrency()),
+                                           static_cast<int>(std::min<int64_t>(n_chunks, 256))));
+  std::vector<std::thread> pool;
+  for (int t = 0; t < nt; ++t) pool.emplace_back(work);
+  for (auto& th : pool) th.join();
+  int found = 0;
+  for (int64_t c = 0; c < prefix && found < n_want; ++c)
+    for (const auto& fc : got[static_cast<std::size_t>(c)]) {
+      if (found >= n_want) break;
+      first[found] = fc.first;
+      count[found] = fc.second;
       ++found;
     }
-  }
   return found;
 }
 

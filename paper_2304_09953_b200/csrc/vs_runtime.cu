@@ -205,6 +205,8 @@ struct vs_handle {
   std::vector<int> pkind;        // kernel kind of each pair (0 start .. 3 finish)
   bool timed = false;
   bool staged_run = false;
+  double rescore_ms = -1.0;  // device time of the rescore kernels of the last vs_rescore
+  cudaEvent_t rev0 = nullptr, rev1 = nullptr;
 };
 
 namespace {
@@ -520,6 +522,8 @@ void vs_destroy(vs_handle* h) {
   cudaEventDestroy(h->ev0);
   cudaEventDestroy(h->ev1);
   for (cudaEvent_t e : h->pev) cudaEventDestroy(e);
+  if (h->rev0) cudaEventDestroy(h->rev0);
+  if (h->rev1) cudaEventDestroy(h->rev1);
   cudaStreamDestroy(h->own);
   delete h;
 }
@@ -607,6 +611,8 @@ int vs_set_pocket(vs_handle* h, const vs_pocket* p, double spacing, double pad) 
     int* dims[3] = {&g.nx, &g.ny, &g.nz};
     for (int c = 0; c < 3; ++c)
       *dims[c] = static_cast<int>(std::ceil((p->hi[c] - p->lo[c] + 2.0 * pad) / spacing)) + 1;
+    g.cx = g.nx - 1;
+    g.cxy = (g.nx - 1) * (g.ny - 1);
     const size_t nodes = static_cast<size_t>(g.nx) * g.ny * g.nz;
     const size_t cells = static_cast<size_t>(g.nx - 1) * (g.ny - 1) * (g.nz - 1);
     // cell arrays 256 B aligned: each 32 B cell is one 256-bit load (ldg_cell)
@@ -817,6 +823,8 @@ double vs_last_dock_ms(const vs_handle* h) {
 }
 
 uint64_t vs_launch_count(const vs_handle* h) { return h->launches; }
+
+double vs_last_rescore_ms(const vs_handle* h) { return h->rescore_ms; }
 
 int vs_last_phase_ms(vs_handle* h, double out[4]) {
   if (!h->timed) return fail(h, VS_ERR_STATE, "no dock has run");
@@ -1116,6 +1124,11 @@ int vs_rescore(vs_handle* h, const vs_library* L, int64_t n_poses, const int32_t
   }
   const bool grid = h->pk.grid_mode != 0;
   const LibDev ld = P.dev();
+  if (!h->rev0) {
+    VS_CUDA(h, cudaEventCreate(&h->rev0));
+    VS_CUDA(h, cudaEventCreate(&h->rev1));
+  }
+  h->rescore_ms = 0.0;
   // one launch per size bucket with bucket-local, LPT-ordered pose lists
   for (const Bucket& b : P.buckets) {
     std::vector<int> rl, ro, orig;
@@ -1158,14 +1171,21 @@ int vs_rescore(vs_handle* h, const vs_library* L, int64_t n_poses, const int32_t
     const int count = static_cast<int>(rl.size());
     const size_t smem = rescore_smem_per_block(b.nmax, b.tmax, b.mvmax);
     const int blocks = std::max(1, std::min((count + kWarpsPerBlock - 1) / kWarpsPerBlock, 4 * h->sms));
+    VS_CUDA(h, cudaEventRecord(h->rev0, st));
     VS_CUDA(h, launch_rescore(grid, blocks, smem, st, ld, h->pk, a.as<int>(), count, cc.as<int>(),
                               bo.as<int>(), c.as<long>(), d.as<float4>(), e.as<float4>(),
                               f.as<float>(), b.nmax, b.tmax, b.mvmax, g.as<float>(), gr.as<float>()));
+    VS_CUDA(h, cudaEventRecord(h->rev1, st));
     ++h->launches;
     std::vector<float> og(orig.size()), orr(orig.size());
     VS_CUDA(h, cudaMemcpyAsync(og.data(), g.p, og.size() * 4, cudaMemcpyDeviceToHost, st));
     VS_CUDA(h, cudaMemcpyAsync(orr.data(), gr.p, orr.size() * 4, cudaMemcpyDeviceToHost, st));
     VS_CUDA(h, cudaStreamSynchronize(st));
+    {
+      float ms = 0.0f;
+      VS_CUDA(h, cudaEventElapsedTime(&ms, h->rev0, h->rev1));
+      h->rescore_ms += ms;
+    }
     for (size_t k = 0; k < orig.size(); ++k) {
       if (geo) geo[orig[k]] = og[k];
       if (resc) resc[orig[k]] = orr[k];

@@ -29,6 +29,7 @@ struct GridDev {
   float ox, oy, oz;  // node (0,0,0) position
   float h, inv_h;
   int nx, ny, nz;
+  int cx, cxy;          // cell strides: nx - 1, (nx - 1)(ny - 1)
   const float* steric;  // node values, x fastest
   const float* hbond;
   const float* lipo;

@@ -330,6 +330,10 @@ class Engine:
     def last_dock_ms(self) -> float:
         return float(_lib.vs_last_dock_ms(self._h))
 
+    def last_rescore_ms(self) -> float:
+        """Device ms of the rescore kernels of the last rescore() call."""
+        return float(_lib.vs_last_rescore_ms(self._h))
+
     def launch_count(self) -> int:
         return int(_lib.vs_launch_count(self._h))
 
