@@ -194,7 +194,7 @@ __device__ __forceinline__ float wall_term(const PocketDev& pk, float x, float y
 __device__ __forceinline__ float pair_term_d(const PocketDev& pk, double dx, double dy,
                                              double dz) {
   const double d2 = det_norm2_d(dx, dy, dz);
-  if (d2 > static_cast<double>(c_pk.cut2)) return 0.0f;
+  if (d2 > c_pk.cut2_d) return 0.0f;
   return det_softplus((c_pk.r - sqrtf(static_cast<float>(d2))) * 10.0f);
 }
 // clash softplus of a pair inside the cutoff, from its FP64 squared distance
@@ -205,7 +205,7 @@ __device__ __forceinline__ float pair_soft(double d2) {
 __device__ __forceinline__ float pair_term_d(const PocketDev& pk, double dx, double dy, double dz,
                                              int& n_active) {
   const double d2 = det_norm2_d(dx, dy, dz);
-  if (d2 > static_cast<double>(c_pk.cut2)) return 0.0f;
+  if (d2 > c_pk.cut2_d) return 0.0f;
   ++n_active;
   return pair_soft(d2);
 }

@@ -287,7 +287,7 @@ static __device__ VS_PHASE int sweep_phase(const PocketDev& pk, const Dims d,
 // + moved part(candidate: moving_j atoms rotated about the state's axis j
 // and their cross pairs; lane pair (a, h), lane h takes moving positions
 // = h mod 2).  Returns the score of the final state.
-template <int kGrid>
+template <int kGrid, bool kPacked = false>
 static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, int N, int T,
                                                 int F, int A, float step, const PoseF* P,
                                                 int lane, unsigned long long* n_active,
@@ -349,6 +349,20 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
         }
       }
     }
+    // kPacked: the partners of this step (atoms outside moving_j, ascending)
+    // packed into the conformer's region, which the staged flex kernel no
+    // longer reads; the candidate loop then walks a plain list
+    int np = 0;
+    if (kPacked && do_flex) {  // (np stays 0 otherwise)
+      for (int i0 = 0; i0 < N; i0 += 32) {
+        const int i = i0 + lane;
+        const bool pt = i < N && !in_mask(mk, i);
+        const unsigned bal = __ballot_sync(kFull, pt);
+        if (pt) s.y0[np + __popc(bal & ((1u << lane) - 1u))] = s.ys[i];
+        np += __popc(bal);
+      }
+      __syncwarp();
+    }
     fb = warp_sum(fb);
     wb = warp_sum(wb);
     pb = warp_sum(pb);
@@ -382,20 +396,32 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
         atom_terms_s<kGrid>(s.pose, yx, yy, yz, &fi, &wi);
         fm = fm + fi;
         wm = wm + wi;
-        for (int wd = 0; wd < W; ++wd) {
-          unsigned b2 = ~mk[wd];
-          if (wd == W - 1 && (N & 31)) b2 &= (1u << (N & 31)) - 1u;
-          if (!b2) continue;
-          // the next partner's coordinates are loaded before this pair's
-          // test (shared-memory latency off the dependent chain)
-          const double4* yw = s.ys + wd * 32;
-          double4 yk = yw[__ffs(b2) - 1];
-          while (true) {
-            b2 &= b2 - 1u;
-            const double4 yn = yw[b2 ? __ffs(b2) - 1 : 0];
+        if constexpr (kPacked) {
+          // next partner loaded before this pair's test; part[np] (np < N:
+          // moving_j holds b_j) is in the buffer and unused
+          const double4* part = s.y0;
+          double4 yk = part[0];
+          for (int p = 0; p < np; ++p) {
+            const double4 yn = part[p + 1];
             pc = pc + pair_term_d(pk, yx - yk.x, yy - yk.y, yz - yk.z, nact);
-            if (!b2) break;
             yk = yn;
+          }
+        } else {
+          for (int wd = 0; wd < W; ++wd) {
+            unsigned b2 = ~mk[wd];
+            if (wd == W - 1 && (N & 31)) b2 &= (1u << (N & 31)) - 1u;
+            if (!b2) continue;
+            // the next partner's coordinates are loaded before this pair's
+            // test (shared-memory latency off the dependent chain)
+            const double4* yw = s.ys + wd * 32;
+            double4 yk = yw[__ffs(b2) - 1];
+            while (true) {
+              b2 &= b2 - 1u;
+              const double4 yn = yw[b2 ? __ffs(b2) - 1 : 0];
+              pc = pc + pair_term_d(pk, yx - yk.x, yy - yk.y, yz - yk.z, nact);
+              if (!b2) break;
+              yk = yn;
+            }
           }
         }
       }
@@ -852,7 +878,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_FLEX)
     P.q[3] = pq.w;
     __syncwarp();
     unsigned long long nact = 0;
-    float S = flex_phase<kGrid>(pk, d, N, T, prm.F, prm.A, step, &P, lane, &nact, prm.polish);
+    float S = flex_phase<kGrid, true>(pk, d, N, T, prm.F, prm.A, step, &P, lane, &nact,
+                                      prm.polish);
 #ifndef VS_FUSED_POLISH
     if (prm.polish >= 1) {
       // the polish + keep run in vs_polish_kernel: hand over the flexed state

@@ -595,6 +595,7 @@ int vs_set_pocket(vs_handle* h, const vs_pocket* p, double spacing, double pad) 
   pk.lam = static_cast<float>(p->clash_penalty);
   const float rr = pk.r + 3.0f;
   pk.cut2 = rr * rr;
+  pk.cut2_d = static_cast<double>(pk.cut2);
   pk.n_steric = counts[0];
   pk.n_hbond = counts[1];
   pk.n_lipo = counts[2];

@@ -50,6 +50,7 @@ struct PocketDev {
   float r;                  // clash_radius
   float lam;                // clash_penalty
   float cut2;               // (r + 3)^2: pair skip threshold (z < -30)
+  double cut2_d;            // the same threshold widened to FP64 (pair tests compare in FP64)
   int n_steric, n_hbond, n_lipo;
   const SiteF* sites;       // [steric | hbond | lipo], pocket order within kind
   int grid_mode;            // 0 analytic field, 1 grid maps
