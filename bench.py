@@ -253,15 +253,15 @@ def algorithmic_work(lib, prm, stats, grid: bool, n_steric: int):
                                               np.minimum(to[:-1], len(m))) * (T > 0))) * R
     atom_f = ATOM_FLOP_KEY if grid else 31 + 11 * n_steric
     atom_x = ATOM_XU_KEY if grid else 2 * n_steric
-    # translation lattice (27 lanes) or, with polish, the rigid compass (25 lanes)
-    lanes = 25.0 if getattr(prm, "polish", 0) >= 1 else 27.0
+    # translation lattice (27 lanes) or, with polish, the rigid compass (31 lanes)
+    lanes = 31.0 if getattr(prm, "polish", 0) >= 1 else 27.0
     pose_atoms = float(np.sum(R * K * N)) + lanes * stats["translation_iter_atoms"]
     sweep_flop = pose_atoms * atom_f + R * K * len(lib) * POSE_ROT_FLOP
     sweep_xu = pose_atoms * atom_x + R * K * len(lib) * POSE_ROT_XU
     if getattr(prm, "polish", 0) >= 1:
-        # post-flex compass (25 lanes per iteration) + the final score of each
+        # post-flex compass (31 lanes per iteration) + the final score of each
         # restart's pose (atom terms + every pair tested) run in the flex kernel
-        post_atoms = 25.0 * stats.get("post_compass_iter_atoms", 0)
+        post_atoms = 31.0 * stats.get("post_compass_iter_atoms", 0)
         flex_flop += post_atoms * atom_f + float(np.sum(R * (N * TERMS_FLOP + PAIR_TEST_FLOP * P)))
         flex_xu += post_atoms * atom_x + R * float(np.sum(N)) * TERMS_XU
     return {"sweep": (sweep_flop, sweep_xu), "flex": (flex_flop, flex_xu),

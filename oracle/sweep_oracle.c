@@ -566,7 +566,8 @@ static uint32_t orderable(float f) {
 #define POLISH_SC0 0.5f         /* A */
 #define POLISH_ANG_MIN 0.015625f
 #define POLISH_ANG_MAX 0.5625f  /* expansion cap */
-#define POLISH_ITERS 24
+#define POLISH_ITERS 8
+#define COMPASS_CANDS 31
 
 #define TRANS_ITERS 16
 #define TRANS_MIN (1.0f / 64.0f)
@@ -581,10 +582,11 @@ static void trans_offset(int l, float sc, float* o) {
 
 /* polish rigid compass (SWEEP_V1.md §3.5).  Candidates: l = 0 keeps the
  * pose; l = 1..6 rotate by +-ang about world x, y, z through the posed
- * centroid; l = 7..12 translate by +-sc along x, y, z; l = 13..24 are the
- * same moves at twice the step.  The argmax of the sweep key (ties to the
- * lowest l) is taken: l = 0 halves ang and sc; a twice-step winner doubles
- * them while ang < POLISH_ANG_MAX.  Returns the iterations run. */
+ * centroid; l = 7..12 translate by +-sc along x, y, z; l = 13..18 rotate by
+ * +-3 ang, l = 19..24 translate by +-2 sc, l = 25..30 translate by +-12 sc.
+ * The argmax of the sweep key (ties to the lowest l) is taken: l = 0 halves
+ * ang and sc; a winner l >= 13 doubles them while ang < POLISH_ANG_MAX.
+ * Returns the iterations run. */
 static int rigid_compass(const vso_pocket* p, const lig_t* L, const float* ysf, const float* c,
                          float* pq, float* pt) {
   const float zero[3] = {0.0f, 0.0f, 0.0f};
@@ -596,9 +598,11 @@ static int rigid_compass(const vso_pocket* p, const lig_t* L, const float* ysf, 
     apply(&R0, c, pt, Cw);
     float bk = -INFINITY, bq[4], bt[3];
     int bl = 0;
-    for (int l = 0; l < 25; ++l) {
-      const int big = l >= 13, lm = big ? l - 12 : l;
-      const float a2 = big ? 2.0f * ang : ang, s2 = big ? 2.0f * sc : sc;
+    for (int l = 0; l < COMPASS_CANDS; ++l) {
+      const int big = l >= 13, huge = l >= 25;
+      const int lm = huge ? l - 18 : (big ? l - 12 : l);
+      const float a2 = big ? 3.0f * ang : ang;
+      const float s2 = huge ? 12.0f * sc : (big ? 2.0f * sc : sc);
       float q2[4] = {pq[0], pq[1], pq[2], pq[3]}, t2[3] = {pt[0], pt[1], pt[2]};
       mat3 R2 = R0;
       if (lm >= 1 && lm <= 6) {

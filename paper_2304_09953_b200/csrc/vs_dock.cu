@@ -79,16 +79,18 @@ static __device__ VS_PHASE int start_phase(const PocketDev& pk, const Dims d,
 #endif
 
 // ---- rigid compass of the polish (SWEEP_V1.md §3.5), on the FP32 state
-// copy with the sweep key.  Lane l < 25 is candidate l: 0 keeps the pose;
+// copy with the sweep key.  Lane l < 31 is candidate l: 0 keeps the pose;
 // 1..6 rotate by +-ang about world x y z through the posed centroid (cx, cy,
-// cz); 7..12 translate by +-sc along x y z; 13..24 the same at twice the
-// step.  Argmax, ties to the lowest lane; l = 0 halves the steps, a
-// twice-step winner doubles them while ang < kPolishAngMax.
+// cz); 7..12 translate by +-sc along x y z; 13..18 rotate by +-3 ang,
+// 19..24 translate by +-2 sc; 25..30 translate by +-12 sc.  Argmax, ties to
+// the lowest lane; l = 0 halves the steps, a winner l >= 13 doubles them
+// while ang < kPolishAngMax.  At most kPolishIters iterations.
 constexpr float kPolishAng0 = 0.28125f;
 constexpr float kPolishSc0 = 0.5f;
 constexpr float kPolishAngMin = 0.015625f;
 constexpr float kPolishAngMax = 0.5625f;
-constexpr int kPolishIters = 24;
+constexpr int kPolishIters = 8;
+constexpr int kCompassLanes = 31;
 
 template <int kGrid, bool kInl>
 static __device__ __forceinline__ int rigid_compass(const PocketDev& pk, const float4* ysf, int N,
@@ -104,10 +106,12 @@ static __device__ __forceinline__ int rigid_compass(const PocketDev& pk, const f
     det_apply(R0, cx, cy, cz, tx, ty, tz, &Cx, &Cy, &Cz);
     float w2 = qw, x2 = qx, y2 = qy, z2 = qz, u2 = tx, v2 = ty, s2 = tz;
     float key = -INFINITY;
-    if (lane < 25) {
+    if (lane < kCompassLanes) {
       const bool big = lane >= 13;
-      const int lm = big ? lane - 12 : lane;
-      const float a2 = big ? 2.0f * ang : ang, sc2 = big ? 2.0f * sc : sc;
+      const bool huge = lane >= 25;
+      const int lm = huge ? lane - 18 : (big ? lane - 12 : lane);
+      const float a2 = big ? 3.0f * ang : ang;
+      const float sc2 = huge ? 12.0f * sc : (big ? 2.0f * sc : sc);
       Mat3 R2 = R0;
       if (lm >= 1 && lm <= 6) {
         const int ax = (lm - 1) >> 1;
@@ -133,7 +137,7 @@ static __device__ __forceinline__ int rigid_compass(const PocketDev& pk, const f
       key = kInl ? eval_key<kGrid, 1>(pk, ysf, N, R2, u2, v2, s2)
                  : eval_rigid<kGrid>(pk, ysf, N, R2, u2, v2, s2);
     }
-    int li = lane < 25 ? lane : 0x7fffffff;
+    int li = lane < kCompassLanes ? lane : 0x7fffffff;
     for (int off = 16; off > 0; off >>= 1) {
       const float ok = __shfl_xor_sync(kFull, key, off);
       const int oi = __shfl_xor_sync(kFull, li, off);

@@ -4,7 +4,11 @@ per ligand, the best survivor rescore of our GPU dock (each survivor pose
 re-scored by the reference's FP64 rescore, so grid mode is judged by the
 analytic score too) vs the reference's dock() + rescore + filter_poses.
 
-  python tools/quality_vs_reference.py [n_ligands] [threads] [--grid]
+  python tools/quality_vs_reference.py [n_ligands] [threads] [--grid] [--ref-only]
+
+The reference arm's per-ligand results are cached in
+tests/golden/quality_ref_<n>.json (the reference's own dock() output on
+these inputs; --ref-only computes and writes it without a GPU).
 
 Prints one JSON line: mean / median of (ours - reference) best rescore, the
 fraction of ligands where ours >= reference, and both wall times."""
@@ -17,6 +21,35 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+
+
+def ref_lig(R, lib, i):
+    import bench
+    from paper_2304_09953_b200.chem import random_smiles
+    ao, _, _ = lib.offsets()
+    lg = R.RefLigand(random_smiles(bench.CORPUS_SEED, int(lib.ids[i][1:])), iterations=-1)
+    lg.set_coords(lib.coords[ao[i]:ao[i + 1]])
+    return lg
+
+
+def ref_arm(lib, pocket, prm, threads, cache):
+    """The reference's dock() + rescore + filter_poses + best on these
+    ligands (same conformer bytes and seeds), written to `cache`."""
+    import paper_2304_09953_b200 as V
+    from oracle import ref as R
+    rp = R.RefPocket(V.pocket_to_json(pocket))
+    ligs = [ref_lig(R, lib, i) for i in range(len(lib))]
+    t0 = time.perf_counter()
+    kept, best = R.dock_best_many(ligs, rp, prm.restarts, prm.diversity_delta,
+                                  [int(s) for s in lib.seeds], 500, prm.keep_top, prm.min_score,
+                                  threads)
+    t_ref = time.perf_counter() - t0
+    with open(cache, "w") as f:
+        json.dump({"ids": list(lib.ids), "best": [float(b) if k > 0 else None
+                                                 for k, b in zip(kept, best)],
+                   "ref_s": round(t_ref, 2), "threads": threads,
+                   "knobs": "bench.params(): R=30, delta 1.0, keep_top 4, min_score -5, "
+                            "ls_max_steps 500; bench.make_pocket() analytic"}, f)
 
 
 def main():
@@ -34,6 +67,15 @@ def main():
     lib.seeds = lib_all.seeds[sel]
     pocket = bench.make_pocket()
     prm = bench.params()
+    cache = os.path.join(ROOT, "tests", "golden", f"quality_ref_{n}.json")
+    if "--ref-only" in sys.argv or not os.path.exists(cache):
+        ref_arm(lib, pocket, prm, threads, cache)
+        if "--ref-only" in sys.argv:
+            return
+    with open(cache) as f:
+        c = json.load(f)
+    assert c["ids"] == list(lib.ids), "reference cache is for other ligands"
+    ref = np.array([np.nan if v is None else v for v in c["best"]], np.float64)
     eng = V.Engine(0)
     eng.set_pocket(pocket, grid_spacing=0.4 if grid else 0.0, grid_pad=2.0)
     t0 = time.perf_counter()
@@ -44,23 +86,14 @@ def main():
     # the reference arm: same conformer bytes, same dock seeds, its own ascent
     rp = R.RefPocket(V.pocket_to_json(pocket))
     ao, _, _ = lib.offsets()
-    ligs = []
-    for i in range(len(lib)):
-        lg = R.RefLigand(random_smiles(bench.CORPUS_SEED, int(lib.ids[i][1:])), iterations=-1)
-        lg.set_coords(lib.coords[ao[i]:ao[i + 1]])
-        ligs.append(lg)
+    ligs = [ref_lig(R, lib, i) for i in range(len(lib))]
     for i in range(len(lib)):
         vals = [ligs[i].rescore(rp, np.array(p.translation, np.float64),
                                 np.array(p.rotation, np.float64), np.array(p.torsions, np.float64))
                 for p in res.poses(i, int(lib.n_tors[i]), "surv")]
         if vals:
             ours_ref_scored[i] = max(vals)
-    t0 = time.perf_counter()
-    kept, best = R.dock_best_many(ligs, rp, prm.restarts, prm.diversity_delta,
-                                  [int(s) for s in lib.seeds], 500, prm.keep_top, prm.min_score,
-                                  threads)
-    t_ref = time.perf_counter() - t0
-    ref = np.where(kept > 0, best, np.nan)
+    t_ref = c["ref_s"]
     both = ~np.isnan(ours_ref_scored) & ~np.isnan(ref)
     d = ours_ref_scored[both] - ref[both]  # both sides scored by the reference's FP64 rescore
     out = {"ligands": len(lib), "compared": int(both.sum()), "grid": grid,
