@@ -205,6 +205,8 @@ struct vs_handle {
   std::vector<int> pkind;        // kernel kind of each pair (0 start .. 3 finish)
   bool timed = false;
   bool staged_run = false;
+  Packed rpack;              // vs_rescore's library staging, reused across calls
+  DBuf rbuf[9];              // vs_rescore's per-bucket pose arrays, reused across calls
   double rescore_ms = -1.0;  // device time of the rescore kernels of the last vs_rescore
   cudaEvent_t rev0 = nullptr, rev1 = nullptr;
 };
@@ -513,6 +515,8 @@ void vs_destroy(vs_handle* h) {
   cudaSetDevice(h->device);
   cudaStreamSynchronize(h->own);
   h->lib.release();
+  h->rpack.release();
+  for (DBuf& b : h->rbuf) b.release();
   for (DBuf* b : {&h->d_sites, &h->d_sites64, &h->d_maps, &h->d_surv, &h->d_surv_tors, &h->d_all, &h->d_all_tors,
                   &h->d_best, &h->d_nkept, &h->d_nsurv, &h->d_keys, &h->d_counters, &h->d_sx,
                   &h->d_sp, &h->d_sm, &h->d_rots, &h->d_topk_a, &h->d_topk_b, &h->d_stats,
@@ -1100,7 +1104,7 @@ int vs_rescore(vs_handle* h, const vs_library* L, int64_t n_poses, const int32_t
   for (int64_t p = 1; p < n_poses; ++p)
     if (pose_lig[p] < pose_lig[p - 1])
       return fail(h, VS_ERR_INVALID_ARGUMENT, "pose_lig must be non-decreasing");
-  Packed P;
+  Packed& P = h->rpack;
   int rc = pack_library(h, L, nullptr, 0, P);
   if (rc) return rc;
   for (int64_t p = 0; p < n_poses; ++p)
@@ -1153,7 +1157,8 @@ int vs_rescore(vs_handle* h, const vs_library* L, int64_t n_poses, const int32_t
     if (rl.empty()) continue;
     ro.push_back(static_cast<int>(orig.size()));
     if (rtors.empty()) rtors.push_back(0.0f);
-    DBuf a, bo, c, d, e, f, g, gr, cc;
+    DBuf &a = h->rbuf[0], &bo = h->rbuf[1], &c = h->rbuf[2], &d = h->rbuf[3], &e = h->rbuf[4],
+         &f = h->rbuf[5], &g = h->rbuf[6], &gr = h->rbuf[7], &cc = h->rbuf[8];
     auto up = [&](DBuf& dst, const void* src, size_t bytes) -> cudaError_t {
       cudaError_t err = dst.ensure(bytes);
       if (err != cudaSuccess) return err;
@@ -1191,9 +1196,7 @@ int vs_rescore(vs_handle* h, const vs_library* L, int64_t n_poses, const int32_t
       if (geo) geo[orig[k]] = og[k];
       if (resc) resc[orig[k]] = orr[k];
     }
-    for (DBuf* x : {&a, &bo, &c, &d, &e, &f, &g, &gr, &cc}) x->release();
   }
-  P.release();
   return VS_OK;
 }
 
