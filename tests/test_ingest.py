@@ -82,3 +82,29 @@ def test_read_library_records(V, tmp_path):
 def test_aromatic_atoms_count_as_carbon(V):
     lig = V.make_ligand("b", "c1ccccc1O")
     assert list(lig.atom_classes()) == [1] * 6 + [2]
+
+
+def test_flexible_selection_deterministic_and_in_bounds(V):
+    """C4 population (capi.h vs_flexible_select): chunked parallel scan, so the
+    selection must not depend on scheduling; every pick is a concatenation of
+    consecutive corpus entries inside the atom / torsion-axis bounds."""
+    from paper_2304_09953_b200.chem import flexible_smiles, random_smiles
+    a = flexible_smiles(7, 12)
+    b = flexible_smiles(7, 12)
+    assert a == b and len(a) == 12
+    assert flexible_smiles(7, 5) == a[:5]
+    for s in a[:6]:
+        lg = V.make_ligand("f", s, embed_seed=1)
+        assert 60 <= lg.heavy_atoms <= 80
+        assert 15 <= len(lg.topology.axes) <= 20
+    # each pick is random_smiles(7, i) + random_smiles(7, i + 1) + ...
+    assert a[0].startswith(random_smiles(7, 0)) or any(
+        a[0].startswith(random_smiles(7, i)) for i in range(1, 5000))
+
+
+def test_bench_configs_declared():
+    """bench.py --config names the BASELINE.json configs it measures."""
+    import bench
+    assert set(bench.CONFIGS) == {"c2", "c3", "c4", "c5"}
+    assert bench.CONFIGS["c3"]["scaling"] == "strong"
+    assert bench.CONFIGS["c5"]["grid_spacing"] == 0.2
