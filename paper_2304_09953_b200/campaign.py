@@ -1,0 +1,250 @@
+"""The dock funnel of run_campaign on the B200 path.
+
+`run_dock_stages` runs the parse -> embed -> dock -> rescore -> filter -> rank
+stages of `pipeline::run_campaign` (proj/src/pipeline.cpp:380-537) from the
+reference's campaign JSON (`parse_config_json`, pipeline.cpp:76-160), with the
+dock, rescore, filter and best-score stages in one GPU pass and the ranking
+as the device top-k.  What it keeps from the reference, exactly:
+
+- parse: records of `read_library_file`, unparsable lines skipped, duplicate
+  ids rejected (pipeline.cpp:381-416);
+- embed: seed `Rng(seed).split(1).split(i)` over the parsed ligands, the
+  reference `embed_3d` bit for bit (:418-429);
+- dock: ligands outside every size class dropped, the `BatchQueue` replay
+  with its `dock.b{bi}` tasks and their simulated durations (:433-473), dock
+  seed `Rng(seed).split(2).split(i)` over the in-class ligands (:480-484);
+- filter / rank: `filter_poses(keep_top, min_score)`, best = max rescore,
+  ligands without a surviving pose dropped, `rank_ligands` order and
+  keep = min(n, max(1, floor(keep_after_dock * n))) (:502-537);
+- the stage records {name, in, out, sim_seconds, tasks} of the report.
+
+What it does not do: `sim_seconds` of the dock stage is the cluster
+scheduler simulation (`sched::run_simulation`, out of scope here): the
+stage carries the tasks instead so a caller's scheduler can replay them.
+Compressed (.smzc) libraries need the reference codec (out of scope).  The
+pose generator is sweep-v1 (docs/SWEEP_V1.md), so the ranked scores are
+sweep-v1's, not the gradient ascent's.
+"""
+from __future__ import annotations
+
+import json
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .batcher import DeviceModel, SizeClass, bucket_replay, default_classes
+from .chem import build_library, read_library_file
+from .dock import DockParams, Engine, load_pocket_file
+from .errors import VscreenError
+from .pipeline import RankedLigand, campaign_seeds, keep_count, rank_ligands
+
+
+class ConfigError(VscreenError):
+    """pipeline::ConfigError (pipeline.hpp)."""
+
+
+@dataclass
+class StageKnobs:
+    """pipeline::StageKnobs (pipeline.hpp:33-40)."""
+    embed_iterations: int = 200
+    restarts: int = 4
+    diversity_delta: float = 1.0
+    keep_top: int = 4
+    min_score: float = -1e30
+    ls_max_steps: int = 500
+
+
+@dataclass
+class CampaignConfig:
+    """The dock-funnel fields of pipeline::CampaignConfig (pipeline.hpp:42-65)."""
+    library_path: str = ""
+    dictionary_path: str = ""
+    pocket_path: str = ""
+    keep_after_dock: float = 0.2
+    keep_for_fep: float = 0.5
+    knobs: StageKnobs = field(default_factory=StageKnobs)
+    device: DeviceModel = field(default_factory=DeviceModel)
+    classes: list = field(default_factory=list)
+    master_seed: int = 0
+    threads: int = 1
+    top_n: int = 10
+
+
+@dataclass
+class StageStats:
+    """pipeline::StageStats (pipeline.hpp:71-77)."""
+    name: str
+    in_: int = 0
+    out: int = 0
+    sim_seconds: float | None = 0.0
+    tasks: int = 0
+
+    def to_json(self) -> dict:
+        return {"name": self.name, "in": self.in_, "out": self.out,
+                "sim_seconds": self.sim_seconds, "tasks": self.tasks}
+
+
+@dataclass
+class DockTask:
+    """sched::Task of the dock stage (pipeline.cpp:462-473)."""
+    id: str
+    duration_s: float
+    cls: int
+    ligand_ids: list
+
+
+@dataclass
+class DockFunnel:
+    stages: list
+    ranked: list          # kept RankedLigand, rank order
+    tasks: list           # DockTask per batch
+    ids: list             # docked ligand ids (in-class, post-compaction order)
+    best: np.ndarray      # best rescore per docked ligand (-inf: no surviving pose)
+    dock_ms: float
+
+
+def _resolve(base_dir: str, path: str) -> str:
+    """pipeline.cpp:57-60."""
+    if not path or os.path.isabs(path) or not base_dir:
+        return path
+    return os.path.join(base_dir, path)
+
+
+def parse_config_json(text: str, base_dir: str = "") -> CampaignConfig:
+    """pipeline::parse_config_json (pipeline.cpp:76-160), dock-funnel fields;
+    missing required keys raise ConfigError like the reference."""
+    try:
+        j = json.loads(text)
+    except ValueError as e:
+        raise ConfigError(f"bad campaign JSON: {e}") from e
+    c = CampaignConfig()
+    try:
+        c.library_path = _resolve(base_dir, j["library"])
+        c.dictionary_path = _resolve(base_dir, j.get("dictionary", ""))
+        c.pocket_path = _resolve(base_dir, j["pocket"])
+        c.keep_after_dock = float(j["funnel"]["keep_after_dock"])
+        c.keep_for_fep = float(j["funnel"]["keep_for_fep"])
+        k = j.get("knobs", {})
+        d = StageKnobs()
+        c.knobs = StageKnobs(int(k.get("embed_iterations", d.embed_iterations)),
+                             int(k.get("restarts", d.restarts)),
+                             float(k.get("diversity_delta", d.diversity_delta)),
+                             int(k.get("keep_top", d.keep_top)),
+                             float(k.get("min_score", d.min_score)),
+                             int(k.get("ls_max_steps", d.ls_max_steps)))
+        jd = j["device"]
+        c.device = DeviceModel(float(jd["memory_capacity"]), float(jd.get("mem_fixed", 0.0)),
+                               float(jd["mem_per_atom"]), float(jd["mem_per_rotbond"]),
+                               float(jd["launch_overhead_s"]),
+                               [float(v) for v in jd["service_time_per_class_s"]])
+        if "classes" in j:
+            c.classes = [SizeClass(int(x["atom_lo"]), int(x["atom_hi"]), int(x["rot_lo"]),
+                                   int(x["rot_hi"])) for x in j["classes"]]
+        else:
+            c.classes = default_classes()
+        c.master_seed = int(j.get("seed", 0))
+        c.threads = int(j.get("threads", 1))
+        c.top_n = int(j.get("top_n", 10))
+    except (KeyError, TypeError) as e:
+        raise ConfigError(f"bad campaign config: missing or invalid {e}") from e
+    return c
+
+
+def load_config_file(path: str) -> CampaignConfig:
+    """pipeline::load_config_file (pipeline.cpp:180-188)."""
+    try:
+        with open(path) as f:
+            text = f.read()
+    except OSError as e:
+        raise ConfigError(f"cannot open campaign config: {path}") from e
+    return parse_config_json(text, os.path.dirname(path))
+
+
+def prepare(cfg: CampaignConfig, threads: int | None = None):
+    """parse + embed + the dock stage's class filter and batch replay (no
+    GPU).  Returns (library of in-class ligands with their campaign seeds,
+    stage records so far, dock tasks, dock-stage input count)."""
+    if cfg.library_path.endswith(".smzc"):
+        raise ConfigError("compressed (.smzc) libraries need the reference codec, "
+                          "which is outside the B200 dock path")
+    threads = threads or max(1, cfg.threads)
+    records = read_library_file(cfg.library_path)
+    smiles = [r.smiles for r in records]
+    ids = [r.id for r in records]
+    # parse: graph, descriptors and topology only (no embedding)
+    probe = build_library(smiles, ids, iterations=-1, threads=threads, drop_failed=False)
+    from . import _capi
+    parsed = [i for i in range(len(records)) if probe.status[i] == 0]
+    bad = [i for i in range(len(records))
+           if probe.status[i] not in (0, _capi.VS_ERR_PARSE)]
+    if bad:
+        raise VscreenError(f"ligand {ids[bad[0]]}: graph cannot be embedded "
+                           f"(status {int(probe.status[bad[0]])})")
+    p_ids = [ids[i] for i in parsed]
+    if len(set(p_ids)) != len(p_ids):
+        raise ConfigError("duplicate ligand id in library")
+    stages = [StageStats("parse", len(records), len(parsed), 0.0, 0)]
+    # embed: seeds over the parsed ligands (pipeline.cpp:418-429)
+    n = len(parsed)
+    es = campaign_seeds(cfg.master_seed, n, stage=1)
+    # dock: class filter + batch replay over the parsed ligands (:433-461)
+    atoms = probe.n_atoms[parsed]
+    rot = probe.rot_bonds[parsed]
+    in_range, batches = bucket_replay(atoms, rot, cfg.classes, cfg.device)
+    usable = np.nonzero(in_range)[0]
+    ds = campaign_seeds(cfg.master_seed, len(usable), stage=2)
+    sm = [smiles[parsed[i]] for i in usable]
+    lib = build_library(sm, [p_ids[i] for i in usable], es[usable], ds,
+                        iterations=cfg.knobs.embed_iterations, threads=threads)
+    stages.append(StageStats("embed", n, n, 0.0, 0))
+    tasks = []
+    for bi, (cls, members) in enumerate(batches):
+        tasks.append(DockTask(f"dock.b{bi}",
+                              cfg.device.launch_overhead + len(members) * cfg.device.service_time(cls),
+                              cls, [p_ids[m] for m in members]))
+    return lib, stages, tasks, n
+
+
+def run_dock_stages(cfg: CampaignConfig, engine: Engine | None = None, grid_spacing: float = 0.0,
+                    params: DockParams | None = None) -> DockFunnel:
+    """parse -> embed -> dock -> rescore -> filter -> rank on one GPU.  The
+    pocket is analytic by default (as the reference scores it); grid_spacing
+    > 0 docks on the grid maps."""
+    lib, stages, tasks, n_dock_in = prepare(cfg)
+    pocket = load_pocket_file(cfg.pocket_path)
+    own = engine is None
+    eng = engine or Engine(0)
+    try:
+        eng.set_pocket(pocket, grid_spacing=grid_spacing)
+        k = cfg.knobs
+        prm = params or DockParams(restarts=k.restarts, diversity_delta=k.diversity_delta,
+                                   keep_top=k.keep_top, min_score=k.min_score)
+        res = eng.dock_host(lib, prm, classes=[c.astuple() for c in cfg.classes])
+        dock_ms = eng.last_dock_ms()
+    finally:
+        if own:
+            eng.close()
+    # tasks = batches; sim_seconds needs the scheduler simulation (None here)
+    stages.append(StageStats("dock", n_dock_in, len(lib), None, len(tasks)))
+    stages.append(StageStats("rescore", len(lib), len(lib), 0.0, 0))
+    kept = np.nonzero(res.n_surv > 0)[0]
+    stages.append(StageStats("filter", len(lib), len(kept), 0.0, 0))
+    scores = {lib.ids[i]: float(res.best[i]) for i in kept}
+    ranked = rank_ligands(scores)
+    keep = min(keep_count(len(kept), cfg.keep_after_dock), len(ranked))
+    stages.append(StageStats("rank", len(kept), keep, 0.0, 0))
+    return DockFunnel(stages, [RankedLigand(i, s) for i, s in ranked[:keep]], tasks,
+                      list(lib.ids), res.best, dock_ms)
+
+
+def funnel_to_json(f: DockFunnel) -> str:
+    """The stage records and ranked ligands in the report's field names
+    (CampaignReport::to_json, pipeline.cpp:269-301)."""
+    return json.dumps({"stages": [s.to_json() for s in f.stages],
+                       "ranked": [{"id": r.id, "score": r.score, "delta_g": r.delta_g}
+                                  for r in f.ranked]})
+
+
+__all__ = ["CampaignConfig", "ConfigError", "DockFunnel", "DockTask", "StageKnobs", "StageStats",
+           "funnel_to_json", "load_config_file", "parse_config_json", "prepare", "run_dock_stages"]

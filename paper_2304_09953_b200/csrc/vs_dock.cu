@@ -755,6 +755,9 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t by
 #ifndef VS_MINB_SWEEP
 #define VS_MINB_SWEEP 8
 #endif
+#ifndef VS_MINB_POLISH
+#define VS_MINB_POLISH 8
+#endif
 #ifndef VS_MINB_FLEX
 #define VS_MINB_FLEX 8
 #endif
@@ -922,7 +925,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_FLEX)
 // small shared-memory footprint (no conformer / topology) and a large L1 for
 // its key-map lookups.
 template <int kGrid>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, 8)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_POLISH)
     vs_polish_kernel(const __grid_constant__ LibDev lib, const __grid_constant__ DockParams prm,
                      const int* __restrict__ order, int n_order, int* __restrict__ counter,
                      int nmax, int tmax, int r, const __grid_constant__ StageBufs sb) {
@@ -1086,7 +1089,7 @@ static cudaError_t staged_impl(int sms, cudaStream_t st, const LibDev& lib, cons
   const size_t sm_pol = kWarpsPerBlock * warp_smem_bytes(nmax, tmax, 0,
                                                          kLayState | kLayPosed | kLayFlex |
                                                              kLaySweep);
-  const int b_pol = stage_blocks(vs_polish_kernel<kGrid>, sm_pol, sms, n, 8);
+  const int b_pol = stage_blocks(vs_polish_kernel<kGrid>, sm_pol, sms, n, VS_MINB_POLISH);
   const int T = kWarpsPerBlock * 32;
   int c = 0;
   auto mark = [&](int kind, bool after) {  // event pair c: launch c (counter c)
