@@ -761,6 +761,7 @@ static void dock_one(const vso_pocket* p, const lig_t* L, uint64_t seed, uint32_
     const int do_flex = T > 0 && prm->flex_passes > 0;
     const int steps0 = do_flex ? prm->flex_passes * T : 1;
     const int steps = steps0 + ((do_flex && prm->polish >= 2) ? T : 0);
+    int quiet = 0; /* consecutive coarse steps without a move */
     for (int st = 0; st < steps; ++st) {
       const int fine = st >= steps0; /* polish 2: one pass of fine angles (§3.5) */
       const int j = do_flex ? st % T : -1;
@@ -825,6 +826,13 @@ static void dock_one(const vso_pocket* p, const lig_t* L, uint64_t seed, uint32_
           atom_terms(p, &RS, ptd, &y[3 * idx], &fa[idx], &wa[idx], NULL);
         }
         th[j] = best_th;
+      }
+      /* T coarse steps without a move: a fixed point; the remaining coarse
+       * steps would keep it.  Skip to the last coarse step (its S is the
+       * flex score without the polish) or, with the polish, past it. */
+      if (do_flex && st < steps0) {
+        quiet = best_a != 0 ? 0 : quiet + 1;
+        if (quiet >= T && st < steps0 - 2) st = prm->polish >= 1 ? steps0 - 1 : steps0 - 2;
       }
     }
     if (prm->polish >= 1) { /* §3.5: rigid compass on the flexed state, then S re-scored */

@@ -318,6 +318,7 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
   // polish 2: one more pass over the torsions with fine candidate angles
   const int steps = steps0 + ((do_flex && polish >= 2) ? T : 0);
   const int W = (N + 31) >> 5;
+  int quiet = 0;  // consecutive coarse steps without a move
   float S_cur = 0.0f;
   int nact = 0;  // pair softplus evaluations of this lane (work counter)
   for (int st = 0; st < steps; ++st) {
@@ -459,6 +460,14 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
         atom_terms_s<kGrid>(s.pose, v.x, v.y, v.z, &s.fa[idx], &s.wa[idx]);
       }
       if (lane == 0) s.theta[j] = th_win;
+    }
+    // T coarse steps in a row without a move: every torsion is at its argmax
+    // for the current state, so the remaining coarse steps would evaluate the
+    // same states and keep them.  Skip to the last coarse step (its S is the
+    // flex score when polish is 0) or, with the polish, past it.
+    if (do_flex && st < steps0) {
+      quiet = ai != 0 ? 0 : quiet + 1;
+      if (quiet >= T && st < steps0 - 2) st = polish >= 1 ? steps0 - 1 : steps0 - 2;
     }
     __syncwarp();
   }
