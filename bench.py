@@ -258,19 +258,24 @@ def algorithmic_work(lib, prm, stats, grid: bool, n_steric: int):
     pose_atoms = float(np.sum(R * K * N)) + lanes * stats["translation_iter_atoms"]
     sweep_flop = pose_atoms * atom_f + R * K * len(lib) * POSE_ROT_FLOP
     sweep_xu = pose_atoms * atom_x + R * K * len(lib) * POSE_ROT_XU
+    out = {"sweep": (sweep_flop, sweep_xu), "flex": (flex_flop, flex_xu),
+           "start": (chain_flop, 0.0)}
+    gathers = {"sweep": pose_atoms}
     if getattr(prm, "polish", 0) >= 1:
         # post-flex compass (31 lanes per iteration) + the final score of each
-        # restart's pose (atom terms + every pair tested) run in the flex kernel
+        # restart's pose (atom terms + every pair tested): the polish kernel
         post_atoms = 31.0 * stats.get("post_compass_iter_atoms", 0)
-        flex_flop += post_atoms * atom_f + float(np.sum(R * (N * TERMS_FLOP + PAIR_TEST_FLOP * P)))
-        flex_xu += post_atoms * atom_x + R * float(np.sum(N)) * TERMS_XU
-    return {"sweep": (sweep_flop, sweep_xu), "flex": (flex_flop, flex_xu),
-            "start": (chain_flop, 0.0)}
+        out["polish"] = (post_atoms * atom_f + float(np.sum(R * (N * TERMS_FLOP + PAIR_TEST_FLOP * P))),
+                         post_atoms * atom_x + R * float(np.sum(N)) * TERMS_XU)
+        gathers["polish"] = post_atoms
+    return out, gathers
 
 
-def roofline(work, phase_ms, dock_ms, peaks, traffic):
+def roofline(work, phase_ms, dock_ms, peaks, traffic, gathers=None):
     """Per-kernel achieved FP32 rate over its own device time; the headline
-    is the kernel with the largest share of the dock pass."""
+    is the kernel with the largest share of the dock pass.  The sweep-key
+    kernels (sweep, polish) also carry their gather rate (one 16 B cell per
+    pose-atom) against the measured random-gather peak."""
     per = {}
     for k, (flop, xu) in work.items():
         ms = phase_ms.get(k, 0.0)
@@ -282,10 +287,20 @@ def roofline(work, phase_ms, dock_ms, peaks, traffic):
                   "frac_fp32": round(flop / t / peaks["fp32_flops"], 4),
                   "achieved_xu_tops": round(xu / t / 1e12, 3),
                   "frac_xu": round(xu / t / peaks["xu_ops"], 4)}
+        g = (gathers or {}).get(k)
+        if g and peaks.get("random_gather16_per_s"):
+            # cell lookups per second, against (a) the L1 wavefront peak of
+            # one 128 B line per clock per SM (a lookup touches one line; lanes
+            # that share a line share the wavefront, so this can exceed 1) and
+            # (b) the measured rate of fully random 16 B gathers from L2
+            per[k].update({"gathers": g, "achieved_gathers_per_s": round(g / t, 1),
+                           "x_l1_line_peak": round(g / t / peaks["l1_lines_per_s"], 4),
+                           "x_random_gather": round(g / t / peaks["random_gather16_per_s"], 4)})
     dom = max(per, key=lambda k: per[k]["ms"])
     d = per[dom]
     flop_all = sum(w[0] for w in work.values())
-    name = {"sweep": "vs_sweep_kernel", "flex": "vs_flex_kernel", "start": "vs_start_kernel"}[dom]
+    name = {"sweep": "vs_sweep_kernel", "flex": "vs_flex_kernel", "start": "vs_start_kernel",
+            "polish": "vs_polish_kernel"}[dom]
     return {"bound": "fp32", "achieved": d["achieved_tflops"],
             "peak": round(peaks["fp32_flops"] / 1e12, 3), "unit": "TFLOP/s",
             "frac": d["frac_fp32"], "traffic": (traffic or {}).get(name),
@@ -586,6 +601,9 @@ def main():
     eng = V.Engine(local)
     eng.set_pocket(pocket, grid_spacing=0.4, grid_pad=2.0)
     peaks = eng.measure_peaks()
+    peaks["random_gather16_per_s"] = eng.measure_gather_peak()
+    info0 = eng.device_info()
+    peaks["l1_lines_per_s"] = float(info0["sm_count"]) * info0["clock_khz"] * 1e3
     eng.upload(lib, classes)
     stream = torch.cuda.Stream()  # non-default stream shared by torch events and the C-ABI
     torch.cuda.set_stream(stream)
@@ -618,7 +636,7 @@ def main():
             ev[k][1].record(stream)
             torch.cuda.synchronize()
             dock_ms.append(eng.last_dock_ms())
-            phase.append(eng.phase_ms())
+            phase.append(eng.phase_ms_ex())
     launches = eng.launch_count() - launches0
     total_ms = sum(a.elapsed_time(b) for a, b in ev)
     stats = eng.stats()
@@ -628,9 +646,10 @@ def main():
     total_ms = float(t.item())
     n_total = len(lib) * world
     value = n_total * args.steps / (total_ms * 1e-3)
-    work = algorithmic_work(lib, prm, stats, True, sum(s.kind == "steric" for s in pocket.sites))
+    work, gathers = algorithmic_work(lib, prm, stats, True,
+                                     sum(s.kind == "steric" for s in pocket.sites))
     phase_ms = {k: float(np.mean([p[k] for p in phase])) for k in phase[0]}
-    rl = roofline(work, phase_ms, float(np.mean(dock_ms)), peaks, load_traffic())
+    rl = roofline(work, phase_ms, float(np.mean(dock_ms)), peaks, load_traffic(), gathers)
     top = out.cpu().numpy().view(np.uint64)
     n_ranked = int(np.sum(top != np.uint64(2**64 - 1)))
 

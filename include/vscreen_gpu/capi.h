@@ -169,6 +169,10 @@ uint64_t vs_launch_count(const vs_handle* h);
  * [2] flex+keep, [3] finish (staged mode; the fused kernel reports its whole
  * time in [2]).  CUDA events around every launch on the launch stream. */
 int vs_last_phase_ms(vs_handle* h, double out[4]);
+/* the same split with the polish kernel on its own, up to n entries (returns
+ * how many were written): [0] start, [1] sweep, [2] flex+keep, [3] finish,
+ * [4] polish (vs_last_phase_ms counts [4] in [2]) */
+int vs_last_phase_ms_ex(vs_handle* h, double* out, int32_t n);
 /* work counters of the last vs_dock: [0] translation-sweep iterations,
  * [1] the same weighted by ligand atoms, [2] start attempts, [3] flex pair
  * softplus evaluations (pairs inside the cutoff), [4..7] SM cycles summed
@@ -180,6 +184,11 @@ int vs_last_stats(vs_handle* h, uint64_t out[8]);
 int vs_last_stats_ex(vs_handle* h, uint64_t* out, int32_t n);
 /* measured device peaks (ops/s): FP32 FMA (2 flops), FP64 FMA, MUFU ex2 */
 int vs_measure_peaks(vs_handle* h, double* fp32_flops, double* fp64_flops, double* xu_ops);
+/* measured random-gather peak (16 B loads/s): independent ld.global.nc.v4 of
+ * uniformly random cells of an L2-resident 8 MB array, every lane a distinct
+ * sector, full occupancy and 8 loads in flight per thread -- the access
+ * pattern of the sweep key lookups at the most memory-level parallelism */
+int vs_measure_gather_peak(vs_handle* h, double* loads_per_s);
 
 /* Global top-k of the last run: keys ascending = (score desc, id_rank asc)
  * (rank_ligands, pipeline.cpp:243-251).  key = (~orderable(score) << 32) |

@@ -107,6 +107,8 @@ _SIGS = {
     "vs_last_stats": (C.c_int, [C.c_void_p, P(C.c_uint64)]),
     "vs_last_stats_ex": (C.c_int, [C.c_void_p, P(C.c_uint64), C.c_int32]),
     "vs_measure_peaks": (C.c_int, [C.c_void_p, P(C.c_double), P(C.c_double), P(C.c_double)]),
+    "vs_measure_gather_peak": (C.c_int, [C.c_void_p, P(C.c_double)]),
+    "vs_last_phase_ms_ex": (C.c_int, [C.c_void_p, P(C.c_double), C.c_int32]),
     "vs_topk": (C.c_int, [C.c_void_p, C.c_int32, P(C.c_uint64)]),
     "vs_topk_device": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
     "vs_topk_merge_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,

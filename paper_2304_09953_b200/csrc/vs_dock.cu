@@ -1125,10 +1125,10 @@ static cudaError_t staged_impl(int sms, cudaStream_t st, const LibDev& lib, cons
     *launches += 3;
 #ifndef VS_FUSED_POLISH
     if (prm.polish >= 1) {
-      mark(2, false);
+      mark(4, false);
       vs_polish_kernel<kGrid><<<b_pol, T, sm_pol, st>>>(lib, prm, order, n, counters + c, nmax,
                                                        tmax, r, sb);
-      mark(2, true);
+      mark(4, true);
       ++c;
       *launches += 1;
     }

@@ -287,6 +287,30 @@ __global__ void vs_peak_xu(float* out, int iters, float seed) {
   if (s == -1.2345f) out[threadIdx.x] = s;
 }
 
+// random 16 B gathers: 8 independent LCG streams per thread over n cells
+// (n a power of two); the loaded words feed an xor kept under a never-true
+// predicate
+__global__ void vs_peak_gather(const uint4* __restrict__ cells, unsigned mask, int iters,
+                               unsigned* out) {
+  unsigned h[8];
+  const unsigned t = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int k = 0; k < 8; ++k) h[k] = t * 2654435761u + 0x9E3779B9u * (k + 1);
+  unsigned acc = 0u;
+  for (int i = 0; i < iters; ++i) {
+    uint4 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      h[k] = h[k] * 1664525u + 1013904223u;
+      const uint4* c = cells + ((h[k] >> 7) & mask);
+      asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(v[k].x), "=r"(v[k].y), "=r"(v[k].z), "=r"(v[k].w) : "l"(c));
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc ^= v[k].x ^ v[k].w;
+  }
+  if (acc == 0x9E3779B9u) out[0] = acc;
+}
+
 }  // namespace vs
 
 // ------------------------------------------------------ launch wrappers --
@@ -352,6 +376,34 @@ cudaError_t launch_topk(cudaStream_t st, const unsigned long long* in, long n,
 }
 
 // kind 0 fp32 fma, 1 fp64 fma, 2 ex2; returns ops/s (best of 3)
+double measure_gather_peak(int sms) {
+  const unsigned n = 1u << 19;  // 512 Ki cells x 16 B = 8 MB (L2-resident)
+  void* buf = nullptr;
+  if (cudaMalloc(&buf, size_t(n) * 16 + 256) != cudaSuccess) return 0.0;
+  cudaMemset(buf, 0, size_t(n) * 16 + 256);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const int blocks = sms * 8, threads = 256, iters = 256;
+  double best = 0.0;
+  for (int rep = 0; rep < 4; ++rep) {
+    cudaEventRecord(a);
+    vs_peak_gather<<<blocks, threads>>>(static_cast<const uint4*>(buf), n - 1, iters,
+                                        reinterpret_cast<unsigned*>(static_cast<char*>(buf) +
+                                                                    size_t(n) * 16));
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, a, b);
+    const double loads = static_cast<double>(blocks) * threads * iters * 8;
+    if (rep > 0) best = std::max(best, loads / (ms * 1e-3));
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(buf);
+  return best;
+}
+
 double measure_peak(int kind, int sms) {
   void* buf = nullptr;
   cudaMalloc(&buf, 1024 * 8);

@@ -61,6 +61,7 @@ cudaError_t launch_grid(cudaStream_t st, const PocketDev& pk, float* steric, flo
                         float* lipo, float* key, float4* cells);
 int topk_chunk();
 double measure_peak(int kind, int sms);
+double measure_gather_peak(int sms);
 cudaError_t launch_topk(cudaStream_t st, const unsigned long long* in, long n,
                         unsigned long long* out, int k, int blocks);
 }  // namespace vs
@@ -843,9 +844,28 @@ int vs_last_phase_ms(vs_handle* h, double out[4]) {
     if (h->pkind[i] < 0) continue;
     float ms = 0.0f;
     VS_CUDA(h, cudaEventElapsedTime(&ms, h->pev[2 * i], h->pev[2 * i + 1]));
-    out[h->pkind[i]] += ms;
+    out[h->pkind[i] == 4 ? 2 : h->pkind[i]] += ms;  // polish counted with flex+keep
   }
   return VS_OK;
+}
+
+int vs_last_phase_ms_ex(vs_handle* h, double* out, int32_t n) {
+  if (!h->timed) return fail(h, VS_ERR_STATE, "no dock has run");
+  double v[5] = {0, 0, 0, 0, 0};
+  VS_CUDA(h, cudaEventSynchronize(h->ev1));
+  if (!h->staged_run) {
+    v[2] = vs_last_dock_ms(h);
+  } else {
+    for (size_t i = 0; i < h->pkind.size(); ++i) {
+      if (h->pkind[i] < 0) continue;
+      float ms = 0.0f;
+      VS_CUDA(h, cudaEventElapsedTime(&ms, h->pev[2 * i], h->pev[2 * i + 1]));
+      v[h->pkind[i]] += ms;
+    }
+  }
+  const int k = std::max(0, std::min<int>(n, 5));
+  for (int i = 0; i < k; ++i) out[i] = v[i];
+  return k;
 }
 
 int vs_last_stats(vs_handle* h, uint64_t out[8]) {
@@ -870,6 +890,14 @@ int vs_measure_peaks(vs_handle* h, double* fp32, double* fp64, double* xu) {
   if (fp32) *fp32 = measure_peak(0, h->sms);
   if (fp64) *fp64 = measure_peak(1, h->sms);
   if (xu) *xu = measure_peak(2, h->sms);
+  VS_CUDA(h, cudaGetLastError());
+  return VS_OK;
+}
+
+int vs_measure_gather_peak(vs_handle* h, double* loads_per_s) {
+  cudaSetDevice(h->device);
+  VS_CUDA(h, cudaDeviceSynchronize());
+  if (loads_per_s) *loads_per_s = measure_gather_peak(h->sms);
   VS_CUDA(h, cudaGetLastError());
   return VS_OK;
 }

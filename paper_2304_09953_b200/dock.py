@@ -343,6 +343,21 @@ class Engine:
         check(_lib.vs_last_phase_ms(self._h, out), self._h, "phase_ms")
         return dict(zip(("start", "sweep", "flex", "finish"), (float(v) for v in out)))
 
+    def phase_ms_ex(self) -> dict:
+        """Device ms of the last dock per kernel with the polish kernel on its
+        own (capi.h vs_last_phase_ms_ex)."""
+        out = (C.c_double * 5)()
+        k = _lib.vs_last_phase_ms_ex(self._h, out, 5)
+        if k < 0:
+            check(k, self._h, "phase_ms_ex")
+        return dict(zip(("start", "sweep", "flex", "finish", "polish"), (float(v) for v in out)))
+
+    def measure_gather_peak(self) -> float:
+        """Measured random 16 B gather rate (loads/s, capi.h vs_measure_gather_peak)."""
+        v = C.c_double()
+        check(_lib.vs_measure_gather_peak(self._h, C.byref(v)), self._h, "gather_peak")
+        return v.value
+
     def stats(self) -> dict:
         """Work counters of the last dock (capi.h vs_last_stats)."""
         out = np.zeros(10, np.uint64)
