@@ -6,6 +6,8 @@
 
 #include <algorithm>
 #include <array>
+#include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -206,6 +208,7 @@ struct vs_handle {
   std::vector<int> pkind;        // kernel kind of each pair (0 start .. 3 finish)
   bool timed = false;
   bool staged_run = false;
+  PinnedVec<uint8_t> fetch_stage;  // vs_fetch_results' pinned staging, reused across calls
   Packed rpack;              // vs_rescore's library staging, reused across calls
   DBuf rbuf[9];              // vs_rescore's per-bucket pose arrays, reused across calls
   double rescore_ms = -1.0;  // device time of the rescore kernels of the last vs_rescore
@@ -238,6 +241,29 @@ size_t align16z(size_t x) { return (x + 15) & ~size_t(15); }
 
 // Validation + packing of a host library (SURVEY §8 row A7/A11 checks:
 // AtomCountMismatch for empty conformers and axes outside the conformer).
+// Stable sort of ligand indices by descending cost (ties keep index order):
+// two-pass LSD radix sort on the 32-bit key ~cost (costs fit 32 bits for the
+// GPU limits; a wider cost falls back to std::stable_sort).
+void lpt_sort(std::vector<int>& idx, const std::vector<long>& cost) {
+  long cmax = 0;
+  for (int i : idx) cmax = std::max(cmax, cost[i]);
+  if (cmax >= (1L << 32) || idx.size() < 4096) {
+    std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+    return;
+  }
+  std::vector<int> tmp(idx.size());
+  std::vector<uint32_t> key(cost.size());
+  for (int i : idx) key[i] = ~static_cast<uint32_t>(cost[i]);
+  for (int pass = 0; pass < 2; ++pass) {
+    const int sh = 16 * pass;
+    std::vector<size_t> cnt(65537, 0);
+    for (int i : idx) ++cnt[((key[i] >> sh) & 0xffffu) + 1];
+    for (size_t d = 1; d < cnt.size(); ++d) cnt[d] += cnt[d - 1];
+    for (int i : idx) tmp[cnt[(key[i] >> sh) & 0xffffu]++] = i;
+    idx.swap(tmp);
+  }
+}
+
 int pack_library(vs_handle* h, const vs_library* L, const vs_size_class* classes, int nc,
                  Packed& P) {
   const int n = L->n_ligands;
@@ -345,7 +371,7 @@ int pack_library(vs_handle* h, const vs_library* L, const vs_size_class* classes
   lpt.reserve(n);
   for (int i = 0; i < n; ++i)
     if (P.cls[i] >= 0) lpt.push_back(i);
-  std::stable_sort(lpt.begin(), lpt.end(), [&](int a, int b2) { return cost[a] > cost[b2]; });
+  lpt_sort(lpt, cost);
   const int ncls = (classes && nc > 0) ? nc : 6;
   P.order.clear();
   P.order.reserve(2 * lpt.size() + 1);
@@ -671,13 +697,25 @@ int vs_upload_library(vs_handle* h, const vs_library* L, const vs_size_class* cl
   cudaSetDevice(h->device);
   h->has_lib = false;
   h->has_results = false;
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
   int rc = pack_library(h, L, classes, nc, h->lib);
   if (rc) return rc;
+  const auto t1 = clk::now();
   rc = check_nested(h, h->lib);
   if (rc) return rc;
+  const auto t2 = clk::now();
   rc = upload_packed(h, h->lib, h->own);
   if (rc) return rc;
   VS_CUDA(h, cudaStreamSynchronize(h->own));
+  const auto t3 = clk::now();
+  if (const char* e = std::getenv("VSCREEN_UPLOAD_TIMING"); e && e[0] == '1') {
+    auto ms = [](clk::time_point a, clk::time_point b) {
+      return std::chrono::duration<double, std::milli>(b - a).count();
+    };
+    std::fprintf(stderr, "vs_upload_library: pack %.2f ms, torsion-tree check %.2f ms, H2D %.2f ms\n",
+                 ms(t0, t1), ms(t1, t2), ms(t2, t3));
+  }
   h->has_lib = true;
   return VS_OK;
 }
@@ -902,26 +940,68 @@ int vs_measure_gather_peak(vs_handle* h, double* loads_per_s) {
   return VS_OK;
 }
 
+// D2H of every requested result array into one pinned staging buffer (one
+// DMA each at full link rate), then a threaded copy into the caller's
+// (pageable) buffers, which also spreads their first-touch page faults.
 int vs_fetch_results(vs_handle* h, vs_results* o) {
   cudaSetDevice(h->device);
   if (!h->has_results) return fail(h, VS_ERR_STATE, "no results");
   cudaStream_t st = h->last;
   const Packed& P = h->lib;
   const size_t n = static_cast<size_t>(P.n);
-  const int KT = h->last_prm.keep_top, R = h->last_prm.restarts;
-  if (o->best) VS_CUDA(h, cudaMemcpyAsync(o->best, h->d_best.p, n * 4, cudaMemcpyDeviceToHost, st));
-  if (o->n_kept) VS_CUDA(h, cudaMemcpyAsync(o->n_kept, h->d_nkept.p, n * 4, cudaMemcpyDeviceToHost, st));
-  if (o->n_surv) VS_CUDA(h, cudaMemcpyAsync(o->n_surv, h->d_nsurv.p, n * 4, cudaMemcpyDeviceToHost, st));
-  if (o->surv && KT > 0)
-    VS_CUDA(h, cudaMemcpyAsync(o->surv, h->d_surv.p, n * KT * sizeof(vs_pose), cudaMemcpyDeviceToHost, st));
-  if (o->surv_tors && KT > 0 && P.total_tors > 0)
-    VS_CUDA(h, cudaMemcpyAsync(o->surv_tors, h->d_surv_tors.p, P.total_tors * KT * 4, cudaMemcpyDeviceToHost, st));
-  if (o->all && h->last_prm.write_all_poses)
-    VS_CUDA(h, cudaMemcpyAsync(o->all, h->d_all.p, n * R * sizeof(vs_pose), cudaMemcpyDeviceToHost, st));
-  if (o->all_tors && h->last_prm.write_all_poses && P.total_tors > 0)
-    VS_CUDA(h, cudaMemcpyAsync(o->all_tors, h->d_all_tors.p, P.total_tors * R * 4, cudaMemcpyDeviceToHost, st));
-  if (o->keys) VS_CUDA(h, cudaMemcpyAsync(o->keys, h->d_keys.p, n * 8, cudaMemcpyDeviceToHost, st));
+  const size_t KT = static_cast<size_t>(h->last_prm.keep_top);
+  const size_t R = static_cast<size_t>(h->last_prm.restarts);
+  const size_t TT = static_cast<size_t>(P.total_tors);
+  const bool all = h->last_prm.write_all_poses != 0;
+  struct Part {
+    void* dst;
+    const void* src;
+    size_t bytes;
+    size_t off;
+  };
+  std::vector<Part> parts;
+  size_t total = 0;
+  auto add = [&](void* dst, const DBuf& src, size_t bytes) {
+    if (!dst || bytes == 0) return;
+    parts.push_back(Part{dst, src.p, bytes, total});
+    total += (bytes + 255) & ~size_t(255);
+  };
+  add(o->best, h->d_best, n * 4);
+  add(o->n_kept, h->d_nkept, n * 4);
+  add(o->n_surv, h->d_nsurv, n * 4);
+  if (KT > 0) add(o->surv, h->d_surv, n * KT * sizeof(vs_pose));
+  if (KT > 0) add(o->surv_tors, h->d_surv_tors, TT * KT * 4);
+  if (all) add(o->all, h->d_all, n * R * sizeof(vs_pose));
+  if (all) add(o->all_tors, h->d_all_tors, TT * R * 4);
+  add(o->keys, h->d_keys, n * 8);
+  if (!h->fetch_stage.resize(std::max<size_t>(total, 256)))
+    return fail(h, VS_ERR_CUDA, "pinned host allocation failed");
+  uint8_t* stage = h->fetch_stage.data();
+  for (const Part& p : parts)
+    VS_CUDA(h, cudaMemcpyAsync(stage + p.off, p.src, p.bytes, cudaMemcpyDeviceToHost, st));
   VS_CUDA(h, cudaStreamSynchronize(st));
+  // threaded copy-out in 1 MB slices
+  constexpr size_t kSlice = size_t(1) << 20;
+  std::vector<std::array<size_t, 3>> slices;  // part, offset, bytes
+  for (size_t k = 0; k < parts.size(); ++k)
+    for (size_t b = 0; b < parts[k].bytes; b += kSlice)
+      slices.push_back({k, b, std::min(kSlice, parts[k].bytes - b)});
+  auto copy = [&](size_t t, size_t nt) {
+    for (size_t i = t; i < slices.size(); i += nt) {
+      const Part& p = parts[slices[i][0]];
+      std::memcpy(static_cast<uint8_t*>(p.dst) + slices[i][1], stage + p.off + slices[i][1],
+                  slices[i][2]);
+    }
+  };
+  const size_t nt = std::max<size_t>(
+      1, std::min<size_t>({slices.size(), 16, std::max(1u, std::thread::hardware_concurrency())}));
+  if (nt == 1) {
+    copy(0, 1);
+  } else {
+    std::vector<std::thread> pool;
+    for (size_t t = 0; t < nt; ++t) pool.emplace_back(copy, t, nt);
+    for (auto& th : pool) th.join();
+  }
   for (size_t i = 0; i < n; ++i) {
     if (P.cls[i] < 0) {
       if (o->n_kept) o->n_kept[i] = -1;
