@@ -210,6 +210,8 @@ static mat3d pose_mat_d(const float* qf) {
 /* ----------------------------------------------------------- pocket --- */
 typedef struct { float c[3], w, inv; } site_f;
 
+#define SOFT_N 512 /* nodes of the search pair-softplus table (vs_types.h kSoftN) */
+
 struct vso_pocket {
   float lo[3], hi[3];
   double lo_d[3], hi_d[3];
@@ -223,6 +225,8 @@ struct vso_pocket {
   float *steric, *hbond, *lipo;
   float* key; /* sweep-key map: steric - lam * wall at each node (FP16-rounded) */
   float* keyc; /* per cell: its trilinear polynomial, 8 FP16-rounded coefficients */
+  /* search-only pair term (SWEEP_V1.md §3.4): softplus tabulated on d^2 */
+  float soft_g[SOFT_N], soft_s[SOFT_N], soft_inv_h;
 };
 
 static float site_sum(const site_f* s, int n, float x, float y, float z) {
@@ -297,6 +301,16 @@ int vso_pocket_new(const vso_pocket_desc* d, vso_pocket** out) {
   p->lam = (float)d->clash_penalty;
   float rr = p->r + 3.0f;
   p->cut2 = rr * rr;
+  { /* node k at x_k = k * (cut2 / SOFT_N): g_k and the slope to g_{k+1} (vs_softtab_kernel) */
+    const float hs = p->cut2 * (1.0f / (float)SOFT_N);
+    for (int k = 0; k < SOFT_N; ++k) {
+      const float g0 = vso_softplus((p->r - sqrtf((float)k * hs)) * 10.0f);
+      const float g1 = vso_softplus((p->r - sqrtf((float)(k + 1) * hs)) * 10.0f);
+      p->soft_g[k] = g0;
+      p->soft_s[k] = g1 - g0;
+    }
+    p->soft_inv_h = (float)SOFT_N / p->cut2;
+  }
   if (d->grid_spacing > 0.0 && !p->empty) {
     p->grid = 1;
     p->h = (float)d->grid_spacing;
@@ -432,6 +446,17 @@ static float pair_d(const vso_pocket* p, const double* a, const double* b) {
   double d2 = n2d(a[0] - b[0], a[1] - b[1], a[2] - b[2]);
   if (d2 > (double)p->cut2) return 0.0f;
   return vso_softplus((p->r - sqrtf((float)d2)) * 10.0f);
+}
+
+/* the search pair term (flex with polish >= 1): the tabulated softplus,
+ * linear between nodes (pair_soft_tab) */
+static float pair_tab(const vso_pocket* p, const double* a, const double* b) {
+  double d2 = n2d(a[0] - b[0], a[1] - b[1], a[2] - b[2]);
+  if (d2 > (double)p->cut2) return 0.0f;
+  const float x = (float)d2 * p->soft_inv_h;
+  int i = (int)x;
+  if (i > SOFT_N - 1) i = SOFT_N - 1;
+  return fmaf(x - (float)i, p->soft_s[i], p->soft_g[i]);
 }
 
 /* xor butterfly over 32 lane partial sums (warp_sum of the kernel) */
@@ -762,6 +787,7 @@ static void dock_one(const vso_pocket* p, const lig_t* L, uint64_t seed, uint32_
     const int steps0 = do_flex ? prm->flex_passes * T : 1;
     const int steps = steps0 + ((do_flex && prm->polish >= 2) ? T : 0);
     int quiet = 0; /* consecutive coarse steps without a move */
+    const int tabp = prm->polish >= 1; /* search pair term: tabulated (§3.4) */
     for (int st = 0; st < steps; ++st) {
       const int fine = st >= steps0; /* polish 2: one pass of fine angles (§3.5) */
       const int j = do_flex ? st % T : -1;
@@ -776,7 +802,9 @@ static void dock_one(const vso_pocket* p, const lig_t* L, uint64_t seed, uint32_
       long pi = 0;
       for (int i = 0; i < N; ++i)
         for (int k = i + 1; k < N; ++k, ++pi)
-          if (inm[i] == inm[k]) lp[pi & 31] = lp[pi & 31] + pair_d(p, &y[3 * i], &y[3 * k]);
+          if (inm[i] == inm[k])
+            lp[pi & 31] = lp[pi & 31] + (tabp ? pair_tab(p, &y[3 * i], &y[3 * k])
+                                              : pair_d(p, &y[3 * i], &y[3 * k]));
       const float fb = butterfly(lf), wb = butterfly(lw), pb = butterfly(lp);
       float bestS = -INFINITY, best_th = 0.0f;
       int best_a = 0;
@@ -808,7 +836,8 @@ static void dock_one(const vso_pocket* p, const lig_t* L, uint64_t seed, uint32_
             fm[hh] = fm[hh] + fi;
             wm[hh] = wm[hh] + wi;
             for (int k = 0; k < N; ++k)
-              if (!inm[k]) pc[hh] = pc[hh] + pair_d(p, yn, &y[3 * k]);
+              if (!inm[k])
+                pc[hh] = pc[hh] + (tabp ? pair_tab(p, yn, &y[3 * k]) : pair_d(p, yn, &y[3 * k]));
           }
         }
         const float Sa = (fb + (fm[0] + fm[1])) - p->lam * ((pb + (pc[0] + pc[1])) + (wb + (wm[0] + wm[1])));

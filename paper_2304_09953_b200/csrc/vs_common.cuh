@@ -201,6 +201,24 @@ __device__ __forceinline__ float pair_term_d(const PocketDev& pk, double dx, dou
 __device__ __forceinline__ float pair_soft(double d2) {
   return det_softplus((c_pk.r - sqrtf(static_cast<float>(d2))) * 10.0f);
 }
+// search-only pair term (SWEEP_V1.md §3.4): the clash softplus of a pair
+// inside the cutoff read from the d^2 table by linear interpolation
+__device__ __forceinline__ float pair_soft_tab(const float2* tab, double d2) {
+  const float x = static_cast<float>(d2) * c_pk.soft_inv_h;
+  const int i = min(static_cast<int>(x), kSoftN - 1);
+  const float2 e = tab[i];
+  return fmaf(x - static_cast<float>(i), e.y, e.x);
+}
+// pair term of the flex search: tabulated (kTab) or exact, counting pairs
+// inside the cutoff (work counter)
+template <bool kTab>
+__device__ __forceinline__ float pair_term_s(const float2* tab, double dx, double dy, double dz,
+                                             int& n_active) {
+  const double d2 = det_norm2_d(dx, dy, dz);
+  if (d2 > c_pk.cut2_d) return 0.0f;
+  ++n_active;
+  return kTab ? pair_soft_tab(tab, d2) : pair_soft(d2);
+}
 // same as pair_term_d, counting the pairs inside the cutoff (work counter)
 __device__ __forceinline__ float pair_term_d(const PocketDev& pk, double dx, double dy, double dz,
                                              int& n_active) {

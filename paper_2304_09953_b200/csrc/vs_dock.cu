@@ -291,11 +291,11 @@ static __device__ VS_PHASE int sweep_phase(const PocketDev& pk, const Dims d,
 // + moved part(candidate: moving_j atoms rotated about the state's axis j
 // and their cross pairs; lane pair (a, h), lane h takes moving positions
 // = h mod 2).  Returns the score of the final state.
-template <int kGrid, bool kPacked = false>
+template <int kGrid, bool kPacked = false, bool kTab = false>
 static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, int N, int T,
                                                 int F, int A, float step, const PoseF* P,
                                                 int lane, unsigned long long* n_active,
-                                                int polish) {
+                                                int polish, const float2* tab = nullptr) {
   const WarpSmem s = dock_smem(d);
   const int a_lane = lane & 15;
   const int h = lane >> 4;
@@ -345,7 +345,7 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
       while (i < N - 1) {
         if (in_mask(mk, i) == in_mask(mk, k)) {
           const double4 yi = s.ys[i], yk = s.ys[k];
-          pb = pb + pair_term_d(pk, yi.x - yk.x, yi.y - yk.y, yi.z - yk.z, nact);
+          pb = pb + pair_term_s<kTab>(tab, yi.x - yk.x, yi.y - yk.y, yi.z - yk.z, nact);
         }
         k += 32;
         while (i < N - 1 && k >= N) {
@@ -408,7 +408,7 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
           double4 yk = part[0];
           for (int p = 0; p < np; ++p) {
             const double4 yn = part[p + 1];
-            pc = pc + pair_term_d(pk, yx - yk.x, yy - yk.y, yz - yk.z, nact);
+            pc = pc + pair_term_s<kTab>(tab, yx - yk.x, yy - yk.y, yz - yk.z, nact);
             yk = yn;
           }
         } else {
@@ -423,7 +423,7 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
             while (true) {
               b2 &= b2 - 1u;
               const double4 yn = yw[b2 ? __ffs(b2) - 1 : 0];
-              pc = pc + pair_term_d(pk, yx - yk.x, yy - yk.y, yz - yk.z, nact);
+              pc = pc + pair_term_s<kTab>(tab, yx - yk.x, yy - yk.y, yz - yk.z, nact);
               if (!b2) break;
               yk = yn;
             }
@@ -712,7 +712,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB)
       const long long c1 = clock64();
       const int best_k = sweep_phase<kGrid>(pk, d, rots, prm.K, N, lane, &P, &n_trans, prm.polish);
       const long long c2 = clock64();
-      float S = flex_phase<kGrid>(pk, d, N, T, prm.F, prm.A, step, &P, lane, &st[2], prm.polish);
+      float S = prm.polish >= 1
+                    ? flex_phase<kGrid, false, true>(pk, d, N, T, prm.F, prm.A, step, &P, lane,
+                                                     &st[2], prm.polish, c_pk.soft_tab)
+                    : flex_phase<kGrid>(pk, d, N, T, prm.F, prm.A, step, &P, lane, &st[2],
+                                        prm.polish);
       if (prm.polish >= 1) S = polish_phase<kGrid, false>(pk, d, N, lane, &P, &n_post);
       const long long c3 = clock64();
       if (keep_phase(d, N, T, &P, S, r, att, best_k, kx, nmax, kp, 8 + tmax, km, nk, prm.delta,
@@ -870,6 +874,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_FLEX)
                kLayLig | kLayState | kLayPosed | kLayFlex | kLaySweep | kLayAliasY0};
   const WarpSmem s = dock_smem(d);
   const int lane = threadIdx.x & 31;
+  // the search pair-softplus table (polish >= 1) behind the warps' regions
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float2* tab = reinterpret_cast<float2*>(
+      smem_raw + kWarpsPerBlock * warp_smem_bytes(d.nmax, d.tmax, d.mvmax, d.lay));
+  if (prm.polish >= 1) {
+    for (int k = threadIdx.x; k < kSoftN; k += blockDim.x) tab[k] = c_pk.soft_tab[k];
+    __syncthreads();
+  }
   if (lane == 0) mbar_init(s.bar);
   __syncwarp();
   uint32_t phase = 0;
@@ -894,8 +906,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_FLEX)
     P.q[3] = pq.w;
     __syncwarp();
     unsigned long long nact = 0;
-    float S = flex_phase<kGrid, true>(pk, d, N, T, prm.F, prm.A, step, &P, lane, &nact,
-                                      prm.polish);
+    float S = prm.polish >= 1
+                  ? flex_phase<kGrid, true, true>(pk, d, N, T, prm.F, prm.A, step, &P, lane,
+                                                  &nact, prm.polish, tab)
+                  : flex_phase<kGrid, true, false>(pk, d, N, T, prm.F, prm.A, step, &P, lane,
+                                                   &nact, prm.polish);
 #ifndef VS_FUSED_POLISH
     if (prm.polish >= 1) {
       // the polish + keep run in vs_polish_kernel: hand over the flexed state
@@ -1071,7 +1086,8 @@ size_t stage_smem_per_block(int nmax, int tmax, int mvmax) {
                        kLayLig | kLayKept};
   size_t m = 0;
   for (int l : lays) {
-    const size_t b = kWarpsPerBlock * warp_smem_bytes(nmax, tmax, mvmax, l);
+    const size_t b = kWarpsPerBlock * warp_smem_bytes(nmax, tmax, mvmax, l) +
+                     ((l & kLayAliasY0) ? sizeof(float2) * kSoftN : 0);  // flex: softplus table
     m = b > m ? b : m;
   }
   return m;
@@ -1089,7 +1105,8 @@ static cudaError_t staged_impl(int sms, cudaStream_t st, const LibDev& lib, cons
   const size_t sm_flex = kWarpsPerBlock * warp_smem_bytes(
                                               nmax, tmax, mvmax,
                                               kLayLig | kLayState | kLayPosed | kLayFlex |
-                                                  kLaySweep | kLayAliasY0);
+                                                  kLaySweep | kLayAliasY0) +
+                         sizeof(float2) * kSoftN;  // search pair-softplus table
   const size_t sm_fin = kWarpsPerBlock * warp_smem_bytes(nmax, tmax, mvmax, kLayLig | kLayKept);
   const int b_start = stage_blocks(vs_start_kernel<kGrid>, sm_start, sms, n, 8);
   const int b_sweep = stage_blocks(vs_sweep_kernel<kGrid>, sm_sweep, sms, n, VS_MINB_SWEEP);

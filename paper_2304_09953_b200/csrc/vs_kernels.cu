@@ -216,6 +216,17 @@ __global__ void vs_pack_half_kernel(const GridDev g, const float* __restrict__ n
   }
 }
 
+// =========================================== search pair-softplus table
+// node k: x_k = k * (cut2 / kSoftN) (FP32), g_k = softplus((r - sqrt(x_k)) * 10)
+__global__ void vs_softtab_kernel(float r, float cut2, float2* __restrict__ tab) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= kSoftN) return;
+  const float h = cut2 * (1.0f / static_cast<float>(kSoftN));
+  const float g0 = det_softplus((r - sqrtf(static_cast<float>(k) * h)) * 10.0f);
+  const float g1 = det_softplus((r - sqrtf(static_cast<float>(k + 1) * h)) * 10.0f);
+  tab[k] = make_float2(g0, g1 - g0);
+}
+
 // ============================================================ top-k kernel
 // Block b sorts keys [b*C, (b+1)*C) ascending (bitonic, shared memory) and
 // writes its k smallest to out[b*k ...].  Keys are unique (id_rank in the low
@@ -368,6 +379,11 @@ cudaError_t launch_grid(cudaStream_t st, const PocketDev& pk, float* steric, flo
 }
 
 int topk_chunk() { return kTopkC; }
+
+cudaError_t launch_softtab(cudaStream_t st, float r, float cut2, float2* tab) {
+  vs_softtab_kernel<<<(kSoftN + 255) / 256, 256, 0, st>>>(r, cut2, tab);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_topk(cudaStream_t st, const unsigned long long* in, long n,
                         unsigned long long* out, int k, int blocks) {

@@ -63,6 +63,7 @@ cudaError_t launch_grid(cudaStream_t st, const PocketDev& pk, float* steric, flo
                         float* lipo, float* key, float4* cells);
 int topk_chunk();
 double measure_peak(int kind, int sms);
+cudaError_t launch_softtab(cudaStream_t st, float r, float cut2, float2* tab);
 double measure_gather_peak(int sms);
 cudaError_t launch_topk(cudaStream_t st, const unsigned long long* in, long n,
                         unsigned long long* out, int k, int blocks);
@@ -188,7 +189,7 @@ struct vs_handle {
   bool has_pocket = false;
   bool empty_bounds = false;
   PocketDev pk{};
-  DBuf d_sites, d_maps;
+  DBuf d_sites, d_maps, d_softtab;
   DBuf d_sites64;               // FP64 sites, pocket order (score_gradient)
   int n_sites64 = 0;
   double box_lo[3] = {0, 0, 0}, box_hi[3] = {0, 0, 0}, r64 = 0.0, lam64 = 0.0;
@@ -544,7 +545,7 @@ void vs_destroy(vs_handle* h) {
   h->lib.release();
   h->rpack.release();
   for (DBuf& b : h->rbuf) b.release();
-  for (DBuf* b : {&h->d_sites, &h->d_sites64, &h->d_maps, &h->d_surv, &h->d_surv_tors, &h->d_all, &h->d_all_tors,
+  for (DBuf* b : {&h->d_sites, &h->d_softtab, &h->d_sites64, &h->d_maps, &h->d_surv, &h->d_surv_tors, &h->d_all, &h->d_all_tors,
                   &h->d_best, &h->d_nkept, &h->d_nsurv, &h->d_keys, &h->d_counters, &h->d_sx,
                   &h->d_sp, &h->d_sm, &h->d_rots, &h->d_topk_a, &h->d_topk_b, &h->d_stats,
                   &h->d_sg_ys, &h->d_sg_ysf, &h->d_sg_th, &h->d_sg_pose, &h->d_sg_bk, &h->d_sg_nk,
@@ -627,6 +628,11 @@ int vs_set_pocket(vs_handle* h, const vs_pocket* p, double spacing, double pad) 
   const float rr = pk.r + 3.0f;
   pk.cut2 = rr * rr;
   pk.cut2_d = static_cast<double>(pk.cut2);
+  VS_CUDA(h, h->d_softtab.ensure(sizeof(float2) * kSoftN));
+  VS_CUDA(h, launch_softtab(st, pk.r, pk.cut2, h->d_softtab.as<float2>()));
+  ++h->launches;
+  pk.soft_tab = h->d_softtab.as<const float2>();
+  pk.soft_inv_h = static_cast<float>(kSoftN) / pk.cut2;
   pk.n_steric = counts[0];
   pk.n_hbond = counts[1];
   pk.n_lipo = counts[2];

@@ -55,7 +55,13 @@ struct PocketDev {
   const SiteF* sites;       // [steric | hbond | lipo], pocket order within kind
   int grid_mode;            // 0 analytic field, 1 grid maps
   GridDev grid;
+  // search-only pair term (flex with polish >= 1, SWEEP_V1.md §3.4): the
+  // clash softplus tabulated on d^2 in [0, cut2] at kSoftN + 1 nodes,
+  // entry k = (g_k, g_{k+1} - g_k); soft_inv_h = kSoftN / cut2
+  const float2* soft_tab;
+  float soft_inv_h;
 };
+constexpr int kSoftN = 512;
 
 // Output pose record (40 B); torsions live in a parallel float array.
 struct PoseOut {
