@@ -441,6 +441,37 @@ static void atom_terms(const vso_pocket* p, const mat3d* R, const double* t, con
   if (xo) memcpy(xo, x, 12);
 }
 
+/* the sweep key of one world point (flex search with the polish in grid
+ * mode, SWEEP_V1.md §3.4): f = K(x) (the key map holds S - lam W), w = 0 */
+static float key_at(const vso_pocket* p, const float* x) {
+  const float g[3] = {(x[0] - p->gx0) * p->inv_h, (x[1] - p->gy0) * p->inv_h,
+                      (x[2] - p->gz0) * p->inv_h};
+  const float fx = floorf(g[0]), fy = floorf(g[1]), fz = floorf(g[2]);
+  const int ix = (int)fx, iy = (int)fy, iz = (int)fz;
+  if ((unsigned)ix <= (unsigned)(p->nx - 2) && (unsigned)iy <= (unsigned)(p->ny - 2) &&
+      (unsigned)iz <= (unsigned)(p->nz - 2)) {
+    const float tx = g[0] - fx, ty = g[1] - fy, tz = g[2] - fz;
+    const float* c8 = p->keyc + 8 * (((long)iz * (p->ny - 1) + iy) * (p->nx - 1) + ix);
+    return fmaf(fmaf(fmaf(c8[7], tz, c8[3]), ty, fmaf(c8[5], tz, c8[1])), tx,
+                fmaf(fmaf(c8[6], tz, c8[2]), ty, fmaf(c8[4], tz, c8[0])));
+  }
+  const float wx = fmaf(g[0], p->h, p->gx0), wy = fmaf(g[1], p->h, p->gy0);
+  const float wz = fmaf(g[2], p->h, p->gz0);
+  const float w = fminf(fminf(fminf(wx - p->lo[0], p->hi[0] - wx), fminf(wy - p->lo[1], p->hi[1] - wy)),
+                        fminf(wz - p->lo[2], p->hi[2] - wz));
+  return -(p->lam * ((p->r - w) * 10.0f));
+}
+
+static void flex_terms(const vso_pocket* p, int key, const mat3d* R, const double* t,
+                       const double* y, float* f, float* w) {
+  if (!key) { atom_terms(p, R, t, y, f, w, NULL); return; }
+  double v[3];
+  apply_d(R, y, t, v);
+  const float x[3] = {(float)v[0], (float)v[1], (float)v[2]};
+  *f = key_at(p, x);
+  *w = 0.0f;
+}
+
 /* pair clash softplus from FP64 coordinates (dock.cpp:86-97) */
 static float pair_d(const vso_pocket* p, const double* a, const double* b) {
   double d2 = n2d(a[0] - b[0], a[1] - b[1], a[2] - b[2]);
@@ -781,7 +812,8 @@ static void dock_one(const vso_pocket* p, const lig_t* L, uint64_t seed, uint32_
     float* fa = (float*)malloc(sizeof(float) * (size_t)N);
     float* wa = (float*)malloc(sizeof(float) * (size_t)N);
     unsigned char* inm = (unsigned char*)malloc((size_t)N);
-    for (int i = 0; i < N; ++i) atom_terms(p, &RS, ptd, &y[3 * i], &fa[i], &wa[i], NULL);
+    const int keyt = prm->polish >= 1 && p->grid; /* search atom terms: the sweep key (§3.4) */
+    for (int i = 0; i < N; ++i) flex_terms(p, keyt, &RS, ptd, &y[3 * i], &fa[i], &wa[i]);
     float S = 0.0f;
     const int do_flex = T > 0 && prm->flex_passes > 0;
     const int steps0 = do_flex ? prm->flex_passes * T : 1;
@@ -832,7 +864,7 @@ static void dock_one(const vso_pocket* p, const lig_t* L, uint64_t seed, uint32_
             double v[3] = {y[3 * idx] - o[0], y[3 * idx + 1] - o[1], y[3 * idx + 2] - o[2]}, yn[3];
             apply_d(&M, v, o, yn);
             float fi, wi;
-            atom_terms(p, &RS, ptd, yn, &fi, &wi, NULL);
+            flex_terms(p, keyt, &RS, ptd, yn, &fi, &wi);
             fm[hh] = fm[hh] + fi;
             wm[hh] = wm[hh] + wi;
             for (int k = 0; k < N; ++k)
@@ -852,7 +884,7 @@ static void dock_one(const vso_pocket* p, const lig_t* L, uint64_t seed, uint32_
           const int idx = mv[q2];
           double v[3] = {y[3 * idx] - o[0], y[3 * idx + 1] - o[1], y[3 * idx + 2] - o[2]};
           apply_d(&M, v, o, &y[3 * idx]);
-          atom_terms(p, &RS, ptd, &y[3 * idx], &fa[idx], &wa[idx], NULL);
+          flex_terms(p, keyt, &RS, ptd, &y[3 * idx], &fa[idx], &wa[idx]);
         }
         th[j] = best_th;
       }
