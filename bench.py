@@ -219,6 +219,11 @@ PAIR_TEST_FLOP = 9       # FP64 difference, norm, compare
 PAIR_ACTIVE_FLOP = 52    # sqrt fix-up 4, z 2, softplus 46 (exp 21 + log1p 21 + tails)
 PAIR_ACTIVE_XU = 3       # sqrt, exp shift, float conversion
 AXIS_FLOP = 81           # flex rotation: half angle 3, sincos_d 44, quaternion matrix 30, axis 4
+# the flex search with the polish (SWEEP_V1.md §3.4): sweep-key atom terms
+# (grid mode) and the tabulated pair softplus
+TERMS_FLOP_SEARCH = 41   # FP64 transform 18 + grid frame 6 + fractions 3 + 7 FMAs 14
+PAIR_ACTIVE_FLOP_TAB = 4  # scale 1, fraction 1, interpolation FMA 2
+PAIR_ACTIVE_XU_TAB = 3    # FP64->FP32, float->int, int->float
 MOVE_FLOP = 18           # FP64 rotation of one moving atom
 
 
@@ -233,6 +238,10 @@ def algorithmic_work(lib, prm, stats, grid: bool, n_steric: int):
               cutoff (device counter) add the softplus cost
       start   the FP64 torsion chain of each restart"""
     R, K, A, F = prm.restarts, prm.rotations, prm.flex_angles, prm.flex_passes
+    search = getattr(prm, "polish", 0) >= 1  # flex terms of the search (§3.4)
+    terms_flop = TERMS_FLOP_SEARCH if (search and grid) else TERMS_FLOP
+    pair_flop = PAIR_ACTIVE_FLOP_TAB if search else PAIR_ACTIVE_FLOP
+    pair_xu = PAIR_ACTIVE_XU_TAB if search else PAIR_ACTIVE_XU
     N = lib.n_atoms.astype(np.float64)
     T = lib.n_tors.astype(np.int64)
     _, to, _ = lib.offsets()
@@ -240,15 +249,15 @@ def algorithmic_work(lib, prm, stats, grid: bool, n_steric: int):
     Nt = np.repeat(N, T)                       # ligand atom count per torsion
     pnc = m * (m - 1) / 2 + (Nt - m) * (Nt - m - 1) / 2
     step_flop = (2 * Nt + PAIR_TEST_FLOP * pnc
-                 + A * (AXIS_FLOP + m * (MOVE_FLOP + TERMS_FLOP) + PAIR_TEST_FLOP * m * (Nt - m)))
+                 + A * (AXIS_FLOP + m * (MOVE_FLOP + terms_flop) + PAIR_TEST_FLOP * m * (Nt - m)))
     step_xu = A * m * TERMS_XU
     flex_flop = float(np.sum(step_flop)) * R * F
     flex_xu = float(np.sum(step_xu)) * R * F
     P = N * (N - 1) / 2
     no_flex = (T == 0) | (F == 0)
     flex_flop += float(np.sum(np.where(no_flex, R * (2 * N + PAIR_TEST_FLOP * P), 0.0)))
-    flex_flop += float(np.sum(R * N * TERMS_FLOP)) + stats["active_pairs"] * PAIR_ACTIVE_FLOP
-    flex_xu += stats["active_pairs"] * PAIR_ACTIVE_XU + R * float(np.sum(N)) * TERMS_XU
+    flex_flop += float(np.sum(R * N * terms_flop)) + stats["active_pairs"] * pair_flop
+    flex_xu += stats["active_pairs"] * pair_xu + R * float(np.sum(N)) * TERMS_XU
     chain_flop = float(np.sum(np.add.reduceat(np.r_[AXIS_FLOP + MOVE_FLOP * m, 0.0],
                                               np.minimum(to[:-1], len(m))) * (T > 0))) * R
     atom_f = ATOM_FLOP_KEY if grid else 31 + 11 * n_steric
