@@ -490,6 +490,17 @@ static float pair_tab(const vso_pocket* p, const double* a, const double* b) {
   return fmaf(x - (float)i, p->soft_s[i], p->soft_g[i]);
 }
 
+/* cross pair of the flex search (§3.4): FP32 coordinates, FP32 squared
+ * distance and cutoff, the tabulated softplus (pair_term_f) */
+static float pair_tab_f(const vso_pocket* p, const double* a, const double* b) {
+  const float d2 = n2((float)a[0] - (float)b[0], (float)a[1] - (float)b[1], (float)a[2] - (float)b[2]);
+  if (d2 > p->cut2) return 0.0f;
+  const float x = d2 * p->soft_inv_h;
+  int i = (int)x;
+  if (i > SOFT_N - 1) i = SOFT_N - 1;
+  return fmaf(x - (float)i, p->soft_s[i], p->soft_g[i]);
+}
+
 /* xor butterfly over 32 lane partial sums (warp_sum of the kernel) */
 static float butterfly(const float* in) {
   float a[32], b[32];
@@ -869,7 +880,7 @@ static void dock_one(const vso_pocket* p, const lig_t* L, uint64_t seed, uint32_
             wm[hh] = wm[hh] + wi;
             for (int k = 0; k < N; ++k)
               if (!inm[k])
-                pc[hh] = pc[hh] + (tabp ? pair_tab(p, yn, &y[3 * k]) : pair_d(p, yn, &y[3 * k]));
+                pc[hh] = pc[hh] + (tabp ? pair_tab_f(p, yn, &y[3 * k]) : pair_d(p, yn, &y[3 * k]));
           }
         }
         const float Sa = (fb + (fm[0] + fm[1])) - p->lam * ((pb + (pc[0] + pc[1])) + (wb + (wm[0] + wm[1])));

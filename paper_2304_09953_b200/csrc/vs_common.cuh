@@ -209,6 +209,18 @@ __device__ __forceinline__ float pair_soft_tab(const float2* tab, double d2) {
   const float2 e = tab[i];
   return fmaf(x - static_cast<float>(i), e.y, e.x);
 }
+// cross pair of the flex search from FP32 coordinates (SWEEP_V1.md §3.4):
+// FP32 squared distance, FP32 cutoff, tabulated softplus
+__device__ __forceinline__ float pair_term_f(const float2* tab, float dx, float dy, float dz,
+                                             int& n_active) {
+  const float d2 = det_norm2(dx, dy, dz);
+  if (d2 > c_pk.cut2) return 0.0f;
+  ++n_active;
+  const float x = d2 * c_pk.soft_inv_h;
+  const int i = min(static_cast<int>(x), kSoftN - 1);
+  const float2 e = tab[i];
+  return fmaf(x - static_cast<float>(i), e.y, e.x);
+}
 // pair term of the flex search: tabulated (kTab) or exact, counting pairs
 // inside the cutoff (work counter)
 template <bool kTab>

@@ -374,7 +374,15 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
         const int i = i0 + lane;
         const bool pt = i < N && !in_mask(mk, i);
         const unsigned bal = __ballot_sync(kFull, pt);
-        if (pt) s.y0[np + __popc(bal & ((1u << lane) - 1u))] = s.ys[i];
+        if (pt) {
+          const int p = np + __popc(bal & ((1u << lane) - 1u));
+          const double4 v = s.ys[i];
+          if (kTab)  // the search tests cross pairs in FP32
+            reinterpret_cast<float4*>(s.y0)[p] = make_float4(
+                static_cast<float>(v.x), static_cast<float>(v.y), static_cast<float>(v.z), 0.0f);
+          else
+            s.y0[p] = v;
+        }
         np += __popc(bal);
       }
       __syncwarp();
@@ -412,7 +420,18 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
         flex_terms<kGrid, kTab>(s.pose, yx, yy, yz, &fi, &wi);
         fm = fm + fi;
         wm = wm + wi;
-        if constexpr (kPacked) {
+        if constexpr (kPacked && kTab) {
+          // the search (§3.4): FP32 moved atom against the FP32 partner list
+          const float4* part = reinterpret_cast<const float4*>(s.y0);
+          const float fx = static_cast<float>(yx), fy = static_cast<float>(yy),
+                      fz = static_cast<float>(yz);
+          float4 yk = part[0];
+          for (int p = 0; p < np; ++p) {
+            const float4 yn = part[p + 1];
+            pc = pc + pair_term_f(tab, fx - yk.x, fy - yk.y, fz - yk.z, nact);
+            yk = yn;
+          }
+        } else if constexpr (kPacked) {
           // next partner loaded before this pair's test; part[np] (np < N:
           // moving_j holds b_j) is in the buffer and unused
           const double4* part = s.y0;
@@ -434,7 +453,12 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
             while (true) {
               b2 &= b2 - 1u;
               const double4 yn = yw[b2 ? __ffs(b2) - 1 : 0];
-              pc = pc + pair_term_s<kTab>(tab, yx - yk.x, yy - yk.y, yz - yk.z, nact);
+              if (kTab)  // the search (§3.4): FP32 cross pairs
+                pc = pc + pair_term_f(tab, static_cast<float>(yx) - static_cast<float>(yk.x),
+                                      static_cast<float>(yy) - static_cast<float>(yk.y),
+                                      static_cast<float>(yz) - static_cast<float>(yk.z), nact);
+              else
+                pc = pc + pair_term_s<kTab>(tab, yx - yk.x, yy - yk.y, yz - yk.z, nact);
               if (!b2) break;
               yk = yn;
             }
