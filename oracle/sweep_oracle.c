@@ -479,17 +479,6 @@ static float pair_d(const vso_pocket* p, const double* a, const double* b) {
   return vso_softplus((p->r - sqrtf((float)d2)) * 10.0f);
 }
 
-/* the search pair term (flex with polish >= 1): the tabulated softplus,
- * linear between nodes (pair_soft_tab) */
-static float pair_tab(const vso_pocket* p, const double* a, const double* b) {
-  double d2 = n2d(a[0] - b[0], a[1] - b[1], a[2] - b[2]);
-  if (d2 > (double)p->cut2) return 0.0f;
-  const float x = (float)d2 * p->soft_inv_h;
-  int i = (int)x;
-  if (i > SOFT_N - 1) i = SOFT_N - 1;
-  return fmaf(x - (float)i, p->soft_s[i], p->soft_g[i]);
-}
-
 /* cross pair of the flex search (§3.4): FP32 coordinates, FP32 squared
  * distance and cutoff, the tabulated softplus (pair_term_f) */
 static float pair_tab_f(const vso_pocket* p, const double* a, const double* b) {
@@ -838,17 +827,20 @@ static void dock_one(const vso_pocket* p, const lig_t* L, uint64_t seed, uint32_
       const int* mv = do_flex ? L->moving + L->mstart[j] : NULL;
       memset(inm, 0, (size_t)N);
       for (int q2 = 0; q2 < m; ++q2) inm[mv[q2]] = 1;
+      /* base sums: common to every candidate; the search with the polish
+       * (§3.4) ranks the candidates without them */
       float lf[32], lw[32], lp[32];
       for (int l = 0; l < 32; ++l) lf[l] = lw[l] = lp[l] = 0.0f;
-      for (int i = 0; i < N; ++i)
-        if (!inm[i]) { lf[i & 31] = lf[i & 31] + fa[i]; lw[i & 31] = lw[i & 31] + wa[i]; }
-      long pi = 0;
-      for (int i = 0; i < N; ++i)
-        for (int k = i + 1; k < N; ++k, ++pi)
-          if (inm[i] == inm[k])
-            lp[pi & 31] = lp[pi & 31] + (tabp ? pair_tab(p, &y[3 * i], &y[3 * k])
-                                              : pair_d(p, &y[3 * i], &y[3 * k]));
-      const float fb = butterfly(lf), wb = butterfly(lw), pb = butterfly(lp);
+      if (!tabp) {
+        for (int i = 0; i < N; ++i)
+          if (!inm[i]) { lf[i & 31] = lf[i & 31] + fa[i]; lw[i & 31] = lw[i & 31] + wa[i]; }
+        long pi = 0;
+        for (int i = 0; i < N; ++i)
+          for (int k = i + 1; k < N; ++k, ++pi)
+            if (inm[i] == inm[k]) lp[pi & 31] = lp[pi & 31] + pair_d(p, &y[3 * i], &y[3 * k]);
+      }
+      const float fb = tabp ? 0.0f : butterfly(lf), wb = tabp ? 0.0f : butterfly(lw);
+      const float pb = tabp ? 0.0f : butterfly(lp);
       float bestS = -INFINITY, best_th = 0.0f;
       int best_a = 0;
       const int nc = do_flex ? prm->flex_angles : 1;

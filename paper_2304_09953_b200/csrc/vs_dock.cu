@@ -337,14 +337,17 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
     const int4 ax = do_flex ? s.ax[j] : make_int4(0, 0, 0, 0);
     const int m = ax.w;
     const unsigned* mk = do_flex ? s.tmask + 4 * j : s.mask;
+    // base sums (atoms outside moving_j, pairs not crossing it): common to
+    // every candidate of the step, so the search with the polish (§3.4)
+    // ranks the candidates without them
     float fb = 0.0f, wb = 0.0f, pb = 0.0f;
-    for (int i = lane; i < N; i += 32) {
+    for (int i = lane; !kTab && i < N; i += 32) {
       if (!in_mask(mk, i)) {
         fb = fb + s.fa[i];
         wb = wb + s.wa[i];
       }
     }
-    {
+    if (!kTab) {
       // lane l takes the pairs p = l, l + 32, ... of the row-major (i < k)
       // order, (i, k) advanced incrementally: every lane busy, same pairs and
       // per-lane order as a 32-strided walk of each row
@@ -387,9 +390,11 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
       }
       __syncwarp();
     }
-    fb = warp_sum(fb);
-    wb = warp_sum(wb);
-    pb = warp_sum(pb);
+    if (!kTab) {
+      fb = warp_sum(fb);
+      wb = warp_sum(wb);
+      pb = warp_sum(pb);
+    }
     const bool active = do_flex && a_lane < A;
     float th_new = 0.0f;
     float fm = 0.0f, wm = 0.0f, pc = 0.0f;

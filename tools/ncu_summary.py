@@ -105,11 +105,14 @@ def dock_report(tag):
 
 def main(tag):
     os.makedirs(PROF, exist_ok=True)
-    json.dump(launches(tag), open(os.path.join(PROF, f"{tag}_launches.json"), "w"), indent=1)
-    t = traffic(tag)
-    json.dump(t, open(os.path.join(PROF, "ncu_dock_traffic.json"), "w"), indent=1)
+    t = None
+    if os.path.exists(os.path.join(OUT, f"launches_{tag}.csv")):  # (a full-capture-only round skips these)
+        json.dump(launches(tag), open(os.path.join(PROF, f"{tag}_launches.json"), "w"), indent=1)
+        t = traffic(tag)
+        json.dump(t, open(os.path.join(PROF, "ncu_dock_traffic.json"), "w"), indent=1)
     summ, rep = dock_report(tag)
-    summ["dram_traffic_c2_first_launch"] = t["kernels"]
+    if t:
+        summ["dram_traffic_c2_first_launch"] = t["kernels"]
     json.dump(summ, open(os.path.join(PROF, f"{tag}_dock_ncu.json"), "w"), indent=1)
     import ncu_funcs
     import sass_lines
