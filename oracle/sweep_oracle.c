@@ -18,6 +18,7 @@
 #define PI_D 3.14159265358979323846
 #define PI_F 3.14159274f
 #define TWO_PI_F 6.28318548f
+#define HALF_PI_F 1.57079637f
 #define GOLDEN 0x9e3779b97f4a7c15ull
 #define MAX_R 64
 
@@ -443,9 +444,7 @@ static void atom_terms(const vso_pocket* p, const mat3d* R, const double* t, con
 
 /* the sweep key of one world point (flex search with the polish in grid
  * mode, SWEEP_V1.md §3.4): f = K(x) (the key map holds S - lam W), w = 0 */
-static float key_at(const vso_pocket* p, const float* x) {
-  const float g[3] = {(x[0] - p->gx0) * p->inv_h, (x[1] - p->gy0) * p->inv_h,
-                      (x[2] - p->gz0) * p->inv_h};
+static float key_at_grid(const vso_pocket* p, const float* g) {
   const float fx = floorf(g[0]), fy = floorf(g[1]), fz = floorf(g[2]);
   const int ix = (int)fx, iy = (int)fy, iz = (int)fz;
   if ((unsigned)ix <= (unsigned)(p->nx - 2) && (unsigned)iy <= (unsigned)(p->ny - 2) &&
@@ -460,6 +459,22 @@ static float key_at(const vso_pocket* p, const float* x) {
   const float w = fminf(fminf(fminf(wx - p->lo[0], p->hi[0] - wx), fminf(wy - p->lo[1], p->hi[1] - wy)),
                         fminf(wz - p->lo[2], p->hi[2] - wz));
   return -(p->lam * ((p->r - w) * 10.0f));
+}
+
+static float key_at(const vso_pocket* p, const float* x) {
+  const float g[3] = {(x[0] - p->gx0) * p->inv_h, (x[1] - p->gy0) * p->inv_h,
+                      (x[2] - p->gz0) * p->inv_h};
+  return key_at_grid(p, g);
+}
+
+/* cross pair of the FP32 search: FP32 moved atom vs the FP32-rounded partner */
+static float pair_f32(const vso_pocket* p, const float* a, const double* b) {
+  const float d2 = n2(a[0] - (float)b[0], a[1] - (float)b[1], a[2] - (float)b[2]);
+  if (d2 > p->cut2) return 0.0f;
+  const float x = d2 * p->soft_inv_h;
+  int i = (int)x;
+  if (i > SOFT_N - 1) i = SOFT_N - 1;
+  return fmaf(x - (float)i, p->soft_s[i], p->soft_g[i]);
 }
 
 static void flex_terms(const vso_pocket* p, int key, const mat3d* R, const double* t,
@@ -812,8 +827,19 @@ static void dock_one(const vso_pocket* p, const lig_t* L, uint64_t seed, uint32_
     float* fa = (float*)malloc(sizeof(float) * (size_t)N);
     float* wa = (float*)malloc(sizeof(float) * (size_t)N);
     unsigned char* inm = (unsigned char*)malloc((size_t)N);
-    const int keyt = prm->polish >= 1 && p->grid; /* search atom terms: the sweep key (§3.4) */
-    for (int i = 0; i < N; ++i) flex_terms(p, keyt, &RS, ptd, &y[3 * i], &fa[i], &wa[i]);
+    const int keyt = prm->polish >= 1 && p->grid; /* the FP32 search on the sweep key (§3.4) */
+    float GF[12]; /* the pose's grid frame rows (A = R ih | u = (t - o) ih) */
+    {
+      const float ih = p->inv_h;
+      const mat3 Rq = quat_mat(pq[0], pq[1], pq[2], pq[3]);
+      const float g0[3] = {p->gx0, p->gy0, p->gz0};
+      for (int r = 0; r < 3; ++r) {
+        for (int c = 0; c < 3; ++c) GF[4 * r + c] = Rq.m[3 * r + c] * ih;
+        GF[4 * r + 3] = (pt[r] - g0[r]) * ih;
+      }
+    }
+    if (!keyt)
+      for (int i = 0; i < N; ++i) flex_terms(p, keyt, &RS, ptd, &y[3 * i], &fa[i], &wa[i]);
     float S = 0.0f;
     const int do_flex = T > 0 && prm->flex_passes > 0;
     const int steps0 = do_flex ? prm->flex_passes * T : 1;
@@ -860,8 +886,33 @@ static void dock_one(const vso_pocket* p, const lig_t* L, uint64_t seed, uint32_
             }
             if (thn >= PI_F) thn = thn - TWO_PI_F;
           }
-          mat3d M = flex_mat(&y[3 * L->a[j]], &y[3 * L->b[j]], thn, tho, L->inv_len[j]);
           const double* o = &y[3 * L->a[j]];
+          if (keyt) { /* FP32 candidate rotation about the state's axis (§3.4) */
+            const double* bb = &y[3 * L->b[j]];
+            const float of[3] = {(float)o[0], (float)o[1], (float)o[2]};
+            float hf = 0.5f * (thn - tho);
+            if (hf > HALF_PI_F) hf = hf - PI_F;
+            else if (hf < -HALF_PI_F) hf = hf + PI_F;
+            float sn, cs;
+            vso_sincos(hf, &sn, &cs);
+            const float ks = sn * (float)L->inv_len[j];
+            const mat3 Mf = quat_mat(cs, (float)(bb[0] - o[0]) * ks, (float)(bb[1] - o[1]) * ks,
+                                     (float)(bb[2] - o[2]) * ks);
+            for (int q2 = 0; q2 < m; ++q2) {
+              const int idx = mv[q2], hh = q2 & 1;
+              const float vf[3] = {(float)(y[3 * idx] - o[0]), (float)(y[3 * idx + 1] - o[1]),
+                                   (float)(y[3 * idx + 2] - o[2])};
+              float yf[3], g[3];
+              for (int r = 0; r < 3; ++r)
+                yf[r] = fmaf(Mf.m[3 * r], vf[0], fmaf(Mf.m[3 * r + 1], vf[1], fmaf(Mf.m[3 * r + 2], vf[2], of[r])));
+              for (int r = 0; r < 3; ++r)
+                g[r] = fmaf(GF[4 * r], yf[0], fmaf(GF[4 * r + 1], yf[1], fmaf(GF[4 * r + 2], yf[2], GF[4 * r + 3])));
+              fm[hh] = fm[hh] + key_at_grid(p, g);
+              for (int k = 0; k < N; ++k)
+                if (!inm[k]) pc[hh] = pc[hh] + pair_f32(p, yf, &y[3 * k]);
+            }
+          } else {
+          mat3d M = flex_mat(&y[3 * L->a[j]], &y[3 * L->b[j]], thn, tho, L->inv_len[j]);
           for (int q2 = 0; q2 < m; ++q2) {
             const int idx = mv[q2], hh = q2 & 1;
             double v[3] = {y[3 * idx] - o[0], y[3 * idx + 1] - o[1], y[3 * idx + 2] - o[2]}, yn[3];
@@ -873,6 +924,7 @@ static void dock_one(const vso_pocket* p, const lig_t* L, uint64_t seed, uint32_
             for (int k = 0; k < N; ++k)
               if (!inm[k])
                 pc[hh] = pc[hh] + (tabp ? pair_tab_f(p, yn, &y[3 * k]) : pair_d(p, yn, &y[3 * k]));
+          }
           }
         }
         const float Sa = (fb + (fm[0] + fm[1])) - p->lam * ((pb + (pc[0] + pc[1])) + (wb + (wm[0] + wm[1])));
@@ -887,7 +939,7 @@ static void dock_one(const vso_pocket* p, const lig_t* L, uint64_t seed, uint32_
           const int idx = mv[q2];
           double v[3] = {y[3 * idx] - o[0], y[3 * idx + 1] - o[1], y[3 * idx + 2] - o[2]};
           apply_d(&M, v, o, &y[3 * idx]);
-          flex_terms(p, keyt, &RS, ptd, &y[3 * idx], &fa[idx], &wa[idx]);
+          if (!keyt) flex_terms(p, keyt, &RS, ptd, &y[3 * idx], &fa[idx], &wa[idx]);
         }
         th[j] = best_th;
       }

@@ -21,6 +21,7 @@ constexpr unsigned long long kGolden = 0x9e3779b97f4a7c15ull;
 constexpr double kPiD = 3.14159265358979323846;
 constexpr double kHalfPiD = 1.57079632679489661923;
 constexpr float kPiF = 3.14159274f;     // (float)pi, rounds up
+constexpr float kHalfPiF = 1.57079637f;  // (float)(pi / 2)
 constexpr float kTwoPiF = 6.28318548f;  // (float)(2 pi)
 
 // ------------------------------------------------------------------ RNG --
@@ -546,9 +547,8 @@ static __device__ __forceinline__ float eval_key(const PocketDev& pk, const floa
 // the sweep key of one point in world coordinates (flex search with the
 // polish, SWEEP_V1.md §3.4): g = (x - o) / h, then the key map's cell
 // polynomial (or the linear wall off the grid), as in eval_key
-__device__ __forceinline__ float key_at(float x, float y, float z) {
+__device__ __forceinline__ float key_at_grid(float gx, float gy, float gz) {
   const GridDev& g = c_pk.grid;
-  const float gx = (x - g.ox) * g.inv_h, gy = (y - g.oy) * g.inv_h, gz = (z - g.oz) * g.inv_h;
   const float fx = floorf(gx), fy = floorf(gy), fz = floorf(gz);
   const int ix = static_cast<int>(fx), iy = static_cast<int>(fy), iz = static_cast<int>(fz);
   const bool in = static_cast<unsigned>(ix) <= static_cast<unsigned>(g.nx - 2) &&
@@ -560,6 +560,11 @@ __device__ __forceinline__ float key_at(float x, float y, float z) {
   const float tx1 = gx - fx, ty1 = gy - fy, tz1 = gz - fz;
   return fmaf(fmaf(fmaf(b.w, tz1, a.w), ty1, fmaf(b.y, tz1, a.y)), tx1,
               fmaf(fmaf(b.z, tz1, a.z), ty1, fmaf(b.x, tz1, a.x)));
+}
+
+__device__ __forceinline__ float key_at(float x, float y, float z) {
+  const GridDev& g = c_pk.grid;
+  return key_at_grid((x - g.ox) * g.inv_h, (y - g.oy) * g.inv_h, (z - g.oz) * g.inv_h);
 }
 
 // flex search atom terms with the polish in grid mode: f = K(x) (the key

@@ -310,16 +310,30 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
   const WarpSmem s = dock_smem(d);
   const int a_lane = lane & 15;
   const int h = lane >> 4;
+  // the FP32 search (polish >= 1, grid mode; SWEEP_V1.md §3.4) scores each
+  // candidate's moved atoms on the sweep key in the pose's grid frame and
+  // needs no per-atom caches (the base sums are not part of its score)
+  constexpr bool kSearch32 = kTab && kGrid;
   if (lane == 0) {
-    const Mat3d RD = det_pose_mat_d(P->q[0], P->q[1], P->q[2], P->q[3]);
-    double* pm = s.pose;
-    pm[0] = RD.m00; pm[1] = RD.m01; pm[2] = RD.m02;
-    pm[3] = RD.m10; pm[4] = RD.m11; pm[5] = RD.m12;
-    pm[6] = RD.m20; pm[7] = RD.m21; pm[8] = RD.m22;
-    pm[9] = P->t[0]; pm[10] = P->t[1]; pm[11] = P->t[2];
+    if (kSearch32) {
+      const GridDev& g = c_pk.grid;
+      const float ih = g.inv_h;
+      const Mat3 R = det_quat_mat(P->q[0], P->q[1], P->q[2], P->q[3]);
+      float4* gf = reinterpret_cast<float4*>(s.pose);
+      gf[0] = make_float4(R.m00 * ih, R.m01 * ih, R.m02 * ih, (P->t[0] - g.ox) * ih);
+      gf[1] = make_float4(R.m10 * ih, R.m11 * ih, R.m12 * ih, (P->t[1] - g.oy) * ih);
+      gf[2] = make_float4(R.m20 * ih, R.m21 * ih, R.m22 * ih, (P->t[2] - g.oz) * ih);
+    } else {
+      const Mat3d RD = det_pose_mat_d(P->q[0], P->q[1], P->q[2], P->q[3]);
+      double* pm = s.pose;
+      pm[0] = RD.m00; pm[1] = RD.m01; pm[2] = RD.m02;
+      pm[3] = RD.m10; pm[4] = RD.m11; pm[5] = RD.m12;
+      pm[6] = RD.m20; pm[7] = RD.m21; pm[8] = RD.m22;
+      pm[9] = P->t[0]; pm[10] = P->t[1]; pm[11] = P->t[2];
+    }
   }
   __syncwarp();
-  for (int i = lane; i < N; i += 32) {
+  for (int i = lane; !kSearch32 && i < N; i += 32) {
     const double4 v = s.ys[i];
     flex_terms<kGrid, kTab>(s.pose, v.x, v.y, v.z, &s.fa[i], &s.wa[i]);
   }
@@ -414,6 +428,50 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
         th_new = v;
       }
       const double4 o = s.ys[ax.x], b = s.ys[ax.y];
+      if constexpr (kSearch32) {
+        // FP32 candidate rotation about the state's axis by th_new - th_old
+        const float ofx = static_cast<float>(o.x), ofy = static_cast<float>(o.y),
+                    ofz = static_cast<float>(o.z);
+        float hh = 0.5f * (th_new - th_old);
+        if (hh > kHalfPiF) hh = hh - kPiF;
+        else if (hh < -kHalfPiF) hh = hh + kPiF;
+        float sn, cs;
+        det_sincos(hh, &sn, &cs);
+        const float ks = sn * static_cast<float>(s.axl[j]);
+        const Mat3 Mf = det_quat_mat(cs, static_cast<float>(b.x - o.x) * ks,
+                                     static_cast<float>(b.y - o.y) * ks,
+                                     static_cast<float>(b.z - o.z) * ks);
+        const float4* gf = reinterpret_cast<const float4*>(s.pose);
+        for (int q2 = h; q2 < m; q2 += 2) {
+          const double4 v = s.ys[s.mov[ax.z + q2]];
+          const float vx = static_cast<float>(v.x - o.x), vy = static_cast<float>(v.y - o.y),
+                      vz = static_cast<float>(v.z - o.z);
+          const float fx = fmaf(Mf.m00, vx, fmaf(Mf.m01, vy, fmaf(Mf.m02, vz, ofx)));
+          const float fy = fmaf(Mf.m10, vx, fmaf(Mf.m11, vy, fmaf(Mf.m12, vz, ofy)));
+          const float fz = fmaf(Mf.m20, vx, fmaf(Mf.m21, vy, fmaf(Mf.m22, vz, ofz)));
+          const float4 r0 = gf[0], r1 = gf[1], r2 = gf[2];
+          fm = fm + key_at_grid(fmaf(r0.x, fx, fmaf(r0.y, fy, fmaf(r0.z, fz, r0.w))),
+                                fmaf(r1.x, fx, fmaf(r1.y, fy, fmaf(r1.z, fz, r1.w))),
+                                fmaf(r2.x, fx, fmaf(r2.y, fy, fmaf(r2.z, fz, r2.w))));
+          if constexpr (kPacked) {
+            const float4* part = reinterpret_cast<const float4*>(s.y0);
+            float4 yk = part[0];
+            for (int p = 0; p < np; ++p) {
+              const float4 yn = part[p + 1];
+              pc = pc + pair_term_f(tab, fx - yk.x, fy - yk.y, fz - yk.z, nact);
+              yk = yn;
+            }
+          } else {
+            for (int k = 0; k < N; ++k)
+              if (!in_mask(mk, k)) {
+                const double4 yk = s.ys[k];
+                pc = pc + pair_term_f(tab, fx - static_cast<float>(yk.x),
+                                      fy - static_cast<float>(yk.y),
+                                      fz - static_cast<float>(yk.z), nact);
+              }
+          }
+        }
+      } else {
       const Mat3d M = flex_mat(o.x, o.y, o.z, b.x, b.y, b.z, th_new, th_old, s.axl[j]);
       // partners: the atoms outside moving_j, walked as set bits of the
       // complemented mask (ascending k, same trip count in both halves)
@@ -470,6 +528,7 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
           }
         }
       }
+      }
     }
     const float fm2 = __shfl_xor_sync(kFull, fm, 16);
     const float wm2 = __shfl_xor_sync(kFull, wm, 16);
@@ -497,7 +556,7 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
         double4 v = s.ys[idx];
         det_apply_d(M, v.x - o.x, v.y - o.y, v.z - o.z, o.x, o.y, o.z, &v.x, &v.y, &v.z);
         s.ys[idx] = v;
-        flex_terms<kGrid, kTab>(s.pose, v.x, v.y, v.z, &s.fa[idx], &s.wa[idx]);
+        if (!kSearch32) flex_terms<kGrid, kTab>(s.pose, v.x, v.y, v.z, &s.fa[idx], &s.wa[idx]);
       }
       if (lane == 0) s.theta[j] = th_win;
     }
