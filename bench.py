@@ -224,6 +224,10 @@ AXIS_FLOP = 81           # flex rotation: half angle 3, sincos_d 44, quaternion 
 TERMS_FLOP_SEARCH = 41   # FP64 transform 18 + grid frame 6 + fractions 3 + 7 FMAs 14
 PAIR_ACTIVE_FLOP_TAB = 4  # scale 1, fraction 1, interpolation FMA 2
 PAIR_ACTIVE_XU_TAB = 3    # FP64->FP32, float->int, int->float
+# the FP32 search in grid mode (no base sums, no per-atom caches)
+AXIS_FLOP_F32 = 50       # half angle 2, sincos 28, scale 4, quaternion matrix 16
+MOVE_FLOP_F32 = 56       # difference 3, rotation 18, grid frame 18, fractions 3, 7 FMAs 14
+PAIR_TEST_FLOP_F32 = 8   # difference 3, norm 5
 MOVE_FLOP = 18           # FP64 rotation of one moving atom
 
 
@@ -248,16 +252,20 @@ def algorithmic_work(lib, prm, stats, grid: bool, n_steric: int):
     m = lib.moving_count.astype(np.float64)
     Nt = np.repeat(N, T)                       # ligand atom count per torsion
     pnc = m * (m - 1) / 2 + (Nt - m) * (Nt - m - 1) / 2
-    step_flop = (2 * Nt + PAIR_TEST_FLOP * pnc
-                 + A * (AXIS_FLOP + m * (MOVE_FLOP + terms_flop) + PAIR_TEST_FLOP * m * (Nt - m)))
+    if search and grid:  # FP32 search: candidates only (SWEEP_V1.md §3.4)
+        step_flop = A * (AXIS_FLOP_F32 + m * MOVE_FLOP_F32 + PAIR_TEST_FLOP_F32 * m * (Nt - m))
+    else:
+        step_flop = (2 * Nt + PAIR_TEST_FLOP * pnc
+                     + A * (AXIS_FLOP + m * (MOVE_FLOP + terms_flop) + PAIR_TEST_FLOP * m * (Nt - m)))
     step_xu = A * m * TERMS_XU
     flex_flop = float(np.sum(step_flop)) * R * F
     flex_xu = float(np.sum(step_xu)) * R * F
     P = N * (N - 1) / 2
     no_flex = (T == 0) | (F == 0)
     flex_flop += float(np.sum(np.where(no_flex, R * (2 * N + PAIR_TEST_FLOP * P), 0.0)))
-    flex_flop += float(np.sum(R * N * terms_flop)) + stats["active_pairs"] * pair_flop
-    flex_xu += stats["active_pairs"] * pair_xu + R * float(np.sum(N)) * TERMS_XU
+    caches = 0.0 if (search and grid) else 1.0  # per-atom term caches at the flex start
+    flex_flop += caches * float(np.sum(R * N * terms_flop)) + stats["active_pairs"] * pair_flop
+    flex_xu += stats["active_pairs"] * pair_xu + caches * R * float(np.sum(N)) * TERMS_XU
     chain_flop = float(np.sum(np.add.reduceat(np.r_[AXIS_FLOP + MOVE_FLOP * m, 0.0],
                                               np.minimum(to[:-1], len(m))) * (T > 0))) * R
     atom_f = ATOM_FLOP_KEY if grid else 31 + 11 * n_steric
