@@ -87,6 +87,66 @@ def test_dock_bit_exact_vs_oracle(V, engine, lib200, pocket_json, grid):
     _assert_same(res, ora, prm.keep_top)
 
 
+@pytest.mark.parametrize("polish", [0, 2])
+@pytest.mark.parametrize("grid", [0.0, 0.4])
+def test_dock_polish_modes_bit_exact(V, engine, lib200, pocket_json, grid, polish):
+    """polish 0 (the exact flex score is the restart's score) and polish 2
+    (fine torsion pass) against the oracle, bit for bit."""
+    lib, _ = lib200
+    sub = lib.subset(range(0, len(lib), 2))
+    sub.seeds = lib.seeds[0::2]
+    pocket = V.parse_pocket_json(pocket_json)
+    prm = _params(V, polish=polish)
+    engine.set_pocket(pocket, grid_spacing=grid)
+    res = engine.dock_host(sub, prm)
+    ora = _oracle_dock(pocket, sub, prm, grid)
+    _assert_same(res, ora, prm.keep_top)
+
+
+@pytest.mark.parametrize("grid", [0.0, 0.4])
+def test_fused_mode_matches_staged(V, engine, lib200, pocket_json, grid, monkeypatch):
+    """The single-launch fused kernel (VSCREEN_DOCK_MODE=fused, kept for
+    A/B) gives the staged kernels' results bit for bit, polish 0 and 1."""
+    lib, _ = lib200
+    sub = lib.subset(range(0, 60))
+    sub.seeds = lib.seeds[:60]
+    pocket = V.parse_pocket_json(pocket_json)
+    engine.set_pocket(pocket, grid_spacing=grid)
+    for polish in (0, 1):
+        prm = _params(V, polish=polish)
+        staged = engine.dock_host(sub, prm)
+        monkeypatch.setenv("VSCREEN_DOCK_MODE", "fused")
+        fused = engine.dock_host(sub, prm)
+        monkeypatch.delenv("VSCREEN_DOCK_MODE")
+        np.testing.assert_array_equal(staged.keys, fused.keys)
+        np.testing.assert_array_equal(staged.best.view(np.uint32), fused.best.view(np.uint32))
+        np.testing.assert_array_equal(_bits(staged.surv), _bits(fused.surv))
+
+
+def test_polish0_scores_match_reference(V, engine, lib200, pocket_json):
+    """Without the polish the restart's score is the flex's exact score:
+    emitted poses re-scored by the reference FP64 scorer within 1e-5."""
+    R = need_ref()
+    lib, smis = lib200
+    pocket = V.parse_pocket_json(pocket_json)
+    engine.set_pocket(pocket)
+    res = engine.dock_host(lib, _params(V, polish=0))
+    rp = R.RefPocket(pocket_json)
+    ao, _, _ = lib.offsets()
+    worst, n = 0.0, 0
+    for i in range(0, len(lib), 5):
+        rl = R.RefLigand(smis[i])
+        rl.set_coords(lib.coords[ao[i]:ao[i + 1]])
+        for pose in res.poses(i, int(lib.n_tors[i]), "surv"):
+            t, q = np.array(pose.translation, np.float64), np.array(pose.rotation, np.float64)
+            th = np.array(pose.torsions, np.float64)
+            g = rl.geometric_score(rp, t, q, th)
+            worst = max(worst, abs(g - pose.geometric_score) / max(abs(g), 1.0))
+            n += 1
+    assert n > 20
+    assert worst <= TOL, worst
+
+
 def test_grid_maps_bit_exact(V, engine, pocket_json):
     from oracle import sweep
     pocket = V.parse_pocket_json(pocket_json)
