@@ -139,6 +139,7 @@ struct SweepKnobs {
   int flex_angles = 16;
   int flex_passes = 2;
   uint64_t rotation_seed = 0x5EED;
+  int polish = 1;  // 0 off, 1 rigid compass, 2 + fine torsion pass (SWEEP_V1.md §3.5)
 };
 
 namespace detail {
@@ -302,6 +303,7 @@ inline std::vector<Pose> dock(Device& dev, const Conformer& conf, const TorsionT
   prm.write_all_poses = 1;
   prm.min_score = -1e30;
   prm.rotation_seed = knobs.rotation_seed;
+  prm.polish = knobs.polish;
   const std::size_t T = topo.axes.size();
   float best = 0.0f;
   int32_t n_kept = 0, n_surv = 0;
