@@ -274,7 +274,11 @@ int pack_library(vs_handle* h, const vs_library* L, const vs_size_class* classes
   P.id_rank.assign(n, 0u);
   P.cls.assign(n, -1);
   P.tors_off.assign(n + 1, 0);
-  // pass 1 (sequential, O(n)): counts, offsets, classes, LPT cost
+  const auto pt0 = std::chrono::steady_clock::now();
+  // pass 1: a sequential scan validates the counts (the lowest failing
+  // ligand's error, as a sequential pass reports it) and lays out the atom
+  // and torsion offsets; threads then take the moving-set sizes, classes,
+  // seeds and LPT costs; a second scan lays out the moving-list offsets
   std::vector<long> cost(n, 0), aoff(n + 1, 0), moff(n + 1, 0), msrc(n + 1, 0), toff(n + 1, 0);
   for (int i = 0; i < n; ++i) {
     const int N = L->n_atoms[i], T = L->n_tors[i];
@@ -282,24 +286,43 @@ int pack_library(vs_handle* h, const vs_library* L, const vs_size_class* classes
     if (N > kMaxAtoms || T > kMaxTors)
       return fail(h, VS_ERR_CAPACITY, "ligand " + std::to_string(i) + " exceeds GPU limits");
     if (T < 0) return fail(h, VS_ERR_INVALID_ARGUMENT, "negative torsion count");
-    long mv = 0;
-    for (int j = 0; j < T; ++j) mv += L->moving_count[toff[i] + j];
     aoff[i + 1] = aoff[i] + N;
     toff[i + 1] = toff[i] + T;
-    msrc[i + 1] = msrc[i] + mv;
-    moff[i + 1] = moff[i] + static_cast<long>(align16z(static_cast<size_t>(mv)));
-    P.tors_off[i] = toff[i];
-    P.seeds[i] = L->seeds ? L->seeds[i] : 0ull;
-    P.id_rank[i] = L->id_rank ? L->id_rank[i] : static_cast<unsigned>(i);
-    const int rot = L->rot_bonds ? L->rot_bonds[i] : T;
-    if (classes && nc > 0) {
-      P.cls[i] = vs_size_class_of(N, rot, classes, nc);
-      if (P.cls[i] < 0) P.cls[i] = -1;
-    } else {
-      P.cls[i] = N <= 16 ? 0 : N <= 32 ? 1 : N <= 48 ? 2 : N <= 64 ? 3 : N <= 96 ? 4 : 5;
+  }
+  std::vector<long> mvn(n, 0);
+  const int nth1 = std::max(1, std::min<int>(32, static_cast<int>(std::thread::hardware_concurrency())));
+  auto scan = [&](int t) {
+    const int lo = static_cast<int>(static_cast<long>(n) * t / nth1);
+    const int hi = static_cast<int>(static_cast<long>(n) * (t + 1) / nth1);
+    for (int i = lo; i < hi; ++i) {
+      const int N = L->n_atoms[i], T = L->n_tors[i];
+      long mv = 0;
+      for (int j = 0; j < T; ++j) mv += L->moving_count[toff[i] + j];
+      mvn[i] = mv;
+      P.tors_off[i] = toff[i];
+      P.seeds[i] = L->seeds ? L->seeds[i] : 0ull;
+      P.id_rank[i] = L->id_rank ? L->id_rank[i] : static_cast<unsigned>(i);
+      const int rot = L->rot_bonds ? L->rot_bonds[i] : T;
+      if (classes && nc > 0) {
+        P.cls[i] = vs_size_class_of(N, rot, classes, nc);
+        if (P.cls[i] < 0) P.cls[i] = -1;
+      } else {
+        P.cls[i] = N <= 16 ? 0 : N <= 32 ? 1 : N <= 48 ? 2 : N <= 64 ? 3 : N <= 96 ? 4 : 5;
+      }
+      const long pairs = static_cast<long>(N) * (N - 1) / 2;
+      cost[i] = 256L * N + 32L * T * (N + pairs + mv);
     }
-    const long pairs = static_cast<long>(N) * (N - 1) / 2;
-    cost[i] = 256L * N + 32L * T * (N + pairs + mv);
+  };
+  if (nth1 == 1 || n < 4096) {
+    for (int t = 0; t < nth1; ++t) scan(t);
+  } else {
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nth1; ++t) pool.emplace_back(scan, t);
+    for (auto& th : pool) th.join();
+  }
+  for (int i = 0; i < n; ++i) {
+    msrc[i + 1] = msrc[i] + mvn[i];
+    moff[i + 1] = moff[i] + static_cast<long>(align16z(static_cast<size_t>(mvn[i])));
   }
   if (!P.meta.resize(std::max(n, 1)) || !P.mov.resize(std::max(n, 1)) ||
       !P.atoms.resize(std::max<long>(aoff[n], 1)) || !P.axes.resize(std::max<long>(toff[n], 1)) ||
@@ -308,6 +331,7 @@ int pack_library(vs_handle* h, const vs_library* L, const vs_size_class* classes
   if (aoff[n] == 0) P.atoms[0] = double4{0, 0, 0, 0};
   if (toff[n] == 0) P.axes[0] = int4{0, 0, 0, 0};
   if (moff[n] == 0) std::memset(P.moving.data(), 0, 16);
+  const auto pt1 = std::chrono::steady_clock::now();
   // pass 2 (threads over ligand ranges): fill + validate; the error of the
   // lowest failing ligand is the one reported (same as a sequential pass)
   const int nth = std::max(1, std::min<int>(32, static_cast<int>(std::thread::hardware_concurrency())));
@@ -372,23 +396,29 @@ int pack_library(vs_handle* h, const vs_library* L, const vs_size_class* classes
   lpt.reserve(n);
   for (int i = 0; i < n; ++i)
     if (P.cls[i] >= 0) lpt.push_back(i);
+  const auto pt2 = std::chrono::steady_clock::now();
   lpt_sort(lpt, cost);
+  const auto pt3 = std::chrono::steady_clock::now();
   const int ncls = (classes && nc > 0) ? nc : 6;
   P.order.clear();
   P.order.reserve(2 * lpt.size() + 1);
   P.buckets.clear();
-  for (int c = 0; c < ncls; ++c) {
-    Bucket b;
-    b.start = static_cast<int>(P.order.size());
-    for (int i : lpt) {
-      if (P.cls[i] != c) continue;
-      b.nmax = std::max(b.nmax, P.meta[i].y);
-      b.tmax = std::max(b.tmax, P.meta[i].w);
-      b.mvmax = std::max(b.mvmax, P.mov[i].y);
-      P.order.push_back(i);
+  {
+    // one pass over the LPT order into per-class lists (LPT order kept)
+    std::vector<std::vector<int>> per(static_cast<std::size_t>(ncls));
+    for (int i : lpt) per[static_cast<std::size_t>(P.cls[i])].push_back(i);
+    for (int c = 0; c < ncls; ++c) {
+      Bucket b;
+      b.start = static_cast<int>(P.order.size());
+      for (int i : per[static_cast<std::size_t>(c)]) {
+        b.nmax = std::max(b.nmax, P.meta[i].y);
+        b.tmax = std::max(b.tmax, P.meta[i].w);
+        b.mvmax = std::max(b.mvmax, P.mov[i].y);
+        P.order.push_back(i);
+      }
+      b.count = static_cast<int>(P.order.size()) - b.start;
+      if (b.count > 0) P.buckets.push_back(b);
     }
-    b.count = static_cast<int>(P.order.size()) - b.start;
-    if (b.count > 0) P.buckets.push_back(b);
   }
   P.all = Bucket{};
   P.all.start = static_cast<int>(P.order.size());
@@ -400,6 +430,14 @@ int pack_library(vs_handle* h, const vs_library* L, const vs_size_class* classes
   }
   P.all.count = static_cast<int>(lpt.size());
   if (P.order.empty()) P.order.push_back(0);
+  if (const char* e = std::getenv("VSCREEN_UPLOAD_TIMING"); e && e[0] == '1') {
+    const auto pt4 = std::chrono::steady_clock::now();
+    auto ms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+      return std::chrono::duration<double, std::milli>(b - a).count();
+    };
+    std::fprintf(stderr, "pack_library: pass1 %.2f ms, fill %.2f ms, lpt sort %.2f ms, buckets %.2f ms\n",
+                 ms(pt0, pt1), ms(pt1, pt2), ms(pt2, pt3), ms(pt3, pt4));
+  }
   return VS_OK;
 }
 
