@@ -461,12 +461,6 @@ static float key_at_grid(const vso_pocket* p, const float* g) {
   return -(p->lam * ((p->r - w) * 10.0f));
 }
 
-static float key_at(const vso_pocket* p, const float* x) {
-  const float g[3] = {(x[0] - p->gx0) * p->inv_h, (x[1] - p->gy0) * p->inv_h,
-                      (x[2] - p->gz0) * p->inv_h};
-  return key_at_grid(p, g);
-}
-
 /* cross pair of the FP32 search: FP32 moved atom vs the FP32-rounded partner */
 static float pair_f32(const vso_pocket* p, const float* a, const double* b) {
   const float d2 = n2(a[0] - (float)b[0], a[1] - (float)b[1], a[2] - (float)b[2]);
@@ -475,16 +469,6 @@ static float pair_f32(const vso_pocket* p, const float* a, const double* b) {
   int i = (int)x;
   if (i > SOFT_N - 1) i = SOFT_N - 1;
   return fmaf(x - (float)i, p->soft_s[i], p->soft_g[i]);
-}
-
-static void flex_terms(const vso_pocket* p, int key, const mat3d* R, const double* t,
-                       const double* y, float* f, float* w) {
-  if (!key) { atom_terms(p, R, t, y, f, w, NULL); return; }
-  double v[3];
-  apply_d(R, y, t, v);
-  const float x[3] = {(float)v[0], (float)v[1], (float)v[2]};
-  *f = key_at(p, x);
-  *w = 0.0f;
 }
 
 /* pair clash softplus from FP64 coordinates (dock.cpp:86-97) */
@@ -839,7 +823,7 @@ static void dock_one(const vso_pocket* p, const lig_t* L, uint64_t seed, uint32_
       }
     }
     if (!keyt)
-      for (int i = 0; i < N; ++i) flex_terms(p, keyt, &RS, ptd, &y[3 * i], &fa[i], &wa[i]);
+      for (int i = 0; i < N; ++i) atom_terms(p, &RS, ptd, &y[3 * i], &fa[i], &wa[i], NULL);
     float S = 0.0f;
     const int do_flex = T > 0 && prm->flex_passes > 0;
     const int steps0 = do_flex ? prm->flex_passes * T : 1;
@@ -918,7 +902,7 @@ static void dock_one(const vso_pocket* p, const lig_t* L, uint64_t seed, uint32_
             double v[3] = {y[3 * idx] - o[0], y[3 * idx + 1] - o[1], y[3 * idx + 2] - o[2]}, yn[3];
             apply_d(&M, v, o, yn);
             float fi, wi;
-            flex_terms(p, keyt, &RS, ptd, yn, &fi, &wi);
+            atom_terms(p, &RS, ptd, yn, &fi, &wi, NULL);
             fm[hh] = fm[hh] + fi;
             wm[hh] = wm[hh] + wi;
             for (int k = 0; k < N; ++k)
@@ -939,7 +923,7 @@ static void dock_one(const vso_pocket* p, const lig_t* L, uint64_t seed, uint32_
           const int idx = mv[q2];
           double v[3] = {y[3 * idx] - o[0], y[3 * idx + 1] - o[1], y[3 * idx + 2] - o[2]};
           apply_d(&M, v, o, &y[3 * idx]);
-          if (!keyt) flex_terms(p, keyt, &RS, ptd, &y[3 * idx], &fa[idx], &wa[idx]);
+          if (!keyt) atom_terms(p, &RS, ptd, &y[3 * idx], &fa[idx], &wa[idx], NULL);
         }
         th[j] = best_th;
       }

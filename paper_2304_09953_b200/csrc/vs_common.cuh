@@ -544,9 +544,9 @@ static __device__ __forceinline__ float eval_key(const PocketDev& pk, const floa
   return (fe + fo) - c_pk.lam * (we + wo);
 }
 
-// the sweep key of one point in world coordinates (flex search with the
-// polish, SWEEP_V1.md §3.4): g = (x - o) / h, then the key map's cell
-// polynomial (or the linear wall off the grid), as in eval_key
+// the sweep key at grid coordinates g (the FP32 flex search, SWEEP_V1.md
+// §3.4): the key map's cell polynomial, or the linear wall off the grid,
+// as in eval_key
 __device__ __forceinline__ float key_at_grid(float gx, float gy, float gz) {
   const GridDev& g = c_pk.grid;
   const float fx = floorf(gx), fy = floorf(gy), fz = floorf(gz);
@@ -560,23 +560,6 @@ __device__ __forceinline__ float key_at_grid(float gx, float gy, float gz) {
   const float tx1 = gx - fx, ty1 = gy - fy, tz1 = gz - fz;
   return fmaf(fmaf(fmaf(b.w, tz1, a.w), ty1, fmaf(b.y, tz1, a.y)), tx1,
               fmaf(fmaf(b.z, tz1, a.z), ty1, fmaf(b.x, tz1, a.x)));
-}
-
-__device__ __forceinline__ float key_at(float x, float y, float z) {
-  const GridDev& g = c_pk.grid;
-  return key_at_grid((x - g.ox) * g.inv_h, (y - g.oy) * g.inv_h, (z - g.oz) * g.inv_h);
-}
-
-// flex search atom terms with the polish in grid mode: f = K(x) (the key
-// map holds S - lam W, so the wall is inside f) and w = 0
-__device__ __forceinline__ void atom_terms_key(const double* pm, double yx, double yy, double yz,
-                                               float* f, float* w) {
-  const volatile double* v = pm;
-  const double x = fma(v[0], yx, fma(v[1], yy, fma(v[2], yz, v[9])));
-  const double y = fma(v[3], yx, fma(v[4], yy, fma(v[5], yz, v[10])));
-  const double z = fma(v[6], yx, fma(v[7], yy, fma(v[8], yz, v[11])));
-  *f = key_at(static_cast<float>(x), static_cast<float>(y), static_cast<float>(z));
-  *w = 0.0f;
 }
 
 // out-of-line copy for the fused kernel (one shared body for both sweep loops)

@@ -291,17 +291,6 @@ static __device__ VS_PHASE int sweep_phase(const PocketDev& pk, const Dims d,
 // + moved part(candidate: moving_j atoms rotated about the state's axis j
 // and their cross pairs; lane pair (a, h), lane h takes moving positions
 // = h mod 2).  Returns the score of the final state.
-// atom terms of the flex: exact (field + wall softplus) or, for the search
-// with the polish in grid mode, the sweep key (SWEEP_V1.md §3.4)
-template <int kGrid, bool kTab>
-static __device__ __forceinline__ void flex_terms(const double* pm, double yx, double yy,
-                                                  double yz, float* f, float* w) {
-  if (kTab && kGrid)
-    atom_terms_key(pm, yx, yy, yz, f, w);
-  else
-    atom_terms_s<kGrid>(pm, yx, yy, yz, f, w);
-}
-
 template <int kGrid, bool kPacked = false, bool kTab = false>
 static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, int N, int T,
                                                 int F, int A, float step, const PoseF* P,
@@ -335,7 +324,7 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
   __syncwarp();
   for (int i = lane; !kSearch32 && i < N; i += 32) {
     const double4 v = s.ys[i];
-    flex_terms<kGrid, kTab>(s.pose, v.x, v.y, v.z, &s.fa[i], &s.wa[i]);
+    atom_terms_s<kGrid>(s.pose, v.x, v.y, v.z, &s.fa[i], &s.wa[i]);
   }
   __syncwarp();
   const bool do_flex = T > 0 && F > 0;
@@ -480,7 +469,7 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
         double yx, yy, yz;
         det_apply_d(M, v.x - o.x, v.y - o.y, v.z - o.z, o.x, o.y, o.z, &yx, &yy, &yz);
         float fi, wi;
-        flex_terms<kGrid, kTab>(s.pose, yx, yy, yz, &fi, &wi);
+        atom_terms_s<kGrid>(s.pose, yx, yy, yz, &fi, &wi);
         fm = fm + fi;
         wm = wm + wi;
         if constexpr (kPacked && kTab) {
@@ -556,7 +545,7 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
         double4 v = s.ys[idx];
         det_apply_d(M, v.x - o.x, v.y - o.y, v.z - o.z, o.x, o.y, o.z, &v.x, &v.y, &v.z);
         s.ys[idx] = v;
-        if (!kSearch32) flex_terms<kGrid, kTab>(s.pose, v.x, v.y, v.z, &s.fa[idx], &s.wa[idx]);
+        if (!kSearch32) atom_terms_s<kGrid>(s.pose, v.x, v.y, v.z, &s.fa[idx], &s.wa[idx]);
       }
       if (lane == 0) s.theta[j] = th_win;
     }
