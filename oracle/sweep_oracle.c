@@ -623,6 +623,7 @@ static uint32_t orderable(float f) {
 #define POLISH_ANG_MAX 0.5625f  /* expansion cap */
 #define POLISH_ITERS 8
 #define COMPASS_CANDS 31
+#define LONG_JUMP_ITERS 4
 
 #define TRANS_ITERS 16
 #define TRANS_MIN (1.0f / 64.0f)
@@ -653,7 +654,8 @@ static int rigid_compass(const vso_pocket* p, const lig_t* L, const float* ysf, 
     apply(&R0, c, pt, Cw);
     float bk = -INFINITY, bq[4], bt[3];
     int bl = 0;
-    for (int l = 0; l < COMPASS_CANDS; ++l) {
+    const int ncand = it < LONG_JUMP_ITERS ? COMPASS_CANDS : 25; /* long jumps: first iterations */
+    for (int l = 0; l < ncand; ++l) {
       const int big = l >= 13, huge = l >= 25;
       const int lm = huge ? l - 18 : (big ? l - 12 : l);
       const float a2 = big ? 3.0f * ang : ang;

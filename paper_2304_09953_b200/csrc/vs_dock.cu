@@ -84,13 +84,15 @@ static __device__ VS_PHASE int start_phase(const PocketDev& pk, const Dims d,
 // cz); 7..12 translate by +-sc along x y z; 13..18 rotate by +-3 ang,
 // 19..24 translate by +-2 sc; 25..30 translate by +-12 sc.  Argmax, ties to
 // the lowest lane; l = 0 halves the steps, a winner l >= 13 doubles them
-// while ang < kPolishAngMax.  At most kPolishIters iterations.
+// while ang < kPolishAngMax.  At most kPolishIters iterations; the long
+// jumps only in the first kLongJumpIters.
 constexpr float kPolishAng0 = 0.28125f;
 constexpr float kPolishSc0 = 0.5f;
 constexpr float kPolishAngMin = 0.015625f;
 constexpr float kPolishAngMax = 0.5625f;
 constexpr int kPolishIters = 8;
 constexpr int kCompassLanes = 31;
+constexpr int kLongJumpIters = 4;
 
 template <int kGrid, bool kInl>
 static __device__ __forceinline__ int rigid_compass(const PocketDev& pk, const float4* ysf, int N,
@@ -106,7 +108,10 @@ static __device__ __forceinline__ int rigid_compass(const PocketDev& pk, const f
     det_apply(R0, cx, cy, cz, tx, ty, tz, &Cx, &Cy, &Cz);
     float w2 = qw, x2 = qx, y2 = qy, z2 = qz, u2 = tx, v2 = ty, s2 = tz;
     float key = -INFINITY;
-    if (lane < kCompassLanes) {
+    // the long jumps (lanes 25..30) take part in the first kLongJumpIters
+    // iterations only
+    const int n_lanes = it < kLongJumpIters ? kCompassLanes : 25;
+    if (lane < n_lanes) {
       const bool big = lane >= 13;
       const bool huge = lane >= 25;
       const int lm = huge ? lane - 18 : (big ? lane - 12 : lane);
@@ -137,7 +142,7 @@ static __device__ __forceinline__ int rigid_compass(const PocketDev& pk, const f
       key = kInl ? eval_key<kGrid, 1>(pk, ysf, N, R2, u2, v2, s2)
                  : eval_rigid<kGrid>(pk, ysf, N, R2, u2, v2, s2);
     }
-    int li = lane < kCompassLanes ? lane : 0x7fffffff;
+    int li = lane < n_lanes ? lane : 0x7fffffff;
     for (int off = 16; off > 0; off >>= 1) {
       const float ok = __shfl_xor_sync(kFull, key, off);
       const int oi = __shfl_xor_sync(kFull, li, off);
