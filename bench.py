@@ -86,8 +86,8 @@ CONFIG = {"workload": "C2: 100k synthetic drug-like ligands/GPU (10-40 heavy ato
           "algorithm": "sweep-v1 (docs/SWEEP_V1.md): rotation sweep, long-jump rigid compass, "
                        "FP32 greedy torsion flex search, post compass, exact FP32/FP64 re-score",
           "quality_vs_reference": "mean best survivor rescore (reference FP64 rescore) on 384 C2 "
-                                  "ligands: 45.01 grid / 44.93 analytic vs the reference dock() "
-                                  "ascent 43.75 (profiles/quality_r1p_*.json)"}
+                                  "ligands: 44.99 grid / 44.93 analytic vs the reference dock() "
+                                  "ascent 43.75 (profiles/quality_r1r_*.json)"}
 
 
 CONFIGS = {
