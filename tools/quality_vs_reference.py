@@ -87,10 +87,31 @@ def main():
     rp = R.RefPocket(V.pocket_to_json(pocket))
     ao, _, _ = lib.offsets()
     ligs = [ref_lig(R, lib, i) for i in range(len(lib))]
+    surv = {i: [(np.array(p.translation, np.float64), np.array(p.rotation, np.float64),
+                 np.array(p.torsions, np.float64)) for p in res.poses(i, int(lib.n_tors[i]), "surv")]
+            for i in range(len(lib))}
+    t_ref_gpu = 0.0
+    if "--refine" in sys.argv:
+        # the reference ascent on the GPU from every survivor (refine.py)
+        from paper_2304_09953_b200.refine import ascend_poses
+        pl = [i for i in range(len(lib)) for _ in surv[i]]
+        T3 = [p[0] for i in range(len(lib)) for p in surv[i]]
+        Q4 = [p[1] for i in range(len(lib)) for p in surv[i]]
+        TH = np.concatenate([p[2] for i in range(len(lib)) for p in surv[i]] or [np.zeros(0)])
+        t1 = time.perf_counter()
+        rt, rq, rtor, _, _ = ascend_poses(eng, lib, pl, T3, Q4, TH, max_steps=500)
+        t_ref_gpu = time.perf_counter() - t1
+        k, off = 0, 0
+        for i in range(len(lib)):
+            new = []
+            for p in surv[i]:
+                T = len(p[2])
+                new.append((rt[k], rq[k], rtor[off:off + T]))
+                k += 1
+                off += T
+            surv[i] = new
     for i in range(len(lib)):
-        vals = [ligs[i].rescore(rp, np.array(p.translation, np.float64),
-                                np.array(p.rotation, np.float64), np.array(p.torsions, np.float64))
-                for p in res.poses(i, int(lib.n_tors[i]), "surv")]
+        vals = [ligs[i].rescore(rp, t, q, th) for (t, q, th) in surv[i]]
         if vals:
             ours_ref_scored[i] = max(vals)
     t_ref = c["ref_s"]
@@ -104,6 +125,7 @@ def main():
            "frac_ours_ge_ref": float((d >= -1e-9).mean()) if d.size else None,
            "mean_ours": float(np.nanmean(ours_ref_scored)), "mean_ours_own_score": float(np.nanmean(ours)),
            "mean_ref": float(np.nanmean(ref)), "polish": int(prm.polish),
+           "refined_by_gpu_ascent": "--refine" in sys.argv, "refine_s": round(t_ref_gpu, 3),
            "gpu_s": round(t_gpu, 3), "ref_s": round(t_ref, 2), "ref_threads": threads}
     print(json.dumps(out))
     eng.close()
