@@ -215,6 +215,14 @@ int vs_score_gradient(vs_handle* h, const vs_library* lib, int64_t n_poses,
  * pose order, n_tors of its ligand each. */
 int vs_rescore(vs_handle* h, const vs_library* lib, int64_t n_poses, const int32_t* pose_lig,
                const float* t, const float* q, const float* tors, float* geo, float* resc);
+/* The reference ascent (dock.cpp:168-203: Armijo, step 0.5, shrink 0.5,
+ * c 1e-4, |g| < 1e-6) from the given poses, one warp per pose on the
+ * device, FP64 score_gradient arithmetic; t[3n], q[4n] (w, x, y, z) and the
+ * concatenated torsions are updated in place; score[n] and steps[n]
+ * (accepted steps) optional.  Quality-only refinement. */
+int vs_ascend(vs_handle* h, const vs_library* lib, int64_t n_poses, const int32_t* pose_lig,
+              double* t, double* q, double* tors, int32_t max_steps, double* score,
+              int32_t* steps);
 /* Device time (ms, CUDA events on the launch stream) of the rescore kernels
  * of the last vs_rescore call (-1 before the first). */
 double vs_last_rescore_ms(const vs_handle* h);

@@ -122,6 +122,9 @@ _SIGS = {
     "vs_rescore": (C.c_int, [C.c_void_p, P(vs_library), C.c_int64, P(C.c_int32), P(C.c_float),
                              P(C.c_float), P(C.c_float), P(C.c_float), P(C.c_float)]),
     "vs_last_rescore_ms": (C.c_double, [C.c_void_p]),
+    "vs_ascend": (C.c_int, [C.c_void_p, P(vs_library), C.c_int64, P(C.c_int32), P(C.c_double),
+                            P(C.c_double), P(C.c_double), C.c_int32, P(C.c_double),
+                            P(C.c_int32)]),
     "vs_rng_u64": (C.c_int, [C.c_uint64, P(C.c_uint64), C.c_int32, C.c_int32, P(C.c_uint64)]),
     "vs_random_smiles": (C.c_int, [C.c_uint64, C.c_uint64, C.c_char_p, C.c_int32]),
     "vs_ligand_build": (C.c_int, [C.c_char_p, C.c_uint64, C.c_int32, P(vs_ligand_buf)]),

@@ -240,6 +240,188 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+// ---- the reference ascent (dock.cpp:168-203) per pose, device-resident
+// (refine.ascend_poses_device).  State t (registers), q (registers, as given:
+// the evaluations normalize it like transformed() does), torsions in shared
+// memory; every score and gradient is the arithmetic of vs_grad_kernel.
+
+// score and gradient at (t, q, th); the torsion gradient goes to G
+__device__ double ascent_grad(const LibDev& lib, const GradPocket& pk, int4 meta, int mov_off,
+                              double* th, const double* t, const double* q, double3* y,
+                              double3* x, double3* g, double* gt, double* gq, double* G,
+                              int lane) {
+  const int N = meta.y, T = meta.w;
+  const double n = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+  const double qw = q[0] / n, qx = q[1] / n, qy = q[2] / n, qz = q[3] / n;
+  grad_chain_mv(lib, meta, mov_off, th, y, lane);
+  grad_pose(y, N, qw, qx, qy, qz, t, x, lane);
+  const double s0 = grad_score(pk, x, N, g, lane);
+  __syncwarp();
+  double gtx = 0.0, gty = 0.0, gtz = 0.0, r0 = 0.0, r1 = 0.0, r2 = 0.0, r3 = 0.0;
+  for (int i = lane; i < N; i += 32) {
+    const double3 v = y[i], gi = g[i];
+    gtx += gi.x;
+    gty += gi.y;
+    gtz += gi.z;
+    const double cx = qy * v.z - qz * v.y, cy = qz * v.x - qx * v.z, cz = qx * v.y - qy * v.x;
+    r0 += gi.x * 2.0 * cx + gi.y * 2.0 * cy + gi.z * 2.0 * cz;
+    const double e[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
+    double rj[3];
+    for (int j = 0; j < 3; ++j) {
+      const double ex = e[j][0], ey = e[j][1], ez = e[j][2];
+      const double a1 = ey * v.z - ez * v.y, a2 = ez * v.x - ex * v.z, a3 = ex * v.y - ey * v.x;
+      const double b1 = ey * cz - ez * cy, b2 = ez * cx - ex * cz, b3 = ex * cy - ey * cx;
+      const double c1 = qy * a3 - qz * a2, c2 = qz * a1 - qx * a3, c3 = qx * a2 - qy * a1;
+      const double dvx = 2.0 * qw * a1 + 2.0 * b1 + 2.0 * c1;
+      const double dvy = 2.0 * qw * a2 + 2.0 * b2 + 2.0 * c2;
+      const double dvz = 2.0 * qw * a3 + 2.0 * b3 + 2.0 * c3;
+      rj[j] = gi.x * dvx + gi.y * dvy + gi.z * dvz;
+    }
+    r1 += rj[0];
+    r2 += rj[1];
+    r3 += rj[2];
+  }
+  gt[0] = wsum(gtx);
+  gt[1] = wsum(gty);
+  gt[2] = wsum(gtz);
+  r0 = wsum(r0);
+  r1 = wsum(r1);
+  r2 = wsum(r2);
+  r3 = wsum(r3);
+  const double radial = r0 * qw + r1 * qx + r2 * qy + r3 * qz;
+  gq[0] = r0 - radial * qw;
+  gq[1] = r1 - radial * qx;
+  gq[2] = r2 - radial * qy;
+  gq[3] = r3 - radial * qz;
+  const double h = 1e-5;
+  for (int j = 0; j < T; ++j) {
+    const double v = th[j];
+    double sv[2];
+    for (int sgn = 0; sgn < 2; ++sgn) {
+      __syncwarp();
+      if (lane == 0) th[j] = v + (sgn == 0 ? h : -h);
+      __syncwarp();
+      grad_chain_mv(lib, meta, mov_off, th, y, lane);
+      grad_pose(y, N, qw, qx, qy, qz, t, x, lane);
+      sv[sgn] = grad_score(pk, x, N, nullptr, lane);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      th[j] = v;
+      G[j] = (sv[0] - sv[1]) / (2.0 * h);
+    }
+  }
+  __syncwarp();
+  return s0;
+}
+
+__global__ void __launch_bounds__(128)
+    vs_ascend_kernel(const __grid_constant__ LibDev lib, const __grid_constant__ GradPocket pk,
+                     long n_poses, const int* __restrict__ pose_lig, const long* __restrict__ tb,
+                     double* __restrict__ t, double* __restrict__ q, double* __restrict__ tors,
+                     int nmax, int tmax, int max_steps, double* __restrict__ score,
+                     int* __restrict__ steps_out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
+  double3* y = reinterpret_cast<double3*>(smem) + static_cast<size_t>(wib) * 3 * nmax;
+  double3* x = y + nmax;
+  double3* g = x + nmax;
+  double* th = reinterpret_cast<double*>(reinterpret_cast<double3*>(smem) +
+                                         static_cast<size_t>(nw) * 3 * nmax) +
+               static_cast<size_t>(wib) * 3 * tmax;
+  double* G = th + tmax;
+  double* th2 = G + tmax;
+  const long p = static_cast<long>(blockIdx.x) * nw + wib;
+  if (p >= n_poses) return;
+  const int lig = pose_lig[p];
+  const int4 meta = lib.meta[lig];
+  const int T = meta.w;
+  const int mov_off = lib.mov[lig].x;
+  double pt[3] = {t[3 * p], t[3 * p + 1], t[3 * p + 2]};
+  double pq[4];
+  {  // p.q = p.q.normalized() (dock.cpp:169)
+    const double* q0 = q + 4 * p;
+    const double n = sqrt(q0[0] * q0[0] + q0[1] * q0[1] + q0[2] * q0[2] + q0[3] * q0[3]);
+    for (int c = 0; c < 4; ++c) pq[c] = q0[c] / n;
+  }
+  for (int j = lane; j < T; j += 32) th[j] = tors[tb[p] + j];
+  __syncwarp();
+  double gt[3], gq[4];
+  double s = ascent_grad(lib, pk, meta, mov_off, th, pt, pq, y, x, g, gt, gq, G, lane);
+  int step = 0;
+  for (; step < max_steps; ++step) {
+    // |g|^2 in the reference's order (dock.cpp:176-177)
+    double gn2 = gt[0] * gt[0] + gt[1] * gt[1] + gt[2] * gt[2] + gq[0] * gq[0] + gq[1] * gq[1] +
+                 gq[2] * gq[2] + gq[3] * gq[3];
+    for (int j = 0; j < T; ++j) gn2 += G[j] * G[j];
+    if (sqrt(gn2) < 1e-6) break;
+    double alpha = 0.5;
+    bool accepted = false;
+    while (alpha > 1e-14) {
+      double tt[3], tq[4];
+      for (int c = 0; c < 3; ++c) tt[c] = pt[c] + gt[c] * alpha;
+      for (int c = 0; c < 4; ++c) tq[c] = pq[c] + gq[c] * alpha;
+      const double n = sqrt(tq[0] * tq[0] + tq[1] * tq[1] + tq[2] * tq[2] + tq[3] * tq[3]);
+      for (int c = 0; c < 4; ++c) tq[c] = tq[c] / n;
+      for (int j = lane; j < T; j += 32) th2[j] = th[j] + G[j] * alpha;
+      __syncwarp();
+      // obj.eval(trial): score only
+      const double nn = sqrt(tq[0] * tq[0] + tq[1] * tq[1] + tq[2] * tq[2] + tq[3] * tq[3]);
+      grad_chain_mv(lib, meta, mov_off, th2, y, lane);
+      grad_pose(y, meta.y, tq[0] / nn, tq[1] / nn, tq[2] / nn, tq[3] / nn, tt, x, lane);
+      const double st = grad_score(pk, x, meta.y, nullptr, lane);
+      if (st >= s + 1e-4 * alpha * gn2) {
+        for (int c = 0; c < 3; ++c) pt[c] = tt[c];
+        for (int c = 0; c < 4; ++c) pq[c] = tq[c];
+        __syncwarp();
+        for (int j = lane; j < T; j += 32) th[j] = th2[j];
+        __syncwarp();
+        s = st;
+        accepted = true;
+        break;
+      }
+      alpha *= 0.5;
+    }
+    if (!accepted) break;
+    s = ascent_grad(lib, pk, meta, mov_off, th, pt, pq, y, x, g, gt, gq, G, lane);
+  }
+  if (lane == 0) {
+    for (int c = 0; c < 3; ++c) t[3 * p + c] = pt[c];
+    for (int c = 0; c < 4; ++c) q[4 * p + c] = pq[c];
+    score[p] = s;
+    steps_out[p] = step;
+  }
+  for (int j = lane; j < T; j += 32) tors[tb[p] + j] = th[j];
+}
+
+size_t ascend_smem_per_block(int nmax, int tmax) {
+  return 4 * (3 * static_cast<size_t>(nmax) * sizeof(double3) + 3 * static_cast<size_t>(tmax) * 8);
+}
+
+cudaError_t launch_ascend(cudaStream_t st, const LibDev& lib, const SiteD* sites, int n_sites,
+                          const double lo[3], const double hi[3], double r, double lam,
+                          long n_poses, const int* pose_lig, const long* tb, double* t, double* q,
+                          double* tors, int nmax, int tmax, int max_steps, double* score,
+                          int* steps) {
+  GradPocket pk;
+  pk.sites = sites;
+  pk.n_sites = n_sites;
+  for (int c = 0; c < 3; ++c) {
+    pk.lo[c] = lo[c];
+    pk.hi[c] = hi[c];
+  }
+  pk.r = r;
+  pk.lam = lam;
+  const size_t smem = ascend_smem_per_block(nmax, tmax);
+  cudaFuncSetAttribute(vs_ascend_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(smem));
+  const long blocks = (n_poses + 3) / 4;
+  vs_ascend_kernel<<<static_cast<unsigned>(blocks), 128, smem, st>>>(
+      lib, pk, n_poses, pose_lig, tb, t, q, tors, nmax, tmax, max_steps, score, steps);
+  return cudaGetLastError();
+}
+
 size_t grad_smem_per_block(int nmax, int tmax) {
   return 4 * (3 * static_cast<size_t>(nmax) * sizeof(double3) + static_cast<size_t>(tmax) * 8);
 }

@@ -49,6 +49,12 @@ cudaError_t launch_rescore(bool grid, int blocks, size_t smem, cudaStream_t st, 
                            const float4* pq, const float* ptors, int nmax, int tmax, int mvmax,
                            float* geo, float* resc);
 size_t grad_smem_per_block(int nmax, int tmax);
+size_t ascend_smem_per_block(int nmax, int tmax);
+cudaError_t launch_ascend(cudaStream_t st, const LibDev& lib, const SiteD* sites, int n_sites,
+                          const double lo[3], const double hi[3], double r, double lam,
+                          long n_poses, const int* pose_lig, const long* tb, double* t, double* q,
+                          double* tors, int nmax, int tmax, int max_steps, double* score,
+                          int* steps);
 int relax_max_atoms();
 int relax_max_bonds();
 cudaError_t launch_relax(cudaStream_t st, const long long* atom_off, const int* n_atoms,
@@ -1245,6 +1251,70 @@ int vs_score_gradient(vs_handle* h, const vs_library* L, int64_t n_poses,
   VS_CUDA(h, cudaMemcpyAsync(grad_t, d_gt.p, np * 24, cudaMemcpyDeviceToHost, st));
   VS_CUDA(h, cudaMemcpyAsync(grad_q, d_gq.p, np * 32, cudaMemcpyDeviceToHost, st));
   if (toff > 0) VS_CUDA(h, cudaMemcpyAsync(grad_tors, d_gth.p, toff * 8, cudaMemcpyDeviceToHost, st));
+  VS_CUDA(h, cudaStreamSynchronize(st));
+  return VS_OK;
+}
+
+int vs_ascend(vs_handle* h, const vs_library* L, int64_t n_poses, const int32_t* pose_lig,
+              double* t, double* q, double* tors, int32_t max_steps, double* score,
+              int32_t* steps) {
+  cudaSetDevice(h->device);
+  if (!h->has_pocket) return fail(h, VS_ERR_STATE, "no pocket");
+  if (h->empty_bounds) return fail(h, VS_ERR_EMPTY_BOUNDS, "pocket bounds are empty");
+  if (n_poses < 0 || max_steps < 0) return fail(h, VS_ERR_INVALID_ARGUMENT, "negative count");
+  if (n_poses == 0) return VS_OK;
+  Packed P;
+  DBuf d_pl, d_tb, d_t, d_q, d_th, d_s, d_st;
+  struct Release {
+    std::vector<DBuf*> bufs;
+    Packed* packed;
+    ~Release() {
+      for (DBuf* b : bufs) b->release();
+      packed->release();
+    }
+  } guard{{&d_pl, &d_tb, &d_t, &d_q, &d_th, &d_s, &d_st}, &P};
+  int rc = pack_library(h, L, nullptr, 0, P);
+  if (rc) return rc;
+  std::vector<long> tb(static_cast<size_t>(n_poses));
+  long toff = 0;
+  int nmax = 1, tmax = 1;
+  for (int64_t p = 0; p < n_poses; ++p) {
+    const int l = pose_lig[p];
+    if (l < 0 || l >= P.n) return fail(h, VS_ERR_INVALID_ARGUMENT, "pose ligand index out of range");
+    tb[p] = toff;
+    toff += P.meta[l].w;
+    nmax = std::max(nmax, P.meta[l].y);
+    tmax = std::max(tmax, P.meta[l].w);
+  }
+  if (ascend_smem_per_block(nmax, tmax) > 227 * 1024)
+    return fail(h, VS_ERR_CAPACITY, "ligand too large for the ascent");
+  cudaStream_t st = h->own;
+  rc = upload_packed(h, P, st);
+  if (rc) return rc;
+  const size_t np = static_cast<size_t>(n_poses), nt = static_cast<size_t>(std::max<long>(toff, 1));
+  VS_CUDA(h, d_pl.ensure(np * 4));
+  VS_CUDA(h, d_tb.ensure(np * 8));
+  VS_CUDA(h, d_t.ensure(np * 24));
+  VS_CUDA(h, d_q.ensure(np * 32));
+  VS_CUDA(h, d_th.ensure(nt * 8));
+  VS_CUDA(h, d_s.ensure(np * 8));
+  VS_CUDA(h, d_st.ensure(np * 4));
+  VS_CUDA(h, cudaMemcpyAsync(d_pl.p, pose_lig, np * 4, cudaMemcpyHostToDevice, st));
+  VS_CUDA(h, cudaMemcpyAsync(d_tb.p, tb.data(), np * 8, cudaMemcpyHostToDevice, st));
+  VS_CUDA(h, cudaMemcpyAsync(d_t.p, t, np * 24, cudaMemcpyHostToDevice, st));
+  VS_CUDA(h, cudaMemcpyAsync(d_q.p, q, np * 32, cudaMemcpyHostToDevice, st));
+  if (toff > 0) VS_CUDA(h, cudaMemcpyAsync(d_th.p, tors, toff * 8, cudaMemcpyHostToDevice, st));
+  VS_CUDA(h, launch_ascend(st, P.dev(), h->d_sites64.as<const SiteD>(), h->n_sites64, h->box_lo,
+                           h->box_hi, h->r64, h->lam64, n_poses, d_pl.as<const int>(),
+                           d_tb.as<const long>(), d_t.as<double>(), d_q.as<double>(),
+                           d_th.as<double>(), nmax, tmax, max_steps, d_s.as<double>(),
+                           d_st.as<int>()));
+  ++h->launches;
+  VS_CUDA(h, cudaMemcpyAsync(t, d_t.p, np * 24, cudaMemcpyDeviceToHost, st));
+  VS_CUDA(h, cudaMemcpyAsync(q, d_q.p, np * 32, cudaMemcpyDeviceToHost, st));
+  if (toff > 0) VS_CUDA(h, cudaMemcpyAsync(tors, d_th.p, toff * 8, cudaMemcpyDeviceToHost, st));
+  if (score) VS_CUDA(h, cudaMemcpyAsync(score, d_s.p, np * 8, cudaMemcpyDeviceToHost, st));
+  if (steps) VS_CUDA(h, cudaMemcpyAsync(steps, d_st.p, np * 4, cudaMemcpyDeviceToHost, st));
   VS_CUDA(h, cudaStreamSynchronize(st));
   return VS_OK;
 }

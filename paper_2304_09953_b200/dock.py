@@ -399,6 +399,25 @@ class Engine:
               self._h, "score_gradient")
         return score[:n], gt[:3 * n].reshape(n, 3), gq[:4 * n].reshape(n, 4), gtor[:nt]
 
+    def ascend(self, lib: Library, pose_lig, t, q, tors, max_steps: int = 500):
+        """The reference ascent on the device (capi.h vs_ascend): returns the
+        refined (t[n, 3], q[n, 4], tors, score[n], steps[n]) in FP64."""
+        pose_lig = np.ascontiguousarray(pose_lig, np.int32)
+        n = len(pose_lig)
+        t = np.array(t, np.float64).reshape(-1).copy()
+        q = np.array(q, np.float64).reshape(-1).copy()
+        tors = np.array(tors, np.float64).reshape(-1).copy()
+        nt = tors.size
+        if nt == 0:
+            tors = np.zeros(1, np.float64)
+        score = np.zeros(max(n, 1), np.float64)
+        steps = np.zeros(max(n, 1), np.int32)
+        lc = lib.as_c()
+        check(_lib.vs_ascend(self._h, C.byref(lc), n, ptr(pose_lig, C.c_int32), ptr(t, C.c_double),
+                             ptr(q, C.c_double), ptr(tors, C.c_double), max_steps,
+                             ptr(score, C.c_double), ptr(steps, C.c_int32)), self._h, "ascend")
+        return t[:3 * n].reshape(n, 3), q[:4 * n].reshape(n, 4), tors[:nt], score[:n], steps[:n]
+
     def rescore(self, lib: Library, pose_lig, t, q, tors):
         """K3a: canonical geometric score and rescore of given poses."""
         pose_lig = np.ascontiguousarray(pose_lig, np.int32)

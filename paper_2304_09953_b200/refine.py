@@ -28,6 +28,25 @@ def _normalized(q: np.ndarray) -> np.ndarray:
     return q / np.sqrt(np.sum(q * q, axis=1, keepdims=True))
 
 
+def _gn2(gt, gq, gtor, T, toff):
+    """|g|^2 in the reference's order (dock.cpp:176-177): x, y, z, then the
+    four quaternion terms, then the torsions in axis order."""
+    g = gt[:, 0] * gt[:, 0] + gt[:, 1] * gt[:, 1] + gt[:, 2] * gt[:, 2]
+    for c in range(4):
+        g = g + gq[:, c] * gq[:, c]
+    for k in range(int(T.max()) if len(T) else 0):
+        has = T > k
+        v = np.where(has, gtor[np.minimum(toff[:-1] + k, max(len(gtor) - 1, 0))], 0.0)
+        g = np.where(has, g + v * v, g)
+    return g
+
+
+def ascend_poses_device(engine, lib, pose_lig, t, q, tors, max_steps: int = 500):
+    """The same ascent with the whole loop on the device (capi.h vs_ascend,
+    one warp per pose): bit-identical to ascend_poses."""
+    return engine.ascend(lib, pose_lig, t, q, tors, max_steps)
+
+
 def ascend_poses(engine, lib, pose_lig, t, q, tors, max_steps: int = 500):
     """Refine poses (pose_lig[n] ligand indices, non-decreasing; t[n, 3],
     q[n, 4] (w, x, y, z), tors: concatenated per-pose torsion vectors) by the
@@ -45,7 +64,7 @@ def ascend_poses(engine, lib, pose_lig, t, q, tors, max_steps: int = 500):
     active = np.ones(n, bool)
     steps = np.zeros(n, np.int32)
     for _ in range(max_steps):
-        gn2 = np.sum(gt * gt, 1) + np.sum(gq * gq, 1) + np.bincount(seg, gtor * gtor, minlength=n)
+        gn2 = _gn2(gt, gq, gtor, T, toff)
         active &= np.sqrt(gn2) >= GRAD_TOL
         if not active.any():
             break

@@ -84,3 +84,24 @@ def test_refinement_is_monotone_on_docked_poses(V, engine, pocket_json):
     # the refined poses score the same through the FP64 scorer
     s1, _, _, _ = engine.score_gradient(lib, pl, t, q, tor)
     np.testing.assert_allclose(s1, s, rtol=0, atol=1e-12)
+
+
+def test_device_ascent_equals_host_driven(V, engine, pocket_json):
+    """vs_ascend (the whole loop in one launch, warp per pose) follows the
+    host-driven ascent bit for bit: same scores, gradients and decisions."""
+    from paper_2304_09953_b200.refine import ascend_poses, ascend_poses_device
+    lib, _ = corpus_library(24)
+    engine.set_pocket(V.parse_pocket_json(pocket_json))
+    res = engine.dock_host(lib, V.DockParams(restarts=2, rotations=32, keep_top=2))
+    pl, T, Q, TH = [], [], [], []
+    for i in range(len(lib)):
+        for pose in res.poses(i, int(lib.n_tors[i]), "surv"):
+            pl.append(i)
+            T.append(pose.translation)
+            Q.append(pose.rotation)
+            TH.extend(pose.torsions)
+    TH = np.array(TH, np.float64)
+    h = ascend_poses(engine, lib, pl, T, Q, TH, max_steps=60)
+    d = ascend_poses_device(engine, lib, pl, T, Q, TH, max_steps=60)
+    for a, b in zip(h, d):
+        np.testing.assert_array_equal(np.asarray(a), np.asarray(b))

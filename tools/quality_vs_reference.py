@@ -93,7 +93,7 @@ def main():
     t_ref_gpu = 0.0
     if "--refine" in sys.argv:
         # the reference ascent on the GPU from every survivor (refine.py)
-        from paper_2304_09953_b200.refine import ascend_poses
+        from paper_2304_09953_b200.refine import ascend_poses_device as ascend_poses
         pl = [i for i in range(len(lib)) for _ in surv[i]]
         T3 = [p[0] for i in range(len(lib)) for p in surv[i]]
         Q4 = [p[1] for i in range(len(lib)) for p in surv[i]]
