@@ -218,6 +218,11 @@ struct vs_handle {
   PinnedVec<uint8_t> fetch_stage;  // vs_fetch_results' pinned staging, reused across calls
   Packed rpack;              // vs_rescore's library staging, reused across calls
   DBuf rbuf[9];              // vs_rescore's per-bucket pose arrays, reused across calls
+  // vs_rescore's pinned staging of the concatenated per-bucket pose arrays
+  PinnedVec<int> rs_lig, rs_off, rs_orig;
+  PinnedVec<long> rs_tb;
+  PinnedVec<float4> rs_t, rs_q;
+  PinnedVec<float> rs_tors, rs_geo, rs_resc;
   double rescore_ms = -1.0;  // device time of the rescore kernels of the last vs_rescore
   cudaEvent_t rev0 = nullptr, rev1 = nullptr;
 };
@@ -502,17 +507,22 @@ int check_nested(vs_handle* h, const Packed& P) {
   return VS_OK;
 }
 
-int upload_packed(vs_handle* h, Packed& P, cudaStream_t st) {
+// parts: 1 = the pinned arrays (async DMA, returns at once), 2 = the small
+// pageable ones (a pageable H2D waits for the stream), 3 = both.
+int upload_packed(vs_handle* h, Packed& P, cudaStream_t st, int parts = 3) {
   auto up = [&](DBuf& d, const void* src, size_t bytes) -> cudaError_t {
     cudaError_t e = d.ensure(bytes);
     if (e != cudaSuccess) return e;
     return cudaMemcpyAsync(d.p, src, bytes, cudaMemcpyHostToDevice, st);
   };
-  VS_CUDA(h, up(P.d_meta, P.meta.data(), std::max<size_t>(16, P.meta.size() * sizeof(int4))));
-  VS_CUDA(h, up(P.d_mov, P.mov.data(), std::max<size_t>(8, P.mov.size() * sizeof(int2))));
-  VS_CUDA(h, up(P.d_atoms, P.atoms.data(), P.atoms.size() * sizeof(double4)));
-  VS_CUDA(h, up(P.d_axes, P.axes.data(), P.axes.size() * sizeof(int4)));
-  VS_CUDA(h, up(P.d_moving, P.moving.data(), P.moving.size()));
+  if (parts & 1) {
+    VS_CUDA(h, up(P.d_meta, P.meta.data(), std::max<size_t>(16, P.meta.size() * sizeof(int4))));
+    VS_CUDA(h, up(P.d_mov, P.mov.data(), std::max<size_t>(8, P.mov.size() * sizeof(int2))));
+    VS_CUDA(h, up(P.d_atoms, P.atoms.data(), P.atoms.size() * sizeof(double4)));
+    VS_CUDA(h, up(P.d_axes, P.axes.data(), P.axes.size() * sizeof(int4)));
+    VS_CUDA(h, up(P.d_moving, P.moving.data(), P.moving.size()));
+  }
+  if (!(parts & 2)) return VS_OK;
   VS_CUDA(h, up(P.d_seeds, P.seeds.data(), std::max<size_t>(8, P.seeds.size() * 8)));
   VS_CUDA(h, up(P.d_idr, P.id_rank.data(), std::max<size_t>(4, P.id_rank.size() * 4)));
   VS_CUDA(h, up(P.d_order, P.order.data(), P.order.size() * sizeof(int)));
@@ -1322,6 +1332,8 @@ int vs_ascend(vs_handle* h, const vs_library* L, int64_t n_poses, const int32_t*
 int vs_rescore(vs_handle* h, const vs_library* L, int64_t n_poses, const int32_t* pose_lig,
                const float* t, const float* q, const float* tors, float* geo, float* resc) {
   cudaSetDevice(h->device);
+  using clk = std::chrono::steady_clock;
+  const auto r0 = clk::now();
   if (!h->has_pocket) return fail(h, VS_ERR_STATE, "no pocket");
   for (int64_t p = 1; p < n_poses; ++p)
     if (pose_lig[p] < pose_lig[p - 1])
@@ -1332,8 +1344,10 @@ int vs_rescore(vs_handle* h, const vs_library* L, int64_t n_poses, const int32_t
   for (int64_t p = 0; p < n_poses; ++p)
     if (pose_lig[p] < 0 || pose_lig[p] >= P.n)
       return fail(h, VS_ERR_INVALID_ARGUMENT, "pose ligand index out of range");
+  const auto r1 = clk::now();
   cudaStream_t st = h->own;
-  rc = upload_packed(h, P, st);
+  // the library's pinned arrays stream in while the host lays out the poses
+  rc = upload_packed(h, P, st, 1);
   if (rc) return rc;
   // per-ligand pose ranges (contiguous: pose_lig is non-decreasing) and the
   // offset of each ligand's first torsion vector in `tors`
@@ -1349,75 +1363,151 @@ int vs_rescore(vs_handle* h, const vs_library* L, int64_t n_poses, const int32_t
     ++cnt[l];
     toff += P.meta[l].w;
   }
+  const auto rA = clk::now();
   const bool grid = h->pk.grid_mode != 0;
   const LibDev ld = P.dev();
   if (!h->rev0) {
     VS_CUDA(h, cudaEventCreate(&h->rev0));
     VS_CUDA(h, cudaEventCreate(&h->rev1));
   }
-  h->rescore_ms = 0.0;
-  // one launch per size bucket with bucket-local, LPT-ordered pose lists
-  for (const Bucket& b : P.buckets) {
-    std::vector<int> rl, ro, orig;
-    std::vector<long> rt;
-    std::vector<float4> rpt, rpq;
-    std::vector<float> rtors;
+  // One host pass lays every bucket's pose lists (bucket-local, LPT-ordered)
+  // end to end in pinned staging; one DMA per array, the bucket launches back
+  // to back on one stream, one D2H per output and a single synchronize.
+  struct Seg {
+    int lig0, off0, count, bi;
+    long pose0, tors0;
+  };
+  std::vector<Seg> segs;
+  size_t n_work = 0, n_off = 0;
+  long n_pose = 0, n_tors = 0;
+  for (size_t bi = 0; bi < P.buckets.size(); ++bi) {
+    const Bucket& b = P.buckets[bi];
+    int c = 0;
+    long bt = 0;
     for (int w = b.start; w < b.start + b.count; ++w) {
       const int l = P.order[w];
       if (cnt[l] == 0) continue;
-      rl.push_back(l);
-      ro.push_back(static_cast<int>(orig.size()));
-      rt.push_back(static_cast<long>(rtors.size()));
-      for (int p = first[l]; p < first[l] + cnt[l]; ++p) {
-        orig.push_back(p);
-        rpt.push_back(float4{t[3 * p], t[3 * p + 1], t[3 * p + 2], 0.0f});
-        rpq.push_back(float4{q[4 * p], q[4 * p + 1], q[4 * p + 2], q[4 * p + 3]});
+      ++c;
+      bt += static_cast<long>(cnt[l]) * P.meta[l].w;
+    }
+    if (c == 0) continue;
+    long bp = 0;
+    for (int w = b.start; w < b.start + b.count; ++w) bp += cnt[P.order[w]];
+    segs.push_back(Seg{static_cast<int>(n_work), static_cast<int>(n_off), c, static_cast<int>(bi),
+                       n_pose, n_tors});
+    n_work += c;
+    n_off += c + 1;
+    n_pose += bp;
+    n_tors += bt;
+  }
+  if (!h->rs_lig.resize(std::max<size_t>(n_work, 1)) || !h->rs_off.resize(std::max<size_t>(n_off, 1)) ||
+      !h->rs_tb.resize(std::max<size_t>(n_work, 1)) || !h->rs_orig.resize(std::max<long>(n_pose, 1)) ||
+      !h->rs_t.resize(std::max<long>(n_pose, 1)) || !h->rs_q.resize(std::max<long>(n_pose, 1)) ||
+      !h->rs_tors.resize(std::max<long>(n_tors, 1)) || !h->rs_geo.resize(std::max<long>(n_pose, 1)) ||
+      !h->rs_resc.resize(std::max<long>(n_pose, 1)))
+    return fail(h, VS_ERR_CUDA, "pinned rescore staging allocation failed");
+  const auto rB = clk::now();
+  // serial pass: work-item indices and each item's global pose / torsion base;
+  // the pose copies (the bulk) then run over host threads
+  std::vector<long> wpose(n_work), wtors(n_work);
+  for (const Seg& sg : segs) {
+    const Bucket& b = P.buckets[sg.bi];
+    int k = 0;
+    long pl = 0, tl = 0;  // bucket-local pose / torsion cursors
+    for (int w = b.start; w < b.start + b.count; ++w) {
+      const int l = P.order[w];
+      if (cnt[l] == 0) continue;
+      h->rs_lig[sg.lig0 + k] = l;
+      h->rs_off[sg.off0 + k] = static_cast<int>(pl);
+      h->rs_tb[sg.lig0 + k] = tl;
+      wpose[sg.lig0 + k] = sg.pose0 + pl;
+      wtors[sg.lig0 + k] = sg.tors0 + tl;
+      pl += cnt[l];
+      tl += static_cast<long>(cnt[l]) * P.meta[l].w;
+      ++k;
+    }
+    h->rs_off[sg.off0 + k] = static_cast<int>(pl);
+  }
+  auto fill = [&](size_t k0, size_t k1) {
+    for (size_t k = k0; k < k1; ++k) {
+      const int l = h->rs_lig[k];
+      long g = wpose[k];
+      for (int p = first[l]; p < first[l] + cnt[l]; ++p, ++g) {
+        h->rs_orig[g] = p;
+        h->rs_t[g] = float4{t[3 * p], t[3 * p + 1], t[3 * p + 2], 0.0f};
+        h->rs_q[g] = float4{q[4 * p], q[4 * p + 1], q[4 * p + 2], q[4 * p + 3]};
       }
       const long nt = static_cast<long>(cnt[l]) * P.meta[l].w;
-      rtors.insert(rtors.end(), tors + tb[l], tors + tb[l] + nt);
+      if (nt) std::memcpy(h->rs_tors.data() + wtors[k], tors + tb[l], nt * sizeof(float));
     }
-    if (rl.empty()) continue;
-    ro.push_back(static_cast<int>(orig.size()));
-    if (rtors.empty()) rtors.push_back(0.0f);
-    DBuf &a = h->rbuf[0], &bo = h->rbuf[1], &c = h->rbuf[2], &d = h->rbuf[3], &e = h->rbuf[4],
-         &f = h->rbuf[5], &g = h->rbuf[6], &gr = h->rbuf[7], &cc = h->rbuf[8];
-    auto up = [&](DBuf& dst, const void* src, size_t bytes) -> cudaError_t {
-      cudaError_t err = dst.ensure(bytes);
-      if (err != cudaSuccess) return err;
-      return cudaMemcpyAsync(dst.p, src, bytes, cudaMemcpyHostToDevice, st);
-    };
-    VS_CUDA(h, up(a, rl.data(), rl.size() * 4));
-    VS_CUDA(h, up(bo, ro.data(), ro.size() * 4));
-    VS_CUDA(h, up(c, rt.data(), rt.size() * 8));
-    VS_CUDA(h, up(d, rpt.data(), rpt.size() * 16));
-    VS_CUDA(h, up(e, rpq.data(), rpq.size() * 16));
-    VS_CUDA(h, up(f, rtors.data(), rtors.size() * 4));
-    VS_CUDA(h, g.ensure(orig.size() * 4));
-    VS_CUDA(h, gr.ensure(orig.size() * 4));
-    VS_CUDA(h, cc.ensure(4));
-    VS_CUDA(h, cudaMemsetAsync(cc.p, 0, 4, st));
-    const int count = static_cast<int>(rl.size());
+  };
+  {
+    const size_t nth = std::max<size_t>(
+        1, std::min<size_t>({n_work / 4096 + 1, 16, std::max(1u, std::thread::hardware_concurrency())}));
+    std::vector<std::thread> pool;
+    const size_t chunk = (n_work + nth - 1) / nth;
+    for (size_t tI = 1; tI < nth; ++tI)
+      pool.emplace_back(fill, std::min(n_work, tI * chunk), std::min(n_work, (tI + 1) * chunk));
+    fill(0, std::min(n_work, chunk));
+    for (auto& th : pool) th.join();
+  }
+  const auto r2 = clk::now();
+  DBuf &a = h->rbuf[0], &bo = h->rbuf[1], &c = h->rbuf[2], &d = h->rbuf[3], &e = h->rbuf[4],
+       &f = h->rbuf[5], &g = h->rbuf[6], &gr = h->rbuf[7], &cc = h->rbuf[8];
+  rc = upload_packed(h, P, st, 2);
+  if (rc) return rc;
+  auto up = [&](DBuf& dst, const void* src, size_t bytes) -> cudaError_t {
+    cudaError_t err = dst.ensure(std::max<size_t>(bytes, 16));
+    if (err != cudaSuccess || bytes == 0) return err;
+    return cudaMemcpyAsync(dst.p, src, bytes, cudaMemcpyHostToDevice, st);
+  };
+  VS_CUDA(h, up(a, h->rs_lig.data(), n_work * 4));
+  VS_CUDA(h, up(bo, h->rs_off.data(), n_off * 4));
+  VS_CUDA(h, up(c, h->rs_tb.data(), n_work * 8));
+  VS_CUDA(h, up(d, h->rs_t.data(), n_pose * 16));
+  VS_CUDA(h, up(e, h->rs_q.data(), n_pose * 16));
+  VS_CUDA(h, up(f, h->rs_tors.data(), n_tors * 4));
+  VS_CUDA(h, g.ensure(std::max<long>(n_pose, 1) * 4));
+  VS_CUDA(h, gr.ensure(std::max<long>(n_pose, 1) * 4));
+  VS_CUDA(h, cc.ensure(std::max<size_t>(segs.size(), 1) * 4));
+  VS_CUDA(h, cudaMemsetAsync(cc.p, 0, std::max<size_t>(segs.size(), 1) * 4, st));
+  VS_CUDA(h, cudaEventRecord(h->rev0, st));
+  for (size_t si = 0; si < segs.size(); ++si) {
+    const Seg& sg = segs[si];
+    const Bucket& b = P.buckets[sg.bi];
     const size_t smem = rescore_smem_per_block(b.nmax, b.tmax, b.mvmax);
-    const int blocks = std::max(1, std::min((count + kWarpsPerBlock - 1) / kWarpsPerBlock, 4 * h->sms));
-    VS_CUDA(h, cudaEventRecord(h->rev0, st));
-    VS_CUDA(h, launch_rescore(grid, blocks, smem, st, ld, h->pk, a.as<int>(), count, cc.as<int>(),
-                              bo.as<int>(), c.as<long>(), d.as<float4>(), e.as<float4>(),
-                              f.as<float>(), b.nmax, b.tmax, b.mvmax, g.as<float>(), gr.as<float>()));
-    VS_CUDA(h, cudaEventRecord(h->rev1, st));
+    const int blocks =
+        std::max(1, std::min((sg.count + kWarpsPerBlock - 1) / kWarpsPerBlock, 4 * h->sms));
+    VS_CUDA(h, launch_rescore(grid, blocks, smem, st, ld, h->pk, a.as<int>() + sg.lig0, sg.count,
+                              cc.as<int>() + si, bo.as<int>() + sg.off0, c.as<long>() + sg.lig0,
+                              d.as<float4>() + sg.pose0, e.as<float4>() + sg.pose0,
+                              f.as<float>() + sg.tors0, b.nmax, b.tmax, b.mvmax,
+                              g.as<float>() + sg.pose0, gr.as<float>() + sg.pose0));
     ++h->launches;
-    std::vector<float> og(orig.size()), orr(orig.size());
-    VS_CUDA(h, cudaMemcpyAsync(og.data(), g.p, og.size() * 4, cudaMemcpyDeviceToHost, st));
-    VS_CUDA(h, cudaMemcpyAsync(orr.data(), gr.p, orr.size() * 4, cudaMemcpyDeviceToHost, st));
-    VS_CUDA(h, cudaStreamSynchronize(st));
-    {
-      float ms = 0.0f;
-      VS_CUDA(h, cudaEventElapsedTime(&ms, h->rev0, h->rev1));
-      h->rescore_ms += ms;
-    }
-    for (size_t k = 0; k < orig.size(); ++k) {
-      if (geo) geo[orig[k]] = og[k];
-      if (resc) resc[orig[k]] = orr[k];
-    }
+  }
+  VS_CUDA(h, cudaEventRecord(h->rev1, st));
+  if (n_pose) {
+    VS_CUDA(h, cudaMemcpyAsync(h->rs_geo.data(), g.p, n_pose * 4, cudaMemcpyDeviceToHost, st));
+    VS_CUDA(h, cudaMemcpyAsync(h->rs_resc.data(), gr.p, n_pose * 4, cudaMemcpyDeviceToHost, st));
+  }
+  VS_CUDA(h, cudaStreamSynchronize(st));
+  const auto r3 = clk::now();
+  {
+    float ms = 0.0f;
+    VS_CUDA(h, cudaEventElapsedTime(&ms, h->rev0, h->rev1));
+    h->rescore_ms = ms;
+  }
+  for (long k = 0; k < n_pose; ++k) {
+    if (geo) geo[h->rs_orig[k]] = h->rs_geo[k];
+    if (resc) resc[h->rs_orig[k]] = h->rs_resc[k];
+  }
+  if (const char* ev = std::getenv("VSCREEN_UPLOAD_TIMING"); ev && ev[0] == '1') {
+    auto ms = [](clk::time_point x, clk::time_point y) {
+      return std::chrono::duration<double, std::milli>(y - x).count();
+    };
+    std::fprintf(stderr, "vs_rescore: check+pack %.2f ms, ranges %.2f + segs %.2f + staging %.2f ms, H2D+kernels+D2H %.2f ms "
+                 "(kernels %.2f), scatter %.2f ms\n", ms(r0, r1), ms(r1, rA), ms(rA, rB), ms(rB, r2), ms(r2, r3), h->rescore_ms,
+                 ms(r3, clk::now()));
   }
   return VS_OK;
 }
