@@ -276,8 +276,12 @@ void lpt_sort(std::vector<int>& idx, const std::vector<long>& cost) {
   }
 }
 
+int upload_packed(vs_handle* h, Packed& P, cudaStream_t st, int parts);
+
+// early: when non-null, the pinned arrays' DMA is issued on it as soon as they
+// are filled, so it runs under the LPT sort and bucketing.
 int pack_library(vs_handle* h, const vs_library* L, const vs_size_class* classes, int nc,
-                 Packed& P) {
+                 Packed& P, cudaStream_t early = nullptr) {
   const int n = L->n_ligands;
   if (n < 0) return fail(h, VS_ERR_INVALID_ARGUMENT, "negative ligand count");
   P.n = n;
@@ -403,6 +407,10 @@ int pack_library(vs_handle* h, const vs_library* L, const vs_size_class* classes
   // one stable LPT sort (descending cost, then index); the per-class buckets
   // are class-filtered views of it (same order inside each class), and the
   // global queue over every class is the dock launch's
+  if (early) {
+    const int urc = upload_packed(h, P, early, 1);
+    if (urc) return urc;
+  }
   std::vector<int> lpt;
   lpt.reserve(n);
   for (int i = 0; i < n; ++i)
@@ -509,7 +517,7 @@ int check_nested(vs_handle* h, const Packed& P) {
 
 // parts: 1 = the pinned arrays (async DMA, returns at once), 2 = the small
 // pageable ones (a pageable H2D waits for the stream), 3 = both.
-int upload_packed(vs_handle* h, Packed& P, cudaStream_t st, int parts = 3) {
+int upload_packed(vs_handle* h, Packed& P, cudaStream_t st, int parts) {
   auto up = [&](DBuf& d, const void* src, size_t bytes) -> cudaError_t {
     cudaError_t e = d.ensure(bytes);
     if (e != cudaSuccess) return e;
@@ -759,13 +767,14 @@ int vs_upload_library(vs_handle* h, const vs_library* L, const vs_size_class* cl
   h->has_results = false;
   using clk = std::chrono::steady_clock;
   const auto t0 = clk::now();
-  int rc = pack_library(h, L, classes, nc, h->lib);
-  if (rc) return rc;
+  // the pinned arrays' DMA runs under the bucketing and the torsion-tree
+  // check; a failure drains it before returning (the next pack rewrites them)
+  int rc = pack_library(h, L, classes, nc, h->lib, h->own);
+  if (rc) {
+    cudaStreamSynchronize(h->own);
+    return rc;
+  }
   const auto t1 = clk::now();
-  // the pinned arrays' DMA runs under the torsion-tree check; a failed check
-  // drains it before returning (the next pack rewrites the pinned arrays)
-  rc = upload_packed(h, h->lib, h->own, 1);
-  if (rc) return rc;
   rc = check_nested(h, h->lib);
   if (rc) {
     cudaStreamSynchronize(h->own);
@@ -1241,7 +1250,7 @@ int vs_score_gradient(vs_handle* h, const vs_library* L, int64_t n_poses,
   if (grad_smem_per_block(nmax, tmax) > 227 * 1024)
     return fail(h, VS_ERR_CAPACITY, "ligand too large for score_gradient");
   cudaStream_t st = h->own;
-  rc = upload_packed(h, P, st);
+  rc = upload_packed(h, P, st, 3);
   if (rc) return rc;
   const size_t np = static_cast<size_t>(n_poses), nt = static_cast<size_t>(std::max<long>(toff, 1));
   VS_CUDA(h, d_pl.ensure(np * 4));
@@ -1306,7 +1315,7 @@ int vs_ascend(vs_handle* h, const vs_library* L, int64_t n_poses, const int32_t*
   if (ascend_smem_per_block(nmax, tmax) > 227 * 1024)
     return fail(h, VS_ERR_CAPACITY, "ligand too large for the ascent");
   cudaStream_t st = h->own;
-  rc = upload_packed(h, P, st);
+  rc = upload_packed(h, P, st, 3);
   if (rc) return rc;
   const size_t np = static_cast<size_t>(n_poses), nt = static_cast<size_t>(std::max<long>(toff, 1));
   VS_CUDA(h, d_pl.ensure(np * 4));
@@ -1346,16 +1355,19 @@ int vs_rescore(vs_handle* h, const vs_library* L, int64_t n_poses, const int32_t
     if (pose_lig[p] < pose_lig[p - 1])
       return fail(h, VS_ERR_INVALID_ARGUMENT, "pose_lig must be non-decreasing");
   Packed& P = h->rpack;
-  int rc = pack_library(h, L, nullptr, 0, P);
-  if (rc) return rc;
+  // the library's pinned arrays stream in under the bucketing and the pose staging
+  int rc = pack_library(h, L, nullptr, 0, P, h->own);
+  if (rc) {
+    cudaStreamSynchronize(h->own);
+    return rc;
+  }
   for (int64_t p = 0; p < n_poses; ++p)
-    if (pose_lig[p] < 0 || pose_lig[p] >= P.n)
+    if (pose_lig[p] < 0 || pose_lig[p] >= P.n) {
+      cudaStreamSynchronize(h->own);
       return fail(h, VS_ERR_INVALID_ARGUMENT, "pose ligand index out of range");
+    }
   const auto r1 = clk::now();
   cudaStream_t st = h->own;
-  // the library's pinned arrays stream in while the host lays out the poses
-  rc = upload_packed(h, P, st, 1);
-  if (rc) return rc;
   // per-ligand pose ranges (contiguous: pose_lig is non-decreasing) and the
   // offset of each ligand's first torsion vector in `tors`
   std::vector<int> first(P.n, -1), cnt(P.n, 0);
