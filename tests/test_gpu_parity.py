@@ -352,3 +352,41 @@ def test_dock_smiles_single_site(V):
     # is reported, sorted by score
     assert best["geometric_score"] >= poses[-1]["geometric_score"]
     assert set(best) == {"ligand", "translation", "rotation", "torsions", "geometric_score", "rescore"}
+
+
+def test_rescore_batched_buckets_and_error_paths(V, engine, lib200, pocket_json):
+    """vs_rescore stages every size bucket in one pass: ligands with no poses,
+    uneven pose counts across buckets, and rejected calls (out-of-range or
+    decreasing pose_lig, dock.cpp:322-323) leave the handle usable; results
+    stay bit-exact vs the oracle and identical across calls."""
+    from oracle import sweep
+    lib, _ = lib200
+    pocket = V.parse_pocket_json(pocket_json)
+    engine.set_pocket(pocket)
+    rng = np.random.default_rng(11)
+    L = lib.subset(list(range(0, 200, 3)))
+    pl, T, Q, TH = [], [], [], []
+    for i in range(len(L)):
+        if i % 5 == 2:
+            continue  # no poses for this ligand
+        for _ in range(1 + (i * 7) % 9):
+            pl.append(i)
+            T.append(rng.uniform(-5, 5, 3))
+            q = rng.normal(size=4)
+            Q.append(q / np.linalg.norm(q))
+            TH.extend(rng.uniform(-np.pi, np.pi, int(L.n_tors[i])))
+    T = np.array(T, np.float32); Q = np.array(Q, np.float32); TH = np.array(TH, np.float32)
+    pl = np.array(pl, np.int32)
+    geo, resc = engine.rescore(L, pl, T, Q, TH)
+    og, orr = sweep.score_poses(sweep.OraclePocket(pocket), L, pl, T, Q, TH)
+    np.testing.assert_array_equal(geo.view(np.uint32), og.view(np.uint32))
+    np.testing.assert_array_equal(resc.view(np.uint32), orr.view(np.uint32))
+    bad = pl.copy()
+    bad[-1] = len(L)
+    with pytest.raises(ValueError):
+        engine.rescore(L, bad, T, Q, TH)
+    with pytest.raises(ValueError):
+        engine.rescore(L, pl[::-1].copy(), T, Q, TH)
+    g2, r2 = engine.rescore(L, pl, T, Q, TH)
+    np.testing.assert_array_equal(g2.view(np.uint32), geo.view(np.uint32))
+    np.testing.assert_array_equal(r2.view(np.uint32), resc.view(np.uint32))
