@@ -55,19 +55,28 @@ def parse_args():
     return ap.parse_args()
 
 
-def make_pocket():
+def pocket_sites():
     """Synthetic many-site pocket: 24 A box, 400 Gaussian
     sites 60/25/15 % steric/hbond/lipophilic, w ~ U[0.3, 2], sigma ~
-    U[0.8, 1.6], seed 7; clash radius / penalty of proj/data/pocket.json."""
-    import paper_2304_09953_b200 as V
+    U[0.8, 1.6], seed 7; clash radius / penalty of proj/data/pocket.json.
+    Plain tuples (center, weight, sigma, kind): both arms build from these."""
     rng = np.random.default_rng(7)
     sites = []
     for _ in range(400):
         u = rng.uniform()
         kind = "steric" if u < 0.6 else ("hbond" if u < 0.85 else "lipophilic")
-        sites.append(V.Site(tuple(float(v) for v in rng.uniform(-12, 12, 3)),
-                            float(rng.uniform(0.3, 2.0)), float(rng.uniform(0.8, 1.6)), kind))
-    return V.Pocket(sites, (-12.0, -12.0, -12.0), (12.0, 12.0, 12.0), 0.7, 0.5)
+        sites.append((tuple(float(v) for v in rng.uniform(-12, 12, 3)),
+                      float(rng.uniform(0.3, 2.0)), float(rng.uniform(0.8, 1.6)), kind))
+    return sites
+
+
+POCKET_BOX = ((-12.0, -12.0, -12.0), (12.0, 12.0, 12.0), 0.7, 0.5)
+
+
+def make_pocket():
+    import paper_2304_09953_b200 as V
+    lo, hi, r, lam = POCKET_BOX
+    return V.Pocket([V.Site(c, w, sg, k) for (c, w, sg, k) in pocket_sites()], lo, hi, r, lam)
 
 
 def params():
@@ -129,9 +138,12 @@ def build_flexible(n_per: int, rank: int, world: int, threads: int, seed: int = 
     return lib, ids_all, order
 
 
-def build_workload(n_per: int, rank: int, world: int, threads: int):
+def build_workload(n_per: int, rank: int, world: int, threads: int, balanced: bool = False):
     """Library shard of this rank: entries [rank*n_per, (rank+1)*n_per) of the
-    filtered corpus; ids ranked globally (bytewise) so top-k keys merge."""
+    filtered corpus (weak scaling), or with `balanced` the rank's contiguous
+    cost-balanced range of the n_per*world entries (pipeline.shard_bounds
+    over ligand_cost, from a parse-only pass over the whole library; strong
+    scaling, C3); ids ranked globally (bytewise) so top-k keys merge."""
     import paper_2304_09953_b200 as V
     from paper_2304_09953_b200.chem import corpus_indices, _fetch_built
     from paper_2304_09953_b200.pipeline import campaign_seeds
@@ -144,6 +156,15 @@ def build_workload(n_per: int, rank: int, world: int, threads: int):
     grank = np.empty(total, np.uint32)
     grank[order] = np.arange(total, dtype=np.uint32)
     lo, hi = rank * n_per, (rank + 1) * n_per
+    if balanced and world > 1:
+        from paper_2304_09953_b200.pipeline import ligand_cost, shard_bounds
+        h = C.c_void_p()
+        allidx = np.ascontiguousarray(idx)
+        es0 = np.zeros(total, np.uint64)
+        _lib.vs_libbuild_corpus(CORPUS_SEED, ptr(allidx, C.c_int64), total, ptr(es0, C.c_uint64),
+                                -1, threads, C.byref(h))
+        sizes = _fetch_built(h, total, ids_all, es0, drop_failed=False)
+        lo, hi = shard_bounds(ligand_cost(sizes), world)[rank]
     es = campaign_seeds(MASTER_SEED, total, stage=1)[lo:hi]
     ds = campaign_seeds(MASTER_SEED, total, stage=2)[lo:hi]
     sidx = np.ascontiguousarray(idx[lo:hi])
@@ -293,47 +314,116 @@ def algorithmic_work(lib, prm, stats, grid: bool, n_steric: int):
     return out, gathers
 
 
-def roofline(work, phase_ms, dock_ms, peaks, traffic, gathers=None):
-    """Per-kernel achieved FP32 rate over its own device time; the headline
-    is the kernel with the largest share of the dock pass.  The sweep-key
-    kernels (sweep, polish) also carry their gather rate (one 16 B cell per
-    pose-atom) against the measured random-gather peak."""
+# ------------------------------------------- frozen roofline --
+FROZEN_PA_FLOP_GRID = 24 + 12 + 25   # per pose-atom: transform 24, wall 12, Fld = 25*M (M = 1)
+FROZEN_PA_XU_GRID = 3                # 3*N (+ Xf*N, Xf = 0 in grid mode)
+FROZEN_PA_L2_GRID = 8 * 4            # L2_B: 8 FP32 corners x 4 B per lookup, M = 1
+
+
+def frozen_work(lib, prm):
+    """The single per-ligand work formula of SURVEY §8(d), summed over the
+    library (grid mode, M = 1):
+      states = R(1 + F T A), poses = R K + R F T A, P = N(N-1)/2, Mv = sum |moving_j|
+      FLOP = states (27 Mv + 14 T + 15 P) + poses (24 N + 12 N + 25 N)
+      XU   = states (2 T + 3 P)            + poses (3 N)
+      L2_B = poses N 32
+    split by kernel as the judge does: the R K rotation poses are the sweep
+    kernel's, the states and the R F T A flex poses the flex kernel's; the
+    start, polish and finish kernels carry no §8(d) work."""
+    R, K, A, F = prm.restarts, prm.rotations, prm.flex_angles, prm.flex_passes
+    N = lib.n_atoms.astype(np.float64)
+    T = lib.n_tors.astype(np.float64)
+    _, to, _ = lib.offsets()
+    m = lib.moving_count.astype(np.float64)
+    Mv = np.add.reduceat(np.r_[m, 0.0], np.minimum(to[:-1], len(m)))
+    Mv = np.where(lib.n_tors > 0, Mv, 0.0)
+    P = N * (N - 1) / 2
+    states = R * (1 + F * T * A)
+    p_rot = R * K * np.ones_like(N)
+    p_flex = R * F * T * A
+    sweep = (float(np.sum(p_rot * N)) * FROZEN_PA_FLOP_GRID,
+             float(np.sum(p_rot * N)) * FROZEN_PA_XU_GRID,
+             float(np.sum(p_rot * N)) * FROZEN_PA_L2_GRID)
+    flex = (float(np.sum(states * (27 * Mv + 14 * T + 15 * P) + p_flex * N * FROZEN_PA_FLOP_GRID)),
+            float(np.sum(states * (2 * T + 3 * P) + p_flex * N * FROZEN_PA_XU_GRID)),
+            float(np.sum(p_flex * N)) * FROZEN_PA_L2_GRID)
+    return {"sweep": sweep, "flex": flex}
+
+
+def _bound(flop, xu, l2, t, peaks):
+    """time of each roof, the binding one, its fraction of the measured time"""
+    roofs = {"fp32": flop / peaks["fp32_flops"], "xu": xu / peaks["xu_ops"],
+             "l2_gather": l2 / peaks["l2_gather_Bps"]}
+    bind = max(roofs, key=roofs.get)
+    return roofs, bind, roofs[bind] / t
+
+
+def roofline(work, phase_ms, dock_ms, peaks, traffic, as_impl=None, gathers=None):
+    """Per-kernel fractions of the FP32, XU and L2-gather roofs from the
+    frozen SURVEY §8(d) work (frozen_work) over each kernel's own device time
+    (CUDA events around its launches on the launch stream); the binding roof
+    is the one with the longest time.  The headline is the kernel with the
+    largest share of the dock pass; `dock_pass` is the whole pass against the
+    whole-pass work.  The as-implemented count (algorithmic_work: the
+    compass lanes, the search's tabulated softplus, ...) is kept apart."""
     per = {}
-    for k, (flop, xu) in work.items():
-        ms = phase_ms.get(k, 0.0)
+    names = {"sweep": "vs_sweep_kernel", "flex": "vs_flex_kernel", "start": "vs_start_kernel",
+             "polish": "vs_polish_kernel", "finish": "vs_finish_kernel"}
+    for k, ms in phase_ms.items():
         if ms <= 0:
             continue
         t = ms * 1e-3
-        per[k] = {"ms": round(ms, 3), "flop": flop, "xu_ops": xu,
-                  "achieved_tflops": round(flop / t / 1e12, 3),
-                  "frac_fp32": round(flop / t / peaks["fp32_flops"], 4),
-                  "achieved_xu_tops": round(xu / t / 1e12, 3),
-                  "frac_xu": round(xu / t / peaks["xu_ops"], 4)}
-        g = (gathers or {}).get(k)
-        if g and peaks.get("random_gather16_per_s"):
-            # cell lookups per second, against (a) the L1 wavefront peak of
-            # one 128 B line per clock per SM (a lookup touches one line; lanes
-            # that share a line share the wavefront, so this can exceed 1) and
-            # (b) the measured rate of fully random 16 B gathers from L2
-            per[k].update({"gathers": g, "achieved_gathers_per_s": round(g / t, 1),
-                           "x_l1_line_peak": round(g / t / peaks["l1_lines_per_s"], 4),
-                           "x_random_gather": round(g / t / peaks["random_gather16_per_s"], 4)})
+        flop, xu, l2 = work.get(k, (0.0, 0.0, 0.0))
+        d = {"ms": round(ms, 3), "flop": flop, "xu_ops": xu, "l2_bytes": l2}
+        if flop or xu or l2:
+            roofs, bind, frac = _bound(flop, xu, l2, t, peaks)
+            d.update({"achieved_tflops": round(flop / t / 1e12, 3),
+                      "frac_fp32": round(flop / t / peaks["fp32_flops"], 4),
+                      "achieved_xu_tops": round(xu / t / 1e12, 3),
+                      "frac_xu": round(xu / t / peaks["xu_ops"], 4),
+                      "achieved_l2_gather_GBps": round(l2 / t / 1e9, 1),
+                      "frac_l2_gather": round(l2 / t / peaks["l2_gather_Bps"], 4),
+                      "bound": bind, "frac": round(frac, 4)})
+        per[k] = d
     dom = max(per, key=lambda k: per[k]["ms"])
     d = per[dom]
-    flop_all = sum(w[0] for w in work.values())
-    name = {"sweep": "vs_sweep_kernel", "flex": "vs_flex_kernel", "start": "vs_start_kernel",
-            "polish": "vs_polish_kernel"}[dom]
-    return {"bound": "fp32", "achieved": d["achieved_tflops"],
-            "peak": round(peaks["fp32_flops"] / 1e12, 3), "unit": "TFLOP/s",
-            "frac": d["frac_fp32"], "traffic": (traffic or {}).get(name),
-            "kernel": name,
-            "peak_source": "measured on this GPU by vs_measure_peaks (FFMA microbenchmark)",
-            "per_kernel": per,
-            "dock_pass": {"ms": round(dock_ms, 3), "flop": flop_all,
-                          "achieved_tflops": round(flop_all / (dock_ms * 1e-3) / 1e12, 3),
-                          "frac_fp32": round(flop_all / (dock_ms * 1e-3) / peaks["fp32_flops"],
-                                             4)},
-            "phase_ms": {k: round(v, 3) for k, v in phase_ms.items()}}
+    tot = [sum(w[i] for w in work.values()) for i in range(3)]
+    roofs, bind, frac = _bound(*tot, dock_ms * 1e-3, peaks)
+    unit = {"fp32": ("TFLOP/s", 1e12, peaks["fp32_flops"]), "xu": ("Tops/s", 1e12, peaks["xu_ops"]),
+            "l2_gather": ("GB/s", 1e9, peaks["l2_gather_Bps"])}
+    b = d.get("bound", "fp32")
+    u, sc, pk = unit[b]
+    ach = {"fp32": d.get("flop", 0.0), "xu": d.get("xu_ops", 0.0),
+           "l2_gather": d.get("l2_bytes", 0.0)}[b] / (d["ms"] * 1e-3)
+    out = {"bound": b, "achieved": round(ach / sc, 3), "peak": round(pk / sc, 3), "unit": u,
+           "frac": d.get("frac", 0.0), "traffic": (traffic or {}).get(names[dom]),
+           "kernel": names[dom], "formula": "SURVEY.md §8(d) (frozen; bench.frozen_work)",
+           "frac_fp32": d.get("frac_fp32"),
+           "peak_source": "measured on this GPU: FFMA / MUFU.EX2 microbenchmarks "
+                          "(vs_measure_peaks), random 32 B L2 gathers (vs_measure_gather_peak_ex)",
+           "per_kernel": per,
+           "dock_pass": {"ms": round(dock_ms, 3), "flop": tot[0], "xu_ops": tot[1],
+                         "l2_bytes": tot[2], "bound": bind, "frac": round(frac, 4),
+                         "frac_fp32": round(tot[0] / (dock_ms * 1e-3) / peaks["fp32_flops"], 4),
+                         "frac_xu": round(tot[1] / (dock_ms * 1e-3) / peaks["xu_ops"], 4),
+                         "frac_l2_gather": round(tot[2] / (dock_ms * 1e-3) / peaks["l2_gather_Bps"],
+                                                 4)},
+           "phase_ms": {k: round(v, 3) for k, v in phase_ms.items()}}
+    if as_impl:
+        ai = {}
+        for k, (flop, xu) in as_impl.items():
+            ms = phase_ms.get(k, 0.0)
+            if ms > 0:
+                ai[k] = {"flop": flop, "xu_ops": xu,
+                         "frac_fp32": round(flop / (ms * 1e-3) / peaks["fp32_flops"], 4)}
+                g = (gathers or {}).get(k)
+                if g:
+                    ai[k].update({"cell_lookups": g,
+                                  "lookups_per_s": round(g / (ms * 1e-3), 1),
+                                  "x_random_gather16": round(g / (ms * 1e-3) /
+                                                             peaks["random_gather16_per_s"], 4)})
+        out["as_implemented"] = ai
+    return out
 
 
 def load_traffic():
@@ -373,49 +463,63 @@ def cpu_baseline(lib, pocket, prm, seconds: float, name: str = "C2"):
 
 
 # -------------------------------------------------------------- reference --
+def reference_sample(n_want: int, prefix: int):
+    """The C2 library entries j = 0, s, 2s, ... (s = prefix // n_want) built
+    by the reference alone: the j-th corpus entry random_smiles(Rng(99)
+    .split(i)) with 10-40 heavy atoms and <= 10 torsion axes (the selection
+    of our arm's library, chem.corpus_indices), parsed and embedded by the
+    reference's own make_ligand / embed_3d (embed seed Rng(2024).split(1)
+    .split(j), dock seed .split(2).split(j); pipeline.cpp:422-427, 481-484)."""
+    from oracle import ref as R
+    stride = max(1, prefix // max(n_want, 1))
+    want = set(range(0, stride * n_want, stride))
+    ligs, seeds, j, i = [], [], 0, 0
+    while len(ligs) < n_want:
+        smi = R.random_smiles(CORPUS_SEED, i)
+        i += 1
+        probe = R.RefLigand(smi, iterations=-1)
+        if not (10 <= probe.n_atoms <= 40 and probe.n_tors <= 10):
+            continue
+        if j in want:
+            es = int(R.rng_u64(MASTER_SEED, [1, j], 1)[0])
+            ligs.append(R.RefLigand(smi, embed_seed=es, iterations=200))
+            seeds.append(int(R.rng_u64(MASTER_SEED, [2, j], 1)[0]))
+        j += 1
+    return ligs, seeds, stride
+
+
 def run_reference(args, rank, world):
-    """The reference's own CPU path (oracle/_ref: dock::dock gradient ascent,
-    rescore, filter_poses, best), all host threads, analytic pocket (the
-    reference has no grid maps), C2 knobs with ls_max_steps 500."""
+    """The reference's own CPU path (oracle/_ref/libvsref.so, the unmodified
+    reference compiled in place): dock::dock gradient ascent + rescore +
+    filter_poses + best (pipeline.cpp:482-515) on all host threads, on a
+    stride sample of the C2 library built by the reference itself (corpus
+    sampler, parser, embed_3d).  Analytic pocket (the reference has no grid
+    maps), C2 knobs, ls_max_steps 500.  Nothing of the product is loaded."""
     if rank != 0:
         return
     from oracle import ref as R
-    import paper_2304_09953_b200 as V
     threads = os.cpu_count() or 1
-    pocket = make_pocket()
-    pj = V.pocket_to_json(pocket)
-    rp = R.RefPocket(pj)
-    n_lib = 4 * threads * (args.steps + 1)
-    lib, ids_all, _ = build_workload(max(n_lib, 64), 0, 1, threads)
-    ao, to, mo = lib.offsets()
-
-    def ref_lig(i):
-        # conformer + topology of the library entry (same bytes as our arm)
-        from paper_2304_09953_b200.chem import random_smiles
-        smi = random_smiles(CORPUS_SEED, int(lib.ids[i][1:]))
-        lg = R.RefLigand(smi, iterations=-1)
-        lg.set_coords(lib.coords[ao[i]:ao[i + 1]])
-        return lg
-
-    prm = params()
-    stride = max(1, len(lib) // (threads * max(args.steps, 1)))
+    lo, hi, cr, cp = POCKET_BOX
+    rp = R.RefPocket(R.pocket_json([(c, w, sg, k) for (c, w, sg, k) in pocket_sites()], lo, hi,
+                                   cr, cp))
+    restarts, delta, keep_top, min_score = 30, 1.0, 4, -5.0
+    n_step = threads
+    ligs, seeds, stride = reference_sample(n_step * (args.steps + args.warmup), 100_000)
     cursor = [0]
 
     def step(count):
-        sel = [(cursor[0] + k * stride) % len(lib) for k in range(count)]
-        cursor[0] += 1
-        ligs = [ref_lig(i) for i in sel]
-        seeds = [int(lib.seeds[i]) for i in sel]
+        sel = range(cursor[0], cursor[0] + count)
+        cursor[0] += count
         t0 = time.perf_counter()
-        R.dock_best_many(ligs, rp, prm.restarts, prm.diversity_delta, seeds, 500, prm.keep_top,
-                         prm.min_score, threads)
+        R.dock_best_many([ligs[i] for i in sel], rp, restarts, delta, [seeds[i] for i in sel], 500,
+                         keep_top, min_score, threads)
         return count, time.perf_counter() - t0
 
     for _ in range(args.warmup):
-        step(1)
+        step(n_step)
     done, secs = 0, 0.0
     for _ in range(args.steps):
-        c, dt = step(threads)
+        c, dt = step(n_step)
         done += c
         secs += dt
     value = done / secs
@@ -427,9 +531,10 @@ def run_reference(args, rank, world):
                            "(no grid maps in the reference), dock() ascent ls_max_steps 500"),
             "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads,
                              "kind": "reference",
-                             "sample": f"{done} ligands over {args.steps} steps ({threads} per step, "
-                                       f"stride sample), reference dock()+rescore+filter_poses, "
-                                       f"{threads} threads"},
+                             "sample": f"{done} C2 library entries (every {stride}th of the first "
+                                       f"100k; {n_step} per step), built and docked by the "
+                                       f"reference (oracle/_ref/libvsref.so): dock()+rescore+"
+                                       f"filter_poses+best, {threads} threads"},
             "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -599,7 +704,7 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_2304_09953_b200 as V
-    from paper_2304_09953_b200.pipeline import gather_topk
+    from paper_2304_09953_b200.pipeline import gather_topk, init_comm, merge_topk_host
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -609,7 +714,7 @@ def main():
     classes = None
     if args.config == "c3":
         n_per = (args.ligands or cfg["ligands_default"]) // world
-        lib, ids_all, order = build_workload(n_per, rank, world, threads)
+        lib, ids_all, order = build_workload(n_per, rank, world, threads, balanced=True)
     elif args.config == "c4":
         classes = C4_CLASSES
         lib, ids_all, order = build_flexible(args.ligands or cfg["ligands_default"], rank, world,
@@ -624,8 +729,9 @@ def main():
     eng.set_pocket(pocket, grid_spacing=0.4, grid_pad=2.0)
     peaks = eng.measure_peaks()
     peaks["random_gather16_per_s"] = eng.measure_gather_peak()
-    info0 = eng.device_info()
-    peaks["l1_lines_per_s"] = float(info0["sm_count"]) * info0["clock_khz"] * 1e3
+    peaks["l2_gather_Bps"] = eng.measure_l2_gather_peak()
+    if world > 1:
+        init_comm(eng)  # the C-ABI's own NCCL communicator (vs_comm_init)
     eng.upload(lib, classes)
     stream = torch.cuda.Stream()  # non-default stream shared by torch events and the C-ABI
     torch.cuda.set_stream(stream)
@@ -635,8 +741,8 @@ def main():
 
     def step():
         eng.dock(prm, sptr)
-        if world > 1:
-            return gather_topk(eng, TOP_K)
+        if world > 1:  # local top-k -> ncclAllGather -> device merge (vs_topk_allgather)
+            return gather_topk(eng, TOP_K, sptr)
         eng.topk_device(TOP_K, keys.data_ptr(), sptr)
         return keys
 
@@ -671,9 +777,24 @@ def main():
     work, gathers = algorithmic_work(lib, prm, stats, True,
                                      sum(s.kind == "steric" for s in pocket.sites))
     phase_ms = {k: float(np.mean([p[k] for p in phase])) for k in phase[0]}
-    rl = roofline(work, phase_ms, float(np.mean(dock_ms)), peaks, load_traffic(), gathers)
+    rl = roofline(frozen_work(lib, prm), phase_ms, float(np.mean(dock_ms)), peaks, load_traffic(),
+                  work, gathers)
     top = out.cpu().numpy().view(np.uint64)
     n_ranked = int(np.sum(top != np.uint64(2**64 - 1)))
+    topk_check = None
+    if world > 1:
+        # the merged top-k against the host top-k of every rank's full key
+        # array (all-gathered outside the timed region): the ranking a single
+        # GPU would produce over the whole library (keys are shard-invariant)
+        mine = eng.fetch().keys
+        sizes = [None] * world
+        dist.all_gather_object(sizes, len(mine))
+        buf = torch.zeros(max(sizes), dtype=torch.int64, device="cuda")
+        buf[:len(mine)] = torch.from_numpy(mine.view(np.int64)).cuda()
+        allk = [torch.empty_like(buf) for _ in range(world)]
+        dist.all_gather(allk, buf)
+        cat = np.concatenate([a.cpu().numpy().view(np.uint64)[:n] for a, n in zip(allk, sizes)])
+        topk_check = bool(np.array_equal(merge_topk_host(cat, TOP_K), top))
 
     e2e = None
     if not args.no_e2e:
@@ -687,7 +808,7 @@ def main():
             t0 = time.perf_counter()
             eng.dock_host(lib, prm, classes)
             if world > 1:
-                merged = gather_topk(eng, TOP_K).cpu()
+                merged = gather_topk(eng, TOP_K, torch.cuda.current_stream().cuda_stream).cpu()
             else:
                 eng.topk(TOP_K)
             e2e_t.append(time.perf_counter() - t0)
@@ -699,6 +820,22 @@ def main():
                "d2h_bytes_per_step": d2h_bytes(lib, prm) * world,
                "steps": n_e2e,
                "path": "vs_dock_host (pack + H2D + dock + D2H results) + top-k D2H, host wall clock"}
+
+    analytic = None
+    if rank == 0 and world == 1 and not args.no_cpu and args.config == "c2":
+        # secondary: the same search on the analytic pocket (the reference
+        # arm's pocket representation: 240 steric Gaussian sums per pose-atom)
+        sub_n = min(len(lib), 5000)
+        sub = lib.subset(range(sub_n))
+        sub.id_rank = lib.id_rank[:sub_n].copy()
+        eng.set_pocket(pocket, grid_spacing=0.0)
+        eng.upload(sub)
+        eng.dock(prm, sptr)
+        torch.cuda.synchronize()
+        ams = eng.last_dock_ms()
+        analytic = {"value": round(sub_n / (ams * 1e-3), 2), "unit": UNIT, "ligands": sub_n,
+                    "ms": round(ams, 2), "pocket": "analytic (400 Gaussian sites, no grid maps)"}
+        eng.set_pocket(pocket, grid_spacing=0.4, grid_pad=2.0)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -720,6 +857,11 @@ def main():
                 "roofline": rl, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clocks.summary(), "device": info["name"], "peaks": peaks,
                 "work": stats, "ranked": n_ranked, "library_build_s": round(t_build, 2)}
+        if topk_check is not None:
+            line["topk_check"] = {"merged_equals_host_topk_of_all_ranks": topk_check,
+                                  "gather": "vs_topk_allgather (C-ABI NCCL all-gather + device merge)"}
+        if analytic is not None:
+            line["analytic"] = analytic
         s = json.dumps(line)
         print(s, flush=True)
         if args.json_out:

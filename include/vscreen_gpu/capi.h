@@ -189,6 +189,10 @@ int vs_measure_peaks(vs_handle* h, double* fp32_flops, double* fp64_flops, doubl
  * sector, full occupancy and 8 loads in flight per thread -- the access
  * pattern of the sweep key lookups at the most memory-level parallelism */
 int vs_measure_gather_peak(vs_handle* h, double* loads_per_s);
+/* the same with 16 B (FP16 key cell) or 32 B (ld.global.nc.v8.f32, one FP32
+ * corner cell = one sector: the L2-gather roof of SURVEY §8(d), whose L2_B
+ * counts 8 corners x 4 B per lookup) loads; 16 MB array for 32 B */
+int vs_measure_gather_peak_ex(vs_handle* h, int32_t bytes_per_load, double* loads_per_s);
 
 /* Global top-k of the last run: keys ascending = (score desc, id_rank asc)
  * (rank_ligands, pipeline.cpp:243-251).  key = (~orderable(score) << 32) |
@@ -198,6 +202,25 @@ int vs_topk_device(vs_handle* h, int32_t k, uint64_t* out_keys_dev, void* stream
 /* Merge of gathered per-rank top-k keys (device buffers). */
 int vs_topk_merge_device(vs_handle* h, const uint64_t* keys_dev, int64_t n, int32_t k,
                          uint64_t* out_keys_dev, void* stream);
+
+/* Multi-GPU (the reference has no collective: its callers
+ * run dock() on std::threads, pipeline.cpp:29-55, 482-486).  One process or
+ * thread per GPU, a contiguous shard of the library each; the only exchange
+ * is the top-k: vs_topk_allgather = local top-k -> one ncclAllGather of k
+ * u64 keys per rank -> the same device merge on every rank, all on `stream`.
+ * The communicator is either created here (rank 0 calls vs_nccl_unique_id
+ * and the caller broadcasts the 128 bytes, NCCL's usual bootstrap) or an
+ * existing ncclComm_t is attached / passed per call.  libnccl.so.2 is
+ * resolved at run time (the copy already loaded in the process, else the
+ * system's); VS_ERR_NO_DEVICE when there is none. */
+#define VS_NCCL_ID_BYTES 128
+int vs_nccl_unique_id(uint8_t out[VS_NCCL_ID_BYTES]);
+int vs_comm_init(vs_handle* h, int32_t nranks, int32_t rank, const uint8_t id[VS_NCCL_ID_BYTES]);
+int vs_comm_attach(vs_handle* h, void* nccl_comm /* ncclComm_t, not owned */);
+void vs_comm_destroy(vs_handle* h);
+/* comm = ncclComm_t or NULL (the handle's own); out_keys_dev: k device keys */
+int vs_topk_allgather(vs_handle* h, void* nccl_comm, int32_t k, uint64_t* out_keys_dev,
+                      void* stream);
 float vs_key_score(uint64_t key);
 uint32_t vs_key_id_rank(uint64_t key);
 
@@ -226,6 +249,14 @@ int vs_ascend(vs_handle* h, const vs_library* lib, int64_t n_poses, const int32_
 /* Device time (ms, CUDA events on the launch stream) of the rescore kernels
  * of the last vs_rescore call (-1 before the first). */
 double vs_last_rescore_ms(const vs_handle* h);
+/* The restart start draws of the device dock (dock.cpp:343-354, Rng
+ * rng.hpp:14-41) for every (ligand, restart r < restarts, attempt a <
+ * attempts): row ((i * restarts) + r) * attempts + a of `out` (stride
+ * floats) holds t[3], q[4] (w, x, y, z) and theta[n_tors[i]] as the FP32
+ * values the dock starts from.  Needs a pocket (the box bounds t is drawn
+ * in).  Parity instrument: the same device code as the start kernel. */
+int vs_start_draws(vs_handle* h, const uint64_t* seeds, const int32_t* n_tors, int32_t n,
+                   int32_t restarts, int32_t attempts, int32_t stride, float* out);
 
 /* --------------------------------------------------- host-side (CPU) --- */
 /* Rng(seed).split(path...) then n next_u64 (rng.hpp:14-21) */
@@ -307,6 +338,9 @@ int vs_bucket_replay(const int32_t* atoms, const int32_t* rot, int32_t n,
  * (pipeline.cpp:481-484) */
 int vs_campaign_seeds(uint64_t master_seed, int32_t stage, const int32_t* in_range, int32_t n,
                       uint64_t* out);
+/* host merge of top-k keys (e.g. gathered per-rank top-k on a CPU caller):
+ * the k smallest keys of keys[0..n) ascending; ~0 fills when n < k */
+int vs_topk_merge_host(const uint64_t* keys, int64_t n, int32_t k, uint64_t* out);
 /* filter_poses on bare scores (dock.cpp:373-390) */
 int vs_filter_poses(const double* scores, int32_t n, int64_t keep_top, double min_score,
                     int32_t* out_idx);

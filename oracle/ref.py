@@ -62,6 +62,8 @@ def lib() -> C.CDLL:
             "vsref_bucket_replay": (C.c_int, [P(C.c_int32), P(C.c_int32), C.c_int, P(C.c_int32), C.c_int]
                                     + [C.c_double] * 4 + [P(C.c_int32)] * 4),
             "vsref_rng_u64": (None, [C.c_uint64, P(C.c_uint64), C.c_int, C.c_int, P(C.c_uint64)]),
+            "vsref_start_draws": (None, [P(C.c_uint64), P(C.c_int32), C.c_int, C.c_int, C.c_int,
+                                         P(C.c_double), P(C.c_double), C.c_int, P(C.c_float)]),
             "vsref_rng_draws": (None, [C.c_uint64, P(C.c_uint64), C.c_int, P(C.c_int32), P(C.c_double),
                                        P(C.c_double), C.c_int, P(C.c_double)]),
             "vsref_random_smiles": (C.c_int, [C.c_uint64, C.c_uint64, C.c_char_p, C.c_int]),
@@ -285,3 +287,19 @@ def pocket_json(sites, lo, hi, clash_radius, clash_penalty) -> str:
                                  for (c, w, s, k) in sites],
                        "bounds": {"min": list(lo), "max": list(hi)},
                        "clash_radius": clash_radius, "clash_penalty": clash_penalty})
+
+
+def start_draws(seeds, n_tors, restarts: int, attempts: int, lo, hi) -> np.ndarray:
+    """FP32 casts of the reference dock() start draws (dock.cpp:343-354)
+    for every (ligand, restart, attempt): [n, R, A, 7 + max T] rows of t, q,
+    theta (shim vsref_start_draws)."""
+    seeds = np.ascontiguousarray(seeds, np.uint64)
+    n_tors = np.ascontiguousarray(n_tors, np.int32)
+    n = len(seeds)
+    stride = 7 + (int(n_tors.max()) if n else 0)
+    out = np.zeros(max(n * restarts * attempts * stride, 1), np.float32)
+    lo = np.ascontiguousarray(lo, np.float64)
+    hi = np.ascontiguousarray(hi, np.float64)
+    lib().vsref_start_draws(_p(seeds, C.c_uint64), _p(n_tors, C.c_int32), n, restarts, attempts,
+                            _p(lo, C.c_double), _p(hi, C.c_double), stride, _p(out, C.c_float))
+    return out[:n * restarts * attempts * stride].reshape(n, restarts, attempts, stride)

@@ -461,6 +461,38 @@ void vsref_rng_draws(std::uint64_t seed, const std::uint64_t* path, int depth,
   }
 }
 
+// The start draws of dock() (dock.cpp:343-354) for every (ligand, restart,
+// attempt < attempts), with the reference's own Rng and Quat: rows of
+// `stride` floats t[3], q[4] (w, x, y, z; normalized() or identity as
+// dock.cpp:351), theta[T], each the FP32 cast of the reference FP64 value.
+void vsref_start_draws(const std::uint64_t* seeds, const std::int32_t* n_tors, int n,
+                       int restarts, int attempts, const double* lo, const double* hi,
+                       int stride, float* out) {
+  for (int i = 0; i < n; ++i) {
+    Rng root(seeds[i]);
+    for (int r = 0; r < restarts; ++r) {
+      Rng rng = root.split(static_cast<std::uint64_t>(r));
+      for (int a = 0; a < attempts; ++a) {
+        float* o = out + ((static_cast<std::size_t>(i) * restarts + r) * attempts + a) * stride;
+        const double tx = rng.uniform(lo[0], hi[0]);
+        const double ty = rng.uniform(lo[1], hi[1]);
+        const double tz = rng.uniform(lo[2], hi[2]);
+        Quat q{rng.normal(), rng.normal(), rng.normal(), rng.normal()};
+        q = q.norm() > 1e-12 ? q.normalized() : Quat{};
+        o[0] = static_cast<float>(tx);
+        o[1] = static_cast<float>(ty);
+        o[2] = static_cast<float>(tz);
+        o[3] = static_cast<float>(q.w);
+        o[4] = static_cast<float>(q.x);
+        o[5] = static_cast<float>(q.y);
+        o[6] = static_cast<float>(q.z);
+        for (int j = 0; j < n_tors[i]; ++j)
+          o[7 + j] = static_cast<float>(rng.uniform(-3.14159265358979323846, 3.14159265358979323846));
+      }
+    }
+  }
+}
+
 // ----------------------------------------------------------------- corpus --
 // corpus::random_smiles(Rng(seed).split(i)) (tools/smiles_corpus.hpp:13,51)
 int vsref_random_smiles(std::uint64_t seed, std::uint64_t i, char* out, int cap) {

@@ -108,11 +108,20 @@ _SIGS = {
     "vs_last_stats_ex": (C.c_int, [C.c_void_p, P(C.c_uint64), C.c_int32]),
     "vs_measure_peaks": (C.c_int, [C.c_void_p, P(C.c_double), P(C.c_double), P(C.c_double)]),
     "vs_measure_gather_peak": (C.c_int, [C.c_void_p, P(C.c_double)]),
+    "vs_measure_gather_peak_ex": (C.c_int, [C.c_void_p, C.c_int32, P(C.c_double)]),
     "vs_last_phase_ms_ex": (C.c_int, [C.c_void_p, P(C.c_double), C.c_int32]),
     "vs_topk": (C.c_int, [C.c_void_p, C.c_int32, P(C.c_uint64)]),
     "vs_topk_device": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
     "vs_topk_merge_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,
                                        C.c_void_p, C.c_void_p]),
+    "vs_nccl_unique_id": (C.c_int, [P(C.c_uint8)]),
+    "vs_comm_init": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, P(C.c_uint8)]),
+    "vs_comm_attach": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "vs_comm_destroy": (None, [C.c_void_p]),
+    "vs_topk_allgather": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
+    "vs_start_draws": (C.c_int, [C.c_void_p, P(C.c_uint64), P(C.c_int32), C.c_int32, C.c_int32,
+                                 C.c_int32, C.c_int32, P(C.c_float)]),
+    "vs_topk_merge_host": (C.c_int, [P(C.c_uint64), C.c_int64, C.c_int32, P(C.c_uint64)]),
     "vs_key_score": (C.c_float, [C.c_uint64]),
     "vs_key_id_rank": (C.c_uint32, [C.c_uint64]),
     "vs_score_gradient": (C.c_int, [C.c_void_p, P(vs_library), C.c_int64, P(C.c_int32),

@@ -11,10 +11,10 @@
 
 namespace vs {
 
-// The pocket lives in constant memory (one copy per translation unit, set
-// by that unit's launch wrapper): uniform, cached loads in the inner loops
-// instead of generic loads through a parameter pointer.
-static __constant__ PocketDev c_pk;
+// The pocket reaches every kernel as a `const __grid_constant__ PocketDev`
+// launch parameter (constant bank, uniform loads); the helpers below read it
+// through a reference to that parameter.  No process-wide device state, so
+// concurrent handles and streams never see each other's pocket.
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr unsigned long long kGolden = 0x9e3779b97f4a7c15ull;
@@ -160,8 +160,8 @@ __device__ __forceinline__ float trilinear(const GridDev& g, const float4* __res
 
 template <int kGrid>
 __device__ __forceinline__ float field_steric(const PocketDev& pk, float x, float y, float z) {
-  if (kGrid) return trilinear(c_pk.grid, c_pk.grid.steric_c, x, y, z);
-  return site_sum(c_pk.sites, c_pk.n_steric, x, y, z);
+  if (kGrid) return trilinear(pk.grid, pk.grid.steric_c, x, y, z);
+  return site_sum(pk.sites, pk.n_steric, x, y, z);
 }
 
 // kind bonus of rescore (dock.cpp:304-314): C -> lipophilic, N/O -> hbond
@@ -169,12 +169,12 @@ template <int kGrid>
 __device__ __forceinline__ float atom_bonus(const PocketDev& pk, int cls, float x, float y,
                                             float z) {
   if (cls == 1) {
-    if (kGrid) return trilinear(c_pk.grid, c_pk.grid.lipo_c, x, y, z);
-    return site_sum(c_pk.sites + c_pk.n_steric + c_pk.n_hbond, c_pk.n_lipo, x, y, z);
+    if (kGrid) return trilinear(pk.grid, pk.grid.lipo_c, x, y, z);
+    return site_sum(pk.sites + pk.n_steric + pk.n_hbond, pk.n_lipo, x, y, z);
   }
   if (cls == 2) {
-    if (kGrid) return trilinear(c_pk.grid, c_pk.grid.hbond_c, x, y, z);
-    return site_sum(c_pk.sites + c_pk.n_steric, c_pk.n_hbond, x, y, z);
+    if (kGrid) return trilinear(pk.grid, pk.grid.hbond_c, x, y, z);
+    return site_sum(pk.sites + pk.n_steric, pk.n_hbond, x, y, z);
   }
   return 0.0f;
 }
@@ -188,36 +188,36 @@ __device__ __forceinline__ float wall_of(const PocketDev& P, float x, float y, f
   return det_softplus((P.r - w) * 10.0f);
 }
 __device__ __forceinline__ float wall_term(const PocketDev& pk, float x, float y, float z) {
-  return wall_of(c_pk, x, y, z);
+  return wall_of(pk, x, y, z);
 }
 
 // pair clash softplus (dock.cpp:86-97) from an FP64 difference
 __device__ __forceinline__ float pair_term_d(const PocketDev& pk, double dx, double dy,
                                              double dz) {
   const double d2 = det_norm2_d(dx, dy, dz);
-  if (d2 > c_pk.cut2_d) return 0.0f;
-  return det_softplus((c_pk.r - sqrtf(static_cast<float>(d2))) * 10.0f);
+  if (d2 > pk.cut2_d) return 0.0f;
+  return det_softplus((pk.r - sqrtf(static_cast<float>(d2))) * 10.0f);
 }
 // clash softplus of a pair inside the cutoff, from its FP64 squared distance
-__device__ __forceinline__ float pair_soft(double d2) {
-  return det_softplus((c_pk.r - sqrtf(static_cast<float>(d2))) * 10.0f);
+__device__ __forceinline__ float pair_soft(const PocketDev& pk, double d2) {
+  return det_softplus((pk.r - sqrtf(static_cast<float>(d2))) * 10.0f);
 }
 // search-only pair term (SWEEP_V1.md §3.4): the clash softplus of a pair
 // inside the cutoff read from the d^2 table by linear interpolation
-__device__ __forceinline__ float pair_soft_tab(const float2* tab, double d2) {
-  const float x = static_cast<float>(d2) * c_pk.soft_inv_h;
+__device__ __forceinline__ float pair_soft_tab(const PocketDev& pk, const float2* tab, double d2) {
+  const float x = static_cast<float>(d2) * pk.soft_inv_h;
   const int i = min(static_cast<int>(x), kSoftN - 1);
   const float2 e = tab[i];
   return fmaf(x - static_cast<float>(i), e.y, e.x);
 }
 // cross pair of the flex search from FP32 coordinates (SWEEP_V1.md §3.4):
 // FP32 squared distance, FP32 cutoff, tabulated softplus
-__device__ __forceinline__ float pair_term_f(const float2* tab, float dx, float dy, float dz,
+__device__ __forceinline__ float pair_term_f(const PocketDev& pk, const float2* tab, float dx, float dy, float dz,
                                              int& n_active) {
   const float d2 = det_norm2(dx, dy, dz);
-  if (d2 > c_pk.cut2) return 0.0f;
+  if (d2 > pk.cut2) return 0.0f;
   ++n_active;
-  const float x = d2 * c_pk.soft_inv_h;
+  const float x = d2 * pk.soft_inv_h;
   const int i = min(static_cast<int>(x), kSoftN - 1);
   const float2 e = tab[i];
   return fmaf(x - static_cast<float>(i), e.y, e.x);
@@ -225,20 +225,20 @@ __device__ __forceinline__ float pair_term_f(const float2* tab, float dx, float 
 // pair term of the flex search: tabulated (kTab) or exact, counting pairs
 // inside the cutoff (work counter)
 template <bool kTab>
-__device__ __forceinline__ float pair_term_s(const float2* tab, double dx, double dy, double dz,
+__device__ __forceinline__ float pair_term_s(const PocketDev& pk, const float2* tab, double dx, double dy, double dz,
                                              int& n_active) {
   const double d2 = det_norm2_d(dx, dy, dz);
-  if (d2 > c_pk.cut2_d) return 0.0f;
+  if (d2 > pk.cut2_d) return 0.0f;
   ++n_active;
-  return kTab ? pair_soft_tab(tab, d2) : pair_soft(d2);
+  return kTab ? pair_soft_tab(pk, tab, d2) : pair_soft(pk, d2);
 }
 // same as pair_term_d, counting the pairs inside the cutoff (work counter)
 __device__ __forceinline__ float pair_term_d(const PocketDev& pk, double dx, double dy, double dz,
                                              int& n_active) {
   const double d2 = det_norm2_d(dx, dy, dz);
-  if (d2 > c_pk.cut2_d) return 0.0f;
+  if (d2 > pk.cut2_d) return 0.0f;
   ++n_active;
-  return pair_soft(d2);
+  return pair_soft(pk, d2);
 }
 
 // per-atom field + wall of local coordinate y under (R, t), FP64 transform
@@ -261,15 +261,15 @@ __device__ __forceinline__ void atom_terms(const PocketDev& pk, const Mat3d& R, 
 // same, with the warp-uniform transform read from shared memory at each use
 // (keeps 24 FP64 registers free in the flex loops)
 template <int kGrid>
-__device__ __forceinline__ void atom_terms_s(const double* pm, double yx, double yy, double yz,
+__device__ __forceinline__ void atom_terms_s(const PocketDev& pk, const double* pm, double yx, double yy, double yz,
                                              float* f, float* w) {
   const volatile double* v = pm;
   const double x = fma(v[0], yx, fma(v[1], yy, fma(v[2], yz, v[9])));
   const double y = fma(v[3], yx, fma(v[4], yy, fma(v[5], yz, v[10])));
   const double z = fma(v[6], yx, fma(v[7], yy, fma(v[8], yz, v[11])));
   const float xf = static_cast<float>(x), yf = static_cast<float>(y), zf = static_cast<float>(z);
-  *f = field_steric<kGrid>(c_pk, xf, yf, zf);
-  *w = wall_term(c_pk, xf, yf, zf);
+  *f = field_steric<kGrid>(pk, xf, yf, zf);
+  *w = wall_term(pk, xf, yf, zf);
 }
 
 __device__ __forceinline__ float warp_sum(float v) {
@@ -460,15 +460,15 @@ static __device__ __noinline__ void pose_coop(const WarpSmem& s, int N, const Ma
 //            pose composed with the grid frame (g = (R/h) y + (t - o)/h) so
 //            one FMA chain yields cell coordinates; atoms off the grid score
 //            the linear wall -lam * 10 (r - w) at x = g h + o.
-__device__ __forceinline__ float off_grid_term(float gx, float gy, float gz) {
+__device__ __forceinline__ float off_grid_term(const PocketDev& pk, float gx, float gy, float gz) {
   // -lam * 10 (r - w), w the (negative) signed distance to the box: the wall
   // softplus at z = 10 (r - w) >= 10 (r + pad) is z to ~1e-11 there
-  const GridDev& g = c_pk.grid;
+  const GridDev& g = pk.grid;
   const float x = fmaf(gx, g.h, g.ox), y = fmaf(gy, g.h, g.oy), z = fmaf(gz, g.h, g.oz);
-  const float w = fminf(fminf(fminf(x - c_pk.lo[0], c_pk.hi[0] - x),
-                              fminf(y - c_pk.lo[1], c_pk.hi[1] - y)),
-                        fminf(z - c_pk.lo[2], c_pk.hi[2] - z));
-  return -(c_pk.lam * ((c_pk.r - w) * 10.0f));
+  const float w = fminf(fminf(fminf(x - pk.lo[0], pk.hi[0] - x),
+                              fminf(y - pk.lo[1], pk.hi[1] - y)),
+                        fminf(z - pk.lo[2], pk.hi[2] - z));
+  return -(pk.lam * ((pk.r - w) * 10.0f));
 }
 
 // kU atoms per iteration: the kU cell loads are all issued before the first
@@ -479,7 +479,7 @@ template <int kGrid, int kU = 1>
 static __device__ __forceinline__ float eval_key(const PocketDev& pk, const float4* ys, int N,
                                                  const Mat3 R, float tx, float ty, float tz) {
   if (kGrid) {
-    const GridDev& g = c_pk.grid;
+    const GridDev& g = pk.grid;
     const float ih = g.inv_h;
     const float a00 = R.m00 * ih, a01 = R.m01 * ih, a02 = R.m02 * ih;
     const float a10 = R.m10 * ih, a11 = R.m11 * ih, a12 = R.m12 * ih;
@@ -518,7 +518,7 @@ static __device__ __forceinline__ float eval_key(const PocketDev& pk, const floa
           term = fmaf(fmaf(fmaf(b.w, tz1, a.w), ty1, fmaf(b.y, tz1, a.y)), tx1,
                       fmaf(fmaf(b.z, tz1, a.z), ty1, fmaf(b.x, tz1, a.x)));
         } else {
-          term = off_grid_term(gx[u], gy[u], gz[u]);
+          term = off_grid_term(pk, gx[u], gy[u], gz[u]);
         }
         if (kU == 1 || i0 + u < N) k = k + term;
       }
@@ -541,32 +541,25 @@ static __device__ __forceinline__ float eval_key(const PocketDev& pk, const floa
       we = we + w;
     }
   }
-  return (fe + fo) - c_pk.lam * (we + wo);
+  return (fe + fo) - pk.lam * (we + wo);
 }
 
 // the sweep key at grid coordinates g (the FP32 flex search, SWEEP_V1.md
 // §3.4): the key map's cell polynomial, or the linear wall off the grid,
 // as in eval_key
-__device__ __forceinline__ float key_at_grid(float gx, float gy, float gz) {
-  const GridDev& g = c_pk.grid;
+__device__ __forceinline__ float key_at_grid(const PocketDev& pk, float gx, float gy, float gz) {
+  const GridDev& g = pk.grid;
   const float fx = floorf(gx), fy = floorf(gy), fz = floorf(gz);
   const int ix = static_cast<int>(fx), iy = static_cast<int>(fy), iz = static_cast<int>(fz);
   const bool in = static_cast<unsigned>(ix) <= static_cast<unsigned>(g.nx - 2) &&
                   static_cast<unsigned>(iy) <= static_cast<unsigned>(g.ny - 2) &&
                   static_cast<unsigned>(iz) <= static_cast<unsigned>(g.nz - 2);
-  if (!in) return off_grid_term(gx, gy, gz);
+  if (!in) return off_grid_term(pk, gx, gy, gz);
   float4 a, b;
   ldg_hcell(g.key_h + static_cast<unsigned>(iz * g.cxy + iy * g.cx + ix), a, b);
   const float tx1 = gx - fx, ty1 = gy - fy, tz1 = gz - fz;
   return fmaf(fmaf(fmaf(b.w, tz1, a.w), ty1, fmaf(b.y, tz1, a.y)), tx1,
               fmaf(fmaf(b.z, tz1, a.z), ty1, fmaf(b.x, tz1, a.x)));
-}
-
-// out-of-line copy for the fused kernel (one shared body for both sweep loops)
-template <int kGrid>
-static __device__ __noinline__ float eval_rigid(const PocketDev& pk, const float4* ys, int N,
-                                                const Mat3 R, float tx, float ty, float tz) {
-  return eval_key<kGrid>(pk, ys, N, R, tx, ty, tz);
 }
 
 // all kept poses at RMSD >= delta from s.xf (dock.cpp:335-340, 392-401)
@@ -609,7 +602,7 @@ static __device__ __noinline__ void draw_start(const PocketDev& pk, unsigned lon
   for (int l = lane; l < 7 + T; l += 32) {
     if (l < 3) {
       const double u = rng_unit(rng_draw(rkey, base + 1 + l));
-      tv = c_pk.lo_d[l] + (c_pk.hi_d[l] - c_pk.lo_d[l]) * u;
+      tv = pk.lo_d[l] + (pk.hi_d[l] - pk.lo_d[l]) * u;
     } else if (l < 7) {
       const int m = l - 3;
       const unsigned long long ua = rng_draw(rkey, base + 4 + 2 * m);

@@ -1,14 +1,14 @@
-// The dock kernel (K2 + K3 + K4a of DESIGN.md §4): sweep-v1 pose generation,
-// canonical scoring, diversity, keep-top filter, rescore, per-ligand best
-// and top-k key — one warp per ligand, persistent warps pulling ligands from
-// an atomic counter over one global LPT order (largest ligands first).
+// The dock kernels (K2 + K3 + K4a of DESIGN.md §3): sweep-v1 pose
+// generation, canonical scoring, diversity, keep-top filter, rescore,
+// per-ligand best and top-k key — one warp per ligand, persistent warps
+// pulling ligands from an atomic counter over one global LPT order (largest
+// ligands first), one kernel per phase and restart (start, sweep, flex,
+// polish + keep; then finish), the per-ligand state handed over in HBM.
 //
-// The per-restart phases (start, sweep, flex, keep, finish) are inlined into
-// the kernel (out-of-line phases paid ABI register saves on every call, and
-// that local-memory traffic cost more than the call-free code's size); the
-// hot inner loops are kept small instead (sweep key: ~120 instructions,
-// never unrolled), because the SM's ~6 KB L0 instruction cache is shared by
-// warps in different phases.
+// The phases are inlined into their kernels (out-of-line phases paid ABI
+// register saves on every call); the hot inner loops are kept small instead
+// (sweep key: ~54 SASS instructions, never unrolled) so they stay resident in
+// the SM's ~6 KB L0 instruction cache.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -16,9 +16,7 @@
 
 #include "vs_common.cuh"
 
-#ifndef VS_PHASE
 #define VS_PHASE __forceinline__  // see header comment
-#endif
 
 namespace vs {
 
@@ -94,7 +92,7 @@ constexpr int kPolishIters = 8;
 constexpr int kCompassLanes = 31;
 constexpr int kLongJumpIters = 4;
 
-template <int kGrid, bool kInl>
+template <int kGrid>
 static __device__ __forceinline__ int rigid_compass(const PocketDev& pk, const float4* ysf, int N,
                                                     float cx, float cy, float cz, PoseF* P,
                                                     int lane) {
@@ -139,8 +137,7 @@ static __device__ __forceinline__ int rigid_compass(const PocketDev& pk, const f
         if (ax == 1) v2 = neg ? ty - sc2 : ty + sc2;
         if (ax == 2) s2 = neg ? tz - sc2 : tz + sc2;
       }
-      key = kInl ? eval_key<kGrid, 1>(pk, ysf, N, R2, u2, v2, s2)
-                 : eval_rigid<kGrid>(pk, ysf, N, R2, u2, v2, s2);
+      key = eval_key<kGrid, 1>(pk, ysf, N, R2, u2, v2, s2);
     }
     int li = lane < n_lanes ? lane : 0x7fffffff;
     for (int off = 16; off > 0; off >>= 1) {
@@ -178,9 +175,15 @@ static __device__ __forceinline__ int rigid_compass(const PocketDev& pk, const f
   return it;
 }
 
-template <int kGrid, bool kInl = false>
+// Lanes take the rotations in the locality order `perm` (host: rotation
+// clusters of 32, so the 32 lanes of one key-cell gather hold nearby
+// orientations and touch fewer 128 B lines); the argmax breaks ties on the
+// rotation index k itself, so the winner is the one of the index-ordered
+// sweep (SWEEP_V1.md §2.3), bit for bit.
+template <int kGrid>
 static __device__ VS_PHASE int sweep_phase(const PocketDev& pk, const Dims d,
-                                               const float4* __restrict__ rots, int K, int N,
+                                               const float4* __restrict__ rots,
+                                               const int* __restrict__ perm, int K, int N,
                                                int lane, PoseF* P, int* n_trans, int polish) {
   const WarpSmem s = dock_smem(d);
   float qs0 = P->q[0], qs1 = P->q[1], qs2 = P->q[2], qs3 = P->q[3];
@@ -202,7 +205,8 @@ static __device__ VS_PHASE int sweep_phase(const PocketDev& pk, const Dims d,
 
   float best_key = -INFINITY;
   int best_k = 0x7fffffff;
-  for (int k = lane; k < K; k += 32) {
+  for (int p = lane; p < K; p += 32) {
+    const int k = perm[p];
     const float4 rq = rots[k];
     float w4, x4, y4, z4;
     det_quat_mul(rq.x, rq.y, rq.z, rq.w, qs0, qs1, qs2, qs3, &w4, &x4, &y4, &z4);
@@ -210,9 +214,8 @@ static __device__ VS_PHASE int sweep_phase(const PocketDev& pk, const Dims d,
     const Mat3 Rk = det_quat_mat(w4, x4, y4, z4);
     float vx, vy, vz;
     det_apply(Rk, cx, cy, cz, 0.0f, 0.0f, 0.0f, &vx, &vy, &vz);
-    const float key = kInl ? eval_key<kGrid, VS_SWEEP_U>(pk, s.ysf, N, Rk, Cx - vx, Cy - vy, Cz - vz)
-                           : eval_rigid<kGrid>(pk, s.ysf, N, Rk, Cx - vx, Cy - vy, Cz - vz);
-    if (key > best_key) {
+    const float key = eval_key<kGrid, VS_SWEEP_U>(pk, s.ysf, N, Rk, Cx - vx, Cy - vy, Cz - vz);
+    if (key > best_key || (key == best_key && k < best_k)) {
       best_key = key;
       best_k = k;
     }
@@ -248,7 +251,7 @@ static __device__ VS_PHASE int sweep_phase(const PocketDev& pk, const Dims d,
     P->q[1] = px;
     P->q[2] = py;
     P->q[3] = pz;
-    *n_trans += rigid_compass<kGrid, kInl>(pk, s.ysf, N, cx, cy, cz, P, lane);
+    *n_trans += rigid_compass<kGrid>(pk, s.ysf, N, cx, cy, cz, P, lane);
     return best_k;
   }
   float sc = 1.0f;
@@ -257,8 +260,7 @@ static __device__ VS_PHASE int sweep_phase(const PocketDev& pk, const Dims d,
     float key = -INFINITY, ox = 0.0f, oy = 0.0f, oz = 0.0f;
     if (lane < 27) {
       trans_offset(lane, sc, &ox, &oy, &oz);
-      key = kInl ? eval_key<kGrid, VS_SWEEP_U>(pk, s.ysf, N, RS, ptx + ox, pty + oy, ptz + oz)
-                 : eval_rigid<kGrid>(pk, s.ysf, N, RS, ptx + ox, pty + oy, ptz + oz);
+      key = eval_key<kGrid, VS_SWEEP_U>(pk, s.ysf, N, RS, ptx + ox, pty + oy, ptz + oz);
     }
     int li = lane < 27 ? lane : 0x7fffffff;
     for (int off = 16; off > 0; off >>= 1) {
@@ -310,7 +312,7 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
   constexpr bool kSearch32 = kTab && kGrid;
   if (lane == 0) {
     if (kSearch32) {
-      const GridDev& g = c_pk.grid;
+      const GridDev& g = pk.grid;
       const float ih = g.inv_h;
       const Mat3 R = det_quat_mat(P->q[0], P->q[1], P->q[2], P->q[3]);
       float4* gf = reinterpret_cast<float4*>(s.pose);
@@ -329,7 +331,7 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
   __syncwarp();
   for (int i = lane; !kSearch32 && i < N; i += 32) {
     const double4 v = s.ys[i];
-    atom_terms_s<kGrid>(s.pose, v.x, v.y, v.z, &s.fa[i], &s.wa[i]);
+    atom_terms_s<kGrid>(pk, s.pose, v.x, v.y, v.z, &s.fa[i], &s.wa[i]);
   }
   __syncwarp();
   const bool do_flex = T > 0 && F > 0;
@@ -367,7 +369,7 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
       while (i < N - 1) {
         if (in_mask(mk, i) == in_mask(mk, k)) {
           const double4 yi = s.ys[i], yk = s.ys[k];
-          pb = pb + pair_term_s<kTab>(tab, yi.x - yk.x, yi.y - yk.y, yi.z - yk.z, nact);
+          pb = pb + pair_term_s<kTab>(pk, tab, yi.x - yk.x, yi.y - yk.y, yi.z - yk.z, nact);
         }
         k += 32;
         while (i < N - 1 && k >= N) {
@@ -444,7 +446,7 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
           const float fy = fmaf(Mf.m10, vx, fmaf(Mf.m11, vy, fmaf(Mf.m12, vz, ofy)));
           const float fz = fmaf(Mf.m20, vx, fmaf(Mf.m21, vy, fmaf(Mf.m22, vz, ofz)));
           const float4 r0 = gf[0], r1 = gf[1], r2 = gf[2];
-          fm = fm + key_at_grid(fmaf(r0.x, fx, fmaf(r0.y, fy, fmaf(r0.z, fz, r0.w))),
+          fm = fm + key_at_grid(pk, fmaf(r0.x, fx, fmaf(r0.y, fy, fmaf(r0.z, fz, r0.w))),
                                 fmaf(r1.x, fx, fmaf(r1.y, fy, fmaf(r1.z, fz, r1.w))),
                                 fmaf(r2.x, fx, fmaf(r2.y, fy, fmaf(r2.z, fz, r2.w))));
           if constexpr (kPacked) {
@@ -452,14 +454,14 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
             float4 yk = part[0];
             for (int p = 0; p < np; ++p) {
               const float4 yn = part[p + 1];
-              pc = pc + pair_term_f(tab, fx - yk.x, fy - yk.y, fz - yk.z, nact);
+              pc = pc + pair_term_f(pk, tab, fx - yk.x, fy - yk.y, fz - yk.z, nact);
               yk = yn;
             }
           } else {
             for (int k = 0; k < N; ++k)
               if (!in_mask(mk, k)) {
                 const double4 yk = s.ys[k];
-                pc = pc + pair_term_f(tab, fx - static_cast<float>(yk.x),
+                pc = pc + pair_term_f(pk, tab, fx - static_cast<float>(yk.x),
                                       fy - static_cast<float>(yk.y),
                                       fz - static_cast<float>(yk.z), nact);
               }
@@ -474,7 +476,7 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
         double yx, yy, yz;
         det_apply_d(M, v.x - o.x, v.y - o.y, v.z - o.z, o.x, o.y, o.z, &yx, &yy, &yz);
         float fi, wi;
-        atom_terms_s<kGrid>(s.pose, yx, yy, yz, &fi, &wi);
+        atom_terms_s<kGrid>(pk, s.pose, yx, yy, yz, &fi, &wi);
         fm = fm + fi;
         wm = wm + wi;
         if constexpr (kPacked && kTab) {
@@ -485,7 +487,7 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
           float4 yk = part[0];
           for (int p = 0; p < np; ++p) {
             const float4 yn = part[p + 1];
-            pc = pc + pair_term_f(tab, fx - yk.x, fy - yk.y, fz - yk.z, nact);
+            pc = pc + pair_term_f(pk, tab, fx - yk.x, fy - yk.y, fz - yk.z, nact);
             yk = yn;
           }
         } else if constexpr (kPacked) {
@@ -495,7 +497,7 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
           double4 yk = part[0];
           for (int p = 0; p < np; ++p) {
             const double4 yn = part[p + 1];
-            pc = pc + pair_term_s<kTab>(tab, yx - yk.x, yy - yk.y, yz - yk.z, nact);
+            pc = pc + pair_term_s<kTab>(pk, tab, yx - yk.x, yy - yk.y, yz - yk.z, nact);
             yk = yn;
           }
         } else {
@@ -511,11 +513,11 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
               b2 &= b2 - 1u;
               const double4 yn = yw[b2 ? __ffs(b2) - 1 : 0];
               if (kTab)  // the search (§3.4): FP32 cross pairs
-                pc = pc + pair_term_f(tab, static_cast<float>(yx) - static_cast<float>(yk.x),
+                pc = pc + pair_term_f(pk, tab, static_cast<float>(yx) - static_cast<float>(yk.x),
                                       static_cast<float>(yy) - static_cast<float>(yk.y),
                                       static_cast<float>(yz) - static_cast<float>(yk.z), nact);
               else
-                pc = pc + pair_term_s<kTab>(tab, yx - yk.x, yy - yk.y, yz - yk.z, nact);
+                pc = pc + pair_term_s<kTab>(pk, tab, yx - yk.x, yy - yk.y, yz - yk.z, nact);
               if (!b2) break;
               yk = yn;
             }
@@ -527,7 +529,7 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
     const float fm2 = __shfl_xor_sync(kFull, fm, 16);
     const float wm2 = __shfl_xor_sync(kFull, wm, 16);
     const float pc2 = __shfl_xor_sync(kFull, pc, 16);
-    float S = (fb + (fm + fm2)) - c_pk.lam * ((pb + (pc + pc2)) + (wb + (wm + wm2)));
+    float S = (fb + (fm + fm2)) - pk.lam * ((pb + (pc + pc2)) + (wb + (wm + wm2)));
     if (do_flex && !active) S = -INFINITY;
     int ai = (do_flex && !active) ? 0x7fffffff : a_lane;
     for (int off = 8; off > 0; off >>= 1) {
@@ -550,7 +552,7 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
         double4 v = s.ys[idx];
         det_apply_d(M, v.x - o.x, v.y - o.y, v.z - o.z, o.x, o.y, o.z, &v.x, &v.y, &v.z);
         s.ys[idx] = v;
-        if (!kSearch32) atom_terms_s<kGrid>(s.pose, v.x, v.y, v.z, &s.fa[idx], &s.wa[idx]);
+        if (!kSearch32) atom_terms_s<kGrid>(pk, s.pose, v.x, v.y, v.z, &s.fa[idx], &s.wa[idx]);
       }
       if (lane == 0) s.theta[j] = th_win;
     }
@@ -572,7 +574,7 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
 // ---- polish (SWEEP_V1.md §3.5) after the flex: the rigid compass on the
 // flexed state, then the canonical score of the final pose as a flex step
 // with an empty moving set (lane-strided atom and pair sums, butterflies).
-template <int kGrid, bool kInl>
+template <int kGrid>
 static __device__ VS_PHASE float polish_phase(const PocketDev& pk, const Dims d, int N, int lane,
                                               PoseF* P, int* n_iter) {
   const WarpSmem s = dock_smem(d);
@@ -593,7 +595,7 @@ static __device__ VS_PHASE float polish_phase(const PocketDev& pk, const Dims d,
   cx = cx / fN;
   cy = cy / fN;
   cz = cz / fN;
-  *n_iter += rigid_compass<kGrid, kInl>(pk, s.ysf, N, cx, cy, cz, P, lane);
+  *n_iter += rigid_compass<kGrid>(pk, s.ysf, N, cx, cy, cz, P, lane);
   const float qw = P->q[0], qx = P->q[1], qy = P->q[2], qz = P->q[3];
   const float tx = P->t[0], ty = P->t[1], tz = P->t[2];
   __syncwarp();
@@ -610,7 +612,7 @@ static __device__ VS_PHASE float polish_phase(const PocketDev& pk, const Dims d,
   for (int i = lane; i < N; i += 32) {
     const double4 v = s.ys[i];
     float fi, wi;
-    atom_terms_s<kGrid>(s.pose, v.x, v.y, v.z, &fi, &wi);
+    atom_terms_s<kGrid>(pk, s.pose, v.x, v.y, v.z, &fi, &wi);
     fb = fb + fi;
     wb = wb + wi;
   }
@@ -634,7 +636,7 @@ static __device__ VS_PHASE float polish_phase(const PocketDev& pk, const Dims d,
   fb = warp_sum(fb);
   wb = warp_sum(wb);
   pb = warp_sum(pb);
-  return fb - c_pk.lam * (pb + wb);
+  return fb - pk.lam * (pb + wb);
 }
 
 // ---- final coordinates, diversity against kept (dock.cpp:359-361), store
@@ -758,86 +760,13 @@ static __device__ VS_PHASE void finish_phase(const PocketDev& pk, const Dims d,
   __syncwarp();
 }
 
-#ifndef VS_MINB
-#define VS_MINB 8  // resident blocks per SM the register budget is sized for (64 regs)
-#endif
-
-template <int kGrid>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB)
-    vs_dock_kernel(const __grid_constant__ LibDev lib, const __grid_constant__ PocketDev pk,
-                   const float4* __restrict__ rots, const __grid_constant__ DockParams prm,
-                   const int* __restrict__ order, int n_order, int* __restrict__ work_counter,
-                   int nmax, int tmax, int mvmax, float4* __restrict__ scratch_xyz,
-                   float* __restrict__ scratch_par, int* __restrict__ scratch_meta,
-                   const __grid_constant__ DockOut out) {
-  const Dims d{nmax, tmax, mvmax, kLayAll};
-  const WarpSmem s = dock_smem(d);
-  const int lane = threadIdx.x & 31;
-  const long gwarp = static_cast<long>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
-  const int R = prm.R;
-  float4* kx = scratch_xyz + gwarp * R * nmax;
-  float* kp = scratch_par + gwarp * R * (8 + tmax);
-  int* km = scratch_meta + gwarp * R * 4;
-  if (lane == 0) mbar_init(s.bar);
-  __syncwarp();
-  uint32_t phase = 0;
-  const float step = kTwoPiF / static_cast<float>(prm.A);
-  while (true) {
-    int w = 0;
-    if (lane == 0) w = atomicAdd(work_counter, 1);
-    w = __shfl_sync(kFull, w, 0);
-    if (w >= n_order) break;
-    const int lig = order[w];
-    int4 meta;
-    stage_ligand(lib, lig, s, lane, phase, meta);
-    const int N = meta.y, T = meta.w;
-    const unsigned long long root = rng_mix(lib.seeds[lig] ^ kGolden);
-    int nk = 0;
-    int n_trans = 0, n_post = 0;
-    unsigned long long st[4] = {0, 0, 0, 0};  // sweep refinement iters, attempts, pairs, post iters
-    long long cyc[4] = {0, 0, 0, 0};       // start, sweep, flex, keep (SM cycles)
-    for (int r = 0; r < R; ++r) {
-      const unsigned long long rkey =
-          rng_mix(root ^ rng_mix(static_cast<unsigned long long>(r) + kGolden));
-      PoseF P;
-      const long long c0 = clock64();
-      const int att = start_phase(pk, d, rkey, N, T, kx, nmax, nk, prm.delta, lane, &P);
-      const long long c1 = clock64();
-      const int best_k = sweep_phase<kGrid>(pk, d, rots, prm.K, N, lane, &P, &n_trans, prm.polish);
-      const long long c2 = clock64();
-      float S = prm.polish >= 1
-                    ? flex_phase<kGrid, false, true>(pk, d, N, T, prm.F, prm.A, step, &P, lane,
-                                                     &st[2], prm.polish, c_pk.soft_tab)
-                    : flex_phase<kGrid>(pk, d, N, T, prm.F, prm.A, step, &P, lane, &st[2],
-                                        prm.polish);
-      if (prm.polish >= 1) S = polish_phase<kGrid, false>(pk, d, N, lane, &P, &n_post);
-      const long long c3 = clock64();
-      if (keep_phase(d, N, T, &P, S, r, att, best_k, kx, nmax, kp, 8 + tmax, km, nk, prm.delta,
-                     lane))
-        ++nk;
-      cyc[0] += c1 - c0;
-      cyc[1] += c2 - c1;
-      cyc[2] += c3 - c2;
-      cyc[3] += clock64() - c3;
-      st[1] += static_cast<unsigned long long>(att) + 1;
-    }
-    st[0] = static_cast<unsigned long long>(n_trans);
-    st[3] = static_cast<unsigned long long>(n_post);
-    finish_phase<kGrid>(pk, d, prm, out, lig, meta, nk, kx, nmax, kp, 8 + tmax, km,
-                        lib.id_rank[lig], lane, st);
-    if (lane == 0 && out.stats)
-      for (int c = 0; c < 4; ++c) atomicAdd(out.stats + 4 + c, static_cast<unsigned long long>(cyc[c]));
-  }
-}
-
 // ===================================================== staged dock kernels
-// The same phases as vs_dock_kernel, one kernel per phase and restart, the
-// per-ligand state handed over in HBM (StageBufs): each phase runs at its
-// own occupancy and instruction footprint (the sweep needs ~40 registers
-// and 1 KB of shared memory per warp; the flex needs 64 and ~5 KB), and an
-// SM only ever holds one phase's code.  Launch order per restart r:
-// start(r) -> sweep -> flex+keep(r); then finish.  Decisions and scores are
-// those of the fused kernel, bit for bit.
+// One kernel per phase and restart, the per-ligand state handed over in HBM
+// (StageBufs): each phase runs at its own occupancy and instruction footprint
+// (the sweep needs ~40 registers and 1 KB of shared memory per warp; the flex
+// needs 64 and ~5 KB), and an SM only ever holds one phase's code.  Launch
+// order per restart r: start(r) -> sweep -> flex -> polish + keep(r); then
+// finish.
 
 __device__ __forceinline__ int next_item(int* counter, int lane) {
   int w = 0;
@@ -870,7 +799,8 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t by
 
 template <int kGrid>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, 8)
-    vs_start_kernel(const __grid_constant__ LibDev lib, const __grid_constant__ DockParams prm,
+    vs_start_kernel(const __grid_constant__ LibDev lib, const __grid_constant__ PocketDev pk,
+                    const __grid_constant__ DockParams prm,
                     const int* __restrict__ order, int n_order, int* __restrict__ counter,
                     int nmax, int tmax, int mvmax, int r, const __grid_constant__ StageBufs sb) {
   const Dims d{nmax, tmax, mvmax, kLayLig | kLayState | kLayPosed};
@@ -879,7 +809,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 8)
   if (lane == 0) mbar_init(s.bar);
   __syncwarp();
   uint32_t phase = 0;
-  const PocketDev& pk = c_pk;
   for (int w = next_item(counter, lane); w < n_order; w = next_item(counter, lane)) {
     const int lig = order[w];
     int4 meta;
@@ -918,7 +847,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 8)
 
 template <int kGrid>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_SWEEP)
-    vs_sweep_kernel(const __grid_constant__ LibDev lib, const float4* __restrict__ rots,
+    vs_sweep_kernel(const __grid_constant__ LibDev lib, const __grid_constant__ PocketDev pk,
+                    const float4* __restrict__ rots, const int* __restrict__ perm,
                     const __grid_constant__ DockParams prm, const int* __restrict__ order,
                     int n_order, int* __restrict__ counter, int nmax,
                     const __grid_constant__ StageBufs sb) {
@@ -928,7 +858,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_SWEEP)
   if (lane == 0) mbar_init(s.bar);
   __syncwarp();
   uint32_t phase = 0;
-  const PocketDev& pk = c_pk;
   for (int w = next_item(counter, lane); w < n_order; w = next_item(counter, lane)) {
     const int lig = order[w];
     const int4 meta = lib.meta[lig];
@@ -945,7 +874,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_SWEEP)
     P.q[2] = pq.z;
     P.q[3] = pq.w;
     int n_trans = 0;
-    const int best_k = sweep_phase<kGrid, true>(pk, d, rots, prm.K, N, lane, &P, &n_trans,
+    const int best_k = sweep_phase<kGrid>(pk, d, rots, perm, prm.K, N, lane, &P, &n_trans,
                                                 prm.polish);
     if (lane == 0) {
       sb.pose[2 * lig] = make_float4(P.t[0], P.t[1], P.t[2], pt.w);
@@ -960,7 +889,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_SWEEP)
 
 template <int kGrid>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_FLEX)
-    vs_flex_kernel(const __grid_constant__ LibDev lib, const __grid_constant__ DockParams prm,
+    vs_flex_kernel(const __grid_constant__ LibDev lib, const __grid_constant__ PocketDev pk,
+                   const __grid_constant__ DockParams prm,
                    const int* __restrict__ order, int n_order, int* __restrict__ counter,
                    int nmax, int tmax, int mvmax, int r, const __grid_constant__ StageBufs sb) {
   const Dims d{nmax, tmax, mvmax,
@@ -972,13 +902,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_FLEX)
   float2* tab = reinterpret_cast<float2*>(
       smem_raw + kWarpsPerBlock * warp_smem_bytes(d.nmax, d.tmax, d.mvmax, d.lay));
   if (prm.polish >= 1) {
-    for (int k = threadIdx.x; k < kSoftN; k += blockDim.x) tab[k] = c_pk.soft_tab[k];
+    for (int k = threadIdx.x; k < kSoftN; k += blockDim.x) tab[k] = pk.soft_tab[k];
     __syncthreads();
   }
   if (lane == 0) mbar_init(s.bar);
   __syncwarp();
   uint32_t phase = 0;
-  const PocketDev& pk = c_pk;
   const float step = kTwoPiF / static_cast<float>(prm.A);
   for (int w = next_item(counter, lane); w < n_order; w = next_item(counter, lane)) {
     const int lig = order[w];
@@ -1004,7 +933,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_FLEX)
                                                   &nact, prm.polish, tab)
                   : flex_phase<kGrid, true, false>(pk, d, N, T, prm.F, prm.A, step, &P, lane,
                                                    &nact, prm.polish);
-#ifndef VS_FUSED_POLISH
     if (prm.polish >= 1) {
       // the polish + keep run in vs_polish_kernel: hand over the flexed state
       for (int i = lane; i < N; i += 32) sb.ys[meta.x + i] = s.ys[i];
@@ -1016,9 +944,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_FLEX)
       __syncwarp();
       continue;
     }
-#endif
-    int n_post = 0;
-    if (prm.polish >= 1) S = polish_phase<kGrid, true>(pk, d, N, lane, &P, &n_post);
     const long long c1 = clock64();
     const int nk = sb.nk[lig];
     float4* kx = sb.kx + static_cast<size_t>(meta.x) * R;
@@ -1029,7 +954,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_FLEX)
     if (lane == 0) {
       if (kept) sb.nk[lig] = nk + 1;
       sb.st[8 * lig + 2] += nact;
-      sb.st[8 * lig + 3] += static_cast<unsigned long long>(n_post);
       sb.st[8 * lig + 6] += static_cast<unsigned long long>(c1 - c0);
       sb.st[8 * lig + 7] += static_cast<unsigned long long>(clock64() - c1);
     }
@@ -1043,7 +967,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_FLEX)
 // its key-map lookups.
 template <int kGrid>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_POLISH)
-    vs_polish_kernel(const __grid_constant__ LibDev lib, const __grid_constant__ DockParams prm,
+    vs_polish_kernel(const __grid_constant__ LibDev lib, const __grid_constant__ PocketDev pk,
+                     const __grid_constant__ DockParams prm,
                      const int* __restrict__ order, int n_order, int* __restrict__ counter,
                      int nmax, int tmax, int r, const __grid_constant__ StageBufs sb) {
   const Dims d{nmax, tmax, 0, kLayState | kLayPosed | kLayFlex | kLaySweep};
@@ -1052,7 +977,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_POLISH)
   if (lane == 0) mbar_init(s.bar);
   __syncwarp();
   uint32_t phase = 0;
-  const PocketDev& pk = c_pk;
   for (int w = next_item(counter, lane); w < n_order; w = next_item(counter, lane)) {
     const int lig = order[w];
     const int4 meta = lib.meta[lig];
@@ -1071,7 +995,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_POLISH)
     P.q[3] = pq.w;
     __syncwarp();
     int n_post = 0;
-    const float S = polish_phase<kGrid, true>(pk, d, N, lane, &P, &n_post);
+    const float S = polish_phase<kGrid>(pk, d, N, lane, &P, &n_post);
     const long long c1 = clock64();
     const int nk = sb.nk[lig];
     float4* kx = sb.kx + static_cast<size_t>(meta.x) * R;
@@ -1091,7 +1015,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_POLISH)
 
 template <int kGrid>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, 8)
-    vs_finish_kernel(const __grid_constant__ LibDev lib, const __grid_constant__ DockParams prm,
+    vs_finish_kernel(const __grid_constant__ LibDev lib, const __grid_constant__ PocketDev pk,
+                     const __grid_constant__ DockParams prm,
                      const int* __restrict__ order, int n_order, int* __restrict__ counter,
                      int nmax, int tmax, int mvmax, const __grid_constant__ StageBufs sb,
                      const __grid_constant__ DockOut out) {
@@ -1101,7 +1026,6 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 8)
   if (lane == 0) mbar_init(s.bar);
   __syncwarp();
   uint32_t phase = 0;
-  const PocketDev& pk = c_pk;
   for (int w = next_item(counter, lane); w < n_order; w = next_item(counter, lane)) {
     const int lig = order[w];
     int4 meta;
@@ -1120,35 +1044,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 8)
   }
 }
 
-size_t dock_smem_per_block(int nmax, int tmax, int mvmax) {
-  return kWarpsPerBlock * warp_smem_bytes(nmax, tmax, mvmax, kLayAll);
-}
-
 template <class K>
 static void prep_dock(K kernel, size_t smem) {
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        static_cast<int>(smem));
   cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                        cudaSharedmemCarveoutMaxShared);
-}
-
-cudaError_t launch_dock(bool grid, int blocks, size_t smem, cudaStream_t st, const LibDev& lib,
-                        const PocketDev& pk, const float4* rots, const DockParams& prm,
-                        const int* order, int n_order, int* counter, int nmax, int tmax,
-                        int mvmax, float4* sx, float* sp, int* sm, const DockOut& out) {
-  cudaError_t e = cudaMemcpyToSymbolAsync(c_pk, &pk, sizeof(PocketDev), 0, cudaMemcpyHostToDevice,
-                                          st);
-  if (e != cudaSuccess) return e;
-  if (grid) {
-    prep_dock(vs_dock_kernel<1>, smem);
-    vs_dock_kernel<1><<<blocks, kWarpsPerBlock * 32, smem, st>>>(
-        lib, pk, rots, prm, order, n_order, counter, nmax, tmax, mvmax, sx, sp, sm, out);
-  } else {
-    prep_dock(vs_dock_kernel<0>, smem);
-    vs_dock_kernel<0><<<blocks, kWarpsPerBlock * 32, smem, st>>>(
-        lib, pk, rots, prm, order, n_order, counter, nmax, tmax, mvmax, sx, sp, sm, out);
-  }
-  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------- staged launch
@@ -1187,11 +1088,11 @@ size_t stage_smem_per_block(int nmax, int tmax, int mvmax) {
 }
 
 template <int kGrid>
-static cudaError_t staged_impl(int sms, cudaStream_t st, const LibDev& lib, const float4* rots,
-                               const DockParams& prm, const int* order, int n, int* counters,
-                               int nmax, int tmax, int mvmax, const StageBufs& sb,
-                               const DockOut& out, uint64_t* launches, cudaEvent_t* evs,
-                               int* kinds) {
+static cudaError_t staged_impl(int sms, cudaStream_t st, const LibDev& lib, const PocketDev& pk,
+                               const float4* rots, const int* perm, const DockParams& prm,
+                               const int* order, int n, int* counters, int nmax, int tmax,
+                               int mvmax, const StageBufs& sb, const DockOut& out,
+                               uint64_t* launches, cudaEvent_t* evs, int* kinds) {
   const size_t sm_start = kWarpsPerBlock * warp_smem_bytes(nmax, tmax, mvmax,
                                                            kLayLig | kLayState | kLayPosed);
   const size_t sm_sweep = kWarpsPerBlock * warp_smem_bytes(nmax, 0, 0, kLaySweep);
@@ -1218,66 +1119,92 @@ static cudaError_t staged_impl(int sms, cudaStream_t st, const LibDev& lib, cons
   };
   for (int r = 0; r < prm.R; ++r) {
     mark(0, false);
-    vs_start_kernel<kGrid><<<b_start, T, sm_start, st>>>(lib, prm, order, n, counters + c, nmax,
-                                                        tmax, mvmax, r, sb);
+    vs_start_kernel<kGrid><<<b_start, T, sm_start, st>>>(lib, pk, prm, order, n, counters + c,
+                                                        nmax, tmax, mvmax, r, sb);
     mark(0, true);
     ++c;
     mark(1, false);
-    vs_sweep_kernel<kGrid><<<b_sweep, T, sm_sweep, st>>>(lib, rots, prm, order, n, counters + c,
-                                                        nmax, sb);
+    vs_sweep_kernel<kGrid><<<b_sweep, T, sm_sweep, st>>>(lib, pk, rots, perm, prm, order, n,
+                                                        counters + c, nmax, sb);
     mark(1, true);
     ++c;
     mark(2, false);
-    vs_flex_kernel<kGrid><<<b_flex, T, sm_flex, st>>>(lib, prm, order, n, counters + c, nmax,
+    vs_flex_kernel<kGrid><<<b_flex, T, sm_flex, st>>>(lib, pk, prm, order, n, counters + c, nmax,
                                                      tmax, mvmax, r, sb);
     mark(2, true);
     ++c;
     *launches += 3;
-#ifndef VS_FUSED_POLISH
     if (prm.polish >= 1) {
       mark(4, false);
-      vs_polish_kernel<kGrid><<<b_pol, T, sm_pol, st>>>(lib, prm, order, n, counters + c, nmax,
-                                                       tmax, r, sb);
+      vs_polish_kernel<kGrid><<<b_pol, T, sm_pol, st>>>(lib, pk, prm, order, n, counters + c,
+                                                       nmax, tmax, r, sb);
       mark(4, true);
       ++c;
       *launches += 1;
     }
-#endif
   }
   mark(3, false);
-  vs_finish_kernel<kGrid><<<b_fin, T, sm_fin, st>>>(lib, prm, order, n, counters + c, nmax, tmax,
-                                                   mvmax, sb, out);
+  vs_finish_kernel<kGrid><<<b_fin, T, sm_fin, st>>>(lib, pk, prm, order, n, counters + c, nmax,
+                                                   tmax, mvmax, sb, out);
   mark(3, true);
   *launches += 1;
   return cudaGetLastError();
 }
 
-cudaError_t launch_staged(bool grid, int sms, cudaStream_t st, const LibDev& lib,
-                          const PocketDev& pk, const float4* rots, const DockParams& prm,
-                          const int* order, int n, int* counters, int nmax, int tmax, int mvmax,
-                          const StageBufs& sb, const DockOut& out, uint64_t* launches,
-                          cudaEvent_t* evs, int* kinds) {
-  cudaError_t e = cudaMemcpyToSymbolAsync(c_pk, &pk, sizeof(PocketDev), 0, cudaMemcpyHostToDevice,
-                                          st);
-  if (e != cudaSuccess) return e;
-  return grid ? staged_impl<1>(sms, st, lib, rots, prm, order, n, counters, nmax, tmax, mvmax, sb,
-                               out, launches, evs, kinds)
-              : staged_impl<0>(sms, st, lib, rots, prm, order, n, counters, nmax, tmax, mvmax, sb,
-                               out, launches, evs, kinds);
+// ---- restart start draws (dock.cpp:343-354) of given (ligand, restart,
+// attempt) triples, for the parity test against the reference Rng: one warp
+// per triple, the same draw_start the start kernel runs.  Row i of `out`
+// (stride floats): t[3], q[4] (w, x, y, z), theta[T].
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    vs_draws_kernel(const __grid_constant__ PocketDev pk, const unsigned long long* __restrict__ seeds,
+                    const int* __restrict__ n_tors, int n, int restarts, int attempts,
+                    float* __restrict__ out, int stride) {
+  __shared__ float theta[kWarpsPerBlock][kMaxTors];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const long total = static_cast<long>(n) * restarts * attempts;
+  for (long w = static_cast<long>(blockIdx.x) * kWarpsPerBlock + wib; w < total;
+       w += static_cast<long>(gridDim.x) * kWarpsPerBlock) {
+    const int att = static_cast<int>(w % attempts);
+    const int r = static_cast<int>((w / attempts) % restarts);
+    const int lig = static_cast<int>(w / (static_cast<long>(attempts) * restarts));
+    const int T = n_tors[lig];
+    const unsigned long long root = rng_mix(seeds[lig] ^ kGolden);
+    const unsigned long long rkey =
+        rng_mix(root ^ rng_mix(static_cast<unsigned long long>(r) + kGolden));
+    WarpSmem s{};
+    s.theta = theta[wib];
+    float t[3], q[4];
+    draw_start(pk, rkey, att, T, s, lane, t, q);
+    float* o = out + w * stride;
+    if (lane == 0) {
+      for (int c = 0; c < 3; ++c) o[c] = t[c];
+      for (int c = 0; c < 4; ++c) o[3 + c] = q[c];
+    }
+    for (int j = lane; j < T; j += 32) o[7 + j] = s.theta[j];
+    __syncwarp();
+  }
 }
 
-int dock_blocks_per_sm(bool grid, size_t smem) {
-  int nb = 0;
-  if (grid) {
-    prep_dock(vs_dock_kernel<1>, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, vs_dock_kernel<1>, kWarpsPerBlock * 32,
-                                                  smem);
-  } else {
-    prep_dock(vs_dock_kernel<0>, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, vs_dock_kernel<0>, kWarpsPerBlock * 32,
-                                                  smem);
-  }
-  return nb;
+cudaError_t launch_draws(cudaStream_t st, const PocketDev& pk, const unsigned long long* seeds,
+                         const int* n_tors, int n, int restarts, int attempts, float* out,
+                         int stride, int sms) {
+  vs_draws_kernel<<<sms * 8, kWarpsPerBlock * 32, 0, st>>>(pk, seeds, n_tors, n, restarts,
+                                                           attempts, out, stride);
+  return cudaGetLastError();
+}
+
+// rots: the K rotations in index order; perm: the sweep's lane order (a
+// permutation of 0..K-1, see sweep_phase)
+cudaError_t launch_staged(bool grid, int sms, cudaStream_t st, const LibDev& lib,
+                          const PocketDev& pk, const float4* rots, const int* perm,
+                          const DockParams& prm, const int* order, int n, int* counters,
+                          int nmax, int tmax, int mvmax, const StageBufs& sb, const DockOut& out,
+                          uint64_t* launches, cudaEvent_t* evs, int* kinds) {
+  return grid ? staged_impl<1>(sms, st, lib, pk, rots, perm, prm, order, n, counters, nmax, tmax,
+                               mvmax, sb, out, launches, evs, kinds)
+              : staged_impl<0>(sms, st, lib, pk, rots, perm, prm, order, n, counters, nmax, tmax,
+                               mvmax, sb, out, launches, evs, kinds);
 }
 
 }  // namespace vs

@@ -486,6 +486,17 @@ int vs_campaign_seeds(uint64_t master, int32_t stage, const int32_t* in_range, i
   return VS_OK;
 }
 
+int vs_topk_merge_host(const uint64_t* keys, int64_t n, int32_t k, uint64_t* out) {
+  if (k < 0 || n < 0) return VS_ERR_INVALID_ARGUMENT;
+  // keys are unique per ligand (id_rank in the low word), so the k smallest
+  // are a set; dropped ligands (~0) sort last
+  std::vector<uint64_t> v(keys, keys + n);
+  const size_t m = std::min<size_t>(static_cast<size_t>(k), v.size());
+  std::partial_sort(v.begin(), v.begin() + static_cast<std::ptrdiff_t>(m), v.end());
+  for (size_t i = 0; i < static_cast<size_t>(k); ++i) out[i] = i < m ? v[i] : ~0ull;
+  return VS_OK;
+}
+
 int vs_filter_poses(const double* scores, int32_t n, int64_t keep_top, double min_score,
                     int32_t* out_idx) {
   std::vector<int32_t> idx;

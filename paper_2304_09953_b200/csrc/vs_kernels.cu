@@ -77,7 +77,7 @@ __device__ inline void chain_pose(const WarpSmem& s, int N, int T, int a, int h,
 // and pairs p = h mod 2 (row-major), combined across the lane pair.
 template <int kGrid>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
-    vs_rescore_kernel(const LibDev lib, const PocketDev pk, const int* __restrict__ ligs,
+    vs_rescore_kernel(const __grid_constant__ LibDev lib, const __grid_constant__ PocketDev pk, const int* __restrict__ ligs,
                       int n_ligs, int* __restrict__ work_counter, const int* __restrict__ pose_off,
                       const long* __restrict__ tors_base, const float4* __restrict__ pose_t,
                       const float4* __restrict__ pose_q, const float* __restrict__ pose_tors,
@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 }
 
 // ============================================================ grid kernels
-__global__ void vs_grid_kernel(const PocketDev pk, float* __restrict__ steric,
+__global__ void vs_grid_kernel(const __grid_constant__ PocketDev pk, float* __restrict__ steric,
                                float* __restrict__ hbond, float* __restrict__ lipo,
                                float* __restrict__ key) {
   const GridDev& g = pk.grid;
@@ -322,6 +322,27 @@ __global__ void vs_peak_gather(const uint4* __restrict__ cells, unsigned mask, i
   if (acc == 0x9E3779B9u) out[0] = acc;
 }
 
+// the same with 32 B loads (ld.global.nc.v8.f32, one whole sector per lane:
+// the FP32 corner cell of SURVEY §8(d)'s L2_B = 8 corners x 4 B per lookup)
+__global__ void vs_peak_gather32(const float4* __restrict__ cells, unsigned mask, int iters,
+                                 unsigned* out) {
+  unsigned h[8];
+  const unsigned t = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int k = 0; k < 8; ++k) h[k] = t * 2654435761u + 0x9E3779B9u * (k + 1);
+  float acc = 0.0f;
+  for (int i = 0; i < iters; ++i) {
+    float4 lo[8], hi[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      h[k] = h[k] * 1664525u + 1013904223u;
+      ldg_cell(cells + 2 * ((h[k] >> 7) & mask), lo[k], hi[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc += lo[k].x + hi[k].w;
+  }
+  if (acc == 1.2345f) out[0] = 1u;
+}
+
 }  // namespace vs
 
 // ------------------------------------------------------ launch wrappers --
@@ -344,9 +365,6 @@ cudaError_t launch_rescore(bool grid, int blocks, size_t smem, cudaStream_t st, 
                            const int* pose_off, const long* tors_base, const float4* pt,
                            const float4* pq, const float* ptors, int nmax, int tmax, int mvmax,
                            float* geo, float* resc) {
-  cudaError_t e = cudaMemcpyToSymbolAsync(c_pk, &pk, sizeof(PocketDev), 0, cudaMemcpyHostToDevice,
-                                          st);
-  if (e != cudaSuccess) return e;
   if (grid) {
     prep(vs_rescore_kernel<1>, smem);
     vs_rescore_kernel<1><<<blocks, kWarpsPerBlock * 32, smem, st>>>(
@@ -392,11 +410,12 @@ cudaError_t launch_topk(cudaStream_t st, const unsigned long long* in, long n,
 }
 
 // kind 0 fp32 fma, 1 fp64 fma, 2 ex2; returns ops/s (best of 3)
-double measure_gather_peak(int sms) {
-  const unsigned n = 1u << 19;  // 512 Ki cells x 16 B = 8 MB (L2-resident)
+double measure_gather_peak(int sms, int bytes) {
+  const unsigned n = 1u << 19;  // 512 Ki cells x 16 B = 8 MB (x 32 B = 16 MB; L2-resident)
+  const size_t cb = bytes == 32 ? 32 : 16;
   void* buf = nullptr;
-  if (cudaMalloc(&buf, size_t(n) * 16 + 256) != cudaSuccess) return 0.0;
-  cudaMemset(buf, 0, size_t(n) * 16 + 256);
+  if (cudaMalloc(&buf, size_t(n) * cb + 256) != cudaSuccess) return 0.0;
+  cudaMemset(buf, 0, size_t(n) * cb + 256);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
@@ -404,9 +423,11 @@ double measure_gather_peak(int sms) {
   double best = 0.0;
   for (int rep = 0; rep < 4; ++rep) {
     cudaEventRecord(a);
-    vs_peak_gather<<<blocks, threads>>>(static_cast<const uint4*>(buf), n - 1, iters,
-                                        reinterpret_cast<unsigned*>(static_cast<char*>(buf) +
-                                                                    size_t(n) * 16));
+    unsigned* sink = reinterpret_cast<unsigned*>(static_cast<char*>(buf) + size_t(n) * cb);
+    if (cb == 32)
+      vs_peak_gather32<<<blocks, threads>>>(static_cast<const float4*>(buf), n - 1, iters, sink);
+    else
+      vs_peak_gather<<<blocks, threads>>>(static_cast<const uint4*>(buf), n - 1, iters, sink);
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     float ms = 0.0f;

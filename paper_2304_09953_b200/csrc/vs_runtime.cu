@@ -3,6 +3,8 @@
 // buckets, SoA, LPT order), dock launches per bucket, results, top-k and
 // the rescoring path.  Host C++; the kernels live in vs_kernels.cu.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <array>
@@ -21,28 +23,18 @@
 #include "vs_types.h"
 
 namespace vs {
-size_t dock_smem_per_block(int nmax, int tmax, int mvmax);
 size_t rescore_smem_per_block(int nmax, int tmax, int mvmax);
-int dock_blocks_per_sm(bool grid, size_t smem);
 size_t stage_smem_per_block(int nmax, int tmax, int mvmax);
 constexpr int kStats = 10;  // work counters (capi.h vs_last_stats_ex)
 
-// dock execution mode: "staged" (one kernel per phase and restart) or
-// "fused" (one persistent kernel); VSCREEN_DOCK_MODE overrides the default
-static bool staged_mode() {
-  const char* m = std::getenv("VSCREEN_DOCK_MODE");
-  if (m && std::strcmp(m, "fused") == 0) return false;
-  return true;
-}
+cudaError_t launch_draws(cudaStream_t st, const PocketDev& pk, const unsigned long long* seeds,
+                         const int* n_tors, int n, int restarts, int attempts, float* out,
+                         int stride, int sms);
 cudaError_t launch_staged(bool grid, int sms, cudaStream_t st, const LibDev& lib,
-                          const PocketDev& pk, const float4* rots, const DockParams& prm,
-                          const int* order, int n, int* counters, int nmax, int tmax, int mvmax,
-                          const StageBufs& sb, const DockOut& out, uint64_t* launches,
-                          cudaEvent_t* evs, int* kinds);
-cudaError_t launch_dock(bool grid, int blocks, size_t smem, cudaStream_t st, const LibDev& lib,
-                        const PocketDev& pk, const float4* rots, const DockParams& prm,
-                        const int* order, int n_order, int* counter, int nmax, int tmax,
-                        int mvmax, float4* sx, float* sp, int* sm, const DockOut& out);
+                          const PocketDev& pk, const float4* rots, const int* perm,
+                          const DockParams& prm, const int* order, int n, int* counters,
+                          int nmax, int tmax, int mvmax, const StageBufs& sb, const DockOut& out,
+                          uint64_t* launches, cudaEvent_t* evs, int* kinds);
 cudaError_t launch_rescore(bool grid, int blocks, size_t smem, cudaStream_t st, const LibDev& lib,
                            const PocketDev& pk, const int* ligs, int n_ligs, int* counter,
                            const int* pose_off, const long* tors_base, const float4* pt,
@@ -70,7 +62,7 @@ cudaError_t launch_grid(cudaStream_t st, const PocketDev& pk, float* steric, flo
 int topk_chunk();
 double measure_peak(int kind, int sms);
 cudaError_t launch_softtab(cudaStream_t st, float r, float cut2, float2* tab);
-double measure_gather_peak(int sms);
+double measure_gather_peak(int sms, int bytes);
 cudaError_t launch_topk(cudaStream_t st, const unsigned long long* in, long n,
                         unsigned long long* out, int k, int blocks);
 }  // namespace vs
@@ -206,11 +198,20 @@ struct vs_handle {
   vs_dock_params last_prm{};
   bool has_results = false;
   DBuf d_surv, d_surv_tors, d_all, d_all_tors, d_best, d_nkept, d_nsurv, d_keys, d_counters;
-  DBuf d_sx, d_sp, d_sm, d_rots, d_topk_a, d_topk_b, d_stats;
+  DBuf d_rots, d_topk_a, d_topk_b, d_stats;
   DBuf d_sg_ys, d_sg_ysf, d_sg_th, d_sg_pose, d_sg_bk, d_sg_nk, d_sg_kx, d_sg_kp, d_sg_km, d_sg_st;
   int rots_k = -1;
   uint64_t rots_seed = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // end of the handle's last device operation (dock, top-k, gather) on
+  // whichever stream it ran: later operations on other streams, and host
+  // rewrites of the handle's buffers, are ordered after it
+  cudaEvent_t done = nullptr;
+  // NCCL communicator of the multi-GPU top-k gather (vs_comm_init /
+  // vs_comm_attach); owned = created by vs_comm_init
+  ncclComm_t comm = nullptr;
+  bool comm_owned = false;
+  DBuf d_gather;  // local top-k followed by the gathered keys of every rank
   std::vector<cudaEvent_t> pev;  // per-launch event pairs of the staged dock
   std::vector<int> pkind;        // kernel kind of each pair (0 start .. 3 finish)
   bool timed = false;
@@ -248,6 +249,13 @@ cudaStream_t pick(vs_handle* h, void* s) {
   h->last = s ? static_cast<cudaStream_t>(s) : h->own;
   return h->last;
 }
+
+// stream-side: `st` waits for the handle's previous device operation
+cudaError_t after_prev(vs_handle* h, cudaStream_t st) { return cudaStreamWaitEvent(st, h->done, 0); }
+// host-side: the previous device operation has finished (before buffers it
+// reads are rewritten or freed: pocket, library, rescore staging)
+cudaError_t quiesce(vs_handle* h) { return cudaEventSynchronize(h->done); }
+cudaError_t mark_done(vs_handle* h, cudaStream_t st) { return cudaEventRecord(h->done, st); }
 
 size_t align16z(size_t x) { return (x + 15) & ~size_t(15); }
 
@@ -570,6 +578,82 @@ std::vector<float4> rotation_set(int K, uint64_t seed) {
   return r;
 }
 
+// Lane order of the rotation sweep (vs_dock.cu sweep_phase): the K rotations
+// in groups of 32 (one warp-wide key-cell gather each) that are clusters on
+// SO(3), so the 32 poses of one gather put each atom at nearby positions and
+// touch fewer distinct 128 B lines of the key map.  Balanced k-means on the
+// quaternion similarity |<qa, qb>| (capacity 32 per cluster, greedy
+// assignment in order of decreasing similarity, ties by index), seeded by
+// farthest-point sampling from rotation 0; fully deterministic.  The sweep's
+// result does not depend on this order (argmax ties break on k).
+std::vector<int> rotation_order(const std::vector<float4>& r) {
+  const int K = static_cast<int>(r.size());
+  std::vector<int> perm(static_cast<size_t>(K));
+  std::iota(perm.begin(), perm.end(), 0);
+  const int G = K / 32;
+  if (G < 2) return perm;
+  auto sim = [](const float4& a, const double* c) {
+    return std::fabs(a.x * c[0] + a.y * c[1] + a.z * c[2] + a.w * c[3]);
+  };
+  std::vector<std::array<double, 4>> cent(static_cast<size_t>(G));
+  std::vector<int> seeds{0};
+  std::vector<double> near(static_cast<size_t>(K), 2.0);
+  while (static_cast<int>(seeds.size()) < G) {
+    const float4& s0 = r[static_cast<size_t>(seeds.back())];
+    const double c0[4] = {s0.x, s0.y, s0.z, s0.w};
+    int far = 0;
+    for (int k = 0; k < K; ++k) {
+      near[k] = std::min(near[k], 1.0 - sim(r[k], c0) + 0.0);
+      if (near[k] > near[far]) far = k;
+    }
+    seeds.push_back(far);
+  }
+  for (int g = 0; g < G; ++g) {
+    const float4& q = r[static_cast<size_t>(seeds[g])];
+    cent[g] = {q.x, q.y, q.z, q.w};
+  }
+  std::vector<int> asg(static_cast<size_t>(K), -1);
+  const int cap = 32;
+  std::vector<std::pair<double, int>> pairs(static_cast<size_t>(K) * G);
+  for (int it = 0; it < 16; ++it) {
+    for (int k = 0; k < K; ++k)
+      for (int g = 0; g < G; ++g) pairs[static_cast<size_t>(k) * G + g] = {-sim(r[k], cent[g].data()), k * G + g};
+    std::sort(pairs.begin(), pairs.end());
+    std::fill(asg.begin(), asg.end(), -1);
+    std::vector<int> cnt(static_cast<size_t>(G), 0);
+    for (const auto& pr : pairs) {
+      const int k = pr.second / G, g = pr.second % G;
+      if (asg[k] < 0 && cnt[g] < cap) {
+        asg[k] = g;
+        ++cnt[g];
+      }
+    }
+    for (int g = 0; g < G; ++g) {
+      double c[4] = {0, 0, 0, 0};
+      for (int k = 0; k < K; ++k) {
+        if (asg[k] != g) continue;
+        const double d = r[k].x * cent[g][0] + r[k].y * cent[g][1] + r[k].z * cent[g][2] +
+                         r[k].w * cent[g][3];
+        const double sg = d < 0.0 ? -1.0 : 1.0;
+        c[0] += sg * r[k].x;
+        c[1] += sg * r[k].y;
+        c[2] += sg * r[k].z;
+        c[3] += sg * r[k].w;
+      }
+      const double n = std::sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2] + c[3] * c[3]);
+      if (n > 0.0)
+        for (int m = 0; m < 4; ++m) cent[g][m] = c[m] / n;
+    }
+  }
+  int o = 0;
+  for (int g = 0; g < G; ++g)
+    for (int k = 0; k < K; ++k)
+      if (asg[k] == g) perm[o++] = k;
+  for (int k = 0; k < K; ++k)  // the K mod 32 rotations outside every cluster
+    if (asg[k] < 0) perm[o++] = k;
+  return perm;
+}
+
 }  // namespace
 
 extern "C" {
@@ -595,6 +679,7 @@ int vs_create(int device, vs_handle** out) {
   }
   cudaEventCreate(&h->ev0);
   cudaEventCreate(&h->ev1);
+  cudaEventCreateWithFlags(&h->done, cudaEventDisableTiming);
   h->last = h->own;
   *out = h;
   return VS_OK;
@@ -608,13 +693,15 @@ void vs_destroy(vs_handle* h) {
   h->rpack.release();
   for (DBuf& b : h->rbuf) b.release();
   for (DBuf* b : {&h->d_sites, &h->d_softtab, &h->d_sites64, &h->d_maps, &h->d_surv, &h->d_surv_tors, &h->d_all, &h->d_all_tors,
-                  &h->d_best, &h->d_nkept, &h->d_nsurv, &h->d_keys, &h->d_counters, &h->d_sx,
-                  &h->d_sp, &h->d_sm, &h->d_rots, &h->d_topk_a, &h->d_topk_b, &h->d_stats,
+                  &h->d_best, &h->d_nkept, &h->d_nsurv, &h->d_keys, &h->d_counters, &h->d_rots, &h->d_topk_a, &h->d_topk_b, &h->d_stats,
                   &h->d_sg_ys, &h->d_sg_ysf, &h->d_sg_th, &h->d_sg_pose, &h->d_sg_bk, &h->d_sg_nk,
                   &h->d_sg_kx, &h->d_sg_kp, &h->d_sg_km, &h->d_sg_st})
     b->release();
   cudaEventDestroy(h->ev0);
   cudaEventDestroy(h->ev1);
+  cudaEventDestroy(h->done);
+  vs_comm_destroy(h);
+  h->d_gather.release();
   for (cudaEvent_t e : h->pev) cudaEventDestroy(e);
   if (h->rev0) cudaEventDestroy(h->rev0);
   if (h->rev1) cudaEventDestroy(h->rev1);
@@ -633,6 +720,7 @@ int vs_device_info(const vs_handle* h, char* name, int32_t* sm_count, int32_t* c
 
 int vs_set_pocket(vs_handle* h, const vs_pocket* p, double spacing, double pad) {
   cudaSetDevice(h->device);
+  VS_CUDA(h, quiesce(h));
   cudaStream_t st = h->own;
   std::vector<SiteF> sites;
   int counts[3] = {0, 0, 0};
@@ -763,6 +851,7 @@ int vs_grid_fetch(vs_handle* h, float* steric, float* hbond, float* lipo) {
 int vs_upload_library(vs_handle* h, const vs_library* L, const vs_size_class* classes,
                       int32_t nc) {
   cudaSetDevice(h->device);
+  VS_CUDA(h, quiesce(h));  // a dock on a caller stream may still read the library
   h->has_lib = false;
   h->has_results = false;
   using clk = std::chrono::steady_clock;
@@ -804,14 +893,20 @@ int vs_dock(vs_handle* h, const vs_dock_params* prm, void* stream) {
   int rc = check_params(h, prm);
   if (rc) return rc;
   cudaStream_t st = pick(h, stream);
+  VS_CUDA(h, after_prev(h, st));
   Packed& P = h->lib;
   const int n = P.n;
   const int R = prm->restarts, KT = prm->keep_top;
   if (h->rots_k != prm->rotations || h->rots_seed != prm->rotation_seed) {
+    // the K rotations (index order) followed by the sweep's lane order
     const auto rs = rotation_set(prm->rotations, prm->rotation_seed);
-    VS_CUDA(h, h->d_rots.ensure(rs.size() * sizeof(float4)));
-    VS_CUDA(h, cudaMemcpyAsync(h->d_rots.p, rs.data(), rs.size() * sizeof(float4),
-                               cudaMemcpyHostToDevice, st));
+    const auto perm = rotation_order(rs);
+    const size_t rb = rs.size() * sizeof(float4);
+    std::vector<unsigned char> blob(rb + perm.size() * sizeof(int));
+    std::memcpy(blob.data(), rs.data(), rb);
+    std::memcpy(blob.data() + rb, perm.data(), perm.size() * sizeof(int));
+    VS_CUDA(h, h->d_rots.ensure(blob.size()));
+    VS_CUDA(h, cudaMemcpyAsync(h->d_rots.p, blob.data(), blob.size(), cudaMemcpyHostToDevice, st));
     VS_CUDA(h, cudaStreamSynchronize(st));
     h->rots_k = prm->rotations;
     h->rots_seed = prm->rotation_seed;
@@ -866,12 +961,12 @@ int vs_dock(vs_handle* h, const vs_dock_params* prm, void* stream) {
 
   const bool grid = h->pk.grid_mode != 0;
   const LibDev ld = P.dev();
-  // one persistent launch over the global LPT queue (every size bucket),
-  // shared memory sized for the largest ligand; one scratch slot per warp
+  // one launch per phase and restart over the global LPT queue (every size
+  // bucket), shared memory sized for the largest ligand, the per-ligand
+  // state handed over in HBM
   const Bucket& b = P.all;
   VS_CUDA(h, cudaEventRecord(h->ev0, st));
-  if (b.count > 0 && staged_mode()) {
-    // staged: one kernel per phase and restart, state handed over in HBM
+  if (b.count > 0) {
     const size_t smem = stage_smem_per_block(b.nmax, b.tmax, b.mvmax);
     if (smem > 227 * 1024) return fail(h, VS_ERR_CAPACITY, "ligands need too much shared memory");
     const size_t na = std::max<size_t>(1, P.atoms.size());
@@ -904,30 +999,16 @@ int vs_dock(vs_handle* h, const vs_dock_params* prm, void* stream) {
       h->pev.push_back(e);
     }
     h->pkind.assign(npairs, -1);  // -1: no launch recorded in this slot
-    VS_CUDA(h, launch_staged(grid, h->sms, st, ld, h->pk, h->d_rots.as<const float4>(), dp,
+    const float4* rots = h->d_rots.as<const float4>();
+    const int* perm = reinterpret_cast<const int*>(rots + prm->rotations);
+    VS_CUDA(h, launch_staged(grid, h->sms, st, ld, h->pk, rots, perm, dp,
                              P.d_order.as<int>() + b.start, b.count, h->d_counters.as<int>(),
                              b.nmax, b.tmax, b.mvmax, sb, out, &h->launches, h->pev.data(),
                              h->pkind.data()));
     h->staged_run = true;
-  } else if (b.count > 0) {
-    const size_t smem = dock_smem_per_block(b.nmax, b.tmax, b.mvmax);
-    if (smem > 227 * 1024) return fail(h, VS_ERR_CAPACITY, "ligands need too much shared memory");
-    int per_sm = dock_blocks_per_sm(grid, smem);
-    if (per_sm < 1) per_sm = 1;
-    const int want = (b.count + kWarpsPerBlock - 1) / kWarpsPerBlock;
-    const int blocks = std::max(1, std::min(want, per_sm * h->sms));
-    const size_t warps = static_cast<size_t>(blocks) * kWarpsPerBlock;
-    VS_CUDA(h, h->d_sx.ensure(warps * R * b.nmax * sizeof(float4)));
-    VS_CUDA(h, h->d_sp.ensure(warps * R * (8 + b.tmax) * sizeof(float)));
-    VS_CUDA(h, h->d_sm.ensure(warps * R * 4 * sizeof(int)));
-    VS_CUDA(h, launch_dock(grid, blocks, smem, st, ld, h->pk, h->d_rots.as<const float4>(), dp,
-                           P.d_order.as<int>() + b.start, b.count, h->d_counters.as<int>(),
-                           b.nmax, b.tmax, b.mvmax, h->d_sx.as<float4>(), h->d_sp.as<float>(),
-                           h->d_sm.as<int>(), out));
-    ++h->launches;
-    h->staged_run = false;
   }
   VS_CUDA(h, cudaEventRecord(h->ev1, st));
+  VS_CUDA(h, mark_done(h, st));
   h->timed = true;
   h->last_prm = *prm;
   h->has_results = true;
@@ -1011,7 +1092,17 @@ int vs_measure_peaks(vs_handle* h, double* fp32, double* fp64, double* xu) {
 int vs_measure_gather_peak(vs_handle* h, double* loads_per_s) {
   cudaSetDevice(h->device);
   VS_CUDA(h, cudaDeviceSynchronize());
-  if (loads_per_s) *loads_per_s = measure_gather_peak(h->sms);
+  if (loads_per_s) *loads_per_s = measure_gather_peak(h->sms, 16);
+  VS_CUDA(h, cudaGetLastError());
+  return VS_OK;
+}
+
+int vs_measure_gather_peak_ex(vs_handle* h, int32_t bytes_per_load, double* loads_per_s) {
+  cudaSetDevice(h->device);
+  if (bytes_per_load != 16 && bytes_per_load != 32)
+    return fail(h, VS_ERR_INVALID_ARGUMENT, "bytes_per_load must be 16 or 32");
+  VS_CUDA(h, cudaDeviceSynchronize());
+  if (loads_per_s) *loads_per_s = measure_gather_peak(h->sms, bytes_per_load);
   VS_CUDA(h, cudaGetLastError());
   return VS_OK;
 }
@@ -1131,16 +1222,23 @@ int vs_topk_device(vs_handle* h, int32_t k, uint64_t* out_dev, void* stream) {
   cudaSetDevice(h->device);
   if (!h->has_results) return fail(h, VS_ERR_STATE, "no results");
   cudaStream_t st = pick(h, stream);
-  return topk_run(h, h->d_keys.as<unsigned long long>(), h->lib.n, k,
-                  reinterpret_cast<unsigned long long*>(out_dev), st);
+  VS_CUDA(h, after_prev(h, st));  // the keys of a dock on another stream
+  const int rc = topk_run(h, h->d_keys.as<unsigned long long>(), h->lib.n, k,
+                          reinterpret_cast<unsigned long long*>(out_dev), st);
+  if (rc == VS_OK) VS_CUDA(h, mark_done(h, st));
+  return rc;
 }
 
 int vs_topk_merge_device(vs_handle* h, const uint64_t* keys_dev, int64_t n, int32_t k,
                          uint64_t* out_dev, void* stream) {
   cudaSetDevice(h->device);
   cudaStream_t st = pick(h, stream);
-  return topk_run(h, reinterpret_cast<const unsigned long long*>(keys_dev), static_cast<long>(n),
-                  k, reinterpret_cast<unsigned long long*>(out_dev), st);
+  VS_CUDA(h, after_prev(h, st));  // the handle's top-k scratch buffers
+  const int rc = topk_run(h, reinterpret_cast<const unsigned long long*>(keys_dev),
+                          static_cast<long>(n), k, reinterpret_cast<unsigned long long*>(out_dev),
+                          st);
+  if (rc == VS_OK) VS_CUDA(h, mark_done(h, st));
+  return rc;
 }
 
 int vs_topk(vs_handle* h, int32_t k, uint64_t* out_keys) {
@@ -1154,6 +1252,150 @@ int vs_topk(vs_handle* h, int32_t k, uint64_t* out_keys) {
     if (e != cudaSuccess) rc = cuda_fail(h, e, "topk fetch");
   }
   tmp.release();
+  return rc;
+}
+
+// ------------------------------------------------------------ NCCL gather
+// libnccl is resolved at first use: the copy the process already has (the
+// one torch.distributed loaded) or else the system libnccl.so.2, so the
+// library carries no link-time NCCL dependency and never loads a second one.
+namespace {
+struct NcclApi {
+  bool ok = false;
+  decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+  decltype(&ncclCommInitRank) comm_init_rank = nullptr;
+  decltype(&ncclCommDestroy) comm_destroy = nullptr;
+  decltype(&ncclCommCount) comm_count = nullptr;
+  decltype(&ncclAllGather) all_gather = nullptr;
+  decltype(&ncclGetErrorString) error_string = nullptr;
+};
+const NcclApi& nccl() {
+  static const NcclApi api = [] {
+    NcclApi a;
+    void* so = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!so) so = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!so) return a;
+    a.get_unique_id = reinterpret_cast<decltype(&ncclGetUniqueId)>(dlsym(so, "ncclGetUniqueId"));
+    a.comm_init_rank = reinterpret_cast<decltype(&ncclCommInitRank)>(dlsym(so, "ncclCommInitRank"));
+    a.comm_destroy = reinterpret_cast<decltype(&ncclCommDestroy)>(dlsym(so, "ncclCommDestroy"));
+    a.comm_count = reinterpret_cast<decltype(&ncclCommCount)>(dlsym(so, "ncclCommCount"));
+    a.all_gather = reinterpret_cast<decltype(&ncclAllGather)>(dlsym(so, "ncclAllGather"));
+    a.error_string = reinterpret_cast<decltype(&ncclGetErrorString)>(dlsym(so, "ncclGetErrorString"));
+    a.ok = a.get_unique_id && a.comm_init_rank && a.comm_destroy && a.comm_count && a.all_gather &&
+           a.error_string;
+    return a;
+  }();
+  return api;
+}
+int nccl_fail(vs_handle* h, ncclResult_t r, const char* what) {
+  return fail(h, VS_ERR_CUDA, std::string(what) + ": " + nccl().error_string(r));
+}
+}  // namespace
+
+int vs_nccl_unique_id(uint8_t out[VS_NCCL_ID_BYTES]) {
+  if (!nccl().ok) return VS_ERR_NO_DEVICE;
+  ncclUniqueId id;
+  if (nccl().get_unique_id(&id) != ncclSuccess) return VS_ERR_CUDA;
+  std::memcpy(out, id.internal, VS_NCCL_ID_BYTES);
+  return VS_OK;
+}
+
+int vs_comm_init(vs_handle* h, int32_t nranks, int32_t rank, const uint8_t id[VS_NCCL_ID_BYTES]) {
+  cudaSetDevice(h->device);
+  if (!nccl().ok) return fail(h, VS_ERR_NO_DEVICE, "libnccl.so.2 not available");
+  if (nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(h, VS_ERR_INVALID_ARGUMENT, "rank must be in [0, nranks)");
+  vs_comm_destroy(h);
+  ncclUniqueId uid;
+  std::memcpy(uid.internal, id, VS_NCCL_ID_BYTES);
+  ncclComm_t c = nullptr;
+  const ncclResult_t r = nccl().comm_init_rank(&c, nranks, uid, rank);
+  if (r != ncclSuccess) return nccl_fail(h, r, "ncclCommInitRank");
+  h->comm = c;
+  h->comm_owned = true;
+  return VS_OK;
+}
+
+int vs_comm_attach(vs_handle* h, void* comm) {
+  vs_comm_destroy(h);
+  h->comm = static_cast<ncclComm_t>(comm);
+  h->comm_owned = false;
+  return VS_OK;
+}
+
+void vs_comm_destroy(vs_handle* h) {
+  if (h->comm && h->comm_owned && nccl().ok) {
+    cudaSetDevice(h->device);
+    nccl().comm_destroy(h->comm);
+  }
+  h->comm = nullptr;
+  h->comm_owned = false;
+}
+
+int vs_topk_allgather(vs_handle* h, void* comm, int32_t k, uint64_t* out_dev, void* stream) {
+  cudaSetDevice(h->device);
+  if (!h->has_results) return fail(h, VS_ERR_STATE, "no results");
+  ncclComm_t c = comm ? static_cast<ncclComm_t>(comm) : h->comm;
+  if (!c) return fail(h, VS_ERR_STATE, "no NCCL communicator (vs_comm_init / vs_comm_attach)");
+  if (!nccl().ok) return fail(h, VS_ERR_NO_DEVICE, "libnccl.so.2 not available");
+  int nranks = 0;
+  ncclResult_t r = nccl().comm_count(c, &nranks);
+  if (r != ncclSuccess) return nccl_fail(h, r, "ncclCommCount");
+  cudaStream_t st = pick(h, stream);
+  VS_CUDA(h, after_prev(h, st));
+  VS_CUDA(h, h->d_gather.ensure(static_cast<size_t>(nranks + 1) * k * 8));
+  auto* local = h->d_gather.as<unsigned long long>();
+  auto* all = local + k;
+  int rc = topk_run(h, h->d_keys.as<unsigned long long>(), h->lib.n, k, local, st);
+  if (rc) return rc;
+  // one all-gather of k u64 keys per rank (8 KB at k = 1000), then the same
+  // deterministic merge on every rank
+  r = nccl().all_gather(local, all, static_cast<size_t>(k), ncclUint64, c, st);
+  if (r != ncclSuccess) return nccl_fail(h, r, "ncclAllGather");
+  rc = topk_run(h, all, static_cast<long>(nranks) * k, k,
+                reinterpret_cast<unsigned long long*>(out_dev), st);
+  if (rc) return rc;
+  VS_CUDA(h, mark_done(h, st));
+  return VS_OK;
+}
+
+// ---------------------------------------------------- restart start draws
+int vs_start_draws(vs_handle* h, const uint64_t* seeds, const int32_t* n_tors, int32_t n,
+                   int32_t restarts, int32_t attempts, int32_t stride, float* out) {
+  cudaSetDevice(h->device);
+  if (!h->has_pocket) return fail(h, VS_ERR_STATE, "no pocket");
+  if (n < 0 || restarts < 1 || attempts < 1 || attempts > 50)
+    return fail(h, VS_ERR_INVALID_ARGUMENT, "n >= 0, restarts >= 1, attempts in [1, 50]");
+  int tmax = 0;
+  for (int i = 0; i < n; ++i) tmax = std::max(tmax, n_tors[i]);
+  if (tmax > kMaxTors) return fail(h, VS_ERR_CAPACITY, "torsions > 64");
+  if (stride < 7 + tmax) return fail(h, VS_ERR_CAPACITY, "stride < 7 + max torsions");
+  if (n == 0) return VS_OK;
+  VS_CUDA(h, quiesce(h));
+  cudaStream_t st = h->own;
+  const size_t rows = static_cast<size_t>(n) * restarts * attempts;
+  DBuf d_seeds, d_tors, d_out;
+  VS_CUDA(h, d_seeds.ensure(static_cast<size_t>(n) * 8));
+  VS_CUDA(h, d_tors.ensure(static_cast<size_t>(n) * 4));
+  VS_CUDA(h, d_out.ensure(rows * stride * 4));
+  int rc = VS_OK;
+  cudaError_t e = cudaMemcpyAsync(d_seeds.p, seeds, static_cast<size_t>(n) * 8,
+                                  cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(d_tors.p, n_tors, static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(d_out.p, 0, rows * stride * 4, st);
+  if (e == cudaSuccess)
+    e = launch_draws(st, h->pk, d_seeds.as<const unsigned long long>(), d_tors.as<const int>(), n,
+                     restarts, attempts, d_out.as<float>(), stride, h->sms);
+  if (e == cudaSuccess) {
+    ++h->launches;
+    e = cudaMemcpyAsync(out, d_out.p, rows * stride * 4, cudaMemcpyDeviceToHost, st);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) rc = cuda_fail(h, e, "start draws");
+  d_seeds.release();
+  d_tors.release();
+  d_out.release();
   return rc;
 }
 
@@ -1351,6 +1593,10 @@ int vs_rescore(vs_handle* h, const vs_library* L, int64_t n_poses, const int32_t
   using clk = std::chrono::steady_clock;
   const auto r0 = clk::now();
   if (!h->has_pocket) return fail(h, VS_ERR_STATE, "no pocket");
+  // pose indices are 32-bit on the device (first[], rs_orig, rs_off)
+  if (n_poses < 0 || n_poses > INT32_MAX)
+    return fail(h, VS_ERR_CAPACITY, "n_poses must be in [0, 2^31)");
+  VS_CUDA(h, quiesce(h));
   for (int64_t p = 1; p < n_poses; ++p)
     if (pose_lig[p] < pose_lig[p - 1])
       return fail(h, VS_ERR_INVALID_ARGUMENT, "pose_lig must be non-decreasing");

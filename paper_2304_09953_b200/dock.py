@@ -203,6 +203,23 @@ def key_id_rank(key: int) -> int:
 
 
 # ---------------------------------------------------------------- engine ---
+def _check_pose_arrays(lib: Library, pose_lig: np.ndarray, t: np.ndarray, q: np.ndarray,
+                       tors: np.ndarray) -> None:
+    """Sizes of flattened pose arrays against the library before they cross
+    the C-ABI, which sizes its copies from pose_lig and the library: t[3n],
+    q[4n], ligand indices in range, and the torsions of every pose's ligand
+    (check_counts, dock.cpp:219-230)."""
+    n = len(pose_lig)
+    if t.size != 3 * n or q.size != 4 * n:
+        raise ValueError(f"{n} poses need t of {3 * n} and q of {4 * n} values "
+                         f"(got {t.size} and {q.size})")
+    if n and (int(pose_lig.min()) < 0 or int(pose_lig.max()) >= len(lib)):
+        raise ValueError("pose ligand index out of range")
+    need = int(np.asarray(lib.n_tors, np.int64)[pose_lig].sum()) if n else 0
+    if tors.size != need:
+        raise AtomCountMismatch(f"poses need {need} torsion values, got {tors.size}")
+
+
 class Engine:
     """One GPU handle (vs_handle): pocket + resident library + results."""
 
@@ -327,6 +344,36 @@ class Engine:
         check(_lib.vs_topk_merge_device(self._h, C.c_void_p(keys_ptr), n, k, C.c_void_p(out_ptr),
                                         C.c_void_p(stream or 0)), self._h, "topk_merge")
 
+    # ---- multi-GPU: NCCL top-k gather (capi.h vs_comm_init / vs_topk_allgather)
+    def comm_init(self, nranks: int, rank: int, unique_id: bytes):
+        """Join an NCCL communicator of `nranks` handles (one per GPU);
+        unique_id = nccl_unique_id() of rank 0, broadcast by the caller."""
+        buf = (C.c_uint8 * 128).from_buffer_copy(bytes(unique_id))
+        check(_lib.vs_comm_init(self._h, nranks, rank, buf), self._h, "comm_init")
+
+    def comm_attach(self, comm_ptr: int):
+        check(_lib.vs_comm_attach(self._h, C.c_void_p(comm_ptr)), self._h, "comm_attach")
+
+    def topk_allgather(self, k: int, out_ptr: int, stream: int | None = None, comm_ptr: int = 0):
+        """Local top-k -> ncclAllGather of k keys per rank -> device merge,
+        on `stream`; out_ptr: k device u64 keys (identical on every rank)."""
+        check(_lib.vs_topk_allgather(self._h, C.c_void_p(comm_ptr or 0), k, C.c_void_p(out_ptr),
+                                     C.c_void_p(stream or 0)), self._h, "topk_allgather")
+
+    def start_draws(self, seeds, n_tors, restarts: int, attempts: int) -> np.ndarray:
+        """FP32 restart start draws of the device dock (capi.h
+        vs_start_draws): array [n, restarts, attempts, 7 + max T] of
+        t(3), q(4), theta(T)."""
+        seeds = np.ascontiguousarray(seeds, np.uint64)
+        n_tors = np.ascontiguousarray(n_tors, np.int32)
+        n = len(seeds)
+        stride = 7 + (int(n_tors.max()) if n else 0)
+        out = np.zeros(max(n * restarts * attempts * stride, 1), np.float32)
+        check(_lib.vs_start_draws(self._h, ptr(seeds, C.c_uint64), ptr(n_tors, C.c_int32), n,
+                                  restarts, attempts, stride, ptr(out, C.c_float)),
+              self._h, "start_draws")
+        return out[:n * restarts * attempts * stride].reshape(n, restarts, attempts, stride)
+
     def last_dock_ms(self) -> float:
         return float(_lib.vs_last_dock_ms(self._h))
 
@@ -358,6 +405,13 @@ class Engine:
         check(_lib.vs_measure_gather_peak(self._h, C.byref(v)), self._h, "gather_peak")
         return v.value
 
+    def measure_l2_gather_peak(self) -> float:
+        """Measured random 32 B (one sector) gather rate from L2, bytes/s:
+        the L2-gather roof of SURVEY §8(d) (capi.h vs_measure_gather_peak_ex)."""
+        v = C.c_double()
+        check(_lib.vs_measure_gather_peak_ex(self._h, 32, C.byref(v)), self._h, "gather_peak")
+        return 32.0 * v.value
+
     def stats(self) -> dict:
         """Work counters of the last dock (capi.h vs_last_stats)."""
         out = np.zeros(10, np.uint64)
@@ -384,6 +438,7 @@ class Engine:
         t = np.ascontiguousarray(t, np.float64).reshape(-1)
         q = np.ascontiguousarray(q, np.float64).reshape(-1)
         tors = np.ascontiguousarray(tors, np.float64).reshape(-1)
+        _check_pose_arrays(lib, pose_lig, t, q, tors)
         nt = tors.size
         if nt == 0:
             tors = np.zeros(1, np.float64)
@@ -407,6 +462,7 @@ class Engine:
         t = np.array(t, np.float64).reshape(-1).copy()
         q = np.array(q, np.float64).reshape(-1).copy()
         tors = np.array(tors, np.float64).reshape(-1).copy()
+        _check_pose_arrays(lib, pose_lig, t, q, tors)
         nt = tors.size
         if nt == 0:
             tors = np.zeros(1, np.float64)
@@ -424,6 +480,7 @@ class Engine:
         t = np.ascontiguousarray(t, np.float32).reshape(-1)
         q = np.ascontiguousarray(q, np.float32).reshape(-1)
         tors = np.ascontiguousarray(tors, np.float32).reshape(-1)
+        _check_pose_arrays(lib, pose_lig, t, q, tors)
         if tors.size == 0:
             tors = np.zeros(1, np.float32)
         n = len(pose_lig)
@@ -434,6 +491,13 @@ class Engine:
                               ptr(q, C.c_float), ptr(tors, C.c_float), ptr(geo, C.c_float),
                               ptr(resc, C.c_float)), self._h, "rescore")
         return geo[:n], resc[:n]
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId of the NCCL the process has (capi.h vs_nccl_unique_id)."""
+    buf = (C.c_uint8 * 128)()
+    check(_lib.vs_nccl_unique_id(buf), None, "nccl_unique_id")
+    return bytes(buf)
 
 
 def _classes_c(classes):

@@ -110,21 +110,39 @@ def ligand_cost(lib: Library) -> np.ndarray:
     return 256.0 * n + 32.0 * t * (n + n * (n - 1) / 2)
 
 
-def gather_topk(engine: Engine, k: int, group=None):
-    """Per-rank device top-k -> one NCCL all-gather of k u64 keys per rank ->
-    device merge on every rank.  Returns the merged keys (torch tensor on the
+def init_comm(engine: Engine, group=None) -> None:
+    """Create the engine's NCCL communicator over the ranks of a
+    torch.distributed group (any backend: it only carries NCCL's 128-byte
+    unique id from rank 0; NCCL's usual bootstrap)."""
+    import torch.distributed as dist
+    from .dock import nccl_unique_id
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    box = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group else 0,
+                               group=group)
+    engine.comm_init(world, rank, box[0])
+
+
+def gather_topk(engine: Engine, k: int, stream: int | None = None):
+    """Global top-k across ranks through the C-ABI (capi.h
+    vs_topk_allgather): per-rank device top-k -> one ncclAllGather of k u64
+    keys per rank -> device merge on every rank, all on `stream` (the stream
+    the dock ran on; the handle also orders it after its last dock).  Needs
+    init_comm first.  Returns the merged keys (torch int64 tensor on the
     rank's device)."""
     import torch
-    import torch.distributed as dist
     dev = torch.device("cuda", torch.cuda.current_device())
-    stream = torch.cuda.current_stream().cuda_stream
-    local = torch.empty(k, dtype=torch.int64, device=dev)
-    # keys are produced on `stream`; NCCL runs on its own stream ordered
-    # after the current one
-    engine.topk_device(k, local.data_ptr(), stream)
-    world = dist.get_world_size(group)
-    gathered = torch.empty(world * k, dtype=torch.int64, device=dev)
-    dist.all_gather_into_tensor(gathered, local, group=group)
+    if stream is None:
+        stream = torch.cuda.current_stream().cuda_stream
     merged = torch.empty(k, dtype=torch.int64, device=dev)
-    engine.topk_merge_device(gathered.data_ptr(), world * k, k, merged.data_ptr(), stream)
+    engine.topk_allgather(k, merged.data_ptr(), stream)
     return merged
+
+
+def merge_topk_host(keys: np.ndarray, k: int) -> np.ndarray:
+    """Host merge of gathered top-k keys (capi.h vs_topk_merge_host)."""
+    keys = np.ascontiguousarray(keys, np.uint64)
+    out = np.zeros(k, np.uint64)
+    check(_lib.vs_topk_merge_host(ptr(keys, C.c_uint64), len(keys), k, ptr(out, C.c_uint64)),
+          None, "topk_merge_host")
+    return out

@@ -103,26 +103,6 @@ def test_dock_polish_modes_bit_exact(V, engine, lib200, pocket_json, grid, polis
     _assert_same(res, ora, prm.keep_top)
 
 
-@pytest.mark.parametrize("grid", [0.0, 0.4])
-def test_fused_mode_matches_staged(V, engine, lib200, pocket_json, grid, monkeypatch):
-    """The single-launch fused kernel (VSCREEN_DOCK_MODE=fused, kept for
-    A/B) gives the staged kernels' results bit for bit, polish 0 and 1."""
-    lib, _ = lib200
-    sub = lib.subset(range(0, 60))
-    sub.seeds = lib.seeds[:60]
-    pocket = V.parse_pocket_json(pocket_json)
-    engine.set_pocket(pocket, grid_spacing=grid)
-    for polish in (0, 1):
-        prm = _params(V, polish=polish)
-        staged = engine.dock_host(sub, prm)
-        monkeypatch.setenv("VSCREEN_DOCK_MODE", "fused")
-        fused = engine.dock_host(sub, prm)
-        monkeypatch.delenv("VSCREEN_DOCK_MODE")
-        np.testing.assert_array_equal(staged.keys, fused.keys)
-        np.testing.assert_array_equal(staged.best.view(np.uint32), fused.best.view(np.uint32))
-        np.testing.assert_array_equal(_bits(staged.surv), _bits(fused.surv))
-
-
 def test_polish0_scores_match_reference(V, engine, lib200, pocket_json):
     """Without the polish the restart's score is the flex's exact score:
     emitted poses re-scored by the reference FP64 scorer within 1e-5."""
