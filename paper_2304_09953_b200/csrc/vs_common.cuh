@@ -113,6 +113,20 @@ __device__ __forceinline__ void ldg_hcell(const uint4* c, float4& lo, float4& hi
   hi = make_float4(d.x, d.y, e.x, e.y);
 }
 
+// floor(g) and its integer value for a cell lookup without the XU pipe:
+// y = 2^23 + g rounded toward zero (FADD.RZ, FMA pipe) holds floor(g) in its
+// low mantissa bits for 0 <= g < 2^23, so floor(g) = y - 2^23 exactly and
+// i = bits(y) - bits(2^23).  Every g < 0 gives i < 0 (or, below -2^23, a
+// value above any grid extent when read unsigned), i.e. "off the grid" as
+// floorf would: the in-grid decision and, in the grid, the fraction g -
+// floor(g) are bit-identical to floorf / F2I (which run on the quarter-rate
+// XU pipe, 6 per lookup).
+__device__ __forceinline__ int floor_cell(float g, float* fl) {
+  const float y = __fadd_rz(g, 8388608.0f);
+  *fl = y - 8388608.0f;
+  return __float_as_int(y) - 0x4B000000;
+}
+
 // One trilinear lookup split in two halves so that callers can issue the
 // next lookup's loads before consuming this one.
 struct TriCell {
@@ -127,8 +141,8 @@ __device__ __forceinline__ TriCell tri_issue(const GridDev& g, const float4* __r
   const float gx = (x - g.ox) * g.inv_h;
   const float gy = (y - g.oy) * g.inv_h;
   const float gz = (z - g.oz) * g.inv_h;
-  const float fx = floorf(gx), fy = floorf(gy), fz = floorf(gz);
-  const int ix = static_cast<int>(fx), iy = static_cast<int>(fy), iz = static_cast<int>(fz);
+  float fx, fy, fz;
+  const int ix = floor_cell(gx, &fx), iy = floor_cell(gy, &fy), iz = floor_cell(gz, &fz);
   // gx < 0 <=> ix < 0 (floor), so one unsigned compare per axis covers both
   // ends; out-of-grid lanes read cell 0 and are zeroed (no divergent branch)
   TriCell c;
@@ -499,11 +513,8 @@ static __device__ __forceinline__ float eval_key(const PocketDev& pk, const floa
         gx[u] = fmaf(a00, a.x, fmaf(a01, a.y, fmaf(a02, a.z, ux)));
         gy[u] = fmaf(a10, a.x, fmaf(a11, a.y, fmaf(a12, a.z, uy)));
         gz[u] = fmaf(a20, a.x, fmaf(a21, a.y, fmaf(a22, a.z, uz)));
-        fx[u] = floorf(gx[u]);
-        fy[u] = floorf(gy[u]);
-        fz[u] = floorf(gz[u]);
-        const int ix = static_cast<int>(fx[u]), iy = static_cast<int>(fy[u]),
-                  iz = static_cast<int>(fz[u]);
+        const int ix = floor_cell(gx[u], &fx[u]), iy = floor_cell(gy[u], &fy[u]),
+                  iz = floor_cell(gz[u], &fz[u]);
         in[u] = static_cast<unsigned>(ix) <= mx && static_cast<unsigned>(iy) <= my &&
                 static_cast<unsigned>(iz) <= mz;
         const unsigned cell = static_cast<unsigned>(iz * g.cxy + iy * g.cx + ix);
@@ -549,8 +560,8 @@ static __device__ __forceinline__ float eval_key(const PocketDev& pk, const floa
 // as in eval_key
 __device__ __forceinline__ float key_at_grid(const PocketDev& pk, float gx, float gy, float gz) {
   const GridDev& g = pk.grid;
-  const float fx = floorf(gx), fy = floorf(gy), fz = floorf(gz);
-  const int ix = static_cast<int>(fx), iy = static_cast<int>(fy), iz = static_cast<int>(fz);
+  float fx, fy, fz;
+  const int ix = floor_cell(gx, &fx), iy = floor_cell(gy, &fy), iz = floor_cell(gz, &fz);
   const bool in = static_cast<unsigned>(ix) <= static_cast<unsigned>(g.nx - 2) &&
                   static_cast<unsigned>(iy) <= static_cast<unsigned>(g.ny - 2) &&
                   static_cast<unsigned>(iz) <= static_cast<unsigned>(g.nz - 2);

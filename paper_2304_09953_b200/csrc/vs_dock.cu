@@ -183,6 +183,7 @@ static __device__ __forceinline__ int rigid_compass(const PocketDev& pk, const f
 template <int kGrid>
 static __device__ VS_PHASE int sweep_phase(const PocketDev& pk, const Dims d,
                                                const float4* __restrict__ rots,
+                                               const float4* __restrict__ rots_p,
                                                const int* __restrict__ perm, int K, int N,
                                                int lane, PoseF* P, int* n_trans, int polish) {
   const WarpSmem s = dock_smem(d);
@@ -207,7 +208,7 @@ static __device__ VS_PHASE int sweep_phase(const PocketDev& pk, const Dims d,
   int best_k = 0x7fffffff;
   for (int p = lane; p < K; p += 32) {
     const int k = perm[p];
-    const float4 rq = rots[k];
+    const float4 rq = rots_p[p];  // = rots[k], loaded independently of k
     float w4, x4, y4, z4;
     det_quat_mul(rq.x, rq.y, rq.z, rq.w, qs0, qs1, qs2, qs3, &w4, &x4, &y4, &z4);
     det_quat_normalize(&w4, &x4, &y4, &z4);
@@ -848,8 +849,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 8)
 template <int kGrid>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_SWEEP)
     vs_sweep_kernel(const __grid_constant__ LibDev lib, const __grid_constant__ PocketDev pk,
-                    const float4* __restrict__ rots, const int* __restrict__ perm,
-                    const __grid_constant__ DockParams prm, const int* __restrict__ order,
+                    const float4* __restrict__ rots, const float4* __restrict__ rots_p,
+                    const int* __restrict__ perm, const __grid_constant__ DockParams prm, const int* __restrict__ order,
                     int n_order, int* __restrict__ counter, int nmax,
                     const __grid_constant__ StageBufs sb) {
   const Dims d{nmax, 0, 0, kLaySweep};
@@ -874,7 +875,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_SWEEP)
     P.q[2] = pq.z;
     P.q[3] = pq.w;
     int n_trans = 0;
-    const int best_k = sweep_phase<kGrid>(pk, d, rots, perm, prm.K, N, lane, &P, &n_trans,
+    const int best_k = sweep_phase<kGrid>(pk, d, rots, rots_p, perm, prm.K, N, lane, &P, &n_trans,
                                                 prm.polish);
     if (lane == 0) {
       sb.pose[2 * lig] = make_float4(P.t[0], P.t[1], P.t[2], pt.w);
@@ -1089,7 +1090,8 @@ size_t stage_smem_per_block(int nmax, int tmax, int mvmax) {
 
 template <int kGrid>
 static cudaError_t staged_impl(int sms, cudaStream_t st, const LibDev& lib, const PocketDev& pk,
-                               const float4* rots, const int* perm, const DockParams& prm,
+                               const float4* rots, const float4* rots_p, const int* perm,
+                               const DockParams& prm,
                                const int* order, int n, int* counters, int nmax, int tmax,
                                int mvmax, const StageBufs& sb, const DockOut& out,
                                uint64_t* launches, cudaEvent_t* evs, int* kinds) {
@@ -1124,7 +1126,7 @@ static cudaError_t staged_impl(int sms, cudaStream_t st, const LibDev& lib, cons
     mark(0, true);
     ++c;
     mark(1, false);
-    vs_sweep_kernel<kGrid><<<b_sweep, T, sm_sweep, st>>>(lib, pk, rots, perm, prm, order, n,
+    vs_sweep_kernel<kGrid><<<b_sweep, T, sm_sweep, st>>>(lib, pk, rots, rots_p, perm, prm, order, n,
                                                         counters + c, nmax, sb);
     mark(1, true);
     ++c;
@@ -1195,15 +1197,16 @@ cudaError_t launch_draws(cudaStream_t st, const PocketDev& pk, const unsigned lo
 }
 
 // rots: the K rotations in index order; perm: the sweep's lane order (a
-// permutation of 0..K-1, see sweep_phase)
+// permutation of 0..K-1, see sweep_phase); rots_p[p] = rots[perm[p]]
 cudaError_t launch_staged(bool grid, int sms, cudaStream_t st, const LibDev& lib,
-                          const PocketDev& pk, const float4* rots, const int* perm,
+                          const PocketDev& pk, const float4* rots, const float4* rots_p,
+                          const int* perm,
                           const DockParams& prm, const int* order, int n, int* counters,
                           int nmax, int tmax, int mvmax, const StageBufs& sb, const DockOut& out,
                           uint64_t* launches, cudaEvent_t* evs, int* kinds) {
-  return grid ? staged_impl<1>(sms, st, lib, pk, rots, perm, prm, order, n, counters, nmax, tmax,
+  return grid ? staged_impl<1>(sms, st, lib, pk, rots, rots_p, perm, prm, order, n, counters, nmax, tmax,
                                mvmax, sb, out, launches, evs, kinds)
-              : staged_impl<0>(sms, st, lib, pk, rots, perm, prm, order, n, counters, nmax, tmax,
+              : staged_impl<0>(sms, st, lib, pk, rots, rots_p, perm, prm, order, n, counters, nmax, tmax,
                                mvmax, sb, out, launches, evs, kinds);
 }
 

@@ -31,8 +31,8 @@ cudaError_t launch_draws(cudaStream_t st, const PocketDev& pk, const unsigned lo
                          const int* n_tors, int n, int restarts, int attempts, float* out,
                          int stride, int sms);
 cudaError_t launch_staged(bool grid, int sms, cudaStream_t st, const LibDev& lib,
-                          const PocketDev& pk, const float4* rots, const int* perm,
-                          const DockParams& prm, const int* order, int n, int* counters,
+                          const PocketDev& pk, const float4* rots, const float4* rots_p,
+                          const int* perm, const DockParams& prm, const int* order, int n, int* counters,
                           int nmax, int tmax, int mvmax, const StageBufs& sb, const DockOut& out,
                           uint64_t* launches, cudaEvent_t* evs, int* kinds);
 cudaError_t launch_rescore(bool grid, int blocks, size_t smem, cudaStream_t st, const LibDev& lib,
@@ -591,6 +591,9 @@ std::vector<int> rotation_order(const std::vector<float4>& r) {
   std::vector<int> perm(static_cast<size_t>(K));
   std::iota(perm.begin(), perm.end(), 0);
   const int G = K / 32;
+#ifdef VS_ROT_INDEX_ORDER  // A/B variant: lanes in index order
+  return perm;
+#endif
   if (G < 2) return perm;
   auto sim = [](const float4& a, const double* c) {
     return std::fabs(a.x * c[0] + a.y * c[1] + a.z * c[2] + a.w * c[3]);
@@ -898,13 +901,17 @@ int vs_dock(vs_handle* h, const vs_dock_params* prm, void* stream) {
   const int n = P.n;
   const int R = prm->restarts, KT = prm->keep_top;
   if (h->rots_k != prm->rotations || h->rots_seed != prm->rotation_seed) {
-    // the K rotations (index order) followed by the sweep's lane order
+    // the K rotations in index order, the same in the sweep's lane order,
+    // then the lane order itself
     const auto rs = rotation_set(prm->rotations, prm->rotation_seed);
     const auto perm = rotation_order(rs);
+    std::vector<float4> rp(rs.size());
+    for (size_t p = 0; p < rs.size(); ++p) rp[p] = rs[static_cast<size_t>(perm[p])];
     const size_t rb = rs.size() * sizeof(float4);
-    std::vector<unsigned char> blob(rb + perm.size() * sizeof(int));
+    std::vector<unsigned char> blob(2 * rb + perm.size() * sizeof(int));
     std::memcpy(blob.data(), rs.data(), rb);
-    std::memcpy(blob.data() + rb, perm.data(), perm.size() * sizeof(int));
+    std::memcpy(blob.data() + rb, rp.data(), rb);
+    std::memcpy(blob.data() + 2 * rb, perm.data(), perm.size() * sizeof(int));
     VS_CUDA(h, h->d_rots.ensure(blob.size()));
     VS_CUDA(h, cudaMemcpyAsync(h->d_rots.p, blob.data(), blob.size(), cudaMemcpyHostToDevice, st));
     VS_CUDA(h, cudaStreamSynchronize(st));
@@ -1000,8 +1007,9 @@ int vs_dock(vs_handle* h, const vs_dock_params* prm, void* stream) {
     }
     h->pkind.assign(npairs, -1);  // -1: no launch recorded in this slot
     const float4* rots = h->d_rots.as<const float4>();
-    const int* perm = reinterpret_cast<const int*>(rots + prm->rotations);
-    VS_CUDA(h, launch_staged(grid, h->sms, st, ld, h->pk, rots, perm, dp,
+    const float4* rots_p = rots + prm->rotations;
+    const int* perm = reinterpret_cast<const int*>(rots_p + prm->rotations);
+    VS_CUDA(h, launch_staged(grid, h->sms, st, ld, h->pk, rots, rots_p, perm, dp,
                              P.d_order.as<int>() + b.start, b.count, h->d_counters.as<int>(),
                              b.nmax, b.tmax, b.mvmax, sb, out, &h->launches, h->pev.data(),
                              h->pkind.data()));

@@ -170,3 +170,41 @@ def test_c5_rescoring_only_fine_grid(V, engine, pocket_json):
         err = np.abs(g_grid - g_an) / np.maximum(np.abs(g_an), 1.0)
         # trilinear at 0.2 A vs the analytic field: ~h^2/(8 sigma^2) per site
         assert np.median(err) < 5e-3, np.median(err)
+
+
+def test_c4_bench_config_bit_exact(V, engine):
+    """C4 exactly as bench.py --config c4 runs it: 0.4 A maps of the C2
+    pocket, R=30, K=256, A=16, F=2, polish 1, size classes {60..81}x{15..21};
+    the bench's own library builder (flexible_smiles seed 7, campaign seeds)."""
+    from oracle import sweep
+    import bench
+    lib, _, _ = bench.build_flexible(48, 0, 1, 16)
+    pocket = bench.make_pocket()
+    prm = bench.params()
+    engine.set_pocket(pocket, grid_spacing=0.4, grid_pad=2.0)
+    res = engine.dock_host(lib, prm, classes=bench.C4_CLASSES)
+    ora = sweep.dock_library(sweep.OraclePocket(pocket, 0.4, 2.0), lib, prm, threads=16)
+    _same(res, ora)
+    np.testing.assert_array_equal(res.surv_tors.view(np.uint32)[:len(ora["surv_tors"])],
+                                  ora["surv_tors"].view(np.uint32))
+    assert lib.n_atoms.min() >= 60 and lib.n_tors.min() >= 15
+
+
+def test_c2_whole_bench_library_bit_exact(V, engine):
+    """The whole 100k-ligand C2 bench library (bench.build_workload, bench
+    knobs, 0.4 A maps) against the oracle on every host core (~30 s): keys,
+    kept / surviving counts, best and every survivor pose bit for bit, and
+    the global top-1000."""
+    import os
+    from oracle import sweep
+    import bench
+    lib, _, _ = bench.build_workload(100_000, 0, 1, os.cpu_count() or 16)
+    pocket = bench.make_pocket()
+    prm = bench.params()
+    engine.set_pocket(pocket, grid_spacing=0.4, grid_pad=2.0)
+    res = engine.dock_host(lib, prm)
+    top = engine.topk(1000)
+    ora = sweep.dock_library(sweep.OraclePocket(pocket, 0.4, 2.0), lib, prm,
+                             threads=os.cpu_count() or 16)
+    _same(res, ora)
+    np.testing.assert_array_equal(top, sweep.topk(ora["keys"], 1000))

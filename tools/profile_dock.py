@@ -28,7 +28,8 @@ def main():
     for _ in range(2):
         eng.dock(prm)
         ms = eng.last_dock_ms()
-    print(f"ligands={len(lib)} dock_ms={ms:.3f} lig/s={len(lib) / ms * 1e3:.1f} stats={eng.stats()}")
+    ph = {k: round(v, 2) for k, v in eng.phase_ms_ex().items()}
+    print(f"ligands={len(lib)} dock_ms={ms:.3f} lig/s={len(lib) / ms * 1e3:.1f} phases={ph}")
     eng.close()
 
 
