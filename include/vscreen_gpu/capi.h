@@ -246,6 +246,33 @@ int vs_rescore(vs_handle* h, const vs_library* lib, int64_t n_poses, const int32
 int vs_ascend(vs_handle* h, const vs_library* lib, int64_t n_poses, const int32_t* pose_lig,
               double* t, double* q, double* tors, int32_t max_steps, double* score,
               int32_t* steps);
+/* geometric_score / rescore (dock.cpp:278-282, 297-316) of given poses in
+ * FP64 on the device (the score_gradient arithmetic without the gradient;
+ * analytic pocket): geo[n], resc[n] optional.  The drop-in's per-pose
+ * scoring (include/vscreen/dock.hpp). */
+int vs_score64(vs_handle* h, const vs_library* lib, int64_t n_poses, const int32_t* pose_lig,
+               const double* t, const double* q, const double* tors, double* geo, double* resc);
+
+/* Refined dock results (caller-owned): ligand i's poses at slots
+ * i * restarts + r, r < n_poses[i], sorted by score descending; torsions at
+ * tors_off(i) * restarts + r * n_tors(i).  q is unit (pose_of, dock.cpp:210). */
+typedef struct {
+  int32_t* n_poses; /* [n]; -1 = out of every size class */
+  double* t;        /* [n * restarts * 3] */
+  double* q;        /* [n * restarts * 4] (w, x, y, z) */
+  double* tors;     /* [sum n_tors * restarts] */
+  double* score;    /* [n * restarts] FP64 geometric score of the refined pose */
+  int32_t* restart; /* [n * restarts] optional: the restart each pose came from */
+} vs_refined;
+/* dock() with the reference's contract (dock.cpp:318-371): the sweep-v1
+ * restarts (vs_dock, every kept pose) each refined by the reference ascent
+ * (vs_ascend, max_steps), then the reference's keep rule on the refined
+ * coordinates in restart order (RMSD >= diversity_delta from every kept
+ * pose) and a stable sort by score descending. */
+int vs_dock_refined_host(vs_handle* h, const vs_library* lib, const vs_size_class* classes,
+                         int32_t n_classes, const vs_dock_params* params, int32_t max_steps,
+                         vs_refined* out);
+
 /* Device time (ms, CUDA events on the launch stream) of the rescore kernels
  * of the last vs_rescore call (-1 before the first). */
 double vs_last_rescore_ms(const vs_handle* h);

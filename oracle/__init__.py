@@ -23,3 +23,7 @@ def build(ref: bool = True) -> None:
     subprocess.run(["make", "-C", HERE, "oracle"], check=True, stdout=subprocess.DEVNULL)
     if ref and os.path.isdir("/root/reference/proj/src"):
         subprocess.run(["make", "-C", HERE, "ref"], check=True, stdout=subprocess.DEVNULL)
+        # the reference's own dock / batcher unit tests, compiled against the
+        # drop-in headers and library (oracle/build_ref_tests.sh)
+        subprocess.run(["bash", os.path.join(HERE, "build_ref_tests.sh")], check=True,
+                       stdout=subprocess.DEVNULL)

@@ -76,6 +76,11 @@ class vs_results(C.Structure):
                 ("all_tors", P(C.c_float)), ("keys", P(C.c_uint64))]
 
 
+class vs_refined(C.Structure):
+    _fields_ = [("n_poses", P(C.c_int32)), ("t", P(C.c_double)), ("q", P(C.c_double)),
+                ("tors", P(C.c_double)), ("score", P(C.c_double)), ("restart", P(C.c_int32))]
+
+
 class vs_ligand_buf(C.Structure):
     _fields_ = [("cap_atoms", C.c_int32), ("cap_bonds", C.c_int32), ("cap_tors", C.c_int32),
                 ("cap_moving", C.c_int32), ("n_atoms", C.c_int32), ("n_bonds", C.c_int32),
@@ -131,6 +136,10 @@ _SIGS = {
     "vs_rescore": (C.c_int, [C.c_void_p, P(vs_library), C.c_int64, P(C.c_int32), P(C.c_float),
                              P(C.c_float), P(C.c_float), P(C.c_float), P(C.c_float)]),
     "vs_last_rescore_ms": (C.c_double, [C.c_void_p]),
+    "vs_score64": (C.c_int, [C.c_void_p, P(vs_library), C.c_int64, P(C.c_int32), P(C.c_double),
+                             P(C.c_double), P(C.c_double), P(C.c_double), P(C.c_double)]),
+    "vs_dock_refined_host": (C.c_int, [C.c_void_p, P(vs_library), P(vs_size_class), C.c_int32,
+                                       P(vs_dock_params), C.c_int32, P(vs_refined)]),
     "vs_ascend": (C.c_int, [C.c_void_p, P(vs_library), C.c_int64, P(C.c_int32), P(C.c_double),
                             P(C.c_double), P(C.c_double), C.c_int32, P(C.c_double),
                             P(C.c_int32)]),

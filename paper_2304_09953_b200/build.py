@@ -15,6 +15,10 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libvscreen_gpu.so")
+# the C++ drop-in for the reference's own API (include/vscreen/*.hpp): the
+# library reference callers link instead of the CPU vscreen_core
+CORE = os.path.join(HERE, "libvscreen_core.so")
+DROPIN = ["vs_dropin_chem.cpp", "vs_dropin_dock.cpp", "vs_dropin_batcher.cpp"]
 SOURCES = ["vs_kernels.cu", "vs_dock.cu", "vs_grad.cu", "vs_embed.cu", "vs_runtime.cu",
            "vs_host.cpp", "vs_ingest.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -23,14 +27,37 @@ FLAGS = ["-std=c++17", "-O3", "-lineinfo", "--fmad=false", "-ccbin", "/usr/bin/g
          "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall", "-diag-suppress", "550"]
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+def _stale(lib=LIB, extra=()) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
+    t = os.path.getmtime(lib)
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + list(extra)
     deps.append(os.path.join(HERE, "..", "include", "vscreen_gpu", "capi.h"))
     deps.append(os.path.abspath(__file__))
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
+
+
+def _json_dir() -> str:
+    import sysconfig
+    return os.path.join(sysconfig.get_paths()["purelib"], "include", "cudnn_frontend", "thirdparty")
+
+
+def build_core(force: bool = False, verbose: bool = False) -> str:
+    """libvscreen_core.so: the drop-in for the reference's C++ API, linked
+    against libvscreen_gpu.so (found next to it at run time)."""
+    inc = os.path.join(HERE, "..", "include")
+    srcs = [os.path.join(CSRC, "dropin", f) for f in DROPIN]
+    extra = srcs + [os.path.join(inc, "vscreen", f) for f in os.listdir(os.path.join(inc, "vscreen"))]
+    if not force and not _stale(CORE, extra) and os.path.getmtime(CORE) >= os.path.getmtime(LIB):
+        return CORE
+    cmd = ["/usr/bin/g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-Wall", f"-I{inc}",
+           f"-I{_json_dir()}", *srcs, f"-L{HERE}", "-lvscreen_gpu", "-Wl,-rpath,$ORIGIN",
+           "-o", CORE + ".tmp"]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+    os.replace(CORE + ".tmp", CORE)
+    return CORE
 
 
 def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
@@ -38,6 +65,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
     (e.g. defines=("VS_MINB=5",), out=".../libvscreen_gpu.minb5.so")."""
     lib = out or LIB
     if not force and not defines and out is None and not _stale():
+        build_core(verbose=verbose)
         return LIB
     tag = "_".join(d.replace("=", "") for d in defines) or "default"
     objs = []
@@ -55,6 +83,8 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
     os.replace(lib + ".tmp", lib)
+    if out is None and not defines:
+        build_core(force=True, verbose=verbose)
     return lib
 
 

@@ -147,7 +147,8 @@ __global__ void __launch_bounds__(128)
                    long n_poses, const int* __restrict__ pose_lig, const long* __restrict__ tb,
                    const double* __restrict__ t, const double* __restrict__ q,
                    const double* __restrict__ tors, int nmax, int tmax, double* __restrict__ score,
-                   double* __restrict__ gt, double* __restrict__ gq, double* __restrict__ gtor) {
+                   double* __restrict__ gt, double* __restrict__ gq, double* __restrict__ gtor,
+                   double* __restrict__ resc) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double3* y = reinterpret_cast<double3*>(smem) + static_cast<size_t>(wib) * 3 * nmax;
@@ -171,8 +172,34 @@ __global__ void __launch_bounds__(128)
   __syncwarp();
   grad_chain_mv(lib, meta, mov_off, th, y, lane);
   grad_pose(y, N, qw, qx, qy, qz, t + 3 * p, x, lane);
-  const double s0 = grad_score(pk, x, N, g, lane);
+  const bool with_grad = gt != nullptr;
+  const double s0 = grad_score(pk, x, N, with_grad ? g : nullptr, lane);
   __syncwarp();
+  if (!with_grad) {
+    // score-only (geometric_score, dock.cpp:278-282), plus the kind bonuses
+    // of rescore (dock.cpp:297-316): hbond sites over N/O atoms (class 2),
+    // lipophilic sites over C atoms (class 1), FP64
+    double b = 0.0;
+    if (resc) {
+      for (int a = lane; a < N; a += 32) {
+        const int cls = static_cast<int>(lib.atoms[meta.x + a].w);
+        if (cls == 0) continue;
+        const int kind = cls == 2 ? 1 : 2;
+        for (int k = 0; k < pk.n_sites; ++k) {
+          const SiteD st = pk.sites[k];
+          if (st.kind != kind) continue;
+          const double dx = x[a].x - st.cx, dy = x[a].y - st.cy, dz = x[a].z - st.cz;
+          b += st.w * exp(-(dx * dx + dy * dy + dz * dz) * st.inv2s2);
+        }
+      }
+      b = wsum(b);
+    }
+    if (lane == 0) {
+      score[p] = s0;
+      if (resc) resc[p] = s0 + b;
+    }
+    return;
+  }
   // translation and raw rotation derivatives, then the tangent projection
   double gtx = 0.0, gty = 0.0, gtz = 0.0, r0 = 0.0, r1 = 0.0, r2 = 0.0, r3 = 0.0;
   for (int i = lane; i < N; i += 32) {
@@ -430,7 +457,7 @@ cudaError_t launch_grad(cudaStream_t st, const LibDev& lib, const SiteD* sites, 
                         const double lo[3], const double hi[3], double r, double lam,
                         long n_poses, const int* pose_lig, const long* tb, const double* t,
                         const double* q, const double* tors, int nmax, int tmax, double* score,
-                        double* gt, double* gq, double* gtor) {
+                        double* gt, double* gq, double* gtor, double* resc) {
   GradPocket pk;
   pk.sites = sites;
   pk.n_sites = n_sites;
@@ -445,7 +472,7 @@ cudaError_t launch_grad(cudaStream_t st, const LibDev& lib, const SiteD* sites, 
                        static_cast<int>(smem));
   const long blocks = (n_poses + 3) / 4;
   vs_grad_kernel<<<static_cast<unsigned>(blocks), 128, smem, st>>>(
-      lib, pk, n_poses, pose_lig, tb, t, q, tors, nmax, tmax, score, gt, gq, gtor);
+      lib, pk, n_poses, pose_lig, tb, t, q, tors, nmax, tmax, score, gt, gq, gtor, resc);
   return cudaGetLastError();
 }
 

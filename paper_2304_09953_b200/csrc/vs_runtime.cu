@@ -56,7 +56,7 @@ cudaError_t launch_grad(cudaStream_t st, const LibDev& lib, const SiteD* sites, 
                         const double lo[3], const double hi[3], double r, double lam,
                         long n_poses, const int* pose_lig, const long* tb, const double* t,
                         const double* q, const double* tors, int nmax, int tmax, double* score,
-                        double* gt, double* gq, double* gtor);
+                        double* gt, double* gq, double* gtor, double* resc = nullptr);
 cudaError_t launch_grid(cudaStream_t st, const PocketDev& pk, float* steric, float* hb,
                         float* lipo, float* key, float4* cells);
 int topk_chunk();
@@ -218,6 +218,11 @@ struct vs_handle {
   bool staged_run = false;
   PinnedVec<uint8_t> fetch_stage;  // vs_fetch_results' pinned staging, reused across calls
   Packed rpack;              // vs_rescore's library staging, reused across calls
+  // the per-pose FP64 paths (vs_score64, vs_score_gradient, vs_ascend):
+  // library staging and pose arrays reused across calls, so a per-pose
+  // caller (the C++ drop-in's geometric_score) allocates nothing per call
+  Packed xpack;
+  DBuf xbuf[10];
   DBuf rbuf[9];              // vs_rescore's per-bucket pose arrays, reused across calls
   // vs_rescore's pinned staging of the concatenated per-bucket pose arrays
   PinnedVec<int> rs_lig, rs_off, rs_orig;
@@ -694,6 +699,8 @@ void vs_destroy(vs_handle* h) {
   cudaStreamSynchronize(h->own);
   h->lib.release();
   h->rpack.release();
+  h->xpack.release();
+  for (DBuf& b : h->xbuf) b.release();
   for (DBuf& b : h->rbuf) b.release();
   for (DBuf* b : {&h->d_sites, &h->d_softtab, &h->d_sites64, &h->d_maps, &h->d_surv, &h->d_surv_tors, &h->d_all, &h->d_all_tors,
                   &h->d_best, &h->d_nkept, &h->d_nsurv, &h->d_keys, &h->d_counters, &h->d_rots, &h->d_topk_a, &h->d_topk_b, &h->d_stats,
@@ -1465,25 +1472,42 @@ int relax_on_device(vs_handle* h, int n, const int64_t* atom_off, const int32_t*
 
 extern "C" {
 
+namespace {
+// FP64 score (+ gradient, or + rescore bonuses) of given poses on the device
+int score64_run(vs_handle* h, const vs_library* L, int64_t n_poses, const int32_t* pose_lig,
+                const double* t, const double* q, const double* tors, double* score,
+                double* grad_t, double* grad_q, double* grad_tors, double* resc);
+}  // namespace
+
 int vs_score_gradient(vs_handle* h, const vs_library* L, int64_t n_poses,
                       const int32_t* pose_lig, const double* t, const double* q,
                       const double* tors, double* score, double* grad_t, double* grad_q,
                       double* grad_tors) {
+  return score64_run(h, L, n_poses, pose_lig, t, q, tors, score, grad_t, grad_q, grad_tors,
+                     nullptr);
+}
+
+int vs_score64(vs_handle* h, const vs_library* L, int64_t n_poses, const int32_t* pose_lig,
+               const double* t, const double* q, const double* tors, double* geo, double* resc) {
+  return score64_run(h, L, n_poses, pose_lig, t, q, tors, geo, nullptr, nullptr, nullptr, resc);
+}
+
+namespace {
+int score64_run(vs_handle* h, const vs_library* L, int64_t n_poses, const int32_t* pose_lig,
+                const double* t, const double* q, const double* tors, double* score,
+                double* grad_t, double* grad_q, double* grad_tors, double* resc) {
   cudaSetDevice(h->device);
+  const bool grad = grad_t != nullptr;
+  // scoring takes any box (the reference checks bounds only in dock(),
+  // dock.cpp:321): an empty box just puts every atom outside a wall
   if (!h->has_pocket) return fail(h, VS_ERR_STATE, "no pocket");
-  if (h->empty_bounds) return fail(h, VS_ERR_EMPTY_BOUNDS, "pocket bounds are empty");
   if (n_poses < 0) return fail(h, VS_ERR_INVALID_ARGUMENT, "negative pose count");
   if (n_poses == 0) return VS_OK;
-  Packed P;
-  DBuf d_pl, d_tb, d_t, d_q, d_th, d_s, d_gt, d_gq, d_gth;
-  struct Release {  // device buffers of this call are freed on every exit path
-    std::vector<DBuf*> bufs;
-    Packed* packed;
-    ~Release() {
-      for (DBuf* b : bufs) b->release();
-      packed->release();
-    }
-  } guard{{&d_pl, &d_tb, &d_t, &d_q, &d_th, &d_s, &d_gt, &d_gq, &d_gth}, &P};
+  VS_CUDA(h, quiesce(h));
+  Packed& P = h->xpack;
+  DBuf &d_pl = h->xbuf[0], &d_tb = h->xbuf[1], &d_t = h->xbuf[2], &d_q = h->xbuf[3],
+       &d_th = h->xbuf[4], &d_s = h->xbuf[5], &d_gt = h->xbuf[6], &d_gq = h->xbuf[7],
+       &d_gth = h->xbuf[8], &d_rs = h->xbuf[9];
   int rc = pack_library(h, L, nullptr, 0, P);
   if (rc) return rc;
   std::vector<long> tb(static_cast<size_t>(n_poses));
@@ -1509,9 +1533,12 @@ int vs_score_gradient(vs_handle* h, const vs_library* L, int64_t n_poses,
   VS_CUDA(h, d_q.ensure(np * 32));
   VS_CUDA(h, d_th.ensure(nt * 8));
   VS_CUDA(h, d_s.ensure(np * 8));
-  VS_CUDA(h, d_gt.ensure(np * 24));
-  VS_CUDA(h, d_gq.ensure(np * 32));
-  VS_CUDA(h, d_gth.ensure(nt * 8));
+  if (grad) {
+    VS_CUDA(h, d_gt.ensure(np * 24));
+    VS_CUDA(h, d_gq.ensure(np * 32));
+    VS_CUDA(h, d_gth.ensure(nt * 8));
+  }
+  if (resc) VS_CUDA(h, d_rs.ensure(np * 8));
   VS_CUDA(h, cudaMemcpyAsync(d_pl.p, pose_lig, np * 4, cudaMemcpyHostToDevice, st));
   VS_CUDA(h, cudaMemcpyAsync(d_tb.p, tb.data(), np * 8, cudaMemcpyHostToDevice, st));
   VS_CUDA(h, cudaMemcpyAsync(d_t.p, t, np * 24, cudaMemcpyHostToDevice, st));
@@ -1520,16 +1547,22 @@ int vs_score_gradient(vs_handle* h, const vs_library* L, int64_t n_poses,
   VS_CUDA(h, launch_grad(st, P.dev(), h->d_sites64.as<const SiteD>(), h->n_sites64, h->box_lo,
                          h->box_hi, h->r64, h->lam64, n_poses, d_pl.as<const int>(),
                          d_tb.as<const long>(), d_t.as<const double>(), d_q.as<const double>(),
-                         d_th.as<const double>(), nmax, tmax, d_s.as<double>(), d_gt.as<double>(),
-                         d_gq.as<double>(), d_gth.as<double>()));
+                         d_th.as<const double>(), nmax, tmax, d_s.as<double>(),
+                         grad ? d_gt.as<double>() : nullptr, grad ? d_gq.as<double>() : nullptr,
+                         grad ? d_gth.as<double>() : nullptr, resc ? d_rs.as<double>() : nullptr));
   ++h->launches;
   VS_CUDA(h, cudaMemcpyAsync(score, d_s.p, np * 8, cudaMemcpyDeviceToHost, st));
-  VS_CUDA(h, cudaMemcpyAsync(grad_t, d_gt.p, np * 24, cudaMemcpyDeviceToHost, st));
-  VS_CUDA(h, cudaMemcpyAsync(grad_q, d_gq.p, np * 32, cudaMemcpyDeviceToHost, st));
-  if (toff > 0) VS_CUDA(h, cudaMemcpyAsync(grad_tors, d_gth.p, toff * 8, cudaMemcpyDeviceToHost, st));
+  if (grad) {
+    VS_CUDA(h, cudaMemcpyAsync(grad_t, d_gt.p, np * 24, cudaMemcpyDeviceToHost, st));
+    VS_CUDA(h, cudaMemcpyAsync(grad_q, d_gq.p, np * 32, cudaMemcpyDeviceToHost, st));
+    if (toff > 0)
+      VS_CUDA(h, cudaMemcpyAsync(grad_tors, d_gth.p, toff * 8, cudaMemcpyDeviceToHost, st));
+  }
+  if (resc) VS_CUDA(h, cudaMemcpyAsync(resc, d_rs.p, np * 8, cudaMemcpyDeviceToHost, st));
   VS_CUDA(h, cudaStreamSynchronize(st));
   return VS_OK;
 }
+}  // namespace
 
 int vs_ascend(vs_handle* h, const vs_library* L, int64_t n_poses, const int32_t* pose_lig,
               double* t, double* q, double* tors, int32_t max_steps, double* score,
@@ -1539,16 +1572,10 @@ int vs_ascend(vs_handle* h, const vs_library* L, int64_t n_poses, const int32_t*
   if (h->empty_bounds) return fail(h, VS_ERR_EMPTY_BOUNDS, "pocket bounds are empty");
   if (n_poses < 0 || max_steps < 0) return fail(h, VS_ERR_INVALID_ARGUMENT, "negative count");
   if (n_poses == 0) return VS_OK;
-  Packed P;
-  DBuf d_pl, d_tb, d_t, d_q, d_th, d_s, d_st;
-  struct Release {
-    std::vector<DBuf*> bufs;
-    Packed* packed;
-    ~Release() {
-      for (DBuf* b : bufs) b->release();
-      packed->release();
-    }
-  } guard{{&d_pl, &d_tb, &d_t, &d_q, &d_th, &d_s, &d_st}, &P};
+  VS_CUDA(h, quiesce(h));
+  Packed& P = h->xpack;
+  DBuf &d_pl = h->xbuf[0], &d_tb = h->xbuf[1], &d_t = h->xbuf[2], &d_q = h->xbuf[3],
+       &d_th = h->xbuf[4], &d_s = h->xbuf[5], &d_st = h->xbuf[6];
   int rc = pack_library(h, L, nullptr, 0, P);
   if (rc) return rc;
   std::vector<long> tb(static_cast<size_t>(n_poses));
@@ -1592,6 +1619,166 @@ int vs_ascend(vs_handle* h, const vs_library* L, int64_t n_poses, const int32_t*
   if (score) VS_CUDA(h, cudaMemcpyAsync(score, d_s.p, np * 8, cudaMemcpyDeviceToHost, st));
   if (steps) VS_CUDA(h, cudaMemcpyAsync(steps, d_st.p, np * 4, cudaMemcpyDeviceToHost, st));
   VS_CUDA(h, cudaStreamSynchronize(st));
+  return VS_OK;
+}
+
+// ---- dock() with the reference's contract (dock.cpp:318-371): sweep-v1
+// restarts (vs_dock, every kept pose), each refined by the reference ascent
+// on the device (vs_ascend, FP64, max_steps), then the reference's keep rule
+// on the refined coordinates in restart order (RMSD >= delta from every
+// kept pose, dock.cpp:359-361) and a stable sort by score descending
+// (dock.cpp:364-366).  The RMSD bookkeeping (<= restarts poses per ligand)
+// runs on the host in FP64 over apply_pose (dock.cpp:52-67, 392-401).
+namespace {
+// transformed() of one pose (dock.cpp:52-67): torsions in axis order about
+// the current coordinates, then x = R(q / |q|) y + t
+void pose_coords(const vs_library* L, int64_t aoff, int n, int64_t toff, int T, int64_t moff,
+                 const double* t, const double* q, const double* th, std::vector<double>& x) {
+  x.assign(L->coords + 3 * aoff, L->coords + 3 * (aoff + n));
+  auto rot = [](double w, double ux, double uy, double uz, double v[3]) {
+    const double cx = uy * v[2] - uz * v[1], cy = uz * v[0] - ux * v[2], cz = ux * v[1] - uy * v[0];
+    const double ex = uy * cz - uz * cy, ey = uz * cx - ux * cz, ez = ux * cy - uy * cx;
+    v[0] = v[0] + 2.0 * w * cx + 2.0 * ex;
+    v[1] = v[1] + 2.0 * w * cy + 2.0 * ey;
+    v[2] = v[2] + 2.0 * w * cz + 2.0 * ez;
+  };
+  int64_t m = moff;
+  for (int j = 0; j < T; ++j) {
+    const int a = L->axis_a[toff + j], b = L->axis_b[toff + j];
+    const double o[3] = {x[3 * a], x[3 * a + 1], x[3 * a + 2]};
+    double d[3] = {x[3 * b] - o[0], x[3 * b + 1] - o[1], x[3 * b + 2] - o[2]};
+    const double nn = std::sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+    if (nn > 0.0)
+      for (double& c : d) c /= nn;
+    else
+      d[0] = d[1] = d[2] = 0.0;
+    const double hh = 0.5 * th[j], sn = std::sin(hh), cs = std::cos(hh);
+    for (int k = 0; k < L->moving_count[toff + j]; ++k) {
+      const int idx = L->moving[m + k];
+      double v[3] = {x[3 * idx] - o[0], x[3 * idx + 1] - o[1], x[3 * idx + 2] - o[2]};
+      rot(cs, d[0] * sn, d[1] * sn, d[2] * sn, v);
+      for (int c = 0; c < 3; ++c) x[3 * idx + c] = o[c] + v[c];
+    }
+    m += L->moving_count[toff + j];
+  }
+  const double qn = std::sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+  for (int i = 0; i < n; ++i) {
+    double v[3] = {x[3 * i], x[3 * i + 1], x[3 * i + 2]};
+    rot(q[0] / qn, q[1] / qn, q[2] / qn, q[3] / qn, v);
+    for (int c = 0; c < 3; ++c) x[3 * i + c] = v[c] + t[c];
+  }
+}
+
+double rmsd_host(const std::vector<double>& a, const std::vector<double>& b) {
+  const size_t n = a.size() / 3;
+  if (n == 0) return 0.0;
+  double s = 0.0;
+  for (size_t i = 0; i < n; ++i) {
+    const double dx = a[3 * i] - b[3 * i], dy = a[3 * i + 1] - b[3 * i + 1],
+                 dz = a[3 * i + 2] - b[3 * i + 2];
+    s += dx * dx + dy * dy + dz * dz;
+  }
+  return std::sqrt(s / static_cast<double>(n));
+}
+}  // namespace
+
+int vs_dock_refined_host(vs_handle* h, const vs_library* L, const vs_size_class* classes,
+                         int32_t nc, const vs_dock_params* params, int32_t max_steps,
+                         vs_refined* out) {
+  if (max_steps < 0) return fail(h, VS_ERR_INVALID_ARGUMENT, "max_steps must be >= 0");
+  const int n = L->n_ligands, R = params->restarts;
+  if (n < 0) return fail(h, VS_ERR_INVALID_ARGUMENT, "negative ligand count");
+  vs_dock_params prm = *params;
+  prm.write_all_poses = 1;
+  std::vector<int64_t> aoff(n + 1, 0), toff(n + 1, 0), moff(n + 1, 0);
+  for (int i = 0; i < n; ++i) {
+    aoff[i + 1] = aoff[i] + L->n_atoms[i];
+    toff[i + 1] = toff[i] + L->n_tors[i];
+  }
+  for (int i = 0; i < n; ++i) {
+    int64_t m = 0;
+    for (int64_t j = toff[i]; j < toff[i + 1]; ++j) m += L->moving_count[j];
+    moff[i + 1] = moff[i] + m;
+  }
+  const size_t nr = static_cast<size_t>(std::max(n, 1)) * std::max(R, 1);
+  std::vector<int32_t> n_kept(std::max(n, 1));
+  std::vector<vs_pose> all(nr);
+  std::vector<float> all_tors(std::max<int64_t>(toff[n], 1) * std::max(R, 1));
+  vs_results res{};
+  res.n_kept = n_kept.data();
+  res.all = all.data();
+  res.all_tors = all_tors.data();
+  int rc = vs_dock_host(h, L, classes, nc, &prm, &res);
+  if (rc) return rc;
+  // every kept pose of every ligand, in restart order, FP64
+  std::vector<int32_t> pl;
+  std::vector<int> slot;  // rank in the ligand's `all` block
+  std::vector<double> t, q, th;
+  std::vector<int64_t> first(n + 1, 0);
+  for (int i = 0; i < n; ++i) {
+    first[i] = static_cast<int64_t>(pl.size());
+    const int k = std::max(n_kept[i], 0);
+    std::vector<int> ord(k);
+    std::iota(ord.begin(), ord.end(), 0);
+    std::sort(ord.begin(), ord.end(), [&](int a, int b) {
+      return all[static_cast<size_t>(i) * R + a].restart < all[static_cast<size_t>(i) * R + b].restart;
+    });
+    const int T = L->n_tors[i];
+    for (int r : ord) {
+      const vs_pose& p = all[static_cast<size_t>(i) * R + r];
+      pl.push_back(i);
+      slot.push_back(p.restart);
+      for (int c = 0; c < 3; ++c) t.push_back(p.t[c]);
+      for (int c = 0; c < 4; ++c) q.push_back(p.q[c]);
+      const float* tt = all_tors.data() + toff[i] * R + static_cast<int64_t>(r) * T;
+      for (int j = 0; j < T; ++j) th.push_back(tt[j]);
+    }
+  }
+  first[n] = static_cast<int64_t>(pl.size());
+  const int64_t np = static_cast<int64_t>(pl.size());
+  std::vector<double> score(std::max<int64_t>(np, 1));
+  if (th.empty()) th.push_back(0.0);
+  rc = vs_ascend(h, L, np, pl.data(), t.data(), q.data(), th.data(), max_steps, score.data(),
+                 nullptr);
+  if (rc) return rc;
+  // per ligand: the keep rule on the refined coordinates, then the sort
+  std::vector<int64_t> tb(np + 1, 0);
+  for (int64_t p = 0; p < np; ++p) tb[p + 1] = tb[p] + L->n_tors[pl[p]];
+  std::vector<std::vector<double>> kept_x;
+  std::vector<double> x;
+  for (int i = 0; i < n; ++i) {
+    out->n_poses[i] = n_kept[i] < 0 ? -1 : 0;
+    if (n_kept[i] <= 0) continue;
+    const int N = L->n_atoms[i], T = L->n_tors[i];
+    std::vector<int64_t> keep;
+    kept_x.clear();
+    for (int64_t p = first[i]; p < first[i + 1]; ++p) {
+      pose_coords(L, aoff[i], N, toff[i], T, moff[i], &t[3 * p], &q[4 * p], &th[tb[p]], x);
+      bool diverse = true;
+      for (const auto& kx : kept_x)
+        if (rmsd_host(x, kx) < params->diversity_delta) {
+          diverse = false;
+          break;
+        }
+      if (!diverse) continue;
+      keep.push_back(p);
+      kept_x.push_back(x);
+    }
+    std::stable_sort(keep.begin(), keep.end(),
+                     [&](int64_t a, int64_t b) { return score[a] > score[b]; });
+    out->n_poses[i] = static_cast<int32_t>(keep.size());
+    for (size_t r = 0; r < keep.size(); ++r) {
+      const int64_t p = keep[r];
+      const size_t o = static_cast<size_t>(i) * R + r;
+      const double qn = std::sqrt(q[4 * p] * q[4 * p] + q[4 * p + 1] * q[4 * p + 1] +
+                                  q[4 * p + 2] * q[4 * p + 2] + q[4 * p + 3] * q[4 * p + 3]);
+      for (int c = 0; c < 3; ++c) out->t[3 * o + c] = t[3 * p + c];
+      for (int c = 0; c < 4; ++c) out->q[4 * o + c] = q[4 * p + c] / qn;  // pose_of, dock.cpp:210
+      out->score[o] = score[p];
+      if (out->restart) out->restart[o] = slot[p];
+      for (int j = 0; j < T; ++j) out->tors[toff[i] * R + static_cast<int64_t>(r) * T + j] = th[tb[p] + j];
+    }
+  }
   return VS_OK;
 }
 

@@ -474,6 +474,53 @@ class Engine:
                              ptr(score, C.c_double), ptr(steps, C.c_int32)), self._h, "ascend")
         return t[:3 * n].reshape(n, 3), q[:4 * n].reshape(n, 4), tors[:nt], score[:n], steps[:n]
 
+    def score64(self, lib: Library, pose_lig, t, q, tors):
+        """geometric_score and rescore of given poses in FP64 on the device
+        (capi.h vs_score64): (geo[n], resc[n])."""
+        pose_lig = np.ascontiguousarray(pose_lig, np.int32)
+        n = len(pose_lig)
+        t = np.ascontiguousarray(t, np.float64).reshape(-1)
+        q = np.ascontiguousarray(q, np.float64).reshape(-1)
+        tors = np.ascontiguousarray(tors, np.float64).reshape(-1)
+        _check_pose_arrays(lib, pose_lig, t, q, tors)
+        if tors.size == 0:
+            tors = np.zeros(1, np.float64)
+        geo = np.zeros(max(n, 1), np.float64)
+        resc = np.zeros(max(n, 1), np.float64)
+        lc = lib.as_c()
+        check(_lib.vs_score64(self._h, C.byref(lc), n, ptr(pose_lig, C.c_int32), ptr(t, C.c_double),
+                              ptr(q, C.c_double), ptr(tors, C.c_double), ptr(geo, C.c_double),
+                              ptr(resc, C.c_double)), self._h, "score64")
+        return geo[:n], resc[:n]
+
+    def dock_refined(self, lib: Library, params: DockParams, max_steps: int = 500, classes=None):
+        """dock() with the reference contract (capi.h vs_dock_refined_host):
+        sweep-v1 restarts refined by the reference ascent, the keep rule on
+        the refined poses, sorted by score.  Returns per ligand a list of
+        (t[3], q[4], torsions, score, restart) tuples (FP64)."""
+        n, R = len(lib), params.restarts
+        tt = int(np.sum(lib.n_tors))
+        cl, ncl = _classes_c(classes)
+        npos = np.zeros(max(n, 1), np.int32)
+        t = np.zeros(max(n, 1) * R * 3)
+        q = np.zeros(max(n, 1) * R * 4)
+        th = np.zeros(max(tt, 1) * R)
+        sc = np.zeros(max(n, 1) * R)
+        rs = np.zeros(max(n, 1) * R, np.int32)
+        out = _capi.vs_refined(ptr(npos, C.c_int32), ptr(t, C.c_double), ptr(q, C.c_double),
+                               ptr(th, C.c_double), ptr(sc, C.c_double), ptr(rs, C.c_int32))
+        lc, pc = lib.as_c(), params.as_c()
+        check(_lib.vs_dock_refined_host(self._h, C.byref(lc), cl, ncl, C.byref(pc), max_steps,
+                                        C.byref(out)), self._h, "dock_refined")
+        _, to, _ = lib.offsets()
+        res = []
+        for i in range(n):
+            T = int(lib.n_tors[i])
+            res.append([(t[3 * (i * R + r):3 * (i * R + r) + 3], q[4 * (i * R + r):4 * (i * R + r) + 4],
+                         th[to[i] * R + r * T:to[i] * R + (r + 1) * T], float(sc[i * R + r]),
+                         int(rs[i * R + r])) for r in range(max(int(npos[i]), 0))])
+        return res
+
     def rescore(self, lib: Library, pose_lig, t, q, tors):
         """K3a: canonical geometric score and rescore of given poses."""
         pose_lig = np.ascontiguousarray(pose_lig, np.int32)
@@ -567,10 +614,10 @@ def _score(conf, topo, poses, pocket, atom_class, engine=None):
         raise AtomCountMismatch("conformer has no atoms")
     lib = _one_ligand_library(conf, topo, atom_class=atom_class)
     n = len(poses)
-    t = np.array([p.translation for p in poses], np.float32)
-    q = np.array([p.rotation for p in poses], np.float32)
-    tors = np.array([v for p in poses for v in p.torsions], np.float32)
-    return eng.rescore(lib, np.zeros(n, np.int32), t, q, tors)
+    t = np.array([p.translation for p in poses], np.float64)
+    q = np.array([p.rotation for p in poses], np.float64)
+    tors = np.array([v for p in poses for v in p.torsions], np.float64)
+    return eng.score64(lib, np.zeros(n, np.int32), t, q, tors)
 
 
 def geometric_score(conf: Conformer, topo: TorsionTopology, pose: Pose, pocket: Pocket,
@@ -620,9 +667,11 @@ def rescore(ligand: Ligand, conf: Conformer, topo: TorsionTopology, pose: Pose, 
 def dock(conf: Conformer, topo: TorsionTopology, pocket: Pocket, restarts: int,
          diversity_delta: float, seed: int, max_steps: int = 500, params: DockParams | None = None,
          engine: Engine | None = None, atom_class=None) -> list[Pose]:
-    """dock::dock (dock.cpp:318-371) with the sweep-v1 generator: kept poses,
-    pairwise RMSD >= diversity_delta, sorted by geometric score descending.
-    `max_steps` (reference ascent length) has no meaning for sweep-v1."""
+    """dock::dock (dock.cpp:318-371): the sweep-v1 restarts refined by the
+    reference ascent (max_steps, FP64 on the device), the reference's keep
+    rule on the refined poses (pairwise RMSD >= diversity_delta, restart
+    order) and a stable sort by geometric score descending
+    (capi.h vs_dock_refined_host)."""
     if pocket.empty():
         raise EmptyBounds()
     if restarts < 1:
@@ -635,16 +684,14 @@ def dock(conf: Conformer, topo: TorsionTopology, pocket: Pocket, restarts: int,
     prm = DockParams(restarts=restarts, diversity_delta=diversity_delta, rotations=prm.rotations,
                      flex_angles=prm.flex_angles, flex_passes=prm.flex_passes,
                      keep_top=prm.keep_top, min_score=prm.min_score,
-                     rotation_seed=prm.rotation_seed, write_all_poses=True)
+                     rotation_seed=prm.rotation_seed, polish=prm.polish)
     eng = engine or default_engine()
     if eng.pocket is not pocket:
         eng.set_pocket(pocket)
     lib = _one_ligand_library(conf, topo, seed=seed, atom_class=atom_class)
-    res = eng.dock_host(lib, prm)
-    out = res.poses(0, len(topo.axes), which="all", ligand_id=conf.ligand_id)
-    for p in out:
-        p.rescore = None
-    return out
+    (poses,) = eng.dock_refined(lib, prm, max_steps)
+    return [Pose(conf.ligand_id, tuple(float(v) for v in t), tuple(float(v) for v in q),
+                 [float(v) for v in th], sc, None, restart=r) for (t, q, th, sc, r) in poses]
 
 
 def filter_poses(poses: Sequence[Pose], keep_top: int, min_score: float) -> list[Pose]:

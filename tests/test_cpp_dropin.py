@@ -1,7 +1,8 @@
-"""The header-only C++ drop-in (include/vscreen_gpu/vscreen_gpu.hpp) compiles
-against the C-ABI, links libvscreen_gpu.so and runs: host functions on the
-CPU; the GPU entry points report DeviceError without a device and return the
-reference's known answer (test_dock.cpp:45-47) with one."""
+"""A reference-style C++ caller (tests/cpp/dropin_example.cpp: the
+reference's own API from include/vscreen/ plus the library-scale C-ABI)
+compiles, links libvscreen_core.so and runs: host functions on the CPU; the
+GPU entry points fail loudly without a device and return the reference's
+known answers (test_dock.cpp:45-47, 172-184) with one."""
 import os
 import subprocess
 
@@ -13,9 +14,10 @@ from conftest import ROOT, gpu_available
 def _build(tmp_path):
     exe = tmp_path / "dropin"
     libdir = os.path.join(ROOT, "paper_2304_09953_b200")
-    subprocess.run(["/usr/bin/g++", "-std=c++17", "-O1", f"-I{ROOT}/include",
+    subprocess.run(["/usr/bin/g++", "-std=c++20", "-O1", f"-I{ROOT}/include",
                     os.path.join(ROOT, "tests", "cpp", "dropin_example.cpp"), f"-L{libdir}",
-                    "-lvscreen_gpu", f"-Wl,-rpath,{libdir}", "-o", str(exe)], check=True)
+                    "-lvscreen_core", "-lvscreen_gpu", f"-Wl,-rpath,{libdir}", "-o", str(exe)],
+                   check=True)
     return str(exe)
 
 
@@ -30,4 +32,4 @@ def test_cpp_dropin_builds_and_runs(tmp_path):
 def test_cpp_dropin_on_gpu(tmp_path):
     out = subprocess.run([_build(tmp_path)], capture_output=True, text=True)
     assert out.returncode == 0, out.stdout + out.stderr
-    assert "gpu ok" in out.stdout
+    assert "gpu ok" in out.stdout and "batch ok" in out.stdout

@@ -1,0 +1,56 @@
+"""The reference's own unit tests of the dock and batcher API
+(proj/tests/test_dock.cpp, test_batcher.cpp — unmodified), compiled against
+the drop-in headers (include/vscreen/) with a doctest shim
+(tests/cpp/doctest.h) and linked to libvscreen_core.so instead of the CPU
+library (oracle/build_ref_tests.sh, run by __graft_entry__.build()).
+
+CPU: test_batcher passes whole; test_dock's host-side cases (filter_poses,
+rmsd, torsion topology / apply_pose) pass and every GPU entry point fails
+loudly (no CPU fallback).  GPU: all 13 test_dock cases pass."""
+import os
+import re
+import subprocess
+
+import pytest
+
+from conftest import ROOT, gpu_available
+
+BIN = os.path.join(ROOT, "oracle", "_ref")
+
+
+def _run(name):
+    exe = os.path.join(BIN, f"ref_{name}")
+    if not os.path.exists(exe):
+        if os.path.isdir("/root/reference/proj/tests"):
+            subprocess.run(["bash", os.path.join(ROOT, "oracle", "build_ref_tests.sh")], check=True)
+        else:
+            pytest.skip(f"{exe} not built (needs /root/reference at build time)")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    res = {name: verdict for verdict, name in re.findall(r"^\[(PASS|FAIL)\] (.+)$", out.stdout, re.M)}
+    return out, res
+
+
+def test_reference_batcher_tests_pass():
+    out, res = _run("test_batcher")
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert len(res) == 6 and all(v == "PASS" for v in res.values()), out.stdout
+
+
+def test_reference_dock_tests_host_cases_on_cpu():
+    if gpu_available():
+        pytest.skip("GPU present: the full run is test_reference_dock_tests_all_pass")
+    out, res = _run("test_dock")
+    assert len(res) == 13, out.stdout
+    for name in ("filter_poses ordering and edge cases", "rmsd formula",
+                 "torsion topology and pose application"):
+        assert res[name] == "PASS", out.stdout
+    # the GPU entry points refuse to run without a device instead of falling back
+    assert "no CPU fallback" in out.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")
+def test_reference_dock_tests_all_pass():
+    out, res = _run("test_dock")
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert len(res) == 13 and all(v == "PASS" for v in res.values()), out.stdout

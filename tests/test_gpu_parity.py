@@ -328,10 +328,32 @@ def test_dock_smiles_single_site(V):
     poses = V.dock_smiles("C", json.dumps(pocket), restarts=2, seed=3)
     assert poses
     best = poses[0]
-    # the sweep has no continuous refinement: the best of 2 random starts
-    # is reported, sorted by score
+    # the reference's own assertions, unmodified: dock() refines the sweep
+    # with the reference ascent (vs_dock_refined_host)
+    import math
+    assert math.dist(best["translation"], [1.0, 0.5, -0.5]) < 1e-3
+    assert best["geometric_score"] == pytest.approx(1.0, abs=1e-6)
     assert best["geometric_score"] >= poses[-1]["geometric_score"]
     assert set(best) == {"ligand", "translation", "rotation", "torsions", "geometric_score", "rescore"}
+
+
+def test_dock_contract_diversity_after_refinement(V, engine, pocket_json):
+    """dock() keeps the reference contract after the ascent: pairwise RMSD
+    of the returned poses >= delta (dock.cpp:359-361), sorted by score, the
+    score equal to the FP64 reference geometric_score of the returned pose,
+    deterministic reruns."""
+    pocket = V.parse_pocket_json(pocket_json)
+    for smi, seed in (("CCCO", 5), ("c1ccccc1CCN", 11)):
+        lig = V.make_ligand("x", smi, embed_seed=seed)
+        a = V.dock(lig.conformer, lig.topology, pocket, 6, 1.5, seed, engine=engine)
+        b = V.dock(lig.conformer, lig.topology, pocket, 6, 1.5, seed, engine=engine)
+        assert [p.geometric_score for p in a] == [p.geometric_score for p in b]
+        assert all(x.geometric_score >= y.geometric_score for x, y in zip(a, a[1:]))
+        for i in range(len(a)):
+            for j in range(i + 1, len(a)):
+                assert V.pose_rmsd(lig.conformer, lig.topology, a[i], a[j]) >= 1.5
+            g = V.geometric_score(lig.conformer, lig.topology, a[i], pocket, engine=engine)
+            assert abs(g - a[i].geometric_score) <= 1e-9 * max(1.0, abs(g))
 
 
 def test_rescore_batched_buckets_and_error_paths(V, engine, lib200, pocket_json):
