@@ -26,6 +26,12 @@ namespace vs {
 size_t rescore_smem_per_block(int nmax, int tmax, int mvmax);
 size_t stage_smem_per_block(int nmax, int tmax, int mvmax);
 constexpr int kStats = 10;  // work counters (capi.h vs_last_stats_ex)
+// vs_dock_host pipelines libraries of at least kPipeMinLigands ligands in
+// contiguous chunks cut at these fractions of the library
+constexpr int kPipeMinLigands = 32768;
+// (four equal chunks, two in flight: measured best of the shapes tried,
+// tools/pipe_ab.sh; profiles/e2e_pipeline_r2.txt)
+constexpr double kPipeSplit[] = {0.25, 0.5, 0.75};
 
 cudaError_t launch_draws(cudaStream_t st, const PocketDev& pk, const unsigned long long* seeds,
                          const int* n_tors, int n, int restarts, int attempts, float* out,
@@ -146,9 +152,10 @@ struct Packed {
   PinnedVec<double4> atoms;
   PinnedVec<int4> axes;
   PinnedVec<uint8_t> moving;
-  std::vector<unsigned long long> seeds;
-  std::vector<unsigned int> id_rank;
+  PinnedVec<unsigned long long> seeds;
+  PinnedVec<unsigned int> id_rank;
   std::vector<int> order;
+  PinnedVec<int> order_pin;  // pinned copy of `order` (async H2D from a pipelined pack)
   std::vector<int> cls;          // class per ligand (-1 dropped)
   std::vector<long> tors_off;    // prefix sum of n_tors
   std::vector<Bucket> buckets;
@@ -174,6 +181,46 @@ struct Packed {
 
 }  // namespace
 
+// per-ligand state of one staged dock (StageBufs) + its launch counters
+struct StageSet {
+  DBuf ys, ysf, th, pose, bk, nk, kx, kp, km, st, counters;
+  cudaError_t ensure(size_t na, size_t nt, size_t nn, size_t R) {
+    cudaError_t e = cudaSuccess;
+    auto en = [&](DBuf& d, size_t bytes) {
+      if (e == cudaSuccess) e = d.ensure(bytes);
+    };
+    en(ys, na * sizeof(double4));
+    en(ysf, na * sizeof(float4));
+    en(th, nt * sizeof(float));
+    en(pose, nn * 2 * sizeof(float4));
+    en(bk, nn * sizeof(int));
+    en(nk, nn * sizeof(int));
+    en(kx, na * R * sizeof(float4));
+    en(kp, (nn * 8 + nt) * R * sizeof(float));
+    en(km, nn * R * 4 * sizeof(int));
+    en(st, nn * 8 * sizeof(unsigned long long));
+    en(counters, 320 * sizeof(int));
+    return e;
+  }
+  StageBufs bufs() const {
+    StageBufs sb;
+    sb.ys = ys.as<double4>();
+    sb.ysf = ysf.as<float4>();
+    sb.th = th.as<float>();
+    sb.pose = pose.as<float4>();
+    sb.bk = bk.as<int>();
+    sb.nk = nk.as<int>();
+    sb.kx = kx.as<float4>();
+    sb.kp = kp.as<float>();
+    sb.km = km.as<int>();
+    sb.st = st.as<unsigned long long>();
+    return sb;
+  }
+  void release() {
+    for (DBuf* b : {&ys, &ysf, &th, &pose, &bk, &nk, &kx, &kp, &km, &st, &counters}) b->release();
+  }
+};
+
 struct vs_handle {
   int device = 0;
   cudaStream_t own = nullptr;
@@ -197,9 +244,23 @@ struct vs_handle {
   Packed lib;
   vs_dock_params last_prm{};
   bool has_results = false;
-  DBuf d_surv, d_surv_tors, d_all, d_all_tors, d_best, d_nkept, d_nsurv, d_keys, d_counters;
+  DBuf d_surv, d_surv_tors, d_all, d_all_tors, d_best, d_nkept, d_nsurv, d_keys;
   DBuf d_rots, d_topk_a, d_topk_b, d_stats;
-  DBuf d_sg_ys, d_sg_ysf, d_sg_th, d_sg_pose, d_sg_bk, d_sg_nk, d_sg_kx, d_sg_kp, d_sg_km, d_sg_st;
+  StageSet sg;  // staged-dock state of vs_dock
+  // what the last results cover: ligand count, class per ligand (-1 =
+  // dropped), total torsions (vs_fetch_results, vs_topk)
+  int res_n = 0;
+  std::vector<int> res_cls;
+  long res_tors = 0;
+  // the pipelined vs_dock_host (dock_host_pipelined): two library slots and
+  // stage sets, a compute stream per slot, H2D and D2H streams, pinned
+  // result staging per slot
+  Packed pipe_lib[2];
+  StageSet pipe_sg[2];
+  cudaStream_t pipe_s[2] = {nullptr, nullptr};
+  cudaStream_t pipe_in = nullptr, pipe_out = nullptr;
+  PinnedVec<uint8_t> pipe_stage[2];
+  std::vector<cudaEvent_t> pipe_ev;
   int rots_k = -1;
   uint64_t rots_seed = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -298,8 +359,8 @@ int pack_library(vs_handle* h, const vs_library* L, const vs_size_class* classes
   const int n = L->n_ligands;
   if (n < 0) return fail(h, VS_ERR_INVALID_ARGUMENT, "negative ligand count");
   P.n = n;
-  P.seeds.assign(n, 0ull);
-  P.id_rank.assign(n, 0u);
+  if (!P.seeds.resize(std::max(n, 1)) || !P.id_rank.resize(std::max(n, 1)))
+    return fail(h, VS_ERR_CUDA, "pinned host allocation failed");
   P.cls.assign(n, -1);
   P.tors_off.assign(n + 1, 0);
   const auto pt0 = std::chrono::steady_clock::now();
@@ -462,6 +523,9 @@ int pack_library(vs_handle* h, const vs_library* L, const vs_size_class* classes
   }
   P.all.count = static_cast<int>(lpt.size());
   if (P.order.empty()) P.order.push_back(0);
+  if (!P.order_pin.resize(P.order.size()))
+    return fail(h, VS_ERR_CUDA, "pinned host allocation failed");
+  std::memcpy(P.order_pin.data(), P.order.data(), P.order.size() * sizeof(int));
   if (const char* e = std::getenv("VSCREEN_UPLOAD_TIMING"); e && e[0] == '1') {
     const auto pt4 = std::chrono::steady_clock::now();
     auto ms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
@@ -546,7 +610,7 @@ int upload_packed(vs_handle* h, Packed& P, cudaStream_t st, int parts) {
   if (!(parts & 2)) return VS_OK;
   VS_CUDA(h, up(P.d_seeds, P.seeds.data(), std::max<size_t>(8, P.seeds.size() * 8)));
   VS_CUDA(h, up(P.d_idr, P.id_rank.data(), std::max<size_t>(4, P.id_rank.size() * 4)));
-  VS_CUDA(h, up(P.d_order, P.order.data(), P.order.size() * sizeof(int)));
+  VS_CUDA(h, up(P.d_order, P.order_pin.data(), P.order_pin.size() * sizeof(int)));
   return VS_OK;
 }
 
@@ -703,10 +767,17 @@ void vs_destroy(vs_handle* h) {
   for (DBuf& b : h->xbuf) b.release();
   for (DBuf& b : h->rbuf) b.release();
   for (DBuf* b : {&h->d_sites, &h->d_softtab, &h->d_sites64, &h->d_maps, &h->d_surv, &h->d_surv_tors, &h->d_all, &h->d_all_tors,
-                  &h->d_best, &h->d_nkept, &h->d_nsurv, &h->d_keys, &h->d_counters, &h->d_rots, &h->d_topk_a, &h->d_topk_b, &h->d_stats,
-                  &h->d_sg_ys, &h->d_sg_ysf, &h->d_sg_th, &h->d_sg_pose, &h->d_sg_bk, &h->d_sg_nk,
-                  &h->d_sg_kx, &h->d_sg_kp, &h->d_sg_km, &h->d_sg_st})
+                  &h->d_best, &h->d_nkept, &h->d_nsurv, &h->d_keys, &h->d_rots, &h->d_topk_a, &h->d_topk_b, &h->d_stats})
     b->release();
+  h->sg.release();
+  for (int k = 0; k < 2; ++k) {
+    h->pipe_sg[k].release();
+    h->pipe_lib[k].release();
+    if (h->pipe_s[k]) cudaStreamDestroy(h->pipe_s[k]);
+  }
+  if (h->pipe_in) cudaStreamDestroy(h->pipe_in);
+  if (h->pipe_out) cudaStreamDestroy(h->pipe_out);
+  for (cudaEvent_t e : h->pipe_ev) cudaEventDestroy(e);
   cudaEventDestroy(h->ev0);
   cudaEventDestroy(h->ev1);
   cudaEventDestroy(h->done);
@@ -895,6 +966,129 @@ int vs_upload_library(vs_handle* h, const vs_library* L, const vs_size_class* cl
   return VS_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// the rotation set and the sweep's lane order, uploaded when they change
+int ensure_rots(vs_handle* h, const vs_dock_params* prm, cudaStream_t st) {
+  if (h->rots_k == prm->rotations && h->rots_seed == prm->rotation_seed) return VS_OK;
+  // the K rotations in index order, the same in the sweep's lane order,
+  // then the lane order itself
+  const auto rs = rotation_set(prm->rotations, prm->rotation_seed);
+  const auto perm = rotation_order(rs);
+  std::vector<float4> rp(rs.size());
+  for (size_t p = 0; p < rs.size(); ++p) rp[p] = rs[static_cast<size_t>(perm[p])];
+  const size_t rb = rs.size() * sizeof(float4);
+  std::vector<unsigned char> blob(2 * rb + perm.size() * sizeof(int));
+  std::memcpy(blob.data(), rs.data(), rb);
+  std::memcpy(blob.data() + rb, rp.data(), rb);
+  std::memcpy(blob.data() + 2 * rb, perm.data(), perm.size() * sizeof(int));
+  VS_CUDA(h, h->d_rots.ensure(blob.size()));
+  VS_CUDA(h, cudaMemcpyAsync(h->d_rots.p, blob.data(), blob.size(), cudaMemcpyHostToDevice, st));
+  VS_CUDA(h, cudaStreamSynchronize(st));
+  h->rots_k = prm->rotations;
+  h->rots_seed = prm->rotation_seed;
+  return VS_OK;
+}
+
+// result arrays for n ligands / tt torsions, cleared on `st`: unused
+// survivor / kept slots read as zeros (not a previous run's poses), keys ~0
+int prepare_results(vs_handle* h, int n, long tt, const vs_dock_params* prm, cudaStream_t st) {
+  const size_t nn = static_cast<size_t>(std::max(n, 1));
+  const size_t R = static_cast<size_t>(prm->restarts), KT = static_cast<size_t>(std::max(prm->keep_top, 1));
+  const size_t nt = static_cast<size_t>(std::max<long>(1, tt));
+  VS_CUDA(h, h->d_surv.ensure(nn * KT * sizeof(PoseOut)));
+  VS_CUDA(h, h->d_surv_tors.ensure(nt * KT * 4));
+  if (prm->write_all_poses) {
+    VS_CUDA(h, h->d_all.ensure(nn * R * sizeof(PoseOut)));
+    VS_CUDA(h, h->d_all_tors.ensure(nt * R * 4));
+  }
+  VS_CUDA(h, h->d_best.ensure(nn * 4));
+  VS_CUDA(h, h->d_nkept.ensure(nn * 4));
+  VS_CUDA(h, h->d_nsurv.ensure(nn * 4));
+  VS_CUDA(h, h->d_keys.ensure(nn * 8));
+  VS_CUDA(h, h->d_stats.ensure(kStats * sizeof(unsigned long long)));
+  VS_CUDA(h, cudaMemsetAsync(h->d_stats.p, 0, kStats * sizeof(unsigned long long), st));
+  VS_CUDA(h, cudaMemsetAsync(h->d_keys.p, 0xff, nn * 8, st));
+  VS_CUDA(h, cudaMemsetAsync(h->d_surv.p, 0, nn * KT * sizeof(PoseOut), st));
+  VS_CUDA(h, cudaMemsetAsync(h->d_surv_tors.p, 0, nt * KT * 4, st));
+  if (prm->write_all_poses) {
+    VS_CUDA(h, cudaMemsetAsync(h->d_all.p, 0, nn * R * sizeof(PoseOut), st));
+    VS_CUDA(h, cudaMemsetAsync(h->d_all_tors.p, 0, nt * R * 4, st));
+  }
+  VS_CUDA(h, cudaMemsetAsync(h->d_nkept.p, 0, nn * 4, st));
+  VS_CUDA(h, cudaMemsetAsync(h->d_nsurv.p, 0, nn * 4, st));
+  return VS_OK;
+}
+
+// the result arrays seen from ligand b (torsion offset tb) on: a chunk of a
+// pipelined dock writes its own disjoint slice
+DockOut results_view(vs_handle* h, const vs_dock_params* prm, long b, long tb) {
+  const long R = prm->restarts, KT = prm->keep_top;
+  DockOut out;
+  out.surv = h->d_surv.as<PoseOut>() + b * KT;
+  out.surv_tors = h->d_surv_tors.as<float>() + tb * KT;
+  out.all = prm->write_all_poses ? h->d_all.as<PoseOut>() + b * R : nullptr;
+  out.all_tors = prm->write_all_poses ? h->d_all_tors.as<float>() + tb * R : nullptr;
+  out.best = h->d_best.as<float>() + b;
+  out.n_kept = h->d_nkept.as<int>() + b;
+  out.n_surv = h->d_nsurv.as<int>() + b;
+  out.keys = h->d_keys.as<unsigned long long>() + b;
+  out.stats = h->d_stats.as<unsigned long long>();
+  return out;
+}
+
+// one launch per phase and restart over P's global LPT queue (every size
+// bucket), shared memory sized for its largest ligand, the per-ligand state
+// in `sg`; per-launch event pairs when `phases`
+int launch_packed(vs_handle* h, const Packed& P, const vs_dock_params* prm, cudaStream_t st,
+                  StageSet& sg, const DockOut& out, bool phases) {
+  const Bucket& b = P.all;
+  if (b.count == 0) return VS_OK;
+  const size_t smem = stage_smem_per_block(b.nmax, b.tmax, b.mvmax);
+  if (smem > 227 * 1024) return fail(h, VS_ERR_CAPACITY, "ligands need too much shared memory");
+  const int R = prm->restarts;
+  VS_CUDA(h, sg.ensure(std::max<size_t>(1, P.atoms.size()),
+                       static_cast<size_t>(std::max<long>(1, P.total_tors)),
+                       static_cast<size_t>(std::max(P.n, 1)), static_cast<size_t>(R)));
+  VS_CUDA(h, cudaMemsetAsync(sg.counters.p, 0, 320 * sizeof(int), st));
+  DockParams dp;
+  dp.R = R;
+  dp.K = prm->rotations;
+  dp.A = prm->flex_angles;
+  dp.F = prm->flex_passes;
+  dp.keep_top = prm->keep_top;
+  dp.write_all = prm->write_all_poses ? 1 : 0;
+  dp.delta = static_cast<float>(prm->diversity_delta);
+  dp.min_score = prm->min_score;
+  dp.polish = prm->polish;
+  cudaEvent_t* evs = nullptr;
+  int* kinds = nullptr;
+  if (phases) {
+    const size_t npairs = 4 * static_cast<size_t>(R) + 1;  // start, sweep, flex, polish; finish
+    while (h->pev.size() < 2 * npairs) {
+      cudaEvent_t e;
+      VS_CUDA(h, cudaEventCreate(&e));
+      h->pev.push_back(e);
+    }
+    h->pkind.assign(npairs, -1);  // -1: no launch recorded in this slot
+    evs = h->pev.data();
+    kinds = h->pkind.data();
+  }
+  const float4* rots = h->d_rots.as<const float4>();
+  const float4* rots_p = rots + prm->rotations;
+  const int* perm = reinterpret_cast<const int*>(rots_p + prm->rotations);
+  VS_CUDA(h, launch_staged(h->pk.grid_mode != 0, h->sms, st, P.dev(), h->pk, rots, rots_p, perm,
+                           dp, P.d_order.as<int>() + b.start, b.count, sg.counters.as<int>(),
+                           b.nmax, b.tmax, b.mvmax, sg.bufs(), out, &h->launches, evs, kinds));
+  return VS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 int vs_dock(vs_handle* h, const vs_dock_params* prm, void* stream) {
   cudaSetDevice(h->device);
   if (!h->has_pocket) return fail(h, VS_ERR_STATE, "no pocket");
@@ -904,129 +1098,23 @@ int vs_dock(vs_handle* h, const vs_dock_params* prm, void* stream) {
   if (rc) return rc;
   cudaStream_t st = pick(h, stream);
   VS_CUDA(h, after_prev(h, st));
-  Packed& P = h->lib;
-  const int n = P.n;
-  const int R = prm->restarts, KT = prm->keep_top;
-  if (h->rots_k != prm->rotations || h->rots_seed != prm->rotation_seed) {
-    // the K rotations in index order, the same in the sweep's lane order,
-    // then the lane order itself
-    const auto rs = rotation_set(prm->rotations, prm->rotation_seed);
-    const auto perm = rotation_order(rs);
-    std::vector<float4> rp(rs.size());
-    for (size_t p = 0; p < rs.size(); ++p) rp[p] = rs[static_cast<size_t>(perm[p])];
-    const size_t rb = rs.size() * sizeof(float4);
-    std::vector<unsigned char> blob(2 * rb + perm.size() * sizeof(int));
-    std::memcpy(blob.data(), rs.data(), rb);
-    std::memcpy(blob.data() + rb, rp.data(), rb);
-    std::memcpy(blob.data() + 2 * rb, perm.data(), perm.size() * sizeof(int));
-    VS_CUDA(h, h->d_rots.ensure(blob.size()));
-    VS_CUDA(h, cudaMemcpyAsync(h->d_rots.p, blob.data(), blob.size(), cudaMemcpyHostToDevice, st));
-    VS_CUDA(h, cudaStreamSynchronize(st));
-    h->rots_k = prm->rotations;
-    h->rots_seed = prm->rotation_seed;
-  }
-  const size_t nn = static_cast<size_t>(std::max(n, 1));
-  VS_CUDA(h, h->d_surv.ensure(nn * std::max(KT, 1) * sizeof(PoseOut)));
-  VS_CUDA(h, h->d_surv_tors.ensure(std::max<size_t>(1, P.total_tors) * std::max(KT, 1) * 4));
-  if (prm->write_all_poses) {
-    VS_CUDA(h, h->d_all.ensure(nn * R * sizeof(PoseOut)));
-    VS_CUDA(h, h->d_all_tors.ensure(std::max<size_t>(1, P.total_tors) * R * 4));
-  }
-  VS_CUDA(h, h->d_best.ensure(nn * 4));
-  VS_CUDA(h, h->d_nkept.ensure(nn * 4));
-  VS_CUDA(h, h->d_nsurv.ensure(nn * 4));
-  VS_CUDA(h, h->d_keys.ensure(nn * 8));
-  VS_CUDA(h, h->d_counters.ensure(320 * sizeof(int)));
-  VS_CUDA(h, h->d_stats.ensure(kStats * sizeof(unsigned long long)));
-  VS_CUDA(h, cudaMemsetAsync(h->d_stats.p, 0, kStats * sizeof(unsigned long long), st));
-  VS_CUDA(h, cudaMemsetAsync(h->d_keys.p, 0xff, nn * 8, st));
-  // unused survivor / kept slots read as zeros (not a previous run's poses)
-  VS_CUDA(h, cudaMemsetAsync(h->d_surv.p, 0, nn * std::max(KT, 1) * sizeof(PoseOut), st));
-  VS_CUDA(h, cudaMemsetAsync(h->d_surv_tors.p, 0,
-                             std::max<size_t>(1, P.total_tors) * std::max(KT, 1) * 4, st));
-  if (prm->write_all_poses) {
-    VS_CUDA(h, cudaMemsetAsync(h->d_all.p, 0, nn * R * sizeof(PoseOut), st));
-    VS_CUDA(h, cudaMemsetAsync(h->d_all_tors.p, 0, std::max<size_t>(1, P.total_tors) * R * 4, st));
-  }
-  VS_CUDA(h, cudaMemsetAsync(h->d_nkept.p, 0, nn * 4, st));
-  VS_CUDA(h, cudaMemsetAsync(h->d_nsurv.p, 0, nn * 4, st));
-  VS_CUDA(h, cudaMemsetAsync(h->d_counters.p, 0, 320 * sizeof(int), st));
-
-  DockParams dp;
-  dp.R = R;
-  dp.K = prm->rotations;
-  dp.A = prm->flex_angles;
-  dp.F = prm->flex_passes;
-  dp.keep_top = KT;
-  dp.write_all = prm->write_all_poses ? 1 : 0;
-  dp.delta = static_cast<float>(prm->diversity_delta);
-  dp.min_score = prm->min_score;
-  dp.polish = prm->polish;
-  DockOut out;
-  out.surv = h->d_surv.as<PoseOut>();
-  out.surv_tors = h->d_surv_tors.as<float>();
-  out.all = prm->write_all_poses ? h->d_all.as<PoseOut>() : nullptr;
-  out.all_tors = prm->write_all_poses ? h->d_all_tors.as<float>() : nullptr;
-  out.best = h->d_best.as<float>();
-  out.n_kept = h->d_nkept.as<int>();
-  out.n_surv = h->d_nsurv.as<int>();
-  out.keys = h->d_keys.as<unsigned long long>();
-  out.stats = h->d_stats.as<unsigned long long>();
-
-  const bool grid = h->pk.grid_mode != 0;
-  const LibDev ld = P.dev();
-  // one launch per phase and restart over the global LPT queue (every size
-  // bucket), shared memory sized for the largest ligand, the per-ligand
-  // state handed over in HBM
-  const Bucket& b = P.all;
+  const Packed& P = h->lib;
+  rc = ensure_rots(h, prm, st);
+  if (rc) return rc;
+  rc = prepare_results(h, P.n, P.total_tors, prm, st);
+  if (rc) return rc;
   VS_CUDA(h, cudaEventRecord(h->ev0, st));
-  if (b.count > 0) {
-    const size_t smem = stage_smem_per_block(b.nmax, b.tmax, b.mvmax);
-    if (smem > 227 * 1024) return fail(h, VS_ERR_CAPACITY, "ligands need too much shared memory");
-    const size_t na = std::max<size_t>(1, P.atoms.size());
-    const size_t nt = static_cast<size_t>(std::max<long>(1, P.total_tors));
-    VS_CUDA(h, h->d_sg_ys.ensure(na * sizeof(double4)));
-    VS_CUDA(h, h->d_sg_ysf.ensure(na * sizeof(float4)));
-    VS_CUDA(h, h->d_sg_th.ensure(nt * sizeof(float)));
-    VS_CUDA(h, h->d_sg_pose.ensure(nn * 2 * sizeof(float4)));
-    VS_CUDA(h, h->d_sg_bk.ensure(nn * sizeof(int)));
-    VS_CUDA(h, h->d_sg_nk.ensure(nn * sizeof(int)));
-    VS_CUDA(h, h->d_sg_kx.ensure(na * R * sizeof(float4)));
-    VS_CUDA(h, h->d_sg_kp.ensure((nn * 8 + nt) * R * sizeof(float)));
-    VS_CUDA(h, h->d_sg_km.ensure(nn * R * 4 * sizeof(int)));
-    VS_CUDA(h, h->d_sg_st.ensure(nn * 8 * sizeof(unsigned long long)));
-    StageBufs sb;
-    sb.ys = h->d_sg_ys.as<double4>();
-    sb.ysf = h->d_sg_ysf.as<float4>();
-    sb.th = h->d_sg_th.as<float>();
-    sb.pose = h->d_sg_pose.as<float4>();
-    sb.bk = h->d_sg_bk.as<int>();
-    sb.nk = h->d_sg_nk.as<int>();
-    sb.kx = h->d_sg_kx.as<float4>();
-    sb.kp = h->d_sg_kp.as<float>();
-    sb.km = h->d_sg_km.as<int>();
-    sb.st = h->d_sg_st.as<unsigned long long>();
-    const size_t npairs = 4 * static_cast<size_t>(R) + 1;  // start, sweep, flex, polish; finish
-    while (h->pev.size() < 2 * npairs) {
-      cudaEvent_t e;
-      VS_CUDA(h, cudaEventCreate(&e));
-      h->pev.push_back(e);
-    }
-    h->pkind.assign(npairs, -1);  // -1: no launch recorded in this slot
-    const float4* rots = h->d_rots.as<const float4>();
-    const float4* rots_p = rots + prm->rotations;
-    const int* perm = reinterpret_cast<const int*>(rots_p + prm->rotations);
-    VS_CUDA(h, launch_staged(grid, h->sms, st, ld, h->pk, rots, rots_p, perm, dp,
-                             P.d_order.as<int>() + b.start, b.count, h->d_counters.as<int>(),
-                             b.nmax, b.tmax, b.mvmax, sb, out, &h->launches, h->pev.data(),
-                             h->pkind.data()));
-    h->staged_run = true;
-  }
+  rc = launch_packed(h, P, prm, st, h->sg, results_view(h, prm, 0, 0), true);
+  if (rc) return rc;
+  h->staged_run = true;
   VS_CUDA(h, cudaEventRecord(h->ev1, st));
   VS_CUDA(h, mark_done(h, st));
   h->timed = true;
   h->last_prm = *prm;
   h->has_results = true;
+  h->res_n = P.n;
+  h->res_cls = P.cls;
+  h->res_tors = P.total_tors;
   return VS_OK;
 }
 
@@ -1122,55 +1210,68 @@ int vs_measure_gather_peak_ex(vs_handle* h, int32_t bytes_per_load, double* load
   return VS_OK;
 }
 
-// D2H of every requested result array into one pinned staging buffer (one
-// DMA each at full link rate), then a threaded copy into the caller's
-// (pageable) buffers, which also spreads their first-touch page faults.
-int vs_fetch_results(vs_handle* h, vs_results* o) {
-  cudaSetDevice(h->device);
-  if (!h->has_results) return fail(h, VS_ERR_STATE, "no results");
-  cudaStream_t st = h->last;
-  const Packed& P = h->lib;
-  const size_t n = static_cast<size_t>(P.n);
+}  // extern "C"
+
+namespace {
+
+// one result array slice: device source, caller destination, offset in the
+// pinned staging buffer
+struct FetchPart {
+  void* dst;
+  const void* src;
+  size_t bytes;
+  size_t off;
+};
+
+// the requested result arrays of ligands [b, b + n) (torsions [tb, tb + tt))
+std::vector<FetchPart> fetch_parts(vs_handle* h, const vs_results* o, size_t b, size_t n,
+                                   size_t tb, size_t tt, size_t* total) {
   const size_t KT = static_cast<size_t>(h->last_prm.keep_top);
   const size_t R = static_cast<size_t>(h->last_prm.restarts);
-  const size_t TT = static_cast<size_t>(P.total_tors);
   const bool all = h->last_prm.write_all_poses != 0;
-  struct Part {
-    void* dst;
-    const void* src;
-    size_t bytes;
-    size_t off;
-  };
-  std::vector<Part> parts;
-  size_t total = 0;
-  auto add = [&](void* dst, const DBuf& src, size_t bytes) {
+  std::vector<FetchPart> parts;
+  *total = 0;
+  auto add = [&](void* dst, const DBuf& src, size_t src_off, size_t bytes) {
     if (!dst || bytes == 0) return;
-    parts.push_back(Part{dst, src.p, bytes, total});
-    total += (bytes + 255) & ~size_t(255);
+    parts.push_back(FetchPart{static_cast<uint8_t*>(dst) + src_off,
+                              static_cast<const uint8_t*>(src.p) + src_off, bytes, *total});
+    *total += (bytes + 255) & ~size_t(255);
   };
-  add(o->best, h->d_best, n * 4);
-  add(o->n_kept, h->d_nkept, n * 4);
-  add(o->n_surv, h->d_nsurv, n * 4);
-  if (KT > 0) add(o->surv, h->d_surv, n * KT * sizeof(vs_pose));
-  if (KT > 0) add(o->surv_tors, h->d_surv_tors, TT * KT * 4);
-  if (all) add(o->all, h->d_all, n * R * sizeof(vs_pose));
-  if (all) add(o->all_tors, h->d_all_tors, TT * R * 4);
-  add(o->keys, h->d_keys, n * 8);
-  if (!h->fetch_stage.resize(std::max<size_t>(total, 256)))
+  add(o->best, h->d_best, b * 4, n * 4);
+  add(o->n_kept, h->d_nkept, b * 4, n * 4);
+  add(o->n_surv, h->d_nsurv, b * 4, n * 4);
+  if (KT > 0) add(o->surv, h->d_surv, b * KT * sizeof(vs_pose), n * KT * sizeof(vs_pose));
+  if (KT > 0) add(o->surv_tors, h->d_surv_tors, tb * KT * 4, tt * KT * 4);
+  if (all) add(o->all, h->d_all, b * R * sizeof(vs_pose), n * R * sizeof(vs_pose));
+  if (all) add(o->all_tors, h->d_all_tors, tb * R * 4, tt * R * 4);
+  add(o->keys, h->d_keys, b * 8, n * 8);
+  return parts;
+}
+
+// D2H of the parts into one pinned staging buffer (one DMA each at full
+// link rate) on `st`, asynchronously
+int fetch_issue(vs_handle* h, const std::vector<FetchPart>& parts, size_t total,
+                PinnedVec<uint8_t>& stage, cudaStream_t st) {
+  if (!stage.resize(std::max<size_t>(total, 256)))
     return fail(h, VS_ERR_CUDA, "pinned host allocation failed");
-  uint8_t* stage = h->fetch_stage.data();
-  for (const Part& p : parts)
-    VS_CUDA(h, cudaMemcpyAsync(stage + p.off, p.src, p.bytes, cudaMemcpyDeviceToHost, st));
-  VS_CUDA(h, cudaStreamSynchronize(st));
-  // threaded copy-out in 1 MB slices
+  for (const FetchPart& p : parts)
+    VS_CUDA(h, cudaMemcpyAsync(stage.data() + p.off, p.src, p.bytes, cudaMemcpyDeviceToHost, st));
+  return VS_OK;
+}
+
+// threaded copy from the staging buffer into the caller's (pageable)
+// buffers, which also spreads their first-touch page faults; then the
+// ligands outside every size class read as dropped
+void fetch_copy_out(const std::vector<FetchPart>& parts, const uint8_t* stage, vs_results* o,
+                    size_t b, const std::vector<int>& cls) {
   constexpr size_t kSlice = size_t(1) << 20;
   std::vector<std::array<size_t, 3>> slices;  // part, offset, bytes
   for (size_t k = 0; k < parts.size(); ++k)
-    for (size_t b = 0; b < parts[k].bytes; b += kSlice)
-      slices.push_back({k, b, std::min(kSlice, parts[k].bytes - b)});
+    for (size_t x = 0; x < parts[k].bytes; x += kSlice)
+      slices.push_back({k, x, std::min(kSlice, parts[k].bytes - x)});
   auto copy = [&](size_t t, size_t nt) {
     for (size_t i = t; i < slices.size(); i += nt) {
-      const Part& p = parts[slices[i][0]];
+      const FetchPart& p = parts[slices[i][0]];
       std::memcpy(static_cast<uint8_t*>(p.dst) + slices[i][1], stage + p.off + slices[i][1],
                   slices[i][2]);
     }
@@ -1184,20 +1285,229 @@ int vs_fetch_results(vs_handle* h, vs_results* o) {
     for (size_t t = 0; t < nt; ++t) pool.emplace_back(copy, t, nt);
     for (auto& th : pool) th.join();
   }
-  for (size_t i = 0; i < n; ++i) {
-    if (P.cls[i] < 0) {
-      if (o->n_kept) o->n_kept[i] = -1;
-      if (o->n_surv) o->n_surv[i] = 0;
-      if (o->best) o->best[i] = -INFINITY;
-    } else if (o->best && o->n_surv && o->n_surv[i] == 0) {
-      o->best[i] = -INFINITY;
+  for (size_t i = 0; i < cls.size(); ++i) {
+    const size_t g = b + i;
+    if (cls[i] < 0) {
+      if (o->n_kept) o->n_kept[g] = -1;
+      if (o->n_surv) o->n_surv[g] = 0;
+      if (o->best) o->best[g] = -INFINITY;
+    } else if (o->best && o->n_surv && o->n_surv[g] == 0) {
+      o->best[g] = -INFINITY;
     }
   }
+}
+
+}  // namespace
+
+extern "C" {
+
+int vs_fetch_results(vs_handle* h, vs_results* o) {
+  cudaSetDevice(h->device);
+  if (!h->has_results) return fail(h, VS_ERR_STATE, "no results");
+  size_t total = 0;
+  const auto parts = fetch_parts(h, o, 0, static_cast<size_t>(h->res_n), 0,
+                                 static_cast<size_t>(h->res_tors), &total);
+  int rc = fetch_issue(h, parts, total, h->fetch_stage, h->last);
+  if (rc) return rc;
+  VS_CUDA(h, cudaStreamSynchronize(h->last));
+  fetch_copy_out(parts, h->fetch_stage.data(), o, 0, h->res_cls);
   return VS_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// vs_dock_host for a large library as a pipeline of contiguous chunks: the
+// host packs chunk k+1 and copies chunk k-1's results out while chunk k
+// docks.  Chunk k uses library slot / stage set / compute stream k % 2, so
+// two chunks' kernel sequences run concurrently and fill each other's
+// launch tails; every chunk writes its own slice of the result arrays (one
+// global LPT order per chunk, the global id ranks and seeds travel with the
+// ligands, so results are those of the one-shot path, bit for bit).
+//   host:  pack(k) [after H2D(k-2)]            copy-out(k-1) [after D2H(k-1)]
+//   in:    H2D(k)  [after dock(k-2)]
+//   s[k%2]: dock(k) [after H2D(k)]
+//   out:   D2H(k)  [after dock(k)]
+int dock_host_pipelined(vs_handle* h, const vs_library* L, const vs_size_class* classes,
+                        int32_t nc, const vs_dock_params* prm, vs_results* out,
+                        const std::vector<double>& split, bool concurrent) {
+  const int chunks = static_cast<int>(split.size()) + 1;
+  if (!h->has_pocket) return fail(h, VS_ERR_STATE, "no pocket");
+  if (h->empty_bounds) return fail(h, VS_ERR_EMPTY_BOUNDS, "pocket bounds box is empty");
+  int rc = check_params(h, prm);
+  if (rc) return rc;
+  VS_CUDA(h, quiesce(h));
+  const int n = L->n_ligands;
+  for (int i = 0; i < n; ++i)  // the counts the chunk views are cut from
+    if (L->n_atoms[i] < 0 || L->n_tors[i] < 0)
+      return fail(h, VS_ERR_INVALID_ARGUMENT, "negative atom or torsion count");
+  std::vector<long> aoff(n + 1, 0), toff(n + 1, 0), moff(n + 1, 0);
+  for (int i = 0; i < n; ++i) {
+    aoff[i + 1] = aoff[i] + L->n_atoms[i];
+    toff[i + 1] = toff[i] + L->n_tors[i];
+  }
+  for (int i = 0; i < n; ++i) {
+    long m = 0;
+    for (long j = toff[i]; j < toff[i + 1]; ++j) m += L->moving_count[j];
+    moff[i + 1] = moff[i] + m;
+  }
+  for (int k = 0; k < 2; ++k) {
+    if (!h->pipe_s[k]) VS_CUDA(h, cudaStreamCreateWithFlags(&h->pipe_s[k], cudaStreamNonBlocking));
+  }
+  if (!h->pipe_in) VS_CUDA(h, cudaStreamCreateWithFlags(&h->pipe_in, cudaStreamNonBlocking));
+  if (!h->pipe_out) VS_CUDA(h, cudaStreamCreateWithFlags(&h->pipe_out, cudaStreamNonBlocking));
+  while (h->pipe_ev.size() < 3 * static_cast<size_t>(chunks)) {
+    cudaEvent_t e;
+    VS_CUDA(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    h->pipe_ev.push_back(e);
+  }
+  cudaEvent_t* evH = h->pipe_ev.data();
+  cudaEvent_t* evD = evH + chunks;
+  cudaEvent_t* evR = evD + chunks;
+  cudaStream_t st0 = h->own;
+  rc = ensure_rots(h, prm, st0);
+  if (rc) return rc;
+  rc = prepare_results(h, n, toff[n], prm, st0);
+  if (rc) return rc;
+  VS_CUDA(h, cudaStreamSynchronize(st0));
+  h->last_prm = *prm;
+  h->has_lib = false;  // the library is not left resident (vs_upload_library does that)
+  h->has_results = false;
+  h->res_cls.assign(n, -1);
+  std::vector<long> cb(chunks + 1, 0);
+  for (int k = 1; k < chunks; ++k)
+    cb[k] = std::max(cb[k - 1], std::min<long>(n, static_cast<long>(split[k - 1] * n)));
+  cb[chunks] = n;
+  std::vector<std::vector<FetchPart>> parts(chunks);
+  std::vector<size_t> totals(chunks, 0);
+  auto view = [&](int k) {
+    vs_library c = *L;
+    const long b = cb[k];
+    c.n_ligands = static_cast<int32_t>(cb[k + 1] - b);
+    c.n_atoms = L->n_atoms + b;
+    c.n_tors = L->n_tors + b;
+    c.rot_bonds = L->rot_bonds ? L->rot_bonds + b : nullptr;
+    c.coords = L->coords + 3 * aoff[b];
+    c.atom_class = L->atom_class + aoff[b];
+    c.axis_a = L->axis_a + toff[b];
+    c.axis_b = L->axis_b + toff[b];
+    c.moving_count = L->moving_count + toff[b];
+    c.moving = L->moving + moff[b];
+    c.seeds = L->seeds ? L->seeds + b : nullptr;
+    c.id_rank = L->id_rank ? L->id_rank + b : nullptr;
+    return c;
+  };
+  using clk = std::chrono::steady_clock;
+  const char* te = std::getenv("VSCREEN_UPLOAD_TIMING");
+  const bool timing = te && te[0] == '1';
+  std::vector<double> t_pack(chunks, 0.0), t_wait(chunks, 0.0), t_copy(chunks, 0.0);
+  const auto t_start = clk::now();
+  auto ms_since = [](clk::time_point a) {
+    return std::chrono::duration<double, std::milli>(clk::now() - a).count();
+  };
+  auto copy_out = [&](int k) -> int {
+    auto t0 = clk::now();
+    VS_CUDA(h, cudaEventSynchronize(evR[k]));
+    t_wait[k] = ms_since(t0);
+    t0 = clk::now();
+    const Packed& P = h->pipe_lib[k % 2];
+    fetch_copy_out(parts[k], h->pipe_stage[k % 2].data(), out, static_cast<size_t>(cb[k]), P.cls);
+    std::copy(P.cls.begin(), P.cls.end(), h->res_cls.begin() + cb[k]);
+    t_copy[k] = ms_since(t0);
+    return VS_OK;
+  };
+  // a failed chunk drains what is in flight before returning
+  auto drain = [&](int r) {
+    for (cudaStream_t x : {h->pipe_s[0], h->pipe_s[1], h->pipe_in, h->pipe_out})
+      cudaStreamSynchronize(x);
+    return r;
+  };
+  VS_CUDA(h, cudaEventRecord(h->ev0, h->pipe_s[0]));
+  VS_CUDA(h, cudaStreamWaitEvent(h->pipe_s[1], h->ev0, 0));
+  for (int k = 0; k < chunks; ++k) {
+    const int s = k % 2;
+    Packed& P = h->pipe_lib[s];
+    if (k >= 2) VS_CUDA(h, cudaEventSynchronize(evH[k - 2]));  // pinned slot free
+    const vs_library c = view(k);
+    const auto tp = clk::now();
+    rc = pack_library(h, &c, classes, nc, P, nullptr);
+    if (rc == VS_OK) rc = check_nested(h, P);
+    if (rc) return drain(rc);
+    t_pack[k] = ms_since(tp);
+    if (k >= 2) VS_CUDA(h, cudaStreamWaitEvent(h->pipe_in, evD[k - 2], 0));  // device slot free
+    rc = upload_packed(h, P, h->pipe_in, 3);
+    if (rc) return drain(rc);
+    VS_CUDA(h, cudaEventRecord(evH[k], h->pipe_in));
+    // concurrent: the chunks alternate between two compute streams (their
+    // launch tails overlap); otherwise one stream runs them in order
+    cudaStream_t cs = h->pipe_s[concurrent ? s : 0];
+    VS_CUDA(h, cudaStreamWaitEvent(cs, evH[k], 0));
+    rc = launch_packed(h, P, prm, cs, h->pipe_sg[concurrent ? s : 0],
+                       results_view(h, prm, cb[k], toff[cb[k]]), false);
+    if (rc) return drain(rc);
+    VS_CUDA(h, cudaEventRecord(evD[k], cs));
+    VS_CUDA(h, cudaStreamWaitEvent(h->pipe_out, evD[k], 0));
+    parts[k] = fetch_parts(h, out, static_cast<size_t>(cb[k]), static_cast<size_t>(cb[k + 1] - cb[k]),
+                           static_cast<size_t>(toff[cb[k]]),
+                           static_cast<size_t>(toff[cb[k + 1]] - toff[cb[k]]), &totals[k]);
+    rc = fetch_issue(h, parts[k], totals[k], h->pipe_stage[s], h->pipe_out);
+    if (rc) return drain(rc);
+    VS_CUDA(h, cudaEventRecord(evR[k], h->pipe_out));
+    if (k >= 1) {
+      rc = copy_out(k - 1);
+      if (rc) return drain(rc);
+    }
+  }
+  rc = copy_out(chunks - 1);
+  if (rc) return drain(rc);
+  if (timing) {
+    std::fprintf(stderr, "vs_dock_host pipeline (%d chunks): total %.2f ms;", chunks, ms_since(t_start));
+    for (int k = 0; k < chunks; ++k)
+      std::fprintf(stderr, " [%d] pack %.2f wait %.2f copy-out %.2f", k, t_pack[k], t_wait[k], t_copy[k]);
+    std::fprintf(stderr, "\n");
+  }
+  // the whole pipeline on the handle's timeline: ev0 .. ev1 spans every
+  // chunk's dock; later operations wait for both compute streams
+  VS_CUDA(h, cudaStreamWaitEvent(h->pipe_s[0], evD[chunks - 1], 0));
+  if (chunks >= 2) VS_CUDA(h, cudaStreamWaitEvent(h->pipe_s[0], evD[chunks - 2], 0));
+  VS_CUDA(h, cudaEventRecord(h->ev1, h->pipe_s[0]));
+  VS_CUDA(h, mark_done(h, h->pipe_s[0]));
+  h->last = h->pipe_s[0];
+  h->timed = true;
+  h->staged_run = false;  // no per-launch phase events in the pipeline
+  h->has_results = true;
+  h->res_n = n;
+  h->res_tors = toff[n];
+  return VS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 int vs_dock_host(vs_handle* h, const vs_library* L, const vs_size_class* classes, int32_t nc,
                  const vs_dock_params* prm, vs_results* out) {
+  // large libraries: the pipelined path (host pack / copy-out under the
+  // dock); VSCREEN_PIPELINE=0 forces the one-shot path
+  const char* pe = std::getenv("VSCREEN_PIPELINE");
+  if (L->n_ligands >= kPipeMinLigands && !(pe && pe[0] == '0')) {
+    cudaSetDevice(h->device);
+    // chunk boundaries as fractions of the library (VSCREEN_PIPE_SPLIT,
+    // comma-separated; VSCREEN_PIPE_CONCURRENT=0 runs them on one stream)
+    std::vector<double> split(kPipeSplit, kPipeSplit + sizeof(kPipeSplit) / sizeof(double));
+    if (const char* e = std::getenv("VSCREEN_PIPE_SPLIT"); e && *e) {
+      split.clear();
+      for (const char* c = e; *c;) {
+        char* end = nullptr;
+        split.push_back(std::strtod(c, &end));
+        c = (*end == ',') ? end + 1 : end;
+        if (end == c && *c) break;
+      }
+    }
+    const char* ce = std::getenv("VSCREEN_PIPE_CONCURRENT");
+    return dock_host_pipelined(h, L, classes, nc, prm, out, split, !(ce && ce[0] == '0'));
+  }
   int rc = vs_upload_library(h, L, classes, nc);
   if (rc) return rc;
   rc = vs_dock(h, prm, nullptr);
@@ -1238,7 +1548,7 @@ int vs_topk_device(vs_handle* h, int32_t k, uint64_t* out_dev, void* stream) {
   if (!h->has_results) return fail(h, VS_ERR_STATE, "no results");
   cudaStream_t st = pick(h, stream);
   VS_CUDA(h, after_prev(h, st));  // the keys of a dock on another stream
-  const int rc = topk_run(h, h->d_keys.as<unsigned long long>(), h->lib.n, k,
+  const int rc = topk_run(h, h->d_keys.as<unsigned long long>(), h->res_n, k,
                           reinterpret_cast<unsigned long long*>(out_dev), st);
   if (rc == VS_OK) VS_CUDA(h, mark_done(h, st));
   return rc;
@@ -1361,7 +1671,7 @@ int vs_topk_allgather(vs_handle* h, void* comm, int32_t k, uint64_t* out_dev, vo
   VS_CUDA(h, h->d_gather.ensure(static_cast<size_t>(nranks + 1) * k * 8));
   auto* local = h->d_gather.as<unsigned long long>();
   auto* all = local + k;
-  int rc = topk_run(h, h->d_keys.as<unsigned long long>(), h->lib.n, k, local, st);
+  int rc = topk_run(h, h->d_keys.as<unsigned long long>(), h->res_n, k, local, st);
   if (rc) return rc;
   // one all-gather of k u64 keys per rank (8 KB at k = 1000), then the same
   // deterministic merge on every rank

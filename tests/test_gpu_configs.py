@@ -208,3 +208,34 @@ def test_c2_whole_bench_library_bit_exact(V, engine):
                              threads=os.cpu_count() or 16)
     _same(res, ora)
     np.testing.assert_array_equal(top, sweep.topk(ora["keys"], 1000))
+
+
+def test_pipelined_dock_host_equals_one_shot(V, engine, monkeypatch):
+    """vs_dock_host on a large library (>= 32768 ligands) runs as a pipeline
+    of chunks (host pack / copy-out under the dock, two chunks' kernels in
+    flight): every output array, the device top-k and a later fetch equal
+    the one-shot path (VSCREEN_PIPELINE=0) bit for bit; class-dropped
+    ligands are marked in every chunk."""
+    import bench
+    lib, _, _ = bench.build_workload(40_000, 0, 1, 16)
+    pocket = bench.make_pocket()
+    prm = V.DockParams(restarts=6, rotations=64, flex_angles=16, flex_passes=1, keep_top=3,
+                       min_score=-5.0, write_all_poses=True)
+    engine.set_pocket(pocket, grid_spacing=0.4)
+    classes = [(10, 30, 0, 11)]  # ligands with >= 30 atoms are dropped
+    a = engine.dock_host(lib, prm, classes=classes)
+    top_a = engine.topk(500)
+    again = engine.fetch()
+    monkeypatch.setenv("VSCREEN_PIPELINE", "0")
+    b = engine.dock_host(lib, prm, classes=classes)
+    top_b = engine.topk(500)
+    assert (a.n_kept == -1).sum() > 0
+    for f in ("best", "n_kept", "n_surv", "keys", "surv_tors", "all_tors"):
+        np.testing.assert_array_equal(np.asarray(getattr(a, f)).view(np.uint8),
+                                      np.asarray(getattr(b, f)).view(np.uint8), err_msg=f)
+        np.testing.assert_array_equal(np.asarray(getattr(again, f)).view(np.uint8),
+                                      np.asarray(getattr(b, f)).view(np.uint8), err_msg=f)
+    for f in ("surv", "all"):
+        np.testing.assert_array_equal(np.ascontiguousarray(getattr(a, f)).view(np.uint8),
+                                      np.ascontiguousarray(getattr(b, f)).view(np.uint8), err_msg=f)
+    np.testing.assert_array_equal(top_a, top_b)
