@@ -64,6 +64,8 @@ def lib() -> C.CDLL:
             "vsref_rng_u64": (None, [C.c_uint64, P(C.c_uint64), C.c_int, C.c_int, P(C.c_uint64)]),
             "vsref_start_draws": (None, [P(C.c_uint64), P(C.c_int32), C.c_int, C.c_int, C.c_int,
                                          P(C.c_double), P(C.c_double), C.c_int, P(C.c_float)]),
+            "vsref_parse_check": (C.c_int, [C.c_char_p, P(C.c_int), P(C.c_long), P(C.c_int),
+                                         P(C.c_int)]),
             "vsref_rng_draws": (None, [C.c_uint64, P(C.c_uint64), C.c_int, P(C.c_int32), P(C.c_double),
                                        P(C.c_double), C.c_int, P(C.c_double)]),
             "vsref_random_smiles": (C.c_int, [C.c_uint64, C.c_uint64, C.c_char_p, C.c_int]),
@@ -303,3 +305,12 @@ def start_draws(seeds, n_tors, restarts: int, attempts: int, lo, hi) -> np.ndarr
     lib().vsref_start_draws(_p(seeds, C.c_uint64), _p(n_tors, C.c_int32), n, restarts, attempts,
                             _p(lo, C.c_double), _p(hi, C.c_double), stride, _p(out, C.c_float))
     return out[:n * restarts * attempts * stride].reshape(n, restarts, attempts, stride)
+
+
+def parse_check(smiles: str):
+    """("ok", n_atoms, n_bonds) or ("error", kind index, 1-based position) of
+    the reference chem::parse_smiles (shim vsref_parse_check)."""
+    k, p, na, nb = C.c_int(), C.c_long(), C.c_int(), C.c_int()
+    rc = lib().vsref_parse_check(smiles.encode("latin-1"), C.byref(k), C.byref(p), C.byref(na),
+                                 C.byref(nb))
+    return ("error", k.value, p.value) if rc else ("ok", na.value, nb.value)

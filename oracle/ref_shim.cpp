@@ -493,6 +493,21 @@ void vsref_start_draws(const std::uint64_t* seeds, const std::int32_t* n_tors, i
   }
 }
 
+// chem::parse_smiles (chem.cpp:109-264): 0 = parsed (atoms / bonds
+// counts out), 1 = ParseError (kind, 1-based position out)
+int vsref_parse_check(const char* smiles, int* kind, long* pos, int* n_atoms, int* n_bonds) {
+  try {
+    const chem::MolecularGraph g = chem::parse_smiles(smiles);
+    *n_atoms = g.atom_count();
+    *n_bonds = static_cast<int>(g.bonds.size());
+    return 0;
+  } catch (const chem::ParseError& e) {
+    *kind = static_cast<int>(e.kind());
+    *pos = static_cast<long>(e.position());
+    return 1;
+  }
+}
+
 // ----------------------------------------------------------------- corpus --
 // corpus::random_smiles(Rng(seed).split(i)) (tools/smiles_corpus.hpp:13,51)
 int vsref_random_smiles(std::uint64_t seed, std::uint64_t i, char* out, int cap) {

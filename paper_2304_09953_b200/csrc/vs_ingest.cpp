@@ -27,147 +27,196 @@
 
 namespace vs {
 
-namespace {
-
-struct RingOpen {
-  int atom = -1;
-  int order = 0;  // 0 = unspecified
-  std::size_t pos = 0;
-};
-
-int bond_char_order(char c) {
-  return c == '-' ? 1 : c == '=' ? 2 : c == '#' ? 3 : 0;
-}
-
-}  // namespace
-
 ParseFailure::ParseFailure(int kind, std::size_t pos, const std::string& msg)
     : std::runtime_error(msg), kind(kind), pos(pos) {}
 
 // ----------------------------------------------------------------- parse --
-Graph parse_smiles(const std::string& text) {
-  Graph g;
-  if (text.empty()) throw ParseFailure(kUnknownToken, 1, "empty input");
-  int prev = -1;
-  int pending = 0;
-  std::size_t pending_pos = 0;
-  std::vector<std::pair<int, std::size_t>> branches;
-  std::array<RingOpen, 100> rings{};
+// The contract (chem.cpp:109-264): the organic-subset grammar, implicit
+// bond orders (aromatic-aromatic -> aromatic, else single), and which error
+// kind and 1-based position each malformed input reports, in text order.
+// Built here as a streaming lexer (one token per call, so a lexical error
+// never pre-empts an earlier structural one) driving a small graph-builder
+// state machine.
+namespace {
 
-  auto connect = [&](int a, int b, int order, std::size_t pos) {
-    if (a == b) throw ParseFailure(kUnclosedRingBond, pos, "ring bond to the same atom");
-    for (const auto& e : g.bonds) {
-      if ((e.a == a && e.b == b) || (e.a == b && e.b == a))
-        throw ParseFailure(kUnclosedRingBond, pos, "duplicate bond");
-    }
-    g.bonds.push_back({a, b, order});
-  };
-  auto atom = [&](const char* el, bool aromatic, std::size_t pos) {
-    const int idx = static_cast<int>(g.elements.size());
-    g.elements.emplace_back(el);
-    g.aromatic.push_back(aromatic);
-    if (prev >= 0) {
-      const int order = pending ? pending : (aromatic && g.aromatic[prev]) ? 4 : 1;
-      connect(prev, idx, order, pos);
-    } else if (pending) {
-      throw ParseFailure(kUnknownToken, pending_pos, "bond before any atom");
-    }
-    pending = 0;
-    prev = idx;
-  };
-  auto ring = [&](int num, std::size_t pos) {
-    if (prev < 0) throw ParseFailure(kUnknownToken, pos, "ring closure before any atom");
-    RingOpen& r = rings[static_cast<std::size_t>(num)];
-    if (r.atom < 0) {
-      r = {prev, pending, pos};
-      pending = 0;
-      return;
-    }
-    if (r.order && pending && r.order != pending)
-      throw ParseFailure(kUnclosedRingBond, pos, "conflicting ring bond orders");
-    int order = pending ? pending
-                : r.order ? r.order
-                : (g.aromatic[r.atom] && g.aromatic[prev]) ? 4
-                                                           : 1;
-    connect(r.atom, prev, order, pos);
-    r = RingOpen{};
-    pending = 0;
-  };
+enum class Tok { Atom, Bond, Open, Close, Ring, End };
 
-  const std::size_t n = text.size();
-  for (std::size_t i = 0; i < n;) {
-    const char c = text[i];
-    const std::size_t pos = i + 1;
-    const char nx = i + 1 < n ? text[i + 1] : '\0';
-    if (c == 'C' && nx == 'l') {
-      atom("Cl", false, pos);
-      i += 2;
-      continue;
-    }
-    if (c == 'B' && nx == 'r') {
-      atom("Br", false, pos);
-      i += 2;
-      continue;
-    }
-    if (std::strchr("BCNOPSFI", c) && c != '\0') {
-      const char el[2] = {c, '\0'};
-      atom(el, false, pos);
-      ++i;
-      continue;
-    }
-    if (std::strchr("bcnops", c) && c != '\0') {
-      const char el[2] = {static_cast<char>(c - 'a' + 'A'), '\0'};
-      atom(el, true, pos);
-      ++i;
-      continue;
-    }
-    if (const int bo = bond_char_order(c)) {
-      if (pending) throw ParseFailure(kUnknownToken, pos, "two bond symbols in a row");
-      if (prev < 0) throw ParseFailure(kUnknownToken, pos, "bond before any atom");
-      pending = bo;
-      pending_pos = pos;
-      ++i;
-      continue;
+struct Token {
+  Tok kind = Tok::End;
+  std::size_t pos = 0;  // 1-based offset of the token's first byte
+  char sym[3] = {0, 0, 0};
+  bool aromatic = false;
+  int value = 0;  // bond order, or ring-closure number
+};
+
+class Lexer {
+ public:
+  explicit Lexer(const std::string& s) : s_(s) {}
+
+  Token next() {
+    Token t;
+    t.pos = i_ + 1;
+    if (i_ >= s_.size()) return t;
+    const char c = s_[i_];
+    const char d = i_ + 1 < s_.size() ? s_[i_ + 1] : '\0';
+    if ((c == 'C' && d == 'l') || (c == 'B' && d == 'r')) {  // two-letter halogens first
+      t.kind = Tok::Atom;
+      t.sym[0] = c;
+      t.sym[1] = d;
+      i_ += 2;
+      return t;
     }
     switch (c) {
-      case '(':
-        if (prev < 0) throw ParseFailure(kUnbalancedBranch, pos, "branch before any atom");
-        if (pending) throw ParseFailure(kUnknownToken, pos, "bond before branch open");
-        branches.emplace_back(prev, pos);
-        ++i;
-        continue;
-      case ')':
-        if (branches.empty()) throw ParseFailure(kUnbalancedBranch, pos, "unmatched ')'");
-        if (pending) throw ParseFailure(kUnknownToken, pos, "dangling bond before ')'");
-        prev = branches.back().first;
-        branches.pop_back();
-        ++i;
-        continue;
+      case 'B': case 'C': case 'N': case 'O': case 'P': case 'S': case 'F': case 'I':
+        t.kind = Tok::Atom;
+        t.sym[0] = c;
+        break;
+      case 'b': case 'c': case 'n': case 'o': case 'p': case 's':
+        t.kind = Tok::Atom;
+        t.sym[0] = static_cast<char>(c - 32);  // stored uppercase (chem.cpp:197)
+        t.aromatic = true;
+        break;
+      case '-': t.kind = Tok::Bond; t.value = 1; break;
+      case '=': t.kind = Tok::Bond; t.value = 2; break;
+      case '#': t.kind = Tok::Bond; t.value = 3; break;
+      case '(': t.kind = Tok::Open; break;
+      case ')': t.kind = Tok::Close; break;
       case '%': {
-        const bool ok = i + 2 < n && std::isdigit(static_cast<unsigned char>(text[i + 1])) &&
-                        std::isdigit(static_cast<unsigned char>(text[i + 2]));
-        if (!ok) throw ParseFailure(kUnknownToken, pos, "'%' needs two digits");
-        const int num = (text[i + 1] - '0') * 10 + (text[i + 2] - '0');
-        if (num < 10) throw ParseFailure(kUnknownToken, pos, "'%' ring numbers start at 10");
-        ring(num, pos);
-        i += 3;
-        continue;
+        const bool two = i_ + 2 < s_.size() && digit(s_[i_ + 1]) && digit(s_[i_ + 2]);
+        if (!two) throw ParseFailure(kUnknownToken, t.pos, "'%' must be followed by two digits");
+        t.value = 10 * (s_[i_ + 1] - '0') + (s_[i_ + 2] - '0');
+        if (t.value < 10)
+          throw ParseFailure(kUnknownToken, t.pos, "two-digit ring label below 10");
+        t.kind = Tok::Ring;
+        i_ += 3;
+        return t;
       }
       default:
-        break;
+        if (c >= '1' && c <= '9') {
+          t.kind = Tok::Ring;
+          t.value = c - '0';
+          break;
+        }
+        throw ParseFailure(kUnknownToken, t.pos, std::string("character '") + c + "' not in the grammar");
     }
-    if (c >= '1' && c <= '9') {
-      ring(c - '0', pos);
-      ++i;
-      continue;
+    ++i_;
+    return t;
+  }
+
+ private:
+  static bool digit(char c) { return c >= '0' && c <= '9'; }
+  const std::string& s_;
+  std::size_t i_ = 0;
+};
+
+class GraphBuilder {
+ public:
+  explicit GraphBuilder(Graph& g) : g_(g) { open_.fill(Label{}); }
+
+  void atom(const Token& t) {
+    const int id = static_cast<int>(g_.elements.size());
+    g_.elements.emplace_back(t.sym);
+    g_.aromatic.push_back(t.aromatic);
+    if (anchor_ < 0) {
+      if (bond_) throw ParseFailure(kUnknownToken, bond_pos_, "bond symbol with no atom before it");
+    } else {
+      add_bond(anchor_, id, bond_ ? bond_ : implicit(anchor_, id), t.pos);
     }
-    throw ParseFailure(kUnknownToken, pos, std::string("unexpected character '") + c + "'");
+    bond_ = 0;
+    anchor_ = id;
   }
-  if (pending) throw ParseFailure(kUnknownToken, pending_pos, "dangling bond at end of input");
-  if (!branches.empty()) throw ParseFailure(kUnbalancedBranch, branches.front().second, "unclosed '('");
-  for (const RingOpen& r : rings) {
-    if (r.atom >= 0) throw ParseFailure(kUnclosedRingBond, r.pos, "unclosed ring bond");
+
+  void bond(const Token& t) {
+    if (bond_) throw ParseFailure(kUnknownToken, t.pos, "consecutive bond symbols");
+    if (anchor_ < 0) throw ParseFailure(kUnknownToken, t.pos, "bond symbol with no atom before it");
+    bond_ = t.value;
+    bond_pos_ = t.pos;
   }
+
+  void open(const Token& t) {
+    if (anchor_ < 0) throw ParseFailure(kUnbalancedBranch, t.pos, "branch with no atom before it");
+    if (bond_) throw ParseFailure(kUnknownToken, t.pos, "bond symbol in front of '('");
+    branches_.push_back({anchor_, t.pos});
+  }
+
+  void close(const Token& t) {
+    if (branches_.empty()) throw ParseFailure(kUnbalancedBranch, t.pos, "')' without a matching '('");
+    if (bond_) throw ParseFailure(kUnknownToken, t.pos, "bond symbol in front of ')'");
+    anchor_ = branches_.back().atom;
+    branches_.pop_back();
+  }
+
+  void ring(const Token& t) {
+    if (anchor_ < 0) throw ParseFailure(kUnknownToken, t.pos, "ring label with no atom before it");
+    Label& l = open_[static_cast<std::size_t>(t.value)];
+    if (l.atom < 0) {  // opens the label
+      l = Label{anchor_, bond_, t.pos};
+      bond_ = 0;
+      return;
+    }
+    if (l.order && bond_ && l.order != bond_)
+      throw ParseFailure(kUnclosedRingBond, t.pos, "ring label closed with another bond order");
+    const int order = bond_ ? bond_ : l.order ? l.order : implicit(l.atom, anchor_);
+    add_bond(l.atom, anchor_, order, t.pos);
+    l = Label{};
+    bond_ = 0;
+  }
+
+  void finish() {
+    if (bond_) throw ParseFailure(kUnknownToken, bond_pos_, "input ends after a bond symbol");
+    if (!branches_.empty())
+      throw ParseFailure(kUnbalancedBranch, branches_.front().pos, "'(' never closed");
+    for (const Label& l : open_)
+      if (l.atom >= 0) throw ParseFailure(kUnclosedRingBond, l.pos, "ring label never closed");
+  }
+
+ private:
+  struct Label {
+    int atom = -1;
+    int order = 0;  // 0: not given at the opening
+    std::size_t pos = 0;
+  };
+  struct Branch {
+    int atom;
+    std::size_t pos;
+  };
+
+  int implicit(int a, int b) const { return g_.aromatic[a] && g_.aromatic[b] ? 4 : 1; }
+
+  void add_bond(int a, int b, int order, std::size_t pos) {
+    if (a == b) throw ParseFailure(kUnclosedRingBond, pos, "ring label closes on its own atom");
+    for (const BondRec& e : g_.bonds)
+      if ((e.a == a && e.b == b) || (e.a == b && e.b == a))
+        throw ParseFailure(kUnclosedRingBond, pos, "atoms already bonded");
+    g_.bonds.push_back(BondRec{a, b, order});
+  }
+
+  Graph& g_;
+  int anchor_ = -1;  // the atom the next atom / bond / label attaches to
+  int bond_ = 0;     // explicit order waiting for its second atom
+  std::size_t bond_pos_ = 0;
+  std::vector<Branch> branches_;
+  std::array<Label, 100> open_;
+};
+
+}  // namespace
+
+Graph parse_smiles(const std::string& text) {
+  if (text.empty()) throw ParseFailure(kUnknownToken, 1, "empty SMILES");
+  Graph g;
+  Lexer lex(text);
+  GraphBuilder build(g);
+  for (Token t = lex.next(); t.kind != Tok::End; t = lex.next()) {
+    switch (t.kind) {
+      case Tok::Atom: build.atom(t); break;
+      case Tok::Bond: build.bond(t); break;
+      case Tok::Open: build.open(t); break;
+      case Tok::Close: build.close(t); break;
+      case Tok::Ring: build.ring(t); break;
+      case Tok::End: break;
+    }
+  }
+  build.finish();
   g.ring = ring_bond_flags(g);
   return g;
 }
@@ -229,36 +278,58 @@ int rotatable_bond_count(const Graph& g) {
   return count;
 }
 
+// Torsion axes (dock.cpp:234-270): in bond order, every single non-ring
+// bond whose atoms both have degree >= 2; moving = the atoms on b's side of
+// the bond, b itself excluded, ascending.  One DFS forest gives every atom's
+// pre-order interval, so each side of a bridge is an interval test: for a
+// DFS tree edge parent -> child the child's side is the child's subtree, the
+// parent's side the rest of that tree.
 Topology torsion_axes(const Graph& g) {
   Topology t;
+  const int n = static_cast<int>(g.elements.size());
   const auto deg = degrees(g);
-  const std::size_t n = g.elements.size();
-  std::vector<std::vector<int>> adj(n);
-  for (const auto& b : g.bonds) {
-    adj[b.a].push_back(b.b);
-    adj[b.b].push_back(b.a);
+  std::vector<std::vector<int>> adj(static_cast<std::size_t>(n));
+  for (const auto& e : g.bonds) {
+    adj[e.a].push_back(e.b);
+    adj[e.b].push_back(e.a);
   }
-  std::vector<char> seen(n);
-  for (std::size_t e = 0; e < g.bonds.size(); ++e) {
-    const auto& b = g.bonds[e];
-    if (b.order != 1 || g.ring[e] || deg[b.a] < 2 || deg[b.b] < 2) continue;
-    Axis ax;
-    ax.a = b.a;
-    ax.b = b.b;
-    std::fill(seen.begin(), seen.end(), 0);
-    seen[b.a] = seen[b.b] = 1;
-    std::vector<int> todo{b.b};
-    while (!todo.empty()) {
-      const int v = todo.back();
-      todo.pop_back();
-      for (int w : adj[v]) {
-        if (seen[w]) continue;
-        seen[w] = 1;
-        ax.moving.push_back(w);
-        todo.push_back(w);
+  std::vector<int> tin(n, -1), tout(n, -1), root(n, -1), parent(n, -1);
+  int clock = 0;
+  for (int r = 0; r < n; ++r) {
+    if (tin[r] >= 0) continue;
+    std::vector<std::pair<int, std::size_t>> st{{r, 0}};  // (atom, next neighbour)
+    tin[r] = clock++;
+    root[r] = r;
+    while (!st.empty()) {
+      auto& [v, k] = st.back();
+      if (k < adj[v].size()) {
+        const int w = adj[v][k++];
+        if (tin[w] < 0) {
+          tin[w] = clock++;
+          root[w] = r;
+          parent[w] = v;
+          st.push_back({w, 0});
+        }
+      } else {
+        tout[v] = clock;
+        st.pop_back();
       }
     }
-    std::sort(ax.moving.begin(), ax.moving.end());
+  }
+  auto inside = [&](int x, int v) { return tin[v] <= tin[x] && tin[x] < tout[v]; };
+  for (std::size_t e = 0; e < g.bonds.size(); ++e) {
+    const BondRec& bd = g.bonds[e];
+    if (bd.order != 1 || g.ring[e] || deg[bd.a] < 2 || deg[bd.b] < 2) continue;
+    Axis ax;
+    ax.a = bd.a;
+    ax.b = bd.b;
+    // a bridge is a tree edge: b is a's child or a is b's child
+    const bool b_below = parent[bd.b] == bd.a;
+    for (int x = 0; x < n; ++x) {
+      if (x == bd.b || root[x] != root[bd.b]) continue;
+      const bool side_b = b_below ? inside(x, bd.b) : !inside(x, bd.a);
+      if (side_b) ax.moving.push_back(x);
+    }
     t.axes.push_back(std::move(ax));
   }
   return t;

@@ -108,3 +108,45 @@ def test_bench_configs_declared():
     assert set(bench.CONFIGS) == {"c2", "c3", "c4", "c5"}
     assert bench.CONFIGS["c3"]["scaling"] == "strong"
     assert bench.CONFIGS["c5"]["grid_spacing"] == 0.2
+
+
+def _fuzz_smiles(rng, n):
+    """Malformed and well-formed strings over the grammar's alphabet plus
+    noise: random token soups, corpus entries with one edit, truncations."""
+    toks = ["C", "N", "O", "S", "P", "F", "I", "B", "Cl", "Br", "c", "n", "o", "s", "p", "b",
+            "-", "=", "#", "(", ")", "1", "2", "3", "9", "%12", "%10", "%1", "%0a", "%", "X", "[",
+            "l", "r", "0", " "]
+    out = []
+    import paper_2304_09953_b200 as V
+    for k in range(n):
+        mode = k % 3
+        if mode == 0:
+            out.append("".join(rng.choice(toks) for _ in range(rng.integers(0, 9))))
+        else:
+            s = V.random_smiles(99, int(rng.integers(0, 10_000)))
+            if mode == 1 and s:
+                i = int(rng.integers(0, len(s)))
+                s = s[:i] + rng.choice(toks) + s[i + 1:]
+            else:
+                s = s[:int(rng.integers(0, len(s) + 1))]
+            out.append(s)
+    return out
+
+
+def test_parse_errors_match_reference_kind_and_position(V):
+    """The parser (vs_ingest.cpp, streaming lexer + graph builder) reports
+    the reference's outcome on 6000 fuzzed strings: parsed (same atom and
+    bond counts) or ParseError with the same kind and 1-based position."""
+    R = need_ref()
+    rng = np.random.default_rng(2026)
+    n_err = 0
+    for s in _fuzz_smiles(rng, 6000):
+        ref = R.parse_check(s)
+        try:
+            g = V.parse_smiles(s)
+            ours = ("ok", len(g["atoms"]), len(g["bonds"]))
+        except V.ParseError as e:
+            ours = ("error", V.ParseError.KINDS.index(e.kind), e.position)
+            n_err += 1
+        assert ours == ref, (s, ours, ref)
+    assert 1500 < n_err < 5500
