@@ -176,6 +176,22 @@ def build_workload(n_per: int, rank: int, world: int, threads: int, balanced: bo
     return lib, ids_all, order
 
 
+def pin_library(lib):
+    """Move the library's arrays into page-locked host memory (torch
+    pin_memory), the e2e contract's "inputs from pinned host memory": the
+    C-ABI then DMAs them straight to the device packer at link rate."""
+    import torch
+    for name in ("n_atoms", "n_tors", "rot_bonds", "coords", "atom_class", "axis_a", "axis_b",
+                 "moving_count", "moving", "seeds", "id_rank"):
+        a = np.ascontiguousarray(getattr(lib, name))
+        t = torch.empty(max(a.nbytes, 1), dtype=torch.uint8, pin_memory=True)
+        pa = t.numpy()[:a.nbytes].view(a.dtype).reshape(a.shape)
+        pa[...] = a
+        setattr(lib, name, pa)
+        setattr(lib, "_pin_" + name, t)  # keeps the pinned storage alive
+    return lib
+
+
 # ------------------------------------------------------------------ clocks --
 class ClockSampler:
     """nvidia-smi sampled during the timed region (B200_PROFILING.md)."""
@@ -798,6 +814,7 @@ def main():
 
     e2e = None
     if not args.no_e2e:
+        pin_library(lib)  # inputs from pinned host memory (outside the timed region)
         n_e2e = max(1, min(args.steps, 3))
         eng.dock_host(lib, prm, classes)  # warm the host path
         if world > 1:
@@ -819,7 +836,8 @@ def main():
                "h2d_bytes_per_step": h2d_bytes(lib) * world,
                "d2h_bytes_per_step": d2h_bytes(lib, prm) * world,
                "steps": n_e2e,
-               "path": "vs_dock_host (pack + H2D + dock + D2H results) + top-k D2H, host wall clock"}
+               "path": "vs_dock_host from pinned host arrays (H2D + device packer + dock + D2H "
+                       "results) + top-k D2H, host wall clock"}
 
     analytic = None
     if rank == 0 and world == 1 and not args.no_cpu and args.config == "c2":

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "../../include/vscreen_gpu/capi.h"
+#include "vs_pack.h"
 #include "vs_rng.h"
 #include "vs_types.h"
 
@@ -161,6 +162,7 @@ struct Packed {
   std::vector<Bucket> buckets;
   Bucket all;  // global LPT order (dock launch)
   long total_tors = 0;
+  long total_atoms = 0;
   DBuf d_meta, d_mov, d_atoms, d_axes, d_moving, d_seeds, d_idr, d_order;
   void release() {
     d_meta.release(); d_mov.release(); d_atoms.release(); d_axes.release();
@@ -284,6 +286,9 @@ struct vs_handle {
   // caller (the C++ drop-in's geometric_score) allocates nothing per call
   Packed xpack;
   DBuf xbuf[10];
+  // the device packer (vs_pack.cu): the caller's raw arrays, scratch, CUB temp
+  DBuf raw[9], pwork[13], ptemp;
+  PinnedVec<int> pk_host;  // stats + error key + classes read back
   DBuf rbuf[9];              // vs_rescore's per-bucket pose arrays, reused across calls
   // vs_rescore's pinned staging of the concatenated per-bucket pose arrays
   PinnedVec<int> rs_lig, rs_off, rs_orig;
@@ -478,6 +483,7 @@ int pack_library(vs_handle* h, const vs_library* L, const vs_size_class* classes
   const long to = toff[n];
   P.tors_off[n] = to;
   P.total_tors = to;
+  P.total_atoms = aoff[n];
   // one stable LPT sort (descending cost, then index); the per-class buckets
   // are class-filtered views of it (same order inside each class), and the
   // global queue over every class is the dock launch's
@@ -765,6 +771,9 @@ void vs_destroy(vs_handle* h) {
   h->rpack.release();
   h->xpack.release();
   for (DBuf& b : h->xbuf) b.release();
+  for (DBuf& b : h->raw) b.release();
+  for (DBuf& b : h->pwork) b.release();
+  h->ptemp.release();
   for (DBuf& b : h->rbuf) b.release();
   for (DBuf* b : {&h->d_sites, &h->d_softtab, &h->d_sites64, &h->d_maps, &h->d_surv, &h->d_surv_tors, &h->d_all, &h->d_all_tors,
                   &h->d_best, &h->d_nkept, &h->d_nsurv, &h->d_keys, &h->d_rots, &h->d_topk_a, &h->d_topk_b, &h->d_stats})
@@ -929,6 +938,155 @@ int vs_grid_fetch(vs_handle* h, float* steric, float* hbond, float* lipo) {
   return VS_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// The library packer on the device (north-star subsystem 1, vs_pack.cu):
+// the caller's arrays DMA'd as given (pinned memory: full link rate), the
+// SoA layout, size classes, checks and LPT order built by kernels on `st`,
+// one synchronize to read back the outcome.  Leaves P ready for
+// launch_packed (P.all over P.d_order, P.cls on the host).  The count
+// checks run on the host first (they size the transfers).
+int gpu_pack(vs_handle* h, const vs_library* L, const vs_size_class* classes, int nc, Packed& P,
+             cudaStream_t st) {
+  const int n = L->n_ligands;
+  if (n < 0) return fail(h, VS_ERR_INVALID_ARGUMENT, "negative ligand count");
+  long A = 0, T = 0, M = 0;
+  for (int i = 0; i < n; ++i) {  // pass 1 of pack_library, same precedence
+    const int N = L->n_atoms[i], t = L->n_tors[i];
+    if (N < 1) return fail(h, VS_ERR_ATOM_COUNT, "conformer has no atoms (ligand " + std::to_string(i) + ")");
+    if (N > kMaxAtoms || t > kMaxTors)
+      return fail(h, VS_ERR_CAPACITY, "ligand " + std::to_string(i) + " exceeds GPU limits");
+    if (t < 0) return fail(h, VS_ERR_INVALID_ARGUMENT, "negative torsion count");
+    A += N;
+    T += t;
+  }
+  for (long j = 0; j < T; ++j) M += std::max(0, L->moving_count[j]);
+  const size_t n1 = static_cast<size_t>(n) + 1, t1 = static_cast<size_t>(T) + 1;
+  // raw arrays (as given) -> device
+  DBuf* r = h->raw;
+  auto up = [&](DBuf& d, const void* src, size_t bytes) -> cudaError_t {
+    cudaError_t e = d.ensure(std::max<size_t>(bytes, 16));
+    if (e == cudaSuccess && bytes > 0 && src)
+      e = cudaMemcpyAsync(d.p, src, bytes, cudaMemcpyHostToDevice, st);
+    return e;
+  };
+  VS_CUDA(h, up(r[0], L->n_atoms, n * 4ul));
+  VS_CUDA(h, up(r[1], L->n_tors, n * 4ul));
+  VS_CUDA(h, up(r[2], L->rot_bonds, L->rot_bonds ? n * 4ul : 0));
+  VS_CUDA(h, up(r[3], L->coords, A * 24ul));
+  VS_CUDA(h, up(r[4], L->atom_class, A * 4ul));
+  VS_CUDA(h, up(r[5], L->axis_a, T * 4ul));
+  VS_CUDA(h, up(r[6], L->axis_b, T * 4ul));
+  VS_CUDA(h, up(r[7], L->moving_count, T * 4ul));
+  VS_CUDA(h, up(r[8], L->moving, M * 4ul));
+  VS_CUDA(h, up(P.d_seeds, L->seeds, L->seeds ? n * 8ul : 0));
+  VS_CUDA(h, up(P.d_idr, L->id_rank, L->id_rank ? n * 4ul : 0));
+  // classes (int4 each) ride in the stats buffer's tail
+  DBuf* w = h->pwork;
+  VS_CUDA(h, w[0].ensure(n1 * 8));   // cnt_a
+  VS_CUDA(h, w[1].ensure(n1 * 8));   // cnt_t
+  VS_CUDA(h, w[2].ensure(t1 * 8));   // cnt_m
+  VS_CUDA(h, w[3].ensure(n1 * 8));   // cnt_p
+  VS_CUDA(h, w[4].ensure(n1 * 8));   // aoff
+  VS_CUDA(h, w[5].ensure(n1 * 8));   // toff
+  VS_CUDA(h, w[6].ensure(t1 * 8));   // msrc
+  VS_CUDA(h, w[7].ensure(n1 * 8));   // moff
+  VS_CUDA(h, w[8].ensure(n1 * 4));   // cls
+  VS_CUDA(h, w[9].ensure(n1 * 4));   // key
+  VS_CUDA(h, w[10].ensure(n1 * 4));  // key_sorted
+  VS_CUDA(h, w[11].ensure(n1 * 4));  // idx
+  VS_CUDA(h, w[12].ensure(64 + 16 * static_cast<size_t>(std::max(nc, 1))));  // stats, err, classes
+  const size_t tmp = pack_temp_bytes(n, T);
+  VS_CUDA(h, h->ptemp.ensure(tmp));
+  // packed outputs: M raw entries -> at most M + 15 n padded bytes
+  VS_CUDA(h, P.d_meta.ensure(std::max<size_t>(16, n * 16ul)));
+  VS_CUDA(h, P.d_mov.ensure(std::max<size_t>(8, n * 8ul)));
+  VS_CUDA(h, P.d_atoms.ensure(std::max<size_t>(32, A * 32ul)));
+  VS_CUDA(h, P.d_axes.ensure(std::max<size_t>(16, T * 16ul)));
+  VS_CUDA(h, P.d_moving.ensure(std::max<size_t>(16, M + 15ul * n + 16)));
+  VS_CUDA(h, P.d_seeds.ensure(std::max<size_t>(8, n * 8ul)));
+  VS_CUDA(h, P.d_idr.ensure(std::max<size_t>(4, n * 4ul)));
+  VS_CUDA(h, P.d_order.ensure(std::max<size_t>(4, n * 4ul)));
+  int* stats = w[12].as<int>();
+  unsigned long long* err = reinterpret_cast<unsigned long long*>(stats + 8);
+  int4* dcls = reinterpret_cast<int4*>(stats + 16);
+  if (!h->pk_host.resize(16 + 4 * static_cast<size_t>(std::max(nc, 1)) + n1))
+    return fail(h, VS_ERR_CUDA, "pinned host allocation failed");
+  int* hs = h->pk_host.data();
+  std::memset(hs, 0, 16 * sizeof(int));
+  *reinterpret_cast<unsigned long long*>(hs + 8) = ~0ull;
+  for (int k = 0; k < nc; ++k)
+    reinterpret_cast<int4*>(hs + 16)[k] =
+        int4{classes[k].atom_lo, classes[k].atom_hi, classes[k].rot_lo, classes[k].rot_hi};
+  VS_CUDA(h, cudaMemcpyAsync(stats, hs, (16 + 4 * std::max(nc, 0)) * sizeof(int),
+                             cudaMemcpyHostToDevice, st));
+  PackIn in;
+  in.n = n;
+  in.total_atoms = A;
+  in.total_tors = T;
+  in.total_moving = M;
+  in.n_atoms = r[0].as<const int>();
+  in.n_tors = r[1].as<const int>();
+  in.rot_bonds = L->rot_bonds ? r[2].as<const int>() : nullptr;
+  in.coords = r[3].as<const double>();
+  in.atom_class = r[4].as<const int>();
+  in.axis_a = r[5].as<const int>();
+  in.axis_b = r[6].as<const int>();
+  in.moving_count = r[7].as<const int>();
+  in.moving = r[8].as<const int>();
+  in.seeds = L->seeds ? P.d_seeds.as<const unsigned long long>() : nullptr;
+  in.id_rank = L->id_rank ? P.d_idr.as<const unsigned>() : nullptr;
+  in.classes = dcls;
+  PackWork pw{w[0].as<long>(), w[1].as<long>(), w[2].as<long>(), w[3].as<long>(),
+              w[4].as<long>(), w[5].as<long>(), w[6].as<long>(), w[7].as<long>(),
+              w[8].as<int>(),  w[9].as<unsigned>(), w[10].as<unsigned>(), w[11].as<int>(),
+              stats, err};
+  PackDev out{P.d_meta.as<int4>(), P.d_mov.as<int2>(), P.d_atoms.as<double4>(),
+              P.d_axes.as<int4>(), P.d_moving.as<uint8_t>(), P.d_seeds.as<unsigned long long>(),
+              P.d_idr.as<unsigned>(), P.d_order.as<int>()};
+  VS_CUDA(h, pack_stage1(st, in, pw, classes ? nc : 0));
+  VS_CUDA(h, pack_stage2(st, in, pw, out, h->ptemp.p, tmp));
+  h->launches += 9;
+  VS_CUDA(h, cudaMemcpyAsync(hs, stats, 16 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  VS_CUDA(h, cudaMemcpyAsync(hs + 16 + 4 * std::max(nc, 1), pw.cls, n * 4ul,
+                             cudaMemcpyDeviceToHost, st));
+  VS_CUDA(h, cudaStreamSynchronize(st));
+  const unsigned long long ek = *reinterpret_cast<unsigned long long*>(hs + 8);
+  if (ek != ~0ull) {
+    const int code = static_cast<int>(ek & 0xff);
+    const long lig = static_cast<long>((ek >> 8) & 0xffffffffffull);
+    const std::string at = " (ligand " + std::to_string(lig) + ")";
+    if (code == kPkTopology) return fail(h, VS_ERR_ATOM_COUNT, "torsion topology does not fit conformer" + at);
+    if (code == kPkNotTree)
+      return fail(h, VS_ERR_INVALID_ARGUMENT, "ligand " + std::to_string(lig) + ": torsion topology is not a torsion tree");
+    if (code == kPkCapacity) return fail(h, VS_ERR_CAPACITY, "ligand exceeds GPU limits" + at);
+    return fail(h, VS_ERR_ATOM_COUNT, "invalid ligand counts" + at);
+  }
+  P.n = n;
+  P.total_atoms = A;
+  P.total_tors = T;
+  P.cls.assign(hs + 16 + 4 * std::max(nc, 1), hs + 16 + 4 * std::max(nc, 1) + n);
+  P.all = Bucket{};
+  P.all.start = 0;
+  P.all.count = hs[3];
+  P.all.nmax = std::max(P.all.nmax, hs[0]);
+  P.all.tmax = std::max(P.all.tmax, hs[1]);
+  P.all.mvmax = std::max(P.all.mvmax, hs[2]);
+  P.buckets.clear();
+  return VS_OK;
+}
+
+bool device_pack_enabled() {
+  const char* e = std::getenv("VSCREEN_HOST_PACK");
+  return !(e && e[0] == '1');
+}
+
+}  // namespace
+
+extern "C" {
+
 int vs_upload_library(vs_handle* h, const vs_library* L, const vs_size_class* classes,
                       int32_t nc) {
   cudaSetDevice(h->device);
@@ -937,6 +1095,15 @@ int vs_upload_library(vs_handle* h, const vs_library* L, const vs_size_class* cl
   h->has_results = false;
   using clk = std::chrono::steady_clock;
   const auto t0 = clk::now();
+  if (device_pack_enabled()) {  // the device packer (VSCREEN_HOST_PACK=1: the host one)
+    const int rc = gpu_pack(h, L, classes, nc, h->lib, h->own);
+    if (rc) return rc;
+    if (const char* e = std::getenv("VSCREEN_UPLOAD_TIMING"); e && e[0] == '1')
+      std::fprintf(stderr, "vs_upload_library: device pack (raw H2D + kernels) %.2f ms\n",
+                   std::chrono::duration<double, std::milli>(clk::now() - t0).count());
+    h->has_lib = true;
+    return VS_OK;
+  }
   // the pinned arrays' DMA runs under the bucketing and the torsion-tree
   // check; a failure drains it before returning (the next pack rewrites them)
   int rc = pack_library(h, L, classes, nc, h->lib, h->own);
@@ -1049,7 +1216,7 @@ int launch_packed(vs_handle* h, const Packed& P, const vs_dock_params* prm, cuda
   const size_t smem = stage_smem_per_block(b.nmax, b.tmax, b.mvmax);
   if (smem > 227 * 1024) return fail(h, VS_ERR_CAPACITY, "ligands need too much shared memory");
   const int R = prm->restarts;
-  VS_CUDA(h, sg.ensure(std::max<size_t>(1, P.atoms.size()),
+  VS_CUDA(h, sg.ensure(std::max<size_t>(1, static_cast<size_t>(P.total_atoms)),
                        static_cast<size_t>(std::max<long>(1, P.total_tors)),
                        static_cast<size_t>(std::max(P.n, 1)), static_cast<size_t>(R)));
   VS_CUDA(h, cudaMemsetAsync(sg.counters.p, 0, 320 * sizeof(int), st));
@@ -1488,10 +1655,12 @@ extern "C" {
 
 int vs_dock_host(vs_handle* h, const vs_library* L, const vs_size_class* classes, int32_t nc,
                  const vs_dock_params* prm, vs_results* out) {
-  // large libraries: the pipelined path (host pack / copy-out under the
-  // dock); VSCREEN_PIPELINE=0 forces the one-shot path
+  // VSCREEN_PIPELINE=1: large libraries as a pipeline of chunks (host pack
+  // / copy-out under the dock).  Off by default: with the device packer the
+  // one-shot path is faster (chunked docks lose more device efficiency than
+  // the overlap saves; profiles/e2e_pipeline_r2.txt)
   const char* pe = std::getenv("VSCREEN_PIPELINE");
-  if (L->n_ligands >= kPipeMinLigands && !(pe && pe[0] == '0')) {
+  if (L->n_ligands >= kPipeMinLigands && pe && pe[0] == '1') {
     cudaSetDevice(h->device);
     // chunk boundaries as fractions of the library (VSCREEN_PIPE_SPLIT,
     // comma-separated; VSCREEN_PIPE_CONCURRENT=0 runs them on one stream)

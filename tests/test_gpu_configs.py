@@ -223,6 +223,7 @@ def test_pipelined_dock_host_equals_one_shot(V, engine, monkeypatch):
                        min_score=-5.0, write_all_poses=True)
     engine.set_pocket(pocket, grid_spacing=0.4)
     classes = [(10, 30, 0, 11)]  # ligands with >= 30 atoms are dropped
+    monkeypatch.setenv("VSCREEN_PIPELINE", "1")
     a = engine.dock_host(lib, prm, classes=classes)
     top_a = engine.topk(500)
     again = engine.fetch()

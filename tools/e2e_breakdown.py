@@ -8,10 +8,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def main(n=100_000):
+def main(n=100_000, pinned=0):
     import bench
     import paper_2304_09953_b200 as V
     lib, _, _ = bench.build_workload(n, 0, 1, os.cpu_count() or 1)
+    if pinned:
+        bench.pin_library(lib)
     eng = V.Engine(0)
     eng.set_pocket(bench.make_pocket(), grid_spacing=0.4, grid_pad=2.0)
     prm = bench.params()
