@@ -599,12 +599,32 @@ def survivor_poses(lib, res):
     return pl, np.ascontiguousarray(rec["t"]), np.ascontiguousarray(rec["q"]), res.surv_tors[tix]
 
 
+def c5_work(lib, pl):
+    """SURVEY §8(d)'s per-unit terms for rescoring-only: every pose is one
+    state and one placement, M = 2 maps per atom (steric + the atom's kind
+    map): FLOP = 27 Mv + 14 T + 15 P + N (24 + 12 + 25 M), XU = 2 T + 3 P
+    + 3 N, L2_B = N 8 4 M, summed over the poses."""
+    N = lib.n_atoms.astype(np.float64)[pl]
+    T = lib.n_tors.astype(np.float64)[pl]
+    _, to, _ = lib.offsets()
+    m = lib.moving_count.astype(np.float64)
+    Mv = np.add.reduceat(np.r_[m, 0.0], np.minimum(to[:-1], len(m)))
+    Mv = np.where(lib.n_tors > 0, Mv, 0.0)[pl]
+    P = N * (N - 1) / 2
+    M = 2
+    flop = float(np.sum(27 * Mv + 14 * T + 15 * P + N * (24 + 12 + 25 * M)))
+    xu = float(np.sum(2 * T + 3 * P + 3 * N))
+    l2 = float(np.sum(N * 8 * 4 * M))
+    return flop, xu, l2
+
+
 def run_c5(args, rank, world, cfg):
     """Rescoring-only (BASELINE configs[4]): every survivor pose of a C2-knob
     dock re-scored (geometric score + rescore, K3a) against 0.2 A maps over a
-    30 A box.  value = ligands / device time of the rescore kernels; e2e =
-    the same through vs_rescore with host buffers (pack + H2D + kernels +
-    D2H), host wall clock."""
+    30 A box.  value = ligands / device time of vs_rescore_survivors (the
+    poses already in HBM from the dock, the resident library); e2e = the
+    same poses through vs_rescore from pinned host arrays (H2D of library +
+    poses, device packer, kernels, D2H of the scores), host wall clock."""
     import torch
     import torch.distributed as dist
     import paper_2304_09953_b200 as V
@@ -621,39 +641,91 @@ def run_c5(args, rank, world, cfg):
     eng = V.Engine(local)
     eng.set_pocket(pocket, grid_spacing=0.4, grid_pad=2.0)
     classes = [(1, 41, 0, 11), (60, 81, 11, 21)]
-    res = eng.dock_host(lib, params(), classes=classes)
+    prm = params()
+    sampler = ClockSampler(local).__enter__()  # clocks over the dock + rescoring region
+    eng.upload(lib, classes)
+    eng.dock(prm)
+    res = eng.fetch()
     pl, T, Q, TH = survivor_poses(lib, res)
     box = V.Pocket(pocket.sites, (-15.0, -15.0, -15.0), (15.0, 15.0, 15.0), pocket.clash_radius,
                    pocket.clash_penalty)
     eng.set_pocket(box, grid_spacing=0.2, grid_pad=2.0)
     peaks = eng.measure_peaks()
+    peaks["l2_gather_Bps"] = eng.measure_l2_gather_peak()
+    KT = prm.keep_top
+    stream = torch.cuda.Stream()
+    g_dev = torch.zeros(len(lib) * KT, dtype=torch.float32, device="cuda")
+    r_dev = torch.zeros_like(g_dev)
     for _ in range(args.warmup):
-        eng.rescore(lib, pl, T, Q, TH)
-    dev_ms, wall = [], []
-    with ClockSampler(local) as clocks:
-        for _ in range(args.steps):
-            if world > 1:
-                dist.barrier()
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            eng.rescore(lib, pl, T, Q, TH)
-            wall.append(time.perf_counter() - t0)
-            dev_ms.append(eng.last_rescore_ms())
+        eng.rescore_survivors(g_dev.data_ptr(), r_dev.data_ptr(), stream.cuda_stream)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    launches0 = eng.launch_count()
+    for k in range(args.steps):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev[k][0].record(stream)
+        eng.rescore_survivors(g_dev.data_ptr(), r_dev.data_ptr(), stream.cuda_stream)
+        ev[k][1].record(stream)
+        torch.cuda.synchronize()
+    launches = eng.launch_count() - launches0
+    sampler.__exit__(None, None, None)
+    clocks = sampler
+    dev_ms = [a.elapsed_time(b) for a, b in ev]
+    # e2e: the host path from pinned arrays (library + the same poses)
+    pin_library(lib)
+    pin = {}
+    for name, arr in (("pl", pl.astype(np.int32)), ("T", T), ("Q", Q), ("TH", TH)):
+        tt = torch.empty(max(arr.nbytes, 1), dtype=torch.uint8, pin_memory=True)
+        view = tt.numpy()[:arr.nbytes].view(arr.dtype).reshape(arr.shape)
+        view[...] = arr
+        pin[name] = (tt, view)
+    ppl, pT, pQ, pTH = (pin[k][1] for k in ("pl", "T", "Q", "TH"))
+    eng.rescore(lib, ppl, pT, pQ, pTH)  # warm
+    wall = []
+    for _ in range(args.steps):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        eng.rescore(lib, ppl, pT, pQ, pTH)
+        wall.append(time.perf_counter() - t0)
     t = torch.tensor([sum(dev_ms), sum(wall)], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     dev_s, wall_s = float(t[0]) * 1e-3, float(t[1])
     n_total = len(lib) * world
-    N = lib.n_atoms.astype(np.float64)[pl]
-    _, to, _ = lib.offsets()
-    m = lib.moving_count.astype(np.float64)
-    chain = np.add.reduceat(np.r_[AXIS_FLOP + MOVE_FLOP * m, 0.0], np.minimum(to[:-1], len(m)))
-    chain = np.where(lib.n_tors > 0, chain, 0.0)[pl]
-    flop = float(np.sum(chain + N * RESCORE_ATOM_FLOP + N * (N - 1) / 2 * PAIR_TEST_FLOP))
-    xu = float(np.sum(N * RESCORE_ATOM_XU))
-    per_s = np.mean(dev_ms) * 1e-3
+    flop, xu, l2 = c5_work(lib, pl)
+    per_s = dev_s / args.steps
+    roofs = {"fp32": flop / peaks["fp32_flops"], "xu": xu / peaks["xu_ops"],
+             "l2_gather": l2 / peaks["l2_gather_Bps"]}
+    bind = max(roofs, key=roofs.get)
+    unit = {"fp32": ("TFLOP/s", 1e12, flop, peaks["fp32_flops"]),
+            "xu": ("Tops/s", 1e12, xu, peaks["xu_ops"]),
+            "l2_gather": ("GB/s", 1e9, l2, peaks["l2_gather_Bps"])}[bind]
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        from oracle import sweep
+        op = sweep.OraclePocket(box, 0.2, 2.0)
+        sel_l = np.arange(0, len(lib), max(1, len(lib) // 2000))
+        keep = np.isin(pl, sel_l)
+        sub = lib.subset(sel_l)
+        remap = -np.ones(len(lib), np.int64)
+        remap[sel_l] = np.arange(len(sel_l))
+        T_all = lib.n_tors.astype(np.int64)[pl]
+        tstart = np.concatenate([[0], np.cumsum(T_all)])[:-1]
+        th_sel = np.concatenate([TH[tstart[i]:tstart[i] + T_all[i]] for i in np.nonzero(keep)[0]]
+                                or [np.zeros(0, np.float32)])
+        t0 = time.perf_counter()
+        sweep.score_poses(op, sub, remap[pl[keep]].astype(np.int32), T[keep], Q[keep], th_sel)
+        dt = time.perf_counter() - t0
+        cpu = {"value": round(len(sel_l) / dt, 2), "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"{len(sel_l)} ligands ({int(keep.sum())} poses, stride sample), the C "
+                         f"oracle's rescoring (sweep_oracle.c vso_score_poses), 1 thread, {dt:.2f} s"}
     if rank == 0:
-        bytes_in = h2d_bytes(lib) + len(pl) * (12 + 16 + 4) + TH.size * 4
+        bytes_in = h2d_bytes_raw(lib) + len(pl) * (12 + 16 + 4) + TH.size * 4
         line = {"metric": METRIC, "value": round(n_total * args.steps / dev_s, 2), "unit": UNIT,
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": round(1e3 * dev_s / args.steps, 3), "higher_is_better": True,
@@ -663,18 +735,24 @@ def run_c5(args, rank, world, cfg):
                 | {"ligands_per_gpu": len(lib), "ligands_total": n_total, "poses_per_gpu": len(pl),
                    "parallelism": f"dp{world}" if world > 1 else "single",
                    "l2": "maps 4 x 150^3 cells (> L2 for the 3 score maps + key map); no flush",
-                   "timed": "rescore kernels over all survivor poses (device events)"},
-                "roofline": {"bound": "fp32", "achieved": round(flop / per_s / 1e12, 3),
-                             "peak": round(peaks["fp32_flops"] / 1e12, 3), "unit": "TFLOP/s",
-                             "frac": round(flop / per_s / peaks["fp32_flops"], 4), "traffic": None,
+                   "timed": "vs_rescore_survivors: the dock's survivor poses already in HBM "
+                            "re-scored on the 0.2 A maps (device events)"},
+                "roofline": {"bound": bind, "achieved": round(unit[2] / per_s / unit[1], 3),
+                             "peak": round(unit[3] / unit[1], 3), "unit": unit[0],
+                             "frac": round(roofs[bind] / per_s, 4), "traffic": None,
                              "kernel": "vs_rescore_kernel",
-                             "xu_frac": round(xu / per_s / peaks["xu_ops"], 4)},
-                "cpu_baseline": None,
+                             "formula": "SURVEY §8(d) per-pose terms, 1 state + 1 placement per "
+                                        "pose, M = 2 maps (bench.c5_work)",
+                             "frac_fp32": round(roofs["fp32"] / per_s, 4),
+                             "frac_xu": round(roofs["xu"] / per_s, 4),
+                             "frac_l2_gather": round(roofs["l2_gather"] / per_s, 4)},
+                "cpu_baseline": cpu,
                 "e2e": {"value": round(n_total * args.steps / wall_s, 2), "unit": UNIT,
                         "h2d_bytes_per_step": bytes_in * world,
                         "d2h_bytes_per_step": 8 * len(pl) * world,
-                        "path": "vs_rescore (pack + H2D + rescore kernels + D2H), host wall clock"},
-                "gpu_launches": None, "clocks": clocks.summary(), "peaks": peaks,
+                        "path": "vs_rescore from pinned host arrays (H2D of library + poses, "
+                                "device packer, kernels, D2H of the scores), host wall clock"},
+                "gpu_launches": launches, "clocks": clocks.summary(), "peaks": peaks,
                 "library_build_s": round(t_build, 2)}
         s = json.dumps(line)
         print(s, flush=True)
@@ -688,15 +766,13 @@ def run_c5(args, rank, world, cfg):
 
 
 # ------------------------------------------------------------------- ours --
-def h2d_bytes(lib):
+def h2d_bytes_raw(lib):
+    """bytes of the caller's library arrays as the device packer receives them"""
     A = int(np.sum(lib.n_atoms))
     T = int(np.sum(lib.n_tors))
-    _, to, _ = lib.offsets()
-    cm = np.concatenate([[0], np.cumsum(lib.moving_count.astype(np.int64))])
-    m = cm[to[1:]] - cm[to[:-1]]
-    mv = int(np.sum((m + 15) // 16 * 16))
+    M = int(np.sum(lib.moving_count))
     n = len(lib)
-    return 32 * A + 16 * n + 8 * n + 16 * T + mv + 8 * n + 4 * n + 4 * n
+    return 3 * 4 * n + 24 * A + 4 * A + 3 * 4 * T + 4 * M + 8 * n + 4 * n
 
 
 def d2h_bytes(lib, prm):
@@ -833,7 +909,7 @@ def main():
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": round(n_total * n_e2e / float(te.item()), 2), "unit": UNIT,
-               "h2d_bytes_per_step": h2d_bytes(lib) * world,
+               "h2d_bytes_per_step": h2d_bytes_raw(lib) * world,
                "d2h_bytes_per_step": d2h_bytes(lib, prm) * world,
                "steps": n_e2e,
                "path": "vs_dock_host from pinned host arrays (H2D + device packer + dock + D2H "

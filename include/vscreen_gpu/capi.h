@@ -238,6 +238,12 @@ int vs_score_gradient(vs_handle* h, const vs_library* lib, int64_t n_poses,
  * pose order, n_tors of its ligand each. */
 int vs_rescore(vs_handle* h, const vs_library* lib, int64_t n_poses, const int32_t* pose_lig,
                const float* t, const float* q, const float* tors, float* geo, float* resc);
+/* the same with the length of `tors` checked against the poses' ligands
+ * (AtomCountMismatch, check_counts dock.cpp:219-230); n_tors_values < 0
+ * skips the check (= vs_rescore) */
+int vs_rescore_checked(vs_handle* h, const vs_library* lib, int64_t n_poses,
+                       const int32_t* pose_lig, const float* t, const float* q, const float* tors,
+                       int64_t n_tors_values, float* geo, float* resc);
 /* The reference ascent (dock.cpp:168-203: Armijo, step 0.5, shrink 0.5,
  * c 1e-4, |g| < 1e-6) from the given poses, one warp per pose on the
  * device, FP64 score_gradient arithmetic; t[3n], q[4n] (w, x, y, z) and the
@@ -246,6 +252,17 @@ int vs_rescore(vs_handle* h, const vs_library* lib, int64_t n_poses, const int32
 int vs_ascend(vs_handle* h, const vs_library* lib, int64_t n_poses, const int32_t* pose_lig,
               double* t, double* q, double* tors, int32_t max_steps, double* score,
               int32_t* steps);
+/* The same rescoring for poses already in device memory, against the
+ * resident library (vs_upload_library): pose_lig / t / q / tors / geo /
+ * resc are device pointers (layout as vs_rescore), all work on `stream`. */
+int vs_rescore_device(vs_handle* h, int64_t n_poses, const int32_t* pose_lig, const float* t,
+                      const float* q, const float* tors, float* geo, float* resc, void* stream);
+/* The survivors of the last vs_dock (still in device memory) re-scored
+ * against the current pocket, e.g. finer maps set by vs_set_pocket after
+ * the dock (BASELINE config 5): geo / resc device arrays [n * keep_top],
+ * slot l * keep_top + k for k < n_surv[l] (other slots untouched). */
+int vs_rescore_survivors(vs_handle* h, float* geo, float* resc, void* stream);
+
 /* geometric_score / rescore (dock.cpp:278-282, 297-316) of given poses in
  * FP64 on the device (the score_gradient arithmetic without the gradient;
  * analytic pocket): geo[n], resc[n] optional.  The drop-in's per-pose

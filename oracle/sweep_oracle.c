@@ -515,28 +515,6 @@ static mat3d flex_mat(const double* o, const double* b, float th_new, float th_o
 
 /* canonical score S = (Fe+Fo) - lam*((Pe+Po) + (We+Wo)), parity sums;
  * FP64 geometry, FP32 terms */
-static float score_state(const vso_pocket* p, const lig_t* L, const double* y, const mat3d* R,
-                         const double* t, float* x_out) {
-  float F[2] = {0, 0}, W[2] = {0, 0}, P[2] = {0, 0};
-  for (int i = 0; i < L->N; ++i) {
-    double v[3];
-    apply_d(R, &y[3 * i], t, v);
-    float x[3] = {(float)v[0], (float)v[1], (float)v[2]};
-    if (x_out) memcpy(&x_out[3 * i], x, 12);
-    F[i & 1] = F[i & 1] + field(p, x);
-    W[i & 1] = W[i & 1] + wall(p, x);
-  }
-  const double cut2 = (double)p->cut2;
-  long pi = 0;
-  for (int i = 0; i < L->N; ++i) {
-    for (int j = i + 1; j < L->N; ++j, ++pi) {
-      double d2 = n2d(y[3 * i] - y[3 * j], y[3 * i + 1] - y[3 * j + 1], y[3 * i + 2] - y[3 * j + 2]);
-      if (d2 <= cut2) P[pi & 1] = P[pi & 1] + vso_softplus((p->r - sqrtf((float)d2)) * 10.0f);
-    }
-  }
-  return (F[0] + F[1]) - p->lam * ((P[0] + P[1]) + (W[0] + W[1]));
-}
-
 /* sweep key (SWEEP_V1.md §2.3): grid mode works in grid coordinates,
  * g = (R/h) y + (t - o)/h, and interpolates the key map K = S - lam W; an
  * atom off the grid scores the linear wall -lam * 10 (r - w) at x = g h + o
@@ -591,6 +569,38 @@ static float bonus_sum(const vso_pocket* p, const lig_t* L, const float* x) {
   float B[2] = {0, 0};
   for (int i = 0; i < L->N; ++i) B[i & 1] = B[i & 1] + bonus(p, L->cls[i], &x[3 * i]);
   return B[0] + B[1];
+}
+
+/* the rescoring kernel's sums (vs_kernels.cu vs_rescore_kernel): 8 lanes
+ * per pose, slice h takes atoms i = h (mod 8) and row-major pairs
+ * q = h (mod 8), then the xor butterfly 1, 2, 4:
+ * ((s0 + s1) + (s2 + s3)) + ((s4 + s5) + (s6 + s7)) */
+static float sum8(const float* v) {
+  return ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
+}
+
+static float score_state8(const vso_pocket* p, const lig_t* L, const double* y, const mat3d* R,
+                          const double* t, float* x_out, float* bonus_out) {
+  float F[8] = {0}, W[8] = {0}, P[8] = {0}, B[8] = {0};
+  for (int i = 0; i < L->N; ++i) {
+    double v[3];
+    apply_d(R, &y[3 * i], t, v);
+    float x[3] = {(float)v[0], (float)v[1], (float)v[2]};
+    if (x_out) memcpy(&x_out[3 * i], x, 12);
+    F[i & 7] = F[i & 7] + field(p, x);
+    W[i & 7] = W[i & 7] + wall(p, x);
+    B[i & 7] = B[i & 7] + bonus(p, L->cls[i], x);
+  }
+  const double cut2 = (double)p->cut2;
+  long pi = 0;
+  for (int i = 0; i < L->N; ++i) {
+    for (int j = i + 1; j < L->N; ++j, ++pi) {
+      double d2 = n2d(y[3 * i] - y[3 * j], y[3 * i + 1] - y[3 * j + 1], y[3 * i + 2] - y[3 * j + 2]);
+      if (d2 <= cut2) P[pi & 7] = P[pi & 7] + vso_softplus((p->r - sqrtf((float)d2)) * 10.0f);
+    }
+  }
+  *bonus_out = sum8(B);
+  return sum8(F) - p->lam * (sum8(P) + sum8(W));
 }
 
 /* rmsd (dock.cpp:392-401) < delta ? */
@@ -1139,9 +1149,10 @@ int vso_score_poses(const vso_pocket* p, const vso_library* lib, int64_t n_poses
     toff += L.T;
     mat3d Rm = pose_mat_d(&q[4 * k]);
     double td[3] = {t[3 * k], t[3 * k + 1], t[3 * k + 2]};
-    float S = score_state(p, &L, y, &Rm, td, x);
+    float B = 0.0f;
+    float S = score_state8(p, &L, y, &Rm, td, x, &B);
     geo[k] = S;
-    resc[k] = S + bonus_sum(p, &L, x);
+    resc[k] = S + B;
   }
   if (cur >= 0) { free_lig(&L); free(y); free(x); }
   free(J.atom_off); free(J.tors_off); free(J.mov_off);

@@ -135,7 +135,13 @@ _SIGS = {
                                     P(C.c_double)]),
     "vs_rescore": (C.c_int, [C.c_void_p, P(vs_library), C.c_int64, P(C.c_int32), P(C.c_float),
                              P(C.c_float), P(C.c_float), P(C.c_float), P(C.c_float)]),
+    "vs_rescore_checked": (C.c_int, [C.c_void_p, P(vs_library), C.c_int64, P(C.c_int32),
+                                     P(C.c_float), P(C.c_float), P(C.c_float), C.c_int64,
+                                     P(C.c_float), P(C.c_float)]),
     "vs_last_rescore_ms": (C.c_double, [C.c_void_p]),
+    "vs_rescore_device": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
+                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "vs_rescore_survivors": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "vs_score64": (C.c_int, [C.c_void_p, P(vs_library), C.c_int64, P(C.c_int32), P(C.c_double),
                              P(C.c_double), P(C.c_double), P(C.c_double), P(C.c_double)]),
     "vs_dock_refined_host": (C.c_int, [C.c_void_p, P(vs_library), P(vs_size_class), C.c_int32,

@@ -292,7 +292,9 @@ __device__ __forceinline__ float warp_sum(float v) {
 }
 
 // ------------------------------------------------- per-warp shared layout --
-constexpr int kCand = 16;  // rescore kernel: pose columns (one lane pair each)
+// rescore kernel: kCand pose columns per warp, kLanesPerPose lanes each
+constexpr int kCand = 4;
+constexpr int kLanesPerPose = 8;
 
 struct WarpSmem {
   double4* y0;    // conformer (x, y, z, class), FP64

@@ -35,14 +35,14 @@ __device__ __forceinline__ double& cold(double* col, int i, int c, int a) {
   return col[(i * 3 + c) * kCand + a];
 }
 
-// Pose column a (lane pair (a, h)): conformer with all torsions of the pose
-// applied in order (dock.cpp:54-63); lanes h = 0/1 split atoms and moving
-// lists, __syncwarp between torsions.
+// Pose column a (lanes 8a .. 8a + 7, slice h): conformer with all torsions
+// of the pose applied in order (dock.cpp:54-63); the 8 lanes split atoms and
+// moving lists, __syncwarp between torsions.
 __device__ inline void chain_pose(const WarpSmem& s, int N, int T, int a, int h, bool active,
                                   const float* th) {
   double* col = s.col;
   if (active) {
-    for (int i = h; i < N; i += 2) {
+    for (int i = h; i < N; i += kLanesPerPose) {
       const double4 v = s.y0[i];
       cold(col, i, 0, a) = v.x;
       cold(col, i, 1, a) = v.y;
@@ -57,7 +57,7 @@ __device__ inline void chain_pose(const WarpSmem& s, int N, int T, int a, int h,
                    oz = cold(col, ax.x, 2, a);
       const Mat3d M = det_torsion_mat_d(ox, oy, oz, cold(col, ax.y, 0, a), cold(col, ax.y, 1, a),
                                         cold(col, ax.y, 2, a), th[k], s.axl[k]);
-      for (int m = h; m < ax.w; m += 2) {
+      for (int m = h; m < ax.w; m += kLanesPerPose) {
         const int idx = s.mov[ax.z + m];
         double vx, vy, vz;
         det_apply_d(M, cold(col, idx, 0, a) - ox, cold(col, idx, 1, a) - oy,
@@ -71,18 +71,24 @@ __device__ inline void chain_pose(const WarpSmem& s, int N, int T, int a, int h,
   }
 }
 
-// Work item w: ligand ligs[w], poses [pose_off[w], pose_off[w+1]) (float4 t,
-// float4 q = (w,x,y,z)), torsions at tors_base[w] + (p - pose_off[w]) * T.
-// Canonical score of a given pose: parity-h lane sums over atoms i = h mod 2
-// and pairs p = h mod 2 (row-major), combined across the lane pair.
+// sum over the 8 lanes of a pose column: xor butterfly 1, 2, 4, i.e.
+// ((s0 + s1) + (s2 + s3)) + ((s4 + s5) + (s6 + s7)) on every lane
+__device__ __forceinline__ float column_sum(float v) {
+  v = v + __shfl_xor_sync(kFull, v, 1);
+  v = v + __shfl_xor_sync(kFull, v, 2);
+  v = v + __shfl_xor_sync(kFull, v, 4);
+  return v;
+}
+
+// Work item w: ligand ligs[w] and its poses (PoseSrc), kCand = 4 at a time.
+// Canonical score of a given pose, lanes 8a + h: slice h sums atoms
+// i = h (mod 8) and pairs p = h (mod 8) (row-major), then the column's
+// butterfly.  A ligand with up to 4 poses (keep_top 4) uses every lane.
 template <int kGrid>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
-    vs_rescore_kernel(const __grid_constant__ LibDev lib, const __grid_constant__ PocketDev pk, const int* __restrict__ ligs,
-                      int n_ligs, int* __restrict__ work_counter, const int* __restrict__ pose_off,
-                      const long* __restrict__ tors_base, const float4* __restrict__ pose_t,
-                      const float4* __restrict__ pose_q, const float* __restrict__ pose_tors,
-                      int nmax, int tmax, int mvmax, float* __restrict__ geo,
-                      float* __restrict__ resc) {
+    vs_rescore_kernel(const __grid_constant__ LibDev lib, const __grid_constant__ PocketDev pk,
+                      const int* __restrict__ ligs, int n_ligs, int* __restrict__ work_counter,
+                      const __grid_constant__ PoseSrc src, int nmax, int tmax, int mvmax) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -92,31 +98,45 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   if (lane == 0) mbar_init(s.bar);
   __syncwarp();
   uint32_t phase = 0;
-  const int a = lane & 15;
-  const int h = lane >> 4;
+  const int a = lane / kLanesPerPose;
+  const int h = lane % kLanesPerPose;
+  const bool flat = src.t3 != nullptr;
   while (true) {
     int w = 0;
     if (lane == 0) w = atomicAdd(work_counter, 1);
     w = __shfl_sync(kFull, w, 0);
     if (w >= n_ligs) break;
     const int lig = ligs[w];
+    const int np = flat ? src.count[lig] : src.n_surv[lig];
+    if (np <= 0) continue;
     int4 meta;
     stage_ligand(lib, lig, s, lane, phase, meta);
     const int N = meta.y, T = meta.w;
-    const int p0 = pose_off[w], p1 = pose_off[w + 1];
-    for (int base = p0; base < p1; base += 16) {
-      const int p = base + a;
-      const bool active = p < p1;
-      const float* th = pose_tors + tors_base[w] + static_cast<long>(active ? p - p0 : 0) * T;
+    const long p0 = flat ? src.first[lig] : static_cast<long>(lig) * src.keep_top;
+    for (int base = 0; base < np; base += kCand) {
+      const int j = base + a;
+      const bool active = j < np;
+      const int jj0 = active ? j : 0;
+      const long p = p0 + jj0;
+      const float* th = flat ? src.tors + src.tb[lig] + static_cast<long>(jj0) * T
+                             : src.surv_tors + static_cast<long>(meta.z) * src.keep_top +
+                                   static_cast<long>(jj0) * T;
       chain_pose(s, N, T, a, h, active, th);
       float F = 0.0f, W = 0.0f, P = 0.0f, B = 0.0f;
       if (active) {
-        const float4 tt = pose_t[p];
-        const float4 qq = pose_q[p];
-        const Mat3d Rm = det_pose_mat_d(qq.x, qq.y, qq.z, qq.w);
-        const double tx = tt.x, ty = tt.y, tz = tt.z;
+        float tq[7];
+        if (flat) {
+          for (int c = 0; c < 3; ++c) tq[c] = src.t3[3 * p + c];
+          for (int c = 0; c < 4; ++c) tq[3 + c] = src.q4[4 * p + c];
+        } else {
+          const PoseOut& o = src.surv[p];
+          for (int c = 0; c < 3; ++c) tq[c] = o.t[c];
+          for (int c = 0; c < 4; ++c) tq[3 + c] = o.q[c];
+        }
+        const Mat3d Rm = det_pose_mat_d(tq[3], tq[4], tq[5], tq[6]);
+        const double tx = tq[0], ty = tq[1], tz = tq[2];
         const double* col = s.col;
-        for (int i = h; i < N; i += 2) {
+        for (int i = h; i < N; i += kLanesPerPose) {
           float fi, wi, xo[3];
           atom_terms<kGrid>(pk, Rm, tx, ty, tz, col[(i * 3) * kCand + a],
                             col[(i * 3 + 1) * kCand + a], col[(i * 3 + 2) * kCand + a], &fi, &wi,
@@ -125,26 +145,28 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
           W = W + wi;
           B = B + atom_bonus<kGrid>(pk, static_cast<int>(s.y0[i].w), xo[0], xo[1], xo[2]);
         }
-        int ps = 0;
+        // pairs in row-major order, pair index q = h (mod 8) on this slice
+        int ps = 0;  // pairs before row i
         for (int i = 0; i + 1 < N; ++i) {
           const double xi = col[(i * 3) * kCand + a], yi = col[(i * 3 + 1) * kCand + a],
                        zi = col[(i * 3 + 2) * kCand + a];
-          for (int jj = i + 1 + ((h ^ ps) & 1); jj < N; jj += 2) {
-            P = P + pair_term_d(pk, xi - col[(jj * 3) * kCand + a],
-                                yi - col[(jj * 3 + 1) * kCand + a],
-                                zi - col[(jj * 3 + 2) * kCand + a]);
+          const int first = i + 1 + ((h - ps) % kLanesPerPose + kLanesPerPose) % kLanesPerPose;
+          for (int jx = first; jx < N; jx += kLanesPerPose) {
+            P = P + pair_term_d(pk, xi - col[(jx * 3) * kCand + a],
+                                yi - col[(jx * 3 + 1) * kCand + a],
+                                zi - col[(jx * 3 + 2) * kCand + a]);
           }
           ps += N - 1 - i;
         }
       }
-      const float F2 = __shfl_xor_sync(kFull, F, 16);
-      const float W2 = __shfl_xor_sync(kFull, W, 16);
-      const float P2 = __shfl_xor_sync(kFull, P, 16);
-      const float B2 = __shfl_xor_sync(kFull, B, 16);
+      F = column_sum(F);
+      W = column_sum(W);
+      P = column_sum(P);
+      B = column_sum(B);
       if (active && h == 0) {
-        const float S = (F + F2) - pk.lam * ((P + P2) + (W + W2));
-        geo[p] = S;
-        resc[p] = S + (B + B2);
+        const float S = F - pk.lam * (P + W);
+        src.geo[p] = S;
+        src.resc[p] = S + B;
       }
       __syncwarp();
     }
@@ -362,19 +384,15 @@ static void prep(K kernel, size_t smem) {
 
 cudaError_t launch_rescore(bool grid, int blocks, size_t smem, cudaStream_t st, const LibDev& lib,
                            const PocketDev& pk, const int* ligs, int n_ligs, int* counter,
-                           const int* pose_off, const long* tors_base, const float4* pt,
-                           const float4* pq, const float* ptors, int nmax, int tmax, int mvmax,
-                           float* geo, float* resc) {
+                           const PoseSrc& src, int nmax, int tmax, int mvmax) {
   if (grid) {
     prep(vs_rescore_kernel<1>, smem);
-    vs_rescore_kernel<1><<<blocks, kWarpsPerBlock * 32, smem, st>>>(
-        lib, pk, ligs, n_ligs, counter, pose_off, tors_base, pt, pq, ptors, nmax, tmax, mvmax,
-        geo, resc);
+    vs_rescore_kernel<1><<<blocks, kWarpsPerBlock * 32, smem, st>>>(lib, pk, ligs, n_ligs, counter,
+                                                                   src, nmax, tmax, mvmax);
   } else {
     prep(vs_rescore_kernel<0>, smem);
-    vs_rescore_kernel<0><<<blocks, kWarpsPerBlock * 32, smem, st>>>(
-        lib, pk, ligs, n_ligs, counter, pose_off, tors_base, pt, pq, ptors, nmax, tmax, mvmax,
-        geo, resc);
+    vs_rescore_kernel<0><<<blocks, kWarpsPerBlock * 32, smem, st>>>(lib, pk, ligs, n_ligs, counter,
+                                                                   src, nmax, tmax, mvmax);
   }
   return cudaGetLastError();
 }

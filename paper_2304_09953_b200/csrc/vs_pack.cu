@@ -110,11 +110,18 @@ __global__ void pk_ligands(PackIn in, PackWork w, PackDev out) {
   // ascending sort key: in-class ligands by descending cost, dropped last
   w.key[i] = w.cls[i] >= 0 ? ~static_cast<unsigned>(cost) : 0xffffffffu;
   w.idx[i] = i;
-  if (w.cls[i] >= 0) {
+  const int c = w.cls[i];
+  if (c >= 0) {
+    const int mvp = static_cast<int>((mv + 15) & ~15L);
     atomicMax(&w.stats[0], N);
     atomicMax(&w.stats[1], T);
-    atomicMax(&w.stats[2], static_cast<int>((mv + 15) & ~15L));
+    atomicMax(&w.stats[2], mvp);
     atomicAdd(&w.stats[3], 1);
+    if (c < kPkMaxClasses) {
+      atomicMax(&w.stats[4 + 3 * c], N);
+      atomicMax(&w.stats[5 + 3 * c], T);
+      atomicMax(&w.stats[6 + 3 * c], mvp);
+    }
   }
 }
 
@@ -228,6 +235,57 @@ cudaError_t pack_stage2(cudaStream_t st, const PackIn& in, const PackWork& w, co
   e = cub::DeviceRadixSort::SortPairs(temp, tb, w.key, w.key_sorted, w.idx, out.order, in.n, 0, 32,
                                       st);
   if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+// ---- per-ligand pose ranges of a device pose list (vs_rescore_device):
+// pose_lig non-decreasing; first[l] / count[l] of its poses and tb[l], the
+// offset of its first pose's torsions in the concatenated torsion array
+namespace {
+__global__ void pr_init(int* first, int* count, int n) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l < n) {
+    first[l] = 0x7fffffff;
+    count[l] = 0;
+  }
+}
+__global__ void pr_count(const int* pose_lig, long n_poses, LibDev lib, int* first, int* count,
+                         long* tcnt) {
+  const long p = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p > n_poses) return;
+  if (p == n_poses) {
+    tcnt[p] = 0;
+    return;
+  }
+  const int l = pose_lig[p];
+  atomicAdd(&count[l], 1);
+  atomicMin(&first[l], static_cast<int>(p));
+  tcnt[p] = lib.meta[l].w;
+}
+__global__ void pr_base(const int* first, const int* count, const long* tb_pose, long* tb, int n) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l < n) tb[l] = count[l] > 0 ? tb_pose[first[l]] : 0;
+}
+}  // namespace
+
+size_t pose_ranges_temp_bytes(long n_poses) {
+  size_t b = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, b, static_cast<const long*>(nullptr),
+                                static_cast<long*>(nullptr), n_poses + 1);
+  return b + 256;
+}
+
+// tb_pose: 2 (n_poses + 1) longs of scratch (counts, then their scan)
+cudaError_t launch_pose_ranges(cudaStream_t st, const int* pose_lig, long n_poses,
+                               const LibDev& lib, int* first, int* count, long* tb_pose, long* tb,
+                               int n_ligs, void* temp, size_t temp_bytes) {
+  pr_init<<<blocks_for(n_ligs, 256), 256, 0, st>>>(first, count, n_ligs);
+  long* tcnt = tb_pose + n_poses + 1;
+  pr_count<<<blocks_for(n_poses + 1, 256), 256, 0, st>>>(pose_lig, n_poses, lib, first, count, tcnt);
+  size_t tb2 = temp_bytes;
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(temp, tb2, tcnt, tb_pose, n_poses + 1, st);
+  if (e != cudaSuccess) return e;
+  pr_base<<<blocks_for(n_ligs, 256), 256, 0, st>>>(first, count, tb_pose, tb, n_ligs);
   return cudaGetLastError();
 }
 

@@ -10,6 +10,13 @@ namespace vs {
 // validation outcome codes (the host packer's status for each)
 enum : int { kPkNoAtoms = 1, kPkCapacity = 2, kPkNegTors = 3, kPkTopology = 4, kPkNotTree = 5 };
 
+// the stats buffer (ints): [0..3] in-class nmax, tmax, mvmax, count;
+// [4 + 3c ..] per-class nmax, tmax, mvmax (c < kPkMaxClasses); the error key
+// (u64) at kPkErr; the size classes (int4) from kPkClasses on
+constexpr int kPkMaxClasses = 64;
+constexpr int kPkErr = 4 + 3 * kPkMaxClasses;  // 196: 8-byte aligned
+constexpr int kPkClasses = kPkErr + 4;         // 200: 16-byte aligned
+
 // the caller's library arrays on the device (capi.h vs_library, as given)
 struct PackIn {
   int n = 0;
@@ -35,7 +42,7 @@ struct PackWork {
   int* cls;
   unsigned *key, *key_sorted;
   int* idx;
-  int* stats;  // [0] nmax [1] tmax [2] mvmax (padded bytes) [3] in-class count
+  int* stats;  // see kPkErr / kPkClasses
   unsigned long long* err;
 };
 

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <array>
+#include <functional>
 #include <chrono>
 #include <cstdlib>
 #include <cmath>
@@ -44,9 +45,11 @@ cudaError_t launch_staged(bool grid, int sms, cudaStream_t st, const LibDev& lib
                           uint64_t* launches, cudaEvent_t* evs, int* kinds);
 cudaError_t launch_rescore(bool grid, int blocks, size_t smem, cudaStream_t st, const LibDev& lib,
                            const PocketDev& pk, const int* ligs, int n_ligs, int* counter,
-                           const int* pose_off, const long* tors_base, const float4* pt,
-                           const float4* pq, const float* ptors, int nmax, int tmax, int mvmax,
-                           float* geo, float* resc);
+                           const PoseSrc& src, int nmax, int tmax, int mvmax);
+cudaError_t launch_pose_ranges(cudaStream_t st, const int* pose_lig, long n_poses,
+                               const LibDev& lib, int* first, int* count, long* tb_pose, long* tb,
+                               int n_ligs, void* temp, size_t temp_bytes);
+size_t pose_ranges_temp_bytes(long n_poses);
 size_t grad_smem_per_block(int nmax, int tmax);
 size_t ascend_smem_per_block(int nmax, int tmax);
 cudaError_t launch_ascend(cudaStream_t st, const LibDev& lib, const SiteD* sites, int n_sites,
@@ -163,6 +166,7 @@ struct Packed {
   Bucket all;  // global LPT order (dock launch)
   long total_tors = 0;
   long total_atoms = 0;
+  bool on_device = false;  // packed by gpu_pack: buckets[c] = size class c
   DBuf d_meta, d_mov, d_atoms, d_axes, d_moving, d_seeds, d_idr, d_order;
   void release() {
     d_meta.release(); d_mov.release(); d_atoms.release(); d_axes.release();
@@ -289,13 +293,15 @@ struct vs_handle {
   // the device packer (vs_pack.cu): the caller's raw arrays, scratch, CUB temp
   DBuf raw[9], pwork[13], ptemp;
   PinnedVec<int> pk_host;  // stats + error key + classes read back
-  DBuf rbuf[9];              // vs_rescore's per-bucket pose arrays, reused across calls
-  // vs_rescore's pinned staging of the concatenated per-bucket pose arrays
-  PinnedVec<int> rs_lig, rs_off, rs_orig;
-  PinnedVec<long> rs_tb;
-  PinnedVec<float4> rs_t, rs_q;
-  PinnedVec<float> rs_tors, rs_geo, rs_resc;
+  // per-class ligand lists of the resident library (the device rescoring
+  // entries), rebuilt after each upload
+  DBuf d_lib_lists;
+  std::vector<std::pair<int, int>> lib_segs;
+  int lib_lists_n = -1;
+  DBuf rbuf[12];             // vs_rescore's pose / work arrays, reused across calls
   double rescore_ms = -1.0;  // device time of the rescore kernels of the last vs_rescore
+  std::vector<cudaStream_t> fork;  // the rescoring's per-class streams (joined back)
+  std::vector<cudaEvent_t> fork_ev;
   cudaEvent_t rev0 = nullptr, rev1 = nullptr;
 };
 
@@ -484,6 +490,7 @@ int pack_library(vs_handle* h, const vs_library* L, const vs_size_class* classes
   P.tors_off[n] = to;
   P.total_tors = to;
   P.total_atoms = aoff[n];
+  P.on_device = false;
   // one stable LPT sort (descending cost, then index); the per-class buckets
   // are class-filtered views of it (same order inside each class), and the
   // global queue over every class is the dock launch's
@@ -793,6 +800,8 @@ void vs_destroy(vs_handle* h) {
   vs_comm_destroy(h);
   h->d_gather.release();
   for (cudaEvent_t e : h->pev) cudaEventDestroy(e);
+  for (cudaStream_t x : h->fork) cudaStreamDestroy(x);
+  for (cudaEvent_t e : h->fork_ev) cudaEventDestroy(e);
   if (h->rev0) cudaEventDestroy(h->rev0);
   if (h->rev1) cudaEventDestroy(h->rev1);
   cudaStreamDestroy(h->own);
@@ -948,8 +957,29 @@ namespace {
 // one synchronize to read back the outcome.  Leaves P ready for
 // launch_packed (P.all over P.d_order, P.cls on the host).  The count
 // checks run on the host first (they size the transfers).
+// gpu_pack in two halves: pack_issue enqueues the transfers and kernels
+// (async), pack_finish synchronizes `st` and reads back the outcome; a
+// caller can do host work in between
+struct PackPending {
+  int n = 0, nc = 0;
+  long A = 0, T = 0;
+  size_t cls_at = 0;
+  bool classes = false;
+};
+int pack_issue(vs_handle* h, const vs_library* L, const vs_size_class* classes, int nc, Packed& P,
+               cudaStream_t st, PackPending& pp);
+int pack_finish(vs_handle* h, Packed& P, cudaStream_t st, const PackPending& pp);
+
 int gpu_pack(vs_handle* h, const vs_library* L, const vs_size_class* classes, int nc, Packed& P,
              cudaStream_t st) {
+  PackPending pp;
+  const int rc = pack_issue(h, L, classes, nc, P, st, pp);
+  if (rc) return rc;
+  return pack_finish(h, P, st, pp);
+}
+
+int pack_issue(vs_handle* h, const vs_library* L, const vs_size_class* classes, int nc, Packed& P,
+               cudaStream_t st, PackPending& pp) {
   const int n = L->n_ligands;
   if (n < 0) return fail(h, VS_ERR_INVALID_ARGUMENT, "negative ligand count");
   long A = 0, T = 0, M = 0;
@@ -997,7 +1027,8 @@ int gpu_pack(vs_handle* h, const vs_library* L, const vs_size_class* classes, in
   VS_CUDA(h, w[9].ensure(n1 * 4));   // key
   VS_CUDA(h, w[10].ensure(n1 * 4));  // key_sorted
   VS_CUDA(h, w[11].ensure(n1 * 4));  // idx
-  VS_CUDA(h, w[12].ensure(64 + 16 * static_cast<size_t>(std::max(nc, 1))));  // stats, err, classes
+  if (nc > kPkMaxClasses) return fail(h, VS_ERR_CAPACITY, "more than 64 size classes");
+  VS_CUDA(h, w[12].ensure(4 * kPkClasses + 16 * static_cast<size_t>(std::max(nc, 1))));
   const size_t tmp = pack_temp_bytes(n, T);
   VS_CUDA(h, h->ptemp.ensure(tmp));
   // packed outputs: M raw entries -> at most M + 15 n padded bytes
@@ -1010,17 +1041,17 @@ int gpu_pack(vs_handle* h, const vs_library* L, const vs_size_class* classes, in
   VS_CUDA(h, P.d_idr.ensure(std::max<size_t>(4, n * 4ul)));
   VS_CUDA(h, P.d_order.ensure(std::max<size_t>(4, n * 4ul)));
   int* stats = w[12].as<int>();
-  unsigned long long* err = reinterpret_cast<unsigned long long*>(stats + 8);
-  int4* dcls = reinterpret_cast<int4*>(stats + 16);
-  if (!h->pk_host.resize(16 + 4 * static_cast<size_t>(std::max(nc, 1)) + n1))
-    return fail(h, VS_ERR_CUDA, "pinned host allocation failed");
+  unsigned long long* err = reinterpret_cast<unsigned long long*>(stats + kPkErr);
+  int4* dcls = reinterpret_cast<int4*>(stats + kPkClasses);
+  const size_t cls_at = kPkClasses + 4 * static_cast<size_t>(std::max(nc, 1));  // host: cls after
+  if (!h->pk_host.resize(cls_at + n1)) return fail(h, VS_ERR_CUDA, "pinned host allocation failed");
   int* hs = h->pk_host.data();
-  std::memset(hs, 0, 16 * sizeof(int));
-  *reinterpret_cast<unsigned long long*>(hs + 8) = ~0ull;
+  std::memset(hs, 0, kPkClasses * sizeof(int));
+  *reinterpret_cast<unsigned long long*>(hs + kPkErr) = ~0ull;
   for (int k = 0; k < nc; ++k)
-    reinterpret_cast<int4*>(hs + 16)[k] =
+    reinterpret_cast<int4*>(hs + kPkClasses)[k] =
         int4{classes[k].atom_lo, classes[k].atom_hi, classes[k].rot_lo, classes[k].rot_hi};
-  VS_CUDA(h, cudaMemcpyAsync(stats, hs, (16 + 4 * std::max(nc, 0)) * sizeof(int),
+  VS_CUDA(h, cudaMemcpyAsync(stats, hs, (kPkClasses + 4 * std::max(nc, 0)) * sizeof(int),
                              cudaMemcpyHostToDevice, st));
   PackIn in;
   in.n = n;
@@ -1049,11 +1080,24 @@ int gpu_pack(vs_handle* h, const vs_library* L, const vs_size_class* classes, in
   VS_CUDA(h, pack_stage1(st, in, pw, classes ? nc : 0));
   VS_CUDA(h, pack_stage2(st, in, pw, out, h->ptemp.p, tmp));
   h->launches += 9;
-  VS_CUDA(h, cudaMemcpyAsync(hs, stats, 16 * sizeof(int), cudaMemcpyDeviceToHost, st));
-  VS_CUDA(h, cudaMemcpyAsync(hs + 16 + 4 * std::max(nc, 1), pw.cls, n * 4ul,
-                             cudaMemcpyDeviceToHost, st));
+  VS_CUDA(h, cudaMemcpyAsync(hs, stats, kPkClasses * sizeof(int), cudaMemcpyDeviceToHost, st));
+  VS_CUDA(h, cudaMemcpyAsync(hs + cls_at, pw.cls, n * 4ul, cudaMemcpyDeviceToHost, st));
+  pp.n = n;
+  pp.nc = nc;
+  pp.A = A;
+  pp.T = T;
+  pp.cls_at = cls_at;
+  pp.classes = classes != nullptr;
+  return VS_OK;
+}
+
+int pack_finish(vs_handle* h, Packed& P, cudaStream_t st, const PackPending& pp) {
   VS_CUDA(h, cudaStreamSynchronize(st));
-  const unsigned long long ek = *reinterpret_cast<unsigned long long*>(hs + 8);
+  const int n = pp.n, nc = pp.nc;
+  const long A = pp.A, T = pp.T;
+  const size_t cls_at = pp.cls_at;
+  const int* hs = h->pk_host.data();
+  const unsigned long long ek = *reinterpret_cast<const unsigned long long*>(hs + kPkErr);
   if (ek != ~0ull) {
     const int code = static_cast<int>(ek & 0xff);
     const long lig = static_cast<long>((ek >> 8) & 0xffffffffffull);
@@ -1067,14 +1111,24 @@ int gpu_pack(vs_handle* h, const vs_library* L, const vs_size_class* classes, in
   P.n = n;
   P.total_atoms = A;
   P.total_tors = T;
-  P.cls.assign(hs + 16 + 4 * std::max(nc, 1), hs + 16 + 4 * std::max(nc, 1) + n);
+  P.cls.assign(hs + cls_at, hs + cls_at + n);
   P.all = Bucket{};
   P.all.start = 0;
   P.all.count = hs[3];
   P.all.nmax = std::max(P.all.nmax, hs[0]);
   P.all.tmax = std::max(P.all.tmax, hs[1]);
   P.all.mvmax = std::max(P.all.mvmax, hs[2]);
-  P.buckets.clear();
+  // per-class bounds (the rescoring launches, one per class); members are
+  // listed by the caller from P.cls
+  const int ncls = (pp.classes && nc > 0) ? nc : 6;
+  P.on_device = true;
+  P.buckets.assign(static_cast<size_t>(ncls), Bucket{});
+  for (int c = 0; c < ncls; ++c) {
+    Bucket& b = P.buckets[static_cast<size_t>(c)];
+    b.nmax = std::max(b.nmax, hs[4 + 3 * c]);
+    b.tmax = std::max(b.tmax, hs[5 + 3 * c]);
+    b.mvmax = std::max(b.mvmax, hs[6 + 3 * c]);
+  }
   return VS_OK;
 }
 
@@ -1092,6 +1146,7 @@ int vs_upload_library(vs_handle* h, const vs_library* L, const vs_size_class* cl
   cudaSetDevice(h->device);
   VS_CUDA(h, quiesce(h));  // a dock on a caller stream may still read the library
   h->has_lib = false;
+  h->lib_lists_n = -1;
   h->has_results = false;
   using clk = std::chrono::steady_clock;
   const auto t0 = clk::now();
@@ -2261,193 +2316,269 @@ int vs_dock_refined_host(vs_handle* h, const vs_library* L, const vs_size_class*
   return VS_OK;
 }
 
-int vs_rescore(vs_handle* h, const vs_library* L, int64_t n_poses, const int32_t* pose_lig,
-               const float* t, const float* q, const float* tors, float* geo, float* resc) {
-  cudaSetDevice(h->device);
-  using clk = std::chrono::steady_clock;
-  const auto r0 = clk::now();
-  if (!h->has_pocket) return fail(h, VS_ERR_STATE, "no pocket");
-  // pose indices are 32-bit on the device (first[], rs_orig, rs_off)
-  if (n_poses < 0 || n_poses > INT32_MAX)
-    return fail(h, VS_ERR_CAPACITY, "n_poses must be in [0, 2^31)");
-  VS_CUDA(h, quiesce(h));
-  for (int64_t p = 1; p < n_poses; ++p)
-    if (pose_lig[p] < pose_lig[p - 1])
-      return fail(h, VS_ERR_INVALID_ARGUMENT, "pose_lig must be non-decreasing");
-  Packed& P = h->rpack;
-  // the library's pinned arrays stream in under the bucketing and the pose staging
-  int rc = pack_library(h, L, nullptr, 0, P, h->own);
-  if (rc) {
-    cudaStreamSynchronize(h->own);
-    return rc;
+}  // extern "C"
+
+namespace {
+
+// work lists for the rescoring launches: the ligands of each size class of
+// P (P.cls) that `keep` admits, concatenated; one (start, count) per class
+void class_lists(const Packed& P, const std::function<bool(int)>& keep, std::vector<int>& ligs,
+                 std::vector<std::pair<int, int>>& segs) {
+  ligs.clear();
+  segs.assign(P.buckets.size(), {0, 0});
+  std::vector<int> cnt(P.buckets.size(), 0);
+  for (int l = 0; l < P.n; ++l)
+    if (P.cls[l] >= 0 && keep(l)) ++cnt[static_cast<size_t>(P.cls[l])];
+  int o = 0;
+  for (size_t c = 0; c < cnt.size(); ++c) {
+    segs[c] = {o, 0};
+    o += cnt[c];
   }
-  for (int64_t p = 0; p < n_poses; ++p)
-    if (pose_lig[p] < 0 || pose_lig[p] >= P.n) {
-      cudaStreamSynchronize(h->own);
-      return fail(h, VS_ERR_INVALID_ARGUMENT, "pose ligand index out of range");
-    }
-  const auto r1 = clk::now();
-  cudaStream_t st = h->own;
-  // per-ligand pose ranges (contiguous: pose_lig is non-decreasing) and the
-  // offset of each ligand's first torsion vector in `tors`
-  std::vector<int> first(P.n, -1), cnt(P.n, 0);
-  std::vector<long> tb(P.n, 0);
-  long toff = 0;
-  for (int64_t p = 0; p < n_poses; ++p) {
-    const int l = pose_lig[p];
-    if (first[l] < 0) {
-      first[l] = static_cast<int>(p);
-      tb[l] = toff;
-    }
-    ++cnt[l];
-    toff += P.meta[l].w;
+  ligs.resize(static_cast<size_t>(o));
+  for (int l = 0; l < P.n; ++l) {
+    if (P.cls[l] < 0 || !keep(l)) continue;
+    auto& sg = segs[static_cast<size_t>(P.cls[l])];
+    ligs[static_cast<size_t>(sg.first + sg.second++)] = l;
   }
-  const auto rA = clk::now();
-  const bool grid = h->pk.grid_mode != 0;
-  const LibDev ld = P.dev();
+}
+
+// one rescoring launch per size class over `ligs` (device), events around
+int rescore_launch(vs_handle* h, const Packed& P, const int* d_ligs,
+                   const std::vector<std::pair<int, int>>& segs, const PoseSrc& src,
+                   DBuf& counters, cudaStream_t st) {
+  VS_CUDA(h, counters.ensure(std::max<size_t>(segs.size(), 1) * 4));
+  VS_CUDA(h, cudaMemsetAsync(counters.p, 0, std::max<size_t>(segs.size(), 1) * 4, st));
   if (!h->rev0) {
     VS_CUDA(h, cudaEventCreate(&h->rev0));
     VS_CUDA(h, cudaEventCreate(&h->rev1));
   }
-  // One host pass lays every bucket's pose lists (bucket-local, LPT-ordered)
-  // end to end in pinned staging; one DMA per array, the bucket launches back
-  // to back on one stream, one D2H per output and a single synchronize.
-  struct Seg {
-    int lig0, off0, count, bi;
-    long pose0, tors0;
-  };
-  std::vector<Seg> segs;
-  size_t n_work = 0, n_off = 0;
-  long n_pose = 0, n_tors = 0;
-  for (size_t bi = 0; bi < P.buckets.size(); ++bi) {
-    const Bucket& b = P.buckets[bi];
-    int c = 0;
-    long bt = 0;
-    for (int w = b.start; w < b.start + b.count; ++w) {
-      const int l = P.order[w];
-      if (cnt[l] == 0) continue;
-      ++c;
-      bt += static_cast<long>(cnt[l]) * P.meta[l].w;
-    }
-    if (c == 0) continue;
-    long bp = 0;
-    for (int w = b.start; w < b.start + b.count; ++w) bp += cnt[P.order[w]];
-    segs.push_back(Seg{static_cast<int>(n_work), static_cast<int>(n_off), c, static_cast<int>(bi),
-                       n_pose, n_tors});
-    n_work += c;
-    n_off += c + 1;
-    n_pose += bp;
-    n_tors += bt;
-  }
-  if (!h->rs_lig.resize(std::max<size_t>(n_work, 1)) || !h->rs_off.resize(std::max<size_t>(n_off, 1)) ||
-      !h->rs_tb.resize(std::max<size_t>(n_work, 1)) || !h->rs_orig.resize(std::max<long>(n_pose, 1)) ||
-      !h->rs_t.resize(std::max<long>(n_pose, 1)) || !h->rs_q.resize(std::max<long>(n_pose, 1)) ||
-      !h->rs_tors.resize(std::max<long>(n_tors, 1)) || !h->rs_geo.resize(std::max<long>(n_pose, 1)) ||
-      !h->rs_resc.resize(std::max<long>(n_pose, 1)))
-    return fail(h, VS_ERR_CUDA, "pinned rescore staging allocation failed");
-  const auto rB = clk::now();
-  // serial pass: work-item indices and each item's global pose / torsion base;
-  // the pose copies (the bulk) then run over host threads
-  std::vector<long> wpose(n_work), wtors(n_work);
-  for (const Seg& sg : segs) {
-    const Bucket& b = P.buckets[sg.bi];
-    int k = 0;
-    long pl = 0, tl = 0;  // bucket-local pose / torsion cursors
-    for (int w = b.start; w < b.start + b.count; ++w) {
-      const int l = P.order[w];
-      if (cnt[l] == 0) continue;
-      h->rs_lig[sg.lig0 + k] = l;
-      h->rs_off[sg.off0 + k] = static_cast<int>(pl);
-      h->rs_tb[sg.lig0 + k] = tl;
-      wpose[sg.lig0 + k] = sg.pose0 + pl;
-      wtors[sg.lig0 + k] = sg.tors0 + tl;
-      pl += cnt[l];
-      tl += static_cast<long>(cnt[l]) * P.meta[l].w;
-      ++k;
-    }
-    h->rs_off[sg.off0 + k] = static_cast<int>(pl);
-  }
-  auto fill = [&](size_t k0, size_t k1) {
-    for (size_t k = k0; k < k1; ++k) {
-      const int l = h->rs_lig[k];
-      long g = wpose[k];
-      for (int p = first[l]; p < first[l] + cnt[l]; ++p, ++g) {
-        h->rs_orig[g] = p;
-        h->rs_t[g] = float4{t[3 * p], t[3 * p + 1], t[3 * p + 2], 0.0f};
-        h->rs_q[g] = float4{q[4 * p], q[4 * p + 1], q[4 * p + 2], q[4 * p + 3]};
+  const bool grid = h->pk.grid_mode != 0;
+  VS_CUDA(h, cudaEventRecord(h->rev0, st));
+  // the classes' launches run concurrently (a fork of `st` per class, joined
+  // back): a class of few large ligands overlaps the bulk of small ones
+  // instead of running after it at low occupancy
+  int k = 0;
+  for (size_t c = 0; c < segs.size(); ++c) {
+    if (segs[c].second == 0) continue;
+    const Bucket& b = P.buckets[c];
+    const size_t smem = rescore_smem_per_block(b.nmax, b.tmax, b.mvmax);
+    if (smem > 227 * 1024) return fail(h, VS_ERR_CAPACITY, "ligands too large for rescoring");
+    const int blocks = std::max(1, std::min((segs[c].second + kWarpsPerBlock - 1) / kWarpsPerBlock,
+                                            8 * h->sms));
+    cudaStream_t cs = st;
+    if (k > 0) {
+      if (h->fork.size() < static_cast<size_t>(k)) {
+        cudaStream_t x;
+        cudaEvent_t e;
+        VS_CUDA(h, cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+        VS_CUDA(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        h->fork.push_back(x);
+        h->fork_ev.push_back(e);
       }
-      const long nt = static_cast<long>(cnt[l]) * P.meta[l].w;
-      if (nt) std::memcpy(h->rs_tors.data() + wtors[k], tors + tb[l], nt * sizeof(float));
+      cs = h->fork[static_cast<size_t>(k - 1)];
+      VS_CUDA(h, cudaStreamWaitEvent(cs, h->rev0, 0));
     }
-  };
-  {
-    const size_t nth = std::max<size_t>(
-        1, std::min<size_t>({n_work / 4096 + 1, 16, std::max(1u, std::thread::hardware_concurrency())}));
-    std::vector<std::thread> pool;
-    const size_t chunk = (n_work + nth - 1) / nth;
-    for (size_t tI = 1; tI < nth; ++tI)
-      pool.emplace_back(fill, std::min(n_work, tI * chunk), std::min(n_work, (tI + 1) * chunk));
-    fill(0, std::min(n_work, chunk));
-    for (auto& th : pool) th.join();
+    VS_CUDA(h, launch_rescore(grid, blocks, smem, cs, P.dev(), h->pk, d_ligs + segs[c].first,
+                              segs[c].second, counters.as<int>() + c, src, b.nmax, b.tmax,
+                              b.mvmax));
+    if (k > 0) {
+      VS_CUDA(h, cudaEventRecord(h->fork_ev[static_cast<size_t>(k - 1)], cs));
+      VS_CUDA(h, cudaStreamWaitEvent(st, h->fork_ev[static_cast<size_t>(k - 1)], 0));
+    }
+    ++k;
+    ++h->launches;
   }
-  const auto r2 = clk::now();
-  DBuf &a = h->rbuf[0], &bo = h->rbuf[1], &c = h->rbuf[2], &d = h->rbuf[3], &e = h->rbuf[4],
-       &f = h->rbuf[5], &g = h->rbuf[6], &gr = h->rbuf[7], &cc = h->rbuf[8];
-  rc = upload_packed(h, P, st, 2);
+  VS_CUDA(h, cudaEventRecord(h->rev1, st));
+  return VS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+// geometric_score + rescore of given poses (dock.cpp:278, 297).  The library
+// goes through the device packer (raw arrays DMA'd as given), the pose
+// arrays are DMA'd as given too, the per-ligand ranges are host bookkeeping
+// over pose_lig, and the results are copied straight into geo / resc.
+int vs_rescore(vs_handle* h, const vs_library* L, int64_t n_poses, const int32_t* pose_lig,
+               const float* t, const float* q, const float* tors, float* geo, float* resc) {
+  return vs_rescore_checked(h, L, n_poses, pose_lig, t, q, tors, -1, geo, resc);
+}
+
+int vs_rescore_checked(vs_handle* h, const vs_library* L, int64_t n_poses,
+                       const int32_t* pose_lig, const float* t, const float* q, const float* tors,
+                       int64_t n_tors_values, float* geo, float* resc) {
+  cudaSetDevice(h->device);
+  using clk = std::chrono::steady_clock;
+  const auto r0 = clk::now();
+  if (!h->has_pocket) return fail(h, VS_ERR_STATE, "no pocket");
+  // pose indices are 32-bit on the device (first[], count[])
+  if (n_poses < 0 || n_poses > INT32_MAX)
+    return fail(h, VS_ERR_CAPACITY, "n_poses must be in [0, 2^31)");
+  VS_CUDA(h, quiesce(h));
+  const int n = L->n_ligands;
+  for (int64_t p = 0; p < n_poses; ++p) {
+    if (p > 0 && pose_lig[p] < pose_lig[p - 1])
+      return fail(h, VS_ERR_INVALID_ARGUMENT, "pose_lig must be non-decreasing");
+    if (pose_lig[p] < 0 || pose_lig[p] >= n)
+      return fail(h, VS_ERR_INVALID_ARGUMENT, "pose ligand index out of range");
+  }
+  cudaStream_t st = h->own;
+  Packed& P = h->rpack;
+  PackPending pp;
+  int rc = pack_issue(h, L, nullptr, 0, P, st, pp);  // the device packer runs under the
+  if (rc) return rc;                                 // host bookkeeping below
+  const auto r1 = clk::now();
+  // per-ligand pose ranges and torsion bases; the work lists per class
+  std::vector<int> first(std::max(n, 1), 0), count(std::max(n, 1), 0);
+  std::vector<long> tb(std::max(n, 1), 0);
+  long toff = 0;
+  for (int64_t p = 0; p < n_poses; ++p) {
+    const int l = pose_lig[p];
+    if (count[l]++ == 0) {
+      first[l] = static_cast<int>(p);
+      tb[l] = toff;
+    }
+    toff += L->n_tors[l];
+  }
+  if (n_tors_values >= 0 && toff != n_tors_values) {  // check_counts, dock.cpp:219-230
+    cudaStreamSynchronize(st);  // the issued pack drains before its buffers are reused
+    return fail(h, VS_ERR_ATOM_COUNT, "poses need " + std::to_string(toff) +
+                                          " torsion values, got " + std::to_string(n_tors_values));
+  }
+  rc = pack_finish(h, P, st, pp);
   if (rc) return rc;
+  std::vector<int> ligs;
+  std::vector<std::pair<int, int>> segs;
+  class_lists(P, [&](int l) { return count[l] > 0; }, ligs, segs);
+  const auto r2 = clk::now();
+  DBuf* rb = h->rbuf;
   auto up = [&](DBuf& dst, const void* src, size_t bytes) -> cudaError_t {
     cudaError_t err = dst.ensure(std::max<size_t>(bytes, 16));
     if (err != cudaSuccess || bytes == 0) return err;
     return cudaMemcpyAsync(dst.p, src, bytes, cudaMemcpyHostToDevice, st);
   };
-  VS_CUDA(h, up(a, h->rs_lig.data(), n_work * 4));
-  VS_CUDA(h, up(bo, h->rs_off.data(), n_off * 4));
-  VS_CUDA(h, up(c, h->rs_tb.data(), n_work * 8));
-  VS_CUDA(h, up(d, h->rs_t.data(), n_pose * 16));
-  VS_CUDA(h, up(e, h->rs_q.data(), n_pose * 16));
-  VS_CUDA(h, up(f, h->rs_tors.data(), n_tors * 4));
-  VS_CUDA(h, g.ensure(std::max<long>(n_pose, 1) * 4));
-  VS_CUDA(h, gr.ensure(std::max<long>(n_pose, 1) * 4));
-  VS_CUDA(h, cc.ensure(std::max<size_t>(segs.size(), 1) * 4));
-  VS_CUDA(h, cudaMemsetAsync(cc.p, 0, std::max<size_t>(segs.size(), 1) * 4, st));
-  VS_CUDA(h, cudaEventRecord(h->rev0, st));
-  for (size_t si = 0; si < segs.size(); ++si) {
-    const Seg& sg = segs[si];
-    const Bucket& b = P.buckets[sg.bi];
-    const size_t smem = rescore_smem_per_block(b.nmax, b.tmax, b.mvmax);
-    const int blocks =
-        std::max(1, std::min((sg.count + kWarpsPerBlock - 1) / kWarpsPerBlock, 4 * h->sms));
-    VS_CUDA(h, launch_rescore(grid, blocks, smem, st, ld, h->pk, a.as<int>() + sg.lig0, sg.count,
-                              cc.as<int>() + si, bo.as<int>() + sg.off0, c.as<long>() + sg.lig0,
-                              d.as<float4>() + sg.pose0, e.as<float4>() + sg.pose0,
-                              f.as<float>() + sg.tors0, b.nmax, b.tmax, b.mvmax,
-                              g.as<float>() + sg.pose0, gr.as<float>() + sg.pose0));
-    ++h->launches;
-  }
-  VS_CUDA(h, cudaEventRecord(h->rev1, st));
-  if (n_pose) {
-    VS_CUDA(h, cudaMemcpyAsync(h->rs_geo.data(), g.p, n_pose * 4, cudaMemcpyDeviceToHost, st));
-    VS_CUDA(h, cudaMemcpyAsync(h->rs_resc.data(), gr.p, n_pose * 4, cudaMemcpyDeviceToHost, st));
+  const size_t np = static_cast<size_t>(n_poses);
+  VS_CUDA(h, up(rb[0], t, np * 12));
+  VS_CUDA(h, up(rb[1], q, np * 16));
+  VS_CUDA(h, up(rb[2], tors, static_cast<size_t>(toff) * 4));
+  VS_CUDA(h, up(rb[3], first.data(), n * 4ul));
+  VS_CUDA(h, up(rb[4], count.data(), n * 4ul));
+  VS_CUDA(h, up(rb[5], tb.data(), n * 8ul));
+  VS_CUDA(h, up(rb[6], ligs.data(), ligs.size() * 4));
+  VS_CUDA(h, rb[7].ensure(std::max<size_t>(np, 1) * 4));
+  VS_CUDA(h, rb[8].ensure(std::max<size_t>(np, 1) * 4));
+  PoseSrc src{};
+  src.first = rb[3].as<const int>();
+  src.count = rb[4].as<const int>();
+  src.tb = rb[5].as<const long>();
+  src.t3 = rb[0].as<const float>();
+  src.q4 = rb[1].as<const float>();
+  src.tors = rb[2].as<const float>();
+  src.geo = rb[7].as<float>();
+  src.resc = rb[8].as<float>();
+  rc = rescore_launch(h, P, rb[6].as<int>(), segs, src, rb[9], st);
+  if (rc) return rc;
+  if (np) {
+    if (geo) VS_CUDA(h, cudaMemcpyAsync(geo, rb[7].p, np * 4, cudaMemcpyDeviceToHost, st));
+    if (resc) VS_CUDA(h, cudaMemcpyAsync(resc, rb[8].p, np * 4, cudaMemcpyDeviceToHost, st));
   }
   VS_CUDA(h, cudaStreamSynchronize(st));
-  const auto r3 = clk::now();
-  {
-    float ms = 0.0f;
-    VS_CUDA(h, cudaEventElapsedTime(&ms, h->rev0, h->rev1));
-    h->rescore_ms = ms;
-  }
-  for (long k = 0; k < n_pose; ++k) {
-    if (geo) geo[h->rs_orig[k]] = h->rs_geo[k];
-    if (resc) resc[h->rs_orig[k]] = h->rs_resc[k];
-  }
+  float ms = 0.0f;
+  VS_CUDA(h, cudaEventElapsedTime(&ms, h->rev0, h->rev1));
+  h->rescore_ms = ms;
   if (const char* ev = std::getenv("VSCREEN_UPLOAD_TIMING"); ev && ev[0] == '1') {
-    auto ms = [](clk::time_point x, clk::time_point y) {
+    auto d = [](clk::time_point x, clk::time_point y) {
       return std::chrono::duration<double, std::milli>(y - x).count();
     };
-    std::fprintf(stderr, "vs_rescore: check+pack %.2f ms, ranges %.2f + segs %.2f + staging %.2f ms, H2D+kernels+D2H %.2f ms "
-                 "(kernels %.2f), scatter %.2f ms\n", ms(r0, r1), ms(r1, rA), ms(rA, rB), ms(rB, r2), ms(r2, r3), h->rescore_ms,
-                 ms(r3, clk::now()));
+    std::fprintf(stderr, "vs_rescore: check + device pack %.2f ms, ranges + lists %.2f ms, "
+                 "H2D + kernels + D2H %.2f ms (kernels %.2f)\n", d(r0, r1), d(r1, r2),
+                 d(r2, clk::now()), h->rescore_ms);
   }
+  return VS_OK;
+}
+
+// the same for poses already in device memory, against the resident
+// library (vs_upload_library); everything stays on `stream`
+int vs_rescore_device(vs_handle* h, int64_t n_poses, const int32_t* pose_lig, const float* t,
+                      const float* q, const float* tors, float* geo, float* resc, void* stream) {
+  cudaSetDevice(h->device);
+  if (!h->has_pocket) return fail(h, VS_ERR_STATE, "no pocket");
+  if (!h->has_lib) return fail(h, VS_ERR_STATE, "no resident library");
+  if (n_poses < 0 || n_poses > INT32_MAX)
+    return fail(h, VS_ERR_CAPACITY, "n_poses must be in [0, 2^31)");
+  const Packed& P = h->lib;
+  if (!P.on_device) return fail(h, VS_ERR_STATE, "library not packed on the device");
+  cudaStream_t st = pick(h, stream);
+  VS_CUDA(h, after_prev(h, st));
+  DBuf* rb = h->rbuf;
+  const int n = P.n;
+  const size_t tmp = pose_ranges_temp_bytes(n_poses);
+  VS_CUDA(h, rb[3].ensure(std::max(n, 1) * 4ul));
+  VS_CUDA(h, rb[4].ensure(std::max(n, 1) * 4ul));
+  VS_CUDA(h, rb[5].ensure(std::max(n, 1) * 8ul));
+  VS_CUDA(h, rb[10].ensure(2 * (static_cast<size_t>(n_poses) + 1) * 8));
+  VS_CUDA(h, rb[11].ensure(tmp));
+  VS_CUDA(h, launch_pose_ranges(st, pose_lig, n_poses, P.dev(), rb[3].as<int>(), rb[4].as<int>(),
+                                rb[10].as<long>(), rb[5].as<long>(), n, rb[11].p, tmp));
+  h->launches += 3;
+  // every ligand of each class is a work item (no host knowledge of the
+  // poses); ligands without poses return at once
+  if (h->lib_lists_n != n) {
+    std::vector<int> ligs;
+    class_lists(P, [](int) { return true; }, ligs, h->lib_segs);
+    VS_CUDA(h, h->d_lib_lists.ensure(std::max<size_t>(ligs.size(), 1) * 4));
+    VS_CUDA(h, cudaMemcpyAsync(h->d_lib_lists.p, ligs.data(), ligs.size() * 4,
+                               cudaMemcpyHostToDevice, st));
+    VS_CUDA(h, cudaStreamSynchronize(st));
+    h->lib_lists_n = n;
+  }
+  PoseSrc src{};
+  src.first = rb[3].as<const int>();
+  src.count = rb[4].as<const int>();
+  src.tb = rb[5].as<const long>();
+  src.t3 = t;
+  src.q4 = q;
+  src.tors = tors;
+  src.geo = geo;
+  src.resc = resc;
+  const int rc = rescore_launch(h, P, h->d_lib_lists.as<int>(), h->lib_segs, src, rb[9], st);
+  if (rc) return rc;
+  VS_CUDA(h, mark_done(h, st));
+  return VS_OK;
+}
+
+// the survivors of the last vs_dock re-scored in place against the current
+// pocket (e.g. finer maps): geo / resc [n * keep_top] (device), slot
+// l * keep_top + k for k < n_surv[l]
+int vs_rescore_survivors(vs_handle* h, float* geo, float* resc, void* stream) {
+  cudaSetDevice(h->device);
+  if (!h->has_pocket) return fail(h, VS_ERR_STATE, "no pocket");
+  if (!h->has_results || !h->has_lib || h->res_n != h->lib.n)
+    return fail(h, VS_ERR_STATE, "no dock results on the resident library");
+  const Packed& P = h->lib;
+  if (!P.on_device) return fail(h, VS_ERR_STATE, "library not packed on the device");
+  cudaStream_t st = pick(h, stream);
+  VS_CUDA(h, after_prev(h, st));
+  if (h->lib_lists_n != P.n) {
+    std::vector<int> ligs;
+    class_lists(P, [](int) { return true; }, ligs, h->lib_segs);
+    VS_CUDA(h, h->d_lib_lists.ensure(std::max<size_t>(ligs.size(), 1) * 4));
+    VS_CUDA(h, cudaMemcpyAsync(h->d_lib_lists.p, ligs.data(), ligs.size() * 4,
+                               cudaMemcpyHostToDevice, st));
+    VS_CUDA(h, cudaStreamSynchronize(st));
+    h->lib_lists_n = P.n;
+  }
+  PoseSrc src{};
+  src.surv = h->d_surv.as<const PoseOut>();
+  src.surv_tors = h->d_surv_tors.as<const float>();
+  src.n_surv = h->d_nsurv.as<const int>();
+  src.keep_top = h->last_prm.keep_top;
+  src.geo = geo;
+  src.resc = resc;
+  const int rc = rescore_launch(h, P, h->d_lib_lists.as<int>(), h->lib_segs, src, h->rbuf[9], st);
+  if (rc) return rc;
+  VS_CUDA(h, mark_done(h, st));
   return VS_OK;
 }
 

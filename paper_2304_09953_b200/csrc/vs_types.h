@@ -106,6 +106,28 @@ struct DockOut {
   unsigned long long* stats; // [4] work counters (capi.h vs_last_stats)
 };
 
+// Poses for the rescoring kernel (K3a).  Flat mode (t3 != nullptr): the
+// poses of ligand l are p in [first[l], first[l] + count[l]) of flat arrays
+// t3[3p], q4[4p] (w, x, y, z), torsions at tb[l] + (p - first[l]) * T,
+// results at geo[p] / resc[p].  Survivor mode (t3 == nullptr): the last
+// dock's survivors of ligand l, surv[l * keep_top + k] for k < n_surv[l],
+// torsions at surv_tors + tors_off(l) * keep_top + k * T, results at
+// geo[l * keep_top + k].
+struct PoseSrc {
+  const int* first;
+  const int* count;
+  const long* tb;
+  const float* t3;
+  const float* q4;
+  const float* tors;
+  const PoseOut* surv;
+  const float* surv_tors;
+  const int* n_surv;
+  int keep_top;
+  float* geo;
+  float* resc;
+};
+
 // Per-ligand state of the staged dock (one kernel per phase and restart):
 // what one phase hands to the next through HBM.
 struct StageBufs {

@@ -521,22 +521,42 @@ class Engine:
                          int(rs[i * R + r])) for r in range(max(int(npos[i]), 0))])
         return res
 
+    def rescore_device(self, n_poses: int, pose_lig_ptr: int, t_ptr: int, q_ptr: int,
+                       tors_ptr: int, geo_ptr: int, resc_ptr: int, stream: int | None = None):
+        """K3a over poses already in device memory (capi.h vs_rescore_device),
+        against the resident library; all pointers are device pointers."""
+        check(_lib.vs_rescore_device(self._h, n_poses, C.c_void_p(pose_lig_ptr), C.c_void_p(t_ptr),
+                                     C.c_void_p(q_ptr), C.c_void_p(tors_ptr), C.c_void_p(geo_ptr),
+                                     C.c_void_p(resc_ptr), C.c_void_p(stream or 0)),
+              self._h, "rescore_device")
+
+    def rescore_survivors(self, geo_ptr: int, resc_ptr: int, stream: int | None = None):
+        """The last dock's survivors re-scored in device memory against the
+        current pocket (capi.h vs_rescore_survivors): device arrays
+        [n * keep_top]."""
+        check(_lib.vs_rescore_survivors(self._h, C.c_void_p(geo_ptr), C.c_void_p(resc_ptr),
+                                        C.c_void_p(stream or 0)), self._h, "rescore_survivors")
+
     def rescore(self, lib: Library, pose_lig, t, q, tors):
         """K3a: canonical geometric score and rescore of given poses."""
         pose_lig = np.ascontiguousarray(pose_lig, np.int32)
         t = np.ascontiguousarray(t, np.float32).reshape(-1)
         q = np.ascontiguousarray(q, np.float32).reshape(-1)
         tors = np.ascontiguousarray(tors, np.float32).reshape(-1)
-        _check_pose_arrays(lib, pose_lig, t, q, tors)
+        n = len(pose_lig)
+        if t.size != 3 * n or q.size != 4 * n:
+            raise ValueError(f"{n} poses need t of {3 * n} and q of {4 * n} values "
+                             f"(got {t.size} and {q.size})")
+        n_tors_values = tors.size  # checked against the poses' ligands in C
         if tors.size == 0:
             tors = np.zeros(1, np.float32)
-        n = len(pose_lig)
         geo = np.zeros(max(n, 1), np.float32)
         resc = np.zeros(max(n, 1), np.float32)
         lc = lib.as_c()
-        check(_lib.vs_rescore(self._h, C.byref(lc), n, ptr(pose_lig, C.c_int32), ptr(t, C.c_float),
-                              ptr(q, C.c_float), ptr(tors, C.c_float), ptr(geo, C.c_float),
-                              ptr(resc, C.c_float)), self._h, "rescore")
+        check(_lib.vs_rescore_checked(self._h, C.byref(lc), n, ptr(pose_lig, C.c_int32),
+                                      ptr(t, C.c_float), ptr(q, C.c_float), ptr(tors, C.c_float),
+                                      n_tors_values, ptr(geo, C.c_float), ptr(resc, C.c_float)),
+              self._h, "rescore")
         return geo[:n], resc[:n]
 
 

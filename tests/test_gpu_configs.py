@@ -240,3 +240,51 @@ def test_pipelined_dock_host_equals_one_shot(V, engine, monkeypatch):
         np.testing.assert_array_equal(np.ascontiguousarray(getattr(a, f)).view(np.uint8),
                                       np.ascontiguousarray(getattr(b, f)).view(np.uint8), err_msg=f)
     np.testing.assert_array_equal(top_a, top_b)
+
+
+def test_rescore_device_entries_equal_host_path(V, engine, pocket_json):
+    """The device-resident rescoring entries give the host path's bits:
+    vs_rescore_survivors on the last dock's survivors (after switching to
+    0.2 A maps) and vs_rescore_device on the same poses in device memory
+    both equal vs_rescore from host arrays and the oracle."""
+    import torch
+    from oracle import sweep
+    import bench
+    lib = bench.c5_library(3000, 0, 1, 16)
+    pocket = bench.make_pocket()
+    engine.set_pocket(pocket, grid_spacing=0.4)
+    classes = [(1, 41, 0, 11), (60, 81, 11, 21)]
+    engine.upload(lib, classes)
+    prm = bench.params()
+    engine.dock(prm)
+    res = engine.fetch()
+    pl, T, Q, TH = bench.survivor_poses(lib, res)
+    box = V.Pocket(pocket.sites, (-15.0, -15.0, -15.0), (15.0, 15.0, 15.0), pocket.clash_radius,
+                   pocket.clash_penalty)
+    engine.set_pocket(box, grid_spacing=0.2, grid_pad=2.0)
+    KT = prm.keep_top
+    g_dev = torch.zeros(len(lib) * KT, dtype=torch.float32, device="cuda")
+    r_dev = torch.zeros_like(g_dev)
+    engine.rescore_survivors(g_dev.data_ptr(), r_dev.data_ptr())
+    torch.cuda.synchronize()
+    slot = (pl.astype(np.int64) * KT + (np.arange(len(pl)) - np.repeat(
+        np.cumsum(np.maximum(res.n_surv, 0)) - np.maximum(res.n_surv, 0), np.maximum(res.n_surv, 0))))
+    g_surv, r_surv = g_dev.cpu().numpy()[slot], r_dev.cpu().numpy()[slot]
+    g_host, r_host = engine.rescore(lib, pl, T, Q, TH)
+    np.testing.assert_array_equal(g_surv.view(np.uint32), g_host.view(np.uint32))
+    np.testing.assert_array_equal(r_surv.view(np.uint32), r_host.view(np.uint32))
+    # the same poses from device arrays, against the resident library
+    engine.upload(lib, classes)
+    dv = {k: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+          for k, a in (("pl", pl.astype(np.int32)), ("t", T.reshape(-1)), ("q", Q.reshape(-1)),
+                       ("th", TH if TH.size else np.zeros(1, np.float32)))}
+    g2 = torch.zeros(len(pl), dtype=torch.float32, device="cuda")
+    r2 = torch.zeros_like(g2)
+    engine.rescore_device(len(pl), dv["pl"].data_ptr(), dv["t"].data_ptr(), dv["q"].data_ptr(),
+                          dv["th"].data_ptr(), g2.data_ptr(), r2.data_ptr())
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(g2.cpu().numpy().view(np.uint32), g_host.view(np.uint32))
+    np.testing.assert_array_equal(r2.cpu().numpy().view(np.uint32), r_host.view(np.uint32))
+    og, orr = sweep.score_poses(sweep.OraclePocket(box, 0.2, 2.0), lib, pl, T, Q, TH)
+    np.testing.assert_array_equal(g_host.view(np.uint32), og.view(np.uint32))
+    np.testing.assert_array_equal(r_host.view(np.uint32), orr.view(np.uint32))
