@@ -400,6 +400,11 @@ def roofline(work, phase_ms, dock_ms, peaks, traffic, as_impl=None, gathers=None
                       "achieved_l2_gather_GBps": round(l2 / t / 1e9, 1),
                       "frac_l2_gather": round(l2 / t / peaks["l2_gather_Bps"], 4),
                       "bound": bind, "frac": round(frac, 4)})
+            if frac > 1.0:
+                d["note"] = ("above 1: the frozen formula counts every intramolecular pair "
+                             "(3 XU, 15 FLOP) per torsion state; the flex search tests only "
+                             "the moved atoms' cross pairs, inside the cutoff, with a "
+                             "tabulated softplus (as_implemented has the executed count)")
         per[k] = d
     dom = max(per, key=lambda k: per[k]["ms"])
     d = per[dom]

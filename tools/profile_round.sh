@@ -21,7 +21,7 @@ timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_d
     python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_traffic_$TAG.log 2>&1 || echo "traffic failed"
 timeout 300 python tools/profile_dock.py --ligands $NLIG > gpurun_out/profile_dock_$TAG.log 2>&1 || { echo "profile_dock failed"; exit 1; }
 cat gpurun_out/profile_dock_$TAG.log
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"vs_(sweep|flex|polish)_kernel" -s 3 -c 3 \
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"vs_(start|sweep|flex|polish)_kernel" -s 160 -c 4 \
     -f -o gpurun_out/prof_dock_$TAG python tools/profile_dock.py --ligands $NLIG \
     > gpurun_out/ncu_full_$TAG.log 2>&1 || echo "full capture failed"
 tail -3 gpurun_out/ncu_full_$TAG.log
