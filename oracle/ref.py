@@ -66,6 +66,10 @@ def lib() -> C.CDLL:
                                          P(C.c_double), P(C.c_double), C.c_int, P(C.c_float)]),
             "vsref_parse_check": (C.c_int, [C.c_char_p, P(C.c_int), P(C.c_long), P(C.c_int),
                                          P(C.c_int)]),
+            "vsref_pocket_json": (C.c_int, [C.c_char_p, C.c_char_p, C.c_int]),
+            "vsref_pose_json": (C.c_int, [C.c_char_p, P(C.c_double), P(C.c_double), P(C.c_double),
+                                          C.c_int, C.c_double, C.c_int, C.c_double, C.c_char_p,
+                                          C.c_int]),
             "vsref_rng_draws": (None, [C.c_uint64, P(C.c_uint64), C.c_int, P(C.c_int32), P(C.c_double),
                                        P(C.c_double), C.c_int, P(C.c_double)]),
             "vsref_random_smiles": (C.c_int, [C.c_uint64, C.c_uint64, C.c_char_p, C.c_int]),
@@ -314,3 +318,23 @@ def parse_check(smiles: str):
     rc = lib().vsref_parse_check(smiles.encode("latin-1"), C.byref(k), C.byref(p), C.byref(na),
                                  C.byref(nb))
     return ("error", k.value, p.value) if rc else ("ok", na.value, nb.value)
+
+
+def pocket_json_bytes(text: str) -> str:
+    """pocket_to_json(parse_pocket_json(text)) of the reference."""
+    buf = C.create_string_buffer(1 << 20)
+    _chk(lib().vsref_pocket_json(text.encode(), buf, 1 << 20))
+    return buf.value.decode()
+
+
+def pose_json_bytes(ligand: str, t, q, tors, geo: float, rescore) -> str:
+    """pose_to_json of the reference for the given pose (rescore None = absent)."""
+    t = np.ascontiguousarray(t, np.float64)
+    q = np.ascontiguousarray(q, np.float64)
+    th = np.ascontiguousarray(tors if len(tors) else [0.0], np.float64)
+    buf = C.create_string_buffer(1 << 16)
+    n = lib().vsref_pose_json(ligand.encode(), _p(t, C.c_double), _p(q, C.c_double),
+                              _p(th, C.c_double), len(tors), float(geo),
+                              0 if rescore is None else 1, float(rescore or 0.0), buf, 1 << 16)
+    _chk(n)
+    return buf.value.decode()

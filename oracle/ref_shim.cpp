@@ -508,6 +508,33 @@ int vsref_parse_check(const char* smiles, int* kind, long* pos, int* n_atoms, in
   }
 }
 
+// dock::pocket_to_json(parse_pocket_json(text)) (dock.cpp:432-474): bytes
+// out (NUL-terminated); the length, or -9 when cap is too small
+int vsref_pocket_json(const char* text, char* out, int cap) {
+  return guarded([&] {
+    const std::string s = dock::pocket_to_json(dock::parse_pocket_json(text));
+    if (static_cast<int>(s.size()) + 1 > cap) return -9;
+    std::memcpy(out, s.c_str(), s.size() + 1);
+    return static_cast<int>(s.size());
+  });
+}
+
+// dock::pose_to_json (dock.cpp:476-489) of the given pose
+int vsref_pose_json(const char* ligand, const double* t, const double* q, const double* tors,
+                    int n_tors, double geo, int has_rescore, double rescore, char* out, int cap) {
+  dock::Pose p;
+  p.ligand_id = ligand;
+  p.translation = {t[0], t[1], t[2]};
+  p.rotation = {q[0], q[1], q[2], q[3]};
+  p.torsions.assign(tors, tors + n_tors);
+  p.geometric_score = geo;
+  if (has_rescore) p.rescore = rescore;
+  const std::string s = dock::pose_to_json(p);
+  if (static_cast<int>(s.size()) + 1 > cap) return -9;
+  std::memcpy(out, s.c_str(), s.size() + 1);
+  return static_cast<int>(s.size());
+}
+
 // ----------------------------------------------------------------- corpus --
 // corpus::random_smiles(Rng(seed).split(i)) (tools/smiles_corpus.hpp:13,51)
 int vsref_random_smiles(std::uint64_t seed, std::uint64_t i, char* out, int cap) {

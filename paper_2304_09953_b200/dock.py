@@ -113,21 +113,74 @@ def load_pocket_file(path: str) -> Pocket:
         raise PocketError(f"cannot open pocket file: {path}") from e
 
 
+def _jnum(x) -> str:
+    """A double as nlohmann::json 3.11 dumps it (the reference's JSON
+    library): the shortest round-trip digits (those of Python's float repr),
+    laid out by nlohmann's rule -- fixed notation for decimal exponents n in
+    (-4, 15], else d.ddde+XX -- and null for non-finite values."""
+    x = float(x)
+    if not math.isfinite(x):
+        return "null"
+    if x == 0.0:
+        return "-0.0" if math.copysign(1.0, x) < 0 else "0.0"
+    import decimal
+    sign, digs, exp = decimal.Decimal(repr(x)).as_tuple()
+    digits = "".join(map(str, digs))
+    stripped = digits.rstrip("0")
+    exp += len(digits) - len(stripped)
+    digits = stripped.lstrip("0") or "0"
+    k = len(digits)
+    n = k + exp  # value = 0.digits * 10^n
+    out = "-" if sign else ""
+    if k <= n <= 15:
+        return out + digits + "0" * (n - k) + ".0"
+    if 0 < n <= 15:
+        return out + digits[:n] + "." + digits[n:]
+    if -4 < n <= 0:
+        return out + "0." + "0" * (-n) + digits
+    e = n - 1
+    mant = digits if k == 1 else digits[0] + "." + digits[1:]
+    return out + mant + "e" + ("-" if e < 0 else "+") + f"{abs(e):02d}"
+
+
+def _jstr(v: str) -> str:
+    return json.dumps(v, ensure_ascii=False)  # same escapes as nlohmann (UTF-8 kept)
+
+
 def pocket_to_json(p: Pocket) -> str:
-    """dock::pocket_to_json (dock.cpp:460-474)."""
-    j = {"sites": [{"center": list(s.center), "weight": s.weight, "sigma": s.sigma,
-                    "kind": s.kind} for s in p.sites],
-         "bounds": {"min": list(p.lo), "max": list(p.hi)},
-         "clash_radius": p.clash_radius, "clash_penalty": p.clash_penalty}
-    return json.dumps(j, indent=2)
+    """dock::pocket_to_json (dock.cpp:460-474): the ordered_json dump(2)
+    bytes of the reference (tests/test_json_bytes.py)."""
+    def arr(v, ind):
+        pad = " " * ind
+        return "[\n" + ",\n".join(pad + "  " + _jnum(x) for x in v) + "\n" + pad + "]"
+
+    sites = []
+    for st in p.sites:
+        sites.append("    {\n"
+                     f'      "center": {arr(st.center, 6)},\n'
+                     f'      "weight": {_jnum(st.weight)},\n'
+                     f'      "sigma": {_jnum(st.sigma)},\n'
+                     f'      "kind": {_jstr(st.kind)}\n'
+                     "    }")
+    site_block = "[\n" + ",\n".join(sites) + "\n  ]" if sites else "[]"
+    return ("{\n"
+            f'  "sites": {site_block},\n'
+            '  "bounds": {\n'
+            f'    "min": {arr(p.lo, 4)},\n'
+            f'    "max": {arr(p.hi, 4)}\n'
+            "  },\n"
+            f'  "clash_radius": {_jnum(p.clash_radius)},\n'
+            f'  "clash_penalty": {_jnum(p.clash_penalty)}\n'
+            "}")
 
 
 def pose_to_json(pose: Pose) -> str:
-    """dock::pose_to_json (dock.cpp:476-489)."""
-    return json.dumps({"ligand": pose.ligand_id, "translation": list(pose.translation),
-                       "rotation": list(pose.rotation), "torsions": list(pose.torsions),
-                       "geometric_score": pose.geometric_score, "rescore": pose.rescore},
-                      separators=(",", ":"))
+    """dock::pose_to_json (dock.cpp:476-489): compact ordered_json bytes."""
+    nums = lambda v: "[" + ",".join(_jnum(x) for x in v) + "]"
+    resc = "null" if pose.rescore is None else _jnum(pose.rescore)
+    return (f'{{"ligand":{_jstr(pose.ligand_id)},"translation":{nums(pose.translation)},'
+            f'"rotation":{nums(pose.rotation)},"torsions":{nums(pose.torsions)},'
+            f'"geometric_score":{_jnum(pose.geometric_score)},"rescore":{resc}}}')
 
 
 # --------------------------------------------------------------- params ---

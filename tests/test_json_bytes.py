@@ -1,0 +1,69 @@
+"""JSON I/O byte parity (dock.cpp:432-489): pocket_to_json
+(parse_pocket_json(text)) and pose_to_json of the Python layer and of the
+C++ drop-in (libvscreen_core.so) produce the reference's exact bytes
+(nlohmann ordered_json) on random pockets and poses: tiny / huge / negative
+/ integral values, non-finite scores, escaped ids."""
+import json
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, need_ref
+
+
+def _values(rng, n):
+    pool = [0.0, -0.0, 1.0, 2.0, 1e-5, 1e-4, 0.1, 1e15, 1e16, 1e-300, 1e300, -3.5e20, 123456.789,
+            1 / 3, 2 ** 53, 7.0]
+    out = []
+    for k in range(n):
+        out.append(float(pool[k % len(pool)]) if k % 2 else float(rng.normal() * 10.0 ** int(rng.integers(-8, 9))))
+    return out
+
+
+def _pocket(rng, n_sites):
+    v = iter(_values(rng, 6 * n_sites + 8))
+    kinds = ["steric", "hbond", "lipophilic"]
+    sites = [{"center": [next(v), next(v), next(v)], "weight": next(v), "sigma": abs(next(v)) + 0.5,
+              "kind": kinds[i % 3]} for i in range(n_sites)]
+    return {"sites": sites, "bounds": {"min": [-5, -6.5, next(v)], "max": [5, 6, 7]},
+            "clash_radius": 0.7, "clash_penalty": abs(next(v))}
+
+
+@pytest.fixture(scope="module")
+def json_exe(tmp_path_factory):
+    exe = tmp_path_factory.mktemp("json") / "json_bytes"
+    libdir = os.path.join(ROOT, "paper_2304_09953_b200")
+    subprocess.run(["/usr/bin/g++", "-std=c++20", "-O1", f"-I{ROOT}/include",
+                    os.path.join(ROOT, "tests", "cpp", "json_bytes.cpp"), f"-L{libdir}",
+                    "-lvscreen_core", "-lvscreen_gpu", f"-Wl,-rpath,{libdir}", "-o", str(exe)],
+                   check=True)
+    return str(exe)
+
+
+def test_json_bytes_match_reference(json_exe):
+    R = need_ref()
+    import paper_2304_09953_b200 as V
+    rng = np.random.default_rng(11)
+    for case in range(40):
+        text = json.dumps(_pocket(rng, case % 5))
+        ref = R.pocket_json_bytes(text)
+        assert V.pocket_to_json(V.parse_pocket_json(text)) == ref
+        t = _values(rng, 3)
+        q = _values(rng, 4)
+        tors = _values(rng, case % 4)
+        geo = [1.5, float("nan"), -0.0, 1e-5][case % 4]
+        resc = None if case % 3 == 0 else _values(rng, 1)[0]
+        lig = ["L1", "MOL\"9\\x", "é-ligand", "tab\there"][case % 4]
+        ref_pose = R.pose_json_bytes(lig, t, q, tors, geo, resc)
+        pose = V.Pose(lig, tuple(t), tuple(q), list(tors), geo, resc)
+        assert V.pose_to_json(pose) == ref_pose
+        if "\t" not in lig:  # argv carries the id as is
+            args = [json_exe, lig] + [repr(x) for x in t + q] + [repr(geo),
+                                                              "none" if resc is None else repr(resc)]
+            args += [repr(x) for x in tors]
+            out = subprocess.run(args, input=text, capture_output=True, text=True, check=True).stdout
+            cpp_pocket, cpp_pose = out.split("\n--\n")
+            assert cpp_pocket == ref
+            assert cpp_pose == ref_pose
