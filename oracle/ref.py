@@ -70,6 +70,7 @@ def lib() -> C.CDLL:
             "vsref_pose_json": (C.c_int, [C.c_char_p, P(C.c_double), P(C.c_double), P(C.c_double),
                                           C.c_int, C.c_double, C.c_int, C.c_double, C.c_char_p,
                                           C.c_int]),
+            "vsref_report_bytes": (C.c_int, [C.c_char_p, C.c_int, C.c_char_p, C.c_int]),
             "vsref_rng_draws": (None, [C.c_uint64, P(C.c_uint64), C.c_int, P(C.c_int32), P(C.c_double),
                                        P(C.c_double), C.c_int, P(C.c_double)]),
             "vsref_random_smiles": (C.c_int, [C.c_uint64, C.c_uint64, C.c_char_p, C.c_int]),
@@ -337,4 +338,11 @@ def pose_json_bytes(ligand: str, t, q, tors, geo: float, rescore) -> str:
                               _p(th, C.c_double), len(tors), float(geo),
                               0 if rescore is None else 1, float(rescore or 0.0), buf, 1 << 16)
     _chk(n)
+    return buf.value.decode()
+
+
+def report_bytes(spec: dict, which: int = 0) -> str:
+    """CampaignReport::to_json (which 0) / results_tsv (1) of the reference."""
+    buf = C.create_string_buffer(1 << 20)
+    _chk(lib().vsref_report_bytes(json.dumps(spec).encode(), which, buf, 1 << 20))
     return buf.value.decode()

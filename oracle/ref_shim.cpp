@@ -17,6 +17,8 @@
 #include <string>
 #include <thread>
 #include <atomic>
+
+#include <json.hpp>
 #include <vector>
 
 #include "smiles_corpus.hpp"  // proj/tools/smiles_corpus.hpp (reference corpus sampler)
@@ -533,6 +535,42 @@ int vsref_pose_json(const char* ligand, const double* t, const double* q, const 
   if (static_cast<int>(s.size()) + 1 > cap) return -9;
   std::memcpy(out, s.c_str(), s.size() + 1);
   return static_cast<int>(s.size());
+}
+
+// pipeline::CampaignReport::to_json / results_tsv (pipeline.cpp:269-313) of a
+// report given as a JSON spec {stages: [[name, in, out, sim, tasks]], ranked:
+// [[id, score, delta_g|null]], pairs: [[id, a, b, est, sem, reps, met]],
+// trace_path}; which = 0 report JSON, 1 TSV
+int vsref_report_bytes(const char* spec, int which, char* out, int cap) {
+  return guarded([&] {
+    const nlohmann::json j = nlohmann::json::parse(spec);
+    pipeline::CampaignReport r;
+    for (const auto& s : j.at("stages"))
+      r.stages.push_back({s.at(0).get<std::string>(), s.at(1).get<std::size_t>(),
+                          s.at(2).get<std::size_t>(), s.at(3).get<double>(),
+                          s.at(4).get<std::size_t>()});
+    for (const auto& x : j.at("ranked")) {
+      pipeline::RankedLigand rl{x.at(0).get<std::string>(), x.at(1).get<double>(), std::nullopt};
+      if (!x.at(2).is_null()) rl.delta_g = x.at(2).get<double>();
+      r.ranked.push_back(rl);
+    }
+    for (const auto& p : j.at("pairs")) {
+      pipeline::PairResult pr;
+      pr.pair_id = p.at(0).get<std::string>();
+      pr.ligand_a = p.at(1).get<std::string>();
+      pr.ligand_b = p.at(2).get<std::string>();
+      pr.result.estimate = p.at(3).get<double>();
+      pr.result.sem = p.at(4).get<double>();
+      pr.result.replicas = p.at(5).get<int>();
+      pr.result.target_met = p.at(6).get<bool>();
+      r.pairs.push_back(pr);
+    }
+    r.trace_path = j.at("trace_path").get<std::string>();
+    const std::string s = which == 0 ? r.to_json() : r.results_tsv();
+    if (static_cast<int>(s.size()) + 1 > cap) return -9;
+    std::memcpy(out, s.c_str(), s.size() + 1);
+    return static_cast<int>(s.size());
+  });
 }
 
 // ----------------------------------------------------------------- corpus --

@@ -238,13 +238,38 @@ def run_dock_stages(cfg: CampaignConfig, engine: Engine | None = None, grid_spac
                       list(lib.ids), res.best, dock_ms)
 
 
-def funnel_to_json(f: DockFunnel) -> str:
-    """The stage records and ranked ligands in the report's field names
-    (CampaignReport::to_json, pipeline.cpp:269-301)."""
-    return json.dumps({"stages": [s.to_json() for s in f.stages],
-                       "ranked": [{"id": r.id, "score": r.score, "delta_g": r.delta_g}
-                                  for r in f.ranked]})
+def report_to_json(stages, ranked, pairs=(), trace_path: str = "") -> str:
+    """CampaignReport::to_json (pipeline.cpp:269-301): the reference's report
+    bytes (nlohmann ordered_json, indent 2).  stages: StageStats; ranked:
+    RankedLigand; pairs: (pair_id, ligand_a, ligand_b, ddg_kT, sem_kT,
+    replicas, target_met) tuples (the FEP stage itself is out of scope)."""
+    from .dock import _jnum, _jstr
+
+    def obj(fields, ind):
+        pad = " " * ind
+        return ("{\n" + ",\n".join(f'{pad}  "{k}": {v}' for k, v in fields) + "\n" + pad + "}")
+
+    def arr(items, ind):
+        pad = " " * ind
+        return "[]" if not items else "[\n" + ",\n".join(pad + "  " + x for x in items) + "\n" + pad + "]"
+
+    st = [obj([("name", _jstr(s.name)), ("in", str(int(s.in_))), ("out", str(int(s.out))),
+               ("sim_seconds", _jnum(s.sim_seconds or 0.0)), ("tasks", str(int(s.tasks)))], 4)
+          for s in stages]
+    rk = [obj([("id", _jstr(r.id)), ("score", _jnum(r.score)),
+               ("delta_g", "null" if r.delta_g is None else _jnum(r.delta_g))], 4) for r in ranked]
+    pr = [obj([("pair_id", _jstr(p[0])), ("ligand_a", _jstr(p[1])), ("ligand_b", _jstr(p[2])),
+               ("ddg_kT", _jnum(p[3])), ("sem_kT", _jnum(p[4])), ("replicas", str(int(p[5]))),
+               ("target_met", "true" if p[6] else "false")], 4) for p in pairs]
+    return obj([("stages", arr(st, 2)), ("ranked", arr(rk, 2)), ("pairs", arr(pr, 2)),
+                ("trace_path", _jstr(trace_path))], 0)
+
+
+def funnel_to_json(f: DockFunnel, trace_path: str = "") -> str:
+    """The dock funnel's stage records and ranked ligands as the reference's
+    report bytes (report_to_json; no pairs: the FEP stages are out of scope)."""
+    return report_to_json(f.stages, f.ranked, (), trace_path)
 
 
 __all__ = ["CampaignConfig", "ConfigError", "DockFunnel", "DockTask", "StageKnobs", "StageStats",
-           "funnel_to_json", "load_config_file", "parse_config_json", "prepare", "run_dock_stages"]
+           "funnel_to_json", "load_config_file", "report_to_json", "parse_config_json", "prepare", "run_dock_stages"]

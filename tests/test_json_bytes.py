@@ -67,3 +67,36 @@ def test_json_bytes_match_reference(json_exe):
             cpp_pocket, cpp_pose = out.split("\n--\n")
             assert cpp_pocket == ref
             assert cpp_pose == ref_pose
+
+
+REPORT_SPEC = {"stages": [["parse", 100, 98, 0.0, 0], ["dock", 98, 91, 12.345678901234567, 7],
+                          ["rank", 91, 9, 0.0, 0]],
+               "ranked": [["L10", 45.25, None], ["L2", -1e-5, 0.1], ["é\"x", 1e20, -3.5]],
+               "pairs": [["P0", "L10", "L2", -1.234567890123, 0.05, 4, True]],
+               "trace_path": "out/campaign_trace.jsonl"}
+
+
+def test_campaign_report_bytes_match_reference(tmp_path):
+    """CampaignReport::to_json / results_tsv (pipeline.cpp:269-313): the
+    Python report writer and the C++ drop-in give the reference's bytes."""
+    R = need_ref()
+    from paper_2304_09953_b200.campaign import StageStats, report_to_json
+    from paper_2304_09953_b200.pipeline import RankedLigand
+    ref = R.report_bytes(REPORT_SPEC, 0)
+    ref_tsv = R.report_bytes(REPORT_SPEC, 1)
+    st = [StageStats(s[0], s[1], s[2], s[3], s[4]) for s in REPORT_SPEC["stages"]]
+    rk = [RankedLigand(*x) for x in REPORT_SPEC["ranked"]]
+    assert report_to_json(st, rk, [tuple(p) for p in REPORT_SPEC["pairs"]],
+                          REPORT_SPEC["trace_path"]) == ref
+    assert report_to_json([], [], (), "") == R.report_bytes(
+        {"stages": [], "ranked": [], "pairs": [], "trace_path": ""}, 0)
+    exe = tmp_path / "report_bytes"
+    libdir = os.path.join(ROOT, "paper_2304_09953_b200")
+    subprocess.run(["/usr/bin/g++", "-std=c++20", "-O1", f"-I{ROOT}/include",
+                    os.path.join(ROOT, "tests", "cpp", "report_bytes.cpp"), f"-L{libdir}",
+                    "-lvscreen_core", "-lvscreen_gpu", f"-Wl,-rpath,{libdir}", "-o", str(exe)],
+                   check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout
+    cpp_json, cpp_tsv = out.split("\n--\n")
+    assert cpp_json == ref
+    assert cpp_tsv == ref_tsv
