@@ -36,7 +36,8 @@ enum vs_status {
   VS_ERR_CUDA = -10,
   VS_ERR_NO_DEVICE = -11,
   VS_ERR_STATE = -12,           /* call order (e.g. dock before pocket/library) */
-  VS_ERR_DISCONNECTED = -13     /* chem::DisconnectedGraph chem.cpp:408 */
+  VS_ERR_DISCONNECTED = -13,    /* chem::DisconnectedGraph chem.cpp:408 */
+  VS_ERR_FORMAT = -14           /* codec::BadFormat / UnknownCode codec.cpp:147-161, 195-289 */
 };
 
 /* ------------------------------------------------------------- pocket -- */
@@ -363,6 +364,19 @@ int vs_libbuild_corpus(uint64_t seed, const int64_t* index, int32_t n, const uin
 int vs_flexible_select(uint64_t seed, int32_t n_want, int32_t atom_lo, int32_t atom_hi,
                        int32_t tors_lo, int32_t tors_hi, int64_t max_scan, int64_t* first,
                        int32_t* count);
+
+/* SMZC library decompression (codec.cpp:147-161, 195-289; ingest row f2):
+ * dict = the SMZ1 dictionary file bytes, data = the .smzc file bytes; out
+ * receives the reference's decompress_stream text (every record + '\n'),
+ * expanded on `threads` host threads.  out = NULL: size query (*out_len).
+ * VS_ERR_FORMAT on a bad magic, a dictionary hash mismatch (SHA-256),
+ * truncation or an unknown code byte (vs_codec_last_error has the text). */
+int vs_smzc_decompress(const uint8_t* dict, int64_t dict_len, const uint8_t* data, int64_t len,
+                       int32_t threads, char* out, int64_t cap, int64_t* out_len);
+const char* vs_codec_last_error(void);
+/* codec::load_dictionary (codec.cpp:188-215): validate an SMZ1 dictionary;
+ * *n_entries = its entry count.  VS_ERR_FORMAT with the reference's message. */
+int vs_smz1_check(const uint8_t* dict, int64_t dict_len, int32_t* n_entries);
 
 /* batcher (batcher.cpp:7-86) */
 int vs_default_classes(vs_size_class* out, int32_t cap);

@@ -71,6 +71,10 @@ def lib() -> C.CDLL:
                                           C.c_int, C.c_double, C.c_int, C.c_double, C.c_char_p,
                                           C.c_int]),
             "vsref_report_bytes": (C.c_int, [C.c_char_p, C.c_int, C.c_char_p, C.c_int]),
+            "vsref_smzc_compress": (C.c_int, [C.c_char_p, C.c_long, C.c_char_p, C.c_char_p, C.c_long]),
+            "vsref_smzc_decompress": (C.c_int, [C.c_char_p, C.c_long, C.c_char_p, C.c_char_p,
+                                                C.c_long]),
+            "vsref_train_dictionary": (C.c_int, [C.c_char_p, C.c_long, C.c_int, C.c_char_p, C.c_long]),
             "vsref_rng_draws": (None, [C.c_uint64, P(C.c_uint64), C.c_int, P(C.c_int32), P(C.c_double),
                                        P(C.c_double), C.c_int, P(C.c_double)]),
             "vsref_random_smiles": (C.c_int, [C.c_uint64, C.c_uint64, C.c_char_p, C.c_int]),
@@ -346,3 +350,25 @@ def report_bytes(spec: dict, which: int = 0) -> str:
     buf = C.create_string_buffer(1 << 20)
     _chk(lib().vsref_report_bytes(json.dumps(spec).encode(), which, buf, 1 << 20))
     return buf.value.decode()
+
+
+def smzc_compress(text: bytes, dict_path: str) -> bytes:
+    """codec::compress_stream of the reference (the dictionary from a file)."""
+    cap = 2 * len(text) + 4096
+    buf = C.create_string_buffer(cap)
+    n = _chk(lib().vsref_smzc_compress(text, len(text), dict_path.encode(), buf, cap))
+    return buf.raw[:n]
+
+
+def smzc_decompress(data: bytes, dict_path: str) -> bytes:
+    cap = 16 * len(data) + 4096
+    buf = C.create_string_buffer(cap)
+    n = _chk(lib().vsref_smzc_decompress(data, len(data), dict_path.encode(), buf, cap))
+    return buf.raw[:n]
+
+
+def train_dictionary(text: bytes, max_entries: int) -> bytes:
+    """codec::train_dictionary + save_dictionary: SMZ1 bytes."""
+    buf = C.create_string_buffer(8192)
+    n = _chk(lib().vsref_train_dictionary(text, len(text), max_entries, buf, 8192))
+    return buf.raw[:n]

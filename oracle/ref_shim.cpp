@@ -14,6 +14,7 @@
 #include <cstdint>
 #include <cstring>
 #include <map>
+#include <sstream>
 #include <string>
 #include <thread>
 #include <atomic>
@@ -23,6 +24,7 @@
 
 #include "smiles_corpus.hpp"  // proj/tools/smiles_corpus.hpp (reference corpus sampler)
 #include "vscreen/batcher.hpp"
+#include "vscreen/codec.hpp"
 #include "vscreen/chem.hpp"
 #include "vscreen/dock.hpp"
 #include "vscreen/pipeline.hpp"
@@ -569,6 +571,48 @@ int vsref_report_bytes(const char* spec, int which, char* out, int cap) {
     const std::string s = which == 0 ? r.to_json() : r.results_tsv();
     if (static_cast<int>(s.size()) + 1 > cap) return -9;
     std::memcpy(out, s.c_str(), s.size() + 1);
+    return static_cast<int>(s.size());
+  });
+}
+
+// codec::compress_stream / decompress_stream (codec.cpp:254-289) with a
+// dictionary file: text <-> SMZC bytes; the length, or -9 when cap is small
+int vsref_smzc_compress(const char* text, long n, const char* dict_path, char* out, long cap) {
+  return guarded([&] {
+    const codec::Dictionary d = codec::load_dictionary_file(dict_path);
+    std::istringstream in(std::string(text, static_cast<size_t>(n)));
+    std::ostringstream o;
+    codec::compress_stream(in, o, d);
+    const std::string s = o.str();
+    if (static_cast<long>(s.size()) > cap) return -9;
+    std::memcpy(out, s.data(), s.size());
+    return static_cast<int>(s.size());
+  });
+}
+int vsref_smzc_decompress(const char* data, long n, const char* dict_path, char* out, long cap) {
+  return guarded([&] {
+    const codec::Dictionary d = codec::load_dictionary_file(dict_path);
+    std::istringstream in(std::string(data, static_cast<size_t>(n)));
+    std::ostringstream o;
+    codec::decompress_stream(in, o, d);
+    const std::string s = o.str();
+    if (static_cast<long>(s.size()) > cap) return -9;
+    std::memcpy(out, s.data(), s.size());
+    return static_cast<int>(s.size());
+  });
+}
+// codec::train_dictionary + save_dictionary (codec.cpp:82-130, 174-186)
+int vsref_train_dictionary(const char* text, long n, int max_entries, char* out, long cap) {
+  return guarded([&] {
+    std::vector<std::string> corpus;
+    std::istringstream in(std::string(text, static_cast<size_t>(n)));
+    for (std::string line; std::getline(in, line);) corpus.push_back(line);
+    const codec::Dictionary d = codec::train_dictionary(corpus, static_cast<size_t>(max_entries));
+    std::ostringstream o;
+    codec::save_dictionary(d, o);
+    const std::string s = o.str();
+    if (static_cast<long>(s.size()) > cap) return -9;
+    std::memcpy(out, s.data(), s.size());
     return static_cast<int>(s.size());
   });
 }

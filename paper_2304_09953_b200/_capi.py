@@ -27,6 +27,7 @@ VS_ERR_CUDA = -10
 VS_ERR_NO_DEVICE = -11
 VS_ERR_STATE = -12
 VS_ERR_DISCONNECTED = -13
+VS_ERR_FORMAT = -14
 
 P = C.POINTER
 
@@ -165,6 +166,10 @@ _SIGS = {
                                      C.c_int32, C.c_int64, P(C.c_int64), P(C.c_int32)]),
     "vs_libbuild_corpus": (C.c_int, [C.c_uint64, P(C.c_int64), C.c_int32, P(C.c_uint64),
                                      C.c_int32, C.c_int32, P(C.c_void_p)]),
+    "vs_smzc_decompress": (C.c_int, [C.c_char_p, C.c_int64, C.c_char_p, C.c_int64, C.c_int32,
+                                     C.c_void_p, C.c_int64, P(C.c_int64)]),
+    "vs_codec_last_error": (C.c_char_p, []),
+    "vs_smz1_check": (C.c_int, [C.c_char_p, C.c_int64, C.POINTER(C.c_int32)]),
     "vs_default_classes": (C.c_int, [P(vs_size_class), C.c_int32]),
     "vs_size_class_of": (C.c_int, [C.c_int32, C.c_int32, P(vs_size_class), C.c_int32]),
     "vs_target_batch_size": (C.c_int, [P(vs_size_class), C.c_double, C.c_double, C.c_double,

@@ -21,7 +21,7 @@ as the device top-k.  What it keeps from the reference, exactly:
 What it does not do: `sim_seconds` of the dock stage is the cluster
 scheduler simulation (`sched::run_simulation`, out of scope here): the
 stage carries the tasks instead so a caller's scheduler can replay them.
-Compressed (.smzc) libraries need the reference codec (out of scope).  The
+Compressed (.smzc) libraries decode through codec.decompress_file.  The
 pose generator is sweep-v1 (docs/SWEEP_V1.md), so the ranked scores are
 sweep-v1's (DESIGN.md §1), not the gradient ascent's.
 """
@@ -148,7 +148,23 @@ def parse_config_json(text: str, base_dir: str = "") -> CampaignConfig:
         c.top_n = int(j.get("top_n", 10))
     except (KeyError, TypeError) as e:
         raise ConfigError(f"bad campaign config: missing or invalid {e}") from e
+    _validate(c)
     return c
+
+
+def _validate(c: CampaignConfig) -> None:
+    """validate_config (pipeline.cpp:162-178), the dock-funnel fields."""
+    if not (0.0 < c.keep_after_dock <= 1.0):
+        raise ConfigError("funnel.keep_after_dock must be in (0, 1]")
+    if not (0.0 < c.keep_for_fep <= 1.0):
+        raise ConfigError("funnel.keep_for_fep must be in (0, 1]")
+    if c.threads < 1:
+        raise ConfigError("threads must be >= 1")
+    for label, p in (("library", c.library_path), ("pocket", c.pocket_path)):
+        if not os.path.exists(p):
+            raise ConfigError(f"{label} file not found: {p}")
+    if c.dictionary_path and not os.path.exists(c.dictionary_path):
+        raise ConfigError(f"dictionary file not found: {c.dictionary_path}")
 
 
 def load_config_file(path: str) -> CampaignConfig:
@@ -165,11 +181,22 @@ def prepare(cfg: CampaignConfig, threads: int | None = None):
     """parse + embed + the dock stage's class filter and batch replay (no
     GPU).  Returns (library of in-class ligands with their campaign seeds,
     stage records so far, dock tasks, dock-stage input count)."""
-    if cfg.library_path.endswith(".smzc"):
-        raise ConfigError("compressed (.smzc) libraries need the reference codec, "
-                          "which is outside the B200 dock path")
     threads = threads or max(1, cfg.threads)
-    records = read_library_file(cfg.library_path)
+    if cfg.library_path.endswith(".smzc"):  # pipeline.cpp:384-396
+        if not cfg.dictionary_path:
+            raise ConfigError("compressed library needs a dictionary")
+        from .codec import decompress, load_dictionary_file
+        d = load_dictionary_file(cfg.dictionary_path)
+        try:
+            with open(cfg.library_path, "rb") as f:
+                data = f.read()
+        except OSError as e:
+            raise ConfigError(f"cannot open library: {cfg.library_path}") from e
+        text = decompress(d, data, threads=os.cpu_count())
+        from .chem import read_library_records
+        records = read_library_records(text.split("\n") if text else [])
+    else:
+        records = read_library_file(cfg.library_path)
     smiles = [r.smiles for r in records]
     ids = [r.id for r in records]
     # parse: graph, descriptors and topology only (no embedding)

@@ -62,6 +62,20 @@ class DeviceError(VscreenError):
     """CUDA failure or no device."""
 
 
+class BadFormat(VscreenError):
+    """codec::BadFormat (codec.hpp:34-37): a malformed SMZ1 dictionary or
+    SMZC library, or a dictionary hash mismatch."""
+
+
+class UnknownCode(VscreenError):
+    """codec::UnknownCode (codec.hpp:23-32): a code byte with no dictionary
+    entry; .code and .offset (within the record) as the reference's."""
+
+    def __init__(self, code: int, offset: int):
+        super().__init__(f"unknown code byte 0x{code:x} at offset {offset}")
+        self.code, self.offset = code, offset
+
+
 _MAP = {
     _capi.VS_ERR_INVALID_ARGUMENT: ValueError,  # std::invalid_argument
     _capi.VS_ERR_ATOM_COUNT: AtomCountMismatch,
@@ -75,6 +89,7 @@ _MAP = {
     _capi.VS_ERR_NO_DEVICE: DeviceError,
     _capi.VS_ERR_STATE: VscreenError,
     _capi.VS_ERR_DISCONNECTED: DisconnectedGraph,
+    _capi.VS_ERR_FORMAT: BadFormat,
 }
 
 

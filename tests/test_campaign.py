@@ -53,7 +53,8 @@ def _library_with_edge_cases(tmp_path):
     big = "".join(random_smiles(99, i) for i in range(40))
     lines[5:5] = ["C1CC(\tBAD1", "Xq\tBAD2", big + "\tBIG0"]
     (tmp_path / "lib.smi").write_text("\n".join(lines) + "\n")
-    shutil.copy(os.path.join(CAMP, "pocket.json"), tmp_path / "pocket.json")
+    for f in ("pocket.json", "smiles.dict"):
+        shutil.copy(os.path.join(CAMP, f), tmp_path / f)
     j = json.load(open(os.path.join(CAMP, "campaign_100.json")))
     j["library"] = "lib.smi"
     (tmp_path / "c.json").write_text(json.dumps(j))
