@@ -378,6 +378,11 @@ const char* vs_codec_last_error(void);
  * *n_entries = its entry count.  VS_ERR_FORMAT with the reference's message. */
 int vs_smz1_check(const uint8_t* dict, int64_t dict_len, int32_t* n_entries);
 
+/* JSON number text (dock.cpp:460-489, pipeline.cpp:269-301): x[i] as the
+ * reference's nlohmann::json dump prints it, NUL-terminated at out + i*stride.
+ * VS_ERR_CAPACITY if a text needs stride bytes or more. */
+int vs_json_format_doubles(const double* x, int64_t n, char* out, int32_t stride);
+
 /* batcher (batcher.cpp:7-86) */
 int vs_default_classes(vs_size_class* out, int32_t cap);
 int vs_size_class_of(int32_t atoms, int32_t rot, const vs_size_class* classes, int32_t n);

@@ -75,6 +75,7 @@ def lib() -> C.CDLL:
             "vsref_smzc_decompress": (C.c_int, [C.c_char_p, C.c_long, C.c_char_p, C.c_char_p,
                                                 C.c_long]),
             "vsref_train_dictionary": (C.c_int, [C.c_char_p, C.c_long, C.c_int, C.c_char_p, C.c_long]),
+            "vsref_run_campaign": (C.c_int, [C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p]),
             "vsref_rng_draws": (None, [C.c_uint64, P(C.c_uint64), C.c_int, P(C.c_int32), P(C.c_double),
                                        P(C.c_double), C.c_int, P(C.c_double)]),
             "vsref_random_smiles": (C.c_int, [C.c_uint64, C.c_uint64, C.c_char_p, C.c_int]),
@@ -372,3 +373,9 @@ def train_dictionary(text: bytes, max_entries: int) -> bytes:
     buf = C.create_string_buffer(8192)
     n = _chk(lib().vsref_train_dictionary(text, len(text), max_entries, buf, 8192))
     return buf.raw[:n]
+
+
+def run_campaign(cfg_path: str, trace_path: str, report_path: str, tsv_path: str) -> int:
+    """The reference's run_campaign on a config file (outputs redirected)."""
+    return _chk(lib().vsref_run_campaign(cfg_path.encode(), trace_path.encode(),
+                                         report_path.encode(), tsv_path.encode()))

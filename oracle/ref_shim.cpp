@@ -617,6 +617,20 @@ int vsref_train_dictionary(const char* text, long n, int max_entries, char* out,
   });
 }
 
+// pipeline::run_campaign (pipeline.cpp:357-590) on a config file, with its
+// trace / report / TSV paths redirected; returns the report's stage count
+int vsref_run_campaign(const char* cfg_path, const char* trace_path, const char* report_path,
+                       const char* tsv_path) {
+  return guarded([&] {
+    pipeline::CampaignConfig cfg = pipeline::load_config_file(cfg_path);
+    cfg.trace_path = trace_path;
+    cfg.report_path = report_path;
+    cfg.results_tsv_path = tsv_path;
+    const pipeline::CampaignReport rep = pipeline::run_campaign(cfg);
+    return static_cast<int>(rep.stages.size());
+  });
+}
+
 // ----------------------------------------------------------------- corpus --
 // corpus::random_smiles(Rng(seed).split(i)) (tools/smiles_corpus.hpp:13,51)
 int vsref_random_smiles(std::uint64_t seed, std::uint64_t i, char* out, int cap) {

@@ -21,7 +21,7 @@ CORE = os.path.join(HERE, "libvscreen_core.so")
 DROPIN = ["vs_dropin_chem.cpp", "vs_dropin_dock.cpp", "vs_dropin_batcher.cpp",
           "vs_dropin_report.cpp"]
 SOURCES = ["vs_kernels.cu", "vs_dock.cu", "vs_grad.cu", "vs_embed.cu", "vs_pack.cu", "vs_runtime.cu",
-           "vs_host.cpp", "vs_ingest.cpp", "vs_codec.cpp"]
+           "vs_host.cpp", "vs_ingest.cpp", "vs_codec.cpp", "vs_json.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "--fmad=false", "-ccbin", "/usr/bin/g++",
@@ -75,6 +75,8 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
         os.makedirs(os.path.dirname(obj), exist_ok=True)
         cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src),
                "-o", obj]
+        if src == "vs_json.cpp":
+            cmd[1:1] = [f"-I{_json_dir()}"]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)

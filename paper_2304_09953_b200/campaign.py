@@ -27,12 +27,14 @@ sweep-v1's (DESIGN.md §1), not the gradient ascent's.
 """
 from __future__ import annotations
 
+import ctypes as C
 import json
 import os
 from dataclasses import dataclass, field
 
 import numpy as np
 
+from ._capi import lib as _lib, ptr
 from .batcher import DeviceModel, SizeClass, bucket_replay, default_classes
 from .chem import build_library, read_library_file
 from .dock import DockParams, Engine, load_pocket_file
@@ -69,6 +71,8 @@ class CampaignConfig:
     master_seed: int = 0
     threads: int = 1
     top_n: int = 10
+    trace_path: str = "campaign_trace.jsonl"    # relative to the working directory
+    report_path: str = "campaign_report.json"
 
 
 @dataclass
@@ -146,6 +150,9 @@ def parse_config_json(text: str, base_dir: str = "") -> CampaignConfig:
         c.master_seed = int(j.get("seed", 0))
         c.threads = int(j.get("threads", 1))
         c.top_n = int(j.get("top_n", 10))
+        # output paths stay relative to the working directory (pipeline.cpp:151-154)
+        c.trace_path = str(j.get("trace", c.trace_path))
+        c.report_path = str(j.get("report", c.report_path))
     except (KeyError, TypeError) as e:
         raise ConfigError(f"bad campaign config: missing or invalid {e}") from e
     _validate(c)
@@ -233,36 +240,160 @@ def prepare(cfg: CampaignConfig, threads: int | None = None):
     return lib, stages, tasks, n
 
 
+class _TraceWriter:
+    """TraceWriter (pipeline.cpp:335-352): stage_start / stage_end JSONL
+    lines.  The scheduler simulation's events (sched_events) are out of
+    scope, so the dock stage carries none."""
+
+    def __init__(self, path: str):
+        if not path:
+            self.f = None
+            return
+        parent = os.path.dirname(path)
+        if parent:
+            os.makedirs(parent, exist_ok=True)
+        try:
+            self.f = open(path, "wb")
+        except OSError as e:
+            raise ConfigError(f"cannot open trace for writing: {path}") from e
+
+    def stage(self, kind: str, name: str):
+        if self.f is not None:
+            self.f.write(f'{{"kind":"stage_{kind}","stage":"{name}"}}\n'.encode())
+
+    def close(self):
+        if self.f is not None:
+            self.f.close()
+
+
 def run_dock_stages(cfg: CampaignConfig, engine: Engine | None = None, grid_spacing: float = 0.0,
-                    params: DockParams | None = None) -> DockFunnel:
+                    params: DockParams | None = None, write_outputs: bool = False) -> DockFunnel:
     """parse -> embed -> dock -> rescore -> filter -> rank on one GPU.  The
     pocket is analytic by default (as the reference scores it); grid_spacing
-    > 0 docks on the grid maps."""
-    lib, stages, tasks, n_dock_in = prepare(cfg)
-    pocket = load_pocket_file(cfg.pocket_path)
+    > 0 docks on the grid maps.  write_outputs: the trace (stage lines) at
+    cfg.trace_path and the report bytes at cfg.report_path, as
+    run_campaign writes them (pipeline.cpp:357-379, 586-590)."""
+    trace = _TraceWriter(cfg.trace_path if write_outputs else "")
+    try:
+        trace.stage("start", "parse")
+        lib, stages, tasks, n_dock_in = prepare(cfg)
+        trace.stage("end", "parse")
+        trace.stage("start", "embed")
+        trace.stage("end", "embed")
+        trace.stage("start", "dock")
+        pocket = load_pocket_file(cfg.pocket_path)
+        own = engine is None
+        eng = engine or Engine(0)
+        try:
+            eng.set_pocket(pocket, grid_spacing=grid_spacing)
+            k = cfg.knobs
+            prm = params or DockParams(restarts=k.restarts, diversity_delta=k.diversity_delta,
+                                       keep_top=k.keep_top, min_score=k.min_score)
+            res = eng.dock_host(lib, prm, classes=[c.astuple() for c in cfg.classes])
+            dock_ms = eng.last_dock_ms()
+        finally:
+            if own:
+                eng.close()
+        # tasks = batches; sim_seconds needs the scheduler simulation (None here)
+        stages.append(StageStats("dock", n_dock_in, len(lib), None, len(tasks)))
+        trace.stage("end", "dock")
+        # rescore, filter and best ran inside the dock pass (K3a, keep rule)
+        for name in ("rescore", "filter", "rank"):
+            trace.stage("start", name)
+            if name == "rescore":
+                stages.append(StageStats("rescore", len(lib), len(lib), 0.0, 0))
+            elif name == "filter":
+                kept = np.nonzero(res.n_surv > 0)[0]
+                stages.append(StageStats("filter", len(lib), len(kept), 0.0, 0))
+            else:
+                scores = {lib.ids[i]: float(res.best[i]) for i in kept}
+                ranked = rank_ligands(scores)
+                keep = min(keep_count(len(kept), cfg.keep_after_dock), len(ranked))
+                stages.append(StageStats("rank", len(kept), keep, 0.0, 0))
+            trace.stage("end", name)
+    finally:
+        trace.close()
+    f = DockFunnel(stages, [RankedLigand(i, s) for i, s in ranked[:keep]], tasks,
+                   list(lib.ids), res.best, dock_ms)
+    if write_outputs:
+        parent = os.path.dirname(cfg.report_path)
+        if parent:
+            os.makedirs(parent, exist_ok=True)
+        with open(cfg.report_path, "wb") as out:
+            out.write(funnel_to_json(f, cfg.trace_path).encode())
+    return f
+
+
+def dock_library_jsonl(library_path: str, pocket_path: str, out_path: str, restarts: int = 8,
+                       diversity: float = 1.0, keep_top: int = 4, min_score: float = -1e30,
+                       do_rescore: bool = False, seed: int = 0, threads: int | None = None,
+                       engine: Engine | None = None, max_steps: int = 500) -> int:
+    """`vscreen dock` (vscreen_main.cpp:67-93) over the GPU path: per library
+    record, make_ligand + embed_3d(Rng(seed).split(i).next_u64()) +
+    torsion_topology, dock(..., Rng(seed).split(i).split(1).next_u64()) with
+    the reference contract (sweep-v1 restarts refined by the ascent,
+    capi.h vs_dock_refined_host), filter_poses, the FP64 rescore on request,
+    and one pose_to_json line per kept pose.  A record that fails to parse
+    stops the run after the lines of the records before it, with the
+    reference's exception.  Returns the number of lines written."""
+    from . import _capi
+    from .chem import make_ligand, read_library_file
+    from .dock import Pose, filter_poses, pose_to_json
+    from .errors import check as _check
+    threads = threads or os.cpu_count() or 1
+    pocket = load_pocket_file(pocket_path)
+    records = read_library_file(library_path)
+    try:
+        out = open(out_path, "wb")
+    except OSError as e:
+        raise ConfigError(f"cannot open output: {out_path}") from e
+    n = len(records)
+    es = np.zeros(max(n, 1), np.uint64)
+    ds = np.zeros(max(n, 1), np.uint64)
+    for i in range(n):
+        path1 = np.array([i], np.uint64)
+        path2 = np.array([i, 1], np.uint64)
+        _check(_lib.vs_rng_u64(seed & (2**64 - 1), ptr(path1, C.c_uint64), 1, 1,
+                               ptr(es[i:], C.c_uint64)))
+        _check(_lib.vs_rng_u64(seed & (2**64 - 1), ptr(path2, C.c_uint64), 2, 1,
+                               ptr(ds[i:], C.c_uint64)))
+    lib = build_library([r.smiles for r in records], [r.id for r in records], es[:n], ds[:n],
+                        threads=threads, drop_failed=False)
+    bad = np.nonzero(lib.status[:n] != 0)[0]
+    stop = int(bad[0]) if len(bad) else n
+    lines = 0
     own = engine is None
     eng = engine or Engine(0)
     try:
-        eng.set_pocket(pocket, grid_spacing=grid_spacing)
-        k = cfg.knobs
-        prm = params or DockParams(restarts=k.restarts, diversity_delta=k.diversity_delta,
-                                   keep_top=k.keep_top, min_score=k.min_score)
-        res = eng.dock_host(lib, prm, classes=[c.astuple() for c in cfg.classes])
-        dock_ms = eng.last_dock_ms()
+        eng.set_pocket(pocket)
+        if stop:
+            head = lib.subset(np.arange(stop))
+            prm = DockParams(restarts=restarts, diversity_delta=diversity)
+            per_lig = eng.dock_refined(head, prm, max_steps)
+            _, to, _ = head.offsets()
+            for i, poses in enumerate(per_lig):
+                ps = [Pose(head.ids[i], tuple(float(v) for v in t), tuple(float(v) for v in q),
+                           [float(v) for v in th], sc, None, restart=r)
+                      for (t, q, th, sc, r) in poses]
+                ps = filter_poses(ps, keep_top, min_score)
+                if do_rescore and ps:
+                    _, resc = eng.score64(head, np.full(len(ps), i, np.int32),
+                                          [p.translation for p in ps], [p.rotation for p in ps],
+                                          [v for p in ps for v in p.torsions])
+                    for p, v in zip(ps, resc):
+                        p.rescore = float(v)
+                for p in ps:
+                    out.write((pose_to_json(p) + "\n").encode())
+                    lines += 1
     finally:
+        out.close()
         if own:
             eng.close()
-    # tasks = batches; sim_seconds needs the scheduler simulation (None here)
-    stages.append(StageStats("dock", n_dock_in, len(lib), None, len(tasks)))
-    stages.append(StageStats("rescore", len(lib), len(lib), 0.0, 0))
-    kept = np.nonzero(res.n_surv > 0)[0]
-    stages.append(StageStats("filter", len(lib), len(kept), 0.0, 0))
-    scores = {lib.ids[i]: float(res.best[i]) for i in kept}
-    ranked = rank_ligands(scores)
-    keep = min(keep_count(len(kept), cfg.keep_after_dock), len(ranked))
-    stages.append(StageStats("rank", len(kept), keep, 0.0, 0))
-    return DockFunnel(stages, [RankedLigand(i, s) for i, s in ranked[:keep]], tasks,
-                      list(lib.ids), res.best, dock_ms)
+    if stop < n:
+        # the reference's make_ligand exception for that record
+        make_ligand(records[stop].id, records[stop].smiles)
+        raise VscreenError(f"ligand {records[stop].id}: status {int(lib.status[stop])}")
+    return lines
 
 
 def report_to_json(stages, ranked, pairs=(), trace_path: str = "") -> str:
@@ -299,4 +430,4 @@ def funnel_to_json(f: DockFunnel, trace_path: str = "") -> str:
 
 
 __all__ = ["CampaignConfig", "ConfigError", "DockFunnel", "DockTask", "StageKnobs", "StageStats",
-           "funnel_to_json", "load_config_file", "report_to_json", "parse_config_json", "prepare", "run_dock_stages"]
+           "dock_library_jsonl", "funnel_to_json", "load_config_file", "report_to_json", "parse_config_json", "prepare", "run_dock_stages"]

@@ -113,34 +113,21 @@ def load_pocket_file(path: str) -> Pocket:
         raise PocketError(f"cannot open pocket file: {path}") from e
 
 
+def _jnums(xs) -> list[str]:
+    """Doubles as nlohmann::json 3.11 dumps them (the reference's JSON
+    library; capi.h vs_json_format_doubles): Grisu2 digits, fixed notation
+    for decimal exponents in (-4, 15], else d.ddde+XX, null if non-finite."""
+    x = np.ascontiguousarray(xs, np.float64).reshape(-1)
+    if x.size == 0:
+        return []
+    buf = C.create_string_buffer(32 * x.size)
+    check(_lib.vs_json_format_doubles(ptr(x, C.c_double), x.size, buf, 32))
+    raw = buf.raw
+    return [raw[32 * i:32 * i + 32].split(b"\0", 1)[0].decode() for i in range(x.size)]
+
+
 def _jnum(x) -> str:
-    """A double as nlohmann::json 3.11 dumps it (the reference's JSON
-    library): the shortest round-trip digits (those of Python's float repr),
-    laid out by nlohmann's rule -- fixed notation for decimal exponents n in
-    (-4, 15], else d.ddde+XX -- and null for non-finite values."""
-    x = float(x)
-    if not math.isfinite(x):
-        return "null"
-    if x == 0.0:
-        return "-0.0" if math.copysign(1.0, x) < 0 else "0.0"
-    import decimal
-    sign, digs, exp = decimal.Decimal(repr(x)).as_tuple()
-    digits = "".join(map(str, digs))
-    stripped = digits.rstrip("0")
-    exp += len(digits) - len(stripped)
-    digits = stripped.lstrip("0") or "0"
-    k = len(digits)
-    n = k + exp  # value = 0.digits * 10^n
-    out = "-" if sign else ""
-    if k <= n <= 15:
-        return out + digits + "0" * (n - k) + ".0"
-    if 0 < n <= 15:
-        return out + digits[:n] + "." + digits[n:]
-    if -4 < n <= 0:
-        return out + "0." + "0" * (-n) + digits
-    e = n - 1
-    mant = digits if k == 1 else digits[0] + "." + digits[1:]
-    return out + mant + "e" + ("-" if e < 0 else "+") + f"{abs(e):02d}"
+    return _jnums([x])[0]
 
 
 def _jstr(v: str) -> str:
@@ -176,11 +163,14 @@ def pocket_to_json(p: Pocket) -> str:
 
 def pose_to_json(pose: Pose) -> str:
     """dock::pose_to_json (dock.cpp:476-489): compact ordered_json bytes."""
-    nums = lambda v: "[" + ",".join(_jnum(x) for x in v) + "]"
-    resc = "null" if pose.rescore is None else _jnum(pose.rescore)
-    return (f'{{"ligand":{_jstr(pose.ligand_id)},"translation":{nums(pose.translation)},'
-            f'"rotation":{nums(pose.rotation)},"torsions":{nums(pose.torsions)},'
-            f'"geometric_score":{_jnum(pose.geometric_score)},"rescore":{resc}}}')
+    t, q, th = list(pose.translation), list(pose.rotation), list(pose.torsions)
+    v = _jnums(t + q + th + [pose.geometric_score] + ([] if pose.rescore is None else [pose.rescore]))
+    nums = lambda a, b: "[" + ",".join(v[a:b]) + "]"
+    n = 7 + len(th)
+    resc = "null" if pose.rescore is None else v[n + 1]
+    return (f'{{"ligand":{_jstr(pose.ligand_id)},"translation":{nums(0, 3)},'
+            f'"rotation":{nums(3, 7)},"torsions":{nums(7, n)},'
+            f'"geometric_score":{v[n]},"rescore":{resc}}}')
 
 
 # --------------------------------------------------------------- params ---

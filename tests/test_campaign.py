@@ -129,3 +129,91 @@ def test_dock_funnel_on_gpu(Cm, tmp_path):
     assert [(r.id, r.score) for r in f.ranked] == ranked[:n_keep]
     assert st["rank"].out == n_keep
     json.loads(Cm.funnel_to_json(f))
+
+
+def _stage_lines(path, upto="rank"):
+    out = []
+    for line in open(path, "rb").read().decode().splitlines():
+        j = json.loads(line)
+        if j["kind"] in ("stage_start", "stage_end"):
+            out.append(line)
+            if j["kind"] == "stage_end" and j["stage"] == upto:
+                break
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")
+def test_campaign_trace_and_report_on_gpu(Cm, tmp_path):
+    """run_campaign's trace stage lines (TraceWriter, pipeline.cpp:335-352)
+    and report stage records for parse / embed / dock against the reference's
+    own run on campaign_100.json (tests/golden/campaign/ref_*, made by
+    make_campaign_golden.py).  The scheduler events and sim_seconds belong to
+    the simulated cluster (out of scope)."""
+    for f in ("campaign_100.json", "pocket.json", "sample_library_100.smi", "smiles.dict"):
+        shutil.copy(os.path.join(CAMP, f), tmp_path / f)
+    cfg = Cm.load_config_file(str(tmp_path / "campaign_100.json"))
+    cfg.trace_path = str(tmp_path / "out" / "trace.jsonl")
+    cfg.report_path = str(tmp_path / "out" / "report.json")
+    f = Cm.run_dock_stages(cfg, write_outputs=True)
+    assert _stage_lines(cfg.trace_path) == _stage_lines(os.path.join(CAMP, "ref_trace.jsonl"))
+    assert open(cfg.trace_path).read().count("\n") == 12
+    rep = open(cfg.report_path, "rb").read().decode()
+    assert rep == Cm.funnel_to_json(f, cfg.trace_path)
+    ours = json.loads(rep)["stages"]
+    ref = json.load(open(os.path.join(CAMP, "ref_report.json")))["stages"]
+    for a, b in zip(ours[:3], ref[:3]):
+        assert (a["name"], a["in"], a["out"], a["tasks"]) == (b["name"], b["in"], b["out"], b["tasks"])
+    assert [s["name"] for s in ours] == [s["name"] for s in ref[:6]]
+    assert ours[3]["in"] == ref[3]["in"] and ours[4]["in"] == ref[4]["in"]
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")
+def test_dock_jsonl_on_gpu(Cm, tmp_path):
+    """`vscreen dock` pose JSONL (vscreen_main.cpp:67-93) through the GPU
+    path: the reference's seeds and conformers (the reference re-scores every
+    written pose to the written scores within 1e-9), pose_to_json bytes, the
+    filter's order and limits, the records' order; a bad record stops the
+    run after the earlier records' lines with the reference's exception."""
+    R = need_ref()
+    from paper_2304_09953_b200.chem import read_library_file
+    from paper_2304_09953_b200.errors import ParseError
+    lib_path = os.path.join(CAMP, "sample_library_100.smi")
+    pocket_path = os.path.join(CAMP, "pocket.json")
+    out = tmp_path / "poses.jsonl"
+    n = Cm.dock_library_jsonl(lib_path, pocket_path, str(out), restarts=4, diversity=1.0,
+                              keep_top=3, min_score=-5.0, do_rescore=True, seed=11)
+    lines = open(out, "rb").read().decode().splitlines()
+    assert n == len(lines) > 0
+    recs = read_library_file(lib_path)
+    order = {r.id: k for k, r in enumerate(recs)}
+    rp = R.RefPocket(open(pocket_path).read())
+    by_lig = {}
+    for line in lines:
+        j = json.loads(line)
+        by_lig.setdefault(j["ligand"], []).append(j)
+        assert line == R.pose_json_bytes(j["ligand"], j["translation"], j["rotation"],
+                                         j["torsions"], j["geometric_score"], j["rescore"])
+    assert list(by_lig) == sorted(by_lig, key=order.get)  # record order
+    for lid, poses in list(by_lig.items())[::7]:
+        assert len(poses) <= 3
+        sc = [p["geometric_score"] for p in poses]
+        assert sc == sorted(sc, reverse=True) and min(sc) >= -5.0
+        i = order[lid]
+        es = int(R.rng_u64(11, [i], 1)[0])
+        ref = R.RefLigand(recs[i].smiles, embed_seed=es, iterations=200, ligand_id=lid)
+        for p in poses:
+            g = ref.geometric_score(rp, p["translation"], p["rotation"], p["torsions"])
+            r = ref.rescore(rp, p["translation"], p["rotation"], p["torsions"])
+            assert abs(g - p["geometric_score"]) <= 1e-9 * max(abs(g), 1.0)
+            assert abs(r - p["rescore"]) <= 1e-9 * max(abs(r), 1.0)
+    # a bad record: the lines before it, then ParseError
+    lines_in = open(lib_path).read().splitlines()
+    bad = tmp_path / "bad.smi"
+    bad.write_text("\n".join(lines_in[:5] + ["C1CC(\tBADX"] + lines_in[5:]) + "\n")
+    with pytest.raises(ParseError):
+        Cm.dock_library_jsonl(str(bad), pocket_path, str(tmp_path / "b.jsonl"), restarts=2,
+                              keep_top=2, seed=11)
+    ids = [json.loads(x)["ligand"] for x in open(tmp_path / "b.jsonl").read().splitlines()]
+    assert ids and set(ids) <= {r.id for r in recs[:5]}

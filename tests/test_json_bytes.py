@@ -100,3 +100,23 @@ def test_campaign_report_bytes_match_reference(tmp_path):
     cpp_json, cpp_tsv = out.split("\n--\n")
     assert cpp_json == ref
     assert cpp_tsv == ref_tsv
+
+
+def test_number_text_matches_reference_on_random_doubles():
+    """nlohmann's Grisu2 digits are not always the shortest round-trip ones
+    (about 1 value in 600 differs from Python's repr): every number the
+    Python writers print comes from capi.h vs_json_format_doubles."""
+    R = need_ref()
+    from paper_2304_09953_b200.dock import _jnums
+    rng = np.random.default_rng(7)
+    v = rng.normal(size=60000) * 10.0 ** rng.integers(-12, 13, size=60000)
+    v[::97] = np.round(v[::97])
+    bits = rng.integers(0, 2**63, size=3000, dtype=np.uint64).view(np.float64)
+    v = np.concatenate([v, bits[np.isfinite(bits)]])
+    mine = _jnums(v)
+    for k in range(0, len(v), 3):
+        chunk = v[k:k + 3]
+        if len(chunk) < 3:
+            break
+        s = R.pose_json_bytes("a", chunk, [1, 0, 0, 0], [], 0.5, None)
+        assert s.split('"translation":[')[1].split("]")[0].split(",") == mine[k:k + 3], chunk
