@@ -26,20 +26,22 @@ __device__ __forceinline__ double nrm(double x, double y, double z) {
   return sqrt(x * x + y * y + z * z);
 }
 
+// inc[ioff[k] .. ioff[k+1]): the bonds of atom k in bond order, as
+// (bond index << 1) | (k is the bond's second atom)
 __device__ void springs_dev(double* px, double* py, double* pz, double* qx, double* qy,
-                            double* qz, const int2* bd, int nb, const unsigned* bonded, int n,
-                            int iters, int lane) {
+                            double* qz, const int2* bd, const short* ioff, const short* inc,
+                            const unsigned* bonded, int n, int iters, int lane) {
   for (int it = 0; it < iters; ++it) {
     for (int k = lane; k < n; k += 32) {
       double gx = 0.0, gy = 0.0, gz = 0.0;
-      for (int e = 0; e < nb; ++e) {  // bonded rest length 1.5
+      for (int u = ioff[k]; u < ioff[k + 1]; ++u) {  // bonded rest length 1.5
+        const int e = inc[u] >> 1;
         const int a = bd[e].x, b = bd[e].y;
-        if (a != k && b != k) continue;
         const double dx = px[a] - px[b], dy = py[a] - py[b], dz = pz[a] - pz[b];
         const double len = nrm(dx, dy, dz);
         if (len < 1e-12) continue;
         const double s = 2.0 * (len - 1.5) / len;
-        if (a == k) {
+        if (!(inc[u] & 1)) {
           gx = gx + dx * s;
           gy = gy + dy * s;
           gz = gz + dz * s;
@@ -49,11 +51,16 @@ __device__ void springs_dev(double* px, double* py, double* pz, double* qx, doub
           gz = gz - dz * s;
         }
       }
+      const unsigned* bk = bonded + 4 * k;
       for (int p = 0; p < n; ++p) {  // non-bonded repulsion below 1.0
-        if (p == k || ((bonded[4 * k + (p >> 5)] >> (p & 31)) & 1u)) continue;
+        if (p == k || ((bk[p >> 5] >> (p & 31)) & 1u)) continue;
         const int a = p < k ? p : k, b = p < k ? k : p;
         const double dx = px[a] - px[b], dy = py[a] - py[b], dz = pz[a] - pz[b];
-        const double len = nrm(dx, dy, dz);
+        // sqrt is monotone and sqrt(1) = 1: |d|^2 >= 1 implies len >= 1, so
+        // the far pairs skip the square root and keep the reference's outcome
+        const double n2 = dx * dx + dy * dy + dz * dz;
+        if (n2 >= 1.0) continue;
+        const double len = sqrt(n2);
         if (len >= 1.0 || len < 1e-12) continue;
         const double s = -2.0 * (1.0 - len) / len;
         if (a == k) {
@@ -88,51 +95,80 @@ __device__ void springs_dev(double* px, double* py, double* pz, double* qx, doub
   }
 }
 
+// min over pairs of |a - b| (chem.cpp:394-400) as sqrt(min |a - b|^2): sqrt
+// is monotone and correctly rounded, so the two agree bit for bit
 __device__ double closest_dev(const double* px, const double* py, const double* pz, int n,
                               int lane) {
   double best = 1.0 / 0.0;
   for (int a = lane; a < n; a += 32)
-    for (int b = a + 1; b < n; ++b)
-      best = fmin(best, nrm(px[a] - px[b], py[a] - py[b], pz[a] - pz[b]));
+    for (int b = a + 1; b < n; ++b) {
+      const double dx = px[a] - px[b], dy = py[a] - py[b], dz = pz[a] - pz[b];
+      best = fmin(best, dx * dx + dy * dy + dz * dz);
+    }
   for (int off = 16; off > 0; off >>= 1) best = fmin(best, __shfl_xor_sync(0xffffffffu, best, off));
-  return best;
+  return sqrt(best);
 }
 
 constexpr int kRelaxMaxAtoms = 128;
 constexpr int kRelaxMaxBonds = 256;
 constexpr int kRelaxWarps = 4;
 
+// per-warp shared-memory region for ligands of <= amax atoms, <= bmax bonds
+__host__ __device__ inline size_t relax_warp_bytes(int amax, int bmax) {
+  const size_t a8 = 48u * amax;                      // p, q: 6 x amax doubles
+  const size_t b8 = 8u * bmax;                       // bonds
+  const size_t m4 = 16u * amax;                      // bonded bitmasks, 4 words per atom
+  const size_t s2 = 2u * ((amax + 2) + 2 * bmax);    // incidence offsets + lists (short)
+  return (a8 + b8 + m4 + s2 + 15u) & ~size_t(15);
+}
+
 __global__ void __launch_bounds__(kRelaxWarps * 32)
-    vs_relax_kernel(const __grid_constant__ RelaxLib L, int n, int iterations) {
-  __shared__ double sp[kRelaxWarps][6][kRelaxMaxAtoms];
-  __shared__ int2 sb[kRelaxWarps][kRelaxMaxBonds];
-  __shared__ unsigned sbond[kRelaxWarps][4 * kRelaxMaxAtoms];
+    vs_relax_kernel(const __grid_constant__ RelaxLib L, int n, int iterations, int amax,
+                    int bmax) {
+  extern __shared__ __align__(16) unsigned char relax_smem[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x * kRelaxWarps + w;
   if (i >= n) return;
   const int na = L.n_atoms[i], nb = L.n_bonds[i];
-  if (na < 2 || na > kRelaxMaxAtoms || nb > kRelaxMaxBonds) return;
-  double *px = sp[w][0], *py = sp[w][1], *pz = sp[w][2];
-  double *qx = sp[w][3], *qy = sp[w][4], *qz = sp[w][5];
+  if (na < 2 || na > amax || nb > bmax) return;
+  unsigned char* base = relax_smem + w * relax_warp_bytes(amax, bmax);
+  double* px = reinterpret_cast<double*>(base);
+  double *py = px + amax, *pz = py + amax, *qx = pz + amax, *qy = qx + amax, *qz = qy + amax;
+  int2* sb = reinterpret_cast<int2*>(qz + amax);
+  unsigned* sbond = reinterpret_cast<unsigned*>(sb + bmax);
+  short* io = reinterpret_cast<short*>(sbond + 4 * amax);
+  short* inc = io + amax + 2;
   double* c = L.coords + 3 * L.atom_off[i];
   for (int k = lane; k < na; k += 32) {
     px[k] = c[3 * k];
     py[k] = c[3 * k + 1];
     pz[k] = c[3 * k + 2];
   }
-  for (int k = lane; k < 4 * na; k += 32) sbond[w][k] = 0u;
-  for (int e = lane; e < nb; e += 32) sb[w][e] = L.bonds[L.bond_off[i] + e];
+  for (int k = lane; k < 4 * na; k += 32) sbond[k] = 0u;
+  for (int e = lane; e < nb; e += 32) sb[e] = L.bonds[L.bond_off[i] + e];
   __syncwarp();
-  if (lane == 0)
+  if (lane == 0) {
+    for (int k = 0; k <= na; ++k) io[k] = 0;
     for (int e = 0; e < nb; ++e) {
-      const int a = sb[w][e].x, b = sb[w][e].y;
-      sbond[w][4 * a + (b >> 5)] |= 1u << (b & 31);
-      sbond[w][4 * b + (a >> 5)] |= 1u << (a & 31);
+      const int a = sb[e].x, b = sb[e].y;
+      sbond[4 * a + (b >> 5)] |= 1u << (b & 31);
+      sbond[4 * b + (a >> 5)] |= 1u << (a & 31);
+      ++io[a + 1];
+      if (b != a) ++io[b + 1];
     }
+    for (int k = 0; k < na; ++k) io[k + 1] += io[k];
+    int* fill = reinterpret_cast<int*>(qx);  // scratch until the springs run
+    for (int k = 0; k < na; ++k) fill[k] = io[k];
+    for (int e = 0; e < nb; ++e) {  // bond order within each atom's list
+      const int a = sb[e].x, b = sb[e].y;
+      inc[fill[a]++] = static_cast<short>(e << 1);
+      if (b != a) inc[fill[b]++] = static_cast<short>((e << 1) | 1);
+    }
+  }
   __syncwarp();
-  springs_dev(px, py, pz, qx, qy, qz, sb[w], nb, sbond[w], na, iterations, lane);
+  springs_dev(px, py, pz, qx, qy, qz, sb, io, inc, sbond, na, iterations, lane);
   for (int round = 0; round < 20 && closest_dev(px, py, pz, na, lane) < 0.5; ++round)
-    springs_dev(px, py, pz, qx, qy, qz, sb[w], nb, sbond[w], na, 50, lane);
+    springs_dev(px, py, pz, qx, qy, qz, sb, io, inc, sbond, na, 50, lane);
   for (int k = lane; k < na; k += 32) {
     c[3 * k] = px[k];
     c[3 * k + 1] = py[k];
@@ -145,10 +181,15 @@ int relax_max_bonds() { return kRelaxMaxBonds; }
 
 cudaError_t launch_relax(cudaStream_t st, const long long* atom_off, const int* n_atoms,
                          const long long* bond_off, const int* n_bonds, const int2* bonds,
-                         double* coords, int n, int iterations) {
+                         double* coords, int n, int iterations, int amax, int bmax) {
   RelaxLib L{atom_off, n_atoms, bond_off, n_bonds, bonds, coords};
   const int blocks = (n + kRelaxWarps - 1) / kRelaxWarps;
-  if (blocks > 0) vs_relax_kernel<<<blocks, kRelaxWarps * 32, 0, st>>>(L, n, iterations);
+  const size_t smem = kRelaxWarps * relax_warp_bytes(amax, bmax);
+  cudaError_t e = cudaFuncSetAttribute(vs_relax_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  if (blocks > 0)
+    vs_relax_kernel<<<blocks, kRelaxWarps * 32, smem, st>>>(L, n, iterations, amax, bmax);
   return cudaGetLastError();
 }
 

@@ -213,6 +213,7 @@ namespace vs {
 int relax_on_device(vs_handle* h, int n, const int64_t* atom_off, const int32_t* n_atoms,
                     double* coords, const int64_t* bond_off, const int32_t* n_bonds,
                     const int32_t* bonds, int iterations);
+void* relax_host_buffer(vs_handle* h, size_t bytes);
 }
 
 extern "C" {
@@ -231,21 +232,28 @@ int vs_libbuild_relax(vs_handle* h, vs_libbuild* b, int32_t iterations) {
     aoff[i + 1] = aoff[i] + na[i];
     boff[i + 1] = boff[i] + nb[i];
   }
-  std::vector<double> xyz(static_cast<std::size_t>(3 * std::max<int64_t>(aoff[n], 1)));
-  std::vector<int32_t> bd(static_cast<std::size_t>(2 * std::max<int64_t>(boff[n], 1)));
+  // one pinned block: xyz (FP64) then the bonds, filled straight from the
+  // per-ligand vectors
+  const size_t xyz_n = static_cast<size_t>(3 * std::max<int64_t>(aoff[n], 1));
+  const size_t bd_n = static_cast<size_t>(2 * std::max<int64_t>(boff[n], 1));
+  unsigned char* pin = static_cast<unsigned char*>(
+      relax_host_buffer(h, xyz_n * sizeof(double) + bd_n * sizeof(int32_t)));
+  if (!pin) return VS_ERR_CUDA;
+  double* xyz = reinterpret_cast<double*>(pin);
+  int32_t* bd = reinterpret_cast<int32_t*>(pin + xyz_n * sizeof(double));
   for (int i = 0; i < n; ++i) {
     if (!na[i]) continue;
     const auto& l = b->ligs[i];
-    std::memcpy(xyz.data() + 3 * aoff[i], l.coords.data(), l.coords.size() * sizeof(double));
-    std::memcpy(bd.data() + 2 * boff[i], l.bonds.data(), l.bonds.size() * sizeof(int32_t));
+    std::memcpy(xyz + 3 * aoff[i], l.coords.data(), l.coords.size() * sizeof(double));
+    std::memcpy(bd + 2 * boff[i], l.bonds.data(), l.bonds.size() * sizeof(int32_t));
   }
-  const int rc = relax_on_device(h, n, aoff.data(), na.data(), xyz.data(), boff.data(), nb.data(),
-                                 bd.data(), iterations);
+  const int rc = relax_on_device(h, n, aoff.data(), na.data(), xyz, boff.data(), nb.data(), bd,
+                                 iterations);
   if (rc) return rc;
   for (int i = 0; i < n; ++i) {
     if (!na[i]) continue;
     auto& l = b->ligs[i];
-    std::memcpy(l.coords.data(), xyz.data() + 3 * aoff[i], l.coords.size() * sizeof(double));
+    std::memcpy(l.coords.data(), xyz + 3 * aoff[i], l.coords.size() * sizeof(double));
     l.bonds.clear();
     l.bonds.shrink_to_fit();
   }

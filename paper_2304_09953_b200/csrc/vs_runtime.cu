@@ -61,7 +61,7 @@ int relax_max_atoms();
 int relax_max_bonds();
 cudaError_t launch_relax(cudaStream_t st, const long long* atom_off, const int* n_atoms,
                          const long long* bond_off, const int* n_bonds, const int2* bonds,
-                         double* coords, int n, int iterations);
+                         double* coords, int n, int iterations, int amax, int bmax);
 cudaError_t launch_grad(cudaStream_t st, const LibDev& lib, const SiteD* sites, int n_sites,
                         const double lo[3], const double hi[3], double r, double lam,
                         long n_poses, const int* pose_lig, const long* tb, const double* t,
@@ -299,6 +299,8 @@ struct vs_handle {
   std::vector<std::pair<int, int>> lib_segs;
   int lib_lists_n = -1;
   DBuf rbuf[12];             // vs_rescore's pose / work arrays, reused across calls
+  DBuf ebuf[6];              // the embed relaxation's arrays, reused across calls
+  PinnedVec<unsigned char> epin;  // their pinned host staging
   double rescore_ms = -1.0;  // device time of the rescore kernels of the last vs_rescore
   std::vector<cudaStream_t> fork;  // the rescoring's per-class streams (joined back)
   std::vector<cudaEvent_t> fork_ev;
@@ -782,6 +784,7 @@ void vs_destroy(vs_handle* h) {
   for (DBuf& b : h->pwork) b.release();
   h->ptemp.release();
   for (DBuf& b : h->rbuf) b.release();
+  for (DBuf& b : h->ebuf) b.release();
   for (DBuf* b : {&h->d_sites, &h->d_softtab, &h->d_sites64, &h->d_maps, &h->d_surv, &h->d_surv_tors, &h->d_all, &h->d_all_tors,
                   &h->d_best, &h->d_nkept, &h->d_nsurv, &h->d_keys, &h->d_rots, &h->d_topk_a, &h->d_topk_b, &h->d_stats})
     b->release();
@@ -1961,6 +1964,12 @@ uint32_t vs_key_id_rank(uint64_t key) { return static_cast<uint32_t>(key & 0xfff
 }  // extern "C"
 
 namespace vs {
+// pinned staging for vs_libbuild_relax's flattened arrays (grow-only, owned
+// by the handle): the copies in relax_on_device are then plain async DMA
+void* relax_host_buffer(vs_handle* h, size_t bytes) {
+  return h->epin.resize(bytes) ? h->epin.data() : nullptr;
+}
+
 // device half of vs_libbuild_relax (vs_host.cpp): the spring relaxation of
 // embed_3d for a flattened batch of placed conformers, in place
 int relax_on_device(vs_handle* h, int n, const int64_t* atom_off, const int32_t* n_atoms,
@@ -1968,19 +1977,18 @@ int relax_on_device(vs_handle* h, int n, const int64_t* atom_off, const int32_t*
                     const int32_t* bonds, int iterations) {
   cudaSetDevice(h->device);
   if (iterations < 0) return fail(h, VS_ERR_INVALID_ARGUMENT, "iterations must be >= 0");
-  for (int i = 0; i < n; ++i)
+  int amax = 2, bmax = 1;
+  for (int i = 0; i < n; ++i) {
     if (n_atoms[i] > relax_max_atoms() || n_bonds[i] > relax_max_bonds())
       return fail(h, VS_ERR_CAPACITY, "ligand " + std::to_string(i) + " too large for the device embed");
+    amax = std::max(amax, static_cast<int>(n_atoms[i]));
+    bmax = std::max(bmax, static_cast<int>(n_bonds[i]));
+  }
   if (n == 0) return VS_OK;
   const size_t na = static_cast<size_t>(std::max<int64_t>(atom_off[n], 1));
   const size_t nbd = static_cast<size_t>(std::max<int64_t>(bond_off[n], 1));
-  DBuf d_ao, d_na, d_bo, d_nb, d_bd, d_xyz;
-  struct Release {
-    std::vector<DBuf*> bufs;
-    ~Release() {
-      for (DBuf* b : bufs) b->release();
-    }
-  } guard{{&d_ao, &d_na, &d_bo, &d_nb, &d_bd, &d_xyz}};
+  DBuf &d_ao = h->ebuf[0], &d_na = h->ebuf[1], &d_bo = h->ebuf[2], &d_nb = h->ebuf[3],
+       &d_bd = h->ebuf[4], &d_xyz = h->ebuf[5];
   cudaStream_t st = h->own;
   VS_CUDA(h, d_ao.ensure((n + 1) * 8));
   VS_CUDA(h, d_na.ensure(n * 4));
@@ -1996,7 +2004,7 @@ int relax_on_device(vs_handle* h, int n, const int64_t* atom_off, const int32_t*
   VS_CUDA(h, cudaMemcpyAsync(d_xyz.p, coords, na * 24, cudaMemcpyHostToDevice, st));
   VS_CUDA(h, launch_relax(st, d_ao.as<const long long>(), d_na.as<const int>(),
                           d_bo.as<const long long>(), d_nb.as<const int>(), d_bd.as<const int2>(),
-                          d_xyz.as<double>(), n, iterations));
+                          d_xyz.as<double>(), n, iterations, amax, bmax));
   ++h->launches;
   VS_CUDA(h, cudaMemcpyAsync(coords, d_xyz.p, na * 24, cudaMemcpyDeviceToHost, st));
   VS_CUDA(h, cudaStreamSynchronize(st));
