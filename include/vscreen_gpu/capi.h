@@ -136,6 +136,12 @@ typedef struct {
 
 typedef struct vs_handle vs_handle;
 
+/* Page-locked host memory (cudaHostAlloc, portable): library arrays and
+ * result buffers placed here move at full link rate, and vs_fetch_results /
+ * vs_dock_host DMA straight into result buffers that live in it. */
+int vs_host_alloc(int64_t bytes, void** out);
+int vs_host_free(void* p);
+
 /* ------------------------------------------------------ GPU runtime ----- */
 int vs_create(int device, vs_handle** out);
 void vs_destroy(vs_handle* h);

@@ -745,6 +745,31 @@ std::vector<int> rotation_order(const std::vector<float4>& r) {
 
 extern "C" {
 
+int vs_host_alloc(int64_t bytes, void** out) {
+  if (!out || bytes < 0) return VS_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return VS_ERR_NO_DEVICE;
+  }
+  if (cudaHostAlloc(out, static_cast<size_t>(std::max<int64_t>(bytes, 1)), cudaHostAllocPortable) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    *out = nullptr;
+    return VS_ERR_CUDA;
+  }
+  return VS_OK;
+}
+
+int vs_host_free(void* p) {
+  if (p && cudaFreeHost(p) != cudaSuccess) {
+    cudaGetLastError();
+    return VS_ERR_CUDA;
+  }
+  return VS_OK;
+}
+
 int vs_create(int device, vs_handle** out) {
   int count = 0;
   if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
@@ -1532,6 +1557,24 @@ int vs_fetch_results(vs_handle* h, vs_results* o) {
   size_t total = 0;
   const auto parts = fetch_parts(h, o, 0, static_cast<size_t>(h->res_n), 0,
                                  static_cast<size_t>(h->res_tors), &total);
+  // caller buffers in page-locked memory (cudaHostAlloc / registered): one
+  // DMA per array straight into them, no staging copy
+  bool pinned = true;
+  for (const FetchPart& p : parts) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p.dst) != cudaSuccess || a.type != cudaMemoryTypeHost) {
+      cudaGetLastError();  // clear the query's error state for unregistered memory
+      pinned = false;
+      break;
+    }
+  }
+  if (pinned) {
+    for (const FetchPart& p : parts)
+      VS_CUDA(h, cudaMemcpyAsync(p.dst, p.src, p.bytes, cudaMemcpyDeviceToHost, h->last));
+    VS_CUDA(h, cudaStreamSynchronize(h->last));
+    fetch_copy_out({}, nullptr, o, 0, h->res_cls);  // the dropped-ligand fix-ups only
+    return VS_OK;
+  }
   int rc = fetch_issue(h, parts, total, h->fetch_stage, h->last);
   if (rc) return rc;
   VS_CUDA(h, cudaStreamSynchronize(h->last));

@@ -263,6 +263,30 @@ def _check_pose_arrays(lib: Library, pose_lig: np.ndarray, t: np.ndarray, q: np.
         raise AtomCountMismatch(f"poses need {need} torsion values, got {tors.size}")
 
 
+class _PinnedOwner:
+    def __init__(self, p: int):
+        self.p = p
+
+    def __del__(self):
+        try:
+            _lib.vs_host_free(C.c_void_p(self.p))
+        except Exception:
+            pass
+
+
+def pinned_empty(shape, dtype) -> np.ndarray:
+    """An uninitialised numpy array in page-locked host memory (capi.h
+    vs_host_alloc); the memory is freed with the array's last view."""
+    dtype = np.dtype(dtype)
+    shape = (shape,) if np.isscalar(shape) else tuple(shape)
+    nbytes = int(np.prod(shape, dtype=np.int64)) * dtype.itemsize
+    p = C.c_void_p()
+    check(_lib.vs_host_alloc(max(nbytes, 1), C.byref(p)), None, "pinned host allocation")
+    buf = (C.c_uint8 * max(nbytes, 1)).from_address(p.value)
+    buf._owner = _PinnedOwner(p.value)
+    return np.frombuffer(buf, np.uint8, count=nbytes).view(dtype).reshape(shape)
+
+
 class Engine:
     """One GPU handle (vs_handle): pocket + resident library + results."""
 
@@ -329,22 +353,40 @@ class Engine:
         check(_lib.vs_dock(self._h, C.byref(self._prm_c), C.c_void_p(stream or 0)), self._h, "dock")
         self._prm = params
 
-    def fetch(self) -> DockResults:
-        return self._fetch(self._lib, self._prm, None)
+    def fetch(self, out: DockResults | None = None) -> DockResults:
+        """The last dock's results (into `out` from alloc_results, if given)."""
+        return self._fetch(self._lib, self._prm, out)
 
-    def _alloc(self, lib: Library, prm: DockParams):
+    @staticmethod
+    def alloc_results(lib: Library, prm: DockParams, pinned: bool = False) -> DockResults:
+        """Result buffers for docking `lib` with `prm`; pinned=True places
+        them in page-locked memory (pinned_empty), so vs_dock_host /
+        vs_fetch_results DMA straight into them.  Pass them back as
+        dock_host(..., out=) to reuse them across calls."""
         n, tt = len(lib), int(np.sum(lib.n_tors))
         kt, R = max(prm.keep_top, 1), prm.restarts
-        res = DockResults(best=np.zeros(max(n, 1), np.float32), n_kept=np.zeros(max(n, 1), np.int32),
-                          n_surv=np.zeros(max(n, 1), np.int32),
-                          surv=np.zeros((max(n, 1), kt), POSE_DTYPE),
-                          surv_tors=np.zeros(max(tt * kt, 1), np.float32),
-                          keys=np.zeros(max(n, 1), np.uint64),
+        mk = pinned_empty if pinned else (lambda shape, dt: np.zeros(shape, dt))
+        res = DockResults(best=mk(max(n, 1), np.float32), n_kept=mk(max(n, 1), np.int32),
+                          n_surv=mk(max(n, 1), np.int32), surv=mk((max(n, 1), kt), POSE_DTYPE),
+                          surv_tors=mk(max(tt * kt, 1), np.float32), keys=mk(max(n, 1), np.uint64),
                           tors_off=np.concatenate([[0], np.cumsum(lib.n_tors, dtype=np.int64)]),
                           keep_top=prm.keep_top, restarts=R)
         if prm.write_all_poses:
-            res.all = np.zeros((max(n, 1), R), POSE_DTYPE)
-            res.all_tors = np.zeros(max(tt * R, 1), np.float32)
+            res.all = mk((max(n, 1), R), POSE_DTYPE)
+            res.all_tors = mk(max(tt * R, 1), np.float32)
+        return res
+
+    def _alloc(self, lib: Library, prm: DockParams, out: DockResults | None = None):
+        if out is None:
+            res = self.alloc_results(lib, prm)
+        else:
+            n, tt = len(lib), int(np.sum(lib.n_tors))
+            kt = max(prm.keep_top, 1)
+            if (len(out.best) < n or out.surv.shape[1:] != (kt,) or len(out.surv) < n
+                    or out.surv_tors.size < tt * kt or out.restarts != prm.restarts
+                    or (prm.write_all_poses and out.all is None)):
+                raise ValueError("out= buffers do not fit this library and parameters")
+            res = out
         r = _capi.vs_results()
         r.best = ptr(res.best, C.c_float)
         r.n_kept = ptr(res.n_kept, C.c_int32)
@@ -357,17 +399,19 @@ class Engine:
             r.all_tors = ptr(res.all_tors, C.c_float)
         return res, r
 
-    def _fetch(self, lib, prm, _):
-        res, r = self._alloc(lib, prm)
+    def _fetch(self, lib, prm, out=None):
+        res, r = self._alloc(lib, prm, out)
         check(_lib.vs_fetch_results(self._h, C.byref(r)), self._h, "fetch")
         return _trim(res, len(lib))
 
-    def dock_host(self, lib: Library, params: DockParams, classes=None) -> DockResults:
-        """Upload + dock + fetch in one C-ABI call (host buffers in and out)."""
+    def dock_host(self, lib: Library, params: DockParams, classes=None,
+                  out: DockResults | None = None) -> DockResults:
+        """Upload + dock + fetch in one C-ABI call (host buffers in and out);
+        out: result buffers from alloc_results to write into (reused)."""
         cl, ncl = _classes_c(classes)
         lc = lib.as_c()
         pc = params.as_c()
-        res, r = self._alloc(lib, params)
+        res, r = self._alloc(lib, params, out)
         check(_lib.vs_dock_host(self._h, C.byref(lc), cl, ncl, C.byref(pc), C.byref(r)),
               self._h, "dock_host")
         self._lib, self._prm = lib, params

@@ -266,6 +266,32 @@ def test_rerun_bit_identical(V, engine, lib200, pocket_json):
     np.testing.assert_array_equal(_bits(a.surv), _bits(b.surv))
 
 
+def test_pinned_result_buffers(V, engine, lib200, pocket_json):
+    """dock_host into reused page-locked result buffers (alloc_results
+    pinned=True: the C-ABI DMAs straight into them) equals the pageable path,
+    including the dropped-ligand fix-ups, on every reuse."""
+    from paper_2304_09953_b200.dock import pinned_empty
+    lib, _ = lib200
+    engine.set_pocket(V.parse_pocket_json(pocket_json), grid_spacing=0.4)
+    prm = _params(V)
+    classes = [(0, 20, 0, 64)]  # ligands above 20 atoms are dropped
+    ref = engine.dock_host(lib, prm, classes)
+    assert (ref.n_kept == -1).any()
+    out = engine.alloc_results(lib, prm, pinned=True)
+    for _ in range(2):
+        got = engine.dock_host(lib, prm, classes, out=out)
+        for f in ("best", "n_kept", "n_surv", "keys"):
+            np.testing.assert_array_equal(getattr(got, f), getattr(ref, f), err_msg=f)
+        np.testing.assert_array_equal(_bits(got.surv), _bits(ref.surv))
+        np.testing.assert_array_equal(got.surv_tors.view(np.uint32), ref.surv_tors.view(np.uint32))
+    a = pinned_empty((3, 5), np.float64)
+    a[...] = 1.5
+    assert a.sum() == 22.5 and a.flags.c_contiguous
+    with pytest.raises(ValueError):
+        small = lib.subset(list(range(10)))
+        engine.dock_host(lib, prm, out=engine.alloc_results(small, prm))
+
+
 def test_edge_cases(V, engine, pocket_json):
     pocket = V.parse_pocket_json(pocket_json)
     engine.set_pocket(pocket)

@@ -17,7 +17,8 @@ def main(n=100_000, pinned=0):
     eng = V.Engine(0)
     eng.set_pocket(bench.make_pocket(), grid_spacing=0.4, grid_pad=2.0)
     prm = bench.params()
-    eng.dock_host(lib, prm)
+    out = eng.alloc_results(lib, prm, pinned=bool(pinned))
+    eng.dock_host(lib, prm, out=out)
     for _ in range(2):
         t0 = time.perf_counter()
         eng.upload(lib)
@@ -25,7 +26,7 @@ def main(n=100_000, pinned=0):
         eng.dock(prm)
         eng.last_dock_ms()  # synchronizes on the dock's end event
         t2 = time.perf_counter()
-        eng.fetch()
+        eng.fetch(out)
         t3 = time.perf_counter()
         eng.topk(1000)
         t4 = time.perf_counter()
@@ -33,7 +34,7 @@ def main(n=100_000, pinned=0):
               f"fetch {1e3 * (t3 - t2):.1f} ms  topk {1e3 * (t4 - t3):.1f} ms  "
               f"total {1e3 * (t4 - t0):.1f} ms  -> {n / (t4 - t0):.0f} ligands/s")
         t0 = time.perf_counter()
-        eng.dock_host(lib, prm)
+        eng.dock_host(lib, prm, out=out)
         t1 = time.perf_counter()
         eng.topk(1000)
         print(f"dock_host {1e3 * (t1 - t0):.1f} ms (device span {eng.last_dock_ms():.1f} ms) "
