@@ -127,6 +127,37 @@ __device__ __forceinline__ int floor_cell(float g, float* fl) {
   return __float_as_int(y) - 0x4B000000;
 }
 
+// Packed FP32 pairs (sm_100a FFMA2 / FADD2): two IEEE FP32 operations per
+// instruction, each element rounded exactly as its scalar form, so code
+// written with them gives the scalar code's bits with fewer issue slots.
+// A pair built from one scalar (f2s) becomes ptxas's broadcast operand.
+__device__ __forceinline__ unsigned long long f2pack(float2 v) {
+  unsigned long long u;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(u) : "f"(v.x), "f"(v.y));
+  return u;
+}
+__device__ __forceinline__ float2 f2unpack(unsigned long long u) {
+  float2 v;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(u));
+  return v;
+}
+__device__ __forceinline__ float2 f2s(float x) { return make_float2(x, x); }
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {  // a * b + c, .rn
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2pack(a)), "l"(f2pack(b)), "l"(f2pack(c)));
+  return f2unpack(d);
+}
+__device__ __forceinline__ float2 f2add_rz(float2 a, float2 b) {
+  unsigned long long d;
+  asm("add.rz.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2pack(a)), "l"(f2pack(b)));
+  return f2unpack(d);
+}
+__device__ __forceinline__ float2 f2sub(float2 a, float2 b) {  // a - b, .rn
+  unsigned long long d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2pack(a)), "l"(f2pack(b)));
+  return f2unpack(d);
+}
+
 // One trilinear lookup split in two halves so that callers can issue the
 // next lookup's loads before consuming this one.
 struct TriCell {
@@ -300,7 +331,8 @@ struct WarpSmem {
   double4* y0;    // conformer (x, y, z, class), FP64
   double4* ys;    // state local coordinates (torsions applied), FP64
   double* pose;   // flex: posed transform R (row-major 9) and t (3), FP64, warp-uniform
-  float4* ysf;    // FP32 copy of the state (sweep)
+  float4* ysf;    // FP32 copy of the state (sweep); with kLayPairs followed by
+                  // its atom pairs (pairs_of)
   float4* xf;     // posed coordinates under test (FP32, decisions)
   float* fa;      // per-atom field term of the posed state
   float* wa;      // per-atom wall term of the posed state
@@ -331,6 +363,7 @@ enum : int {
   // ysf and xf alias the conformer y0 (a kernel that no longer needs y0
   // after staging: the flex kernel) -> 32 B/atom less shared memory, more L1
   kLayAliasY0 = 128,
+  kLayPairs = 256,  // ysf's atom pairs (the grid-mode sweep key, eval_key)
   kLayAll = kLayLig | kLayState | kLaySweep | kLayPosed | kLayFlex | kLayKept,
 };
 
@@ -342,7 +375,9 @@ __host__ __device__ inline size_t warp_layout(int nmax, int tmax, int mvmax, int
       (lay & kLayLig) ? 32 * n : 0,                 // 0 y0
       (lay & kLayState) ? 32 * n : 0,               // 1 ys
       (lay & kLayFlex) ? size_t(96) : 0,                    // 2 pose
-      (lay & kLaySweep) && !(lay & kLayAliasY0) ? 16 * n : 0,  // 3 ysf
+      (lay & kLaySweep) && !(lay & kLayAliasY0)
+          ? 16 * n + ((lay & kLayPairs) ? 16 * ((n + 1) / 2) + align16(8 * ((n + 1) / 2)) : 0)
+          : 0,                                      // 3 ysf (+ pairs)
       (lay & kLayPosed) && !(lay & kLayAliasY0) ? 16 * n : 0,  // 4 xf
       (lay & kLayFlex) ? align16(4 * n) : 0,        // 5 fa
       (lay & kLayFlex) ? align16(4 * n) : 0,        // 6 wa
@@ -469,8 +504,9 @@ static __device__ __noinline__ void pose_coop(const WarpSmem& s, int N, const Ma
 }
 
 // Sweep key of one rigid pose over the FP32 state copy (SWEEP_V1.md §2.3),
-// one atom per iteration and never unrolled so the loop body stays resident
-// in the ~6 KB L0 instruction cache next to the other warps' flex loops.
+// one atom (analytic) or one atom pair (grid) per iteration and never
+// unrolled, so the loop body stays resident in the ~6 KB L0 instruction
+// cache next to the other warps' flex loops.
 //  analytic: F - lam W (parity sums of field and wall)
 //  grid:     sum of the key map K = S - lam W interpolated at the atom, the
 //            pose composed with the grid frame (g = (R/h) y + (t - o)/h) so
@@ -487,12 +523,41 @@ __device__ __forceinline__ float off_grid_term(const PocketDev& pk, float gx, fl
   return -(pk.lam * ((pk.r - w) * 10.0f));
 }
 
-// kU atoms per iteration: the kU cell loads are all issued before the first
-// interpolation, so a warp keeps kU lookups in flight; a ragged tail
-// re-reads the last atom and drops its term.  Grid mode sums the atom terms
-// in atom order into one accumulator, so every kU gives the same key bits.
-template <int kGrid, int kU = 1>
-static __device__ __forceinline__ float eval_key(const PocketDev& pk, const float4* ys, int N,
+// The atoms a sweep key reads: the FP32 state (analytic mode) and its atom
+// pairs (grid mode, built by build_pairs).
+struct KeyAtoms {
+  const float4* ysf;
+  const float4* p4;
+  const float2* p2;
+};
+
+// ysf[nmax] is followed (kLayPairs) by the atom pairs: (x0, x1, y0, y1)
+// float4s, then (z0, z1) float2s; an odd last pair repeats the last atom
+__device__ __forceinline__ KeyAtoms pairs_of(const float4* ysf, int nmax) {
+  const float4* p4 = ysf + nmax;
+  return KeyAtoms{ysf, p4, reinterpret_cast<const float2*>(p4 + (nmax + 1) / 2)};
+}
+
+// the pairs from ysf: lanes over atom pairs
+__device__ __forceinline__ void build_pairs(const KeyAtoms& ka, int N, int lane) {
+  float4* p4 = const_cast<float4*>(ka.p4);
+  float2* p2 = const_cast<float2*>(ka.p2);
+  for (int j = lane; j < (N + 1) / 2; j += 32) {
+    const float4 a = ka.ysf[2 * j], b = ka.ysf[2 * j + 1 < N ? 2 * j + 1 : N - 1];
+    p4[j] = make_float4(a.x, b.x, a.y, b.y);
+    p2[j] = make_float2(a.z, b.z);
+  }
+  __syncwarp();
+}
+
+// Grid mode takes two atoms per iteration in FP32 pairs (FFMA2 / FADD2:
+// the transform, the cell floor and fraction, the cell polynomial), every
+// element the scalar operation of SWEEP_V1.md §2.3, and sums the atom terms
+// in atom order into one FP32 accumulator: the key bits of the one-atom
+// form with ~30 % fewer issued instructions.  An odd last pair repeats the
+// last atom and drops its term.
+template <int kGrid>
+static __device__ __forceinline__ float eval_key(const PocketDev& pk, const KeyAtoms& A, int N,
                                                  const Mat3 R, float tx, float ty, float tz) {
   if (kGrid) {
     const GridDev& g = pk.grid;
@@ -503,41 +568,44 @@ static __device__ __forceinline__ float eval_key(const PocketDev& pk, const floa
     const float ux = (tx - g.ox) * ih, uy = (ty - g.oy) * ih, uz = (tz - g.oz) * ih;
     const unsigned mx = static_cast<unsigned>(g.nx - 2), my = static_cast<unsigned>(g.ny - 2),
                    mz = static_cast<unsigned>(g.nz - 2);
+    const float2 M23 = f2s(8388608.0f);
     float k = 0.0f;
 #pragma unroll 1
-    for (int i0 = 0; i0 < N; i0 += kU) {
-      float gx[kU], gy[kU], gz[kU], fx[kU], fy[kU], fz[kU];
-      bool in[kU];
-      float4 lo[kU], hi[kU];
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const float4 a = ys[i0 + u < N ? i0 + u : N - 1];
-        gx[u] = fmaf(a00, a.x, fmaf(a01, a.y, fmaf(a02, a.z, ux)));
-        gy[u] = fmaf(a10, a.x, fmaf(a11, a.y, fmaf(a12, a.z, uy)));
-        gz[u] = fmaf(a20, a.x, fmaf(a21, a.y, fmaf(a22, a.z, uz)));
-        const int ix = floor_cell(gx[u], &fx[u]), iy = floor_cell(gy[u], &fy[u]),
-                  iz = floor_cell(gz[u], &fz[u]);
-        in[u] = static_cast<unsigned>(ix) <= mx && static_cast<unsigned>(iy) <= my &&
-                static_cast<unsigned>(iz) <= mz;
-        const unsigned cell = static_cast<unsigned>(iz * g.cxy + iy * g.cx + ix);
-        ldg_hcell(g.key_h + (in[u] ? cell : 0u), lo[u], hi[u]);
-      }
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        float term;
-        if (in[u]) {  // the cell's trilinear polynomial (vs_pack_half_kernel), 7 FMAs
-          const float tx1 = gx[u] - fx[u], ty1 = gy[u] - fy[u], tz1 = gz[u] - fz[u];
-          const float4 a = lo[u], b = hi[u];  // (c000 c100 c010 c110), (c001 c101 c011 c111)
-          term = fmaf(fmaf(fmaf(b.w, tz1, a.w), ty1, fmaf(b.y, tz1, a.y)), tx1,
-                      fmaf(fmaf(b.z, tz1, a.z), ty1, fmaf(b.x, tz1, a.x)));
-        } else {
-          term = off_grid_term(pk, gx[u], gy[u], gz[u]);
-        }
-        if (kU == 1 || i0 + u < N) k = k + term;
-      }
+    for (int i0 = 0; i0 < N; i0 += 2) {
+      const float4 xy = A.p4[i0 >> 1];
+      const float2 Z = A.p2[i0 >> 1];
+      const float2 X = make_float2(xy.x, xy.y), Y = make_float2(xy.z, xy.w);
+      const float2 GX = f2fma(f2s(a00), X, f2fma(f2s(a01), Y, f2fma(f2s(a02), Z, f2s(ux))));
+      const float2 GY = f2fma(f2s(a10), X, f2fma(f2s(a11), Y, f2fma(f2s(a12), Z, f2s(uy))));
+      const float2 GZ = f2fma(f2s(a20), X, f2fma(f2s(a21), Y, f2fma(f2s(a22), Z, f2s(uz))));
+      // floor_cell of both atoms: y = g + 2^23 (RZ), floor = y - 2^23
+      const float2 FX = f2add_rz(GX, M23), FY = f2add_rz(GY, M23), FZ = f2add_rz(GZ, M23);
+      const int ix0 = __float_as_int(FX.x) - 0x4B000000, ix1 = __float_as_int(FX.y) - 0x4B000000;
+      const int iy0 = __float_as_int(FY.x) - 0x4B000000, iy1 = __float_as_int(FY.y) - 0x4B000000;
+      const int iz0 = __float_as_int(FZ.x) - 0x4B000000, iz1 = __float_as_int(FZ.y) - 0x4B000000;
+      const bool in0 = static_cast<unsigned>(ix0) <= mx && static_cast<unsigned>(iy0) <= my &&
+                       static_cast<unsigned>(iz0) <= mz;
+      const bool in1 = static_cast<unsigned>(ix1) <= mx && static_cast<unsigned>(iy1) <= my &&
+                       static_cast<unsigned>(iz1) <= mz;
+      const unsigned c0 = static_cast<unsigned>(iz0 * g.cxy + iy0 * g.cx + ix0);
+      const unsigned c1 = static_cast<unsigned>(iz1 * g.cxy + iy1 * g.cx + ix1);
+      float4 lo0, hi0, lo1, hi1;
+      ldg_hcell(g.key_h + (in0 ? c0 : 0u), lo0, hi0);
+      ldg_hcell(g.key_h + (in1 ? c1 : 0u), lo1, hi1);
+      const float2 TX = f2sub(GX, f2sub(FX, M23)), TY = f2sub(GY, f2sub(FY, M23)),
+                   TZ = f2sub(GZ, f2sub(FZ, M23));
+      // the cells' trilinear polynomials (vs_pack_half_kernel), 7 FFMA2
+      const float2 Pw = f2fma(make_float2(hi0.w, hi1.w), TZ, make_float2(lo0.w, lo1.w));
+      const float2 Py = f2fma(make_float2(hi0.y, hi1.y), TZ, make_float2(lo0.y, lo1.y));
+      const float2 Pz = f2fma(make_float2(hi0.z, hi1.z), TZ, make_float2(lo0.z, lo1.z));
+      const float2 Px = f2fma(make_float2(hi0.x, hi1.x), TZ, make_float2(lo0.x, lo1.x));
+      const float2 Tm = f2fma(f2fma(Pw, TY, Py), TX, f2fma(Pz, TY, Px));
+      k = k + (in0 ? Tm.x : off_grid_term(pk, GX.x, GY.x, GZ.x));
+      if (i0 + 1 < N) k = k + (in1 ? Tm.y : off_grid_term(pk, GX.y, GY.y, GZ.y));
     }
     return k;
   }
+  const float4* ys = A.ysf;
   float fe = 0.0f, fo = 0.0f, we = 0.0f, wo = 0.0f;
 #pragma unroll 1
   for (int i = 0; i < N; ++i) {

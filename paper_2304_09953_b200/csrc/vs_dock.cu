@@ -72,9 +72,6 @@ static __device__ VS_PHASE int start_phase(const PocketDev& pk, const Dims d,
 // ---- rigid roto-translation sweep (SWEEP_V1.md §2.3-2.4): K orientations
 // about the posed centroid (lanes over rotations), then a compass search
 // over the 26 lattice neighbours with halving steps.  FP32 key F - lam W.
-#ifndef VS_SWEEP_U
-#define VS_SWEEP_U 1  // atoms per sweep-key iteration in the staged sweep kernel
-#endif
 
 // ---- rigid compass of the polish (SWEEP_V1.md §3.5), on the FP32 state
 // copy with the sweep key.  Lane l < 31 is candidate l: 0 keeps the pose;
@@ -93,7 +90,7 @@ constexpr int kCompassLanes = 31;
 constexpr int kLongJumpIters = 4;
 
 template <int kGrid>
-static __device__ __forceinline__ int rigid_compass(const PocketDev& pk, const float4* ysf, int N,
+static __device__ __forceinline__ int rigid_compass(const PocketDev& pk, const KeyAtoms& ka, int N,
                                                     float cx, float cy, float cz, PoseF* P,
                                                     int lane) {
   float qw = P->q[0], qx = P->q[1], qy = P->q[2], qz = P->q[3];
@@ -137,7 +134,7 @@ static __device__ __forceinline__ int rigid_compass(const PocketDev& pk, const f
         if (ax == 1) v2 = neg ? ty - sc2 : ty + sc2;
         if (ax == 2) s2 = neg ? tz - sc2 : tz + sc2;
       }
-      key = eval_key<kGrid, 1>(pk, ysf, N, R2, u2, v2, s2);
+      key = eval_key<kGrid>(pk, ka, N, R2, u2, v2, s2);
     }
     int li = lane < n_lanes ? lane : 0x7fffffff;
     for (int off = 16; off > 0; off >>= 1) {
@@ -187,6 +184,7 @@ static __device__ VS_PHASE int sweep_phase(const PocketDev& pk, const Dims d,
                                                const int* __restrict__ perm, int K, int N,
                                                int lane, PoseF* P, int* n_trans, int polish) {
   const WarpSmem s = dock_smem(d);
+  const KeyAtoms ka = pairs_of(s.ysf, d.nmax);
   float qs0 = P->q[0], qs1 = P->q[1], qs2 = P->q[2], qs3 = P->q[3];
   det_quat_normalize(&qs0, &qs1, &qs2, &qs3);
   float cx = 0.0f, cy = 0.0f, cz = 0.0f;
@@ -215,7 +213,7 @@ static __device__ VS_PHASE int sweep_phase(const PocketDev& pk, const Dims d,
     const Mat3 Rk = det_quat_mat(w4, x4, y4, z4);
     float vx, vy, vz;
     det_apply(Rk, cx, cy, cz, 0.0f, 0.0f, 0.0f, &vx, &vy, &vz);
-    const float key = eval_key<kGrid, VS_SWEEP_U>(pk, s.ysf, N, Rk, Cx - vx, Cy - vy, Cz - vz);
+    const float key = eval_key<kGrid>(pk, ka, N, Rk, Cx - vx, Cy - vy, Cz - vz);
     if (key > best_key || (key == best_key && k < best_k)) {
       best_key = key;
       best_k = k;
@@ -252,7 +250,7 @@ static __device__ VS_PHASE int sweep_phase(const PocketDev& pk, const Dims d,
     P->q[1] = px;
     P->q[2] = py;
     P->q[3] = pz;
-    *n_trans += rigid_compass<kGrid>(pk, s.ysf, N, cx, cy, cz, P, lane);
+    *n_trans += rigid_compass<kGrid>(pk, ka, N, cx, cy, cz, P, lane);
     return best_k;
   }
   float sc = 1.0f;
@@ -261,7 +259,7 @@ static __device__ VS_PHASE int sweep_phase(const PocketDev& pk, const Dims d,
     float key = -INFINITY, ox = 0.0f, oy = 0.0f, oz = 0.0f;
     if (lane < 27) {
       trans_offset(lane, sc, &ox, &oy, &oz);
-      key = eval_key<kGrid, VS_SWEEP_U>(pk, s.ysf, N, RS, ptx + ox, pty + oy, ptz + oz);
+      key = eval_key<kGrid>(pk, ka, N, RS, ptx + ox, pty + oy, ptz + oz);
     }
     int li = lane < 27 ? lane : 0x7fffffff;
     for (int off = 16; off > 0; off >>= 1) {
@@ -585,6 +583,8 @@ static __device__ VS_PHASE float polish_phase(const PocketDev& pk, const Dims d,
                            static_cast<float>(v.z), 0.0f);
   }
   __syncwarp();
+  const KeyAtoms ka = pairs_of(s.ysf, d.nmax);
+  if (kGrid) build_pairs(ka, N, lane);
   float cx = 0.0f, cy = 0.0f, cz = 0.0f;
   for (int i = 0; i < N; ++i) {
     const float4 v = s.ysf[i];
@@ -596,7 +596,7 @@ static __device__ VS_PHASE float polish_phase(const PocketDev& pk, const Dims d,
   cx = cx / fN;
   cy = cy / fN;
   cz = cz / fN;
-  *n_iter += rigid_compass<kGrid>(pk, s.ysf, N, cx, cy, cz, P, lane);
+  *n_iter += rigid_compass<kGrid>(pk, ka, N, cx, cy, cz, P, lane);
   const float qw = P->q[0], qx = P->q[1], qy = P->q[2], qz = P->q[3];
   const float tx = P->t[0], ty = P->t[1], tz = P->t[2];
   __syncwarp();
@@ -853,7 +853,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_SWEEP)
                     const int* __restrict__ perm, const __grid_constant__ DockParams prm, const int* __restrict__ order,
                     int n_order, int* __restrict__ counter, int nmax,
                     const __grid_constant__ StageBufs sb) {
-  const Dims d{nmax, 0, 0, kLaySweep};
+  const Dims d{nmax, 0, 0, kLaySweep | kLayPairs};
   const WarpSmem s = dock_smem(d);
   const int lane = threadIdx.x & 31;
   if (lane == 0) mbar_init(s.bar);
@@ -864,6 +864,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_SWEEP)
     const int4 meta = lib.meta[lig];
     const int N = meta.y;
     tma_load(s.ysf, sb.ysf + meta.x, 16u * N, s.bar, phase, lane);
+    if (kGrid) build_pairs(pairs_of(s.ysf, d.nmax), N, lane);
     const long long c0 = clock64();
     const float4 pt = sb.pose[2 * lig], pq = sb.pose[2 * lig + 1];
     PoseF P;
@@ -972,7 +973,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_POLISH)
                      const __grid_constant__ DockParams prm,
                      const int* __restrict__ order, int n_order, int* __restrict__ counter,
                      int nmax, int tmax, int r, const __grid_constant__ StageBufs sb) {
-  const Dims d{nmax, tmax, 0, kLayState | kLayPosed | kLayFlex | kLaySweep};
+  const Dims d{nmax, tmax, 0, kLayState | kLayPosed | kLayFlex | kLaySweep | kLayPairs};
   const WarpSmem s = dock_smem(d);
   const int lane = threadIdx.x & 31;
   if (lane == 0) mbar_init(s.bar);
@@ -1076,8 +1077,9 @@ static int stage_blocks(K kernel, size_t smem, int sms, int n_items, int target_
 }
 
 size_t stage_smem_per_block(int nmax, int tmax, int mvmax) {
-  const int lays[4] = {kLayLig | kLayState | kLayPosed, kLaySweep,
+  const int lays[5] = {kLayLig | kLayState | kLayPosed, kLaySweep | kLayPairs,
                        kLayLig | kLayState | kLayPosed | kLayFlex | kLaySweep | kLayAliasY0,
+                       kLayState | kLayPosed | kLayFlex | kLaySweep | kLayPairs,  // polish
                        kLayLig | kLayKept};
   size_t m = 0;
   for (int l : lays) {
@@ -1097,7 +1099,7 @@ static cudaError_t staged_impl(int sms, cudaStream_t st, const LibDev& lib, cons
                                uint64_t* launches, cudaEvent_t* evs, int* kinds) {
   const size_t sm_start = kWarpsPerBlock * warp_smem_bytes(nmax, tmax, mvmax,
                                                            kLayLig | kLayState | kLayPosed);
-  const size_t sm_sweep = kWarpsPerBlock * warp_smem_bytes(nmax, 0, 0, kLaySweep);
+  const size_t sm_sweep = kWarpsPerBlock * warp_smem_bytes(nmax, 0, 0, kLaySweep | kLayPairs);
   const size_t sm_flex = kWarpsPerBlock * warp_smem_bytes(
                                               nmax, tmax, mvmax,
                                               kLayLig | kLayState | kLayPosed | kLayFlex |
@@ -1110,7 +1112,7 @@ static cudaError_t staged_impl(int sms, cudaStream_t st, const LibDev& lib, cons
   const int b_fin = stage_blocks(vs_finish_kernel<kGrid>, sm_fin, sms, n, 8);
   const size_t sm_pol = kWarpsPerBlock * warp_smem_bytes(nmax, tmax, 0,
                                                          kLayState | kLayPosed | kLayFlex |
-                                                             kLaySweep);
+                                                             kLaySweep | kLayPairs);
   const int b_pol = stage_blocks(vs_polish_kernel<kGrid>, sm_pol, sms, n, VS_MINB_POLISH);
   const int T = kWarpsPerBlock * 32;
   int c = 0;
