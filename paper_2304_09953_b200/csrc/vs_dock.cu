@@ -788,6 +788,9 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t by
   phase ^= 1u;
 }
 
+#ifndef VS_MINB_START
+#define VS_MINB_START 8
+#endif
 #ifndef VS_MINB_SWEEP
 #define VS_MINB_SWEEP 8
 #endif
@@ -799,7 +802,7 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t by
 #endif
 
 template <int kGrid>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, 8)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_START)
     vs_start_kernel(const __grid_constant__ LibDev lib, const __grid_constant__ PocketDev pk,
                     const __grid_constant__ DockParams prm,
                     const int* __restrict__ order, int n_order, int* __restrict__ counter,
@@ -1106,7 +1109,7 @@ static cudaError_t staged_impl(int sms, cudaStream_t st, const LibDev& lib, cons
                                                   kLaySweep | kLayAliasY0) +
                          sizeof(float2) * kSoftN;  // search pair-softplus table
   const size_t sm_fin = kWarpsPerBlock * warp_smem_bytes(nmax, tmax, mvmax, kLayLig | kLayKept);
-  const int b_start = stage_blocks(vs_start_kernel<kGrid>, sm_start, sms, n, 8);
+  const int b_start = stage_blocks(vs_start_kernel<kGrid>, sm_start, sms, n, VS_MINB_START);
   const int b_sweep = stage_blocks(vs_sweep_kernel<kGrid>, sm_sweep, sms, n, VS_MINB_SWEEP);
   const int b_flex = stage_blocks(vs_flex_kernel<kGrid>, sm_flex, sms, n, VS_MINB_FLEX);
   const int b_fin = stage_blocks(vs_finish_kernel<kGrid>, sm_fin, sms, n, 8);
