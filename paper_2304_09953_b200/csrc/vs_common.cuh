@@ -113,6 +113,18 @@ __device__ __forceinline__ void ldg_hcell(const uint4* c, float4& lo, float4& hi
   hi = make_float4(d.x, d.y, e.x, e.y);
 }
 
+// the same cell through the texture path (TEX: its own L1 data pipe)
+__device__ __forceinline__ void tex_hcell(unsigned long long tex, unsigned idx, float4& lo,
+                                          float4& hi) {
+  const uint4 u = tex1Dfetch<uint4>(static_cast<cudaTextureObject_t>(tex), static_cast<int>(idx));
+  const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+  const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+  const float2 d = __half22float2(*reinterpret_cast<const __half2*>(&u.z));
+  const float2 e = __half22float2(*reinterpret_cast<const __half2*>(&u.w));
+  lo = make_float4(a.x, a.y, b.x, b.y);
+  hi = make_float4(d.x, d.y, e.x, e.y);
+}
+
 // floor(g) and its integer value for a cell lookup without the XU pipe:
 // y = 2^23 + g rounded toward zero (FADD.RZ, FMA pipe) holds floor(g) in its
 // low mantissa bits for 0 <= g < 2^23, so floor(g) = y - 2^23 exactly and
@@ -556,7 +568,7 @@ __device__ __forceinline__ void build_pairs(const KeyAtoms& ka, int N, int lane)
 // in atom order into one FP32 accumulator: the key bits of the one-atom
 // form with ~30 % fewer issued instructions.  An odd last pair repeats the
 // last atom and drops its term.
-template <int kGrid>
+template <int kGrid, bool kTex = false>
 static __device__ __forceinline__ float eval_key(const PocketDev& pk, const KeyAtoms& A, int N,
                                                  const Mat3 R, float tx, float ty, float tz) {
   if (kGrid) {
@@ -590,8 +602,13 @@ static __device__ __forceinline__ float eval_key(const PocketDev& pk, const KeyA
       const unsigned c0 = static_cast<unsigned>(iz0 * g.cxy + iy0 * g.cx + ix0);
       const unsigned c1 = static_cast<unsigned>(iz1 * g.cxy + iy1 * g.cx + ix1);
       float4 lo0, hi0, lo1, hi1;
-      ldg_hcell(g.key_h + (in0 ? c0 : 0u), lo0, hi0);
-      ldg_hcell(g.key_h + (in1 ? c1 : 0u), lo1, hi1);
+      if (kTex) {
+        tex_hcell(g.key_tex, in0 ? c0 : 0u, lo0, hi0);
+        tex_hcell(g.key_tex, in1 ? c1 : 0u, lo1, hi1);
+      } else {
+        ldg_hcell(g.key_h + (in0 ? c0 : 0u), lo0, hi0);
+        ldg_hcell(g.key_h + (in1 ? c1 : 0u), lo1, hi1);
+      }
       const float2 TX = f2sub(GX, f2sub(FX, M23)), TY = f2sub(GY, f2sub(FY, M23)),
                    TZ = f2sub(GZ, f2sub(FZ, M23));
       // the cells' trilinear polynomials (vs_pack_half_kernel), 7 FFMA2

@@ -18,6 +18,16 @@
 
 #define VS_PHASE __forceinline__  // see header comment
 
+// key-map gathers through the texture path (TEX) or LDG: the sweep
+// kernel's (rotation sweep + compass) run faster on TEX (same bits), the
+// polish kernel's on LDG (profiles/e2e_pipeline_r2.txt)
+#ifndef VS_TEX_SWEEP
+#define VS_TEX_SWEEP true
+#endif
+#ifndef VS_TEX_POLISH
+#define VS_TEX_POLISH false
+#endif
+
 namespace vs {
 
 struct Dims {
@@ -89,7 +99,7 @@ constexpr int kPolishIters = 8;
 constexpr int kCompassLanes = 31;
 constexpr int kLongJumpIters = 4;
 
-template <int kGrid>
+template <int kGrid, bool kTex>
 static __device__ __forceinline__ int rigid_compass(const PocketDev& pk, const KeyAtoms& ka, int N,
                                                     float cx, float cy, float cz, PoseF* P,
                                                     int lane) {
@@ -134,7 +144,7 @@ static __device__ __forceinline__ int rigid_compass(const PocketDev& pk, const K
         if (ax == 1) v2 = neg ? ty - sc2 : ty + sc2;
         if (ax == 2) s2 = neg ? tz - sc2 : tz + sc2;
       }
-      key = eval_key<kGrid>(pk, ka, N, R2, u2, v2, s2);
+      key = eval_key<kGrid, kTex>(pk, ka, N, R2, u2, v2, s2);
     }
     int li = lane < n_lanes ? lane : 0x7fffffff;
     for (int off = 16; off > 0; off >>= 1) {
@@ -213,7 +223,7 @@ static __device__ VS_PHASE int sweep_phase(const PocketDev& pk, const Dims d,
     const Mat3 Rk = det_quat_mat(w4, x4, y4, z4);
     float vx, vy, vz;
     det_apply(Rk, cx, cy, cz, 0.0f, 0.0f, 0.0f, &vx, &vy, &vz);
-    const float key = eval_key<kGrid>(pk, ka, N, Rk, Cx - vx, Cy - vy, Cz - vz);
+    const float key = eval_key<kGrid, VS_TEX_SWEEP>(pk, ka, N, Rk, Cx - vx, Cy - vy, Cz - vz);
     if (key > best_key || (key == best_key && k < best_k)) {
       best_key = key;
       best_k = k;
@@ -250,7 +260,7 @@ static __device__ VS_PHASE int sweep_phase(const PocketDev& pk, const Dims d,
     P->q[1] = px;
     P->q[2] = py;
     P->q[3] = pz;
-    *n_trans += rigid_compass<kGrid>(pk, ka, N, cx, cy, cz, P, lane);
+    *n_trans += rigid_compass<kGrid, VS_TEX_SWEEP>(pk, ka, N, cx, cy, cz, P, lane);
     return best_k;
   }
   float sc = 1.0f;
@@ -259,7 +269,7 @@ static __device__ VS_PHASE int sweep_phase(const PocketDev& pk, const Dims d,
     float key = -INFINITY, ox = 0.0f, oy = 0.0f, oz = 0.0f;
     if (lane < 27) {
       trans_offset(lane, sc, &ox, &oy, &oz);
-      key = eval_key<kGrid>(pk, ka, N, RS, ptx + ox, pty + oy, ptz + oz);
+      key = eval_key<kGrid, VS_TEX_SWEEP>(pk, ka, N, RS, ptx + ox, pty + oy, ptz + oz);
     }
     int li = lane < 27 ? lane : 0x7fffffff;
     for (int off = 16; off > 0; off >>= 1) {
@@ -596,7 +606,7 @@ static __device__ VS_PHASE float polish_phase(const PocketDev& pk, const Dims d,
   cx = cx / fN;
   cy = cy / fN;
   cz = cz / fN;
-  *n_iter += rigid_compass<kGrid>(pk, ka, N, cx, cy, cz, P, lane);
+  *n_iter += rigid_compass<kGrid, VS_TEX_POLISH>(pk, ka, N, cx, cy, cz, P, lane);
   const float qw = P->q[0], qx = P->q[1], qy = P->q[2], qz = P->q[3];
   const float tx = P->t[0], ty = P->t[1], tz = P->t[2];
   __syncwarp();

@@ -410,7 +410,7 @@ cudaError_t launch_grid(cudaStream_t st, const PocketDev& pk, float* steric, flo
   vs_pack_kernel<<<cb, 256, 0, st>>>(g, steric, cells);
   vs_pack_kernel<<<cb, 256, 0, st>>>(g, hb, cells + 2 * nc);
   vs_pack_kernel<<<cb, 256, 0, st>>>(g, lipo, cells + 4 * nc);
-  vs_pack_half_kernel<<<cb, 256, 0, st>>>(g, key, reinterpret_cast<uint4*>(cells + 6 * nc));
+  vs_pack_half_kernel<<<cb, 256, 0, st>>>(g, key, const_cast<uint4*>(g.key_h));
   return cudaGetLastError();
 }
 

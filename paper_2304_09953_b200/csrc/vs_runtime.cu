@@ -229,6 +229,7 @@ struct StageSet {
 
 struct vs_handle {
   int device = 0;
+  cudaTextureObject_t key_tex = 0;  // the key-map cells as a linear texture
   cudaStream_t own = nullptr;
   cudaStream_t last = nullptr;
   std::string err;
@@ -808,6 +809,7 @@ void vs_destroy(vs_handle* h) {
   for (DBuf& b : h->raw) b.release();
   for (DBuf& b : h->pwork) b.release();
   h->ptemp.release();
+  if (h->key_tex) cudaDestroyTextureObject(h->key_tex);
   for (DBuf& b : h->rbuf) b.release();
   for (DBuf& b : h->ebuf) b.release();
   for (DBuf* b : {&h->d_sites, &h->d_softtab, &h->d_sites64, &h->d_maps, &h->d_surv, &h->d_surv_tors, &h->d_all, &h->d_all_tors,
@@ -932,7 +934,7 @@ int vs_set_pocket(vs_handle* h, const vs_pocket* p, double spacing, double pad) 
     const size_t cells = static_cast<size_t>(g.nx - 1) * (g.ny - 1) * (g.nz - 1);
     // cell arrays 256 B aligned: each 32 B cell is one 256-bit load (ldg_cell)
     const size_t node_bytes = (4 * nodes * sizeof(float) + 255) & ~size_t(255);
-    VS_CUDA(h, h->d_maps.ensure(node_bytes + 4 * cells * 2 * sizeof(float4)));
+    VS_CUDA(h, h->d_maps.ensure(node_bytes + 4 * cells * 2 * sizeof(float4) + 512));
     float* m = h->d_maps.as<float>();
     float4* c = reinterpret_cast<float4*>(static_cast<char*>(h->d_maps.p) + node_bytes);
     g.steric = m;
@@ -943,7 +945,23 @@ int vs_set_pocket(vs_handle* h, const vs_pocket* p, double spacing, double pad) 
     g.lipo_c = c + 4 * cells;
     g.key = m + 3 * nodes;
     g.key_c = c + 6 * cells;
-    g.key_h = reinterpret_cast<const uint4*>(c + 6 * cells);
+    // the FP16 key cells at a 512 B boundary (texture alignment) inside the
+    // key_c region, which they replace
+    g.key_h = reinterpret_cast<const uint4*>(
+        (reinterpret_cast<uintptr_t>(c + 6 * cells) + 511) & ~uintptr_t(511));
+    if (h->key_tex) cudaDestroyTextureObject(h->key_tex);
+    h->key_tex = 0;
+    {
+      cudaResourceDesc rd{};
+      rd.resType = cudaResourceTypeLinear;
+      rd.res.linear.devPtr = const_cast<uint4*>(g.key_h);
+      rd.res.linear.desc = cudaCreateChannelDesc<uint4>();
+      rd.res.linear.sizeInBytes = cells * sizeof(uint4);
+      cudaTextureDesc td{};
+      td.readMode = cudaReadModeElementType;
+      VS_CUDA(h, cudaCreateTextureObject(&h->key_tex, &rd, &td, nullptr));
+    }
+    g.key_tex = h->key_tex;
     VS_CUDA(h, launch_grid(st, pk, m, m + nodes, m + 2 * nodes, m + 3 * nodes, c));
     h->launches += 5;
     pk.grid_mode = 1;

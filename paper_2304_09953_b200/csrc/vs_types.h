@@ -42,6 +42,7 @@ struct GridDev {
   const float* key;
   const float4* key_c;
   const uint4* key_h;  // FP16 corner cells of the key map (8 halves, 16 B), the sweep's map
+  unsigned long long key_tex;  // the same cells as a linear uint4 texture (TEX path)
 };
 
 struct PocketDev {
