@@ -340,6 +340,8 @@ int vs_ligand_build(const char* smiles, uint64_t embed_seed, int32_t iterations,
  * -1: zero coordinates; VS_EMBED_PLACE_ONLY: the BFS placement only, to be
  * relaxed on the device by vs_libbuild_relax (GPU embed_3d). */
 #define VS_EMBED_PLACE_ONLY (-2)
+/* parse + topology only; embed_3d entirely on the device by vs_libbuild_embed */
+#define VS_EMBED_DEVICE (-3)
 typedef struct vs_libbuild vs_libbuild;
 int vs_libbuild_run(const char* smiles_blob, int32_t n, const uint64_t* embed_seeds,
                     int32_t iterations, int32_t threads, vs_libbuild** out);
@@ -354,6 +356,12 @@ void vs_libbuild_free(vs_libbuild* b);
  * device for every ligand built with VS_EMBED_PLACE_ONLY; FP64 in the
  * reference's operation order, bit-identical to the host embed. */
 int vs_libbuild_relax(vs_handle* h, vs_libbuild* b, int32_t iterations);
+/* The whole embed_3d (chem.cpp:404-446) on the device for every ligand built
+ * with VS_EMBED_DEVICE: the BFS tetrahedral placement with the reference Rng
+ * jitter (Box-Muller in CUDA FP64 log / cos, which may differ from glibc in
+ * the last bit, so the coordinates match the host embed to a tolerance, not
+ * bit for bit), then the relaxation above. */
+int vs_libbuild_embed(vs_handle* h, vs_libbuild* b, int32_t iterations);
 /* synthetic libraries from the reference corpus sampler: indices i of the
  * first n_want entries random_smiles(Rng(seed).split(i)) within the atom /
  * torsion bounds (inclusive); then build those entries */

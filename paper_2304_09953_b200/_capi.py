@@ -160,6 +160,7 @@ _SIGS = {
                           [P(C.c_int32)] * 5),
     "vs_libbuild_free": (None, [C.c_void_p]),
     "vs_libbuild_relax": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
+    "vs_libbuild_embed": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
     "vs_corpus_select": (C.c_int, [C.c_uint64, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
                                    C.c_int32, C.c_int64, C.c_int32, P(C.c_int64)]),
     "vs_flexible_select": (C.c_int, [C.c_uint64, C.c_int32, C.c_int32, C.c_int32, C.c_int32,

@@ -22,6 +22,7 @@ BOND_ORDER = {1: "single", 2: "double", 3: "triple", 4: "aromatic"}
 
 
 EMBED_PLACE_ONLY = -2  # capi.h VS_EMBED_PLACE_ONLY: BFS placement only
+EMBED_DEVICE = -3      # capi.h VS_EMBED_DEVICE: parse + topology; embed_3d on the device
 
 @dataclass
 class Axis:
@@ -299,22 +300,32 @@ def corpus_indices(seed: int, n: int, atoms: tuple[int, int], tors: tuple[int, i
     return out[:got]
 
 
-def _relax_on(engine, h, iterations):
-    """Placement-only build -> the spring relaxation of embed_3d on the GPU."""
+def _relax_on(engine, h, iterations, place=False):
+    """Placement-only build -> the spring relaxation of embed_3d on the GPU;
+    place: a VS_EMBED_DEVICE build -> the BFS placement there too."""
     try:
-        check(_lib.vs_libbuild_relax(engine._h, h, iterations), engine._h, "embed relax")
+        fn = _lib.vs_libbuild_embed if place else _lib.vs_libbuild_relax
+        check(fn(engine._h, h, iterations), engine._h, "device embed")
     except Exception:
         _lib.vs_libbuild_free(h)
         raise
 
 
+def _embed_mode(engine, device_place, iterations):
+    if engine is None:
+        return iterations
+    return EMBED_DEVICE if device_place else EMBED_PLACE_ONLY
+
+
 def corpus_library(seed: int, n: int, atoms: tuple[int, int], tors: tuple[int, int],
                    embed_master: int = 2024, dock_master: int = 2024, iterations: int = 200,
-                   threads: int = 8, engine=None) -> Library:
+                   threads: int = 8, engine=None, device_place: bool = False) -> Library:
     """Synthetic library: corpus entries filtered to the size
     bounds; embed seed Rng(master).split(1).split(i), dock seed .split(2)
     .split(i) with i the index in the library (pipeline.cpp:422-484).
-    With `engine`, embed_3d's spring relaxation runs on that GPU (bit-identical)."""
+    With `engine`, embed_3d's spring relaxation runs on that GPU (bit-identical);
+    device_place also moves the BFS placement there (CUDA log/cos in the
+    jitter: coordinates within a tolerance of the host embed)."""
     from .pipeline import campaign_seeds
     idx = corpus_indices(seed, n, atoms, tors, threads)
     m = len(idx)
@@ -322,10 +333,10 @@ def corpus_library(seed: int, n: int, atoms: tuple[int, int], tors: tuple[int, i
     ds = campaign_seeds(dock_master, m, stage=2)
     h = C.c_void_p()
     check(_lib.vs_libbuild_corpus(seed, ptr(idx, C.c_int64), m, ptr(es, C.c_uint64),
-                                  EMBED_PLACE_ONLY if engine is not None else iterations, threads,
+                                  _embed_mode(engine, device_place, iterations), threads,
                                   C.byref(h)))
     if engine is not None:
-        _relax_on(engine, h, iterations)
+        _relax_on(engine, h, iterations, device_place)
     ids = [f"Z{int(i)}" for i in idx]
     return _fetch_built(h, m, ids, ds)
 
@@ -375,12 +386,13 @@ def _fetch_built(h, n, ids, ds, drop_failed=True) -> Library:
 def build_library(smiles: Sequence[str], ids: Sequence[str] | None = None,
                   embed_seeds: Sequence[int] | None = None, dock_seeds: Sequence[int] | None = None,
                   iterations: int = 200, threads: int = 8, drop_failed: bool = True,
-                  engine=None) -> Library:
+                  engine=None, device_place: bool = False) -> Library:
     """Parse + embed + topology for many ligands on `threads` host threads
     (the parse/embed stages of run_campaign, pipeline.cpp:383-431).  With
     `engine` (a dock.Engine), the host does parse, topology and embed_3d's
     BFS placement, and the spring relaxation runs on the GPU (bit-identical
-    coordinates)."""
+    coordinates); with device_place the whole embed_3d runs on
+    the GPU (coordinates within a tolerance: CUDA log/cos in the jitter)."""
     n = len(smiles)
     ids = list(ids) if ids is not None else [f"L{i + 1}" for i in range(n)]
     es = np.array([int(s) & (2**64 - 1) for s in (embed_seeds if embed_seeds is not None else [0] * n)],
@@ -388,10 +400,9 @@ def build_library(smiles: Sequence[str], ids: Sequence[str] | None = None,
     blob = b"".join(s.encode() + b"\0" for s in smiles) or b"\0"
     h = C.c_void_p()
     check(_lib.vs_libbuild_run(blob, n, ptr(es, C.c_uint64),
-                               EMBED_PLACE_ONLY if engine is not None else iterations, threads,
-                               C.byref(h)))
+                               _embed_mode(engine, device_place, iterations), threads, C.byref(h)))
     if engine is not None:
-        _relax_on(engine, h, iterations)
+        _relax_on(engine, h, iterations, device_place)
     ds = np.array([int(s) & (2**64 - 1) for s in (dock_seeds if dock_seeds is not None else [0] * n)],
                   np.uint64)
     return _fetch_built(h, n, ids, ds, drop_failed)

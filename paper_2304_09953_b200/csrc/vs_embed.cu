@@ -7,7 +7,8 @@
 //   step = grad * -0.05, clipped to length 0.2, pos += step for every atom.
 // Lanes own atoms (no cross-lane sums); the new positions go to a second
 // buffer so every gradient sees the previous iteration's positions.  The
-// BFS placement (RNG jitter through glibc log/cos) stays on the host.
+// BFS placement runs on the host (bit-identical: glibc log/cos for the
+// jitter) or, with seeds, here (place_dev: CUDA log/cos, within a tolerance).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -20,7 +21,88 @@ struct RelaxLib {
   const int* n_bonds;
   const int2* bonds;
   double* coords;  // [3 * atoms], in / out
+  const unsigned long long* seeds;  // embed seeds: place first (nullptr: relax only)
 };
+
+// Rng (rng.hpp:14-41) at explicit counters: split(0x3d) of Rng(seed), normal
+// draw j from counters 2j + 1, 2j + 2 (single-value Box-Muller, no cache)
+__device__ __forceinline__ unsigned long long emix(unsigned long long z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+constexpr unsigned long long kGold = 0x9e3779b97f4a7c15ull;
+__device__ __forceinline__ double enormal(unsigned long long key, long j) {
+  const unsigned long long a = emix(key + kGold * static_cast<unsigned long long>(2 * j + 1));
+  const unsigned long long b = emix(key + kGold * static_cast<unsigned long long>(2 * j + 2));
+  const double u1 = static_cast<double>((a >> 11) + 1) * 0x1.0p-53;
+  const double u2 = static_cast<double>(b >> 11) * 0x1.0p-53;
+  return sqrt(-2.0 * log(u1)) * cos(2.0 * 3.14159265358979323846 * u2);
+}
+
+// BFS tetrahedral placement (chem.cpp:410-432): lane 0 walks the BFS (the
+// neighbours of an atom in bond order = its incidence list), the lanes draw
+// 32 placements' jitter at a time, lane 0 places them in BFS order:
+// pos[w] = (pos[v] + dir * 1.5) + jit * 0.05.  Scratch: the q arrays.
+__device__ void place_dev(double* px, double* py, double* pz, double* q, const int2* bd,
+                          const short* io, const short* inc, int n, unsigned long long seed,
+                          int lane) {
+  int* ord = reinterpret_cast<int*>(q);  // BFS order (ord[0] = atom 0)
+  int* par = ord + n;                    // parent of ord[m]
+  int* slot = par + n;                   // tetrahedral direction of ord[m]
+  int* kids = slot + n;                  // children placed so far
+  int* seen = kids + n;
+  if (lane == 0) {
+    for (int k = 0; k < n; ++k) {
+      kids[k] = 0;
+      seen[k] = 0;
+      px[k] = py[k] = pz[k] = 0.0;
+    }
+    ord[0] = 0;
+    seen[0] = 1;
+    int tail = 1;
+    for (int qi = 0; qi < tail; ++qi) {
+      const int v = ord[qi];
+      for (int u = io[v]; u < io[v + 1]; ++u) {
+        const int e = inc[u] >> 1;
+        const int w = (inc[u] & 1) ? bd[e].x : bd[e].y;
+        if (seen[w]) continue;
+        seen[w] = 1;
+        par[tail] = v;
+        slot[tail] = kids[v] % 4;
+        ++kids[v];
+        ord[tail++] = w;
+      }
+    }
+  }
+  __syncwarp();
+  const unsigned long long root = emix(seed ^ kGold);
+  const unsigned long long key = emix(root ^ emix(0x3dull + kGold));
+  const double t = 1.0 / sqrt(3.0);
+  for (int c = 1; c < n; c += 32) {
+    const int m = c + lane;  // placement m - 1 draws normals 3(m-1) .. 3(m-1) + 2
+    double jx = 0.0, jy = 0.0, jz = 0.0;
+    if (m < n) {
+      jx = enormal(key, 3L * (m - 1));
+      jy = enormal(key, 3L * (m - 1) + 1);
+      jz = enormal(key, 3L * (m - 1) + 2);
+    }
+    for (int k = 0; k < 32 && c + k < n; ++k) {
+      const double ax = __shfl_sync(0xffffffffu, jx, k), ay = __shfl_sync(0xffffffffu, jy, k),
+                   az = __shfl_sync(0xffffffffu, jz, k);
+      if (lane == 0) {
+        const int w = ord[c + k], v = par[c + k], sl = slot[c + k];
+        const double dx = (sl == 0 || sl == 1) ? t : -t;
+        const double dy = (sl == 0 || sl == 2) ? t : -t;
+        const double dz = (sl == 0 || sl == 3) ? t : -t;
+        px[w] = (px[v] + dx * 1.5) + ax * 0.05;
+        py[w] = (py[v] + dy * 1.5) + ay * 0.05;
+        pz[w] = (pz[v] + dz * 1.5) + az * 0.05;
+      }
+    }
+  }
+  __syncwarp();
+}
 
 __device__ __forceinline__ double nrm(double x, double y, double z) {
   return sqrt(x * x + y * y + z * z);
@@ -139,10 +221,12 @@ __global__ void __launch_bounds__(kRelaxWarps * 32)
   short* io = reinterpret_cast<short*>(sbond + 4 * amax);
   short* inc = io + amax + 2;
   double* c = L.coords + 3 * L.atom_off[i];
-  for (int k = lane; k < na; k += 32) {
-    px[k] = c[3 * k];
-    py[k] = c[3 * k + 1];
-    pz[k] = c[3 * k + 2];
+  if (!L.seeds) {
+    for (int k = lane; k < na; k += 32) {
+      px[k] = c[3 * k];
+      py[k] = c[3 * k + 1];
+      pz[k] = c[3 * k + 2];
+    }
   }
   for (int k = lane; k < 4 * na; k += 32) sbond[k] = 0u;
   for (int e = lane; e < nb; e += 32) sb[e] = L.bonds[L.bond_off[i] + e];
@@ -166,6 +250,7 @@ __global__ void __launch_bounds__(kRelaxWarps * 32)
     }
   }
   __syncwarp();
+  if (L.seeds) place_dev(px, py, pz, qx, sb, io, inc, na, L.seeds[i], lane);
   springs_dev(px, py, pz, qx, qy, qz, sb, io, inc, sbond, na, iterations, lane);
   for (int round = 0; round < 20 && closest_dev(px, py, pz, na, lane) < 0.5; ++round)
     springs_dev(px, py, pz, qx, qy, qz, sb, io, inc, sbond, na, 50, lane);
@@ -181,8 +266,9 @@ int relax_max_bonds() { return kRelaxMaxBonds; }
 
 cudaError_t launch_relax(cudaStream_t st, const long long* atom_off, const int* n_atoms,
                          const long long* bond_off, const int* n_bonds, const int2* bonds,
-                         double* coords, int n, int iterations, int amax, int bmax) {
-  RelaxLib L{atom_off, n_atoms, bond_off, n_bonds, bonds, coords};
+                         double* coords, int n, int iterations, int amax, int bmax,
+                         const unsigned long long* seeds) {
+  RelaxLib L{atom_off, n_atoms, bond_off, n_bonds, bonds, coords, seeds};
   const int blocks = (n + kRelaxWarps - 1) / kRelaxWarps;
   const size_t smem = kRelaxWarps * relax_warp_bytes(amax, bmax);
   cudaError_t e = cudaFuncSetAttribute(vs_relax_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -36,6 +36,8 @@ struct BuiltLigand {
   std::vector<double> coords;
   std::vector<int> cls;
   std::vector<int> bonds;  // (a, b) pairs, kept for the device spring relaxation
+  std::uint64_t seed = 0;  // embed seed (VS_EMBED_DEVICE: the placement runs on the device)
+  bool place = false;      // built with VS_EMBED_DEVICE
   Topology topo;
 };
 
@@ -49,8 +51,15 @@ BuiltLigand build_one(const std::string& smiles, std::uint64_t seed, int iterati
     for (std::size_t i = 0; i < g.elements.size(); ++i) b.cls[i] = element_class(g.elements[i]);
     if (iterations >= 0) {
       b.coords = embed(g, seed, iterations);
-    } else if (iterations == VS_EMBED_PLACE_ONLY) {
-      b.coords = embed_place(g, seed);
+    } else if (iterations == VS_EMBED_PLACE_ONLY || iterations == VS_EMBED_DEVICE) {
+      if (iterations == VS_EMBED_PLACE_ONLY) {
+        b.coords = embed_place(g, seed);
+      } else {
+        require_connected(g);
+        b.coords.assign(3 * g.elements.size(), 0.0);
+        b.seed = seed;
+        b.place = true;
+      }
       b.bonds.reserve(2 * g.bonds.size());
       for (const auto& e : g.bonds) {
         b.bonds.push_back(e.a);
@@ -212,25 +221,29 @@ void vs_libbuild_free(vs_libbuild* b) { delete b; }
 namespace vs {
 int relax_on_device(vs_handle* h, int n, const int64_t* atom_off, const int32_t* n_atoms,
                     double* coords, const int64_t* bond_off, const int32_t* n_bonds,
-                    const int32_t* bonds, int iterations);
+                    const int32_t* bonds, int iterations, const uint64_t* place_seeds);
 void* relax_host_buffer(vs_handle* h, size_t bytes);
 }
 
 extern "C" {
 
-// Spring relaxation (chem.cpp:355-392, 434-445) of every ligand built with
-// iterations = VS_EMBED_PLACE_ONLY, on the device; coordinates updated in place.
-int vs_libbuild_relax(vs_handle* h, vs_libbuild* b, int32_t iterations) {
+namespace {
+// the device half of embed_3d for the ligands built with `mode`
+// (VS_EMBED_PLACE_ONLY: spring relaxation; VS_EMBED_DEVICE: BFS placement +
+// relaxation); coordinates updated in place
+int embed_on_device(vs_handle* h, vs_libbuild* b, int32_t iterations, bool place) {
   const int n = static_cast<int>(b->ligs.size());
   std::vector<int64_t> aoff(n + 1, 0), boff(n + 1, 0);
   std::vector<int32_t> na(n, 0), nb(n, 0);
+  std::vector<uint64_t> seeds(place ? std::max(n, 1) : 0, 0);
   for (int i = 0; i < n; ++i) {
     const auto& l = b->ligs[i];
-    const bool use = l.status == 0 && !l.bonds.empty() && l.bonds.size() / 2 >= 1;
+    const bool use = l.status == 0 && l.place == place && !l.bonds.empty();
     na[i] = use ? static_cast<int32_t>(l.coords.size() / 3) : 0;
     nb[i] = use ? static_cast<int32_t>(l.bonds.size() / 2) : 0;
     aoff[i + 1] = aoff[i] + na[i];
     boff[i + 1] = boff[i] + nb[i];
+    if (place) seeds[i] = l.seed;
   }
   // one pinned block: xyz (FP64) then the bonds, filled straight from the
   // per-ligand vectors
@@ -248,7 +261,7 @@ int vs_libbuild_relax(vs_handle* h, vs_libbuild* b, int32_t iterations) {
     std::memcpy(bd + 2 * boff[i], l.bonds.data(), l.bonds.size() * sizeof(int32_t));
   }
   const int rc = relax_on_device(h, n, aoff.data(), na.data(), xyz, boff.data(), nb.data(), bd,
-                                 iterations);
+                                 iterations, place ? seeds.data() : nullptr);
   if (rc) return rc;
   for (int i = 0; i < n; ++i) {
     if (!na[i]) continue;
@@ -256,8 +269,22 @@ int vs_libbuild_relax(vs_handle* h, vs_libbuild* b, int32_t iterations) {
     std::memcpy(l.coords.data(), xyz + 3 * aoff[i], l.coords.size() * sizeof(double));
     l.bonds.clear();
     l.bonds.shrink_to_fit();
+    l.place = false;
   }
   return VS_OK;
+}
+}  // namespace
+
+// Spring relaxation (chem.cpp:355-392, 434-445) of every ligand built with
+// iterations = VS_EMBED_PLACE_ONLY, on the device; coordinates updated in place.
+int vs_libbuild_relax(vs_handle* h, vs_libbuild* b, int32_t iterations) {
+  return embed_on_device(h, b, iterations, false);
+}
+
+// The whole embed_3d (chem.cpp:404-446: BFS placement with the Rng jitter,
+// then the relaxation) of every ligand built with VS_EMBED_DEVICE.
+int vs_libbuild_embed(vs_handle* h, vs_libbuild* b, int32_t iterations) {
+  return embed_on_device(h, b, iterations, true);
 }
 
 // Scan corpus::random_smiles(Rng(seed).split(i)) for i = 0, 1, ... and keep

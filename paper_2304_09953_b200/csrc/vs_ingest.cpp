@@ -396,32 +396,45 @@ std::vector<double> embed_place(const Graph& g, std::uint64_t seed) {
   return embed(g, seed, -1);
 }
 
-std::vector<double> embed(const Graph& g, std::uint64_t seed, int iterations) {
-  const std::size_t n = g.elements.size();
-  std::vector<V3> pos(n, V3{0, 0, 0});
-  if (n == 0) return {};
-  std::vector<std::vector<int>> adj(n);
+namespace {
+std::vector<std::vector<int>> adjacency(const Graph& g) {
+  std::vector<std::vector<int>> adj(g.elements.size());
   for (const auto& b : g.bonds) {
     adj[b.a].push_back(b.b);
     adj[b.b].push_back(b.a);
   }
-  {  // connectivity (chem.cpp:408)
-    std::vector<char> vis(n, 0);
-    std::vector<int> st{0};
-    vis[0] = 1;
-    std::size_t cnt = 1;
-    while (!st.empty()) {
-      const int v = st.back();
-      st.pop_back();
-      for (int w : adj[v])
-        if (!vis[w]) {
-          vis[w] = 1;
-          ++cnt;
-          st.push_back(w);
-        }
-    }
-    if (cnt != n) throw std::runtime_error("graph is not connected");
+  return adj;
+}
+
+void require_connected(const std::vector<std::vector<int>>& adj) {  // chem.cpp:408
+  const std::size_t n = adj.size();
+  if (n == 0) return;
+  std::vector<char> vis(n, 0);
+  std::vector<int> st{0};
+  vis[0] = 1;
+  std::size_t cnt = 1;
+  while (!st.empty()) {
+    const int v = st.back();
+    st.pop_back();
+    for (int w : adj[v])
+      if (!vis[w]) {
+        vis[w] = 1;
+        ++cnt;
+        st.push_back(w);
+      }
   }
+  if (cnt != n) throw std::runtime_error("graph is not connected");
+}
+}  // namespace
+
+void require_connected(const Graph& g) { require_connected(adjacency(g)); }
+
+std::vector<double> embed(const Graph& g, std::uint64_t seed, int iterations) {
+  const std::size_t n = g.elements.size();
+  std::vector<V3> pos(n, V3{0, 0, 0});
+  if (n == 0) return {};
+  const std::vector<std::vector<int>> adj = adjacency(g);
+  require_connected(adj);
   const double s3 = std::sqrt(3.0);
   const V3 tetra[4] = {{1 / s3, 1 / s3, 1 / s3},
                        {1 / s3, -1 / s3, -1 / s3},

@@ -43,6 +43,8 @@ int rotatable_bond_count(const Graph& g);
 Topology torsion_axes(const Graph& g);
 std::vector<double> embed(const Graph& g, std::uint64_t seed, int iterations);
 std::vector<double> embed_place(const Graph& g, std::uint64_t seed);
+// embed_3d's DisconnectedGraph check (chem.cpp:408): throws if not connected
+void require_connected(const Graph& g);
 int element_class(const std::string& el);
 std::string random_smiles(std::uint64_t seed, std::uint64_t index);
 

@@ -61,7 +61,8 @@ int relax_max_atoms();
 int relax_max_bonds();
 cudaError_t launch_relax(cudaStream_t st, const long long* atom_off, const int* n_atoms,
                          const long long* bond_off, const int* n_bonds, const int2* bonds,
-                         double* coords, int n, int iterations, int amax, int bmax);
+                         double* coords, int n, int iterations, int amax, int bmax,
+                         const unsigned long long* seeds);
 cudaError_t launch_grad(cudaStream_t st, const LibDev& lib, const SiteD* sites, int n_sites,
                         const double lo[3], const double hi[3], double r, double lam,
                         long n_poses, const int* pose_lig, const long* tb, const double* t,
@@ -300,7 +301,7 @@ struct vs_handle {
   std::vector<std::pair<int, int>> lib_segs;
   int lib_lists_n = -1;
   DBuf rbuf[12];             // vs_rescore's pose / work arrays, reused across calls
-  DBuf ebuf[6];              // the embed relaxation's arrays, reused across calls
+  DBuf ebuf[7];              // the device embed's arrays, reused across calls
   PinnedVec<unsigned char> epin;  // their pinned host staging
   double rescore_ms = -1.0;  // device time of the rescore kernels of the last vs_rescore
   std::vector<cudaStream_t> fork;  // the rescoring's per-class streams (joined back)
@@ -2035,7 +2036,7 @@ void* relax_host_buffer(vs_handle* h, size_t bytes) {
 // embed_3d for a flattened batch of placed conformers, in place
 int relax_on_device(vs_handle* h, int n, const int64_t* atom_off, const int32_t* n_atoms,
                     double* coords, const int64_t* bond_off, const int32_t* n_bonds,
-                    const int32_t* bonds, int iterations) {
+                    const int32_t* bonds, int iterations, const uint64_t* place_seeds) {
   cudaSetDevice(h->device);
   if (iterations < 0) return fail(h, VS_ERR_INVALID_ARGUMENT, "iterations must be >= 0");
   int amax = 2, bmax = 1;
@@ -2049,7 +2050,7 @@ int relax_on_device(vs_handle* h, int n, const int64_t* atom_off, const int32_t*
   const size_t na = static_cast<size_t>(std::max<int64_t>(atom_off[n], 1));
   const size_t nbd = static_cast<size_t>(std::max<int64_t>(bond_off[n], 1));
   DBuf &d_ao = h->ebuf[0], &d_na = h->ebuf[1], &d_bo = h->ebuf[2], &d_nb = h->ebuf[3],
-       &d_bd = h->ebuf[4], &d_xyz = h->ebuf[5];
+       &d_bd = h->ebuf[4], &d_xyz = h->ebuf[5], &d_seed = h->ebuf[6];
   cudaStream_t st = h->own;
   VS_CUDA(h, d_ao.ensure((n + 1) * 8));
   VS_CUDA(h, d_na.ensure(n * 4));
@@ -2063,9 +2064,14 @@ int relax_on_device(vs_handle* h, int n, const int64_t* atom_off, const int32_t*
   VS_CUDA(h, cudaMemcpyAsync(d_nb.p, n_bonds, n * 4, cudaMemcpyHostToDevice, st));
   VS_CUDA(h, cudaMemcpyAsync(d_bd.p, bonds, nbd * 8, cudaMemcpyHostToDevice, st));
   VS_CUDA(h, cudaMemcpyAsync(d_xyz.p, coords, na * 24, cudaMemcpyHostToDevice, st));
+  if (place_seeds) {
+    VS_CUDA(h, d_seed.ensure(n * 8));
+    VS_CUDA(h, cudaMemcpyAsync(d_seed.p, place_seeds, n * 8, cudaMemcpyHostToDevice, st));
+  }
   VS_CUDA(h, launch_relax(st, d_ao.as<const long long>(), d_na.as<const int>(),
                           d_bo.as<const long long>(), d_nb.as<const int>(), d_bd.as<const int2>(),
-                          d_xyz.as<double>(), n, iterations, amax, bmax));
+                          d_xyz.as<double>(), n, iterations, amax, bmax,
+                          place_seeds ? d_seed.as<const unsigned long long>() : nullptr));
   ++h->launches;
   VS_CUDA(h, cudaMemcpyAsync(coords, d_xyz.p, na * 24, cudaMemcpyDeviceToHost, st));
   VS_CUDA(h, cudaStreamSynchronize(st));

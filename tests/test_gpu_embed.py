@@ -57,3 +57,30 @@ def test_device_embed_throughput(engine):
     corpus_library(5, 20000, (10, 40), (0, 10), threads=16, engine=engine)
     td = time.perf_counter() - t0
     print(f"library build 20k: host embed {th:.2f} s, device relax {td:.2f} s")
+
+
+def test_device_placement_within_tolerance(engine):
+    """The whole embed_3d on the device (vs_libbuild_embed: BFS placement +
+    relaxation): the jitter's Box-Muller uses CUDA's FP64 log / cos, which
+    can differ from glibc in the last bit, so the coordinates match the host
+    embed within a tolerance, and every other field exactly."""
+    from paper_2304_09953_b200.chem import corpus_library
+    host = corpus_library(99, 3000, (1, 40), (0, 10), threads=16)
+    dev = corpus_library(99, 3000, (1, 40), (0, 10), threads=16, engine=engine, device_place=True)
+    assert host.ids == dev.ids
+    for f in ("n_atoms", "n_tors", "rot_bonds", "atom_class", "axis_a", "axis_b", "moving_count",
+              "moving", "seeds"):
+        np.testing.assert_array_equal(getattr(host, f), getattr(dev, f), err_msg=f)
+    d = np.abs(host.coords - dev.coords).max(axis=1)
+    ao, _, _ = host.offsets()
+    per_lig = np.maximum.reduceat(d, ao[:-1])
+    same = float(np.mean(per_lig == 0.0))
+    print(f"device placement: {same:.3f} of ligands bit-identical, max |dx| {d.max():.3e}, "
+          f"p99 {np.quantile(per_lig, 0.99):.3e}")
+    assert same > 0.5
+    assert d.max() < 1e-10
+    # placement alone (no springs): the last-bit jitter differences only
+    h0 = corpus_library(99, 500, (1, 40), (0, 10), threads=16, iterations=0)
+    d0 = corpus_library(99, 500, (1, 40), (0, 10), threads=16, iterations=0, engine=engine,
+                        device_place=True)
+    assert np.abs(h0.coords - d0.coords).max() < 1e-12
