@@ -3,7 +3,8 @@
 
 Python surface of proj/bindings/module.cpp restricted to the hot path:
 `dock_smiles`, `rmsd`, `target_batch_size`, `simulate_throughput`,
-`rank_ligands` (plus the chem loaders that feed it).  Library-scale
+`rank_ligands`, `run_campaign` (its dock funnel), plus the chem loaders
+that feed it.  Library-scale
 screening is `pipeline.screen` / `dock.Engine`.
 """
 from __future__ import annotations
@@ -24,6 +25,19 @@ from .errors import (AtomCountMismatch, EmptyBounds, ItemTooLarge, LengthMismatc
 from .pipeline import RankedLigand, rank_ligands, screen
 
 __version__ = "0.1.0"
+
+
+def run_campaign(config_path: str) -> dict:
+    """module.cpp:320-325 restricted to the hot path: the dock funnel of
+    pipeline::run_campaign (parse -> embed -> dock -> rescore -> filter ->
+    rank) on the GPU for the campaign config at `config_path`, writing the
+    trace stage lines and the report like the reference; returns the report
+    as a dict.  The pair / FEP stages are out of scope, so
+    `pairs` is empty and the report ends at the rank stage."""
+    from .campaign import load_config_file, run_dock_stages, funnel_to_json
+    cfg = load_config_file(config_path)
+    f = run_dock_stages(cfg, write_outputs=True)
+    return _json.loads(funnel_to_json(f, cfg.trace_path))
 
 
 def dock_smiles(smiles: str, pocket_json: str, restarts: int = 4, diversity_delta: float = 1.0,

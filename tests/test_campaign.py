@@ -166,6 +166,15 @@ def test_campaign_trace_and_report_on_gpu(Cm, tmp_path):
         assert (a["name"], a["in"], a["out"], a["tasks"]) == (b["name"], b["in"], b["out"], b["tasks"])
     assert [s["name"] for s in ours] == [s["name"] for s in ref[:6]]
     assert ours[3]["in"] == ref[3]["in"] and ours[4]["in"] == ref[4]["in"]
+    # the pybind-style entry point (module.cpp:320-325) over the same config
+    import paper_2304_09953_b200 as V
+    j = json.load(open(tmp_path / "campaign_100.json"))
+    j["trace"] = str(tmp_path / "out2" / "trace.jsonl")
+    j["report"] = str(tmp_path / "out2" / "report.json")
+    (tmp_path / "c2.json").write_text(json.dumps(j))
+    rep2 = V.run_campaign(str(tmp_path / "c2.json"))
+    assert rep2 == json.loads(rep) | {"trace_path": j["trace"]}
+    assert _stage_lines(j["trace"]) == _stage_lines(cfg.trace_path)
 
 
 @pytest.mark.gpu
