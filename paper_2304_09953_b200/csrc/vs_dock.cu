@@ -805,7 +805,7 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t by
 #define VS_MINB_SWEEP 8
 #endif
 #ifndef VS_MINB_POLISH
-#define VS_MINB_POLISH 6  // 85 registers: fewer spills in the compass (4/5/8/10: slower)
+#define VS_MINB_POLISH 7  // 72 registers (4/5/6/8/10: slower, profiles/e2e_pipeline_r2.txt)
 #endif
 #ifndef VS_MINB_FLEX
 #define VS_MINB_FLEX 8
