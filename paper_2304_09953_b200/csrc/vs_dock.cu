@@ -807,6 +807,12 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t by
 #ifndef VS_MINB_POLISH
 #define VS_MINB_POLISH 7  // 72 registers (4/5/6/8/10: slower, profiles/e2e_pipeline_r2.txt)
 #endif
+// the polish for ligands above kPolishSmallAtoms atoms (C4-size): fewer
+// blocks, more registers
+#ifndef VS_MINB_POLISH_BIG
+#define VS_MINB_POLISH_BIG 6
+#endif
+constexpr int kPolishSmallAtoms = 48;
 #ifndef VS_MINB_FLEX
 #define VS_MINB_FLEX 8
 #endif
@@ -980,8 +986,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_FLEX)
 // compass runs here rather than in the flex kernel so it gets this kernel's
 // small shared-memory footprint (no conformer / topology) and a large L1 for
 // its key-map lookups.
-template <int kGrid>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_POLISH)
+template <int kGrid, int kMinB>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinB)
     vs_polish_kernel(const __grid_constant__ LibDev lib, const __grid_constant__ PocketDev pk,
                      const __grid_constant__ DockParams prm,
                      const int* __restrict__ order, int n_order, int* __restrict__ counter,
@@ -1126,7 +1132,12 @@ static cudaError_t staged_impl(int sms, cudaStream_t st, const LibDev& lib, cons
   const size_t sm_pol = kWarpsPerBlock * warp_smem_bytes(nmax, tmax, 0,
                                                          kLayState | kLayPosed | kLayFlex |
                                                              kLaySweep | kLayPairs);
-  const int b_pol = stage_blocks(vs_polish_kernel<kGrid>, sm_pol, sms, n, VS_MINB_POLISH);
+  const bool pol_small = nmax <= kPolishSmallAtoms;
+  const int b_pol = pol_small
+                        ? stage_blocks(vs_polish_kernel<kGrid, VS_MINB_POLISH>, sm_pol, sms, n,
+                                       VS_MINB_POLISH)
+                        : stage_blocks(vs_polish_kernel<kGrid, VS_MINB_POLISH_BIG>, sm_pol, sms, n,
+                                       VS_MINB_POLISH_BIG);
   const int T = kWarpsPerBlock * 32;
   int c = 0;
   auto mark = [&](int kind, bool after) {  // event pair c: launch c (counter c)
@@ -1153,8 +1164,12 @@ static cudaError_t staged_impl(int sms, cudaStream_t st, const LibDev& lib, cons
     *launches += 3;
     if (prm.polish >= 1) {
       mark(4, false);
-      vs_polish_kernel<kGrid><<<b_pol, T, sm_pol, st>>>(lib, pk, prm, order, n, counters + c,
-                                                       nmax, tmax, r, sb);
+      if (pol_small)
+        vs_polish_kernel<kGrid, VS_MINB_POLISH><<<b_pol, T, sm_pol, st>>>(
+            lib, pk, prm, order, n, counters + c, nmax, tmax, r, sb);
+      else
+        vs_polish_kernel<kGrid, VS_MINB_POLISH_BIG><<<b_pol, T, sm_pol, st>>>(
+            lib, pk, prm, order, n, counters + c, nmax, tmax, r, sb);
       mark(4, true);
       ++c;
       *launches += 1;
