@@ -813,6 +813,9 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t by
 #define VS_MINB_POLISH_BIG 6
 #endif
 constexpr int kPolishSmallAtoms = 48;
+#ifndef VS_MINB_FLEX_BIG
+#define VS_MINB_FLEX_BIG 6  // C4: 117.5 ms vs 119.3 at 8, 118.9 at 5, 125.4 at 4
+#endif
 #ifndef VS_MINB_FLEX
 #define VS_MINB_FLEX 8
 #endif
@@ -908,8 +911,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_SWEEP)
   }
 }
 
-template <int kGrid>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_FLEX)
+template <int kGrid, int kMinB>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinB)
     vs_flex_kernel(const __grid_constant__ LibDev lib, const __grid_constant__ PocketDev pk,
                    const __grid_constant__ DockParams prm,
                    const int* __restrict__ order, int n_order, int* __restrict__ counter,
@@ -1127,12 +1130,16 @@ static cudaError_t staged_impl(int sms, cudaStream_t st, const LibDev& lib, cons
   const size_t sm_fin = kWarpsPerBlock * warp_smem_bytes(nmax, tmax, mvmax, kLayLig | kLayKept);
   const int b_start = stage_blocks(vs_start_kernel<kGrid>, sm_start, sms, n, VS_MINB_START);
   const int b_sweep = stage_blocks(vs_sweep_kernel<kGrid>, sm_sweep, sms, n, VS_MINB_SWEEP);
-  const int b_flex = stage_blocks(vs_flex_kernel<kGrid>, sm_flex, sms, n, VS_MINB_FLEX);
+  const bool small = nmax <= kPolishSmallAtoms;
+  const int b_flex = small ? stage_blocks(vs_flex_kernel<kGrid, VS_MINB_FLEX>, sm_flex, sms, n,
+                                          VS_MINB_FLEX)
+                           : stage_blocks(vs_flex_kernel<kGrid, VS_MINB_FLEX_BIG>, sm_flex, sms,
+                                          n, VS_MINB_FLEX_BIG);
   const int b_fin = stage_blocks(vs_finish_kernel<kGrid>, sm_fin, sms, n, 8);
   const size_t sm_pol = kWarpsPerBlock * warp_smem_bytes(nmax, tmax, 0,
                                                          kLayState | kLayPosed | kLayFlex |
                                                              kLaySweep | kLayPairs);
-  const bool pol_small = nmax <= kPolishSmallAtoms;
+  const bool pol_small = small;
   const int b_pol = pol_small
                         ? stage_blocks(vs_polish_kernel<kGrid, VS_MINB_POLISH>, sm_pol, sms, n,
                                        VS_MINB_POLISH)
@@ -1157,7 +1164,11 @@ static cudaError_t staged_impl(int sms, cudaStream_t st, const LibDev& lib, cons
     mark(1, true);
     ++c;
     mark(2, false);
-    vs_flex_kernel<kGrid><<<b_flex, T, sm_flex, st>>>(lib, pk, prm, order, n, counters + c, nmax,
+    if (small)
+      vs_flex_kernel<kGrid, VS_MINB_FLEX><<<b_flex, T, sm_flex, st>>>(lib, pk, prm, order, n, counters + c, nmax,
+                                                     tmax, mvmax, r, sb);
+    else
+      vs_flex_kernel<kGrid, VS_MINB_FLEX_BIG><<<b_flex, T, sm_flex, st>>>(lib, pk, prm, order, n, counters + c, nmax,
                                                      tmax, mvmax, r, sb);
     mark(2, true);
     ++c;
