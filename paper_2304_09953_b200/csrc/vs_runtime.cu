@@ -2492,41 +2492,12 @@ int vs_rescore_checked(vs_handle* h, const vs_library* L, int64_t n_poses,
     return fail(h, VS_ERR_CAPACITY, "n_poses must be in [0, 2^31)");
   VS_CUDA(h, quiesce(h));
   const int n = L->n_ligands;
-  for (int64_t p = 0; p < n_poses; ++p) {
-    if (p > 0 && pose_lig[p] < pose_lig[p - 1])
-      return fail(h, VS_ERR_INVALID_ARGUMENT, "pose_lig must be non-decreasing");
-    if (pose_lig[p] < 0 || pose_lig[p] >= n)
-      return fail(h, VS_ERR_INVALID_ARGUMENT, "pose ligand index out of range");
-  }
   cudaStream_t st = h->own;
   Packed& P = h->rpack;
   PackPending pp;
   int rc = pack_issue(h, L, nullptr, 0, P, st, pp);  // the device packer runs under the
   if (rc) return rc;                                 // host bookkeeping below
-  const auto r1 = clk::now();
-  // per-ligand pose ranges and torsion bases; the work lists per class
-  std::vector<int> first(std::max(n, 1), 0), count(std::max(n, 1), 0);
-  std::vector<long> tb(std::max(n, 1), 0);
-  long toff = 0;
-  for (int64_t p = 0; p < n_poses; ++p) {
-    const int l = pose_lig[p];
-    if (count[l]++ == 0) {
-      first[l] = static_cast<int>(p);
-      tb[l] = toff;
-    }
-    toff += L->n_tors[l];
-  }
-  if (n_tors_values >= 0 && toff != n_tors_values) {  // check_counts, dock.cpp:219-230
-    cudaStreamSynchronize(st);  // the issued pack drains before its buffers are reused
-    return fail(h, VS_ERR_ATOM_COUNT, "poses need " + std::to_string(toff) +
-                                          " torsion values, got " + std::to_string(n_tors_values));
-  }
-  rc = pack_finish(h, P, st, pp);
-  if (rc) return rc;
-  std::vector<int> ligs;
-  std::vector<std::pair<int, int>> segs;
-  class_lists(P, [&](int l) { return count[l] > 0; }, ligs, segs);
-  const auto r2 = clk::now();
+  // the pose arrays queue right behind the library (DMA under the host work)
   DBuf* rb = h->rbuf;
   auto up = [&](DBuf& dst, const void* src, size_t bytes) -> cudaError_t {
     cudaError_t err = dst.ensure(std::max<size_t>(bytes, 16));
@@ -2536,10 +2507,48 @@ int vs_rescore_checked(vs_handle* h, const vs_library* L, int64_t n_poses,
   const size_t np = static_cast<size_t>(n_poses);
   VS_CUDA(h, up(rb[0], t, np * 12));
   VS_CUDA(h, up(rb[1], q, np * 16));
+  const auto r1 = clk::now();
+  // checks, per-ligand pose ranges and torsion bases in one pass over the
+  // poses while the library and poses are in flight; the work lists per class
+  std::vector<int> first(std::max(n, 1), 0), count(std::max(n, 1), 0);
+  std::vector<long> tb(std::max(n, 1), 0);
+  long toff = 0;
+  const char* bad = nullptr;
+  for (int64_t p = 0; p < n_poses; ++p) {
+    const int l = pose_lig[p];
+    if (p > 0 && l < pose_lig[p - 1]) {
+      bad = "pose_lig must be non-decreasing";
+      break;
+    }
+    if (l < 0 || l >= n) {
+      bad = "pose ligand index out of range";
+      break;
+    }
+    if (count[l]++ == 0) {
+      first[l] = static_cast<int>(p);
+      tb[l] = toff;
+    }
+    toff += L->n_tors[l];
+  }
+  if (bad) {
+    cudaStreamSynchronize(st);  // the issued pack drains before its buffers are reused
+    return fail(h, VS_ERR_INVALID_ARGUMENT, bad);
+  }
+  if (n_tors_values >= 0 && toff != n_tors_values) {  // check_counts, dock.cpp:219-230
+    cudaStreamSynchronize(st);  // the issued pack drains before its buffers are reused
+    return fail(h, VS_ERR_ATOM_COUNT, "poses need " + std::to_string(toff) +
+                                          " torsion values, got " + std::to_string(n_tors_values));
+  }
   VS_CUDA(h, up(rb[2], tors, static_cast<size_t>(toff) * 4));
   VS_CUDA(h, up(rb[3], first.data(), n * 4ul));
   VS_CUDA(h, up(rb[4], count.data(), n * 4ul));
   VS_CUDA(h, up(rb[5], tb.data(), n * 8ul));
+  rc = pack_finish(h, P, st, pp);
+  if (rc) return rc;
+  std::vector<int> ligs;
+  std::vector<std::pair<int, int>> segs;
+  class_lists(P, [&](int l) { return count[l] > 0; }, ligs, segs);
+  const auto r2 = clk::now();
   VS_CUDA(h, up(rb[6], ligs.data(), ligs.size() * 4));
   VS_CUDA(h, rb[7].ensure(std::max<size_t>(np, 1) * 4));
   VS_CUDA(h, rb[8].ensure(std::max<size_t>(np, 1) * 4));

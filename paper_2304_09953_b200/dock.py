@@ -624,8 +624,10 @@ class Engine:
         check(_lib.vs_rescore_survivors(self._h, C.c_void_p(geo_ptr), C.c_void_p(resc_ptr),
                                         C.c_void_p(stream or 0)), self._h, "rescore_survivors")
 
-    def rescore(self, lib: Library, pose_lig, t, q, tors):
-        """K3a: canonical geometric score and rescore of given poses."""
+    def rescore(self, lib: Library, pose_lig, t, q, tors, out=None):
+        """K3a: canonical geometric score and rescore of given poses; out:
+        (geo, resc) float32 arrays of >= n poses to write into (e.g.
+        pinned_empty buffers, which the scores are DMA'd straight into)."""
         pose_lig = np.ascontiguousarray(pose_lig, np.int32)
         t = np.ascontiguousarray(t, np.float32).reshape(-1)
         q = np.ascontiguousarray(q, np.float32).reshape(-1)
@@ -637,8 +639,15 @@ class Engine:
         n_tors_values = tors.size  # checked against the poses' ligands in C
         if tors.size == 0:
             tors = np.zeros(1, np.float32)
-        geo = np.zeros(max(n, 1), np.float32)
-        resc = np.zeros(max(n, 1), np.float32)
+        if out is not None:
+            geo, resc = out
+            if (geo.dtype != np.float32 or resc.dtype != np.float32 or len(geo) < max(n, 1)
+                    or len(resc) < max(n, 1) or not geo.flags.c_contiguous
+                    or not resc.flags.c_contiguous):
+                raise ValueError("out= needs two contiguous float32 arrays of >= n poses")
+        else:
+            geo = np.zeros(max(n, 1), np.float32)
+            resc = np.zeros(max(n, 1), np.float32)
         lc = lib.as_c()
         check(_lib.vs_rescore_checked(self._h, C.byref(lc), n, ptr(pose_lig, C.c_int32),
                                       ptr(t, C.c_float), ptr(q, C.c_float), ptr(tors, C.c_float),

@@ -284,6 +284,20 @@ def test_pinned_result_buffers(V, engine, lib200, pocket_json):
             np.testing.assert_array_equal(getattr(got, f), getattr(ref, f), err_msg=f)
         np.testing.assert_array_equal(_bits(got.surv), _bits(ref.surv))
         np.testing.assert_array_equal(got.surv_tors.view(np.uint32), ref.surv_tors.view(np.uint32))
+    # rescoring into pinned score buffers
+    n = int(np.sum(ref.n_surv))
+    pl = np.repeat(np.arange(len(lib), dtype=np.int32), ref.n_surv.astype(np.int64))
+    sv = np.concatenate([ref.surv[i][:ref.n_surv[i]] for i in range(len(lib))])
+    to = ref.tors_off
+    th = np.concatenate([ref.surv_tors[to[i] * prm.keep_top + k * lib.n_tors[i]:
+                                       to[i] * prm.keep_top + (k + 1) * lib.n_tors[i]]
+                         for i in range(len(lib)) for k in range(ref.n_surv[i])] or
+                        [np.zeros(0, np.float32)])
+    g0, r0 = engine.rescore(lib, pl, sv["t"], sv["q"], th)
+    outs = (pinned_empty(n, np.float32), pinned_empty(n, np.float32))
+    g1, r1 = engine.rescore(lib, pl, sv["t"], sv["q"], th, out=outs)
+    np.testing.assert_array_equal(g0.view(np.uint32), g1.view(np.uint32))
+    np.testing.assert_array_equal(r0.view(np.uint32), r1.view(np.uint32))
     a = pinned_empty((3, 5), np.float64)
     a[...] = 1.5
     assert a.sum() == 22.5 and a.flags.c_contiguous
