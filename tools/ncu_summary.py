@@ -128,7 +128,12 @@ def main(tag):
                                  capture_output=True, text=True).stdout
             csvp = os.path.join(td, f"{kname}.csv")
             open(csvp, "w").write(src)
-            kp = f"_ZN2vs{len(kname)}{kname}ILi1EE"
+            # the profiled instantiation (e.g. vs_flex_kernel<(int)1, (int)8>) as its
+            # mangled prefix
+            import re
+            m = re.search(kname + r"<([^>]*)>", src.splitlines()[0] if src else "")
+            targs = re.findall(r"\(int\)(\d+)", m.group(1)) if m else ["1"]
+            kp = f"_ZN2vs{len(kname)}{kname}I" + "".join(f"Li{a}E" for a in targs) + "EE"
             for part, fn in (("functions", lambda: ncu_funcs.main(csvp, sass, kp)),
                              ("lines", lambda: sass_lines.main(csvp, sass, kp, 40))):
                 buf = io.StringIO()
