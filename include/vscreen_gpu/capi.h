@@ -391,6 +391,9 @@ const char* vs_codec_last_error(void);
 /* codec::load_dictionary (codec.cpp:188-215): validate an SMZ1 dictionary;
  * *n_entries = its entry count.  VS_ERR_FORMAT with the reference's message. */
 int vs_smz1_check(const uint8_t* dict, int64_t dict_len, int32_t* n_entries);
+/* SHA-256 (FIPS 180-4) of len bytes: codec::dictionary_sha256 over the SMZ1
+ * bytes of a dictionary (codec.cpp:222-229) */
+int vs_sha256(const uint8_t* data, int64_t len, uint8_t* out32);
 
 /* JSON number text (dock.cpp:460-489, pipeline.cpp:269-301): x[i] as the
  * reference's nlohmann::json dump prints it, NUL-terminated at out + i*stride.

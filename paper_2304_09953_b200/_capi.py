@@ -173,6 +173,7 @@ _SIGS = {
     "vs_host_alloc": (C.c_int, [C.c_int64, P(C.c_void_p)]),
     "vs_host_free": (C.c_int, [C.c_void_p]),
     "vs_smz1_check": (C.c_int, [C.c_char_p, C.c_int64, C.POINTER(C.c_int32)]),
+    "vs_sha256": (C.c_int, [C.c_char_p, C.c_int64, C.c_char_p]),
     "vs_json_format_doubles": (C.c_int, [P(C.c_double), C.c_int64, C.c_char_p, C.c_int32]),
     "vs_default_classes": (C.c_int, [P(vs_size_class), C.c_int32]),
     "vs_size_class_of": (C.c_int, [C.c_int32, C.c_int32, P(vs_size_class), C.c_int32]),

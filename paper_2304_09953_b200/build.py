@@ -19,7 +19,7 @@ LIB = os.path.join(HERE, "libvscreen_gpu.so")
 # library reference callers link instead of the CPU vscreen_core
 CORE = os.path.join(HERE, "libvscreen_core.so")
 DROPIN = ["vs_dropin_chem.cpp", "vs_dropin_dock.cpp", "vs_dropin_batcher.cpp",
-          "vs_dropin_report.cpp"]
+          "vs_dropin_report.cpp", "vs_dropin_codec.cpp"]
 SOURCES = ["vs_kernels.cu", "vs_dock.cu", "vs_grad.cu", "vs_embed.cu", "vs_pack.cu", "vs_runtime.cu",
            "vs_host.cpp", "vs_ingest.cpp", "vs_codec.cpp", "vs_json.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

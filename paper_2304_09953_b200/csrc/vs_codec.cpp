@@ -125,6 +125,14 @@ extern "C" {
 
 const char* vs_codec_last_error(void) { return g_codec_err.c_str(); }
 
+int vs_sha256(const uint8_t* data, int64_t len, uint8_t* out32) {
+  if (len < 0 || !out32 || (len > 0 && !data)) return VS_ERR_INVALID_ARGUMENT;
+  Sha256 sha;
+  const auto d = sha.digest(data, static_cast<size_t>(len));
+  std::memcpy(out32, d.data(), 32);
+  return VS_OK;
+}
+
 int vs_smz1_check(const uint8_t* dict, int64_t dict_len, int32_t* n_entries) {
   Dict d;
   std::string msg;

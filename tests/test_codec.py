@@ -157,3 +157,18 @@ def test_campaign_reads_a_compressed_library(tmp_path):
     with pytest.raises(BadFormat, match="bad dictionary magic"):
         Cm.prepare(Cm.parse_config_json(json.dumps(dict(jz, dictionary="bad.dict")),
                                         str(tmp_path)))
+
+
+def test_cpp_dropin_codec_read_side(tmp_path):
+    """include/vscreen/codec.hpp + libvscreen_core.so as a reference C++
+    caller reads an SMZC library (pipeline.cpp:390-396): tests/cpp/codec_read.cpp."""
+    import subprocess
+    from conftest import ROOT
+    exe = tmp_path / "codec_read"
+    libdir = os.path.join(ROOT, "paper_2304_09953_b200")
+    subprocess.run(["/usr/bin/g++", "-std=c++20", "-O1", f"-I{ROOT}/include",
+                    os.path.join(ROOT, "tests", "cpp", "codec_read.cpp"), f"-L{libdir}",
+                    "-lvscreen_core", "-lvscreen_gpu", f"-Wl,-rpath,{libdir}", "-o", str(exe)],
+                   check=True)
+    out = subprocess.run([str(exe), CODEC, CAMP], capture_output=True, text=True)
+    assert out.returncode == 0 and "codec ok" in out.stdout, out.stdout + out.stderr
