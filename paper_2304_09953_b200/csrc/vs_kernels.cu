@@ -31,6 +31,9 @@
 namespace vs {
 
 // ========================================================= rescore kernel
+// the parts the rescore kernel touches: the ligand (conformer, axes, moving
+// lists, axis lengths) and the pose columns
+constexpr int kLayRescore = kLayLig | kLayCols;
 __device__ __forceinline__ double& cold(double* col, int i, int c, int a) {
   return col[(i * 3 + c) * kCand + a];
 }
@@ -84,8 +87,11 @@ __device__ __forceinline__ float column_sum(float v) {
 // Canonical score of a given pose, lanes 8a + h: slice h sums atoms
 // i = h (mod 8) and pairs p = h (mod 8) (row-major), then the column's
 // butterfly.  A ligand with up to 4 poses (keep_top 4) uses every lane.
+#ifndef VS_MINB_RESCORE
+#define VS_MINB_RESCORE 8  // C5: 0.531 ms vs 0.600 (no bound), 0.551 (6), 0.567 (10)
+#endif
 template <int kGrid>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_RESCORE)
     vs_rescore_kernel(const __grid_constant__ LibDev lib, const __grid_constant__ PocketDev pk,
                       const int* __restrict__ ligs, int n_ligs, int* __restrict__ work_counter,
                       const __grid_constant__ PoseSrc src, int nmax, int tmax, int mvmax) {
@@ -93,8 +99,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const WarpSmem s =
-      carve(smem_raw + wib * warp_smem_bytes(nmax, tmax, mvmax, kLayAll | kLayCols), nmax, tmax, mvmax,
-            kLayAll | kLayCols);
+      carve(smem_raw + wib * warp_smem_bytes(nmax, tmax, mvmax, kLayRescore), nmax, tmax, mvmax,
+            kLayRescore);
   if (lane == 0) mbar_init(s.bar);
   __syncwarp();
   uint32_t phase = 0;
@@ -371,7 +377,7 @@ __global__ void vs_peak_gather32(const float4* __restrict__ cells, unsigned mask
 namespace vs {
 
 size_t rescore_smem_per_block(int nmax, int tmax, int mvmax) {
-  return kWarpsPerBlock * warp_smem_bytes(nmax, tmax, mvmax, kLayAll | kLayCols);
+  return kWarpsPerBlock * warp_smem_bytes(nmax, tmax, mvmax, kLayRescore);
 }
 
 template <class K>
