@@ -168,6 +168,15 @@ int vs_fetch_results(vs_handle* h, vs_results* out);
 /* Upload + dock + fetch in one call (host buffers in and out). */
 int vs_dock_host(vs_handle* h, const vs_library* lib, const vs_size_class* classes,
                  int32_t n_classes, const vs_dock_params* params, vs_results* out);
+/* vs_dock_host for L, and the device pack of `next` (may be NULL) started on
+ * the handle's copy stream so that its transfer and packer kernels run under
+ * this dock: the next call with next's library (same arrays, same classes)
+ * adopts it without a transfer.  A stream of libraries then moves each one to
+ * the device while the previous one docks.  The caller keeps next's arrays
+ * alive and unchanged until that call. */
+int vs_dock_host_prefetch(vs_handle* h, const vs_library* L, const vs_library* next,
+                          const vs_size_class* classes, int32_t nc, const vs_dock_params* prm,
+                          vs_results* out);
 /* Device time (ms, CUDA events on the launch stream) of the dock kernels of
  * the last vs_dock call, and the number of kernels this handle launched. */
 double vs_last_dock_ms(const vs_handle* h);

@@ -107,6 +107,9 @@ _SIGS = {
     "vs_fetch_results": (C.c_int, [C.c_void_p, P(vs_results)]),
     "vs_dock_host": (C.c_int, [C.c_void_p, P(vs_library), P(vs_size_class), C.c_int32,
                                P(vs_dock_params), P(vs_results)]),
+    "vs_dock_host_prefetch": (C.c_int, [C.c_void_p, P(vs_library), P(vs_library),
+                                        P(vs_size_class), C.c_int32, P(vs_dock_params),
+                                        P(vs_results)]),
     "vs_last_dock_ms": (C.c_double, [C.c_void_p]),
     "vs_launch_count": (C.c_uint64, [C.c_void_p]),
     "vs_last_phase_ms": (C.c_int, [C.c_void_p, P(C.c_double)]),

@@ -150,6 +150,27 @@ struct PinnedVec {
   const T& operator[](size_t i) const { return p[i]; }
 };
 
+// the device packer's scratch (raw arrays as given, work arrays, CUB temp,
+// pinned readback)
+struct PackScratch {
+  DBuf raw[9], pwork[13], ptemp;
+  PinnedVec<int> pk_host;  // stats + error key + classes read back
+  void release() {
+    for (DBuf& b : raw) b.release();
+    for (DBuf& b : pwork) b.release();
+    ptemp.release();
+  }
+};
+
+// a pack issued (pack_issue) and not yet read back (pack_finish)
+struct PackPending {
+  int n = 0, nc = 0;
+  long A = 0, T = 0;
+  size_t cls_at = 0;
+  bool classes = false;
+  int slot = 0;  // the PackScratch it uses
+};
+
 struct Packed {
   int n = 0;
   PinnedVec<int4> meta;
@@ -249,7 +270,8 @@ struct vs_handle {
   int gdims[3] = {0, 0, 0};
   // library + results
   bool has_lib = false;
-  Packed lib;
+  Packed libs[2];            // the resident library and the spare (prefetch) slot
+  int cur = 0;               // libs[cur] is the resident one
   vs_dock_params last_prm{};
   bool has_results = false;
   DBuf d_surv, d_surv_tors, d_all, d_all_tors, d_best, d_nkept, d_nsurv, d_keys;
@@ -293,8 +315,15 @@ struct vs_handle {
   Packed xpack;
   DBuf xbuf[10];
   // the device packer (vs_pack.cu): the caller's raw arrays, scratch, CUB temp
-  DBuf raw[9], pwork[13], ptemp;
-  PinnedVec<int> pk_host;  // stats + error key + classes read back
+  PackScratch ps[2];       // the device packer's scratch, one per library slot
+  // vs_dock_host_prefetch: the next library packing into libs[1 - cur] on
+  // the copy stream while the current one docks
+  cudaStream_t copy = nullptr;
+  bool spare_pending = false;
+  PackPending spare_pp;
+  vs_library spare_L{};
+  std::vector<vs_size_class> spare_cls;
+  bool spare_has_cls = false;
   // per-class ligand lists of the resident library (the device rescoring
   // entries), rebuilt after each upload
   DBuf d_lib_lists;
@@ -803,13 +832,15 @@ void vs_destroy(vs_handle* h) {
   if (!h) return;
   cudaSetDevice(h->device);
   cudaStreamSynchronize(h->own);
-  h->lib.release();
+  if (h->copy) {
+    cudaStreamSynchronize(h->copy);
+    cudaStreamDestroy(h->copy);
+  }
+  for (Packed& P : h->libs) P.release();
   h->rpack.release();
   h->xpack.release();
   for (DBuf& b : h->xbuf) b.release();
-  for (DBuf& b : h->raw) b.release();
-  for (DBuf& b : h->pwork) b.release();
-  h->ptemp.release();
+  for (PackScratch& x : h->ps) x.release();
   if (h->key_tex) cudaDestroyTextureObject(h->key_tex);
   for (DBuf& b : h->rbuf) b.release();
   for (DBuf& b : h->ebuf) b.release();
@@ -1007,26 +1038,21 @@ namespace {
 // gpu_pack in two halves: pack_issue enqueues the transfers and kernels
 // (async), pack_finish synchronizes `st` and reads back the outcome; a
 // caller can do host work in between
-struct PackPending {
-  int n = 0, nc = 0;
-  long A = 0, T = 0;
-  size_t cls_at = 0;
-  bool classes = false;
-};
 int pack_issue(vs_handle* h, const vs_library* L, const vs_size_class* classes, int nc, Packed& P,
-               cudaStream_t st, PackPending& pp);
+               cudaStream_t st, PackPending& pp, int slot = 0);
 int pack_finish(vs_handle* h, Packed& P, cudaStream_t st, const PackPending& pp);
 
 int gpu_pack(vs_handle* h, const vs_library* L, const vs_size_class* classes, int nc, Packed& P,
-             cudaStream_t st) {
+             cudaStream_t st, int slot = 0) {
   PackPending pp;
-  const int rc = pack_issue(h, L, classes, nc, P, st, pp);
+  const int rc = pack_issue(h, L, classes, nc, P, st, pp, slot);
   if (rc) return rc;
   return pack_finish(h, P, st, pp);
 }
 
 int pack_issue(vs_handle* h, const vs_library* L, const vs_size_class* classes, int nc, Packed& P,
-               cudaStream_t st, PackPending& pp) {
+               cudaStream_t st, PackPending& pp, int slot) {
+  PackScratch& X = h->ps[slot];
   const int n = L->n_ligands;
   if (n < 0) return fail(h, VS_ERR_INVALID_ARGUMENT, "negative ligand count");
   long A = 0, T = 0, M = 0;
@@ -1042,7 +1068,7 @@ int pack_issue(vs_handle* h, const vs_library* L, const vs_size_class* classes, 
   for (long j = 0; j < T; ++j) M += std::max(0, L->moving_count[j]);
   const size_t n1 = static_cast<size_t>(n) + 1, t1 = static_cast<size_t>(T) + 1;
   // raw arrays (as given) -> device
-  DBuf* r = h->raw;
+  DBuf* r = X.raw;
   auto up = [&](DBuf& d, const void* src, size_t bytes) -> cudaError_t {
     cudaError_t e = d.ensure(std::max<size_t>(bytes, 16));
     if (e == cudaSuccess && bytes > 0 && src)
@@ -1061,7 +1087,7 @@ int pack_issue(vs_handle* h, const vs_library* L, const vs_size_class* classes, 
   VS_CUDA(h, up(P.d_seeds, L->seeds, L->seeds ? n * 8ul : 0));
   VS_CUDA(h, up(P.d_idr, L->id_rank, L->id_rank ? n * 4ul : 0));
   // classes (int4 each) ride in the stats buffer's tail
-  DBuf* w = h->pwork;
+  DBuf* w = X.pwork;
   VS_CUDA(h, w[0].ensure(n1 * 8));   // cnt_a
   VS_CUDA(h, w[1].ensure(n1 * 8));   // cnt_t
   VS_CUDA(h, w[2].ensure(t1 * 8));   // cnt_m
@@ -1077,7 +1103,7 @@ int pack_issue(vs_handle* h, const vs_library* L, const vs_size_class* classes, 
   if (nc > kPkMaxClasses) return fail(h, VS_ERR_CAPACITY, "more than 64 size classes");
   VS_CUDA(h, w[12].ensure(4 * kPkClasses + 16 * static_cast<size_t>(std::max(nc, 1))));
   const size_t tmp = pack_temp_bytes(n, T);
-  VS_CUDA(h, h->ptemp.ensure(tmp));
+  VS_CUDA(h, X.ptemp.ensure(tmp));
   // packed outputs: M raw entries -> at most M + 15 n padded bytes
   VS_CUDA(h, P.d_meta.ensure(std::max<size_t>(16, n * 16ul)));
   VS_CUDA(h, P.d_mov.ensure(std::max<size_t>(8, n * 8ul)));
@@ -1091,8 +1117,8 @@ int pack_issue(vs_handle* h, const vs_library* L, const vs_size_class* classes, 
   unsigned long long* err = reinterpret_cast<unsigned long long*>(stats + kPkErr);
   int4* dcls = reinterpret_cast<int4*>(stats + kPkClasses);
   const size_t cls_at = kPkClasses + 4 * static_cast<size_t>(std::max(nc, 1));  // host: cls after
-  if (!h->pk_host.resize(cls_at + n1)) return fail(h, VS_ERR_CUDA, "pinned host allocation failed");
-  int* hs = h->pk_host.data();
+  if (!X.pk_host.resize(cls_at + n1)) return fail(h, VS_ERR_CUDA, "pinned host allocation failed");
+  int* hs = X.pk_host.data();
   std::memset(hs, 0, kPkClasses * sizeof(int));
   *reinterpret_cast<unsigned long long*>(hs + kPkErr) = ~0ull;
   for (int k = 0; k < nc; ++k)
@@ -1125,7 +1151,7 @@ int pack_issue(vs_handle* h, const vs_library* L, const vs_size_class* classes, 
               P.d_axes.as<int4>(), P.d_moving.as<uint8_t>(), P.d_seeds.as<unsigned long long>(),
               P.d_idr.as<unsigned>(), P.d_order.as<int>()};
   VS_CUDA(h, pack_stage1(st, in, pw, classes ? nc : 0));
-  VS_CUDA(h, pack_stage2(st, in, pw, out, h->ptemp.p, tmp));
+  VS_CUDA(h, pack_stage2(st, in, pw, out, X.ptemp.p, tmp));
   h->launches += 9;
   VS_CUDA(h, cudaMemcpyAsync(hs, stats, kPkClasses * sizeof(int), cudaMemcpyDeviceToHost, st));
   VS_CUDA(h, cudaMemcpyAsync(hs + cls_at, pw.cls, n * 4ul, cudaMemcpyDeviceToHost, st));
@@ -1135,6 +1161,7 @@ int pack_issue(vs_handle* h, const vs_library* L, const vs_size_class* classes, 
   pp.T = T;
   pp.cls_at = cls_at;
   pp.classes = classes != nullptr;
+  pp.slot = slot;
   return VS_OK;
 }
 
@@ -1143,7 +1170,7 @@ int pack_finish(vs_handle* h, Packed& P, cudaStream_t st, const PackPending& pp)
   const int n = pp.n, nc = pp.nc;
   const long A = pp.A, T = pp.T;
   const size_t cls_at = pp.cls_at;
-  const int* hs = h->pk_host.data();
+  const int* hs = h->ps[pp.slot].pk_host.data();
   const unsigned long long ek = *reinterpret_cast<const unsigned long long*>(hs + kPkErr);
   if (ek != ~0ull) {
     const int code = static_cast<int>(ek & 0xff);
@@ -1192,13 +1219,17 @@ int vs_upload_library(vs_handle* h, const vs_library* L, const vs_size_class* cl
                       int32_t nc) {
   cudaSetDevice(h->device);
   VS_CUDA(h, quiesce(h));  // a dock on a caller stream may still read the library
+  if (h->spare_pending) {  // a prefetch not taken: drain and drop it
+    VS_CUDA(h, cudaStreamSynchronize(h->copy));
+    h->spare_pending = false;
+  }
   h->has_lib = false;
   h->lib_lists_n = -1;
   h->has_results = false;
   using clk = std::chrono::steady_clock;
   const auto t0 = clk::now();
   if (device_pack_enabled()) {  // the device packer (VSCREEN_HOST_PACK=1: the host one)
-    const int rc = gpu_pack(h, L, classes, nc, h->lib, h->own);
+    const int rc = gpu_pack(h, L, classes, nc, h->libs[h->cur], h->own, h->cur);
     if (rc) return rc;
     if (const char* e = std::getenv("VSCREEN_UPLOAD_TIMING"); e && e[0] == '1')
       std::fprintf(stderr, "vs_upload_library: device pack (raw H2D + kernels) %.2f ms\n",
@@ -1208,19 +1239,19 @@ int vs_upload_library(vs_handle* h, const vs_library* L, const vs_size_class* cl
   }
   // the pinned arrays' DMA runs under the bucketing and the torsion-tree
   // check; a failure drains it before returning (the next pack rewrites them)
-  int rc = pack_library(h, L, classes, nc, h->lib, h->own);
+  int rc = pack_library(h, L, classes, nc, h->libs[h->cur], h->own);
   if (rc) {
     cudaStreamSynchronize(h->own);
     return rc;
   }
   const auto t1 = clk::now();
-  rc = check_nested(h, h->lib);
+  rc = check_nested(h, h->libs[h->cur]);
   if (rc) {
     cudaStreamSynchronize(h->own);
     return rc;
   }
   const auto t2 = clk::now();
-  rc = upload_packed(h, h->lib, h->own, 2);
+  rc = upload_packed(h, h->libs[h->cur], h->own, 2);
   if (rc) return rc;
   VS_CUDA(h, cudaStreamSynchronize(h->own));
   const auto t3 = clk::now();
@@ -1367,7 +1398,7 @@ int vs_dock(vs_handle* h, const vs_dock_params* prm, void* stream) {
   if (rc) return rc;
   cudaStream_t st = pick(h, stream);
   VS_CUDA(h, after_prev(h, st));
-  const Packed& P = h->lib;
+  const Packed& P = h->libs[h->cur];
   rc = ensure_rots(h, prm, st);
   if (rc) return rc;
   rc = prepare_results(h, P.n, P.total_tors, prm, st);
@@ -1799,6 +1830,65 @@ int vs_dock_host(vs_handle* h, const vs_library* L, const vs_size_class* classes
   }
   int rc = vs_upload_library(h, L, classes, nc);
   if (rc) return rc;
+  rc = vs_dock(h, prm, nullptr);
+  if (rc) return rc;
+  return vs_fetch_results(h, out);
+}
+
+namespace {
+bool same_library(const vs_library& a, const vs_library* b) {
+  return a.n_ligands == b->n_ligands && a.n_atoms == b->n_atoms && a.n_tors == b->n_tors &&
+         a.rot_bonds == b->rot_bonds && a.coords == b->coords && a.atom_class == b->atom_class &&
+         a.axis_a == b->axis_a && a.axis_b == b->axis_b && a.moving_count == b->moving_count &&
+         a.moving == b->moving && a.seeds == b->seeds && a.id_rank == b->id_rank;
+}
+}  // namespace
+
+int vs_dock_host_prefetch(vs_handle* h, const vs_library* L, const vs_library* next,
+                          const vs_size_class* classes, int32_t nc, const vs_dock_params* prm,
+                          vs_results* out) {
+  cudaSetDevice(h->device);
+  const bool cls_match =
+      h->spare_has_cls == (classes != nullptr) &&
+      (!classes || (static_cast<size_t>(std::max(nc, 0)) == h->spare_cls.size() &&
+                    std::equal(h->spare_cls.begin(), h->spare_cls.end(), classes,
+                               [](const vs_size_class& x, const vs_size_class& y) {
+                                 return x.atom_lo == y.atom_lo && x.atom_hi == y.atom_hi &&
+                                        x.rot_lo == y.rot_lo && x.rot_hi == y.rot_hi;
+                               })));
+  int rc;
+  if (h->spare_pending && cls_match && same_library(h->spare_L, L)) {
+    // adopt the prefetched pack: its outcome is read back (the same checks
+    // and errors as a synchronous upload), then the slots swap
+    VS_CUDA(h, quiesce(h));
+    h->spare_pending = false;
+    const int spare = 1 - h->cur;
+    h->has_lib = false;
+    h->lib_lists_n = -1;
+    h->has_results = false;
+    rc = pack_finish(h, h->libs[spare], h->copy, h->spare_pp);
+    if (rc) return rc;
+    h->cur = spare;
+    h->has_lib = true;
+  } else {
+    rc = vs_upload_library(h, L, classes, nc);
+    if (rc) return rc;
+  }
+  if (next) {
+    // the spare slot is free (no dock reads it); the next library's DMA and
+    // packer kernels run on the copy stream under this dock
+    if (!h->copy) VS_CUDA(h, cudaStreamCreateWithFlags(&h->copy, cudaStreamNonBlocking));
+    const int spare = 1 - h->cur;
+    rc = pack_issue(h, next, classes, nc, h->libs[spare], h->copy, h->spare_pp, spare);
+    if (rc) {
+      cudaStreamSynchronize(h->copy);
+      return rc;
+    }
+    h->spare_pending = true;
+    h->spare_L = *next;
+    h->spare_has_cls = classes != nullptr;
+    h->spare_cls.assign(classes ? classes : nullptr, classes ? classes + std::max(nc, 0) : nullptr);
+  }
   rc = vs_dock(h, prm, nullptr);
   if (rc) return rc;
   return vs_fetch_results(h, out);
@@ -2495,7 +2585,7 @@ int vs_rescore_checked(vs_handle* h, const vs_library* L, int64_t n_poses,
   cudaStream_t st = h->own;
   Packed& P = h->rpack;
   PackPending pp;
-  int rc = pack_issue(h, L, nullptr, 0, P, st, pp);  // the device packer runs under the
+  int rc = pack_issue(h, L, nullptr, 0, P, st, pp, h->cur);  // the device packer runs under the
   if (rc) return rc;                                 // host bookkeeping below
   // the pose arrays queue right behind the library (DMA under the host work)
   DBuf* rb = h->rbuf;
@@ -2591,7 +2681,7 @@ int vs_rescore_device(vs_handle* h, int64_t n_poses, const int32_t* pose_lig, co
   if (!h->has_lib) return fail(h, VS_ERR_STATE, "no resident library");
   if (n_poses < 0 || n_poses > INT32_MAX)
     return fail(h, VS_ERR_CAPACITY, "n_poses must be in [0, 2^31)");
-  const Packed& P = h->lib;
+  const Packed& P = h->libs[h->cur];
   if (!P.on_device) return fail(h, VS_ERR_STATE, "library not packed on the device");
   cudaStream_t st = pick(h, stream);
   VS_CUDA(h, after_prev(h, st));
@@ -2638,9 +2728,9 @@ int vs_rescore_device(vs_handle* h, int64_t n_poses, const int32_t* pose_lig, co
 int vs_rescore_survivors(vs_handle* h, float* geo, float* resc, void* stream) {
   cudaSetDevice(h->device);
   if (!h->has_pocket) return fail(h, VS_ERR_STATE, "no pocket");
-  if (!h->has_results || !h->has_lib || h->res_n != h->lib.n)
+  if (!h->has_results || !h->has_lib || h->res_n != h->libs[h->cur].n)
     return fail(h, VS_ERR_STATE, "no dock results on the resident library");
-  const Packed& P = h->lib;
+  const Packed& P = h->libs[h->cur];
   if (!P.on_device) return fail(h, VS_ERR_STATE, "library not packed on the device");
   cudaStream_t st = pick(h, stream);
   VS_CUDA(h, after_prev(h, st));

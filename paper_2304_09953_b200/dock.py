@@ -405,15 +405,24 @@ class Engine:
         return _trim(res, len(lib))
 
     def dock_host(self, lib: Library, params: DockParams, classes=None,
-                  out: DockResults | None = None) -> DockResults:
+                  out: DockResults | None = None, prefetch: Library | None = None) -> DockResults:
         """Upload + dock + fetch in one C-ABI call (host buffers in and out);
-        out: result buffers from alloc_results to write into (reused)."""
+        out: result buffers from alloc_results to write into (reused);
+        prefetch: the library of the next call, moved to the device under
+        this dock (capi.h vs_dock_host_prefetch; keep it unchanged until
+        then)."""
         cl, ncl = _classes_c(classes)
         lc = lib.as_c()
         pc = params.as_c()
         res, r = self._alloc(lib, params, out)
-        check(_lib.vs_dock_host(self._h, C.byref(lc), cl, ncl, C.byref(pc), C.byref(r)),
-              self._h, "dock_host")
+        if prefetch is not None:
+            nc_ = prefetch.as_c()
+            self._prefetch_keep = (prefetch, nc_)  # its arrays stay referenced until used
+            check(_lib.vs_dock_host_prefetch(self._h, C.byref(lc), C.byref(nc_), cl, ncl,
+                                             C.byref(pc), C.byref(r)), self._h, "dock_host")
+        else:
+            check(_lib.vs_dock_host(self._h, C.byref(lc), cl, ncl, C.byref(pc), C.byref(r)),
+                  self._h, "dock_host")
         self._lib, self._prm = lib, params
         return _trim(res, len(lib))
 

@@ -306,6 +306,33 @@ def test_pinned_result_buffers(V, engine, lib200, pocket_json):
         engine.dock_host(lib, prm, out=engine.alloc_results(small, prm))
 
 
+def test_prefetched_library_stream(V, engine, lib200, pocket_json):
+    """vs_dock_host_prefetch: the next library packed on the copy stream under
+    the current dock and adopted by the next call gives the one-shot results;
+    a prefetch that the next call does not use is dropped."""
+    lib, _ = lib200
+    engine.set_pocket(V.parse_pocket_json(pocket_json), grid_spacing=0.4)
+    prm = _params(V)
+    lib2 = lib.subset(list(range(0, len(lib), 2)))
+    ref1 = engine.dock_host(lib, prm)
+    ref2 = engine.dock_host(lib2, prm)
+
+    def same(a, b):
+        for f in ("best", "n_kept", "n_surv", "keys"):
+            np.testing.assert_array_equal(getattr(a, f), getattr(b, f), err_msg=f)
+        np.testing.assert_array_equal(_bits(a.surv), _bits(b.surv))
+
+    same(engine.dock_host(lib, prm, prefetch=lib2), ref1)   # sync upload, prefetch lib2
+    same(engine.dock_host(lib2, prm, prefetch=lib), ref2)   # adopts lib2, prefetch lib
+    same(engine.dock_host(lib, prm, prefetch=lib), ref1)    # adopts lib, prefetch lib
+    same(engine.dock_host(lib2, prm), ref2)                 # prefetch dropped
+    same(engine.dock_host(lib, prm), ref1)
+    classes = [(0, 20, 0, 64)]
+    refc = engine.dock_host(lib, prm, classes)
+    same(engine.dock_host(lib, prm, prefetch=lib), ref1)    # prefetch with default classes
+    same(engine.dock_host(lib, prm, classes), refc)         # classes differ: dropped
+
+
 def test_edge_cases(V, engine, pocket_json):
     pocket = V.parse_pocket_json(pocket_json)
     engine.set_pocket(pocket)
