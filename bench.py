@@ -96,7 +96,7 @@ CONFIG = {"workload": "C2: 100k synthetic drug-like ligands/GPU (10-40 heavy ato
                        "FP32 greedy torsion flex search, post compass, exact FP32/FP64 re-score",
           "quality_vs_reference": "mean best survivor rescore (reference FP64 rescore) on 384 C2 "
                                   "ligands: 44.99 grid / 44.93 analytic vs the reference dock() "
-                                  "ascent 43.75 (profiles/quality_r1r_*.json)"}
+                                  "ascent 43.75 (profiles/quality_r2_*.json; unchanged from round 1)"}
 
 
 CONFIGS = {
