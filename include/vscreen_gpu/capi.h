@@ -173,7 +173,8 @@ int vs_dock_host(vs_handle* h, const vs_library* lib, const vs_size_class* class
  * this dock: the next call with next's library (same arrays, same classes)
  * adopts it without a transfer.  A stream of libraries then moves each one to
  * the device while the previous one docks.  The caller keeps next's arrays
- * alive and unchanged until that call. */
+ * alive and unchanged until that call.  A `next` the packer rejects is not
+ * prefetched; the call that docks it reports the error. */
 int vs_dock_host_prefetch(vs_handle* h, const vs_library* L, const vs_library* next,
                           const vs_size_class* classes, int32_t nc, const vs_dock_params* prm,
                           vs_results* out);

@@ -1879,15 +1879,18 @@ int vs_dock_host_prefetch(vs_handle* h, const vs_library* L, const vs_library* n
     // packer kernels run on the copy stream under this dock
     if (!h->copy) VS_CUDA(h, cudaStreamCreateWithFlags(&h->copy, cudaStreamNonBlocking));
     const int spare = 1 - h->cur;
-    rc = pack_issue(h, next, classes, nc, h->libs[spare], h->copy, h->spare_pp, spare);
-    if (rc) {
+    if (pack_issue(h, next, classes, nc, h->libs[spare], h->copy, h->spare_pp, spare) == VS_OK) {
+      h->spare_pending = true;
+      h->spare_L = *next;
+      h->spare_has_cls = classes != nullptr;
+      h->spare_cls.assign(classes ? classes : nullptr,
+                          classes ? classes + std::max(nc, 0) : nullptr);
+    } else {
+      // a library the packer rejects is not prefetched: the call that docks
+      // it uploads it and reports the error
       cudaStreamSynchronize(h->copy);
-      return rc;
+      h->err.clear();
     }
-    h->spare_pending = true;
-    h->spare_L = *next;
-    h->spare_has_cls = classes != nullptr;
-    h->spare_cls.assign(classes ? classes : nullptr, classes ? classes + std::max(nc, 0) : nullptr);
   }
   rc = vs_dock(h, prm, nullptr);
   if (rc) return rc;

@@ -331,6 +331,15 @@ def test_prefetched_library_stream(V, engine, lib200, pocket_json):
     refc = engine.dock_host(lib, prm, classes)
     same(engine.dock_host(lib, prm, prefetch=lib), ref1)    # prefetch with default classes
     same(engine.dock_host(lib, prm, classes), refc)         # classes differ: dropped
+    # a library the packer rejects is not prefetched: this dock runs, the
+    # call that docks it reports the error
+    bad = lib.subset(list(range(len(lib))))
+    bad.n_atoms = bad.n_atoms.copy()
+    bad.n_atoms[0] = 0
+    same(engine.dock_host(lib, prm, prefetch=bad), ref1)
+    with pytest.raises(V.AtomCountMismatch):
+        engine.dock_host(bad, prm)
+    same(engine.dock_host(lib, prm), ref1)
 
 
 def test_edge_cases(V, engine, pocket_json):
