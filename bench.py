@@ -446,6 +446,29 @@ def roofline(work, phase_ms, dock_ms, peaks, traffic, as_impl=None, gathers=None
     return out
 
 
+def hbm_view(rl, prm):
+    """The dominant kernel against the driver-measured HBM copy bandwidth
+    (MEASURED_PEAKS.json hbm_gbs): its DRAM bytes per launch (ncu,
+    roofline.traffic) over its mean launch time.  Context for why the bound
+    is the L1/L2 gather roof, not HBM."""
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        peak = float(json.load(open(p))["hbm_gbs"])
+        src = "MEASURED_PEAKS.json hbm_gbs"
+    except Exception:
+        peak, src = 7700.0, "B200_PROFILING.md nominal HBM3e (no MEASURED_PEAKS.json)"
+    traffic = rl.get("traffic")
+    k = {"vs_sweep_kernel": "sweep", "vs_flex_kernel": "flex"}.get(rl.get("kernel"))
+    ms = rl.get("per_kernel", {}).get(k, {}).get("ms") if k else None
+    launches = prm.restarts
+    if not traffic or not ms:
+        return {"peak": peak, "source": src, "achieved": None, "frac": None}
+    gbps = traffic / (ms * 1e-3 / launches) / 1e9
+    return {"achieved": round(gbps, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(gbps / peak, 4), "source": src,
+            "what": "ncu DRAM bytes per launch of the dominant kernel / its mean launch time"}
+
+
 def load_traffic():
     """DRAM bytes per launch of each dock kernel from the committed ncu pass
     (profiles/ncu_dock_traffic.json, tools/ncu_summary.py)."""
@@ -878,6 +901,7 @@ def main():
     phase_ms = {k: float(np.mean([p[k] for p in phase])) for k in phase[0]}
     rl = roofline(frozen_work(lib, prm), phase_ms, float(np.mean(dock_ms)), peaks, load_traffic(),
                   work, gathers)
+    rl["hbm_view"] = hbm_view(rl, prm)
     top = out.cpu().numpy().view(np.uint64)
     n_ranked = int(np.sum(top != np.uint64(2**64 - 1)))
     topk_check = None
