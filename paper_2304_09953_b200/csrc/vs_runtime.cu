@@ -2524,15 +2524,30 @@ int rescore_launch(vs_handle* h, const Packed& P, const int* d_ligs,
   VS_CUDA(h, cudaEventRecord(h->rev0, st));
   // the classes' launches run concurrently (a fork of `st` per class, joined
   // back): a class of few large ligands overlaps the bulk of small ones
-  // instead of running after it at low occupancy
-  int k = 0;
-  for (size_t c = 0; c < segs.size(); ++c) {
-    if (segs[c].second == 0) continue;
+  // instead of running after it at low occupancy.  The class with the largest
+  // shared-memory footprint launches first, capped at `big` blocks per SM, so
+  // that the others still find 8 - big block slots on every SM: both run from
+  // the start instead of one after the other
+  std::vector<size_t> ord;
+  for (size_t c = 0; c < segs.size(); ++c)
+    if (segs[c].second > 0) ord.push_back(c);
+  auto smem_of = [&](size_t c) {
     const Bucket& b = P.buckets[c];
-    const size_t smem = rescore_smem_per_block(b.nmax, b.tmax, b.mvmax);
+    return rescore_smem_per_block(b.nmax, b.tmax, b.mvmax);
+  };
+  std::stable_sort(ord.begin(), ord.end(),
+                   [&](size_t a, size_t b) { return smem_of(a) > smem_of(b); });
+  int big = 2;
+  if (const char* e = std::getenv("VSCREEN_RESCORE_BIG"); e && *e) big = std::atoi(e);
+  big = std::min(std::max(big, 1), 7);
+  int k = 0;
+  for (size_t c : ord) {
+    const Bucket& b = P.buckets[c];
+    const size_t smem = smem_of(c);
     if (smem > 227 * 1024) return fail(h, VS_ERR_CAPACITY, "ligands too large for rescoring");
+    const int per_sm = ord.size() < 2 ? 8 : (k == 0 ? big : 8 - big);
     const int blocks = std::max(1, std::min((segs[c].second + kWarpsPerBlock - 1) / kWarpsPerBlock,
-                                            8 * h->sms));
+                                            per_sm * h->sms));
     cudaStream_t cs = st;
     if (k > 0) {
       if (h->fork.size() < static_cast<size_t>(k)) {
