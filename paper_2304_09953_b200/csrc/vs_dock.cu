@@ -861,8 +861,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_START)
         sb.nk[lig] = 0;
         for (int c = 0; c < 8; ++c) sb.st[8 * lig + c] = 0ull;
       }
-      sb.st[8 * lig + 1] += static_cast<unsigned long long>(att) + 1;
-      sb.st[8 * lig + 4] += static_cast<unsigned long long>(clock64() - c0);
+      atomicAdd(sb.st + 8 * lig + 1, static_cast<unsigned long long>(att) + 1);
+      atomicAdd(sb.st + 8 * lig + 4, static_cast<unsigned long long>(clock64() - c0));
     }
     __syncwarp();
   }
@@ -904,8 +904,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_SWEEP)
       sb.pose[2 * lig] = make_float4(P.t[0], P.t[1], P.t[2], pt.w);
       sb.pose[2 * lig + 1] = make_float4(P.q[0], P.q[1], P.q[2], P.q[3]);
       sb.bk[lig] = best_k;
-      sb.st[8 * lig + 0] += static_cast<unsigned long long>(n_trans);
-      sb.st[8 * lig + 5] += static_cast<unsigned long long>(clock64() - c0);
+      atomicAdd(sb.st + 8 * lig + 0, static_cast<unsigned long long>(n_trans));
+      atomicAdd(sb.st + 8 * lig + 5, static_cast<unsigned long long>(clock64() - c0));
     }
     __syncwarp();
   }
@@ -962,8 +962,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinB)
       for (int i = lane; i < N; i += 32) sb.ys[meta.x + i] = s.ys[i];
       for (int j = lane; j < T; j += 32) sb.th[meta.z + j] = s.theta[j];
       if (lane == 0) {
-        sb.st[8 * lig + 2] += nact;
-        sb.st[8 * lig + 6] += static_cast<unsigned long long>(clock64() - c0);
+        atomicAdd(sb.st + 8 * lig + 2, nact);
+        atomicAdd(sb.st + 8 * lig + 6, static_cast<unsigned long long>(clock64() - c0));
       }
       __syncwarp();
       continue;
@@ -977,9 +977,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinB)
                                  8 + T, km, nk, prm.delta, lane);
     if (lane == 0) {
       if (kept) sb.nk[lig] = nk + 1;
-      sb.st[8 * lig + 2] += nact;
-      sb.st[8 * lig + 6] += static_cast<unsigned long long>(c1 - c0);
-      sb.st[8 * lig + 7] += static_cast<unsigned long long>(clock64() - c1);
+      atomicAdd(sb.st + 8 * lig + 2, nact);
+      atomicAdd(sb.st + 8 * lig + 6, static_cast<unsigned long long>(c1 - c0));
+      atomicAdd(sb.st + 8 * lig + 7, static_cast<unsigned long long>(clock64() - c1));
     }
     __syncwarp();
   }
@@ -1029,9 +1029,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinB)
                                  8 + T, km, nk, prm.delta, lane);
     if (lane == 0) {
       if (kept) sb.nk[lig] = nk + 1;
-      sb.st[8 * lig + 3] += static_cast<unsigned long long>(n_post);
-      sb.st[8 * lig + 6] += static_cast<unsigned long long>(c1 - c0);
-      sb.st[8 * lig + 7] += static_cast<unsigned long long>(clock64() - c1);
+      atomicAdd(sb.st + 8 * lig + 3, static_cast<unsigned long long>(n_post));
+      atomicAdd(sb.st + 8 * lig + 6, static_cast<unsigned long long>(c1 - c0));
+      atomicAdd(sb.st + 8 * lig + 7, static_cast<unsigned long long>(clock64() - c1));
     }
     __syncwarp();
   }
