@@ -885,10 +885,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, VS_MINB_SWEEP)
     const int lig = order[w];
     const int4 meta = lib.meta[lig];
     const int N = meta.y;
+    // the pose loads issue before the bulk copy's wait (they do not depend on it)
+    const float4 pt = sb.pose[2 * lig], pq = sb.pose[2 * lig + 1];
     tma_load(s.ysf, sb.ysf + meta.x, 16u * N, s.bar, phase, lane);
     if (kGrid) build_pairs(pairs_of(s.ysf, d.nmax), N, lane);
     const long long c0 = clock64();
-    const float4 pt = sb.pose[2 * lig], pq = sb.pose[2 * lig + 1];
     PoseF P;
     P.t[0] = pt.x;
     P.t[1] = pt.y;
@@ -936,12 +937,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinB)
   for (int w = next_item(counter, lane); w < n_order; w = next_item(counter, lane)) {
     const int lig = order[w];
     int4 meta;
+    const float4 pt = sb.pose[2 * lig], pq = sb.pose[2 * lig + 1];  // before the copies' waits
     stage_ligand(lib, lig, s, lane, phase, meta);
     const int N = meta.y, T = meta.w, R = prm.R;
-    tma_load(s.ys, sb.ys + meta.x, 32u * N, s.bar, phase, lane);
     for (int j = lane; j < T; j += 32) s.theta[j] = sb.th[meta.z + j];
+    tma_load(s.ys, sb.ys + meta.x, 32u * N, s.bar, phase, lane);
     const long long c0 = clock64();
-    const float4 pt = sb.pose[2 * lig], pq = sb.pose[2 * lig + 1];
     PoseF P;
     P.t[0] = pt.x;
     P.t[1] = pt.y;
@@ -1005,10 +1006,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinB)
     const int lig = order[w];
     const int4 meta = lib.meta[lig];
     const int N = meta.y, T = meta.w, R = prm.R;
-    tma_load(s.ys, sb.ys + meta.x, 32u * N, s.bar, phase, lane);
-    for (int j = lane; j < T; j += 32) s.theta[j] = sb.th[meta.z + j];
-    const long long c0 = clock64();
+    // loads that do not depend on the bulk copy issue before its wait
     const float4 pt = sb.pose[2 * lig], pq = sb.pose[2 * lig + 1];
+    const int nk = sb.nk[lig], bk = sb.bk[lig];
+    for (int j = lane; j < T; j += 32) s.theta[j] = sb.th[meta.z + j];
+    tma_load(s.ys, sb.ys + meta.x, 32u * N, s.bar, phase, lane);
+    const long long c0 = clock64();
     PoseF P;
     P.t[0] = pt.x;
     P.t[1] = pt.y;
@@ -1021,11 +1024,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, kMinB)
     int n_post = 0;
     const float S = polish_phase<kGrid>(pk, d, N, lane, &P, &n_post);
     const long long c1 = clock64();
-    const int nk = sb.nk[lig];
     float4* kx = sb.kx + static_cast<size_t>(meta.x) * R;
     float* kp = sb.kp + (static_cast<size_t>(lig) * 8 + meta.z) * R;
     int* km = sb.km + static_cast<size_t>(lig) * R * 4;
-    const bool kept = keep_phase(d, N, T, &P, S, r, __float_as_int(pt.w), sb.bk[lig], kx, N, kp,
+    const bool kept = keep_phase(d, N, T, &P, S, r, __float_as_int(pt.w), bk, kx, N, kp,
                                  8 + T, km, nk, prm.delta, lane);
     if (lane == 0) {
       if (kept) sb.nk[lig] = nk + 1;
