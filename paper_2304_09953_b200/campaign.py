@@ -249,10 +249,10 @@ class _TraceWriter:
         if not path:
             self.f = None
             return
-        parent = os.path.dirname(path)
-        if parent:
-            os.makedirs(parent, exist_ok=True)
         try:
+            parent = os.path.dirname(path)
+            if parent:
+                os.makedirs(parent, exist_ok=True)
             self.f = open(path, "wb")
         except OSError as e:
             raise ConfigError(f"cannot open trace for writing: {path}") from e

@@ -226,3 +226,29 @@ def test_dock_jsonl_on_gpu(Cm, tmp_path):
                               keep_top=2, seed=11)
     ids = [json.loads(x)["ligand"] for x in open(tmp_path / "b.jsonl").read().splitlines()]
     assert ids and set(ids) <= {r.id for r in recs[:5]}
+
+
+def test_trace_writer_and_config_paths(Cm, tmp_path):
+    """TraceWriter (pipeline.cpp:335-352): parent directories created, the
+    stage lines' bytes, ConfigError when the trace cannot be opened; the
+    config's output paths (trace / report) stay as given (pipeline.cpp:151-154)."""
+    tw = Cm._TraceWriter(str(tmp_path / "a" / "b" / "t.jsonl"))
+    tw.stage("start", "parse")
+    tw.stage("end", "parse")
+    tw.close()
+    assert open(tmp_path / "a" / "b" / "t.jsonl", "rb").read() == (
+        b'{"kind":"stage_start","stage":"parse"}\n{"kind":"stage_end","stage":"parse"}\n')
+    (tmp_path / "f").write_text("x")
+    with pytest.raises(Cm.ConfigError, match="cannot open trace for writing"):
+        Cm._TraceWriter(str(tmp_path / "f" / "t.jsonl"))
+    for f in ("pocket.json", "sample_library_100.smi", "smiles.dict"):
+        shutil.copy(os.path.join(CAMP, f), tmp_path / f)
+    j = json.load(open(os.path.join(CAMP, "campaign_100.json")))
+    cfg = Cm.parse_config_json(json.dumps(dict(j, trace="out/t.jsonl", report="out/r.json")),
+                               str(tmp_path))
+    assert cfg.trace_path == "out/t.jsonl" and cfg.report_path == "out/r.json"
+    d = Cm.parse_config_json(json.dumps(j), str(tmp_path))
+    assert d.trace_path == "campaign_trace.jsonl" and d.report_path == "campaign_report.json"
+    bad = dict(j, funnel={"keep_after_dock": 0.0, "keep_for_fep": 0.5})
+    with pytest.raises(Cm.ConfigError, match="keep_after_dock"):
+        Cm.parse_config_json(json.dumps(bad), str(tmp_path))
