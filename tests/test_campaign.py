@@ -247,7 +247,8 @@ def test_trace_writer_and_config_paths(Cm, tmp_path):
     cfg = Cm.parse_config_json(json.dumps(dict(j, trace="out/t.jsonl", report="out/r.json")),
                                str(tmp_path))
     assert cfg.trace_path == "out/t.jsonl" and cfg.report_path == "out/r.json"
-    d = Cm.parse_config_json(json.dumps(j), str(tmp_path))
+    j2 = {k: v for k, v in j.items() if k not in ("trace", "report")}
+    d = Cm.parse_config_json(json.dumps(j2), str(tmp_path))  # pipeline.hpp:62-63 defaults
     assert d.trace_path == "campaign_trace.jsonl" and d.report_path == "campaign_report.json"
     bad = dict(j, funnel={"keep_after_dock": 0.0, "keep_for_fep": 0.5})
     with pytest.raises(Cm.ConfigError, match="keep_after_dock"):
