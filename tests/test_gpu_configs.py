@@ -288,3 +288,23 @@ def test_rescore_device_entries_equal_host_path(V, engine, pocket_json):
     og, orr = sweep.score_poses(sweep.OraclePocket(box, 0.2, 2.0), lib, pl, T, Q, TH)
     np.testing.assert_array_equal(g_host.view(np.uint32), og.view(np.uint32))
     np.testing.assert_array_equal(r_host.view(np.uint32), orr.view(np.uint32))
+
+
+@pytest.mark.parametrize("polish", [1, 2])
+def test_largest_ligands_bit_exact(V, engine, polish):
+    """Ligands near the GPU limits (110-128 heavy atoms, 36-40 torsions):
+    the widest shared layouts (packed atom pairs, the large-ligand flex and
+    polish instantiations), grid mode, against the oracle bit for bit."""
+    from oracle import sweep
+    import bench
+    from paper_2304_09953_b200.chem import flexible_smiles
+    smis = flexible_smiles(5, 6, atoms=(110, 128), tors=(20, 40), max_scan=400000)
+    lib = V.build_library(smis, [f"X{i}" for i in range(len(smis))], list(range(1, 7)),
+                          list(range(1, 7)), threads=16)
+    assert len(lib) == 6 and lib.n_atoms.min() >= 110 and lib.n_tors.max() >= 36
+    pocket = bench.make_pocket()
+    prm = V.DockParams(**dict(FULL, restarts=6, polish=polish))
+    engine.set_pocket(pocket, grid_spacing=0.4, grid_pad=2.0)
+    res = engine.dock_host(lib, prm)
+    ora = sweep.dock_library(sweep.OraclePocket(pocket, 0.4, 2.0), lib, prm, threads=6)
+    _same(res, ora)
