@@ -294,7 +294,8 @@ def test_rescore_device_entries_equal_host_path(V, engine, pocket_json):
 def test_largest_ligands_bit_exact(V, engine, polish):
     """Ligands near the GPU limits (110-128 heavy atoms, 36-40 torsions):
     the widest shared layouts (packed atom pairs, the large-ligand flex and
-    polish instantiations), grid mode, against the oracle bit for bit."""
+    polish instantiations), grid mode, against the oracle bit for bit, and
+    K3a on the survivors against the oracle's rescoring."""
     from oracle import sweep
     import bench
     from paper_2304_09953_b200.chem import flexible_smiles
@@ -308,3 +309,16 @@ def test_largest_ligands_bit_exact(V, engine, polish):
     res = engine.dock_host(lib, prm)
     ora = sweep.dock_library(sweep.OraclePocket(pocket, 0.4, 2.0), lib, prm, threads=6)
     _same(res, ora)
+    # K3a on the survivors at this size (the widest pose columns)
+    pl, T, Q, TH = [], [], [], []
+    for i in range(len(lib)):
+        for pose in res.poses(i, int(lib.n_tors[i]), "surv"):
+            pl.append(i)
+            T.append(pose.translation)
+            Q.append(pose.rotation)
+            TH.extend(pose.torsions)
+    T, Q, TH = (np.array(a, np.float32) for a in (T, Q, TH))
+    g, r = engine.rescore(lib, pl, T, Q, TH)
+    og, orr = sweep.score_poses(sweep.OraclePocket(pocket, 0.4, 2.0), lib, pl, T, Q, TH)
+    np.testing.assert_array_equal(g.view(np.uint32), og.view(np.uint32))
+    np.testing.assert_array_equal(r.view(np.uint32), orr.view(np.uint32))
