@@ -322,3 +322,44 @@ def test_largest_ligands_bit_exact(V, engine, polish):
     og, orr = sweep.score_poses(sweep.OraclePocket(pocket, 0.4, 2.0), lib, pl, T, Q, TH)
     np.testing.assert_array_equal(g.view(np.uint32), og.view(np.uint32))
     np.testing.assert_array_equal(r.view(np.uint32), orr.view(np.uint32))
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_random_pockets_and_spacings_bit_exact(V, engine, seed):
+    """Random pockets (site count, kinds, weights, widths, box shape, clash
+    radius / penalty) at random map spacings, small random libraries:
+    GPU dock and K3a against the oracle bit for bit."""
+    from oracle import sweep
+    from paper_2304_09953_b200.chem import corpus_library
+    rng = np.random.default_rng(seed)
+    lo = rng.uniform(-9, -5, 3)
+    hi = rng.uniform(5, 9, 3)
+    kinds = ["steric", "hbond", "lipophilic"]
+    sites = [V.Site(tuple(float(v) for v in rng.uniform(lo + 1, hi - 1)),
+                    float(rng.uniform(-0.5, 2.0)), float(rng.uniform(0.6, 2.5)),
+                    kinds[int(rng.integers(0, 3))])
+             for _ in range(int(rng.integers(3, 40)))]
+    pocket = V.Pocket(sites, tuple(float(v) for v in lo), tuple(float(v) for v in hi),
+                      float(rng.uniform(0.5, 1.2)),
+                      float(rng.uniform(0.1, 1.0)))
+    lib = corpus_library(100 + seed, 60, (1, 40), (0, 10), threads=16)
+    prm = V.DockParams(restarts=4, rotations=64, flex_angles=16, flex_passes=2, keep_top=3,
+                       min_score=-1e30, diversity_delta=float(rng.uniform(0.5, 2.0)))
+    spacing = float(rng.choice([0.3, 0.45, 0.6]))
+    engine.set_pocket(pocket, grid_spacing=spacing, grid_pad=2.0)
+    res = engine.dock_host(lib, prm)
+    op = sweep.OraclePocket(pocket, spacing, 2.0)
+    ora = sweep.dock_library(op, lib, prm, threads=16)
+    _same(res, ora)
+    pl, T, Q, TH = [], [], [], []
+    for i in range(len(lib)):
+        for pose in res.poses(i, int(lib.n_tors[i]), "surv"):
+            pl.append(i)
+            T.append(pose.translation)
+            Q.append(pose.rotation)
+            TH.extend(pose.torsions)
+    T, Q, TH = (np.array(a, np.float32) for a in (T, Q, TH))
+    g, r = engine.rescore(lib, pl, T, Q, TH)
+    og, orr = sweep.score_poses(op, lib, pl, T, Q, TH)
+    np.testing.assert_array_equal(g.view(np.uint32), og.view(np.uint32))
+    np.testing.assert_array_equal(r.view(np.uint32), orr.view(np.uint32))
