@@ -76,6 +76,7 @@ def lib() -> C.CDLL:
                                                 C.c_long]),
             "vsref_train_dictionary": (C.c_int, [C.c_char_p, C.c_long, C.c_int, C.c_char_p, C.c_long]),
             "vsref_run_campaign": (C.c_int, [C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p]),
+            "vsref_dictionary_entries": (C.c_int, [C.c_char_p, C.c_char_p, C.c_long]),
             "vsref_rng_draws": (None, [C.c_uint64, P(C.c_uint64), C.c_int, P(C.c_int32), P(C.c_double),
                                        P(C.c_double), C.c_int, P(C.c_double)]),
             "vsref_random_smiles": (C.c_int, [C.c_uint64, C.c_uint64, C.c_char_p, C.c_int]),
@@ -379,3 +380,10 @@ def run_campaign(cfg_path: str, trace_path: str, report_path: str, tsv_path: str
     """The reference's run_campaign on a config file (outputs redirected)."""
     return _chk(lib().vsref_run_campaign(cfg_path.encode(), trace_path.encode(),
                                          report_path.encode(), tsv_path.encode()))
+
+
+def dictionary_entries(path: str) -> list[str]:
+    """codec::load_dictionary_file(path).entries of the reference."""
+    buf = C.create_string_buffer(8192)
+    n = _chk(lib().vsref_dictionary_entries(path.encode(), buf, 8192))
+    return [x.decode() for x in buf.raw[:n].split(b"\0")[:-1]]

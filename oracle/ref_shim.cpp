@@ -631,6 +631,22 @@ int vsref_run_campaign(const char* cfg_path, const char* trace_path, const char*
   });
 }
 
+// codec::load_dictionary_file (codec.cpp:217-221): entries NUL-separated;
+// the total length, or -9 when cap is small
+int vsref_dictionary_entries(const char* path, char* out, long cap) {
+  return guarded([&] {
+    const codec::Dictionary d = codec::load_dictionary_file(path);
+    std::string s;
+    for (const auto& e : d.entries) {
+      s += e;
+      s.push_back('\0');
+    }
+    if (static_cast<long>(s.size()) > cap) return -9;
+    std::memcpy(out, s.data(), s.size());
+    return static_cast<int>(s.size());
+  });
+}
+
 // ----------------------------------------------------------------- corpus --
 // corpus::random_smiles(Rng(seed).split(i)) (tools/smiles_corpus.hpp:13,51)
 int vsref_random_smiles(std::uint64_t seed, std::uint64_t i, char* out, int cap) {

@@ -3,8 +3,8 @@
 
 Python surface of proj/bindings/module.cpp restricted to the hot path:
 `dock_smiles`, `rmsd`, `target_batch_size`, `simulate_throughput`,
-`rank_ligands`, `run_campaign` (its dock funnel), plus the chem loaders
-that feed it.  Library-scale
+`rank_ligands`, `run_campaign` (its dock funnel), the codec read side
+(`load_dictionary`, `decompress_line`), plus the chem loaders that feed it.  Library-scale
 screening is `pipeline.screen` / `dock.Engine`.
 """
 from __future__ import annotations
@@ -20,6 +20,7 @@ from .chem import (Conformer, Library, Ligand, build_library, embed_3d, make_lig
 from .dock import (DockParams, Engine, Pocket, Pose, ScoreGradient, Site, apply_pose, dock,
                    filter_poses, geometric_score, load_pocket_file, parse_pocket_json,
                    pocket_to_json, pose_rmsd, pose_to_json, rescore, rmsd, score_gradient)
+from .codec import decompress_line, load_dictionary
 from .errors import (AtomCountMismatch, EmptyBounds, ItemTooLarge, LengthMismatch, OutOfRange,
                      ParseError)
 from .pipeline import RankedLigand, rank_ligands, screen

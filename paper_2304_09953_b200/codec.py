@@ -56,3 +56,30 @@ def decompress_file(path: str, dictionary_path: str, threads: int | None = None)
     with open(path, "rb") as f:
         data = f.read()
     return decompress(d, data, threads)
+
+
+def load_dictionary(path: str) -> list[str]:
+    """module.cpp:123-125: the entries of an SMZ1 dictionary file (code byte
+    0x80 + i <-> entries[i]); BadFormat as the reference raises it."""
+    d = load_dictionary_file(path)
+    out, o = [], 5
+    for _ in range(d[4]):
+        n = d[o]
+        out.append(d[o + 1:o + 1 + n].decode("ascii"))
+        o += 1 + n
+    return out
+
+
+def decompress_line(data: bytes, entries: list[str]) -> str:
+    """module.cpp:114-121 / codec.cpp:147-161: one record's bytes expanded
+    with the dictionary entries; UnknownCode(code, offset) for a code byte
+    without an entry."""
+    out = []
+    for i, b in enumerate(bytes(data)):
+        if b < 0x80:
+            out.append(chr(b))
+        elif b - 0x80 < len(entries):
+            out.append(entries[b - 0x80])
+        else:
+            raise UnknownCode(b, i)
+    return "".join(out)

@@ -172,3 +172,19 @@ def test_cpp_dropin_codec_read_side(tmp_path):
                    check=True)
     out = subprocess.run([str(exe), CODEC, CAMP], capture_output=True, text=True)
     assert out.returncode == 0 and "codec ok" in out.stdout, out.stdout + out.stderr
+
+
+def test_pybind_codec_read_functions(tmp_path):
+    """load_dictionary / decompress_line as module.cpp:114-125 expose them
+    (known answers of test_codec.cpp:92-108 and the golden dictionary)."""
+    import paper_2304_09953_b200 as V
+    assert V.decompress_line(bytes([0x80, ord("O")]), ["CC"]) == "CCO"
+    assert V.decompress_line(b"", []) == ""
+    with pytest.raises(V.codec.UnknownCode) as e:
+        V.decompress_line(bytes([0x90]), [])
+    assert e.value.code == 0x90 and e.value.offset == 0
+    entries = V.load_dictionary(os.path.join(CAMP, "smiles.dict"))
+    raw = open(os.path.join(CAMP, "smiles.dict"), "rb").read()
+    assert len(entries) == raw[4] and all(2 <= len(x) <= 8 for x in entries)
+    R = need_ref()
+    assert entries == R.dictionary_entries(os.path.join(CAMP, "smiles.dict"))
