@@ -447,6 +447,7 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
                                      static_cast<float>(b.y - o.y) * ks,
                                      static_cast<float>(b.z - o.z) * ks);
         const float4* gf = reinterpret_cast<const float4*>(s.pose);
+        const float4 r0 = gf[0], r1 = gf[1], r2 = gf[2];  // the pose's grid frame
         for (int q2 = h; q2 < m; q2 += 2) {
           const double4 v = s.ys[s.mov[ax.z + q2]];
           const float vx = static_cast<float>(v.x - o.x), vy = static_cast<float>(v.y - o.y),
@@ -454,7 +455,6 @@ static __device__ VS_PHASE float flex_phase(const PocketDev& pk, const Dims d, i
           const float fx = fmaf(Mf.m00, vx, fmaf(Mf.m01, vy, fmaf(Mf.m02, vz, ofx)));
           const float fy = fmaf(Mf.m10, vx, fmaf(Mf.m11, vy, fmaf(Mf.m12, vz, ofy)));
           const float fz = fmaf(Mf.m20, vx, fmaf(Mf.m21, vy, fmaf(Mf.m22, vz, ofz)));
-          const float4 r0 = gf[0], r1 = gf[1], r2 = gf[2];
           fm = fm + key_at_grid(pk, fmaf(r0.x, fx, fmaf(r0.y, fy, fmaf(r0.z, fz, r0.w))),
                                 fmaf(r1.x, fx, fmaf(r1.y, fy, fmaf(r1.z, fz, r1.w))),
                                 fmaf(r2.x, fx, fmaf(r2.y, fy, fmaf(r2.z, fz, r2.w))));
