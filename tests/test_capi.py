@@ -69,3 +69,22 @@ def test_key_encoding_roundtrip():
         key = ((~ordv & 0xFFFFFFFF) << 32) | 17
         assert _capi.lib.vs_key_score(key) == f
         assert _capi.lib.vs_key_id_rank(key) == 17
+
+
+def test_no_device_entry_points_fail_loudly():
+    """Without a GPU the device entry points report it (no CPU fallback):
+    page-locked allocation and handle creation."""
+    import ctypes as C
+    from conftest import gpu_available
+    if gpu_available():
+        pytest.skip("a GPU is present")
+    import numpy as np
+    from paper_2304_09953_b200 import _capi
+    from paper_2304_09953_b200.dock import pinned_empty
+    from paper_2304_09953_b200.errors import VscreenError
+    with pytest.raises(VscreenError):
+        pinned_empty(16, np.float32)
+    h = C.c_void_p()
+    assert _capi.lib.vs_create(0, C.byref(h)) == _capi.VS_ERR_NO_DEVICE
+    p = C.c_void_p()
+    assert _capi.lib.vs_host_alloc(64, C.byref(p)) == _capi.VS_ERR_NO_DEVICE and not p.value
