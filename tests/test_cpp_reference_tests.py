@@ -1,10 +1,12 @@
-"""The reference's own unit tests of the dock and batcher API
-(proj/tests/test_dock.cpp, test_batcher.cpp — unmodified), compiled against
+"""The reference's own unit tests of the dock, batcher and chem API
+(proj/tests/test_dock.cpp, test_batcher.cpp, test_chem.cpp — unmodified;
+smiles_corpus.hpp from proj/tools), compiled against
 the drop-in headers (include/vscreen/) with a doctest shim
 (tests/cpp/doctest.h) and linked to libvscreen_core.so instead of the CPU
 library (oracle/build_ref_tests.sh, run by __graft_entry__.build()).
 
-CPU: test_batcher passes whole; test_dock's host-side cases (filter_poses,
+CPU: test_batcher and test_chem (15 cases: parser, ring flags, rotatable
+bonds, embed_3d, records, make_ligand) pass whole; test_dock's host-side cases (filter_poses,
 rmsd, torsion topology / apply_pose) pass and every GPU entry point fails
 loudly (no CPU fallback).  GPU: all 13 test_dock cases pass."""
 import os
@@ -34,6 +36,12 @@ def test_reference_batcher_tests_pass():
     out, res = _run("test_batcher")
     assert out.returncode == 0, out.stdout + out.stderr
     assert len(res) == 6 and all(v == "PASS" for v in res.values()), out.stdout
+
+
+def test_reference_chem_tests_pass():
+    out, res = _run("test_chem")
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert len(res) == 15 and all(v == "PASS" for v in res.values()), out.stdout
 
 
 def test_reference_dock_tests_host_cases_on_cpu():
